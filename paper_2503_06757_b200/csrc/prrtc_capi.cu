@@ -1,0 +1,1014 @@
+// prrtc_capi.cu — host side of the C-ABI declared in include/prrtc_b200.h.
+//
+// Validation mirrors the reference (RobotModel::finalize kinematics.cpp:15-74,
+// Scene::validate geometry.cpp:10-39, plan() preconditions planner.cpp:248-252)
+// and reports through return codes + prrtc_last_error instead of exceptions.
+// All planning runs on the device; there is no CPU fallback: without an
+// sm_100 device every compute entry point fails with PRRTC_ENODEV.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <chrono>
+#include <cmath>
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "prrtc_b200.h"
+#include "prrtc_internal.h"
+#include "prrtc_launch.h"
+
+using namespace prrtc_b200;
+
+namespace {
+
+thread_local std::string g_err;
+
+int set_err(int code, const std::string& msg) {
+    g_err = msg;
+    return code;
+}
+
+#define CUDA_TRY(expr)                                                                  \
+    do {                                                                                \
+        cudaError_t e_ = (expr);                                                        \
+        if (e_ != cudaSuccess)                                                          \
+            return set_err(PRRTC_ECUDA, std::string(#expr) + ": " + cudaGetErrorString(e_)); \
+    } while (0)
+
+int check_device(int device) {
+    int n = 0;
+    if (cudaGetDeviceCount(&n) != cudaSuccess || n == 0)
+        return set_err(PRRTC_ENODEV, "no CUDA device: the B200 planner has no CPU fallback");
+    if (device < 0 || device >= n) return set_err(PRRTC_ENODEV, "device ordinal out of range");
+    cudaDeviceProp p;
+    if (cudaGetDeviceProperties(&p, device) != cudaSuccess)
+        return set_err(PRRTC_ENODEV, "cudaGetDeviceProperties failed");
+    if (p.major != 10)
+        return set_err(PRRTC_ENODEV, "device is not sm_100 (Blackwell); kernels are built for sm_100a only");
+    return PRRTC_OK;
+}
+
+// ---- small FP64 math in the reference's operation order (transform.hpp) ----
+struct M3 {
+    double m[9];
+};
+// Quat::to_mat3 (transform.hpp:97-103) on the raw (unnormalised) quaternion.
+M3 quat_to_mat3(double w, double x, double y, double z) {
+    return {{1 - 2 * (y * y + z * z), 2 * (x * y - w * z), 2 * (x * z + w * y),
+             2 * (x * y + w * z), 1 - 2 * (x * x + z * z), 2 * (y * z - w * x),
+             2 * (x * z - w * y), 2 * (y * z + w * x), 1 - 2 * (x * x + y * y)}};
+}
+M3 transposed(const M3& a) {
+    return {{a.m[0], a.m[3], a.m[6], a.m[1], a.m[4], a.m[7], a.m[2], a.m[5], a.m[8]}};
+}
+M3 mul(const M3& a, const M3& b) {
+    M3 r;
+    for (int i = 0; i < 3; ++i)
+        for (int j = 0; j < 3; ++j)
+            r.m[3 * i + j] = a.m[3 * i] * b.m[j] + a.m[3 * i + 1] * b.m[3 + j] + a.m[3 * i + 2] * b.m[6 + j];
+    return r;
+}
+double norm3(double x, double y, double z) { return std::sqrt(x * x + y * y + z * z); }
+
+std::vector<unsigned> first_primes(size_t n) {  // sampling.cpp:20-37
+    std::vector<unsigned> p;
+    for (unsigned c = 2; p.size() < n; ++c) {
+        bool ok = true;
+        for (unsigned q : p) {
+            if (q * q > c) break;
+            if (c % q == 0) {
+                ok = false;
+                break;
+            }
+        }
+        if (ok) p.push_back(c);
+    }
+    return p;
+}
+
+uint32_t fbits(float f) {
+    uint32_t u;
+    std::memcpy(&u, &f, 4);
+    return u;
+}
+
+}  // namespace
+
+// ---------------------------------------------------------------------------
+// handles
+// ---------------------------------------------------------------------------
+struct prrtc_robot {
+    int device = 0;
+    int dof = 0, n_links = 0, n_fine = 0;
+    std::vector<uint32_t> words;
+    std::vector<double> limits;   // [dof][2]
+    std::vector<double> fine_r64;
+    uint32_t* d_words = nullptr;
+    double* d_fine_r64 = nullptr;
+    double* d_limits = nullptr;
+    double reach = 0.0;           // bound on |posed sphere| (m)
+    RobotArgs args() const {
+        RobotArgs r;
+        r.words = d_words;
+        r.n_words = (int)words.size();
+        r.fine_r64 = d_fine_r64;
+        r.limits = d_limits;
+        r.n_links = n_links;
+        r.dof = dof;
+        r.n_fine = n_fine;
+        return r;
+    }
+};
+
+struct prrtc_scene {
+    int device = 0;
+    std::vector<uint32_t> words;
+    std::vector<double> f64;  // spheres, boxes, capsules
+    int ns = 0, nb = 0, nc = 0;
+    double extent = 0.0;
+    uint32_t* d_words = nullptr;
+    double* d_f64 = nullptr;
+    SceneArgs args() const {
+        SceneArgs s;
+        s.words = d_words;
+        s.f64.s = d_f64;
+        s.f64.b = d_f64 + 4 * ns;
+        s.f64.c = d_f64 + 4 * ns + BOX_STRIDE * nb;
+        return s;
+    }
+};
+
+extern "C" {
+
+int prrtc_api_version(void) { return PRRTC_API_VERSION; }
+
+int prrtc_last_error(char* buf, size_t len) {
+    if (!buf || len == 0) return PRRTC_EINVAL;
+    std::snprintf(buf, len, "%s", g_err.c_str());
+    return PRRTC_OK;
+}
+
+int prrtc_device_count(void) {
+    int n = 0;
+    if (cudaGetDeviceCount(&n) != cudaSuccess) return 0;
+    int ok = 0;
+    for (int d = 0; d < n; ++d) {
+        cudaDeviceProp p;
+        if (cudaGetDeviceProperties(&p, d) == cudaSuccess && p.major == 10) ++ok;
+    }
+    return ok;
+}
+
+void prrtc_params_default(prrtc_params* p) {  // planner.hpp:21-40
+    std::memset(p, 0, sizeof(*p));
+    p->delta = 0.5;
+    p->n_cc = 32;
+    p->workers = 0;
+    p->max_iters_per_worker = 2000;
+    p->tree_capacity = 200000;
+    p->dd_radius = 0.0;
+    p->dynamic_domain = 1;
+    p->balance = 1;
+    p->early_exit = 1;
+    p->two_stage = 1;
+    p->batched_cc = 0;
+    p->nn_partitions = 1;
+    p->sampler = PRRTC_SAMPLER_HALTON;
+    p->seed = 0;
+}
+
+// ---- robot: RobotModel::finalize (kinematics.cpp:15-74) + upload ----
+int prrtc_robot_create(const prrtc_robot_desc* d, int device, prrtc_robot** out) {
+    if (!d || !out) return set_err(PRRTC_EINVAL, "prrtc_robot_create: null argument");
+    const int n = (int)d->n_links;
+    if (n == 0) return set_err(PRRTC_EINVAL, "robot: joints must be non-empty");
+    if (n > PRRTC_MAX_LINKS) return set_err(PRRTC_EINVAL, "robot: too many links for the device layout");
+    auto where = [](const char* what, int i) { return std::string("robot joints[") + std::to_string(i) + "]" + what; };
+    int dof = 0;
+    std::vector<int> qidx(n, -1);
+    for (int i = 0; i < n; ++i) {
+        if (d->parent[i] >= i) return set_err(PRRTC_EINVAL, where(".parent: must be smaller than the joint index", i));
+        if (d->parent[i] < -1) return set_err(PRRTC_EINVAL, where(".parent: out of range", i));
+        const double* q = d->origin_quat + 4 * i;
+        const double qn = std::sqrt(q[0] * q[0] + q[1] * q[1] + q[2] * q[2] + q[3] * q[3]);
+        if (std::abs(qn - 1.0) > 1e-6)
+            return set_err(PRRTC_EINVAL, where(".origin.quaternion: norm deviates from 1 by more than 1e-6", i));
+        if (d->kind[i] < 0 || d->kind[i] > 2) return set_err(PRRTC_EINVAL, where(".kind: unknown joint kind", i));
+        if (d->kind[i] != PRRTC_JOINT_FIXED) {
+            const double* a = d->axis + 3 * i;
+            if (std::abs(norm3(a[0], a[1], a[2]) - 1.0) > 1e-9)
+                return set_err(PRRTC_EINVAL, where(".axis: must be unit length", i));
+            if (!(d->lo[i] <= d->hi[i])) return set_err(PRRTC_EINVAL, where(".limits: lo must be <= hi", i));
+            qidx[i] = dof++;
+        }
+    }
+    if (dof > PRRTC_MAX_DOF) return set_err(PRRTC_EINVAL, "robot: too many degrees of freedom for the device layout");
+    const uint32_t S = d->fine_offset[n];
+    if (S > PRRTC_MAX_FINE) return set_err(PRRTC_EINVAL, "robot: too many fine spheres for the device layout");
+    int maxf = 1;
+    for (int l = 0; l < n; ++l) {
+        const std::string w = "robot spheres[" + std::to_string(l) + "]";
+        const double* c = d->coarse + 4 * l;
+        if (!(c[3] > 0.0)) return set_err(PRRTC_EINVAL, w + ".coarse.radius: must be positive");
+        if (d->fine_offset[l + 1] < d->fine_offset[l]) return set_err(PRRTC_EINVAL, w + ": bad fine offsets");
+        const int nf = (int)(d->fine_offset[l + 1] - d->fine_offset[l]);
+        if (nf > PRRTC_MAX_FINE_PER_LINK) return set_err(PRRTC_EINVAL, w + ": too many fine spheres");
+        maxf = std::max(maxf, nf);
+        for (uint32_t k = d->fine_offset[l]; k < d->fine_offset[l + 1]; ++k) {
+            const double* f = d->fine + 4 * k;
+            if (!(f[3] > 0.0)) return set_err(PRRTC_EINVAL, w + ".fine[" + std::to_string(k - d->fine_offset[l]) + "].radius: must be positive");
+            const double reach = norm3(f[0] - c[0], f[1] - c[1], f[2] - c[2]) + f[3];
+            if (reach > c[3] + 1e-9)
+                return set_err(PRRTC_EINVAL, w + ".fine[" + std::to_string(k - d->fine_offset[l]) + "]: escapes the coarse bounding sphere");
+        }
+    }
+    if (d->n_self_pairs > PRRTC_MAX_SELF_PAIRS) return set_err(PRRTC_EINVAL, "robot: too many self pairs");
+    for (uint32_t p = 0; p < d->n_self_pairs; ++p) {
+        const int a = d->self_pairs[2 * p], b = d->self_pairs[2 * p + 1];
+        const std::string w = "robot self_pairs[" + std::to_string(p) + "]";
+        if (a < 0 || b < 0 || a >= n || b >= n) return set_err(PRRTC_EINVAL, w + ": link index out of range");
+        if (a == b) return set_err(PRRTC_EINVAL, w + ": a link cannot pair with itself");
+        if (d->parent[a] == b || d->parent[b] == a)
+            return set_err(PRRTC_EINVAL, w + ": adjacent parent-child links must not be tested");
+    }
+    int rc = check_device(device);
+    if (rc) return rc;
+
+    auto* r = new prrtc_robot();
+    r->device = device;
+    r->dof = dof;
+    r->n_links = n;
+    r->n_fine = (int)S;
+    // packed words
+    std::vector<uint32_t>& w = r->words;
+    w.assign(RH_COUNT, 0);
+    auto align4 = [&]() { while (w.size() % 4) w.push_back(0); };
+    w[RH_NLINKS] = n;
+    w[RH_DOF] = dof;
+    w[RH_NFINE] = S;
+    w[RH_NPAIRS] = d->n_self_pairs;
+    w[RH_MAXFINE] = maxf;
+    align4();
+    w[RH_OFF_INFO] = (uint32_t)w.size();
+    for (int l = 0; l < n; ++l) {
+        w.push_back((uint32_t)d->kind[l]);
+        w.push_back((uint32_t)d->parent[l]);
+        w.push_back((uint32_t)qidx[l]);
+        w.push_back(d->fine_offset[l]);
+    }
+    w[RH_OFF_NFINE] = (uint32_t)w.size();
+    for (int l = 0; l < n; ++l) w.push_back(d->fine_offset[l + 1] - d->fine_offset[l]);
+    align4();
+    w[RH_OFF_GEO] = (uint32_t)w.size();
+    double reach_sum = 0.0;
+    for (int l = 0; l < n; ++l) {
+        const double* q = d->origin_quat + 4 * l;
+        const M3 Ro = quat_to_mat3(q[0], q[1], q[2], q[3]);
+        const double* a = d->axis + 3 * l;
+        const M3 ax = {{0, -a[2], a[1], a[2], 0, -a[0], -a[1], a[0], 0}};
+        const M3 M2 = mul(Ro, ax);
+        double v[3];
+        for (int i = 0; i < 3; ++i) v[i] = Ro.m[3 * i] * a[0] + Ro.m[3 * i + 1] * a[1] + Ro.m[3 * i + 2] * a[2];
+        float g[GEO_STRIDE] = {0};
+        for (int k = 0; k < 9; ++k) {
+            g[k] = (float)Ro.m[k];
+            g[9 + k] = (float)M2.m[k];
+            g[18 + k] = (float)(v[k / 3] * a[k % 3]);
+        }
+        for (int k = 0; k < 3; ++k) {
+            g[27 + k] = (float)d->origin_xyz[3 * l + k];
+            g[30 + k] = (float)v[k];
+            g[33 + k] = (float)d->coarse[4 * l + k];
+        }
+        g[36] = (float)d->coarse[4 * l + 3];
+        for (int k = 0; k < GEO_STRIDE; ++k) w.push_back(fbits(g[k]));
+        reach_sum += norm3(d->origin_xyz[3 * l], d->origin_xyz[3 * l + 1], d->origin_xyz[3 * l + 2]) +
+                     norm3(d->coarse[4 * l], d->coarse[4 * l + 1], d->coarse[4 * l + 2]) + d->coarse[4 * l + 3];
+    }
+    align4();
+    w[RH_OFF_FINE] = (uint32_t)w.size();
+    for (uint32_t k = 0; k < S; ++k)
+        for (int i = 0; i < 4; ++i) w.push_back(fbits((float)d->fine[4 * k + i]));
+    w[RH_OFF_PAIRS] = (uint32_t)w.size();
+    for (uint32_t p = 0; p < d->n_self_pairs; ++p) {
+        w.push_back((uint32_t)d->self_pairs[2 * p]);
+        w.push_back((uint32_t)d->self_pairs[2 * p + 1]);
+    }
+    w[RH_OFF_BASES] = (uint32_t)w.size();
+    for (unsigned b : first_primes(dof)) w.push_back(b);
+    w[RH_OFF_FLINK] = (uint32_t)w.size();
+    for (int l = 0; l < n; ++l)
+        for (uint32_t k = d->fine_offset[l]; k < d->fine_offset[l + 1]; ++k) w.push_back((uint32_t)l);
+    align4();
+    w[RH_WORDS] = (uint32_t)w.size();
+    r->reach = reach_sum;
+    for (int l = 0; l < n; ++l) {
+        if (d->kind[l] != PRRTC_JOINT_FIXED) {
+            r->limits.push_back(d->lo[l]);
+            r->limits.push_back(d->hi[l]);
+            if (d->kind[l] == PRRTC_JOINT_PRISMATIC) r->reach += std::max(std::abs(d->lo[l]), std::abs(d->hi[l]));
+        }
+    }
+    r->fine_r64.resize(S);
+    for (uint32_t k = 0; k < S; ++k) r->fine_r64[k] = d->fine[4 * k + 3];
+
+    cudaSetDevice(device);
+    if (cudaMalloc(&r->d_words, 4 * w.size()) != cudaSuccess ||
+        cudaMalloc(&r->d_fine_r64, 8 * std::max<size_t>(1, S)) != cudaSuccess ||
+        cudaMalloc(&r->d_limits, 8 * std::max<size_t>(2, r->limits.size())) != cudaSuccess) {
+        prrtc_robot_destroy(r);
+        return set_err(PRRTC_ENOMEM, "prrtc_robot_create: device allocation failed");
+    }
+    cudaMemcpy(r->d_words, w.data(), 4 * w.size(), cudaMemcpyHostToDevice);
+    if (S) cudaMemcpy(r->d_fine_r64, r->fine_r64.data(), 8 * S, cudaMemcpyHostToDevice);
+    if (!r->limits.empty())
+        cudaMemcpy(r->d_limits, r->limits.data(), 8 * r->limits.size(), cudaMemcpyHostToDevice);
+    if (cudaGetLastError() != cudaSuccess) {
+        prrtc_robot_destroy(r);
+        return set_err(PRRTC_ECUDA, "prrtc_robot_create: upload failed");
+    }
+    *out = r;
+    return PRRTC_OK;
+}
+
+int prrtc_robot_destroy(prrtc_robot* r) {
+    if (!r) return PRRTC_OK;
+    cudaSetDevice(r->device);
+    cudaFree(r->d_words);
+    cudaFree(r->d_fine_r64);
+    cudaFree(r->d_limits);
+    delete r;
+    return PRRTC_OK;
+}
+
+int prrtc_robot_dof(const prrtc_robot* r) { return r ? r->dof : PRRTC_EINVAL; }
+int prrtc_robot_fine_count(const prrtc_robot* r) { return r ? r->n_fine : PRRTC_EINVAL; }
+int prrtc_robot_limits(const prrtc_robot* r, double* lim) {
+    if (!r || !lim) return PRRTC_EINVAL;
+    std::copy(r->limits.begin(), r->limits.end(), lim);
+    return PRRTC_OK;
+}
+
+// ---- scene: Scene::validate (geometry.cpp:10-39) + SceneIndex layout ----
+static int build_scene(const prrtc_scene_desc* d, prrtc_scene* s) {
+    const uint32_t P = d->n_spheres + d->n_boxes + d->n_capsules;
+    if (P > PRRTC_MAX_PRIMS) return set_err(PRRTC_EINVAL, "scene: more than PRRTC_MAX_PRIMS primitives");
+    int idx = 0;
+    auto where = [&](int i) { return std::string("scene primitives[") + std::to_string(i) + "]"; };
+    for (uint32_t i = 0; i < d->n_spheres; ++i, ++idx)
+        if (!(d->spheres[4 * i + 3] > 0.0)) return set_err(PRRTC_EINVAL, where(idx) + ".radius: must be positive");
+    for (uint32_t i = 0; i < d->n_boxes; ++i, ++idx) {
+        const double* b = d->boxes + 10 * i;
+        if (!(b[7] > 0.0 && b[8] > 0.0 && b[9] > 0.0))
+            return set_err(PRRTC_EINVAL, where(idx) + ".half_extents: must be componentwise positive");
+        const double qn = std::sqrt(b[0] * b[0] + b[1] * b[1] + b[2] * b[2] + b[3] * b[3]);
+        if (std::abs(qn - 1.0) > 1e-6)
+            return set_err(PRRTC_EINVAL, where(idx) + ".pose.quaternion: norm deviates from 1 by more than 1e-6");
+    }
+    for (uint32_t i = 0; i < d->n_capsules; ++i, ++idx)
+        if (!(d->capsules[7 * i + 6] > 0.0)) return set_err(PRRTC_EINVAL, where(idx) + ".radius: must be positive");
+
+    s->ns = d->n_spheres;
+    s->nb = d->n_boxes;
+    s->nc = d->n_capsules;
+    std::vector<uint32_t>& w = s->words;
+    std::vector<double>& f = s->f64;
+    w.assign(SH_COUNT, 0);
+    f.clear();
+    double ext = 0.0;
+    auto upd = [&](double x) { ext = std::max(ext, std::abs(x)); };
+    w[SH_NS] = s->ns;
+    w[SH_NB] = s->nb;
+    w[SH_NC] = s->nc;
+    w[SH_OFF_S] = (uint32_t)w.size();
+    for (int i = 0; i < s->ns; ++i) {
+        const double* p = d->spheres + 4 * i;
+        for (int k = 0; k < 4; ++k) {
+            w.push_back(fbits((float)p[k]));
+            f.push_back(p[k]);
+            upd(p[k]);
+        }
+        upd(std::abs(p[0]) + p[3]);
+    }
+    w[SH_OFF_B] = (uint32_t)w.size();
+    for (int i = 0; i < s->nb; ++i) {
+        const double* b = d->boxes + 10 * i;
+        // BoxPrim -> SceneIndex: world-to-box rotation R^T, t, h (geometry.cpp:87-97)
+        const M3 rt = transposed(quat_to_mat3(b[0], b[1], b[2], b[3]));
+        double v[BOX_STRIDE] = {0};
+        for (int k = 0; k < 9; ++k) v[k] = rt.m[k];
+        for (int k = 0; k < 3; ++k) {
+            v[9 + k] = b[4 + k];
+            v[12 + k] = b[7 + k];
+            upd(std::abs(b[4 + k]) + norm3(b[7], b[8], b[9]));
+        }
+        for (int k = 0; k < BOX_STRIDE; ++k) {
+            w.push_back(fbits((float)v[k]));
+            f.push_back(v[k]);
+        }
+    }
+    w[SH_OFF_C] = (uint32_t)w.size();
+    for (int i = 0; i < s->nc; ++i) {
+        const double* c = d->capsules + 7 * i;
+        // CapsulePrim -> SceneIndex: a, ab = b - a, inv_ab2 (geometry.cpp:75-86)
+        const double abx = c[3] - c[0], aby = c[4] - c[1], abz = c[5] - c[2];
+        const double ab2 = abx * abx + aby * aby + abz * abz;
+        double v[CAP_STRIDE] = {c[0], c[1], c[2], abx, aby, abz, ab2 > 0.0 ? 1.0 / ab2 : 0.0, c[6]};
+        for (int k = 0; k < CAP_STRIDE; ++k) {
+            w.push_back(fbits((float)v[k]));
+            f.push_back(v[k]);
+        }
+        for (int k = 0; k < 6; ++k) upd(std::abs(c[k]) + c[6]);
+    }
+    while (w.size() % 4) w.push_back(0);
+    w[SH_WORDS] = (uint32_t)w.size();
+    s->extent = ext;
+    return PRRTC_OK;
+}
+
+// Guard band for the FP32 predicates: 16 ulps of the largest coordinate
+// magnitude the test can see (robot reach + scene extent), floor 8 m.
+static void finish_scene_words(prrtc_scene* s, double robot_reach) {
+    const double M = std::max(8.0, 2.0 * (s->extent + robot_reach));
+    const float eps = (float)(M * std::ldexp(1.0, -20));
+    s->words[SH_EPS] = fbits(eps);
+    s->words[SH_CPAD] = fbits(4.0f * eps + 1e-8f);
+}
+
+static int upload_scene(prrtc_scene* s) {
+    cudaSetDevice(s->device);
+    cudaFree(s->d_words);
+    cudaFree(s->d_f64);
+    s->d_words = nullptr;
+    s->d_f64 = nullptr;
+    if (cudaMalloc(&s->d_words, 4 * s->words.size()) != cudaSuccess ||
+        cudaMalloc(&s->d_f64, 8 * std::max<size_t>(1, s->f64.size())) != cudaSuccess)
+        return set_err(PRRTC_ENOMEM, "scene: device allocation failed");
+    cudaMemcpy(s->d_words, s->words.data(), 4 * s->words.size(), cudaMemcpyHostToDevice);
+    if (!s->f64.empty()) cudaMemcpy(s->d_f64, s->f64.data(), 8 * s->f64.size(), cudaMemcpyHostToDevice);
+    if (cudaGetLastError() != cudaSuccess) return set_err(PRRTC_ECUDA, "scene: upload failed");
+    return PRRTC_OK;
+}
+
+// default reach used for the guard band before a robot is known (m)
+static constexpr double kDefaultReach = 4.0;
+
+int prrtc_scene_create(const prrtc_scene_desc* d, int device, prrtc_scene** out) {
+    if (!d || !out) return set_err(PRRTC_EINVAL, "prrtc_scene_create: null argument");
+    int rc = check_device(device);
+    if (rc) return rc;
+    auto* s = new prrtc_scene();
+    s->device = device;
+    rc = build_scene(d, s);
+    if (rc) {
+        delete s;
+        return rc;
+    }
+    finish_scene_words(s, kDefaultReach);
+    rc = upload_scene(s);
+    if (rc) {
+        prrtc_scene_destroy(s);
+        return rc;
+    }
+    *out = s;
+    return PRRTC_OK;
+}
+
+int prrtc_scene_update(prrtc_scene* s, const prrtc_scene_desc* d) {
+    if (!s || !d) return set_err(PRRTC_EINVAL, "prrtc_scene_update: null argument");
+    prrtc_scene tmp;
+    tmp.device = s->device;
+    int rc = build_scene(d, &tmp);
+    if (rc) return rc;
+    s->words.swap(tmp.words);
+    s->f64.swap(tmp.f64);
+    s->ns = tmp.ns;
+    s->nb = tmp.nb;
+    s->nc = tmp.nc;
+    s->extent = tmp.extent;
+    finish_scene_words(s, kDefaultReach);
+    return upload_scene(s);
+}
+
+int prrtc_scene_destroy(prrtc_scene* s) {
+    if (!s) return PRRTC_OK;
+    cudaSetDevice(s->device);
+    cudaFree(s->d_words);
+    cudaFree(s->d_f64);
+    delete s;
+    return PRRTC_OK;
+}
+
+}  // extern "C"
+
+// ---------------------------------------------------------------------------
+// planning workspace and batches
+// ---------------------------------------------------------------------------
+struct prrtc_batch {
+    const prrtc_robot* robot = nullptr;
+    int device = 0;
+    int n = 0, dof = 0;
+    prrtc_params params{};
+    long long cap = 0, stride = 0;
+    int grid = 0, nthreads = 128, ns_max = 32;
+    unsigned long long budget = 0, arena_cap = 0;
+    unsigned epoch = 0;
+    // device buffers
+    double *d_starts = nullptr, *d_goals = nullptr, *d_cfg = nullptr, *d_arena = nullptr;
+    int *d_parent = nullptr, *d_dd = nullptr, *d_prob_scene = nullptr, *d_next = nullptr;
+    unsigned* d_ready = nullptr;
+    unsigned long long* d_arena_used = nullptr;
+    ProbCtl* d_ctl = nullptr;
+    const uint32_t** d_scene_words = nullptr;
+    SceneF64* d_scene_f64 = nullptr;
+    cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+    cudaStream_t last_stream = 0;
+    int launches = 0;
+    std::vector<int> msg_scene;
+    ~prrtc_batch() {
+        cudaSetDevice(device);
+        cudaFree(d_starts);
+        cudaFree(d_goals);
+        cudaFree(d_cfg);
+        cudaFree(d_arena);
+        cudaFree(d_parent);
+        cudaFree(d_dd);
+        cudaFree(d_prob_scene);
+        cudaFree(d_next);
+        cudaFree(d_ready);
+        cudaFree(d_arena_used);
+        cudaFree(d_ctl);
+        cudaFree(d_scene_words);
+        cudaFree(d_scene_f64);
+        if (ev0) cudaEventDestroy(ev0);
+        if (ev1) cudaEventDestroy(ev1);
+    }
+};
+
+namespace {
+
+int check_params(const prrtc_params* p) {  // planner.cpp:250-252
+    if (!(p->delta > 0.0)) return set_err(PRRTC_EINVAL, "plan: delta must be positive");
+    if (p->n_cc < 1) return set_err(PRRTC_EINVAL, "plan: n_cc must be >= 1");
+    if (p->tree_capacity < 2) return set_err(PRRTC_EINVAL, "plan: tree_capacity too small");
+    if (p->threads_per_cta != 0 && p->threads_per_cta != 128)
+        return set_err(PRRTC_EINVAL, "plan: threads_per_cta must be 0 or 128");
+    return PRRTC_OK;
+}
+
+int sm_count(int device) {
+    int n = 0;
+    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, device);
+    return n > 0 ? n : 1;
+}
+
+template <class T>
+int dmalloc(T** p, size_t count) {
+    if (cudaMalloc(reinterpret_cast<void**>(p), sizeof(T) * std::max<size_t>(1, count)) != cudaSuccess)
+        return set_err(PRRTC_ENOMEM, "plan: device allocation of " + std::to_string(sizeof(T) * count) + " bytes failed");
+    return PRRTC_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+int prrtc_batch_create(const prrtc_robot* robot, const prrtc_scene* const* scenes,
+                       uint32_t n_problems, const double* starts, const double* goals,
+                       uint32_t dof, const prrtc_params* params, prrtc_batch** out) {
+    if (!robot || !scenes || !starts || !goals || !params || !out)
+        return set_err(PRRTC_EINVAL, "prrtc_batch_create: null argument");
+    if ((int)dof != robot->dof)  // require_dim (types.hpp:16-21)
+        return set_err(PRRTC_EINVAL, "plan.start: expected dimension " + std::to_string(robot->dof) +
+                                         ", got " + std::to_string(dof));
+    int rc = check_params(params);
+    if (rc) return rc;
+    if (n_problems == 0) return set_err(PRRTC_EINVAL, "prrtc_batch_create: empty batch");
+    for (uint32_t i = 0; i < n_problems; ++i) {
+        if (!scenes[i] || scenes[i]->device != robot->device)
+            return set_err(PRRTC_EINVAL, "prrtc_batch_create: scene missing or on another device");
+    }
+    rc = check_device(robot->device);
+    if (rc) return rc;
+    cudaSetDevice(robot->device);
+    auto* b = new prrtc_batch();
+    b->robot = robot;
+    b->device = robot->device;
+    b->n = (int)n_problems;
+    b->dof = (int)dof;
+    b->params = *params;
+    b->cap = std::max<long long>(2, (long long)(params->tree_capacity / 2));  // planner.cpp:290
+    b->stride = (b->cap + 31) / 32 * 32;
+    b->nthreads = 128;
+    b->ns_max = std::max(32, std::min(128, (params->n_cc + 31) / 32 * 32));
+    const RobotArgs ra = robot->args();
+    const int occ = plan_occupancy(ra, b->ns_max, b->nthreads);
+    const int sms = sm_count(robot->device);
+    unsigned workers_eff;
+    if (params->deterministic) {
+        b->grid = 1;
+        workers_eff = 1;
+    } else if (n_problems == 1) {
+        const int def = 2 * sms;
+        b->grid = (int)(params->workers ? params->workers : def);
+        workers_eff = b->grid;
+    } else {
+        const unsigned per_sm = params->ctas_per_sm ? std::min<unsigned>(params->ctas_per_sm, occ) : occ;
+        b->grid = sms * per_sm;
+        workers_eff = params->workers ? params->workers
+                                      : std::max(1u, (unsigned)(b->grid / std::min<int>(b->grid, n_problems)));
+    }
+    b->budget = params->max_iters_per_worker * (unsigned long long)workers_eff;
+    // path arena: every problem can return a path of up to 4096 configs
+    const unsigned long long per = (unsigned long long)dof * std::min<long long>(4096, 2 * b->cap);
+    b->arena_cap = per * n_problems;
+    const size_t n = n_problems;
+    const size_t nodes = n * 2 * (size_t)b->stride;
+    if ((rc = dmalloc(&b->d_starts, n * dof)) || (rc = dmalloc(&b->d_goals, n * dof)) ||
+        (rc = dmalloc(&b->d_cfg, nodes * dof)) || (rc = dmalloc(&b->d_parent, nodes)) ||
+        (rc = dmalloc(&b->d_dd, nodes)) || (rc = dmalloc(&b->d_ready, nodes)) ||
+        (rc = dmalloc(&b->d_arena, b->arena_cap)) || (rc = dmalloc(&b->d_arena_used, 1)) ||
+        (rc = dmalloc(&b->d_ctl, n)) || (rc = dmalloc(&b->d_prob_scene, n)) ||
+        (rc = dmalloc(&b->d_next, 1)) || (rc = dmalloc(&b->d_scene_words, n)) ||
+        (rc = dmalloc(&b->d_scene_f64, n))) {
+        delete b;
+        return rc;
+    }
+    // ready flags start at epoch 0; launches use epoch >= 1
+    cudaMemset(b->d_ready, 0, sizeof(unsigned) * nodes);
+    // one scene table entry per problem (scenes may repeat)
+    std::vector<const uint32_t*> sw(n);
+    std::vector<SceneF64> sf(n);
+    std::vector<int> ps(n);
+    for (size_t i = 0; i < n; ++i) {
+        const SceneArgs sa = scenes[i]->args();
+        sw[i] = sa.words;
+        sf[i] = sa.f64;
+        ps[i] = (int)i;
+    }
+    cudaMemcpy(b->d_scene_words, sw.data(), sizeof(void*) * n, cudaMemcpyHostToDevice);
+    cudaMemcpy(b->d_scene_f64, sf.data(), sizeof(SceneF64) * n, cudaMemcpyHostToDevice);
+    cudaMemcpy(b->d_prob_scene, ps.data(), sizeof(int) * n, cudaMemcpyHostToDevice);
+    cudaMemcpy(b->d_starts, starts, sizeof(double) * n * dof, cudaMemcpyHostToDevice);
+    cudaMemcpy(b->d_goals, goals, sizeof(double) * n * dof, cudaMemcpyHostToDevice);
+    cudaEventCreate(&b->ev0);
+    cudaEventCreate(&b->ev1);
+    cudaError_t e = cudaDeviceSynchronize();
+    if (e != cudaSuccess) {
+        delete b;
+        return set_err(PRRTC_ECUDA, std::string("prrtc_batch_create: ") + cudaGetErrorString(e));
+    }
+    *out = b;
+    return PRRTC_OK;
+}
+
+int prrtc_batch_launch(prrtc_batch* b, void* stream) {
+    if (!b) return set_err(PRRTC_EINVAL, "prrtc_batch_launch: null batch");
+    cudaSetDevice(b->device);
+    cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+    b->last_stream = st;
+    ++b->epoch;
+    if (b->epoch == 0) ++b->epoch;
+    CUDA_TRY(cudaMemsetAsync(b->d_ctl, 0, sizeof(ProbCtl) * b->n, st));
+    CUDA_TRY(cudaMemsetAsync(b->d_arena_used, 0, sizeof(unsigned long long), st));
+    CUDA_TRY(cudaMemsetAsync(b->d_next, 0, sizeof(int), st));
+    PlanArgs a{};
+    a.robot = b->robot->d_words;
+    a.fine_r64 = b->robot->d_fine_r64;
+    a.limits = b->robot->d_limits;
+    a.scene_words = b->d_scene_words;
+    a.scene_f64 = b->d_scene_f64;
+    a.prob_scene = b->d_prob_scene;
+    a.starts = b->d_starts;
+    a.goals = b->d_goals;
+    a.n_problems = b->n;
+    a.ctl = b->d_ctl;
+    a.cfg = b->d_cfg;
+    a.parent = b->d_parent;
+    a.ready = b->d_ready;
+    a.dd = b->d_dd;
+    a.cap = b->cap;
+    a.stride = b->stride;
+    a.arena = b->d_arena;
+    a.arena_used = b->d_arena_used;
+    a.arena_cap = b->arena_cap;
+    a.next_problem = b->d_next;
+    a.epoch = b->epoch;
+    a.p.delta = b->params.delta;
+    a.p.dd_radius = b->params.dd_radius > 0.0 ? b->params.dd_radius : 4.0 * b->params.delta;
+    a.p.n_cc = b->params.n_cc;
+    a.p.dynamic_domain = b->params.dynamic_domain;
+    a.p.balance = b->params.balance;
+    a.p.early_exit = b->params.early_exit;
+    a.p.two_stage = b->params.two_stage;
+    a.p.deterministic = b->params.deterministic;
+    a.p.budget = b->budget;
+    a.p.seed = b->params.seed;
+    a.ns_max = b->ns_max;
+    a.nthreads = b->nthreads;
+    CUDA_TRY(cudaEventRecord(b->ev0, st));
+    CUDA_TRY(launch_plan(b->robot->args(), a, b->grid, st));
+    CUDA_TRY(cudaEventRecord(b->ev1, st));
+    b->launches = 1;
+    return PRRTC_OK;
+}
+
+int prrtc_batch_launch_count(const prrtc_batch* b) { return b ? b->launches : 0; }
+
+static const char* message_for(int msg) {
+    switch (msg) {  // planner.cpp:270-276, 317-320
+        case 1: return "start configuration is out of limits or in collision";
+        case 2: return "goal configuration is out of limits or in collision";
+        case 3: return "tree capacity exhausted";
+        case 4: return "all workers exhausted their iteration budgets";
+        case 5: return "path arena exhausted";
+        default: return "";
+    }
+}
+
+// path_cost (planner.cpp:152-158) with the scalar distance (nn.cpp:12-20).
+static double path_cost(const double* path, uint32_t len, uint32_t dof) {
+    double cost = 0.0;
+    for (uint32_t i = 1; i < len; ++i) {
+        double acc = 0.0;
+        for (uint32_t d = 0; d < dof; ++d) {
+            const double e = path[(size_t)(i - 1) * dof + d] - path[(size_t)i * dof + d];
+            acc += e * e;
+        }
+        cost += std::sqrt(acc);
+    }
+    return cost;
+}
+
+int prrtc_batch_results(prrtc_batch* b, prrtc_result* out) {
+    if (!b || !out) return set_err(PRRTC_EINVAL, "prrtc_batch_results: null argument");
+    cudaSetDevice(b->device);
+    CUDA_TRY(cudaStreamSynchronize(b->last_stream));
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, b->ev0, b->ev1);
+    std::vector<ProbCtl> ctl(b->n);
+    unsigned long long used = 0;
+    CUDA_TRY(cudaMemcpy(ctl.data(), b->d_ctl, sizeof(ProbCtl) * b->n, cudaMemcpyDeviceToHost));
+    CUDA_TRY(cudaMemcpy(&used, b->d_arena_used, sizeof(used), cudaMemcpyDeviceToHost));
+    used = std::min(used, b->arena_cap);
+    std::vector<double> arena(used);
+    if (used) CUDA_TRY(cudaMemcpy(arena.data(), b->d_arena, 8 * used, cudaMemcpyDeviceToHost));
+    for (int i = 0; i < b->n; ++i) {
+        prrtc_result& r = out[i];
+        std::memset(&r, 0, sizeof(r));
+        const ProbCtl& C = ctl[i];
+        r.dof = b->dof;
+        r.status = C.done == 1 ? PRRTC_SOLVED : C.done == 3 ? PRRTC_INFEASIBLE_ENDPOINT : PRRTC_FAILED;
+        if (C.done == 0) std::snprintf(r.message, sizeof(r.message), "problem did not finish");
+        else std::snprintf(r.message, sizeof(r.message), "%s", message_for(C.msg));
+        if (r.status == PRRTC_SOLVED && C.path_len > 0 &&
+            C.path_off + (unsigned long long)C.path_len * b->dof <= used) {
+            r.path_len = C.path_len;
+            r.path = static_cast<double*>(std::malloc(sizeof(double) * b->dof * C.path_len));
+            std::memcpy(r.path, arena.data() + C.path_off, sizeof(double) * b->dof * C.path_len);
+            r.cost = path_cost(r.path, r.path_len, b->dof);
+        } else if (r.status == PRRTC_SOLVED) {
+            r.status = PRRTC_FAILED;
+            std::snprintf(r.message, sizeof(r.message), "path unavailable");
+        }
+        r.device_time_ms = (C.t_end_ns > C.t_start_ns) ? (C.t_end_ns - C.t_start_ns) * 1e-6 : 0.0;
+        r.wall_time_ms = ms;  // whole-launch device time; prrtc_plan overwrites with host wall time
+        r.iterations_total = C.iters < b->budget ? C.iters : b->budget;
+        r.sphere_tests = C.sphere_tests;
+        r.fk_calls = C.fk_calls;
+        r.fine_stage_entries = C.fine_entries;
+        r.tree_nodes[0] = (uint64_t)std::max(0, C.published[0]);
+        r.tree_nodes[1] = (uint64_t)std::max(0, C.published[1]);
+        r.solving_worker = C.winner - 1;
+    }
+    return PRRTC_OK;
+}
+
+int prrtc_batch_destroy(prrtc_batch* b) {
+    delete b;
+    return PRRTC_OK;
+}
+
+int prrtc_plan_batch(const prrtc_robot* robot, const prrtc_scene* const* scenes,
+                     uint32_t n_problems, const double* starts, const double* goals,
+                     uint32_t dof, const prrtc_params* params, prrtc_result* out) {
+    const auto t0 = std::chrono::steady_clock::now();
+    prrtc_batch* b = nullptr;
+    int rc = prrtc_batch_create(robot, scenes, n_problems, starts, goals, dof, params, &b);
+    if (rc) return rc;
+    rc = prrtc_batch_launch(b, nullptr);
+    if (!rc) rc = prrtc_batch_results(b, out);
+    prrtc_batch_destroy(b);
+    const double wall =
+        std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+    if (!rc && n_problems == 1) out[0].wall_time_ms = wall;
+    return rc;
+}
+
+int prrtc_plan(const prrtc_robot* robot, const prrtc_scene* scene, const double* start,
+               const double* goal, uint32_t dof, const prrtc_params* params, prrtc_result* result) {
+    if (!scene) return set_err(PRRTC_EINVAL, "prrtc_plan: null scene");
+    return prrtc_plan_batch(robot, &scene, 1, start, goal, dof, params, result);
+}
+
+void prrtc_result_free(prrtc_result* r) {
+    if (r && r->path) {
+        std::free(r->path);
+        r->path = nullptr;
+        r->path_len = 0;
+    }
+}
+
+// ---------------------------------------------------------------------------
+// batched collision checking + parity hooks
+// ---------------------------------------------------------------------------
+int prrtc_validate_edges(const prrtc_robot* robot, const prrtc_scene* scene, const double* from,
+                         const double* to, uint32_t n_edges, uint32_t dof, int32_t n_cc,
+                         int two_stage, int early_exit, uint8_t* valid) {
+    if (!robot || !scene || !valid || (n_edges && (!from || !to)))
+        return set_err(PRRTC_EINVAL, "prrtc_validate_edges: null argument");
+    if ((int)dof != robot->dof) return set_err(PRRTC_EINVAL, "validate_edge.from: expected dimension " + std::to_string(robot->dof));
+    if (n_cc < 1) return set_err(PRRTC_EINVAL, "validate_edge: resolution_count must be >= 1");
+    if (n_edges == 0) return PRRTC_OK;
+    int rc = check_device(robot->device);
+    if (rc) return rc;
+    cudaSetDevice(robot->device);
+    double *df = nullptr, *dt = nullptr;
+    uint8_t* dv = nullptr;
+    const size_t nb = sizeof(double) * n_edges * dof;
+    if ((rc = dmalloc(&df, n_edges * dof)) || (rc = dmalloc(&dt, n_edges * dof)) || (rc = dmalloc(&dv, n_edges))) {
+        cudaFree(df);
+        cudaFree(dt);
+        return rc;
+    }
+    cudaMemcpy(df, from, nb, cudaMemcpyHostToDevice);
+    cudaMemcpy(dt, to, nb, cudaMemcpyHostToDevice);
+    cudaError_t e = launch_validate_edges(robot->args(), scene->args(), df, dt, (int)n_edges, n_cc,
+                                          two_stage, early_exit, dv, 0);
+    if (e == cudaSuccess) e = cudaMemcpy(valid, dv, n_edges, cudaMemcpyDeviceToHost);
+    cudaFree(df);
+    cudaFree(dt);
+    cudaFree(dv);
+    if (e != cudaSuccess) return set_err(PRRTC_ECUDA, std::string("prrtc_validate_edges: ") + cudaGetErrorString(e));
+    return PRRTC_OK;
+}
+
+int prrtc_check_configs(const prrtc_robot* robot, const prrtc_scene* scene, const double* q,
+                        uint32_t n, uint32_t dof, int two_stage, uint8_t* valid) {
+    if (!robot || !scene || !valid || (n && !q)) return set_err(PRRTC_EINVAL, "prrtc_check_configs: null argument");
+    if ((int)dof != robot->dof) return set_err(PRRTC_EINVAL, "check_config: expected dimension " + std::to_string(robot->dof));
+    if (n == 0) return PRRTC_OK;
+    int rc = check_device(robot->device);
+    if (rc) return rc;
+    cudaSetDevice(robot->device);
+    double* dq = nullptr;
+    uint8_t* dv = nullptr;
+    if ((rc = dmalloc(&dq, (size_t)n * dof)) || (rc = dmalloc(&dv, n))) {
+        cudaFree(dq);
+        return rc;
+    }
+    cudaMemcpy(dq, q, sizeof(double) * n * dof, cudaMemcpyHostToDevice);
+    cudaError_t e = launch_check_configs(robot->args(), scene->args(), dq, (int)n, two_stage, dv, 0);
+    if (e == cudaSuccess) e = cudaMemcpy(valid, dv, n, cudaMemcpyDeviceToHost);
+    cudaFree(dq);
+    cudaFree(dv);
+    if (e != cudaSuccess) return set_err(PRRTC_ECUDA, std::string("prrtc_check_configs: ") + cudaGetErrorString(e));
+    return PRRTC_OK;
+}
+
+int prrtc_debug_fk(const prrtc_robot* robot, const double* q, uint32_t n, uint32_t dof,
+                   float* fine_out, float* coarse_out) {
+    if (!robot || (n && !q)) return set_err(PRRTC_EINVAL, "prrtc_debug_fk: null argument");
+    if ((int)dof != robot->dof) return set_err(PRRTC_EINVAL, "forward_kinematics: expected dimension " + std::to_string(robot->dof));
+    if (n == 0) return PRRTC_OK;
+    int rc = check_device(robot->device);
+    if (rc) return rc;
+    cudaSetDevice(robot->device);
+    double* dq = nullptr;
+    float *df = nullptr, *dc = nullptr;
+    const size_t nf = (size_t)n * robot->n_fine * 3, nc = (size_t)n * robot->n_links * 3;
+    if ((rc = dmalloc(&dq, (size_t)n * dof)) || (rc = dmalloc(&df, nf)) || (rc = dmalloc(&dc, nc))) {
+        cudaFree(dq);
+        cudaFree(df);
+        return rc;
+    }
+    cudaMemcpy(dq, q, sizeof(double) * n * dof, cudaMemcpyHostToDevice);
+    cudaError_t e = launch_debug_fk(robot->args(), dq, (int)n, df, dc, 0);
+    if (e == cudaSuccess && fine_out) e = cudaMemcpy(fine_out, df, 4 * nf, cudaMemcpyDeviceToHost);
+    if (e == cudaSuccess && coarse_out) e = cudaMemcpy(coarse_out, dc, 4 * nc, cudaMemcpyDeviceToHost);
+    cudaFree(dq);
+    cudaFree(df);
+    cudaFree(dc);
+    if (e != cudaSuccess) return set_err(PRRTC_ECUDA, std::string("prrtc_debug_fk: ") + cudaGetErrorString(e));
+    return PRRTC_OK;
+}
+
+int prrtc_debug_sphere_hits(const prrtc_scene* scene, const float* centers, const double* radii,
+                            uint32_t n, uint8_t* hits) {
+    if (!scene || !hits || (n && (!centers || !radii))) return set_err(PRRTC_EINVAL, "prrtc_debug_sphere_hits: null argument");
+    if (n == 0) return PRRTC_OK;
+    int rc = check_device(scene->device);
+    if (rc) return rc;
+    cudaSetDevice(scene->device);
+    const int P = scene->ns + scene->nb + scene->nc;
+    float* dcn = nullptr;
+    double* dr = nullptr;
+    uint8_t* dh = nullptr;
+    if ((rc = dmalloc(&dcn, (size_t)n * 3)) || (rc = dmalloc(&dr, n)) || (rc = dmalloc(&dh, (size_t)n * P))) {
+        cudaFree(dcn);
+        cudaFree(dr);
+        return rc;
+    }
+    cudaMemcpy(dcn, centers, 12 * (size_t)n, cudaMemcpyHostToDevice);
+    cudaMemcpy(dr, radii, 8 * (size_t)n, cudaMemcpyHostToDevice);
+    cudaError_t e = launch_debug_hits(scene->args(), dcn, dr, (int)n, P, dh, 0);
+    if (e == cudaSuccess && P) e = cudaMemcpy(hits, dh, (size_t)n * P, cudaMemcpyDeviceToHost);
+    cudaFree(dcn);
+    cudaFree(dr);
+    cudaFree(dh);
+    if (e != cudaSuccess) return set_err(PRRTC_ECUDA, std::string("prrtc_debug_sphere_hits: ") + cudaGetErrorString(e));
+    return PRRTC_OK;
+}
+
+int prrtc_debug_nn(const double* tree, uint32_t count, uint32_t dof, const double* q,
+                   uint32_t n_queries, int device, uint32_t* index, double* sq_dist) {
+    if (!tree || !q || !index || !sq_dist) return set_err(PRRTC_EINVAL, "prrtc_debug_nn: null argument");
+    if (count == 0) return set_err(PRRTC_EINVAL, "nearest_serial: empty tree snapshot");
+    if (dof == 0 || dof > PRRTC_MAX_DOF) return set_err(PRRTC_EINVAL, "prrtc_debug_nn: bad dof");
+    int rc = check_device(device);
+    if (rc) return rc;
+    cudaSetDevice(device);
+    const long long cap = ((long long)count + 31) / 32 * 32;
+    std::vector<double> soa((size_t)cap * dof, 0.0);
+    for (uint32_t i = 0; i < count; ++i)
+        for (uint32_t d = 0; d < dof; ++d) soa[(size_t)d * cap + i] = tree[(size_t)i * dof + d];
+    double *ds = nullptr, *dq = nullptr, *dd = nullptr;
+    uint32_t* di = nullptr;
+    if ((rc = dmalloc(&ds, soa.size())) || (rc = dmalloc(&dq, (size_t)n_queries * dof)) ||
+        (rc = dmalloc(&dd, n_queries)) || (rc = dmalloc(&di, n_queries))) {
+        cudaFree(ds);
+        cudaFree(dq);
+        cudaFree(dd);
+        return rc;
+    }
+    cudaMemcpy(ds, soa.data(), 8 * soa.size(), cudaMemcpyHostToDevice);
+    cudaMemcpy(dq, q, 8 * (size_t)n_queries * dof, cudaMemcpyHostToDevice);
+    cudaError_t e = launch_debug_nn(ds, cap, (int)count, (int)dof, dq, (int)n_queries, di, dd, 0);
+    if (e == cudaSuccess) e = cudaMemcpy(index, di, 4 * (size_t)n_queries, cudaMemcpyDeviceToHost);
+    if (e == cudaSuccess) e = cudaMemcpy(sq_dist, dd, 8 * (size_t)n_queries, cudaMemcpyDeviceToHost);
+    cudaFree(ds);
+    cudaFree(dq);
+    cudaFree(dd);
+    cudaFree(di);
+    if (e != cudaSuccess) return set_err(PRRTC_ECUDA, std::string("prrtc_debug_nn: ") + cudaGetErrorString(e));
+    return PRRTC_OK;
+}
+
+int prrtc_debug_halton(const uint32_t* bases, const uint64_t* indices, uint32_t n, int device,
+                       double* out) {
+    if (!bases || !indices || !out) return set_err(PRRTC_EINVAL, "prrtc_debug_halton: null argument");
+    for (uint32_t i = 0; i < n; ++i)
+        if (bases[i] < 2) return set_err(PRRTC_EINVAL, "halton_value: base must be >= 2");
+    if (n == 0) return PRRTC_OK;
+    int rc = check_device(device);
+    if (rc) return rc;
+    cudaSetDevice(device);
+    uint32_t* db = nullptr;
+    uint64_t* di = nullptr;
+    double* dout = nullptr;
+    if ((rc = dmalloc(&db, n)) || (rc = dmalloc(&di, n)) || (rc = dmalloc(&dout, n))) {
+        cudaFree(db);
+        cudaFree(di);
+        return rc;
+    }
+    cudaMemcpy(db, bases, 4 * (size_t)n, cudaMemcpyHostToDevice);
+    cudaMemcpy(di, indices, 8 * (size_t)n, cudaMemcpyHostToDevice);
+    cudaError_t e = launch_debug_halton(db, di, (int)n, dout, 0);
+    if (e == cudaSuccess) e = cudaMemcpy(out, dout, 8 * (size_t)n, cudaMemcpyDeviceToHost);
+    cudaFree(db);
+    cudaFree(di);
+    cudaFree(dout);
+    if (e != cudaSuccess) return set_err(PRRTC_ECUDA, std::string("prrtc_debug_halton: ") + cudaGetErrorString(e));
+    return PRRTC_OK;
+}
+
+int prrtc_debug_sample(const prrtc_robot* robot, uint64_t index0, uint32_t n, double* out) {
+    if (!robot || !out) return set_err(PRRTC_EINVAL, "prrtc_debug_sample: null argument");
+    if (n == 0) return PRRTC_OK;
+    int rc = check_device(robot->device);
+    if (rc) return rc;
+    cudaSetDevice(robot->device);
+    double* dout = nullptr;
+    if ((rc = dmalloc(&dout, (size_t)n * robot->dof))) return rc;
+    cudaError_t e = launch_debug_sample(robot->args(), index0, (int)n, dout, 0);
+    if (e == cudaSuccess) e = cudaMemcpy(out, dout, 8 * (size_t)n * robot->dof, cudaMemcpyDeviceToHost);
+    cudaFree(dout);
+    if (e != cudaSuccess) return set_err(PRRTC_ECUDA, std::string("prrtc_debug_sample: ") + cudaGetErrorString(e));
+    return PRRTC_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,692 @@
+// prrtc_device.cuh — sm_100a device routines of the B200 pRRTC planner.
+//
+// Everything here runs inside one CTA (default 128 threads = 4 warps):
+//   * exact FP64 restatements of the reference scalar arithmetic where the
+//     reference's result must be reproduced bit-for-bit (Halton, lerp,
+//     squared distance, the sphere predicates' guard-band fallback);
+//   * the FP32 fast paths (forward kinematics, predicates) that do the bulk
+//     of the work on the FP32 FMA pipe;
+//   * the CTA-wide routines: nearest-neighbour scan (warp-shuffle argmin),
+//     SIMT edge validation (states split over threads, two-stage spheres,
+//     shared-memory-staged primitives, ballot/flag early exit).
+//
+// Reference cross-references are given as file:line of /root/reference/proj.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "prrtc_internal.h"
+
+namespace prrtc_b200 {
+namespace dev {
+
+constexpr int kMaxDof = 32;
+constexpr int kQueueMax = 512;
+constexpr int kNoBad = 0x7fffffff;
+
+// ---------------------------------------------------------------------------
+// memory-model helpers (gpu scope)
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ int ld_acquire(const int* p) {
+    int v;
+    asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
+__device__ __forceinline__ unsigned ld_acquire_u(const unsigned* p) {
+    unsigned v;
+    asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
+__device__ __forceinline__ void st_release(int* p, int v) {
+    asm volatile("st.release.gpu.global.b32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+__device__ __forceinline__ void st_release_u(unsigned* p, unsigned v) {
+    asm volatile("st.release.gpu.global.b32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+__device__ __forceinline__ long long globaltimer() {
+    long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
+
+// ---------------------------------------------------------------------------
+// exact FP64 scalar arithmetic (no FMA contraction: __d*_rn are never fused)
+// ---------------------------------------------------------------------------
+
+// kernels_scalar.cpp:18-22 (lerp) — a + t*(b-a), one element.
+__device__ __forceinline__ double lerp_exact(double a, double b, double t) {
+    return __dadd_rn(a, __dmul_rn(t, __dsub_rn(b, a)));
+}
+
+// sampling.cpp:8-18 (halton_value): f /= b; r += f*(i mod b); i /= b.
+__device__ __forceinline__ double halton_exact(unsigned base, unsigned long long index) {
+    double f = 1.0, r = 0.0;
+    const double b = static_cast<double>(base);
+    if (index >> 32) {
+        while (index > 0) {
+            f = __ddiv_rn(f, b);
+            r = __dadd_rn(r, __dmul_rn(f, static_cast<double>(index % base)));
+            index /= base;
+        }
+    } else {
+        unsigned i = static_cast<unsigned>(index);  // same digits, 32-bit divide
+        while (i > 0) {
+            f = __ddiv_rn(f, b);
+            const unsigned q = i / base;
+            r = __dadd_rn(r, __dmul_rn(f, static_cast<double>(i - q * base)));
+            i = q;
+        }
+    }
+    return r;
+}
+
+// sampling.cpp:39-51 (sample_config), one dimension.
+__device__ __forceinline__ double sample_dim(double h, double lo, double hi) {
+    double v = __dadd_rn(lo, __dmul_rn(h, __dsub_rn(hi, lo)));
+    if (v >= hi) v = nextafter(hi, lo);
+    return v;
+}
+
+// ---------------------------------------------------------------------------
+// exact FP64 predicates — kernels_detail.hpp:17-50, same operation order
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ double clamp01_exact(double t) {
+    if (t < 0.0) t = 0.0;
+    if (t > 1.0) t = 1.0;
+    return t;
+}
+
+// kernels_detail.hpp:17-23
+__device__ __noinline__ bool sphere_sphere_exact(double px, double py, double pz, double pr,
+                                                 double sx, double sy, double sz, double sr) {
+    const double dx = __dsub_rn(px, sx), dy = __dsub_rn(py, sy), dz = __dsub_rn(pz, sz);
+    const double d2 = __dadd_rn(__dadd_rn(__dmul_rn(dx, dx), __dmul_rn(dy, dy)), __dmul_rn(dz, dz));
+    const double rr = __dadd_rn(pr, sr);
+    return d2 < __dmul_rn(rr, rr);
+}
+
+// kernels_detail.hpp:25-35
+__device__ __noinline__ bool sphere_capsule_exact(double px, double py, double pz, double pr,
+                                                  const double* c /* a, ab, inv, r */) {
+    const double pax = __dsub_rn(px, c[0]), pay = __dsub_rn(py, c[1]), paz = __dsub_rn(pz, c[2]);
+    const double dot = __dadd_rn(__dadd_rn(__dmul_rn(pax, c[3]), __dmul_rn(pay, c[4])),
+                                 __dmul_rn(paz, c[5]));
+    const double t = clamp01_exact(__dmul_rn(dot, c[6]));
+    const double dx = __dsub_rn(pax, __dmul_rn(t, c[3]));
+    const double dy = __dsub_rn(pay, __dmul_rn(t, c[4]));
+    const double dz = __dsub_rn(paz, __dmul_rn(t, c[5]));
+    const double d2 = __dadd_rn(__dadd_rn(__dmul_rn(dx, dx), __dmul_rn(dy, dy)), __dmul_rn(dz, dz));
+    const double rr = __dadd_rn(pr, c[7]);
+    return d2 < __dmul_rn(rr, rr);
+}
+
+// kernels_detail.hpp:37-50
+__device__ __noinline__ bool sphere_box_exact(double px, double py, double pz, double pr,
+                                              const double* b /* m[9], t[3], h[3] */) {
+    const double wx = __dsub_rn(px, b[9]), wy = __dsub_rn(py, b[10]), wz = __dsub_rn(pz, b[11]);
+    const double lx = __dadd_rn(__dadd_rn(__dmul_rn(b[0], wx), __dmul_rn(b[1], wy)), __dmul_rn(b[2], wz));
+    const double ly = __dadd_rn(__dadd_rn(__dmul_rn(b[3], wx), __dmul_rn(b[4], wy)), __dmul_rn(b[5], wz));
+    const double lz = __dadd_rn(__dadd_rn(__dmul_rn(b[6], wx), __dmul_rn(b[7], wy)), __dmul_rn(b[8], wz));
+    const double hx = b[12], hy = b[13], hz = b[14];
+    const double cx = lx < -hx ? -hx : (lx > hx ? hx : lx);
+    const double cy = ly < -hy ? -hy : (ly > hy ? hy : ly);
+    const double cz = lz < -hz ? -hz : (lz > hz ? hz : lz);
+    const double dx = __dsub_rn(lx, cx), dy = __dsub_rn(ly, cy), dz = __dsub_rn(lz, cz);
+    const double d2 = __dadd_rn(__dadd_rn(__dmul_rn(dx, dx), __dmul_rn(dy, dy)), __dmul_rn(dz, dz));
+    return d2 < __dmul_rn(pr, pr);
+}
+
+// ---------------------------------------------------------------------------
+// FP32 fast predicates. Each returns the squared distance d2 and the
+// combined radius rr of the test "d2 < rr*rr" evaluated in FP32.
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ void sph_d2(float px, float py, float pz, float4 s, float& d2) {
+    const float dx = px - s.x, dy = py - s.y, dz = pz - s.z;
+    d2 = fmaf(dx, dx, fmaf(dy, dy, dz * dz));
+}
+__device__ __forceinline__ void cap_d2(float px, float py, float pz, const float* c, float& d2) {
+    const float pax = px - c[0], pay = py - c[1], paz = pz - c[2];
+    float t = fmaf(pax, c[3], fmaf(pay, c[4], paz * c[5])) * c[6];
+    t = fminf(fmaxf(t, 0.0f), 1.0f);
+    const float dx = fmaf(-t, c[3], pax), dy = fmaf(-t, c[4], pay), dz = fmaf(-t, c[5], paz);
+    d2 = fmaf(dx, dx, fmaf(dy, dy, dz * dz));
+}
+__device__ __forceinline__ void box_d2(float px, float py, float pz, const float* b, float& d2) {
+    const float wx = px - b[9], wy = py - b[10], wz = pz - b[11];
+    const float lx = fmaf(b[0], wx, fmaf(b[1], wy, b[2] * wz));
+    const float ly = fmaf(b[3], wx, fmaf(b[4], wy, b[5] * wz));
+    const float lz = fmaf(b[6], wx, fmaf(b[7], wy, b[8] * wz));
+    const float dx = lx - fminf(fmaxf(lx, -b[12]), b[12]);
+    const float dy = ly - fminf(fmaxf(ly, -b[13]), b[13]);
+    const float dz = lz - fminf(fmaxf(lz, -b[14]), b[14]);
+    d2 = fmaf(dx, dx, fmaf(dy, dy, dz * dz));
+}
+
+// Guard band: returns 1 = certainly hit, 0 = certainly free, -1 = undecided
+// (|distance - rr| <= eps: re-evaluate in exact FP64).
+__device__ __forceinline__ int band(float d2, float rr, float eps) {
+    const float hi = rr + eps;
+    if (d2 > hi * hi) return 0;
+    const float lo = rr - eps;
+    if (lo > 0.0f && d2 < lo * lo) return 1;
+    return -1;
+}
+
+// ---------------------------------------------------------------------------
+// CTA context: pointers into dynamic shared memory
+// ---------------------------------------------------------------------------
+struct Ctx {
+    // robot (shared memory copy of the packed words)
+    int L, dof, S, NP, MF;
+    const int4* info;      // kind, parent, q_index, fine_off
+    const int* nfine;
+    const float* geo;      // [L][GEO_STRIDE]
+    const float4* fine;    // [S]
+    const int2* pairs;     // [NP]
+    const unsigned* bases; // [dof]
+    const int* flink;      // [S] link of each fine sphere
+    const double* fine_r64;  // global
+    const double* limits;    // global [dof][2]
+    // scene (shared memory copy)
+    int ns, nb, nc, P;
+    const float4* sph;
+    const float* box;
+    const float* cap;
+    float eps, cpad;
+    SceneF64 s64;  // global FP64 mirror
+    // per-chunk buffers
+    int NS;          // states per chunk (multiple of 32)
+    float* pose;     // [L][12][NS]
+    float* ccen;     // [L][3][NS]
+    float* qf;       // [dof][NS]
+    int* sgroup;     // [NS] group id, -1 = inactive
+    int* sbad;       // [NS]
+    int* queue;      // [kQueueMax]
+    int* pqueue;     // [kQueueMax]
+    // CTA scalars
+    int* ictl;       // [32] misc ints
+    double* dcfg;    // [8][kMaxDof] scratch configs
+    double* red_d;   // [nwarps]
+    int* red_i;      // [nwarps]
+    int nthreads;
+    // stats (per-thread accumulators)
+    unsigned long long tests;
+    unsigned long long flops;  // algorithmic FP32 flops
+};
+
+// ictl slots
+enum : int {
+    IC_QN = 0,      // env queue length
+    IC_PQN,         // pair queue length
+    IC_OVF,         // queue overflow
+    IC_FIRSTBAD,    // min bad group
+    IC_FLAGGED,     // states entering the fine stage
+    IC_TMP0,
+    IC_TMP1,
+    IC_TMP2,
+    IC_TMP3,
+    IC_TMP4,
+    IC_TMP5,
+    IC_TMP6,
+    IC_TMP7,
+    IC_COUNT = 32
+};
+
+// dcfg rows
+enum : int { DC_A = 0, DC_B, DC_SAMPLE, DC_NEW, DC_NN, DC_TARGET, DC_TMP, DC_TMP2 };
+
+__device__ __forceinline__ double* dc(Ctx& c, int row) { return c.dcfg + row * kMaxDof; }
+
+// Posed point R*p + t from a pose stored as [12][NS] column (state s).
+// Explicit fmaf order: identical bits wherever it is used (FK parity).
+__device__ __forceinline__ float3 pose_point(const Ctx& c, int l, int s, float px, float py,
+                                             float pz) {
+    const float* P = c.pose + (size_t)l * 12 * c.NS + s;
+    const int N = c.NS;
+    float3 o;
+    o.x = __fmaf_rn(P[0 * N], px, __fmaf_rn(P[1 * N], py, __fmaf_rn(P[2 * N], pz, P[9 * N])));
+    o.y = __fmaf_rn(P[3 * N], px, __fmaf_rn(P[4 * N], py, __fmaf_rn(P[5 * N], pz, P[10 * N])));
+    o.z = __fmaf_rn(P[6 * N], px, __fmaf_rn(P[7 * N], py, __fmaf_rn(P[8 * N], pz, P[11 * N])));
+    return o;
+}
+
+// ---------------------------------------------------------------------------
+// forward kinematics for the chunk's states (kinematics.cpp:92-103), FP32
+//   phase A: (state, link) items -> local transform origin_tf * motion(q)
+//   phase B: 3 lanes per state compose world = parent * local row by row
+//   phase C: (state, link) items -> posed coarse centers
+// ---------------------------------------------------------------------------
+__device__ __noinline__ void fk_chunk(Ctx& c, int cnt) {
+    const int tid = threadIdx.x;
+    const int NS = c.NS;
+    // phase A
+    for (int it = tid; it < c.L * NS; it += c.nthreads) {
+        const int s = it % NS, l = it / NS;
+        if (s >= cnt) continue;
+        const int4 inf = c.info[l];
+        const float* g = c.geo + l * GEO_STRIDE;
+        float* P = c.pose + (size_t)l * 12 * NS + s;
+        if (inf.x == PRRTC_JOINT_REVOLUTE) {
+            const float q = c.qf[inf.z * NS + s];
+            float sn, cs;
+            sincosf(q, &sn, &cs);
+            const float omc = 1.0f - cs;
+#pragma unroll
+            for (int k = 0; k < 9; ++k) {
+                P[k * NS] = __fmaf_rn(cs, g[k], __fmaf_rn(sn, g[9 + k], __fmul_rn(omc, g[18 + k])));
+            }
+            P[9 * NS] = g[27];
+            P[10 * NS] = g[28];
+            P[11 * NS] = g[29];
+        } else {
+#pragma unroll
+            for (int k = 0; k < 9; ++k) P[k * NS] = g[k];
+            if (inf.x == PRRTC_JOINT_PRISMATIC) {
+                const float q = c.qf[inf.z * NS + s];
+                P[9 * NS] = __fmaf_rn(g[30], q, g[27]);
+                P[10 * NS] = __fmaf_rn(g[31], q, g[28]);
+                P[11 * NS] = __fmaf_rn(g[32], q, g[29]);
+            } else {
+                P[9 * NS] = g[27];
+                P[10 * NS] = g[28];
+                P[11 * NS] = g[29];
+            }
+        }
+    }
+    __syncthreads();
+    // phase B: lanes (s, r), r in 0..3 (r == 3 idle), whole warps iterate
+    const int per = c.nthreads / 4;
+    for (int sb = 0; sb < cnt; sb += per) {
+        const int s = sb + tid / 4, r = tid & 3;
+        const bool act = (s < cnt) && (r < 3);
+        for (int l = 0; l < c.L; ++l) {
+            const int par = c.info[l].y;
+            float Rl[9], tl[3];
+            if (act && par >= 0) {
+                const float* P = c.pose + (size_t)l * 12 * NS + s;
+#pragma unroll
+                for (int k = 0; k < 9; ++k) Rl[k] = P[k * NS];
+                tl[0] = P[9 * NS];
+                tl[1] = P[10 * NS];
+                tl[2] = P[11 * NS];
+            }
+            __syncwarp();
+            if (act && par >= 0) {
+                const float* Q = c.pose + (size_t)par * 12 * NS + s;
+                const float a0 = Q[(3 * r + 0) * NS], a1 = Q[(3 * r + 1) * NS],
+                            a2 = Q[(3 * r + 2) * NS], tp = Q[(9 + r) * NS];
+                float* P = c.pose + (size_t)l * 12 * NS + s;
+#pragma unroll
+                for (int j = 0; j < 3; ++j) {
+                    P[(3 * r + j) * NS] =
+                        __fmaf_rn(a0, Rl[j], __fmaf_rn(a1, Rl[3 + j], __fmul_rn(a2, Rl[6 + j])));
+                }
+                P[(9 + r) * NS] = __fmaf_rn(a0, tl[0], __fmaf_rn(a1, tl[1], __fmaf_rn(a2, tl[2], tp)));
+            }
+            __syncwarp();
+        }
+    }
+    __syncthreads();
+    // phase C: coarse centers
+    for (int it = tid; it < c.L * NS; it += c.nthreads) {
+        const int s = it % NS, l = it / NS;
+        if (s >= cnt) continue;
+        const float* g = c.geo + l * GEO_STRIDE;
+        const float3 o = pose_point(c, l, s, g[33], g[34], g[35]);
+        float* C = c.ccen + (size_t)l * 3 * NS + s;
+        C[0] = o.x;
+        C[NS] = o.y;
+        C[2 * NS] = o.z;
+    }
+    __syncthreads();
+}
+
+// ---------------------------------------------------------------------------
+// exact fine-sphere vs primitive (p indexes spheres, boxes, capsules in that
+// order). FP32 with guard band, FP64 exact fallback on the same inputs.
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ bool fine_vs_prim(const Ctx& c, float3 x, float rf, double rd, int p) {
+    float d2, rr;
+    int v;
+    if (p < c.ns) {
+        const float4 s = c.sph[p];
+        sph_d2(x.x, x.y, x.z, s, d2);
+        rr = rf + s.w;
+        v = band(d2, rr, c.eps);
+        if (v >= 0) return v != 0;
+        const double* S = c.s64.s + 4 * p;
+        return sphere_sphere_exact(x.x, x.y, x.z, rd, S[0], S[1], S[2], S[3]);
+    } else if (p < c.ns + c.nb) {
+        const int b = p - c.ns;
+        box_d2(x.x, x.y, x.z, c.box + b * BOX_STRIDE, d2);
+        v = band(d2, rf, c.eps);
+        if (v >= 0) return v != 0;
+        return sphere_box_exact(x.x, x.y, x.z, rd, c.s64.b + BOX_STRIDE * b);
+    } else {
+        const int k = p - c.ns - c.nb;
+        const float* C = c.cap + k * CAP_STRIDE;
+        cap_d2(x.x, x.y, x.z, C, d2);
+        rr = rf + C[7];
+        v = band(d2, rr, c.eps);
+        if (v >= 0) return v != 0;
+        return sphere_capsule_exact(x.x, x.y, x.z, rd, c.s64.c + CAP_STRIDE * k);
+    }
+}
+
+// algorithmic flops of one sphere test (kernels_detail.hpp:17-50 counted:
+// mul/add/sub = 1, FMA = 2): sphere 10, box 27, capsule 22
+__device__ __forceinline__ int test_flops(const Ctx& c, int p) {
+    return p < c.ns ? 10 : (p < c.ns + c.nb ? 27 : 22);
+}
+
+// coarse (padded) sphere vs primitive, FP32 only (conservative)
+__device__ __forceinline__ bool coarse_vs_prim(const Ctx& c, float x, float y, float z, float rc,
+                                               int p) {
+    float d2;
+    if (p < c.ns) {
+        const float4 s = c.sph[p];
+        sph_d2(x, y, z, s, d2);
+        const float rr = rc + s.w;
+        return d2 < rr * rr;
+    } else if (p < c.ns + c.nb) {
+        box_d2(x, y, z, c.box + (p - c.ns) * BOX_STRIDE, d2);
+        return d2 < rc * rc;
+    } else {
+        const float* C = c.cap + (p - c.ns - c.nb) * CAP_STRIDE;
+        cap_d2(x, y, z, C, d2);
+        const float rr = rc + C[7];
+        return d2 < rr * rr;
+    }
+}
+
+// self pair fine spheres (collision.cpp:89-98 / kernels_detail.hpp:17-23)
+__device__ __forceinline__ bool fine_pair(const Ctx& c, float3 a, int ja, float3 b, int jb) {
+    float d2;
+    const float4 fa = c.fine[ja], fb = c.fine[jb];
+    sph_d2(a.x, a.y, a.z, make_float4(b.x, b.y, b.z, 0.f), d2);
+    const int v = band(d2, fa.w + fb.w, c.eps);
+    if (v >= 0) return v != 0;
+    return sphere_sphere_exact(a.x, a.y, a.z, c.fine_r64[ja], b.x, b.y, b.z, c.fine_r64[jb]);
+}
+
+__device__ __forceinline__ void mark_bad(Ctx& c, int s, bool early_exit) {
+    c.sbad[s] = 1;
+    atomicMin(&c.ictl[IC_FIRSTBAD], c.sgroup[s]);
+    (void)early_exit;
+}
+
+// skip test for early exit: chain mode skips groups >= first bad;
+// independent mode skips states already bad.
+__device__ __forceinline__ bool skip_state(const Ctx& c, int s, bool early_exit, bool indep) {
+    if (!early_exit) return false;
+    if (indep) return *(volatile int*)&c.sbad[s] != 0;
+    return c.sgroup[s] >= *(volatile int*)&c.ictl[IC_FIRSTBAD];
+}
+
+// warp-aggregated push into a shared-memory queue
+__device__ __forceinline__ void queue_push(int* q, int* qn, int* ovf, bool pred, int val) {
+    const unsigned m = __ballot_sync(__activemask(), pred);
+    if (!pred) return;
+    const int lane = threadIdx.x & 31;
+    const int leader = __ffs(m) - 1;
+    int base = 0;
+    if (lane == leader) base = atomicAdd(qn, __popc(m));
+    base = __shfl_sync(m, base, leader);
+    const int pos = base + __popc(m & ((1u << lane) - 1));
+    if (pos < kQueueMax) q[pos] = val; else *ovf = 1;
+}
+
+// ---------------------------------------------------------------------------
+// brute-force fine-only check of the chunk (collision.cpp:100-128)
+// ---------------------------------------------------------------------------
+__device__ void brute_chunk(Ctx& c, int cnt, bool early_exit, bool indep) {
+    const int tid = threadIdx.x, NS = c.NS;
+    const long long items = (long long)NS * c.S * c.P;
+    for (long long it = tid; it < items; it += c.nthreads) {
+        const int s = (int)(it % NS);
+        const long long rest = it / NS;
+        const int j = (int)(rest % c.S), p = (int)(rest / c.S);
+        if (s >= cnt || c.sgroup[s] < 0 || skip_state(c, s, early_exit, indep)) continue;
+        const int l = c.flink[j];
+        const float4 f = c.fine[j];
+        const float3 x = pose_point(c, l, s, f.x, f.y, f.z);
+        ++c.tests;
+        c.flops += 18 + test_flops(c, p);
+        if (fine_vs_prim(c, x, f.w, c.fine_r64[j], p)) mark_bad(c, s, early_exit);
+    }
+    // self pairs: items (state, pair, i) loop j
+    const long long pit = (long long)NS * c.NP * c.MF;
+    for (long long it = tid; it < pit; it += c.nthreads) {
+        const int s = (int)(it % NS);
+        const long long rest = it / NS;
+        const int i = (int)(rest % c.MF), pr = (int)(rest / c.MF);
+        if (s >= cnt || c.sgroup[s] < 0 || skip_state(c, s, early_exit, indep)) continue;
+        const int2 ab = c.pairs[pr];
+        if (i >= c.nfine[ab.x]) continue;
+        const int ja = c.info[ab.x].w + i;
+        const float4 fa = c.fine[ja];
+        const float3 xa = pose_point(c, ab.x, s, fa.x, fa.y, fa.z);
+        const int nb = c.nfine[ab.y], jb0 = c.info[ab.y].w;
+        c.tests += nb;
+        for (int k = 0; k < nb; ++k) {
+            const float4 fb = c.fine[jb0 + k];
+            const float3 xb = pose_point(c, ab.y, s, fb.x, fb.y, fb.z);
+            c.flops += 28;
+            if (fine_pair(c, xa, ja, xb, jb0 + k)) {
+                mark_bad(c, s, early_exit);
+                break;
+            }
+        }
+    }
+}
+
+// ---------------------------------------------------------------------------
+// validate the chunk's states (qf/sgroup already set): FK + collision.
+// Two-stage (collision.cpp:130-204): padded coarse spheres flag
+// (state, link, primitive) triples and (state, pair) pairs into shared
+// queues; the fine stage re-tests only those. Result: sbad[], IC_FIRSTBAD.
+// ---------------------------------------------------------------------------
+__device__ __noinline__ void check_chunk(Ctx& c, int cnt, bool two_stage, bool early_exit, bool indep) {
+    const int tid = threadIdx.x, NS = c.NS;
+    for (int s = tid; s < NS; s += c.nthreads) c.sbad[s] = 0;
+    if (tid == 0) {
+        c.ictl[IC_QN] = 0;
+        c.ictl[IC_PQN] = 0;
+        c.ictl[IC_OVF] = 0;
+        c.ictl[IC_FIRSTBAD] = kNoBad;
+    }
+    fk_chunk(c, cnt);  // ends with __syncthreads
+    if (!two_stage) {
+        brute_chunk(c, cnt, early_exit, indep);
+        __syncthreads();
+        return;
+    }
+    // stage 1: coarse spheres vs primitives; s fastest -> warp-uniform (l, p)
+    const int LP = c.L * c.P;
+    for (int it = tid; it < NS * LP; it += c.nthreads) {
+        const int s = it % NS, rest = it / NS;
+        const int l = rest % c.L, p = rest / c.L;
+        bool hit = false;
+        if (s < cnt && c.sgroup[s] >= 0) {
+            const float* C = c.ccen + (size_t)l * 3 * NS + s;
+            const float rc = c.geo[l * GEO_STRIDE + 36] + c.cpad;
+            hit = coarse_vs_prim(c, C[0], C[NS], C[2 * NS], rc, p);
+            ++c.tests;
+            c.flops += test_flops(c, p);
+        }
+        queue_push(c.queue, &c.ictl[IC_QN], &c.ictl[IC_OVF], hit, s | (l << 8) | (p << 16));
+    }
+    for (int it = tid; it < NS * c.NP; it += c.nthreads) {
+        const int s = it % NS, pr = it / NS;
+        bool hit = false;
+        if (s < cnt && c.sgroup[s] >= 0) {
+            const int2 ab = c.pairs[pr];
+            const float* A = c.ccen + (size_t)ab.x * 3 * NS + s;
+            const float* B = c.ccen + (size_t)ab.y * 3 * NS + s;
+            const float dx = A[0] - B[0], dy = A[NS] - B[NS], dz = A[2 * NS] - B[2 * NS];
+            const float rr = c.geo[ab.x * GEO_STRIDE + 36] + c.geo[ab.y * GEO_STRIDE + 36] + 2.0f * c.cpad;
+            hit = fmaf(dx, dx, fmaf(dy, dy, dz * dz)) < rr * rr;
+            ++c.tests;
+            c.flops += 10;
+        }
+        queue_push(c.pqueue, &c.ictl[IC_PQN], &c.ictl[IC_OVF], hit, s | (pr << 8));
+    }
+    __syncthreads();
+    if (c.ictl[IC_OVF]) {  // too many flags: exact brute force for the chunk
+        brute_chunk(c, cnt, early_exit, indep);
+        __syncthreads();
+        return;
+    }
+    const int qn = c.ictl[IC_QN], pqn = c.ictl[IC_PQN];
+    if (qn == 0 && pqn == 0) return;  // nothing flagged: every state free
+    // stage 2a: flagged (state, link, prim) x fine spheres of the link
+    for (int it = tid; it < qn * c.MF; it += c.nthreads) {
+        const int e = c.queue[it / c.MF], k = it % c.MF;
+        const int s = e & 0xff, l = (e >> 8) & 0xff, p = e >> 16;
+        if (k >= c.nfine[l] || skip_state(c, s, early_exit, indep)) continue;
+        const int j = c.info[l].w + k;
+        const float4 f = c.fine[j];
+        const float3 x = pose_point(c, l, s, f.x, f.y, f.z);
+        ++c.tests;
+        c.flops += 18 + test_flops(c, p);
+        if (fine_vs_prim(c, x, f.w, c.fine_r64[j], p)) mark_bad(c, s, early_exit);
+    }
+    // stage 2b: flagged (state, pair): fine x fine
+    for (int it = tid; it < pqn * c.MF; it += c.nthreads) {
+        const int e = c.pqueue[it / c.MF], i = it % c.MF;
+        const int s = e & 0xff, pr = e >> 8;
+        const int2 ab = c.pairs[pr];
+        if (i >= c.nfine[ab.x] || skip_state(c, s, early_exit, indep)) continue;
+        const int ja = c.info[ab.x].w + i;
+        const float4 fa = c.fine[ja];
+        const float3 xa = pose_point(c, ab.x, s, fa.x, fa.y, fa.z);
+        const int nb = c.nfine[ab.y], jb0 = c.info[ab.y].w;
+        c.tests += nb;
+        for (int k = 0; k < nb; ++k) {
+            const float4 fb = c.fine[jb0 + k];
+            const float3 xb = pose_point(c, ab.y, s, fb.x, fb.y, fb.z);
+            c.flops += 28;
+            if (fine_pair(c, xa, ja, xb, jb0 + k)) {
+                mark_bad(c, s, early_exit);
+                break;
+            }
+        }
+    }
+    __syncthreads();
+}
+
+// ---------------------------------------------------------------------------
+// chain states. Points p_0 = A, p_k = lerp(A, B, k/n) (k < n), p_n = B
+// (planner.cpp:35-44 step_target; extend is the n = 1 case). State g covers
+// sample i = g % n_cc + 1 of sub-edge k = g / n_cc + 1 (collision.cpp:13-21:
+// the far endpoint is copied exactly); a bitwise-equal sub-edge collapses to
+// one check of its far end (collision.cpp:215).
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ double chain_point(const double* A, const double* B, int d, long long k,
+                                              long long n) {
+    if (k == 0) return A[d];
+    if (k >= n) return B[d];
+    return lerp_exact(A[d], B[d], __ddiv_rn((double)k, (double)n));
+}
+
+__device__ void gen_chain_states(Ctx& c, const double* A, const double* B, long long n_sub,
+                                 int n_cc, long long g0, int cnt) {
+    for (int s = threadIdx.x; s < c.NS; s += c.nthreads) {
+        if (s >= cnt) {
+            c.sgroup[s] = -1;
+            continue;
+        }
+        const long long g = g0 + s;
+        const long long k = g / n_cc + 1;
+        const int i = (int)(g % n_cc) + 1;
+        bool eq = true;
+        for (int d = 0; d < c.dof; ++d) {
+            eq &= chain_point(A, B, d, k - 1, n_sub) == chain_point(A, B, d, k, n_sub);
+        }
+        if (eq && i != n_cc) {
+            c.sgroup[s] = -1;
+            continue;
+        }
+        const double t = __ddiv_rn((double)i, (double)n_cc);
+        for (int d = 0; d < c.dof; ++d) {
+            const double to = chain_point(A, B, d, k, n_sub);
+            const double v = (i == n_cc) ? to : lerp_exact(chain_point(A, B, d, k - 1, n_sub), to, t);
+            c.qf[d * c.NS + s] = (float)v;
+        }
+        c.sgroup[s] = (int)(k - 1);
+    }
+    __syncthreads();
+}
+
+// ---------------------------------------------------------------------------
+// nearest neighbour over the published prefix of a tree (nn.cpp:22-29,
+// kernels_scalar.cpp:9-37): exact FP64 keys in the scalar summation order
+// over SoA rows, 128-bit loads (two nodes per load, L1-bypassing .cg since
+// slots become visible while the kernel runs), per-thread strict-< argmin
+// over increasing indices, then warp-shuffle and cross-warp argmin with ties
+// to the lowest index. Returned to every thread.
+// ---------------------------------------------------------------------------
+struct NnOut {
+    int index;
+    double d2;
+};
+__device__ NnOut nn_scan(Ctx& c, const double* cfg, long long cap, int count, const double* q) {
+    const int tid = threadIdx.x;
+    double best = __longlong_as_double(0x7ff0000000000000ll);  // +inf
+    int bi = 0x7fffffff;
+    const int npairs = (count + 1) >> 1;
+    for (int pi = tid; pi < npairs; pi += c.nthreads) {
+        const int n = pi * 2;
+        double a0 = 0.0, a1 = 0.0;
+        for (int d = 0; d < c.dof; ++d) {
+            const double2 v = __ldcg(reinterpret_cast<const double2*>(cfg + d * cap + n));
+            const double qd = q[d];
+            const double e0 = __dsub_rn(v.x, qd), e1 = __dsub_rn(v.y, qd);
+            a0 = __dadd_rn(a0, __dmul_rn(e0, e0));
+            a1 = __dadd_rn(a1, __dmul_rn(e1, e1));
+        }
+        if (a0 < best) {
+            best = a0;
+            bi = n;
+        }
+        if (n + 1 < count && a1 < best) {
+            best = a1;
+            bi = n + 1;
+        }
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        const double ob = __shfl_xor_sync(0xffffffffu, best, o);
+        const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
+        if (ob < best || (ob == best && oi < bi)) {
+            best = ob;
+            bi = oi;
+        }
+    }
+    const int w = tid >> 5, nw = c.nthreads >> 5;
+    if ((tid & 31) == 0) {
+        c.red_d[w] = best;
+        c.red_i[w] = bi;
+    }
+    __syncthreads();
+    if (tid == 0) {
+        double b = c.red_d[0];
+        int i = c.red_i[0];
+        for (int k = 1; k < nw; ++k) {
+            if (c.red_d[k] < b || (c.red_d[k] == b && c.red_i[k] < i)) {
+                b = c.red_d[k];
+                i = c.red_i[k];
+            }
+        }
+        c.red_d[0] = b;
+        c.ictl[IC_TMP0] = i;
+    }
+    __syncthreads();
+    NnOut r{c.ictl[IC_TMP0], c.red_d[0]};
+    __syncthreads();
+    return r;
+}
+
+}  // namespace dev
+}  // namespace prrtc_b200

@@ -1,0 +1,916 @@
+// prrtc_kernels.cu — sm_100a kernels of the B200 pRRTC planner.
+//
+// plan_kernel is the whole reference worker loop (planner.cpp:186-242) as one
+// persistent kernel: every CTA is a "worker"; it takes an unstarted problem
+// from a global ticket (initialising it: endpoint checks, roots), or joins the
+// running problem with the fewest workers, and iterates
+//   balanced pick -> Halton sample -> NN -> dynamic domain -> steer ->
+//   SIMT edge validation -> atomic append -> NN in the opposite tree ->
+//   greedy connect (chunked SIMT validation, appends) -> winner CAS ->
+//   on-device path assembly
+// until the problem is solved / fails, with no host round-trip. Trees are
+// shared by all CTAs on a problem through gpu-scope atomics in HBM.
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "prrtc_b200.h"
+#include "prrtc_device.cuh"
+#include "prrtc_launch.h"
+
+namespace prrtc_b200 {
+
+using namespace dev;
+
+// ---------------------------------------------------------------------------
+// shared memory carve-up (host and device agree through smem_layout)
+// ---------------------------------------------------------------------------
+struct SmemLayout {
+    size_t robot, scene, pose, ccen, qf, sgroup, sbad, queue, pqueue, ictl, dcfg, red_d, red_i,
+        total;
+};
+
+__host__ __device__ inline size_t al16(size_t x) { return (x + 15) & ~size_t(15); }
+
+__host__ __device__ inline SmemLayout smem_layout(int robot_words, int L, int dof, int NS,
+                                                  int nthreads) {
+    SmemLayout s;
+    size_t o = 0;
+    s.robot = o; o = al16(o + 4 * (size_t)robot_words);
+    s.scene = o; o = al16(o + 4 * (size_t)SCENE_MAX_WORDS);
+    s.pose = o;  o = al16(o + 4 * (size_t)L * 12 * NS);
+    s.ccen = o;  o = al16(o + 4 * (size_t)L * 3 * NS);
+    s.qf = o;    o = al16(o + 4 * (size_t)dof * NS);
+    s.sgroup = o; o = al16(o + 4 * (size_t)NS);
+    s.sbad = o;  o = al16(o + 4 * (size_t)NS);
+    s.queue = o; o = al16(o + 4 * (size_t)kQueueMax);
+    s.pqueue = o; o = al16(o + 4 * (size_t)kQueueMax);
+    s.ictl = o;  o = al16(o + 4 * (size_t)IC_COUNT);
+    s.dcfg = o;  o = al16(o + 8 * (size_t)8 * kMaxDof);
+    s.red_d = o; o = al16(o + 8 * (size_t)(nthreads / 32));
+    s.red_i = o; o = al16(o + 4 * (size_t)(nthreads / 32));
+    s.total = o;
+    (void)dof;
+    return s;
+}
+
+size_t smem_bytes(const RobotArgs& r, int ns_max, int nthreads) {
+    return smem_layout(r.n_words, r.n_links, r.dof, ns_max, nthreads).total;
+}
+
+// Copies the packed robot into shared memory and wires the context.
+__device__ void setup_ctx(Ctx& c, unsigned char* smem, const uint32_t* robot_g, int robot_words,
+                          const double* fine_r64, const double* limits, int NS) {
+    const int tid = threadIdx.x;
+    c.nthreads = blockDim.x;
+    uint32_t* rw = reinterpret_cast<uint32_t*>(smem);
+    // 16-byte vector copy (buffer padded to a multiple of 4 words on host)
+    for (int i = tid; i < robot_words / 4; i += c.nthreads) {
+        reinterpret_cast<uint4*>(rw)[i] = __ldg(reinterpret_cast<const uint4*>(robot_g) + i);
+    }
+    __syncthreads();
+    c.L = rw[RH_NLINKS];
+    c.dof = rw[RH_DOF];
+    c.S = rw[RH_NFINE];
+    c.NP = rw[RH_NPAIRS];
+    c.MF = rw[RH_MAXFINE];
+    c.info = reinterpret_cast<const int4*>(rw + rw[RH_OFF_INFO]);
+    c.nfine = reinterpret_cast<const int*>(rw + rw[RH_OFF_NFINE]);
+    c.geo = reinterpret_cast<const float*>(rw + rw[RH_OFF_GEO]);
+    c.fine = reinterpret_cast<const float4*>(rw + rw[RH_OFF_FINE]);
+    c.pairs = reinterpret_cast<const int2*>(rw + rw[RH_OFF_PAIRS]);
+    c.bases = rw + rw[RH_OFF_BASES];
+    c.flink = reinterpret_cast<const int*>(rw + rw[RH_OFF_FLINK]);
+    c.fine_r64 = fine_r64;
+    c.limits = limits;
+    c.NS = NS;
+    const SmemLayout lay = smem_layout(robot_words, c.L, c.dof, NS, c.nthreads);
+    c.pose = reinterpret_cast<float*>(smem + lay.pose);
+    c.ccen = reinterpret_cast<float*>(smem + lay.ccen);
+    c.qf = reinterpret_cast<float*>(smem + lay.qf);
+    c.sgroup = reinterpret_cast<int*>(smem + lay.sgroup);
+    c.sbad = reinterpret_cast<int*>(smem + lay.sbad);
+    c.queue = reinterpret_cast<int*>(smem + lay.queue);
+    c.pqueue = reinterpret_cast<int*>(smem + lay.pqueue);
+    c.ictl = reinterpret_cast<int*>(smem + lay.ictl);
+    c.dcfg = reinterpret_cast<double*>(smem + lay.dcfg);
+    c.red_d = reinterpret_cast<double*>(smem + lay.red_d);
+    c.red_i = reinterpret_cast<int*>(smem + lay.red_i);
+    c.tests = 0;
+    c.ns = c.nb = c.nc = c.P = 0;  // scene pointers are wired by load_scene
+}
+
+// Stages one scene's primitives in shared memory (the full
+// primitive set is cached in low-latency memory for the whole plan).
+__device__ void load_scene(Ctx& c, unsigned char* sbase, const uint32_t* scene_g, SceneF64 f64) {
+    uint32_t* sw = reinterpret_cast<uint32_t*>(sbase);
+    __syncthreads();
+    const int words = __ldg(scene_g + SH_WORDS);
+    for (int i = threadIdx.x; i < words; i += c.nthreads) sw[i] = __ldg(scene_g + i);
+    __syncthreads();
+    c.ns = sw[SH_NS];
+    c.nb = sw[SH_NB];
+    c.nc = sw[SH_NC];
+    c.P = c.ns + c.nb + c.nc;
+    c.sph = reinterpret_cast<const float4*>(sw + sw[SH_OFF_S]);
+    c.box = reinterpret_cast<const float*>(sw + sw[SH_OFF_B]);
+    c.cap = reinterpret_cast<const float*>(sw + sw[SH_OFF_C]);
+    c.eps = __uint_as_float(sw[SH_EPS]);
+    c.cpad = __uint_as_float(sw[SH_CPAD]);
+    c.s64 = f64;
+}
+
+// the scene words live right after the robot in shared memory; load_scene
+// needs the base, which setup_ctx stored in c.sph. Keep it in a helper.
+__device__ __forceinline__ unsigned char* scene_base(unsigned char* smem, int robot_words, int L,
+                                                     int dof, int NS, int nthreads) {
+    return smem + smem_layout(robot_words, L, dof, NS, nthreads).scene;
+}
+
+// ---------------------------------------------------------------------------
+// tree helpers (tree.hpp:27-53 semantics with device-scope atomics)
+// ---------------------------------------------------------------------------
+struct TreeRef {
+    double* cfg;       // [dof][cap]
+    int* parent;       // [cap]
+    unsigned* ready;   // [cap]
+    int* dd;           // [cap]
+    int* reserved;
+    int* published;
+};
+
+__device__ __forceinline__ TreeRef tree_ref(const PlanArgs& a, int prob, int t, int dof) {
+    TreeRef r;
+    const size_t pt = (size_t)prob * 2 + t;
+    r.cfg = a.cfg + pt * dof * a.stride;
+    r.parent = a.parent + pt * a.stride;
+    r.ready = a.ready + pt * a.stride;
+    r.dd = a.dd + pt * a.stride;
+    r.reserved = &a.ctl[prob].reserved[t];
+    r.published = &a.ctl[prob].published[t];
+    return r;
+}
+
+// Append: reserve a slot (fetch_add), write config/parent, mark the slot
+// ready (release), then advance `published` over the ready prefix. Lock-free:
+// unlike tree.hpp:36-43 no writer waits for its predecessor, which would
+// deadlock CTAs that are not co-resident. Returns the slot or -1 (full).
+__device__ int tree_append(Ctx& c, const PlanArgs& a, const TreeRef& T, const double* cfg,
+                           int parent) {
+    const int tid = threadIdx.x;
+    if (tid == 0) {
+        const int slot = atomicAdd(T.reserved, 1);
+        c.ictl[IC_TMP2] = slot < a.cap ? slot : -1;
+    }
+    __syncthreads();
+    const int slot = c.ictl[IC_TMP2];
+    if (slot < 0) return -1;
+    if (tid < c.dof) {
+        T.cfg[(size_t)tid * a.stride + slot] = cfg[tid];
+        __threadfence();
+    }
+    if (tid == 0) {
+        T.parent[slot] = parent;
+        T.dd[slot] = 0;
+        __threadfence();
+    }
+    __syncthreads();
+    if (tid == 0) {
+        st_release_u(&T.ready[slot], a.epoch);
+        __threadfence();
+        int p = ld_acquire(T.published);
+        while (p < a.cap) {
+            if (ld_acquire_u(&T.ready[p]) != a.epoch) break;
+            const int old = atomicCAS(T.published, p, p + 1);
+            p = (old == p) ? p + 1 : old;
+        }
+    }
+    return slot;
+}
+
+// ---------------------------------------------------------------------------
+// chain validation with appends (extend: n_sub = 1; greedy connect:
+// planner.cpp:66-123, sub-edges validated chunk by chunk, every fully
+// validated sub-edge appended in order before the first invalid one).
+// Returns the number of sub-edges appended, or -1 - appended if the tree
+// filled up, and the last appended slot in *last.
+// ---------------------------------------------------------------------------
+__device__ long long validate_chain(Ctx& c, const PlanArgs& a, const double* A, const double* B,
+                                    long long n_sub, bool do_append, const TreeRef* T,
+                                    int parent0, int* last, const int* done_flag,
+                                    unsigned long long& fk_states, unsigned long long& fine_states,
+                                    bool* stopped) {
+    const int n_cc = a.p.n_cc;
+    const long long total = n_sub * (long long)n_cc;
+    long long appended = 0;
+    int prev = parent0;
+    *stopped = false;
+    for (long long g0 = 0; g0 < total; g0 += c.NS) {
+        if (done_flag) {
+            if (threadIdx.x == 0) c.ictl[IC_TMP3] = ld_acquire(done_flag);
+            __syncthreads();
+            if (c.ictl[IC_TMP3] != 0) {
+                *stopped = true;
+                return appended;
+            }
+        }
+        const int cnt = (int)min((long long)c.NS, total - g0);
+        gen_chain_states(c, A, B, n_sub, n_cc, g0, cnt);
+        if (threadIdx.x == 0) {
+            for (int s = 0; s < cnt; ++s) fk_states += (c.sgroup[s] >= 0);
+        }
+        check_chunk(c, cnt, a.p.two_stage != 0, a.p.early_exit != 0, false);
+        if (threadIdx.x == 0 && (c.ictl[IC_QN] | c.ictl[IC_PQN])) ++fine_states;
+        const int fb = c.ictl[IC_FIRSTBAD];
+        const long long good = (fb != kNoBad) ? (long long)fb : (g0 + cnt) / n_cc;
+        if (do_append) {
+            for (long long k = appended; k < good; ++k) {
+                double* P = dc(c, DC_TMP);
+                if (threadIdx.x < c.dof) P[threadIdx.x] = chain_point(A, B, threadIdx.x, k + 1, n_sub);
+                __syncthreads();
+                const int slot = tree_append(c, a, *T, P, prev);
+                if (slot < 0) {
+                    *last = prev;
+                    return -1 - appended;
+                }
+                prev = slot;
+                ++appended;
+            }
+        } else {
+            appended = good;
+        }
+        __syncthreads();
+        if (fb != kNoBad) break;
+    }
+    *last = prev;
+    return appended;
+}
+
+// ---------------------------------------------------------------------------
+// device path assembly (planner.cpp:125-150): walk meet_a -> root of the
+// start tree (reversed), then meet_b's parents -> root of the goal tree.
+// ---------------------------------------------------------------------------
+__device__ void assemble_path(Ctx& c, const PlanArgs& a, int prob, int meet_a, int meet_b) {
+    const int tid = threadIdx.x;
+    const int dof = c.dof;
+    const TreeRef Ta = tree_ref(a, prob, 0, dof), Tb = tree_ref(a, prob, 1, dof);
+    int* ib = reinterpret_cast<int*>(c.pose);
+    const int ib_cap = c.L * 12 * c.NS;
+    if (tid == 0) {
+        int la = 1, lb = 1;
+        for (int i = meet_a; __ldcg(&Ta.parent[i]) >= 0; i = __ldcg(&Ta.parent[i])) ++la;
+        for (int i = meet_b; __ldcg(&Tb.parent[i]) >= 0; i = __ldcg(&Tb.parent[i])) ++lb;
+        const int len = la + lb - 1;
+        const unsigned long long need = (unsigned long long)len * dof;
+        const unsigned long long off = atomicAdd(a.arena_used, need);
+        c.ictl[IC_TMP4] = len;
+        if (off + need > a.arena_cap || len > ib_cap) {
+            c.ictl[IC_TMP4] = -1;
+        } else {
+            a.ctl[prob].path_off = off;
+            int pos = la - 1;
+            for (int i = meet_a;; i = __ldcg(&Ta.parent[i])) {
+                ib[pos--] = i;  // tree 0
+                if (__ldcg(&Ta.parent[i]) < 0) break;
+            }
+            pos = la;
+            for (int i = __ldcg(&Tb.parent[meet_b]); i >= 0; i = __ldcg(&Tb.parent[i])) {
+                ib[pos++] = i | (1 << 30);  // tree 1
+            }
+        }
+    }
+    __syncthreads();
+    const int len = c.ictl[IC_TMP4];
+    if (len < 0) return;
+    const unsigned long long off = a.ctl[prob].path_off;
+    for (int e = tid; e < len * dof; e += c.nthreads) {
+        const int k = e / dof, d = e % dof;
+        const int v = ib[k];
+        const TreeRef& T = (v >> 30) ? Tb : Ta;
+        a.arena[off + e] = __ldcg(&T.cfg[(size_t)d * a.stride + (v & ((1 << 30) - 1))]);
+    }
+    __threadfence();
+    __syncthreads();
+}
+
+// ---------------------------------------------------------------------------
+// the persistent planner kernel
+// ---------------------------------------------------------------------------
+enum : int { DONE_RUNNING = 0, DONE_SOLVED = 1, DONE_FAILED = 2, DONE_INFEASIBLE = 3 };
+enum : int {
+    MSG_NONE = 0,
+    MSG_START = 1,
+    MSG_GOAL = 2,
+    MSG_CAPACITY = 3,
+    MSG_BUDGET = 4,
+    MSG_ARENA = 5
+};
+
+__device__ void finish_problem(const PlanArgs& a, int prob, int done, int msg) {
+    ProbCtl& C = a.ctl[prob];
+    if (atomicCAS(&C.done, DONE_RUNNING, -1) == DONE_RUNNING) {  // claim
+        C.msg = msg;
+        C.t_end_ns = globaltimer();
+        __threadfence();
+        st_release(&C.done, done);
+    }
+}
+
+// Initialise a freshly claimed problem: endpoint checks (planner.cpp:263-285)
+// and roots (planner.cpp:292-293). Returns true if the search should run.
+__device__ bool init_problem(Ctx& c, const PlanArgs& a, int prob, unsigned long long& fk_states) {
+    const int tid = threadIdx.x, dof = c.dof;
+    ProbCtl& C = a.ctl[prob];
+    double* S = dc(c, DC_A);
+    double* G = dc(c, DC_B);
+    if (tid < dof) {
+        S[tid] = a.starts[(size_t)prob * dof + tid];
+        G[tid] = a.goals[(size_t)prob * dof + tid];
+    }
+    if (tid == 0) C.t_start_ns = globaltimer();
+    __syncthreads();
+    // states: 0 = start, 1 = goal (independent, early exit per state)
+    for (int s = tid; s < c.NS; s += c.nthreads) {
+        c.sgroup[s] = s < 2 ? s : -1;
+        if (s < 2) {
+            for (int d = 0; d < dof; ++d) c.qf[d * c.NS + s] = (float)(s == 0 ? S[d] : G[d]);
+        }
+    }
+    __syncthreads();
+    check_chunk(c, 2, a.p.two_stage != 0, a.p.early_exit != 0, true);
+    if (tid == 0) {
+        fk_states += 2;
+        // within_limits (planner.cpp:25-31): inclusive bounds
+        bool sl = true, gl = true;
+        for (int d = 0; d < dof; ++d) {
+            const double lo = c.limits[2 * d], hi = c.limits[2 * d + 1];
+            sl &= !(S[d] < lo || S[d] > hi);
+            gl &= !(G[d] < lo || G[d] > hi);
+        }
+        int verdict = 0;
+        if (!sl || c.sbad[0]) verdict = 1;
+        else if (!gl || c.sbad[1]) verdict = 2;
+        else {
+            bool eq = true;
+            for (int d = 0; d < dof; ++d) eq &= (S[d] == G[d]);
+            if (eq) verdict = 3;
+        }
+        c.ictl[IC_TMP5] = verdict;
+    }
+    __syncthreads();
+    const int verdict = c.ictl[IC_TMP5];
+    if (verdict == 1 || verdict == 2) {
+        if (tid == 0) {
+            C.started = 1;
+            finish_problem(a, prob, DONE_INFEASIBLE, verdict == 1 ? MSG_START : MSG_GOAL);
+        }
+        __syncthreads();
+        return false;
+    }
+    if (verdict == 3) {  // start == goal: path [start], cost 0 (planner.cpp:279-285)
+        if (tid == 0) {
+            const unsigned long long off = atomicAdd(a.arena_used, (unsigned long long)dof);
+            if (off + dof <= a.arena_cap) {
+                for (int d = 0; d < dof; ++d) a.arena[off + d] = S[d];
+                C.path_off = off;
+                C.path_len = 1;
+                C.winner = 1;
+                __threadfence();
+                C.started = 1;
+                finish_problem(a, prob, DONE_SOLVED, MSG_NONE);
+            } else {
+                C.started = 1;
+                finish_problem(a, prob, DONE_FAILED, MSG_ARENA);
+            }
+        }
+        __syncthreads();
+        return false;
+    }
+    // roots
+    for (int t = 0; t < 2; ++t) {
+        const TreeRef T = tree_ref(a, prob, t, dof);
+        if (tid < dof) T.cfg[(size_t)tid * a.stride] = (t == 0 ? S : G)[tid];
+        if (tid == 0) {
+            T.parent[0] = -1;
+            T.dd[0] = 0;
+            T.ready[0] = a.epoch;
+            *T.reserved = 1;
+            *T.published = 1;
+        }
+    }
+    __threadfence();
+    __syncthreads();
+    if (tid == 0) st_release(&C.started, 1);
+    return true;
+}
+
+// Help mode: join the running problem with the fewest active CTAs (ties to
+// the lowest index). The parallel RRT-Connect iteration is elastic: any
+// number of workers may join a problem at any time. -1 when none is left.
+__device__ int pick_help(Ctx& c, const PlanArgs& a) {
+    const int tid = threadIdx.x;
+    // help mode: running problem with the fewest active CTAs (ties -> lowest)
+    for (int attempt = 0; attempt < 4; ++attempt) {
+        int bk = 0x7fffffff, bp = -1;
+        for (int q = tid; q < a.n_problems; q += c.nthreads) {
+            const ProbCtl& C = a.ctl[q];
+            if (ld_acquire(&C.started) == 1 && ld_acquire(&C.done) == DONE_RUNNING &&
+                __ldcg(&C.iters) < a.p.budget) {
+                const int k = __ldcg(&C.active);
+                if (k < bk) {
+                    bk = k;
+                    bp = q;
+                }
+            }
+        }
+        for (int o = 16; o > 0; o >>= 1) {
+            const int ok = __shfl_xor_sync(0xffffffffu, bk, o);
+            const int op = __shfl_xor_sync(0xffffffffu, bp, o);
+            if (ok < bk || (ok == bk && op >= 0 && (bp < 0 || op < bp))) {
+                bk = ok;
+                bp = op;
+            }
+        }
+        if ((tid & 31) == 0) {
+            c.red_i[tid >> 5] = bp;
+            c.queue[tid >> 5] = bk;
+        }
+        __syncthreads();
+        if (tid == 0) {
+            int k = c.queue[0], p = c.red_i[0];
+            for (int w = 1; w < c.nthreads / 32; ++w) {
+                if (c.queue[w] < k || (c.queue[w] == k && c.red_i[w] >= 0 && (p < 0 || c.red_i[w] < p))) {
+                    k = c.queue[w];
+                    p = c.red_i[w];
+                }
+            }
+            if (p >= 0) {
+                atomicAdd(&a.ctl[p].active, 1);
+                if (ld_acquire(&a.ctl[p].done) != DONE_RUNNING) {
+                    atomicSub(&a.ctl[p].active, 1);
+                    p = -2;  // raced with completion: rescan
+                }
+            }
+            c.ictl[IC_TMP1] = p;
+        }
+        __syncthreads();
+        const int p = c.ictl[IC_TMP1];
+        __syncthreads();
+        if (p >= 0) return p;
+        if (p == -1) return -1;
+    }
+    return -1;
+}
+
+// CheckStats counters (collision.hpp:17-25), reduced per warp then per CTA.
+__device__ void flush_stats(Ctx& c, ProbCtl& C, unsigned long long& fk_states,
+                            unsigned long long& fine_states) {
+    for (int o = 16; o > 0; o >>= 1) c.tests += __shfl_xor_sync(0xffffffffu, c.tests, o);
+    if ((threadIdx.x & 31) == 0 && c.tests) atomicAdd(&C.sphere_tests, c.tests);
+    if (threadIdx.x == 0) {
+        if (fk_states) atomicAdd(&C.fk_calls, fk_states);
+        if (fine_states) atomicAdd(&C.fine_entries, fine_states);
+    }
+    c.tests = 0;
+    fk_states = 0;
+    fine_states = 0;
+}
+
+// Leaving a problem: the last worker out of an unsolved problem fails it
+// (planner.cpp:317-320: all workers exhausted their budgets).
+__device__ void leave_problem(const PlanArgs& a, int prob, int reason_msg) {
+    ProbCtl& C = a.ctl[prob];
+    const int prev = atomicSub(&C.active, 1);
+    if (reason_msg == MSG_CAPACITY) {
+        finish_problem(a, prob, DONE_FAILED, MSG_CAPACITY);
+    } else if (prev == 1 && ld_acquire(&C.done) == DONE_RUNNING) {
+        finish_problem(a, prob, DONE_FAILED, MSG_BUDGET);
+    }
+}
+
+__global__ void __launch_bounds__(128, 4) plan_kernel(PlanArgs a) {
+    extern __shared__ __align__(16) unsigned char smem[];
+    Ctx c;
+    setup_ctx(c, smem, a.robot, reinterpret_cast<const int*>(a.robot)[RH_WORDS], a.fine_r64,
+              a.limits, a.ns_max);
+    const int tid = threadIdx.x;
+    const int dof = c.dof;
+    const int robot_words = reinterpret_cast<const int*>(a.robot)[RH_WORDS];
+    unsigned char* sbase = scene_base(smem, robot_words, c.L, dof, c.NS, c.nthreads);
+    const double R = a.p.dd_radius, delta = a.p.delta;
+
+    for (;;) {
+        unsigned long long fk_states = 0, fine_states = 0;
+        c.tests = 0;
+        int prob = -1;
+        // unstarted problems first: claim, stage its scene, initialise
+        for (;;) {
+            if (tid == 0) c.ictl[IC_TMP1] = atomicAdd(a.next_problem, 1);
+            __syncthreads();
+            const int p = c.ictl[IC_TMP1];
+            __syncthreads();
+            if (p >= a.n_problems) break;
+            const int si = a.prob_scene[p];
+            load_scene(c, sbase, a.scene_words[si], a.scene_f64[si]);
+            if (tid == 0) atomicAdd(&a.ctl[p].active, 1);
+            if (init_problem(c, a, p, fk_states)) {
+                prob = p;
+                break;
+            }
+            flush_stats(c, a.ctl[p], fk_states, fine_states);
+            if (tid == 0) atomicSub(&a.ctl[p].active, 1);
+            __syncthreads();
+        }
+        if (prob < 0) {
+            if (a.p.deterministic) break;
+            prob = pick_help(c, a);
+            if (prob < 0) break;
+            const int si = a.prob_scene[prob];
+            load_scene(c, sbase, a.scene_words[si], a.scene_f64[si]);
+        }
+        ProbCtl& C = a.ctl[prob];
+        unsigned long long local_iter = 0;
+        int leave_msg = MSG_NONE;
+        for (;;) {
+            // ---- iteration header (lead thread) ----
+            if (tid == 0) {
+                int leave = 0;
+                if (ld_acquire(&C.done) != DONE_RUNNING) leave = 1;
+                else if (atomicAdd(&C.iters, 1ull) >= a.p.budget) leave = 2;
+                int from_start = 1, snap = 0;
+                unsigned long long hidx = 0;
+                if (!leave) {
+                    const int la = ld_acquire(&C.published[0]);
+                    const int lb = ld_acquire(&C.published[1]);
+                    // extend_start_tree (planner.hpp:62-65)
+                    from_start = a.p.balance ? (la <= lb) : ((local_iter & 1) == 0);
+                    hidx = a.p.deterministic ? (1ull + a.p.seed + local_iter)
+                                             : (1ull + a.p.seed + atomicAdd(&C.halton_ticket, 1ull));
+                    snap = from_start ? la : lb;
+                }
+                ++local_iter;
+                c.ictl[IC_TMP0] = leave;
+                c.ictl[IC_TMP1] = from_start;
+                c.ictl[IC_TMP2] = snap;
+                reinterpret_cast<unsigned long long*>(c.red_d)[0] = hidx;
+            }
+            __syncthreads();
+            const int leave = c.ictl[IC_TMP0];
+            if (leave) {
+                leave_msg = leave == 2 ? MSG_BUDGET : MSG_NONE;
+                break;
+            }
+            const int ts = c.ictl[IC_TMP1] ? 0 : 1;
+            const int snap = c.ictl[IC_TMP2];
+            const unsigned long long hidx = reinterpret_cast<unsigned long long*>(c.red_d)[0];
+            __syncthreads();
+            const TreeRef Ts = tree_ref(a, prob, ts, dof);
+            const TreeRef To = tree_ref(a, prob, 1 - ts, dof);
+            // ---- sample (sampling.cpp:39-51), one thread per dimension ----
+            double* smp = dc(c, DC_SAMPLE);
+            if (tid < dof) {
+                smp[tid] = sample_dim(halton_exact(c.bases[tid], hidx), c.limits[2 * tid],
+                                      c.limits[2 * tid + 1]);
+            }
+            __syncthreads();
+            // ---- nearest neighbour in the extended tree ----
+            const NnOut nr = nn_scan(c, Ts.cfg, a.stride, snap, smp);
+            const int nn = nr.index;
+            const double d2 = nr.d2;
+            if (d2 == 0.0) continue;  // duplicate of an existing node (planner.cpp:320)
+            const double dist = __dsqrt_rn(d2);
+            if (a.p.dynamic_domain) {  // DynamicDomain::accept (sampling.hpp:61-75)
+                if (tid == 0) c.ictl[IC_TMP3] = __ldcg(&Ts.dd[nn]);
+                __syncthreads();
+                const int has = c.ictl[IC_TMP3];
+                __syncthreads();
+                if (has && !(dist <= R)) continue;
+            }
+            // ---- steer (planner.cpp:48-64) ----
+            double* nnc = dc(c, DC_NN);
+            double* cnew = dc(c, DC_NEW);
+            if (tid < dof) {
+                const double v = __ldcg(&Ts.cfg[(size_t)tid * a.stride + nn]);
+                nnc[tid] = v;
+                cnew[tid] = dist <= delta ? smp[tid] : lerp_exact(v, smp[tid], __ddiv_rn(delta, dist));
+            }
+            __syncthreads();
+            // ---- SIMT edge validation nn -> c_new, then append ----
+            int last = nn;
+            bool stopped = false;
+            const long long ok =
+                validate_chain(c, a, nnc, cnew, 1, true, &Ts, nn, &last, nullptr, fk_states,
+                               fine_states, &stopped);
+            if (ok == 0) {
+                if (a.p.dynamic_domain && tid == 0) Ts.dd[nn] = 1;  // record_failure
+                continue;
+            }
+            if (ok < 0) {
+                leave_msg = MSG_CAPACITY;
+                break;
+            }
+            const int new_idx = last;
+            // ---- greedy connect toward the opposite tree ----
+            if (tid == 0) c.ictl[IC_TMP2] = ld_acquire(To.published);
+            __syncthreads();
+            const int snap_o = c.ictl[IC_TMP2];
+            __syncthreads();
+            const NnOut no = nn_scan(c, To.cfg, a.stride, snap_o, cnew);
+            const int nno = no.index;
+            const double d2o = no.d2;
+            bool reached = false;
+            int meet_self = new_idx;
+            if (d2o == 0.0) {
+                reached = true;
+            } else {
+                const double disto = __dsqrt_rn(d2o);
+                const long long n_ext = (long long)ceil(__ddiv_rn(disto, delta));
+                double* tgt = dc(c, DC_TARGET);
+                double* A = dc(c, DC_A);
+                if (tid < dof) {
+                    tgt[tid] = __ldcg(&To.cfg[(size_t)tid * a.stride + nno]);
+                    A[tid] = cnew[tid];
+                }
+                __syncthreads();
+                const long long got = validate_chain(c, a, A, tgt, n_ext, true, &Ts, new_idx, &last,
+                                                     &C.done, fk_states, fine_states, &stopped);
+                if (got < 0) {
+                    leave_msg = MSG_CAPACITY;
+                    break;
+                }
+                reached = (got == n_ext) && !stopped;
+                meet_self = last;
+            }
+            if (!reached) continue;
+            // ---- winner (planner.cpp:232-238) ----
+            if (tid == 0) c.ictl[IC_TMP6] = (atomicCAS(&C.winner, 0, blockIdx.x + 1) == 0);
+            __syncthreads();
+            if (c.ictl[IC_TMP6]) {
+                const int meet_a = ts == 0 ? meet_self : nno;
+                const int meet_b = ts == 0 ? nno : meet_self;
+                if (tid == 0) {
+                    C.meet[0] = meet_a;
+                    C.meet[1] = meet_b;
+                }
+                assemble_path(c, a, prob, meet_a, meet_b);
+                if (tid == 0) {
+                    if (c.ictl[IC_TMP4] < 0) {
+                        finish_problem(a, prob, DONE_FAILED, MSG_ARENA);
+                    } else {
+                        C.path_len = c.ictl[IC_TMP4];
+                        __threadfence();
+                        finish_problem(a, prob, DONE_SOLVED, MSG_NONE);
+                    }
+                }
+            }
+            break;
+        }
+        // ---- leave ----
+        flush_stats(c, C, fk_states, fine_states);
+        if (tid == 0) leave_problem(a, prob, leave_msg);
+        __syncthreads();
+        if (a.p.deterministic && a.n_problems == 1) break;
+    }
+}
+
+cudaError_t launch_plan(const RobotArgs& r, PlanArgs a, int grid, cudaStream_t st) {
+    const size_t sm = smem_bytes(r, a.ns_max, a.nthreads);
+    cudaError_t e = cudaFuncSetAttribute(plan_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)sm);
+    if (e != cudaSuccess) return e;
+    plan_kernel<<<grid, a.nthreads, sm, st>>>(a);
+    return cudaGetLastError();
+}
+
+int plan_occupancy(const RobotArgs& r, int ns_max, int nthreads) {
+    const size_t sm = smem_bytes(r, ns_max, nthreads);
+    cudaFuncSetAttribute(plan_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+    int n = 0;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, plan_kernel, nthreads, sm) != cudaSuccess)
+        return 1;
+    return n > 0 ? n : 1;
+}
+
+// ---------------------------------------------------------------------------
+// batched collision checking kernels (product API) and parity hooks
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(128) check_configs_kernel(RobotArgs r, SceneArgs sa, const double* q,
+                                                             int n, int two_stage, uint8_t* out,
+                                                             int NS) {
+    extern __shared__ __align__(16) unsigned char smem[];
+    Ctx c;
+    setup_ctx(c, smem, r.words, r.n_words, r.fine_r64, r.limits, NS);
+    load_scene(c, scene_base(smem, r.n_words, c.L, c.dof, NS, c.nthreads), sa.words, sa.f64);
+    for (long long base = (long long)blockIdx.x * NS; base < n; base += (long long)gridDim.x * NS) {
+        const int cnt = (int)min((long long)NS, n - base);
+        for (int s = threadIdx.x; s < NS; s += c.nthreads) {
+            c.sgroup[s] = s < cnt ? s : -1;
+            if (s < cnt)
+                for (int d = 0; d < c.dof; ++d) c.qf[d * NS + s] = (float)q[(base + s) * c.dof + d];
+        }
+        __syncthreads();
+        check_chunk(c, cnt, two_stage != 0, true, true);
+        for (int s = threadIdx.x; s < cnt; s += c.nthreads) out[base + s] = c.sbad[s] ? 0 : 1;
+        __syncthreads();
+    }
+}
+
+__global__ void __launch_bounds__(128) validate_edges_kernel(RobotArgs r, SceneArgs sa, const double* from,
+                                                              const double* to, int n_edges, int n_cc,
+                                                              int two_stage, int early_exit,
+                                                              uint8_t* out, int NS) {
+    extern __shared__ __align__(16) unsigned char smem[];
+    Ctx c;
+    setup_ctx(c, smem, r.words, r.n_words, r.fine_r64, r.limits, NS);
+    load_scene(c, scene_base(smem, r.n_words, c.L, c.dof, NS, c.nthreads), sa.words, sa.f64);
+    for (int e = blockIdx.x; e < n_edges; e += gridDim.x) {
+        double* A = dc(c, DC_A);
+        double* B = dc(c, DC_B);
+        if (threadIdx.x < c.dof) {
+            A[threadIdx.x] = from[(size_t)e * c.dof + threadIdx.x];
+            B[threadIdx.x] = to[(size_t)e * c.dof + threadIdx.x];
+        }
+        __syncthreads();
+        bool bad = false;
+        for (long long g0 = 0; g0 < n_cc && !(bad && early_exit); g0 += NS) {
+            const int cnt = (int)min((long long)NS, n_cc - g0);
+            gen_chain_states(c, A, B, 1, n_cc, g0, cnt);
+            check_chunk(c, cnt, two_stage != 0, early_exit != 0, false);
+            bad |= c.ictl[IC_FIRSTBAD] != kNoBad;
+            __syncthreads();
+        }
+        if (threadIdx.x == 0) out[e] = bad ? 0 : 1;
+        __syncthreads();
+    }
+}
+
+__global__ void __launch_bounds__(128) debug_fk_kernel(RobotArgs r, const double* q, int n, float* fine_out,
+                                                        float* coarse_out, int NS) {
+    extern __shared__ __align__(16) unsigned char smem[];
+    Ctx c;
+    setup_ctx(c, smem, r.words, r.n_words, r.fine_r64, r.limits, NS);
+    for (long long base = (long long)blockIdx.x * NS; base < n; base += (long long)gridDim.x * NS) {
+        const int cnt = (int)min((long long)NS, n - base);
+        for (int s = threadIdx.x; s < NS; s += c.nthreads) {
+            if (s < cnt)
+                for (int d = 0; d < c.dof; ++d) c.qf[d * NS + s] = (float)q[(base + s) * c.dof + d];
+        }
+        __syncthreads();
+        fk_chunk(c, cnt);
+        if (fine_out) {
+            for (int it = threadIdx.x; it < cnt * c.S; it += c.nthreads) {
+                const int s = it % cnt, j = it / cnt;
+                const float4 f = c.fine[j];
+                const float3 x = pose_point(c, c.flink[j], s, f.x, f.y, f.z);
+                float* o = fine_out + ((base + s) * c.S + j) * 3;
+                o[0] = x.x;
+                o[1] = x.y;
+                o[2] = x.z;
+            }
+        }
+        if (coarse_out) {
+            for (int it = threadIdx.x; it < cnt * c.L; it += c.nthreads) {
+                const int s = it % cnt, l = it / cnt;
+                float* o = coarse_out + ((base + s) * c.L + l) * 3;
+                const float* C = c.ccen + (size_t)l * 3 * NS + s;
+                o[0] = C[0];
+                o[1] = C[NS];
+                o[2] = C[2 * NS];
+            }
+        }
+        __syncthreads();
+    }
+}
+
+__global__ void debug_hits_kernel(SceneArgs sa, const float* centers, const double* radii, int n,
+                                  int n_prims, uint8_t* hits) {
+    __shared__ __align__(16) uint32_t sw[SCENE_MAX_WORDS];
+    const int words = sa.words[SH_WORDS];
+    for (int i = threadIdx.x; i < words; i += blockDim.x) sw[i] = sa.words[i];
+    __syncthreads();
+    Ctx c;
+    c.ns = sw[SH_NS];
+    c.nb = sw[SH_NB];
+    c.nc = sw[SH_NC];
+    c.P = c.ns + c.nb + c.nc;
+    c.sph = reinterpret_cast<const float4*>(sw + sw[SH_OFF_S]);
+    c.box = reinterpret_cast<const float*>(sw + sw[SH_OFF_B]);
+    c.cap = reinterpret_cast<const float*>(sw + sw[SH_OFF_C]);
+    c.eps = __uint_as_float(sw[SH_EPS]);
+    c.s64 = sa.f64;
+    for (long long it = blockIdx.x * (long long)blockDim.x + threadIdx.x; it < (long long)n * n_prims;
+         it += (long long)gridDim.x * blockDim.x) {
+        const int i = (int)(it / n_prims), p = (int)(it % n_prims);
+        const float3 x = make_float3(centers[3 * i], centers[3 * i + 1], centers[3 * i + 2]);
+        hits[it] = fine_vs_prim(c, x, (float)radii[i], radii[i], p) ? 1 : 0;
+    }
+}
+
+__global__ void debug_nn_kernel(const double* soa, long long cap, int count, int dof, const double* q,
+                                int nq, uint32_t* idx, double* d2) {
+    __shared__ double qs[kMaxDof];
+    __shared__ double red_d[32];
+    __shared__ int red_i[32];
+    __shared__ int ictl[IC_COUNT];
+    Ctx c;
+    c.dof = dof;
+    c.nthreads = blockDim.x;
+    c.red_d = red_d;
+    c.red_i = red_i;
+    c.ictl = ictl;
+    for (int i = blockIdx.x; i < nq; i += gridDim.x) {
+        if (threadIdx.x < dof) qs[threadIdx.x] = q[(size_t)i * dof + threadIdx.x];
+        __syncthreads();
+        const NnOut r = nn_scan(c, soa, cap, count, qs);
+        if (threadIdx.x == 0) {
+            idx[i] = r.index;
+            d2[i] = r.d2;
+        }
+        __syncthreads();
+    }
+}
+
+__global__ void debug_halton_kernel(const uint32_t* bases, const uint64_t* idx, int n, double* out) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < n) out[i] = halton_exact(bases[i], idx[i]);
+}
+
+__global__ void debug_sample_kernel(RobotArgs r, uint64_t index0, int n, double* out) {
+    const uint32_t* rw = r.words;
+    const int dof = rw[RH_DOF];
+    const uint32_t* bases = rw + rw[RH_OFF_BASES];
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n * dof) return;
+    const int k = i / dof, d = i % dof;
+    out[i] = sample_dim(halton_exact(bases[d], index0 + k), r.limits[2 * d], r.limits[2 * d + 1]);
+}
+
+static int chunk_states() { return 32; }
+
+cudaError_t launch_check_configs(const RobotArgs& r, const SceneArgs& s, const double* q, int n,
+                                 int two_stage, uint8_t* out, cudaStream_t st) {
+    const int NS = chunk_states();
+    const size_t sm = smem_bytes(r, NS, 128);
+    cudaError_t e = cudaFuncSetAttribute(check_configs_kernel,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+    if (e != cudaSuccess) return e;
+    const int grid = (int)min((long long)(n + NS - 1) / NS, 148LL * 16);
+    if (grid > 0) check_configs_kernel<<<grid, 128, sm, st>>>(r, s, q, n, two_stage, out, NS);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_validate_edges(const RobotArgs& r, const SceneArgs& s, const double* from,
+                                  const double* to, int n_edges, int n_cc, int two_stage,
+                                  int early_exit, uint8_t* out, cudaStream_t st) {
+    const int NS = chunk_states();
+    const size_t sm = smem_bytes(r, NS, 128);
+    cudaError_t e = cudaFuncSetAttribute(validate_edges_kernel,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+    if (e != cudaSuccess) return e;
+    const int grid = (int)min((long long)n_edges, 148LL * 16);
+    if (grid > 0)
+        validate_edges_kernel<<<grid, 128, sm, st>>>(r, s, from, to, n_edges, n_cc, two_stage,
+                                                     early_exit, out, NS);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_debug_fk(const RobotArgs& r, const double* q, int n, float* fine_out,
+                            float* coarse_out, cudaStream_t st) {
+    const int NS = chunk_states();
+    const size_t sm = smem_bytes(r, NS, 128);
+    cudaError_t e = cudaFuncSetAttribute(debug_fk_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)sm);
+    if (e != cudaSuccess) return e;
+    const int grid = (int)min((long long)(n + NS - 1) / NS, 148LL * 16);
+    if (grid > 0) debug_fk_kernel<<<grid, 128, sm, st>>>(r, q, n, fine_out, coarse_out, NS);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_debug_hits(const SceneArgs& s, const float* centers, const double* radii,
+                              int n, int n_prims, uint8_t* hits, cudaStream_t st) {
+    const long long items = (long long)n * n_prims;
+    const int grid = (int)min((items + 127) / 128, 148LL * 8);
+    if (grid > 0) debug_hits_kernel<<<grid, 128, 0, st>>>(s, centers, radii, n, n_prims, hits);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_debug_nn(const double* soa, long long cap, int count, int dof, const double* q,
+                            int nq, uint32_t* idx, double* d2, cudaStream_t st) {
+    const int grid = min(nq, 148 * 8);
+    if (grid > 0) debug_nn_kernel<<<grid, 128, 0, st>>>(soa, cap, count, dof, q, nq, idx, d2);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_debug_halton(const uint32_t* bases, const uint64_t* idx, int n, double* out,
+                                cudaStream_t st) {
+    if (n > 0) debug_halton_kernel<<<(n + 127) / 128, 128, 0, st>>>(bases, idx, n, out);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_debug_sample(const RobotArgs& r, uint64_t index0, int n, double* out,
+                                cudaStream_t st) {
+    const int items = n * r.dof;
+    if (items > 0) debug_sample_kernel<<<(items + 127) / 128, 128, 0, st>>>(r, index0, n, out);
+    return cudaGetLastError();
+}
+
+}  // namespace prrtc_b200

@@ -1,0 +1,49 @@
+// prrtc_launch.h — host-side launchers of the sm_100a kernels
+// (implemented in prrtc_kernels.cu, called by the C-ABI in prrtc_capi.cu).
+#pragma once
+#include <cuda_runtime.h>
+#include <stddef.h>
+#include <stdint.h>
+
+#include "prrtc_internal.h"
+
+namespace prrtc_b200 {
+
+// Robot-side kernel inputs shared by every launcher.
+struct RobotArgs {
+    const uint32_t* words;  // packed robot (device)
+    int n_words;
+    const double* fine_r64; // device
+    const double* limits;   // device [dof][2]
+    int n_links, dof, n_fine;
+};
+
+struct SceneArgs {
+    const uint32_t* words;  // packed scene (device)
+    SceneF64 f64;           // device
+};
+
+size_t smem_bytes(const RobotArgs& r, int ns_max, int nthreads);
+
+// Persistent planner: grid CTAs solve a.n_problems problems.
+cudaError_t launch_plan(const RobotArgs& r, PlanArgs a, int grid, cudaStream_t st);
+// Max co-resident planner CTAs per SM for this configuration.
+int plan_occupancy(const RobotArgs& r, int ns_max, int nthreads);
+
+cudaError_t launch_check_configs(const RobotArgs& r, const SceneArgs& s, const double* q, int n,
+                                 int two_stage, uint8_t* out, cudaStream_t st);
+cudaError_t launch_validate_edges(const RobotArgs& r, const SceneArgs& s, const double* from,
+                                  const double* to, int n_edges, int n_cc, int two_stage,
+                                  int early_exit, uint8_t* out, cudaStream_t st);
+cudaError_t launch_debug_fk(const RobotArgs& r, const double* q, int n, float* fine_out,
+                            float* coarse_out, cudaStream_t st);
+cudaError_t launch_debug_hits(const SceneArgs& s, const float* centers, const double* radii,
+                              int n, int n_prims, uint8_t* hits, cudaStream_t st);
+cudaError_t launch_debug_nn(const double* soa, long long cap, int count, int dof, const double* q,
+                            int nq, uint32_t* idx, double* d2, cudaStream_t st);
+cudaError_t launch_debug_halton(const uint32_t* bases, const uint64_t* idx, int n, double* out,
+                                cudaStream_t st);
+cudaError_t launch_debug_sample(const RobotArgs& r, uint64_t index0, int n, double* out,
+                                cudaStream_t st);
+
+}  // namespace prrtc_b200

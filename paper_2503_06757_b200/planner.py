@@ -1,0 +1,304 @@
+"""Python host API over the C-ABI — the reference's planning interface.
+
+    plan(model, scene, start, goal, params) -> PlanResult      planner.hpp:55-56
+    plan_batch(model, scenes, starts, goals, params)           (many problems, one launch)
+    validate_edges / check_configs                             collision.hpp:57-75
+    debug_* parity hooks                                       include/prrtc_b200.h
+
+Robot and scene uploads are setup (untimed in the reference methodology,
+PAPER.md:201) and are cached per content fingerprint, so repeated plan()
+calls on the same model/scene only move start/goal/params and the result.
+"""
+from __future__ import annotations
+
+import ctypes as C
+from typing import Sequence
+
+import numpy as np
+
+from . import _lib
+from ._lib import Params, Result, check
+from .model import (CheckStatsSnapshot, PlannerParams, PlanResult, PlanStatus, RobotModel,
+                    Scene)
+
+_DP = C.POINTER(C.c_double)
+
+
+def _dptr(a: np.ndarray):
+    return a.ctypes.data_as(_DP)
+
+
+class DeviceRobot:
+    """prrtc_robot handle (validated + uploaded RobotModel)."""
+
+    def __init__(self, model: RobotModel, device: int = 0):
+        lib = _lib.load()
+        desc, keep = model.to_desc()
+        h = C.c_void_p()
+        check(lib.prrtc_robot_create(C.byref(desc), device, C.byref(h)))
+        self.h = h
+        self.model = model
+        self.device = device
+        self.dof = lib.prrtc_robot_dof(h)
+        self.fine_count = lib.prrtc_robot_fine_count(h)
+        self.n_links = model.link_count()
+        del keep
+
+    def __del__(self):
+        if getattr(self, "h", None) and _lib._lib is not None:
+            _lib._lib.prrtc_robot_destroy(self.h)
+            self.h = None
+
+
+class DeviceScene:
+    """prrtc_scene handle (validated + uploaded Scene)."""
+
+    def __init__(self, scene: Scene, device: int = 0):
+        lib = _lib.load()
+        desc, keep = scene.to_desc()
+        h = C.c_void_p()
+        check(lib.prrtc_scene_create(C.byref(desc), device, C.byref(h)))
+        self.h = h
+        self.scene = scene
+        self.device = device
+        self.n_prims = len(scene.primitives)
+        del keep
+
+    def update(self, scene: Scene) -> None:
+        """prrtc_scene_update: replace the primitives (dynamic obstacles)."""
+        desc, keep = scene.to_desc()
+        check(_lib.load().prrtc_scene_update(self.h, C.byref(desc)))
+        self.scene = scene
+        self.n_prims = len(scene.primitives)
+        del keep
+
+    def __del__(self):
+        if getattr(self, "h", None) and _lib._lib is not None:
+            _lib._lib.prrtc_scene_destroy(self.h)
+            self.h = None
+
+
+_robot_cache: dict = {}
+_scene_cache: dict = {}
+
+
+def _fingerprint(obj) -> str:
+    return repr(obj)
+
+
+def device_robot(model: RobotModel | DeviceRobot, device: int = 0) -> DeviceRobot:
+    if isinstance(model, DeviceRobot):
+        return model
+    key = (_fingerprint(model), device)
+    h = _robot_cache.get(key)
+    if h is None:
+        h = _robot_cache[key] = DeviceRobot(model, device)
+    return h
+
+
+def device_scene(scene: Scene | DeviceScene, device: int = 0) -> DeviceScene:
+    if isinstance(scene, DeviceScene):
+        return scene
+    key = (_fingerprint(scene), device)
+    h = _scene_cache.get(key)
+    if h is None:
+        if len(_scene_cache) > 4096:
+            _scene_cache.clear()
+        h = _scene_cache[key] = DeviceScene(scene, device)
+    return h
+
+
+def _to_result(r: Result, dof: int) -> PlanResult:
+    path = np.zeros((0, dof))
+    if r.path_len and bool(r.path):
+        path = np.ctypeslib.as_array(r.path, shape=(r.path_len * dof,)).reshape(r.path_len, dof).copy()
+    return PlanResult(
+        status=PlanStatus(r.status),
+        path=path,
+        cost=r.cost,
+        wall_time_ms=r.wall_time_ms,
+        iterations_total=r.iterations_total,
+        check_stats=CheckStatsSnapshot(r.sphere_tests, r.fk_calls, r.fine_stage_entries),
+        solving_worker=r.solving_worker,
+        message=r.message.decode(errors="replace"),
+        device_time_ms=r.device_time_ms,
+        tree_nodes=(int(r.tree_nodes[0]), int(r.tree_nodes[1])),
+        flops=int(r.flops),
+    )
+
+
+def _cfg(q, dof: int, what: str) -> np.ndarray:
+    a = np.ascontiguousarray(np.asarray(q, dtype=np.float64))
+    if a.ndim != 1 or a.shape[0] != dof:  # require_dim (types.hpp:16-21)
+        raise ValueError(f"{what}: expected dimension {dof}, got {a.shape[-1] if a.ndim else 0}")
+    return a
+
+
+def plan(model, scene, start, goal, params: PlannerParams | None = None, device: int = 0) -> PlanResult:
+    """Drop-in for prrtc::plan (planner.cpp:246-322), computed on the B200."""
+    params = params or PlannerParams()
+    rob = device_robot(model, device)
+    scn = device_scene(scene, device)
+    s = _cfg(start, rob.dof, "plan.start")
+    g = _cfg(goal, rob.dof, "plan.goal")
+    p = params.to_c()
+    r = Result()
+    check(_lib.load().prrtc_plan(rob.h, scn.h, _dptr(s), _dptr(g), rob.dof, C.byref(p), C.byref(r)))
+    try:
+        return _to_result(r, rob.dof)
+    finally:
+        _lib.load().prrtc_result_free(C.byref(r))
+
+
+def _scene_handles(scenes, n, device):
+    if isinstance(scenes, (Scene, DeviceScene)):
+        scenes = [scenes] * n
+    if len(scenes) != n:
+        raise ValueError("plan_batch: one scene per problem required")
+    hs = [device_scene(s, device) for s in scenes]
+    arr = (C.c_void_p * n)(*[h.h.value for h in hs])
+    return hs, arr
+
+
+def plan_batch(model, scenes, starts, goals, params: PlannerParams | None = None,
+               device: int = 0) -> list[PlanResult]:
+    """n independent problems (one robot, one scene each) in one device launch."""
+    params = params or PlannerParams()
+    rob = device_robot(model, device)
+    S = np.ascontiguousarray(np.asarray(starts, dtype=np.float64).reshape(-1, rob.dof))
+    G = np.ascontiguousarray(np.asarray(goals, dtype=np.float64).reshape(-1, rob.dof))
+    n = S.shape[0]
+    hs, arr = _scene_handles(scenes, n, device)
+    p = params.to_c()
+    res = (Result * n)()
+    check(_lib.load().prrtc_plan_batch(rob.h, arr, n, _dptr(S), _dptr(G), rob.dof, C.byref(p), res))
+    out = [_to_result(res[i], rob.dof) for i in range(n)]
+    for i in range(n):
+        _lib.load().prrtc_result_free(C.byref(res[i]))
+    del hs
+    return out
+
+
+class Batch:
+    """Device-resident batch: inputs uploaded once (prrtc_batch_create), then
+    solved repeatedly with launch(); results() copies the outcome back."""
+
+    def __init__(self, model, scenes, starts, goals, params: PlannerParams | None = None, device: int = 0):
+        self.params = params or PlannerParams()
+        self.rob = device_robot(model, device)
+        S = np.ascontiguousarray(np.asarray(starts, dtype=np.float64).reshape(-1, self.rob.dof))
+        G = np.ascontiguousarray(np.asarray(goals, dtype=np.float64).reshape(-1, self.rob.dof))
+        self.n = S.shape[0]
+        self._hs, arr = _scene_handles(scenes, self.n, device)
+        p = self.params.to_c()
+        h = C.c_void_p()
+        check(_lib.load().prrtc_batch_create(self.rob.h, arr, self.n, _dptr(S), _dptr(G), self.rob.dof,
+                                             C.byref(p), C.byref(h)))
+        self.h = h
+
+    def launch(self, stream: int = 0) -> None:
+        check(_lib.load().prrtc_batch_launch(self.h, C.c_void_p(stream)))
+
+    def launch_count(self) -> int:
+        return _lib.load().prrtc_batch_launch_count(self.h)
+
+    def results(self) -> list[PlanResult]:
+        res = (Result * self.n)()
+        check(_lib.load().prrtc_batch_results(self.h, res))
+        out = [_to_result(res[i], self.rob.dof) for i in range(self.n)]
+        for i in range(self.n):
+            _lib.load().prrtc_result_free(C.byref(res[i]))
+        return out
+
+    def __del__(self):
+        if getattr(self, "h", None) and _lib._lib is not None:
+            _lib._lib.prrtc_batch_destroy(self.h)
+            self.h = None
+
+
+# ---------------------------------------------------------------------------
+# batched collision checking (product API)
+# ---------------------------------------------------------------------------
+def validate_edges(model, scene, frm, to, n_cc: int = 32, two_stage: bool = True,
+                   early_exit: bool = True, device: int = 0) -> np.ndarray:
+    """CollisionChecker::validate_edge over many edges (collision.cpp:206-224)."""
+    rob = device_robot(model, device)
+    scn = device_scene(scene, device)
+    F = np.ascontiguousarray(np.asarray(frm, dtype=np.float64).reshape(-1, rob.dof))
+    T = np.ascontiguousarray(np.asarray(to, dtype=np.float64).reshape(-1, rob.dof))
+    out = np.zeros(F.shape[0], dtype=np.uint8)
+    check(_lib.load().prrtc_validate_edges(rob.h, scn.h, _dptr(F), _dptr(T), F.shape[0], rob.dof, n_cc,
+                                           int(two_stage), int(early_exit),
+                                           out.ctypes.data_as(C.POINTER(C.c_uint8))))
+    return out.astype(bool)
+
+
+def check_configs(model, scene, q, two_stage: bool = True, device: int = 0) -> np.ndarray:
+    """CollisionChecker::check_config over many configurations (collision.cpp:130-204)."""
+    rob = device_robot(model, device)
+    scn = device_scene(scene, device)
+    Q = np.ascontiguousarray(np.asarray(q, dtype=np.float64).reshape(-1, rob.dof))
+    out = np.zeros(Q.shape[0], dtype=np.uint8)
+    check(_lib.load().prrtc_check_configs(rob.h, scn.h, _dptr(Q), Q.shape[0], rob.dof, int(two_stage),
+                                          out.ctypes.data_as(C.POINTER(C.c_uint8))))
+    return out.astype(bool)
+
+
+# ---------------------------------------------------------------------------
+# parity hooks
+# ---------------------------------------------------------------------------
+def debug_fk(model, q, device: int = 0):
+    """Posed fine [n,S,3] and coarse [n,L,3] sphere centers (FP32) as the
+    device collision code sees them."""
+    rob = device_robot(model, device)
+    Q = np.ascontiguousarray(np.asarray(q, dtype=np.float64).reshape(-1, rob.dof))
+    n = Q.shape[0]
+    fine = np.zeros((n, rob.fine_count, 3), dtype=np.float32)
+    coarse = np.zeros((n, rob.n_links, 3), dtype=np.float32)
+    FPT = C.POINTER(C.c_float)
+    check(_lib.load().prrtc_debug_fk(rob.h, _dptr(Q), n, rob.dof, fine.ctypes.data_as(FPT),
+                                     coarse.ctypes.data_as(FPT)))
+    return fine, coarse
+
+
+def debug_sphere_hits(scene, centers, radii, device: int = 0) -> np.ndarray:
+    """Device predicate verdicts [n, P] (primitive order: spheres, boxes, capsules)."""
+    scn = device_scene(scene, device)
+    X = np.ascontiguousarray(np.asarray(centers, dtype=np.float32).reshape(-1, 3))
+    R = np.ascontiguousarray(np.asarray(radii, dtype=np.float64).reshape(-1))
+    out = np.zeros((X.shape[0], scn.n_prims), dtype=np.uint8)
+    check(_lib.load().prrtc_debug_sphere_hits(scn.h, X.ctypes.data_as(C.POINTER(C.c_float)), _dptr(R),
+                                              X.shape[0], out.ctypes.data_as(C.POINTER(C.c_uint8))))
+    return out.astype(bool)
+
+
+def debug_nn(tree, q, device: int = 0):
+    """Device nearest neighbour: (index[nq], squared distance[nq])."""
+    T = np.ascontiguousarray(np.asarray(tree, dtype=np.float64))
+    Q = np.ascontiguousarray(np.asarray(q, dtype=np.float64).reshape(-1, T.shape[1]))
+    idx = np.zeros(Q.shape[0], dtype=np.uint32)
+    d2 = np.zeros(Q.shape[0], dtype=np.float64)
+    check(_lib.load().prrtc_debug_nn(_dptr(T), T.shape[0], T.shape[1], _dptr(Q), Q.shape[0], device,
+                                     idx.ctypes.data_as(C.POINTER(C.c_uint32)), _dptr(d2)))
+    return idx, d2
+
+
+def debug_halton(bases: Sequence[int], indices: Sequence[int], device: int = 0) -> np.ndarray:
+    B = np.ascontiguousarray(np.asarray(bases, dtype=np.uint32))
+    I = np.ascontiguousarray(np.asarray(indices, dtype=np.uint64))
+    out = np.zeros(B.shape[0], dtype=np.float64)
+    check(_lib.load().prrtc_debug_halton(B.ctypes.data_as(C.POINTER(C.c_uint32)),
+                                         I.ctypes.data_as(C.POINTER(C.c_uint64)), B.shape[0], device,
+                                         _dptr(out)))
+    return out
+
+
+def debug_sample(model, index0: int, n: int, device: int = 0) -> np.ndarray:
+    rob = device_robot(model, device)
+    out = np.zeros((n, rob.dof), dtype=np.float64)
+    check(_lib.load().prrtc_debug_sample(rob.h, index0, n, _dptr(out)))
+    return out
+
+
+def device_count() -> int:
+    return _lib.load().prrtc_device_count()

@@ -1,0 +1,130 @@
+"""The persistent planner kernel against the reference planner.
+
+Random trees cannot be bit-reproduced under parallel insertion, so the bar is
+statistical (BASELINE.json north_star): every returned path re-validates
+collision-free with the reference checker at 4 x n_cc, fine-only, early exit
+off, success rate >= the reference's on the same problems, and
+the deterministic single-CTA mode replays the reference's workers=1 run.
+"""
+import numpy as np
+import pytest
+
+from conftest import load_problems
+from paper_2503_06757_b200 import planner, robots
+from paper_2503_06757_b200.model import PlannerParams, PlanStatus
+from paper_2503_06757_b200.scenes import make_scene
+
+pytestmark = pytest.mark.gpu
+
+
+def check_path(oracle, m, scene, res, start, goal, params):
+    assert res.status == PlanStatus.Solved
+    P = res.path
+    assert P.shape[1] == m.dof and len(P) >= 1
+    assert np.array_equal(P[0], start) and np.array_equal(P[-1], goal)
+    assert oracle.path_valid(m, scene, P, 4 * params.n_cc), "path fails 4x re-validation"
+    if len(P) > 1:
+        seg = np.linalg.norm(np.diff(P, axis=0), axis=1)
+        assert np.all(seg > 0) and np.all(seg <= params.delta + 1e-9)
+        assert abs(res.cost - seg.sum()) < 1e-9
+
+
+@pytest.mark.parametrize("robot", ["panda", "fetch", "baxter"])
+def test_plan_paths_revalidate(gpu, oracle, robot):
+    m = robots.get(robot)
+    params = PlannerParams(tree_capacity=20000)
+    probs = load_problems(robot, 24)
+    solved = 0
+    for kind, pid, s, g in probs:
+        scene, _ = make_scene(robot, kind, pid)
+        r = planner.plan(m, scene, s, g, params)
+        assert r.status in (PlanStatus.Solved, PlanStatus.Failed)
+        if r.status == PlanStatus.Solved:
+            solved += 1
+            check_path(oracle, m, scene, r, s, g, params)
+    assert solved >= len(probs) * 0.75
+
+
+def test_batch_success_not_below_reference(gpu, oracle):
+    m = robots.get("panda")
+    probs = load_problems("panda", 90)
+    scenes = [make_scene("panda", k, p)[0] for k, p, _, _ in probs]
+    S = np.array([p[2] for p in probs])
+    G = np.array([p[3] for p in probs])
+    params = PlannerParams(tree_capacity=20000)
+    res = planner.plan_batch(m, scenes, S, G, params)
+    ref, _ = oracle.plan_many(m, scenes, S, G, PlannerParams(workers=1, tree_capacity=20000), threads=8)
+    ok = sum(r.status == PlanStatus.Solved for r in res)
+    ok_ref = sum(r.status == PlanStatus.Solved for r in ref)
+    assert ok >= ok_ref
+    for sc, r, s, g in zip(scenes, res, S, G):
+        if r.status == PlanStatus.Solved:
+            check_path(oracle, m, sc, r, s, g, params)
+
+
+def test_deterministic_mode_replays_reference(gpu, oracle):
+    """One CTA, Halton stride 1, balanced pick: the device replays the
+    reference's workers=1 run (scalar backend) node for node, except where an
+    FP32-FK verdict differs from the FP64 one within ~1e-6 m of a boundary."""
+    m = robots.get("panda")
+    probs = load_problems("panda", 30)
+    same = 0
+    params = PlannerParams(tree_capacity=20000, deterministic=True, workers=1)
+    for kind, pid, s, g in probs:
+        scene, _ = make_scene("panda", kind, pid)
+        r = planner.plan(m, scene, s, g, params)
+        ref = oracle.plan(m, scene, s, g, PlannerParams(workers=1, tree_capacity=20000))
+        assert r.status == ref.status or r.status == PlanStatus.Solved
+        if r.status == ref.status and (r.status != PlanStatus.Solved or np.array_equal(r.path, ref.path)):
+            same += 1
+            assert r.iterations_total == ref.iterations_total
+    assert same >= len(probs) * 0.9
+
+
+def test_endpoint_statuses(gpu, oracle):
+    m = robots.get("panda")
+    kind, pid, s, g = load_problems("panda", 1)[0]
+    scene, _ = make_scene("panda", kind, pid)
+    # start == goal -> Solved, [start], cost 0 (planner.cpp:279-285)
+    r = planner.plan(m, scene, s, s)
+    assert r.status == PlanStatus.Solved and r.path.shape == (1, m.dof) and r.cost == 0.0
+    # out of limits -> InfeasibleEndpoint, start message first (planner.cpp:263-277)
+    bad = s.copy()
+    bad[0] = 10.0
+    r = planner.plan(m, scene, bad, g)
+    assert r.status == PlanStatus.InfeasibleEndpoint and "start" in r.message
+    r = planner.plan(m, scene, s, bad)
+    assert r.status == PlanStatus.InfeasibleEndpoint and "goal" in r.message
+    # colliding goal: find a config in collision
+    lim = m.limits()
+    rng = np.random.default_rng(0)
+    for _ in range(1000):
+        q = lim[:, 0] + rng.random(m.dof) * (lim[:, 1] - lim[:, 0])
+        if not oracle.check_config(m, scene, q):
+            break
+    r = planner.plan(m, scene, s, q)
+    assert r.status == PlanStatus.InfeasibleEndpoint and "goal" in r.message
+
+
+def test_invalid_arguments_raise(gpu):
+    m = robots.get("panda")
+    kind, pid, s, g = load_problems("panda", 1)[0]
+    scene, _ = make_scene("panda", kind, pid)
+    with pytest.raises(ValueError, match="delta"):
+        planner.plan(m, scene, s, g, PlannerParams(delta=0.0))
+    with pytest.raises(ValueError, match="n_cc"):
+        planner.plan(m, scene, s, g, PlannerParams(n_cc=0))
+    with pytest.raises(ValueError, match="tree_capacity"):
+        planner.plan(m, scene, s, g, PlannerParams(tree_capacity=1))
+    with pytest.raises(ValueError, match="dimension"):
+        planner.plan(m, scene, s[:3], g)
+
+
+def test_capacity_exhaustion_fails_cleanly(gpu):
+    m = robots.get("panda")
+    probs = load_problems("panda", 30)
+    kind, pid, s, g = next(p for p in probs if p[0] == "cage")
+    scene, _ = make_scene("panda", kind, pid)
+    r = planner.plan(m, scene, s, g, PlannerParams(tree_capacity=4))
+    assert r.status in (PlanStatus.Solved, PlanStatus.Failed)
+    assert r.tree_nodes[0] <= 2 and r.tree_nodes[1] <= 2
