@@ -507,46 +507,127 @@ int prrtc_scene_destroy(prrtc_scene* s) {
 
 // ---------------------------------------------------------------------------
 // planning workspace and batches
+//
+// A workspace owns every device buffer a launch needs, laid out so one call
+// costs one packed H2D copy, one memset, one kernel and one D2H copy:
+//   io   (pinned host) : starts | goals | scene-word ptrs | scene-f64 ptrs | prob_scene
+//   d_in (device)      : same layout
+//   d_out (device)     : [hdr 128 B: arena_used u64, next_problem, n_done]
+//                        [ProbCtl x n][path arena]
+//   trees              : cfg [n][2][dof][stride], parent/ready/dd [n][2][stride]
+// Workspaces grow monotonically and are cached per device for prrtc_plan /
+// prrtc_plan_batch (allocation is setup, not part of a plan call).
 // ---------------------------------------------------------------------------
+namespace {
+
+struct Workspace {
+    int device = -1;
+    size_t n_cap = 0, dof_cap = 0, nodes_cap = 0, arena_cap = 0;
+    unsigned epoch = 0;
+    void* h_io = nullptr;
+    size_t io_bytes = 0;
+    void* h_out = nullptr;
+    size_t out_bytes = 0;
+    unsigned char* d_in = nullptr;
+    unsigned char* d_out = nullptr;
+    double* d_cfg = nullptr;
+    int* d_parent = nullptr;
+    int* d_dd = nullptr;
+    unsigned* d_ready = nullptr;
+    cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+    cudaStream_t stream = nullptr;
+
+    static size_t in_bytes(size_t n, size_t dof) {
+        return 8 * 2 * n * dof + sizeof(void*) * n + sizeof(SceneF64) * n + 4 * n + 64;
+    }
+    static size_t out_hdr(size_t n) { return 128 + sizeof(ProbCtl) * n; }
+
+    void release() {
+        if (device < 0) return;
+        cudaSetDevice(device);
+        cudaFreeHost(h_io);
+        cudaFreeHost(h_out);
+        cudaFree(d_in);
+        cudaFree(d_out);
+        cudaFree(d_cfg);
+        cudaFree(d_parent);
+        cudaFree(d_dd);
+        cudaFree(d_ready);
+        if (ev0) cudaEventDestroy(ev0);
+        if (ev1) cudaEventDestroy(ev1);
+        if (stream) cudaStreamDestroy(stream);
+        *this = Workspace();
+    }
+    ~Workspace() { release(); }
+
+    // Grow to hold n problems of dof with the given tree stride and arena.
+    int reserve(int dev, size_t n, size_t dof, size_t stride, size_t arena) {
+        const size_t nodes = n * 2 * stride;
+        if (device == dev && n <= n_cap && dof <= dof_cap && nodes * dof <= nodes_cap * dof_cap &&
+            nodes <= nodes_cap && arena <= arena_cap)
+            return PRRTC_OK;
+        const size_t nn = std::max(n, n_cap), nd = std::max(dof, dof_cap);
+        const size_t nnodes = std::max(nodes, nodes_cap), narena = std::max(arena, arena_cap);
+        release();
+        device = dev;
+        cudaSetDevice(dev);
+        io_bytes = in_bytes(nn, nd);
+        out_bytes = out_hdr(nn) + 8 * narena;
+        if (cudaMallocHost(&h_io, io_bytes) != cudaSuccess ||
+            cudaMallocHost(&h_out, out_hdr(nn) + 8 * std::min<size_t>(narena, 1 << 16)) != cudaSuccess ||
+            cudaMalloc(&d_in, io_bytes) != cudaSuccess || cudaMalloc(&d_out, out_bytes) != cudaSuccess ||
+            cudaMalloc(&d_cfg, 8 * nnodes * nd) != cudaSuccess ||
+            cudaMalloc(&d_parent, 4 * nnodes) != cudaSuccess ||
+            cudaMalloc(&d_dd, 4 * nnodes) != cudaSuccess ||
+            cudaMalloc(&d_ready, 4 * nnodes) != cudaSuccess) {
+            release();
+            return set_err(PRRTC_ENOMEM, "plan: device workspace allocation failed (" +
+                                             std::to_string((8 * nd + 12) * nnodes) + " bytes of trees)");
+        }
+        // ready flags are epoch tagged: zero once, launches use epoch >= 1
+        cudaMemset(d_ready, 0, 4 * nnodes);
+        cudaEventCreate(&ev0);
+        cudaEventCreate(&ev1);
+        cudaStreamCreateWithFlags(&stream, cudaStreamNonBlocking);
+        n_cap = nn;
+        dof_cap = nd;
+        nodes_cap = nnodes;
+        arena_cap = narena;
+        epoch = 0;
+        if (cudaDeviceSynchronize() != cudaSuccess) {
+            release();
+            return set_err(PRRTC_ECUDA, "plan: workspace initialisation failed");
+        }
+        return PRRTC_OK;
+    }
+};
+
+std::mutex g_ws_mu[64];
+Workspace g_ws[64];
+
+}  // namespace
+
 struct prrtc_batch {
     const prrtc_robot* robot = nullptr;
+    Workspace own;
+    Workspace* ws = nullptr;
     int device = 0;
     int n = 0, dof = 0;
     prrtc_params params{};
     long long cap = 0, stride = 0;
     int grid = 0, nthreads = 128, ns_max = 32;
-    unsigned long long budget = 0, arena_cap = 0;
-    unsigned epoch = 0;
-    // device buffers
-    double *d_starts = nullptr, *d_goals = nullptr, *d_cfg = nullptr, *d_arena = nullptr;
-    int *d_parent = nullptr, *d_dd = nullptr, *d_prob_scene = nullptr, *d_next = nullptr;
-    unsigned* d_ready = nullptr;
-    unsigned long long* d_arena_used = nullptr;
-    ProbCtl* d_ctl = nullptr;
-    const uint32_t** d_scene_words = nullptr;
-    SceneF64* d_scene_f64 = nullptr;
-    cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+    unsigned long long budget = 0, arena = 0;
     cudaStream_t last_stream = 0;
     int launches = 0;
-    std::vector<int> msg_scene;
-    ~prrtc_batch() {
-        cudaSetDevice(device);
-        cudaFree(d_starts);
-        cudaFree(d_goals);
-        cudaFree(d_cfg);
-        cudaFree(d_arena);
-        cudaFree(d_parent);
-        cudaFree(d_dd);
-        cudaFree(d_prob_scene);
-        cudaFree(d_next);
-        cudaFree(d_ready);
-        cudaFree(d_arena_used);
-        cudaFree(d_ctl);
-        cudaFree(d_scene_words);
-        cudaFree(d_scene_f64);
-        if (ev0) cudaEventDestroy(ev0);
-        if (ev1) cudaEventDestroy(ev1);
-    }
+    // device views into ws->d_in / d_out
+    double *d_starts = nullptr, *d_goals = nullptr;
+    const uint32_t** d_scene_words = nullptr;
+    SceneF64* d_scene_f64 = nullptr;
+    int* d_prob_scene = nullptr;
+    unsigned long long* d_arena_used = nullptr;
+    int *d_next = nullptr, *d_ndone = nullptr;
+    ProbCtl* d_ctl = nullptr;
+    double* d_arena = nullptr;
 };
 
 namespace {
@@ -557,6 +638,8 @@ int check_params(const prrtc_params* p) {  // planner.cpp:250-252
     if (p->tree_capacity < 2) return set_err(PRRTC_EINVAL, "plan: tree_capacity too small");
     if (p->threads_per_cta != 0 && p->threads_per_cta != 128)
         return set_err(PRRTC_EINVAL, "plan: threads_per_cta must be 0 or 128");
+    if (p->sampler != PRRTC_SAMPLER_HALTON)
+        return set_err(PRRTC_EINVAL, "plan: the device sampler is Halton only (SamplerKind::Uniform is a property-test sampler, sampling.hpp:40-54)");
     return PRRTC_OK;
 }
 
@@ -569,33 +652,27 @@ int sm_count(int device) {
 template <class T>
 int dmalloc(T** p, size_t count) {
     if (cudaMalloc(reinterpret_cast<void**>(p), sizeof(T) * std::max<size_t>(1, count)) != cudaSuccess)
-        return set_err(PRRTC_ENOMEM, "plan: device allocation of " + std::to_string(sizeof(T) * count) + " bytes failed");
+        return set_err(PRRTC_ENOMEM, "device allocation of " + std::to_string(sizeof(T) * count) + " bytes failed");
     return PRRTC_OK;
 }
 
-}  // namespace
-
-extern "C" {
-
-int prrtc_batch_create(const prrtc_robot* robot, const prrtc_scene* const* scenes,
-                       uint32_t n_problems, const double* starts, const double* goals,
-                       uint32_t dof, const prrtc_params* params, prrtc_batch** out) {
-    if (!robot || !scenes || !starts || !goals || !params || !out)
-        return set_err(PRRTC_EINVAL, "prrtc_batch_create: null argument");
+// Validates the request and fills the batch sizing (no device work).
+int batch_setup(prrtc_batch* b, const prrtc_robot* robot, const prrtc_scene* const* scenes,
+                uint32_t n_problems, const double* starts, const double* goals, uint32_t dof,
+                const prrtc_params* params) {
+    if (!robot || !scenes || !starts || !goals || !params)
+        return set_err(PRRTC_EINVAL, "plan: null argument");
     if ((int)dof != robot->dof)  // require_dim (types.hpp:16-21)
         return set_err(PRRTC_EINVAL, "plan.start: expected dimension " + std::to_string(robot->dof) +
                                          ", got " + std::to_string(dof));
     int rc = check_params(params);
     if (rc) return rc;
-    if (n_problems == 0) return set_err(PRRTC_EINVAL, "prrtc_batch_create: empty batch");
-    for (uint32_t i = 0; i < n_problems; ++i) {
+    if (n_problems == 0) return set_err(PRRTC_EINVAL, "plan: empty batch");
+    for (uint32_t i = 0; i < n_problems; ++i)
         if (!scenes[i] || scenes[i]->device != robot->device)
-            return set_err(PRRTC_EINVAL, "prrtc_batch_create: scene missing or on another device");
-    }
+            return set_err(PRRTC_EINVAL, "plan: scene missing or on another device");
     rc = check_device(robot->device);
     if (rc) return rc;
-    cudaSetDevice(robot->device);
-    auto* b = new prrtc_batch();
     b->robot = robot;
     b->device = robot->device;
     b->n = (int)n_problems;
@@ -605,16 +682,14 @@ int prrtc_batch_create(const prrtc_robot* robot, const prrtc_scene* const* scene
     b->stride = (b->cap + 31) / 32 * 32;
     b->nthreads = 128;
     b->ns_max = std::max(32, std::min(128, (params->n_cc + 31) / 32 * 32));
-    const RobotArgs ra = robot->args();
-    const int occ = plan_occupancy(ra, b->ns_max, b->nthreads);
+    const int occ = plan_occupancy(robot->args(), b->ns_max, b->nthreads);
     const int sms = sm_count(robot->device);
     unsigned workers_eff;
     if (params->deterministic) {
         b->grid = 1;
         workers_eff = 1;
     } else if (n_problems == 1) {
-        const int def = 2 * sms;
-        b->grid = (int)(params->workers ? params->workers : def);
+        b->grid = (int)(params->workers ? std::min<unsigned>(params->workers, sms * occ) : 2 * sms);
         workers_eff = b->grid;
     } else {
         const unsigned per_sm = params->ctas_per_sm ? std::min<unsigned>(params->ctas_per_sm, occ) : occ;
@@ -623,59 +698,63 @@ int prrtc_batch_create(const prrtc_robot* robot, const prrtc_scene* const* scene
                                       : std::max(1u, (unsigned)(b->grid / std::min<int>(b->grid, n_problems)));
     }
     b->budget = params->max_iters_per_worker * (unsigned long long)workers_eff;
-    // path arena: every problem can return a path of up to 4096 configs
-    const unsigned long long per = (unsigned long long)dof * std::min<long long>(4096, 2 * b->cap);
-    b->arena_cap = per * n_problems;
-    const size_t n = n_problems;
-    const size_t nodes = n * 2 * (size_t)b->stride;
-    if ((rc = dmalloc(&b->d_starts, n * dof)) || (rc = dmalloc(&b->d_goals, n * dof)) ||
-        (rc = dmalloc(&b->d_cfg, nodes * dof)) || (rc = dmalloc(&b->d_parent, nodes)) ||
-        (rc = dmalloc(&b->d_dd, nodes)) || (rc = dmalloc(&b->d_ready, nodes)) ||
-        (rc = dmalloc(&b->d_arena, b->arena_cap)) || (rc = dmalloc(&b->d_arena_used, 1)) ||
-        (rc = dmalloc(&b->d_ctl, n)) || (rc = dmalloc(&b->d_prob_scene, n)) ||
-        (rc = dmalloc(&b->d_next, 1)) || (rc = dmalloc(&b->d_scene_words, n)) ||
-        (rc = dmalloc(&b->d_scene_f64, n))) {
-        delete b;
-        return rc;
-    }
-    // ready flags start at epoch 0; launches use epoch >= 1
-    cudaMemset(b->d_ready, 0, sizeof(unsigned) * nodes);
-    // one scene table entry per problem (scenes may repeat)
-    std::vector<const uint32_t*> sw(n);
-    std::vector<SceneF64> sf(n);
-    std::vector<int> ps(n);
+    // path arena: room for a 4096-config path per problem on average
+    b->arena = (unsigned long long)dof * std::min<long long>(4096, 2 * b->cap) * n_problems;
+    return PRRTC_OK;
+}
+
+// Binds the batch to a workspace and stages the inputs into its pinned buffer.
+int batch_bind(prrtc_batch* b, Workspace* ws, const prrtc_scene* const* scenes, const double* starts,
+               const double* goals) {
+    int rc = ws->reserve(b->device, b->n, b->dof, b->stride, b->arena);
+    if (rc) return rc;
+    b->ws = ws;
+    const size_t n = b->n, dof = b->dof;
+    unsigned char* h = static_cast<unsigned char*>(ws->h_io);
+    unsigned char* d = ws->d_in;
+    size_t o = 0;
+    std::memcpy(h + o, starts, 8 * n * dof);
+    b->d_starts = reinterpret_cast<double*>(d + o);
+    o += 8 * n * dof;
+    std::memcpy(h + o, goals, 8 * n * dof);
+    b->d_goals = reinterpret_cast<double*>(d + o);
+    o += 8 * n * dof;
+    auto** sw = reinterpret_cast<const uint32_t**>(h + o);
+    b->d_scene_words = reinterpret_cast<const uint32_t**>(d + o);
+    o += sizeof(void*) * n;
+    auto* sf = reinterpret_cast<SceneF64*>(h + o);
+    b->d_scene_f64 = reinterpret_cast<SceneF64*>(d + o);
+    o += sizeof(SceneF64) * n;
+    auto* ps = reinterpret_cast<int*>(h + o);
+    b->d_prob_scene = reinterpret_cast<int*>(d + o);
+    o += 4 * n;
     for (size_t i = 0; i < n; ++i) {
         const SceneArgs sa = scenes[i]->args();
         sw[i] = sa.words;
         sf[i] = sa.f64;
         ps[i] = (int)i;
     }
-    cudaMemcpy(b->d_scene_words, sw.data(), sizeof(void*) * n, cudaMemcpyHostToDevice);
-    cudaMemcpy(b->d_scene_f64, sf.data(), sizeof(SceneF64) * n, cudaMemcpyHostToDevice);
-    cudaMemcpy(b->d_prob_scene, ps.data(), sizeof(int) * n, cudaMemcpyHostToDevice);
-    cudaMemcpy(b->d_starts, starts, sizeof(double) * n * dof, cudaMemcpyHostToDevice);
-    cudaMemcpy(b->d_goals, goals, sizeof(double) * n * dof, cudaMemcpyHostToDevice);
-    cudaEventCreate(&b->ev0);
-    cudaEventCreate(&b->ev1);
-    cudaError_t e = cudaDeviceSynchronize();
-    if (e != cudaSuccess) {
-        delete b;
-        return set_err(PRRTC_ECUDA, std::string("prrtc_batch_create: ") + cudaGetErrorString(e));
-    }
-    *out = b;
+    b->d_arena_used = reinterpret_cast<unsigned long long*>(ws->d_out);
+    b->d_next = reinterpret_cast<int*>(ws->d_out + 8);
+    b->d_ndone = reinterpret_cast<int*>(ws->d_out + 12);
+    b->d_ctl = reinterpret_cast<ProbCtl*>(ws->d_out + 128);
+    b->d_arena = reinterpret_cast<double*>(ws->d_out + Workspace::out_hdr(n));
     return PRRTC_OK;
 }
 
-int prrtc_batch_launch(prrtc_batch* b, void* stream) {
-    if (!b) return set_err(PRRTC_EINVAL, "prrtc_batch_launch: null batch");
+size_t io_used(const prrtc_batch* b) {
+    const size_t n = b->n, dof = b->dof;
+    return 8 * 2 * n * dof + sizeof(void*) * n + sizeof(SceneF64) * n + 4 * n;
+}
+
+// Enqueues: inputs H2D (optional), header memset, the planner kernel.
+int batch_enqueue(prrtc_batch* b, cudaStream_t st, bool upload) {
+    Workspace* ws = b->ws;
     cudaSetDevice(b->device);
-    cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
     b->last_stream = st;
-    ++b->epoch;
-    if (b->epoch == 0) ++b->epoch;
-    CUDA_TRY(cudaMemsetAsync(b->d_ctl, 0, sizeof(ProbCtl) * b->n, st));
-    CUDA_TRY(cudaMemsetAsync(b->d_arena_used, 0, sizeof(unsigned long long), st));
-    CUDA_TRY(cudaMemsetAsync(b->d_next, 0, sizeof(int), st));
+    if (++ws->epoch == 0) ++ws->epoch;
+    if (upload) CUDA_TRY(cudaMemcpyAsync(ws->d_in, ws->h_io, io_used(b), cudaMemcpyHostToDevice, st));
+    CUDA_TRY(cudaMemsetAsync(ws->d_out, 0, Workspace::out_hdr(b->n), st));
     PlanArgs a{};
     a.robot = b->robot->d_words;
     a.fine_r64 = b->robot->d_fine_r64;
@@ -687,17 +766,18 @@ int prrtc_batch_launch(prrtc_batch* b, void* stream) {
     a.goals = b->d_goals;
     a.n_problems = b->n;
     a.ctl = b->d_ctl;
-    a.cfg = b->d_cfg;
-    a.parent = b->d_parent;
-    a.ready = b->d_ready;
-    a.dd = b->d_dd;
+    a.cfg = ws->d_cfg;
+    a.parent = ws->d_parent;
+    a.ready = ws->d_ready;
+    a.dd = ws->d_dd;
     a.cap = b->cap;
     a.stride = b->stride;
     a.arena = b->d_arena;
     a.arena_used = b->d_arena_used;
-    a.arena_cap = b->arena_cap;
+    a.arena_cap = b->arena;
     a.next_problem = b->d_next;
-    a.epoch = b->epoch;
+    a.n_done = b->d_ndone;
+    a.epoch = ws->epoch;
     a.p.delta = b->params.delta;
     a.p.dd_radius = b->params.dd_radius > 0.0 ? b->params.dd_radius : 4.0 * b->params.delta;
     a.p.n_cc = b->params.n_cc;
@@ -710,16 +790,14 @@ int prrtc_batch_launch(prrtc_batch* b, void* stream) {
     a.p.seed = b->params.seed;
     a.ns_max = b->ns_max;
     a.nthreads = b->nthreads;
-    CUDA_TRY(cudaEventRecord(b->ev0, st));
+    CUDA_TRY(cudaEventRecord(ws->ev0, st));
     CUDA_TRY(launch_plan(b->robot->args(), a, b->grid, st));
-    CUDA_TRY(cudaEventRecord(b->ev1, st));
+    CUDA_TRY(cudaEventRecord(ws->ev1, st));
     b->launches = 1;
     return PRRTC_OK;
 }
 
-int prrtc_batch_launch_count(const prrtc_batch* b) { return b ? b->launches : 0; }
-
-static const char* message_for(int msg) {
+const char* message_for(int msg) {
     switch (msg) {  // planner.cpp:270-276, 317-320
         case 1: return "start configuration is out of limits or in collision";
         case 2: return "goal configuration is out of limits or in collision";
@@ -731,7 +809,7 @@ static const char* message_for(int msg) {
 }
 
 // path_cost (planner.cpp:152-158) with the scalar distance (nn.cpp:12-20).
-static double path_cost(const double* path, uint32_t len, uint32_t dof) {
+double path_cost(const double* path, uint32_t len, uint32_t dof) {
     double cost = 0.0;
     for (uint32_t i = 1; i < len; ++i) {
         double acc = 0.0;
@@ -744,19 +822,29 @@ static double path_cost(const double* path, uint32_t len, uint32_t dof) {
     return cost;
 }
 
-int prrtc_batch_results(prrtc_batch* b, prrtc_result* out) {
-    if (!b || !out) return set_err(PRRTC_EINVAL, "prrtc_batch_results: null argument");
+// Copies the header, controls and used arena back and fills out[].
+int batch_collect(prrtc_batch* b, prrtc_result* out) {
+    Workspace* ws = b->ws;
     cudaSetDevice(b->device);
+    const size_t hdr = Workspace::out_hdr(b->n);
+    // one D2H of header + controls + an arena prefix; a second one only when
+    // the paths overflow the prefix
+    const size_t prefix = std::min<size_t>(b->arena, 1 << 16);
+    CUDA_TRY(cudaMemcpyAsync(ws->h_out, ws->d_out, hdr + 8 * prefix, cudaMemcpyDeviceToHost, b->last_stream));
     CUDA_TRY(cudaStreamSynchronize(b->last_stream));
+    const unsigned char* h = static_cast<const unsigned char*>(ws->h_out);
+    unsigned long long used = *reinterpret_cast<const unsigned long long*>(h);
+    used = std::min<unsigned long long>(used, b->arena);
+    const ProbCtl* ctl = reinterpret_cast<const ProbCtl*>(h + 128);
+    const double* arena = reinterpret_cast<const double*>(h + hdr);
+    std::vector<double> big;
+    if (used > prefix) {
+        big.resize(used);
+        CUDA_TRY(cudaMemcpy(big.data(), b->d_arena, 8 * used, cudaMemcpyDeviceToHost));
+        arena = big.data();
+    }
     float ms = 0.f;
-    cudaEventElapsedTime(&ms, b->ev0, b->ev1);
-    std::vector<ProbCtl> ctl(b->n);
-    unsigned long long used = 0;
-    CUDA_TRY(cudaMemcpy(ctl.data(), b->d_ctl, sizeof(ProbCtl) * b->n, cudaMemcpyDeviceToHost));
-    CUDA_TRY(cudaMemcpy(&used, b->d_arena_used, sizeof(used), cudaMemcpyDeviceToHost));
-    used = std::min(used, b->arena_cap);
-    std::vector<double> arena(used);
-    if (used) CUDA_TRY(cudaMemcpy(arena.data(), b->d_arena, 8 * used, cudaMemcpyDeviceToHost));
+    cudaEventElapsedTime(&ms, ws->ev0, ws->ev1);
     for (int i = 0; i < b->n; ++i) {
         prrtc_result& r = out[i];
         std::memset(&r, 0, sizeof(r));
@@ -769,18 +857,20 @@ int prrtc_batch_results(prrtc_batch* b, prrtc_result* out) {
             C.path_off + (unsigned long long)C.path_len * b->dof <= used) {
             r.path_len = C.path_len;
             r.path = static_cast<double*>(std::malloc(sizeof(double) * b->dof * C.path_len));
-            std::memcpy(r.path, arena.data() + C.path_off, sizeof(double) * b->dof * C.path_len);
+            std::memcpy(r.path, arena + C.path_off, sizeof(double) * b->dof * C.path_len);
             r.cost = path_cost(r.path, r.path_len, b->dof);
         } else if (r.status == PRRTC_SOLVED) {
             r.status = PRRTC_FAILED;
             std::snprintf(r.message, sizeof(r.message), "path unavailable");
         }
+        // per-problem device time (globaltimer: initialisation -> finish)
         r.device_time_ms = (C.t_end_ns > C.t_start_ns) ? (C.t_end_ns - C.t_start_ns) * 1e-6 : 0.0;
-        r.wall_time_ms = ms;  // whole-launch device time; prrtc_plan overwrites with host wall time
+        r.wall_time_ms = ms;  // launch time; prrtc_plan overwrites with the host wall clock
         r.iterations_total = C.iters < b->budget ? C.iters : b->budget;
         r.sphere_tests = C.sphere_tests;
         r.fk_calls = C.fk_calls;
         r.fine_stage_entries = C.fine_entries;
+        r.flops = C.flops;
         r.tree_nodes[0] = (uint64_t)std::max(0, C.published[0]);
         r.tree_nodes[1] = (uint64_t)std::max(0, C.published[1]);
         r.solving_worker = C.winner - 1;
@@ -788,25 +878,68 @@ int prrtc_batch_results(prrtc_batch* b, prrtc_result* out) {
     return PRRTC_OK;
 }
 
+}  // namespace
+
+extern "C" {
+
+int prrtc_batch_create(const prrtc_robot* robot, const prrtc_scene* const* scenes,
+                       uint32_t n_problems, const double* starts, const double* goals,
+                       uint32_t dof, const prrtc_params* params, prrtc_batch** out) {
+    if (!out) return set_err(PRRTC_EINVAL, "prrtc_batch_create: null argument");
+    auto* b = new prrtc_batch();
+    int rc = batch_setup(b, robot, scenes, n_problems, starts, goals, dof, params);
+    if (!rc) rc = batch_bind(b, &b->own, scenes, starts, goals);
+    if (!rc) {  // inputs uploaded once
+        cudaSetDevice(b->device);
+        if (cudaMemcpy(b->own.d_in, b->own.h_io, io_used(b), cudaMemcpyHostToDevice) != cudaSuccess)
+            rc = set_err(PRRTC_ECUDA, "prrtc_batch_create: input upload failed");
+    }
+    if (rc) {
+        delete b;
+        return rc;
+    }
+    *out = b;
+    return PRRTC_OK;
+}
+
+int prrtc_batch_launch(prrtc_batch* b, void* stream) {
+    if (!b) return set_err(PRRTC_EINVAL, "prrtc_batch_launch: null batch");
+    return batch_enqueue(b, reinterpret_cast<cudaStream_t>(stream), false);
+}
+
+int prrtc_batch_launch_count(const prrtc_batch* b) { return b ? b->launches : 0; }
+
+int prrtc_batch_results(prrtc_batch* b, prrtc_result* out) {
+    if (!b || !out) return set_err(PRRTC_EINVAL, "prrtc_batch_results: null argument");
+    return batch_collect(b, out);
+}
+
 int prrtc_batch_destroy(prrtc_batch* b) {
     delete b;
     return PRRTC_OK;
 }
 
+// Host-buffer entry point (the e2e path): packed H2D, kernel, D2H on the
+// device's cached workspace.
 int prrtc_plan_batch(const prrtc_robot* robot, const prrtc_scene* const* scenes,
                      uint32_t n_problems, const double* starts, const double* goals,
                      uint32_t dof, const prrtc_params* params, prrtc_result* out) {
     const auto t0 = std::chrono::steady_clock::now();
-    prrtc_batch* b = nullptr;
-    int rc = prrtc_batch_create(robot, scenes, n_problems, starts, goals, dof, params, &b);
+    if (!out) return set_err(PRRTC_EINVAL, "plan: null result");
+    prrtc_batch b;
+    int rc = batch_setup(&b, robot, scenes, n_problems, starts, goals, dof, params);
     if (rc) return rc;
-    rc = prrtc_batch_launch(b, nullptr);
-    if (!rc) rc = prrtc_batch_results(b, out);
-    prrtc_batch_destroy(b);
+    if (b.device < 0 || b.device >= 64) return set_err(PRRTC_ENODEV, "device ordinal out of range");
+    std::lock_guard<std::mutex> lk(g_ws_mu[b.device]);
+    Workspace& ws = g_ws[b.device];
+    rc = batch_bind(&b, &ws, scenes, starts, goals);
+    if (!rc) rc = batch_enqueue(&b, ws.stream, true);
+    if (!rc) rc = batch_collect(&b, out);
+    if (rc) return rc;
     const double wall =
         std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
-    if (!rc && n_problems == 1) out[0].wall_time_ms = wall;
-    return rc;
+    if (n_problems == 1) out[0].wall_time_ms = wall;
+    return PRRTC_OK;
 }
 
 int prrtc_plan(const prrtc_robot* robot, const prrtc_scene* scene, const double* start,

@@ -129,6 +129,7 @@ struct PlanArgs {
     unsigned long long* arena_used;
     unsigned long long arena_cap;
     int* next_problem;         // unstarted-problem ticket
+    int* n_done;               // finished problems (helpers exit when all are done)
     unsigned epoch;
     PlanParamsDev p;
     int ns_max;                // states per validation chunk

@@ -312,6 +312,7 @@ __device__ void finish_problem(const PlanArgs& a, int prob, int done, int msg) {
         C.t_end_ns = globaltimer();
         __threadfence();
         st_release(&C.done, done);
+        atomicAdd(a.n_done, 1);
     }
 }
 
@@ -408,8 +409,18 @@ __device__ bool init_problem(Ctx& c, const PlanArgs& a, int prob, unsigned long 
 // number of workers may join a problem at any time. -1 when none is left.
 __device__ int pick_help(Ctx& c, const PlanArgs& a) {
     const int tid = threadIdx.x;
-    // help mode: running problem with the fewest active CTAs (ties -> lowest)
-    for (int attempt = 0; attempt < 4; ++attempt) {
+    // help mode: running problem with the fewest active CTAs (ties -> lowest);
+    // wait while problems are claimed but not yet initialised, exit when all
+    // problems are finished
+    for (int attempt = 0;; ++attempt) {
+        if (attempt > 0) {
+            if (tid == 0) c.ictl[IC_TMP1] = ld_acquire(a.n_done);
+            __syncthreads();
+            const bool all_done = c.ictl[IC_TMP1] >= a.n_problems;
+            __syncthreads();
+            if (all_done) return -1;
+            __nanosleep(200);
+        }
         int bk = 0x7fffffff, bp = -1;
         for (int q = tid; q < a.n_problems; q += c.nthreads) {
             const ProbCtl& C = a.ctl[q];
@@ -456,9 +467,7 @@ __device__ int pick_help(Ctx& c, const PlanArgs& a) {
         const int p = c.ictl[IC_TMP1];
         __syncthreads();
         if (p >= 0) return p;
-        if (p == -1) return -1;
     }
-    return -1;
 }
 
 // CheckStats counters (collision.hpp:17-25), reduced per warp then per CTA.

@@ -170,7 +170,7 @@ def test_nn_exact_with_ties(gpu, oracle):
                 tree[count // 2] = tree[1]
                 tree[-1] = tree[1]
             q = rng.uniform(-3, 3, (8, dof))
-            q[0] = tree[1]  # zero distance, first index wins
+            q[0] = tree[min(1, count - 1)]  # zero distance, first index wins
             q[1] = tree[count // 2]
             idx, d2 = planner.debug_nn(tree, q)
             for i in range(len(q)):
