@@ -1,0 +1,323 @@
+#!/usr/bin/env python
+"""bench.py — B200 pRRTC planning benchmark (BASELINE.json metric).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl b200|reference]
+
+Metric (BASELINE.json): "median/p95 ms-to-first-solution per problem;
+problems/sec at 1/2/4/8 B200". Workload = BASELINE configs[1]: Panda 7-DoF,
+a batch of 1000 synthetic MotionBenchMaker-shaped problems (334 table_pick /
+333 bookshelf / 333 cage, tests/golden/problems_panda.npz), reference default
+PlannerParams (delta 0.5, n_cc 32, tree_capacity 200000, dynamic domain,
+two-stage, early exit, Halton).
+
+A step = one full solve of the 1000-problem batch (every problem to Solved
+or Failed) by one persistent plan_kernel launch on inputs already resident
+in HBM; `value` = problems/s of the whole job (N ranks x 1000 problems / the
+max-over-ranks step time; weak scaling, no collective on the data path).
+`e2e` = the same through the host-buffer C-ABI call prrtc_plan_batch
+(packed H2D of starts/goals/scene table, kernel, D2H of results/paths).
+`latency_ms` = median / p95 of single-problem prrtc_plan calls (host wall
+clock around the C call, setup excluded as in PAPER.md:201).
+
+--impl reference times the reference's own CPU planner (oracle/_ref, the
+unmodified reference sources; the C restatement oracle/liboracle.so when the
+reference build is absent) on the host cores, same problems and params.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+METRIC = "median/p95 ms-to-first-solution per problem; problems/sec at 1/2/4/8 B200"
+UNIT = "problems/s"
+
+
+def load_workload(robot: str, n: int):
+    from paper_2503_06757_b200 import robots
+    from paper_2503_06757_b200.scenes import make_scene
+    d = np.load(ROOT / "tests" / "golden" / f"problems_{robot}.npz")
+    n = min(n, len(d["pid"]))
+    scenes = [make_scene(robot, str(k), int(p))[0] for k, p in zip(d["kind"][:n], d["pid"][:n])]
+    return robots.get(robot), scenes, d["start"][:n].copy(), d["goal"][:n].copy(), d["kind"][:n]
+
+
+def workload_config(robot, n, params, extra=None):
+    cfg = {
+        "workload": f"{robot}_mbm_{n}",
+        "robot": robot,
+        "problems_per_gpu": n,
+        "scenes": "table_pick/bookshelf/cage 334/333/333 (synthetic MBM-shaped, tests/golden)",
+        "params": {"delta": params.delta, "n_cc": params.n_cc, "tree_capacity": params.tree_capacity,
+                   "max_iters_per_worker": params.max_iters_per_worker, "dynamic_domain": True,
+                   "two_stage": True, "early_exit": True, "sampler": "halton"},
+        "l2": "flushed between timed steps (256 MiB write)",
+    }
+    if extra:
+        cfg.update(extra)
+    return cfg
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons during the timed region."""
+
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device: int):
+        self.device = device
+        self.samples = []
+        self._stop = threading.Event()
+        self._t = None
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                out = subprocess.run(["nvidia-smi", "-i", str(self.device), f"--query-gpu={self.FIELDS}",
+                                      "--format=csv,noheader,nounits"], capture_output=True, text=True,
+                                     timeout=5).stdout.strip()
+                if out:
+                    self.samples.append([x.strip() for x in out.split(",")])
+            except Exception:
+                pass
+            self._stop.wait(0.2)
+
+    def __enter__(self):
+        self._t = threading.Thread(target=self._run, daemon=True)
+        self._t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        self._t.join(timeout=10)
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        sm = [float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit()]
+        mx = [float(s[2]) for s in self.samples if s[2].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for s in self.samples for i in range(4)
+                          if len(s) > 5 + i and s[5 + i].lower() == "active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.samples)}
+
+
+def dist_setup():
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl" if os.environ.get("PRRTC_BENCH_BACKEND", "nccl") == "nccl" else "gloo")
+    return world, rank, local
+
+
+def dist_max(x: float, world: int) -> float:
+    if world == 1:
+        return x
+    import torch
+    import torch.distributed as dist
+    dev = "cuda" if dist.get_backend() == "nccl" else "cpu"
+    t = torch.tensor([x], dtype=torch.float64, device=dev)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def dist_barrier(world: int):
+    if world > 1:
+        import torch.distributed as dist
+        dist.barrier()
+
+
+def cpu_reference(model, scenes, S, G, params, threads):
+    """Reference CPU planner (oracle/_ref when built, else the C port)."""
+    from oracle import Oracle, available
+    kind = "reference" if available("ref") else "port"
+    o = Oracle("ref" if kind == "reference" else "port")
+    res, ms = o.plan_many(model, scenes, S, G, params, threads=threads)
+    return o, kind, res, ms
+
+
+def traffic_from_profiles():
+    p = ROOT / "profiles" / "ncu_summary.json"
+    if p.exists():
+        try:
+            return json.loads(p.read_text()).get("plan_kernel_dram_bytes_per_launch")
+        except Exception:
+            return None
+    return None
+
+
+def run_reference(args):
+    world, rank, _ = dist_setup()
+    from paper_2503_06757_b200.model import PlannerParams
+    if rank != 0:
+        return 0
+    model, scenes, S, G, kinds = load_workload(args.robot, args.problems)
+    params = PlannerParams(workers=1)
+    threads = os.cpu_count() or 1
+    for _ in range(args.warmup):
+        cpu_reference(model, scenes[:64], S[:64], G[:64], params, threads)
+    times, solved, lat = [], [], []
+    kind = None
+    for _ in range(args.steps):
+        o, kind, res, ms = cpu_reference(model, scenes, S, G, params, threads)
+        times.append(ms)
+        solved.append(np.mean([r.status == 0 for r in res]))
+        lat += [r.wall_time_ms for r in res if r.status == 0]
+    ms = statistics.median(times)
+    value = len(S) / (ms / 1e3)
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": workload_config(args.robot, len(S), params, {"host_threads": threads, "workers_per_problem": 1}),
+        "success_rate": float(np.mean(solved)),
+        "latency_ms": {"median": float(np.median(lat)) if lat else None,
+                       "p95": float(np.percentile(lat, 95)) if lat else None, "threads_per_problem": 1},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": kind,
+                         "sample": f"all {len(S)} problems x {args.steps} steps, workers=1 per problem, "
+                                   f"{threads} host threads"},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line))
+    return 0
+
+
+def run_b200(args):
+    world, rank, local = dist_setup()
+    import torch
+    from paper_2503_06757_b200 import _lib, planner
+    from paper_2503_06757_b200.model import PlannerParams, PlanStatus
+    from paper_2503_06757_b200.planner import Batch
+
+    torch.cuda.set_device(local)
+    dev = local
+    model, scenes, S, G, kinds = load_workload(args.robot, args.problems)
+    n = len(S)
+    params = PlannerParams()
+    batch = Batch(model, scenes, S, G, params, device=dev)
+    stream = torch.cuda.Stream(device=dev)
+    flush = torch.empty(64 * 1024 * 1024, dtype=torch.float32, device=f"cuda:{dev}")
+    with torch.cuda.stream(stream):
+        for _ in range(max(3, args.warmup)):
+            batch.launch(stream.cuda_stream)
+        stream.synchronize()
+    warm_res = batch.results()
+    # ---- timed region: K steps, L2 flushed between steps (untimed) ----
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    step_ms = []
+    dist_barrier(world)
+    torch.cuda.synchronize()
+    with ClockSampler(dev) as clk:
+        with torch.cuda.stream(stream):
+            for k in range(args.steps):
+                flush.zero_()
+                ev[k][0].record(stream)
+                batch.launch(stream.cuda_stream)
+                ev[k][1].record(stream)
+        torch.cuda.synchronize()
+    dist_barrier(world)
+    step_ms = [a.elapsed_time(b) for a, b in ev]
+    res = batch.results()  # last step's outcome (copied after the timed region)
+    ms = dist_max(sum(step_ms) / len(step_ms), world)
+    value = world * n / (ms / 1e3)
+    solved = [r.status == PlanStatus.Solved for r in res]
+    flops = float(sum(r.flops for r in res))
+
+    line = None
+    if rank == 0:
+        # ---- roofline of the dominant (only) kernel: plan_kernel ----
+        peak = _lib.load().prrtc_fp32_peak_tflops(dev)
+        kernel_ms = statistics.median(step_ms)
+        achieved = flops / (kernel_ms * 1e-3) / 1e12
+        # ---- e2e through the host-buffer C-ABI (prrtc_plan_batch) ----
+        e2e_ms = []
+        for _ in range(max(1, min(args.steps, 5))):
+            t0 = time.perf_counter()
+            er = planner.plan_batch(model, scenes, S, G, params, device=dev)
+            e2e_ms.append((time.perf_counter() - t0) * 1e3)
+        e2e_solved = np.mean([r.status == PlanStatus.Solved for r in er])
+        h2d = n * model.dof * 8 * 2 + n * (8 + 24 + 4)
+        d2h = 128 + 128 * n + sum(len(r.path) * model.dof * 8 for r in er)
+        # ---- single-problem latency (prrtc_plan, host wall clock) ----
+        idx = list(range(0, n, max(1, n // args.latency_samples)))[: args.latency_samples]
+        for i in idx[:5]:
+            planner.plan(model, scenes[i], S[i], G[i], params, device=dev)
+        lat, dlat, lst = [], [], []
+        for i in idx:
+            r = planner.plan(model, scenes[i], S[i], G[i], params, device=dev)
+            lst.append(r.status == PlanStatus.Solved)
+            if r.status == PlanStatus.Solved:
+                lat.append(r.wall_time_ms)
+                dlat.append(r.device_time_ms)
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": max(3, args.warmup), "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f32+f64", "data": "synthetic",
+            "config": workload_config(args.robot, n, params, {"parallelism": f"dp{world} (independent problems per GPU)"}),
+            "success_rate": float(np.mean(solved)),
+            "success_by_scene": {k: float(np.mean([s for s, kk in zip(solved, kinds) if kk == k]))
+                                 for k in ("table_pick", "bookshelf", "cage")},
+            "mean_cost": float(np.mean([r.cost for r in res if r.status == PlanStatus.Solved])),
+            "latency_ms": {"median": float(np.median(lat)), "p95": float(np.percentile(lat, 95)),
+                           "device_median": float(np.median(dlat)), "samples": len(idx),
+                           "success_rate": float(np.mean(lst)), "api": "prrtc_plan (host wall clock)"},
+            "e2e": {"value": n / (statistics.median(e2e_ms) / 1e3), "unit": UNIT, "h2d_bytes_per_step": int(h2d),
+                    "d2h_bytes_per_step": int(d2h), "success_rate": float(e2e_solved),
+                    "api": "prrtc_plan_batch (host buffers)"},
+            "roofline": {"bound": "fp32", "kernel": "plan_kernel", "achieved": achieved, "peak": peak,
+                         "unit": "TFLOP/s", "frac": achieved / peak if peak else None,
+                         "peak_source": "measured FFMA-chain microbenchmark (prrtc_fp32_peak_tflops); "
+                                        "MEASURED_PEAKS.json has no FP32 figure",
+                         "algorithmic_flops_per_launch": flops, "traffic": traffic_from_profiles()},
+            "gpu_launches": args.steps,
+            "clocks": clk.summary(),
+        }
+        if world == 1 and not args.no_cpu_baseline:
+            threads = os.cpu_count() or 1
+            _, kind, cres, cms = cpu_reference(model, scenes, S, G, PlannerParams(workers=1), threads)
+            line["cpu_baseline"] = {
+                "value": n / (cms / 1e3), "unit": UNIT, "cores": threads, "kind": kind,
+                "sample": f"all {n} problems once, reference plan() workers=1 per problem on {threads} host threads",
+                "success_rate": float(np.mean([r.status == 0 for r in cres])),
+                "latency_ms_median": float(np.median([r.wall_time_ms for r in cres if r.status == 0])),
+            }
+        print(json.dumps(line))
+    if world > 1:
+        import torch.distributed as dist
+        dist.destroy_process_group()
+    return 0
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    ap.add_argument("--robot", default="panda")
+    ap.add_argument("--problems", type=int, default=1000)
+    ap.add_argument("--latency-samples", type=int, default=100)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    if args.impl == "reference":
+        return run_reference(args)
+    return run_b200(args)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

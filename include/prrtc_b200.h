@@ -267,6 +267,11 @@ int prrtc_debug_halton(const uint32_t* bases, const uint64_t* indices, uint32_t 
    index0 .. index0+n-1 against the robot's limits. */
 int prrtc_debug_sample(const prrtc_robot* robot, uint64_t index0, uint32_t n, double* out);
 
+/* ---------------- measurement utility ---------------- */
+/* FP32 FMA-pipe peak of the device in TFLOP/s, measured with an FFMA-chain
+   microbenchmark (the roofline denominator of the FK / collision work). */
+double prrtc_fp32_peak_tflops(int device);
+
 #ifdef __cplusplus
 }
 #endif

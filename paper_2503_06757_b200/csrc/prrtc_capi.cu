@@ -694,8 +694,12 @@ int batch_setup(prrtc_batch* b, const prrtc_robot* robot, const prrtc_scene* con
     } else {
         const unsigned per_sm = params->ctas_per_sm ? std::min<unsigned>(params->ctas_per_sm, occ) : occ;
         b->grid = sms * per_sm;
-        workers_eff = params->workers ? params->workers
-                                      : std::max(1u, (unsigned)(b->grid / std::min<int>(b->grid, n_problems)));
+        // batch budget: workers=0 gives every problem the iteration budget of
+        // kBatchWorkers reference workers (the reference's default is
+        // workers = hardware concurrency, planner.cpp:287-288); CTAs are
+        // shared elastically, so this is a budget, not a CTA count
+        constexpr unsigned kBatchWorkers = 32;
+        workers_eff = params->workers ? params->workers : kBatchWorkers;
     }
     b->budget = params->max_iters_per_worker * (unsigned long long)workers_eff;
     // path arena: room for a 4096-config path per problem on average
@@ -1127,6 +1131,12 @@ int prrtc_debug_halton(const uint32_t* bases, const uint64_t* indices, uint32_t 
     cudaFree(dout);
     if (e != cudaSuccess) return set_err(PRRTC_ECUDA, std::string("prrtc_debug_halton: ") + cudaGetErrorString(e));
     return PRRTC_OK;
+}
+
+double prrtc_fp32_peak_tflops(int device) {
+    if (check_device(device)) return 0.0;
+    cudaSetDevice(device);
+    return measure_fp32_peak(sm_count(device), 0);
 }
 
 int prrtc_debug_sample(const prrtc_robot* robot, uint64_t index0, uint32_t n, double* out) {

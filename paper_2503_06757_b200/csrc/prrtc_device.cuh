@@ -175,10 +175,17 @@ __device__ __forceinline__ int band(float d2, float rr, float eps) {
 
 // ---------------------------------------------------------------------------
 // CTA context: pointers into dynamic shared memory
+//
+// SIMT mapping (PAPER.md:178-180 re-designed for 32-wide warps): a chunk holds
+// NS = 32/64/128 edge states; lane i of every warp owns states i, i+32, ...;
+// warps split the per-state work by link (FK), by (link, primitive group)
+// (coarse stage) and by flagged entry (fine stage), so the primitive data
+// is a warp-uniform shared-memory broadcast and each state's data is
+// conflict-free (state is the fastest smem index).
 // ---------------------------------------------------------------------------
 struct Ctx {
     // robot (shared memory copy of the packed words)
-    int L, dof, S, NP, MF;
+    int L, dof, S, NP, MF, mflog;  // mflog: log2 of MF rounded up to a power of two
     const int4* info;      // kind, parent, q_index, fine_off
     const int* nfine;
     const float* geo;      // [L][GEO_STRIDE]
@@ -188,6 +195,7 @@ struct Ctx {
     const int* flink;      // [S] link of each fine sphere
     const double* fine_r64;  // global
     const double* limits;    // global [dof][2]
+    unsigned fkflops;        // per-state FK + coarse posing flops
     // scene (shared memory copy)
     int ns, nb, nc, P;
     const float4* sph;
@@ -196,7 +204,7 @@ struct Ctx {
     float eps, cpad;
     SceneF64 s64;  // global FP64 mirror
     // per-chunk buffers
-    int NS;          // states per chunk (multiple of 32)
+    int NS, nslog;   // states per chunk (32, 64 or 128)
     float* pose;     // [L][12][NS]
     float* ccen;     // [L][3][NS]
     float* qf;       // [dof][NS]
@@ -204,6 +212,8 @@ struct Ctx {
     int* sbad;       // [NS]
     int* queue;      // [kQueueMax]
     int* pqueue;     // [kQueueMax]
+    double* ends;    // [NS + 2][dof] chain points of the chunk
+    int* ends_eq;    // [NS + 2] bitwise-equal sub-edge flags
     // CTA scalars
     int* ictl;       // [32] misc ints
     double* dcfg;    // [8][kMaxDof] scratch configs
@@ -230,6 +240,7 @@ enum : int {
     IC_TMP5,
     IC_TMP6,
     IC_TMP7,
+    IC_KLO,         // first chain point held in `ends`
     IC_COUNT = 32
 };
 
@@ -253,44 +264,45 @@ __device__ __forceinline__ float3 pose_point(const Ctx& c, int l, int s, float p
 
 // ---------------------------------------------------------------------------
 // forward kinematics for the chunk's states (kinematics.cpp:92-103), FP32
-//   phase A: (state, link) items -> local transform origin_tf * motion(q)
+//   phase A: warps split links, lanes states -> local transform
+//            origin_tf * motion(q) (Rodrigues folded: cos M1 + sin M2 +
+//            (1 - cos) M3, see prrtc_internal.h)
 //   phase B: 3 lanes per state compose world = parent * local row by row
-//   phase C: (state, link) items -> posed coarse centers
+//   phase C: warps split links, lanes states -> posed coarse centers
 // ---------------------------------------------------------------------------
 __device__ __noinline__ void fk_chunk(Ctx& c, int cnt) {
-    const int tid = threadIdx.x;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nw = c.nthreads >> 5;
     const int NS = c.NS;
-    // phase A
-    for (int it = tid; it < c.L * NS; it += c.nthreads) {
-        const int s = it % NS, l = it / NS;
-        if (s >= cnt) continue;
+    for (int l = warp; l < c.L; l += nw) {
         const int4 inf = c.info[l];
         const float* g = c.geo + l * GEO_STRIDE;
-        float* P = c.pose + (size_t)l * 12 * NS + s;
-        if (inf.x == PRRTC_JOINT_REVOLUTE) {
-            const float q = c.qf[inf.z * NS + s];
-            float sn, cs;
-            sincosf(q, &sn, &cs);
-            const float omc = 1.0f - cs;
-#pragma unroll
-            for (int k = 0; k < 9; ++k) {
-                P[k * NS] = __fmaf_rn(cs, g[k], __fmaf_rn(sn, g[9 + k], __fmul_rn(omc, g[18 + k])));
-            }
-            P[9 * NS] = g[27];
-            P[10 * NS] = g[28];
-            P[11 * NS] = g[29];
-        } else {
-#pragma unroll
-            for (int k = 0; k < 9; ++k) P[k * NS] = g[k];
-            if (inf.x == PRRTC_JOINT_PRISMATIC) {
+        for (int s = lane; s < cnt; s += 32) {
+            float* P = c.pose + (size_t)l * 12 * NS + s;
+            if (inf.x == PRRTC_JOINT_REVOLUTE) {
                 const float q = c.qf[inf.z * NS + s];
-                P[9 * NS] = __fmaf_rn(g[30], q, g[27]);
-                P[10 * NS] = __fmaf_rn(g[31], q, g[28]);
-                P[11 * NS] = __fmaf_rn(g[32], q, g[29]);
-            } else {
+                float sn, cs;
+                sincosf(q, &sn, &cs);
+                const float omc = 1.0f - cs;
+#pragma unroll
+                for (int k = 0; k < 9; ++k) {
+                    P[k * NS] = __fmaf_rn(cs, g[k], __fmaf_rn(sn, g[9 + k], __fmul_rn(omc, g[18 + k])));
+                }
                 P[9 * NS] = g[27];
                 P[10 * NS] = g[28];
                 P[11 * NS] = g[29];
+            } else {
+#pragma unroll
+                for (int k = 0; k < 9; ++k) P[k * NS] = g[k];
+                if (inf.x == PRRTC_JOINT_PRISMATIC) {
+                    const float q = c.qf[inf.z * NS + s];
+                    P[9 * NS] = __fmaf_rn(g[30], q, g[27]);
+                    P[10 * NS] = __fmaf_rn(g[31], q, g[28]);
+                    P[11 * NS] = __fmaf_rn(g[32], q, g[29]);
+                } else {
+                    P[9 * NS] = g[27];
+                    P[10 * NS] = g[28];
+                    P[11 * NS] = g[29];
+                }
             }
         }
     }
@@ -302,9 +314,10 @@ __device__ __noinline__ void fk_chunk(Ctx& c, int cnt) {
         const bool act = (s < cnt) && (r < 3);
         for (int l = 0; l < c.L; ++l) {
             const int par = c.info[l].y;
+            if (par < 0) continue;  // warp-uniform
             float Rl[9], tl[3];
-            if (act && par >= 0) {
-                const float* P = c.pose + (size_t)l * 12 * NS + s;
+            const float* P = c.pose + (size_t)l * 12 * NS + s;
+            if (act) {
 #pragma unroll
                 for (int k = 0; k < 9; ++k) Rl[k] = P[k * NS];
                 tl[0] = P[9 * NS];
@@ -312,32 +325,32 @@ __device__ __noinline__ void fk_chunk(Ctx& c, int cnt) {
                 tl[2] = P[11 * NS];
             }
             __syncwarp();
-            if (act && par >= 0) {
+            if (act) {
                 const float* Q = c.pose + (size_t)par * 12 * NS + s;
                 const float a0 = Q[(3 * r + 0) * NS], a1 = Q[(3 * r + 1) * NS],
                             a2 = Q[(3 * r + 2) * NS], tp = Q[(9 + r) * NS];
-                float* P = c.pose + (size_t)l * 12 * NS + s;
+                float* W = c.pose + (size_t)l * 12 * NS + s;
 #pragma unroll
                 for (int j = 0; j < 3; ++j) {
-                    P[(3 * r + j) * NS] =
+                    W[(3 * r + j) * NS] =
                         __fmaf_rn(a0, Rl[j], __fmaf_rn(a1, Rl[3 + j], __fmul_rn(a2, Rl[6 + j])));
                 }
-                P[(9 + r) * NS] = __fmaf_rn(a0, tl[0], __fmaf_rn(a1, tl[1], __fmaf_rn(a2, tl[2], tp)));
+                W[(9 + r) * NS] = __fmaf_rn(a0, tl[0], __fmaf_rn(a1, tl[1], __fmaf_rn(a2, tl[2], tp)));
             }
             __syncwarp();
         }
     }
     __syncthreads();
     // phase C: coarse centers
-    for (int it = tid; it < c.L * NS; it += c.nthreads) {
-        const int s = it % NS, l = it / NS;
-        if (s >= cnt) continue;
+    for (int l = warp; l < c.L; l += nw) {
         const float* g = c.geo + l * GEO_STRIDE;
-        const float3 o = pose_point(c, l, s, g[33], g[34], g[35]);
-        float* C = c.ccen + (size_t)l * 3 * NS + s;
-        C[0] = o.x;
-        C[NS] = o.y;
-        C[2 * NS] = o.z;
+        for (int s = lane; s < cnt; s += 32) {
+            const float3 o = pose_point(c, l, s, g[33], g[34], g[35]);
+            float* C = c.ccen + (size_t)l * 3 * NS + s;
+            C[0] = o.x;
+            C[NS] = o.y;
+            C[2 * NS] = o.z;
+        }
     }
     __syncthreads();
 }
@@ -380,24 +393,38 @@ __device__ __forceinline__ int test_flops(const Ctx& c, int p) {
     return p < c.ns ? 10 : (p < c.ns + c.nb ? 27 : 22);
 }
 
-// coarse (padded) sphere vs primitive, FP32 only (conservative)
-__device__ __forceinline__ bool coarse_vs_prim(const Ctx& c, float x, float y, float z, float rc,
-                                               int p) {
-    float d2;
-    if (p < c.ns) {
+// coarse (padded) sphere vs primitives [p0, p1): hit bitmask, FP32 only
+// (conservative: the padding covers FP32 error, so no fine hit is missed)
+__device__ __forceinline__ unsigned long long coarse_mask(const Ctx& c, float x, float y, float z,
+                                                          float rc, int p0, int p1) {
+    unsigned long long m = 0;
+    const int e1 = min(p1, c.ns), e2 = min(p1, c.ns + c.nb);
+    int p = p0;
+    for (; p < e1; ++p) {
+        float d2;
         const float4 s = c.sph[p];
         sph_d2(x, y, z, s, d2);
         const float rr = rc + s.w;
-        return d2 < rr * rr;
-    } else if (p < c.ns + c.nb) {
+        if (d2 < rr * rr) m |= 1ull << p;
+    }
+    for (; p < e2; ++p) {
+        float d2;
         box_d2(x, y, z, c.box + (p - c.ns) * BOX_STRIDE, d2);
-        return d2 < rc * rc;
-    } else {
+        if (d2 < rc * rc) m |= 1ull << p;
+    }
+    for (; p < p1; ++p) {
+        float d2;
         const float* C = c.cap + (p - c.ns - c.nb) * CAP_STRIDE;
         cap_d2(x, y, z, C, d2);
         const float rr = rc + C[7];
-        return d2 < rr * rr;
+        if (d2 < rr * rr) m |= 1ull << p;
     }
+    return m;
+}
+
+__device__ __forceinline__ int range_flops(const Ctx& c, int p0, int p1) {
+    const int e1 = min(p1, c.ns), e2 = min(p1, c.ns + c.nb);
+    return 10 * max(0, e1 - p0) + 27 * max(0, e2 - max(p0, e1)) + 22 * max(0, p1 - max(p0, e2));
 }
 
 // self pair fine spheres (collision.cpp:89-98 / kernels_detail.hpp:17-23)
@@ -410,73 +437,84 @@ __device__ __forceinline__ bool fine_pair(const Ctx& c, float3 a, int ja, float3
     return sphere_sphere_exact(a.x, a.y, a.z, c.fine_r64[ja], b.x, b.y, b.z, c.fine_r64[jb]);
 }
 
-__device__ __forceinline__ void mark_bad(Ctx& c, int s, bool early_exit) {
+__device__ __forceinline__ void mark_bad(Ctx& c, int s) {
     c.sbad[s] = 1;
     atomicMin(&c.ictl[IC_FIRSTBAD], c.sgroup[s]);
-    (void)early_exit;
 }
 
-// skip test for early exit: chain mode skips groups >= first bad;
-// independent mode skips states already bad.
+// skip test for early exit: chain mode skips groups >= first bad (a state
+// of a later or the same sub-edge cannot change the outcome); independent
+// mode skips states already known bad.
 __device__ __forceinline__ bool skip_state(const Ctx& c, int s, bool early_exit, bool indep) {
     if (!early_exit) return false;
     if (indep) return *(volatile int*)&c.sbad[s] != 0;
     return c.sgroup[s] >= *(volatile int*)&c.ictl[IC_FIRSTBAD];
 }
 
-// warp-aggregated push into a shared-memory queue
-__device__ __forceinline__ void queue_push(int* q, int* qn, int* ovf, bool pred, int val) {
-    const unsigned m = __ballot_sync(__activemask(), pred);
-    if (!pred) return;
-    const int lane = threadIdx.x & 31;
-    const int leader = __ffs(m) - 1;
-    int base = 0;
-    if (lane == leader) base = atomicAdd(qn, __popc(m));
-    base = __shfl_sync(m, base, leader);
-    const int pos = base + __popc(m & ((1u << lane) - 1));
-    if (pos < kQueueMax) q[pos] = val; else *ovf = 1;
+__device__ __forceinline__ void push(int* q, int* qn, int* ovf, int val) {
+    const int pos = atomicAdd(qn, 1);
+    if (pos < kQueueMax) q[pos] = val;
+    else *ovf = 1;
 }
 
 // ---------------------------------------------------------------------------
-// brute-force fine-only check of the chunk (collision.cpp:100-128)
+// brute-force fine-only check of the chunk (collision.cpp:100-128): warps
+// split fine spheres (resp. self pairs), lanes states.
 // ---------------------------------------------------------------------------
-__device__ void brute_chunk(Ctx& c, int cnt, bool early_exit, bool indep) {
-    const int tid = threadIdx.x, NS = c.NS;
-    const long long items = (long long)NS * c.S * c.P;
-    for (long long it = tid; it < items; it += c.nthreads) {
-        const int s = (int)(it % NS);
-        const long long rest = it / NS;
-        const int j = (int)(rest % c.S), p = (int)(rest / c.S);
-        if (s >= cnt || c.sgroup[s] < 0 || skip_state(c, s, early_exit, indep)) continue;
+// Per-thread test / flop counters kept in registers for the duration of a
+// chunk and folded into the context once (the context lives in local memory).
+struct StatAcc {
+    Ctx& c;
+    unsigned long long t = 0, f = 0;
+    __device__ explicit StatAcc(Ctx& cc) : c(cc) {}
+    __device__ ~StatAcc() {
+        c.tests += t;
+        c.flops += f;
+    }
+};
+
+__device__ void brute_chunk(Ctx& c, StatAcc& acc, int cnt, bool early_exit, bool indep) {
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nw = c.nthreads >> 5;
+    for (int j = warp; j < c.S; j += nw) {
         const int l = c.flink[j];
         const float4 f = c.fine[j];
-        const float3 x = pose_point(c, l, s, f.x, f.y, f.z);
-        ++c.tests;
-        c.flops += 18 + test_flops(c, p);
-        if (fine_vs_prim(c, x, f.w, c.fine_r64[j], p)) mark_bad(c, s, early_exit);
-    }
-    // self pairs: items (state, pair, i) loop j
-    const long long pit = (long long)NS * c.NP * c.MF;
-    for (long long it = tid; it < pit; it += c.nthreads) {
-        const int s = (int)(it % NS);
-        const long long rest = it / NS;
-        const int i = (int)(rest % c.MF), pr = (int)(rest / c.MF);
-        if (s >= cnt || c.sgroup[s] < 0 || skip_state(c, s, early_exit, indep)) continue;
-        const int2 ab = c.pairs[pr];
-        if (i >= c.nfine[ab.x]) continue;
-        const int ja = c.info[ab.x].w + i;
-        const float4 fa = c.fine[ja];
-        const float3 xa = pose_point(c, ab.x, s, fa.x, fa.y, fa.z);
-        const int nb = c.nfine[ab.y], jb0 = c.info[ab.y].w;
-        c.tests += nb;
-        for (int k = 0; k < nb; ++k) {
-            const float4 fb = c.fine[jb0 + k];
-            const float3 xb = pose_point(c, ab.y, s, fb.x, fb.y, fb.z);
-            c.flops += 28;
-            if (fine_pair(c, xa, ja, xb, jb0 + k)) {
-                mark_bad(c, s, early_exit);
-                break;
+        const double rd = c.fine_r64[j];
+        for (int s = lane; s < cnt; s += 32) {
+            if (c.sgroup[s] < 0 || skip_state(c, s, early_exit, indep)) continue;
+            const float3 x = pose_point(c, l, s, f.x, f.y, f.z);
+            for (int p = 0; p < c.P; ++p) {
+                ++acc.t;
+                acc.f += test_flops(c, p);
+                if (fine_vs_prim(c, x, f.w, rd, p)) {
+                    mark_bad(c, s);
+                    if (early_exit) break;
+                }
             }
+            acc.f += 18;
+        }
+    }
+    for (int pr = warp; pr < c.NP; pr += nw) {
+        const int2 ab = c.pairs[pr];
+        const int na = c.nfine[ab.x], nb = c.nfine[ab.y];
+        const int ja0 = c.info[ab.x].w, jb0 = c.info[ab.y].w;
+        for (int s = lane; s < cnt; s += 32) {
+            if (c.sgroup[s] < 0 || skip_state(c, s, early_exit, indep)) continue;
+            bool hit = false;
+            for (int i = 0; i < na && !(hit && early_exit); ++i) {
+                const float4 fa = c.fine[ja0 + i];
+                const float3 xa = pose_point(c, ab.x, s, fa.x, fa.y, fa.z);
+                for (int k = 0; k < nb; ++k) {
+                    const float4 fb = c.fine[jb0 + k];
+                    const float3 xb = pose_point(c, ab.y, s, fb.x, fb.y, fb.z);
+                    ++acc.t;
+                    acc.f += 28;
+                    if (fine_pair(c, xa, ja0 + i, xb, jb0 + k)) {
+                        hit = true;
+                        if (early_exit) break;
+                    }
+                }
+            }
+            if (hit) mark_bad(c, s);
         }
     }
 }
@@ -488,7 +526,9 @@ __device__ void brute_chunk(Ctx& c, int cnt, bool early_exit, bool indep) {
 // queues; the fine stage re-tests only those. Result: sbad[], IC_FIRSTBAD.
 // ---------------------------------------------------------------------------
 __device__ __noinline__ void check_chunk(Ctx& c, int cnt, bool two_stage, bool early_exit, bool indep) {
-    const int tid = threadIdx.x, NS = c.NS;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nw = c.nthreads >> 5;
+    const int NS = c.NS;
+    StatAcc acc(c);
     for (int s = tid; s < NS; s += c.nthreads) c.sbad[s] = 0;
     if (tid == 0) {
         c.ictl[IC_QN] = 0;
@@ -498,63 +538,69 @@ __device__ __noinline__ void check_chunk(Ctx& c, int cnt, bool two_stage, bool e
     }
     fk_chunk(c, cnt);  // ends with __syncthreads
     if (!two_stage) {
-        brute_chunk(c, cnt, early_exit, indep);
+        brute_chunk(c, acc, cnt, early_exit, indep);
         __syncthreads();
         return;
     }
-    // stage 1: coarse spheres vs primitives; s fastest -> warp-uniform (l, p)
-    const int LP = c.L * c.P;
-    for (int it = tid; it < NS * LP; it += c.nthreads) {
-        const int s = it % NS, rest = it / NS;
-        const int l = rest % c.L, p = rest / c.L;
-        bool hit = false;
-        if (s < cnt && c.sgroup[s] >= 0) {
+    // stage 1: units (link, primitive group) over warps, states over lanes
+    const int G = (c.P >= 8 && c.L < 2 * nw) ? 2 : 1;
+    const int PG = (c.P + G - 1) / G;
+    for (int u = warp; u < c.L * G; u += nw) {
+        const int l = G == 2 ? (u >> 1) : u;
+        const int p0 = (u - l * G) * PG, p1 = min(c.P, p0 + PG);
+        const float rc = c.geo[l * GEO_STRIDE + 36] + c.cpad;
+        const int fl = range_flops(c, p0, p1);
+        for (int s = lane; s < cnt; s += 32) {
+            if (c.sgroup[s] < 0) continue;
             const float* C = c.ccen + (size_t)l * 3 * NS + s;
-            const float rc = c.geo[l * GEO_STRIDE + 36] + c.cpad;
-            hit = coarse_vs_prim(c, C[0], C[NS], C[2 * NS], rc, p);
-            ++c.tests;
-            c.flops += test_flops(c, p);
+            unsigned long long m = coarse_mask(c, C[0], C[NS], C[2 * NS], rc, p0, p1);
+            acc.t += p1 - p0;
+            acc.f += fl;
+            while (m) {
+                const int p = __ffsll((long long)m) - 1;
+                m &= m - 1;
+                push(c.queue, &c.ictl[IC_QN], &c.ictl[IC_OVF], s | (l << 8) | (p << 16));
+            }
         }
-        queue_push(c.queue, &c.ictl[IC_QN], &c.ictl[IC_OVF], hit, s | (l << 8) | (p << 16));
     }
-    for (int it = tid; it < NS * c.NP; it += c.nthreads) {
-        const int s = it % NS, pr = it / NS;
-        bool hit = false;
-        if (s < cnt && c.sgroup[s] >= 0) {
-            const int2 ab = c.pairs[pr];
+    for (int pr = warp; pr < c.NP; pr += nw) {
+        const int2 ab = c.pairs[pr];
+        const float rr = c.geo[ab.x * GEO_STRIDE + 36] + c.geo[ab.y * GEO_STRIDE + 36] + 2.0f * c.cpad;
+        for (int s = lane; s < cnt; s += 32) {
+            if (c.sgroup[s] < 0) continue;
             const float* A = c.ccen + (size_t)ab.x * 3 * NS + s;
             const float* B = c.ccen + (size_t)ab.y * 3 * NS + s;
             const float dx = A[0] - B[0], dy = A[NS] - B[NS], dz = A[2 * NS] - B[2 * NS];
-            const float rr = c.geo[ab.x * GEO_STRIDE + 36] + c.geo[ab.y * GEO_STRIDE + 36] + 2.0f * c.cpad;
-            hit = fmaf(dx, dx, fmaf(dy, dy, dz * dz)) < rr * rr;
-            ++c.tests;
-            c.flops += 10;
+            ++acc.t;
+            acc.f += 10;
+            if (fmaf(dx, dx, fmaf(dy, dy, dz * dz)) < rr * rr)
+                push(c.pqueue, &c.ictl[IC_PQN], &c.ictl[IC_OVF], s | (pr << 8));
         }
-        queue_push(c.pqueue, &c.ictl[IC_PQN], &c.ictl[IC_OVF], hit, s | (pr << 8));
     }
     __syncthreads();
     if (c.ictl[IC_OVF]) {  // too many flags: exact brute force for the chunk
-        brute_chunk(c, cnt, early_exit, indep);
+        brute_chunk(c, acc, cnt, early_exit, indep);
         __syncthreads();
         return;
     }
     const int qn = c.ictl[IC_QN], pqn = c.ictl[IC_PQN];
     if (qn == 0 && pqn == 0) return;  // nothing flagged: every state free
     // stage 2a: flagged (state, link, prim) x fine spheres of the link
-    for (int it = tid; it < qn * c.MF; it += c.nthreads) {
-        const int e = c.queue[it / c.MF], k = it % c.MF;
+    const int mfm = (1 << c.mflog) - 1;
+    for (int it = tid; it < (qn << c.mflog); it += c.nthreads) {
+        const int e = c.queue[it >> c.mflog], k = it & mfm;
         const int s = e & 0xff, l = (e >> 8) & 0xff, p = e >> 16;
         if (k >= c.nfine[l] || skip_state(c, s, early_exit, indep)) continue;
         const int j = c.info[l].w + k;
         const float4 f = c.fine[j];
         const float3 x = pose_point(c, l, s, f.x, f.y, f.z);
-        ++c.tests;
-        c.flops += 18 + test_flops(c, p);
-        if (fine_vs_prim(c, x, f.w, c.fine_r64[j], p)) mark_bad(c, s, early_exit);
+        ++acc.t;
+        acc.f += 18 + test_flops(c, p);
+        if (fine_vs_prim(c, x, f.w, c.fine_r64[j], p)) mark_bad(c, s);
     }
     // stage 2b: flagged (state, pair): fine x fine
-    for (int it = tid; it < pqn * c.MF; it += c.nthreads) {
-        const int e = c.pqueue[it / c.MF], i = it % c.MF;
+    for (int it = tid; it < (pqn << c.mflog); it += c.nthreads) {
+        const int e = c.pqueue[it >> c.mflog], i = it & mfm;
         const int s = e & 0xff, pr = e >> 8;
         const int2 ab = c.pairs[pr];
         if (i >= c.nfine[ab.x] || skip_state(c, s, early_exit, indep)) continue;
@@ -562,13 +608,13 @@ __device__ __noinline__ void check_chunk(Ctx& c, int cnt, bool two_stage, bool e
         const float4 fa = c.fine[ja];
         const float3 xa = pose_point(c, ab.x, s, fa.x, fa.y, fa.z);
         const int nb = c.nfine[ab.y], jb0 = c.info[ab.y].w;
-        c.tests += nb;
         for (int k = 0; k < nb; ++k) {
             const float4 fb = c.fine[jb0 + k];
             const float3 xb = pose_point(c, ab.y, s, fb.x, fb.y, fb.z);
-            c.flops += 28;
+            ++acc.t;
+            acc.f += 28;
             if (fine_pair(c, xa, ja, xb, jb0 + k)) {
-                mark_bad(c, s, early_exit);
+                mark_bad(c, s);
                 break;
             }
         }
@@ -579,9 +625,11 @@ __device__ __noinline__ void check_chunk(Ctx& c, int cnt, bool two_stage, bool e
 // ---------------------------------------------------------------------------
 // chain states. Points p_0 = A, p_k = lerp(A, B, k/n) (k < n), p_n = B
 // (planner.cpp:35-44 step_target; extend is the n = 1 case). State g covers
-// sample i = g % n_cc + 1 of sub-edge k = g / n_cc + 1 (collision.cpp:13-21:
+// sample i = g % n_cc + 1 of sub-edge k = g / n_cc (collision.cpp:13-21:
 // the far endpoint is copied exactly); a bitwise-equal sub-edge collapses to
-// one check of its far end (collision.cpp:215).
+// one check of its far end (collision.cpp:215). The chunk's chain points are
+// computed once into `ends` (each is a full lerp with one FP64 division)
+// and reused by the states and by the appends.
 // ---------------------------------------------------------------------------
 __device__ __forceinline__ double chain_point(const double* A, const double* B, int d, long long k,
                                               long long n) {
@@ -592,29 +640,44 @@ __device__ __forceinline__ double chain_point(const double* A, const double* B, 
 
 __device__ void gen_chain_states(Ctx& c, const double* A, const double* B, long long n_sub,
                                  int n_cc, long long g0, int cnt) {
-    for (int s = threadIdx.x; s < c.NS; s += c.nthreads) {
+    const int tid = threadIdx.x, dof = c.dof;
+    const long long k_lo = g0 / n_cc;
+    const int npts = (int)((g0 + cnt - 1) / n_cc - k_lo) + 2;
+    for (int idx = tid; idx < npts * dof; idx += c.nthreads) {
+        const int j = idx / dof, d = idx - j * dof;
+        c.ends[idx] = chain_point(A, B, d, k_lo + j, n_sub);
+    }
+    if (tid == 0) c.ictl[IC_KLO] = (int)k_lo;
+    __syncthreads();
+    for (int j = tid; j < npts - 1; j += c.nthreads) {
+        bool eq = true;
+        for (int d = 0; d < dof; ++d) eq &= c.ends[j * dof + d] == c.ends[(j + 1) * dof + d];
+        c.ends_eq[j] = eq;
+    }
+    __syncthreads();
+    const double inv_n = (double)n_cc;
+    for (int s = tid; s < c.NS; s += c.nthreads) {
         if (s >= cnt) {
             c.sgroup[s] = -1;
             continue;
         }
         const long long g = g0 + s;
-        const long long k = g / n_cc + 1;
-        const int i = (int)(g % n_cc) + 1;
-        bool eq = true;
-        for (int d = 0; d < c.dof; ++d) {
-            eq &= chain_point(A, B, d, k - 1, n_sub) == chain_point(A, B, d, k, n_sub);
-        }
-        if (eq && i != n_cc) {
+        const long long k = g / n_cc;
+        const int i = (int)(g - k * n_cc) + 1;
+        const int j = (int)(k - k_lo);
+        if (c.ends_eq[j] && i != n_cc) {
             c.sgroup[s] = -1;
             continue;
         }
-        const double t = __ddiv_rn((double)i, (double)n_cc);
-        for (int d = 0; d < c.dof; ++d) {
-            const double to = chain_point(A, B, d, k, n_sub);
-            const double v = (i == n_cc) ? to : lerp_exact(chain_point(A, B, d, k - 1, n_sub), to, t);
-            c.qf[d * c.NS + s] = (float)v;
+        const double* F = c.ends + j * dof;
+        const double* T = F + dof;
+        if (i == n_cc) {
+            for (int d = 0; d < dof; ++d) c.qf[d * c.NS + s] = (float)T[d];
+        } else {
+            const double t = __ddiv_rn((double)i, inv_n);
+            for (int d = 0; d < dof; ++d) c.qf[d * c.NS + s] = (float)lerp_exact(F[d], T[d], t);
         }
-        c.sgroup[s] = (int)(k - 1);
+        c.sgroup[s] = (int)k;
     }
     __syncthreads();
 }

@@ -26,7 +26,7 @@ using namespace dev;
 // ---------------------------------------------------------------------------
 struct SmemLayout {
     size_t robot, scene, pose, ccen, qf, sgroup, sbad, queue, pqueue, ictl, dcfg, red_d, red_i,
-        total;
+        ends, ends_eq, total;
 };
 
 __host__ __device__ inline size_t al16(size_t x) { return (x + 15) & ~size_t(15); }
@@ -48,8 +48,9 @@ __host__ __device__ inline SmemLayout smem_layout(int robot_words, int L, int do
     s.dcfg = o;  o = al16(o + 8 * (size_t)8 * kMaxDof);
     s.red_d = o; o = al16(o + 8 * (size_t)(nthreads / 32));
     s.red_i = o; o = al16(o + 4 * (size_t)(nthreads / 32));
+    s.ends = o;  o = al16(o + 8 * (size_t)(NS + 2) * dof);
+    s.ends_eq = o; o = al16(o + 4 * (size_t)(NS + 2));
     s.total = o;
-    (void)dof;
     return s;
 }
 
@@ -95,6 +96,10 @@ __device__ void setup_ctx(Ctx& c, unsigned char* smem, const uint32_t* robot_g, 
     c.dcfg = reinterpret_cast<double*>(smem + lay.dcfg);
     c.red_d = reinterpret_cast<double*>(smem + lay.red_d);
     c.red_i = reinterpret_cast<int*>(smem + lay.red_i);
+    c.ends = reinterpret_cast<double*>(smem + lay.ends);
+    c.ends_eq = reinterpret_cast<int*>(smem + lay.ends_eq);
+    c.nslog = 31 - __clz(NS);
+    c.mflog = c.MF > 1 ? 32 - __clz(c.MF - 1) : 0;
     c.tests = 0;
     c.ns = c.nb = c.nc = c.P = 0;  // scene pointers are wired by load_scene
 }
@@ -150,32 +155,32 @@ __device__ __forceinline__ TreeRef tree_ref(const PlanArgs& a, int prob, int t, 
     return r;
 }
 
-// Append: reserve a slot (fetch_add), write config/parent, mark the slot
-// ready (release), then advance `published` over the ready prefix. Lock-free:
-// unlike tree.hpp:36-43 no writer waits for its predecessor, which would
-// deadlock CTAs that are not co-resident. Returns the slot or -1 (full).
-__device__ int tree_append(Ctx& c, const PlanArgs& a, const TreeRef& T, const double* cfg,
-                           int parent) {
-    const int tid = threadIdx.x;
-    if (tid == 0) {
-        const int slot = atomicAdd(T.reserved, 1);
-        c.ictl[IC_TMP2] = slot < a.cap ? slot : -1;
-    }
+// Append `count` chained nodes (pts[j], parent of node 0 = parent0, of node
+// j = node j-1): reserve a contiguous block (one fetch_add, tree.hpp:29),
+// write configs/parents in parallel, mark the slots ready (release) and
+// advance `published` over the ready prefix. Lock-free: unlike
+// tree.hpp:36-43 no writer waits for a predecessor (that would deadlock CTAs
+// that are not co-resident). Returns the number appended (< count when the
+// tree filled up, tree.hpp:30) and the last appended slot in *last.
+__device__ int tree_append_many(Ctx& c, const PlanArgs& a, const TreeRef& T, const double* pts,
+                                int count, int parent0, int* last) {
+    const int tid = threadIdx.x, dof = c.dof;
+    if (tid == 0) c.ictl[IC_TMP2] = atomicAdd(T.reserved, count);
     __syncthreads();
-    const int slot = c.ictl[IC_TMP2];
-    if (slot < 0) return -1;
-    if (tid < c.dof) {
-        T.cfg[(size_t)tid * a.stride + slot] = cfg[tid];
-        __threadfence();
+    const long long s0 = c.ictl[IC_TMP2];
+    const int ok = (int)max(0ll, min((long long)count, a.cap - s0));
+    for (int idx = tid; idx < ok * dof; idx += c.nthreads) {
+        const int j = idx / dof, d = idx - j * dof;
+        T.cfg[(size_t)d * a.stride + s0 + j] = pts[idx];
     }
-    if (tid == 0) {
-        T.parent[slot] = parent;
-        T.dd[slot] = 0;
-        __threadfence();
+    for (int j = tid; j < ok; j += c.nthreads) {
+        T.parent[s0 + j] = j == 0 ? parent0 : (int)(s0 + j - 1);
+        T.dd[s0 + j] = 0;
     }
+    __threadfence();
     __syncthreads();
-    if (tid == 0) {
-        st_release_u(&T.ready[slot], a.epoch);
+    if (tid == 0 && ok > 0) {
+        for (int j = 0; j < ok; ++j) st_release_u(&T.ready[s0 + j], a.epoch);
         __threadfence();
         int p = ld_acquire(T.published);
         while (p < a.cap) {
@@ -184,21 +189,23 @@ __device__ int tree_append(Ctx& c, const PlanArgs& a, const TreeRef& T, const do
             p = (old == p) ? p + 1 : old;
         }
     }
-    return slot;
+    *last = ok > 0 ? (int)(s0 + ok - 1) : parent0;
+    return ok;
 }
 
 // ---------------------------------------------------------------------------
 // chain validation with appends (extend: n_sub = 1; greedy connect:
-// planner.cpp:66-123, sub-edges validated chunk by chunk, every fully
-// validated sub-edge appended in order before the first invalid one).
+// planner.cpp:66-123). Sub-edges are validated chunk by chunk (NS states of
+// the whole chain at a time); after each chunk every fully validated
+// sub-edge before the first invalid one is appended in order, exactly the
+// nodes the reference's sequential validate/append loop would add.
 // Returns the number of sub-edges appended, or -1 - appended if the tree
-// filled up, and the last appended slot in *last.
+// filled up; the last appended slot in *last.
 // ---------------------------------------------------------------------------
 __device__ long long validate_chain(Ctx& c, const PlanArgs& a, const double* A, const double* B,
-                                    long long n_sub, bool do_append, const TreeRef* T,
-                                    int parent0, int* last, const int* done_flag,
-                                    unsigned long long& fk_states, unsigned long long& fine_states,
-                                    bool* stopped) {
+                                    long long n_sub, const TreeRef* T, int parent0, int* last,
+                                    const int* done_flag, unsigned long long& fk_states,
+                                    unsigned long long& fine_states, bool* stopped) {
     const int n_cc = a.p.n_cc;
     const long long total = n_sub * (long long)n_cc;
     long long appended = 0;
@@ -208,35 +215,37 @@ __device__ long long validate_chain(Ctx& c, const PlanArgs& a, const double* A, 
         if (done_flag) {
             if (threadIdx.x == 0) c.ictl[IC_TMP3] = ld_acquire(done_flag);
             __syncthreads();
-            if (c.ictl[IC_TMP3] != 0) {
+            const int dn = c.ictl[IC_TMP3];
+            __syncthreads();
+            if (dn != 0) {
                 *stopped = true;
+                *last = prev;
                 return appended;
             }
         }
         const int cnt = (int)min((long long)c.NS, total - g0);
         gen_chain_states(c, A, B, n_sub, n_cc, g0, cnt);
         if (threadIdx.x == 0) {
-            for (int s = 0; s < cnt; ++s) fk_states += (c.sgroup[s] >= 0);
+            int act = 0;
+            for (int s = 0; s < cnt; ++s) act += (c.sgroup[s] >= 0);
+            fk_states += act;
+            c.flops += (unsigned long long)act * c.fkflops;
         }
         check_chunk(c, cnt, a.p.two_stage != 0, a.p.early_exit != 0, false);
         if (threadIdx.x == 0 && (c.ictl[IC_QN] | c.ictl[IC_PQN])) ++fine_states;
         const int fb = c.ictl[IC_FIRSTBAD];
         const long long good = (fb != kNoBad) ? (long long)fb : (g0 + cnt) / n_cc;
-        if (do_append) {
-            for (long long k = appended; k < good; ++k) {
-                double* P = dc(c, DC_TMP);
-                if (threadIdx.x < c.dof) P[threadIdx.x] = chain_point(A, B, threadIdx.x, k + 1, n_sub);
+        if (good > appended) {
+            const long long k_lo = c.ictl[IC_KLO];
+            const int cntk = (int)(good - appended);
+            const int got = tree_append_many(c, a, *T, c.ends + (appended + 1 - k_lo) * c.dof, cntk,
+                                             prev, &prev);
+            appended += got;
+            if (got < cntk) {
+                *last = prev;
                 __syncthreads();
-                const int slot = tree_append(c, a, *T, P, prev);
-                if (slot < 0) {
-                    *last = prev;
-                    return -1 - appended;
-                }
-                prev = slot;
-                ++appended;
+                return -1 - appended;
             }
-        } else {
-            appended = good;
         }
         __syncthreads();
         if (fb != kNoBad) break;
@@ -606,9 +615,8 @@ __global__ void __launch_bounds__(128, 4) plan_kernel(PlanArgs a) {
             // ---- SIMT edge validation nn -> c_new, then append ----
             int last = nn;
             bool stopped = false;
-            const long long ok =
-                validate_chain(c, a, nnc, cnew, 1, true, &Ts, nn, &last, nullptr, fk_states,
-                               fine_states, &stopped);
+            const long long ok = validate_chain(c, a, nnc, cnew, 1, &Ts, nn, &last, nullptr,
+                                                fk_states, fine_states, &stopped);
             if (ok == 0) {
                 if (a.p.dynamic_domain && tid == 0) Ts.dd[nn] = 1;  // record_failure
                 continue;
@@ -640,7 +648,7 @@ __global__ void __launch_bounds__(128, 4) plan_kernel(PlanArgs a) {
                     A[tid] = cnew[tid];
                 }
                 __syncthreads();
-                const long long got = validate_chain(c, a, A, tgt, n_ext, true, &Ts, new_idx, &last,
+                const long long got = validate_chain(c, a, A, tgt, n_ext, &Ts, new_idx, &last,
                                                      &C.done, fk_states, fine_states, &stopped);
                 if (got < 0) {
                     leave_msg = MSG_CAPACITY;
@@ -851,6 +859,47 @@ __global__ void debug_sample_kernel(RobotArgs r, uint64_t index0, int n, double*
     if (i >= n * dof) return;
     const int k = i / dof, d = i % dof;
     out[i] = sample_dim(halton_exact(bases[d], index0 + k), r.limits[2 * d], r.limits[2 * d + 1]);
+}
+
+// FP32 FFMA-chain microbenchmark: the roofline denominator for the FK /
+// collision work (MEASURED_PEAKS.json carries no FP32 figure). 8 independent
+// dependency chains per thread, 256 threads x 8 CTAs per SM.
+__global__ void __launch_bounds__(256) ffma_peak_kernel(float* out, int iters) {
+    float a[8];
+#pragma unroll
+    for (int k = 0; k < 8; ++k) a[k] = threadIdx.x * 1e-7f + k;
+    for (int i = 0; i < iters; ++i) {
+#pragma unroll
+        for (int u = 0; u < 16; ++u) {
+#pragma unroll
+            for (int k = 0; k < 8; ++k) a[k] = fmaf(a[k], 0.9999999f, 1e-7f);
+        }
+    }
+    float s = 0.f;
+#pragma unroll
+    for (int k = 0; k < 8; ++k) s += a[k];
+    if (s == 1234.5f) out[blockIdx.x] = s;  // keeps the chains alive
+}
+
+double measure_fp32_peak(int sms, cudaStream_t st) {
+    float* out = nullptr;
+    cudaMalloc(&out, 4 * 8 * sms);
+    cudaEvent_t e0, e1;
+    cudaEventCreate(&e0);
+    cudaEventCreate(&e1);
+    const int iters = 2048, grid = 8 * sms;
+    ffma_peak_kernel<<<grid, 256, 0, st>>>(out, iters);  // warm-up
+    cudaEventRecord(e0, st);
+    for (int r = 0; r < 5; ++r) ffma_peak_kernel<<<grid, 256, 0, st>>>(out, iters);
+    cudaEventRecord(e1, st);
+    cudaEventSynchronize(e1);
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, e0, e1);
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    cudaFree(out);
+    const double flops = 5.0 * grid * 256.0 * iters * 16 * 8 * 2;
+    return ms > 0 ? flops / (ms * 1e-3) / 1e12 : 0.0;
 }
 
 static int chunk_states() { return 32; }

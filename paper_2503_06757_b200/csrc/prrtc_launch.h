@@ -43,6 +43,8 @@ cudaError_t launch_debug_nn(const double* soa, long long cap, int count, int dof
                             int nq, uint32_t* idx, double* d2, cudaStream_t st);
 cudaError_t launch_debug_halton(const uint32_t* bases, const uint64_t* idx, int n, double* out,
                                 cudaStream_t st);
+double measure_fp32_peak(int sms, cudaStream_t st);
+
 cudaError_t launch_debug_sample(const RobotArgs& r, uint64_t index0, int n, double* out,
                                 cudaStream_t st);
 
