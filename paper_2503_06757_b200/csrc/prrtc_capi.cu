@@ -13,6 +13,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <atomic>
 #include <mutex>
 #include <string>
 #include <vector>
@@ -39,15 +40,26 @@ int set_err(int code, const std::string& msg) {
             return set_err(PRRTC_ECUDA, std::string(#expr) + ": " + cudaGetErrorString(e_)); \
     } while (0)
 
+// Device capability check, cached per ordinal (cudaGetDeviceProperties costs
+// milliseconds; a plan call must not pay it).
+std::atomic<int> g_dev_state[64];  // 0 unknown, 1 ok, 2 not sm_100
+
 int check_device(int device) {
+    if (device >= 0 && device < 64) {
+        const int st = g_dev_state[device].load(std::memory_order_relaxed);
+        if (st == 1) return PRRTC_OK;
+        if (st == 2)
+            return set_err(PRRTC_ENODEV, "device is not sm_100 (Blackwell); kernels are built for sm_100a only");
+    }
     int n = 0;
     if (cudaGetDeviceCount(&n) != cudaSuccess || n == 0)
         return set_err(PRRTC_ENODEV, "no CUDA device: the B200 planner has no CPU fallback");
-    if (device < 0 || device >= n) return set_err(PRRTC_ENODEV, "device ordinal out of range");
-    cudaDeviceProp p;
-    if (cudaGetDeviceProperties(&p, device) != cudaSuccess)
-        return set_err(PRRTC_ENODEV, "cudaGetDeviceProperties failed");
-    if (p.major != 10)
+    if (device < 0 || device >= n || device >= 64) return set_err(PRRTC_ENODEV, "device ordinal out of range");
+    int major = 0;
+    if (cudaDeviceGetAttribute(&major, cudaDevAttrComputeCapabilityMajor, device) != cudaSuccess)
+        return set_err(PRRTC_ENODEV, "cudaDeviceGetAttribute failed");
+    g_dev_state[device].store(major == 10 ? 1 : 2, std::memory_order_relaxed);
+    if (major != 10)
         return set_err(PRRTC_ENODEV, "device is not sm_100 (Blackwell); kernels are built for sm_100a only");
     return PRRTC_OK;
 }
@@ -111,6 +123,7 @@ struct prrtc_robot {
     double* d_fine_r64 = nullptr;
     double* d_limits = nullptr;
     double reach = 0.0;           // bound on |posed sphere| (m)
+    mutable std::atomic<int> occ[5] = {};  // planner CTAs per SM, by ns_max / 32
     RobotArgs args() const {
         RobotArgs r;
         r.words = d_words;
@@ -157,8 +170,9 @@ int prrtc_device_count(void) {
     if (cudaGetDeviceCount(&n) != cudaSuccess) return 0;
     int ok = 0;
     for (int d = 0; d < n; ++d) {
-        cudaDeviceProp p;
-        if (cudaGetDeviceProperties(&p, d) == cudaSuccess && p.major == 10) ++ok;
+        int major = 0;
+        if (cudaDeviceGetAttribute(&major, cudaDevAttrComputeCapabilityMajor, d) == cudaSuccess && major == 10)
+            ++ok;
     }
     return ok;
 }
@@ -299,7 +313,15 @@ int prrtc_robot_create(const prrtc_robot_desc* d, int device, prrtc_robot** out)
         w.push_back((uint32_t)d->self_pairs[2 * p + 1]);
     }
     w[RH_OFF_BASES] = (uint32_t)w.size();
-    for (unsigned b : first_primes(dof)) w.push_back(b);
+    const std::vector<unsigned> bases = first_primes(dof);
+    for (unsigned b : bases) w.push_back(b);
+    if (w.size() % 2) w.push_back(0);
+    w[RH_OFF_MAGIC] = (uint32_t)w.size();
+    for (unsigned b : bases) {  // ceil(2^64 / b): q = umul64hi(n, M) is exact for n < 2^32
+        const uint64_t m = UINT64_MAX / b + 1;
+        w.push_back((uint32_t)(m & 0xffffffffu));
+        w.push_back((uint32_t)(m >> 32));
+    }
     w[RH_OFF_FLINK] = (uint32_t)w.size();
     for (int l = 0; l < n; ++l)
         for (uint32_t k = d->fine_offset[l]; k < d->fine_offset[l + 1]; ++k) w.push_back((uint32_t)l);
@@ -682,7 +704,11 @@ int batch_setup(prrtc_batch* b, const prrtc_robot* robot, const prrtc_scene* con
     b->stride = (b->cap + 31) / 32 * 32;
     b->nthreads = 128;
     b->ns_max = std::max(32, std::min(128, (params->n_cc + 31) / 32 * 32));
-    const int occ = plan_occupancy(robot->args(), b->ns_max, b->nthreads);
+    int occ = robot->occ[b->ns_max / 32].load(std::memory_order_relaxed);
+    if (occ == 0) {
+        occ = plan_occupancy(robot->args(), b->ns_max, b->nthreads);
+        robot->occ[b->ns_max / 32].store(occ, std::memory_order_relaxed);
+    }
     const int sms = sm_count(robot->device);
     unsigned workers_eff;
     if (params->deterministic) {

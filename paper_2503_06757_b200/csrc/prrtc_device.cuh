@@ -38,6 +38,12 @@ __device__ __forceinline__ unsigned ld_acquire_u(const unsigned* p) {
     asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
     return v;
 }
+__device__ __forceinline__ int ld_relaxed(const int* p) {
+    int v;
+    asm volatile("ld.relaxed.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
+__device__ __forceinline__ void fence_acq_rel() { asm volatile("fence.acq_rel.gpu;" ::: "memory"); }
 __device__ __forceinline__ void st_release(int* p, int v) {
     asm volatile("st.release.gpu.global.b32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
@@ -77,6 +83,27 @@ __device__ __forceinline__ double halton_exact(unsigned base, unsigned long long
             r = __dadd_rn(r, __dmul_rn(f, static_cast<double>(i - q * base)));
             i = q;
         }
+    }
+    return r;
+}
+
+// halton_exact with the reciprocal powers f_k = (((1/b)/b).../b) taken from a
+// table (the same IEEE divisions, computed once per CTA) and the digit
+// division done by multiply-high with M = ceil(2^64 / b) (exact for 32-bit
+// indices): bit-identical to halton_exact, without the per-digit FP64 and
+// integer divides.
+constexpr int kHaltonTab = 40;
+__device__ __forceinline__ double halton_tab(unsigned base, unsigned long long magic, const double* ftab,
+                                             unsigned long long index) {
+    if (index >> 32) return halton_exact(base, index);
+    unsigned i = static_cast<unsigned>(index);
+    double r = 0.0;
+    for (int k = 0; i > 0; ++k) {
+        const unsigned q = (unsigned)__umul64hi((unsigned long long)i, magic);
+        const double f = k < kHaltonTab ? ftab[k] : 0.0;
+        if (k >= kHaltonTab) return halton_exact(base, index);
+        r = __dadd_rn(r, __dmul_rn(f, static_cast<double>(i - q * base)));
+        i = q;
     }
     return r;
 }
@@ -192,6 +219,8 @@ struct Ctx {
     const float4* fine;    // [S]
     const int2* pairs;     // [NP]
     const unsigned* bases; // [dof]
+    const unsigned long long* magic;  // [dof] ceil(2^64 / base)
+    double* htab;          // [dof][kHaltonTab] Halton reciprocal powers
     const int* flink;      // [S] link of each fine sphere
     const double* fine_r64;  // global
     const double* limits;    // global [dof][2]
@@ -699,23 +728,39 @@ __device__ NnOut nn_scan(Ctx& c, const double* cfg, long long cap, int count, co
     double best = __longlong_as_double(0x7ff0000000000000ll);  // +inf
     int bi = 0x7fffffff;
     const int npairs = (count + 1) >> 1;
-    for (int pi = tid; pi < npairs; pi += c.nthreads) {
-        const int n = pi * 2;
-        double a0 = 0.0, a1 = 0.0;
+    // two node pairs (4 nodes) per thread per step: 2 x 128-bit loads per
+    // dimension in flight; candidates visited in increasing index order so
+    // strict < keeps the lowest index (kernels_scalar.cpp:30-34)
+    for (int pi = tid; pi < npairs; pi += 2 * c.nthreads) {
+        const int n0 = pi * 2, pj = pi + c.nthreads, n1 = pj * 2;
+        const bool has1 = pj < npairs;
+        double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
         for (int d = 0; d < c.dof; ++d) {
-            const double2 v = __ldcg(reinterpret_cast<const double2*>(cfg + d * cap + n));
+            const double2 v = __ldcg(reinterpret_cast<const double2*>(cfg + d * cap + n0));
+            const double2 w = has1 ? __ldcg(reinterpret_cast<const double2*>(cfg + d * cap + n1)) : v;
             const double qd = q[d];
             const double e0 = __dsub_rn(v.x, qd), e1 = __dsub_rn(v.y, qd);
+            const double e2 = __dsub_rn(w.x, qd), e3 = __dsub_rn(w.y, qd);
             a0 = __dadd_rn(a0, __dmul_rn(e0, e0));
             a1 = __dadd_rn(a1, __dmul_rn(e1, e1));
+            a2 = __dadd_rn(a2, __dmul_rn(e2, e2));
+            a3 = __dadd_rn(a3, __dmul_rn(e3, e3));
         }
         if (a0 < best) {
             best = a0;
-            bi = n;
+            bi = n0;
         }
-        if (n + 1 < count && a1 < best) {
+        if (n0 + 1 < count && a1 < best) {
             best = a1;
-            bi = n + 1;
+            bi = n0 + 1;
+        }
+        if (has1 && a2 < best) {
+            best = a2;
+            bi = n1;
+        }
+        if (has1 && n1 + 1 < count && a3 < best) {
+            best = a3;
+            bi = n1 + 1;
         }
     }
 #pragma unroll

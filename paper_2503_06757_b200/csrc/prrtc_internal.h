@@ -33,6 +33,7 @@ enum RobotHdr : int {
     RH_OFF_BASES, // uint32[dof] Halton bases
     RH_OFF_FLINK, // int[S] link of each fine sphere
     RH_FKFLOPS,   // algorithmic FP32 flops of FK + coarse posing per state
+    RH_OFF_MAGIC, // uint64[dof] ceil(2^64 / base): exact 32-bit division by the Halton bases
     RH_COUNT = 16
 };
 

@@ -26,7 +26,7 @@ using namespace dev;
 // ---------------------------------------------------------------------------
 struct SmemLayout {
     size_t robot, scene, pose, ccen, qf, sgroup, sbad, queue, pqueue, ictl, dcfg, red_d, red_i,
-        ends, ends_eq, total;
+        ends, ends_eq, htab, total;
 };
 
 __host__ __device__ inline size_t al16(size_t x) { return (x + 15) & ~size_t(15); }
@@ -50,6 +50,7 @@ __host__ __device__ inline SmemLayout smem_layout(int robot_words, int L, int do
     s.red_i = o; o = al16(o + 4 * (size_t)(nthreads / 32));
     s.ends = o;  o = al16(o + 8 * (size_t)(NS + 2) * dof);
     s.ends_eq = o; o = al16(o + 4 * (size_t)(NS + 2));
+    s.htab = o;  o = al16(o + 8 * (size_t)dof * kHaltonTab);
     s.total = o;
     return s;
 }
@@ -80,6 +81,7 @@ __device__ void setup_ctx(Ctx& c, unsigned char* smem, const uint32_t* robot_g, 
     c.fine = reinterpret_cast<const float4*>(rw + rw[RH_OFF_FINE]);
     c.pairs = reinterpret_cast<const int2*>(rw + rw[RH_OFF_PAIRS]);
     c.bases = rw + rw[RH_OFF_BASES];
+    c.magic = reinterpret_cast<const unsigned long long*>(rw + rw[RH_OFF_MAGIC]);
     c.flink = reinterpret_cast<const int*>(rw + rw[RH_OFF_FLINK]);
     c.fine_r64 = fine_r64;
     c.limits = limits;
@@ -98,9 +100,20 @@ __device__ void setup_ctx(Ctx& c, unsigned char* smem, const uint32_t* robot_g, 
     c.red_i = reinterpret_cast<int*>(smem + lay.red_i);
     c.ends = reinterpret_cast<double*>(smem + lay.ends);
     c.ends_eq = reinterpret_cast<int*>(smem + lay.ends_eq);
+    c.htab = reinterpret_cast<double*>(smem + lay.htab);
+    for (int d = tid; d < c.dof; d += c.nthreads) {  // f_k of halton_value (sampling.cpp:12)
+        double f = 1.0;
+        for (int k = 0; k < kHaltonTab; ++k) {
+            f = __ddiv_rn(f, (double)c.bases[d]);
+            c.htab[d * kHaltonTab + k] = f;
+        }
+    }
+    __syncthreads();
     c.nslog = 31 - __clz(NS);
     c.mflog = c.MF > 1 ? 32 - __clz(c.MF - 1) : 0;
     c.tests = 0;
+    c.flops = 0;
+    c.fkflops = rw[RH_FKFLOPS];
     c.ns = c.nb = c.nc = c.P = 0;  // scene pointers are wired by load_scene
 }
 
@@ -349,6 +362,7 @@ __device__ bool init_problem(Ctx& c, const PlanArgs& a, int prob, unsigned long 
     check_chunk(c, 2, a.p.two_stage != 0, a.p.early_exit != 0, true);
     if (tid == 0) {
         fk_states += 2;
+        c.flops += 2ull * c.fkflops;
         // within_limits (planner.cpp:25-31): inclusive bounds
         bool sl = true, gl = true;
         for (int d = 0; d < dof; ++d) {
@@ -482,13 +496,18 @@ __device__ int pick_help(Ctx& c, const PlanArgs& a) {
 // CheckStats counters (collision.hpp:17-25), reduced per warp then per CTA.
 __device__ void flush_stats(Ctx& c, ProbCtl& C, unsigned long long& fk_states,
                             unsigned long long& fine_states) {
-    for (int o = 16; o > 0; o >>= 1) c.tests += __shfl_xor_sync(0xffffffffu, c.tests, o);
+    for (int o = 16; o > 0; o >>= 1) {
+        c.tests += __shfl_xor_sync(0xffffffffu, c.tests, o);
+        c.flops += __shfl_xor_sync(0xffffffffu, c.flops, o);
+    }
     if ((threadIdx.x & 31) == 0 && c.tests) atomicAdd(&C.sphere_tests, c.tests);
+    if ((threadIdx.x & 31) == 0 && c.flops) atomicAdd(&C.flops, c.flops);
     if (threadIdx.x == 0) {
         if (fk_states) atomicAdd(&C.fk_calls, fk_states);
         if (fine_states) atomicAdd(&C.fine_entries, fine_states);
     }
     c.tests = 0;
+    c.flops = 0;
     fk_states = 0;
     fine_states = 0;
 }
@@ -551,20 +570,20 @@ __global__ void __launch_bounds__(128, 4) plan_kernel(PlanArgs a) {
         for (;;) {
             // ---- iteration header (lead thread) ----
             if (tid == 0) {
-                int leave = 0;
-                if (ld_acquire(&C.done) != DONE_RUNNING) leave = 1;
-                else if (atomicAdd(&C.iters, 1ull) >= a.p.budget) leave = 2;
-                int from_start = 1, snap = 0;
-                unsigned long long hidx = 0;
-                if (!leave) {
-                    const int la = ld_acquire(&C.published[0]);
-                    const int lb = ld_acquire(&C.published[1]);
-                    // extend_start_tree (planner.hpp:62-65)
-                    from_start = a.p.balance ? (la <= lb) : ((local_iter & 1) == 0);
-                    hidx = a.p.deterministic ? (1ull + a.p.seed + local_iter)
-                                             : (1ull + a.p.seed + atomicAdd(&C.halton_ticket, 1ull));
-                    snap = from_start ? la : lb;
-                }
+                // one global ticket per iteration is both the budget counter
+                // and the Halton index (no stride-W bias);
+                // the four accesses are issued back to back, then one fence
+                // gives the published snapshot acquire semantics
+                const int dn = ld_relaxed(&C.done);
+                const unsigned long long it = atomicAdd(&C.iters, 1ull);
+                const int la = ld_relaxed(&C.published[0]);
+                const int lb = ld_relaxed(&C.published[1]);
+                fence_acq_rel();
+                const int leave = dn != DONE_RUNNING ? 1 : (it >= a.p.budget ? 2 : 0);
+                // extend_start_tree (planner.hpp:62-65)
+                const int from_start = a.p.balance ? (la <= lb) : ((local_iter & 1) == 0);
+                const unsigned long long hidx = 1ull + a.p.seed + (a.p.deterministic ? local_iter : it);
+                const int snap = from_start ? la : lb;
                 ++local_iter;
                 c.ictl[IC_TMP0] = leave;
                 c.ictl[IC_TMP1] = from_start;
@@ -586,8 +605,8 @@ __global__ void __launch_bounds__(128, 4) plan_kernel(PlanArgs a) {
             // ---- sample (sampling.cpp:39-51), one thread per dimension ----
             double* smp = dc(c, DC_SAMPLE);
             if (tid < dof) {
-                smp[tid] = sample_dim(halton_exact(c.bases[tid], hidx), c.limits[2 * tid],
-                                      c.limits[2 * tid + 1]);
+                smp[tid] = sample_dim(halton_tab(c.bases[tid], c.magic[tid], c.htab + tid * kHaltonTab, hidx),
+                                      c.limits[2 * tid], c.limits[2 * tid + 1]);
             }
             __syncthreads();
             // ---- nearest neighbour in the extended tree ----
@@ -846,9 +865,20 @@ __global__ void debug_nn_kernel(const double* soa, long long cap, int count, int
     }
 }
 
+// planner's Halton path: reciprocal-power table + multiply-high digits
+__device__ double halton_planner(unsigned base, unsigned long long index) {
+    double ftab[kHaltonTab];
+    double f = 1.0;
+    for (int k = 0; k < kHaltonTab; ++k) {
+        f = __ddiv_rn(f, (double)base);
+        ftab[k] = f;
+    }
+    return halton_tab(base, ~0ull / base + 1, ftab, index);
+}
+
 __global__ void debug_halton_kernel(const uint32_t* bases, const uint64_t* idx, int n, double* out) {
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
-    if (i < n) out[i] = halton_exact(bases[i], idx[i]);
+    if (i < n) out[i] = halton_planner(bases[i], idx[i]);
 }
 
 __global__ void debug_sample_kernel(RobotArgs r, uint64_t index0, int n, double* out) {
@@ -858,7 +888,7 @@ __global__ void debug_sample_kernel(RobotArgs r, uint64_t index0, int n, double*
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= n * dof) return;
     const int k = i / dof, d = i % dof;
-    out[i] = sample_dim(halton_exact(bases[d], index0 + k), r.limits[2 * d], r.limits[2 * d + 1]);
+    out[i] = sample_dim(halton_planner(bases[d], index0 + k), r.limits[2 * d], r.limits[2 * d + 1]);
 }
 
 // FP32 FFMA-chain microbenchmark: the roofline denominator for the FK /
