@@ -170,11 +170,14 @@ __device__ __forceinline__ TreeRef tree_ref(const PlanArgs& a, int prob, int t, 
 
 // Append `count` chained nodes (pts[j], parent of node 0 = parent0, of node
 // j = node j-1): reserve a contiguous block (one fetch_add, tree.hpp:29),
-// write configs/parents in parallel, mark the slots ready (release) and
-// advance `published` over the ready prefix. Lock-free: unlike
+// write configs/parents in parallel, set the slots' ready flags, then publish
+// the block with one CAS published: s0 -> s0 + ok. Lock-free: unlike
 // tree.hpp:36-43 no writer waits for a predecessor (that would deadlock CTAs
-// that are not co-resident). Returns the number appended (< count when the
-// tree filled up, tree.hpp:30) and the last appended slot in *last.
+// that are not co-resident). If a predecessor block is still being written
+// the CAS fails and that predecessor's writer, after publishing its own
+// block, carries `published` forward over every ready slot. Returns the
+// number appended (< count when the tree filled up, tree.hpp:30) and the
+// last appended slot in *last.
 __device__ int tree_append_many(Ctx& c, const PlanArgs& a, const TreeRef& T, const double* pts,
                                 int count, int parent0, int* last) {
     const int tid = threadIdx.x, dof = c.dof;
@@ -189,17 +192,21 @@ __device__ int tree_append_many(Ctx& c, const PlanArgs& a, const TreeRef& T, con
     for (int j = tid; j < ok; j += c.nthreads) {
         T.parent[s0 + j] = j == 0 ? parent0 : (int)(s0 + j - 1);
         T.dd[s0 + j] = 0;
+        T.ready[s0 + j] = a.epoch;
     }
-    __threadfence();
+    __threadfence();  // data and flags before the publishing CAS
     __syncthreads();
     if (tid == 0 && ok > 0) {
-        for (int j = 0; j < ok; ++j) st_release_u(&T.ready[s0 + j], a.epoch);
-        __threadfence();
-        int p = ld_acquire(T.published);
-        while (p < a.cap) {
-            if (ld_acquire_u(&T.ready[p]) != a.epoch) break;
-            const int old = atomicCAS(T.published, p, p + 1);
-            p = (old == p) ? p + 1 : old;
+        int p = atomicCAS(T.published, (int)s0, (int)(s0 + ok));
+        if (p == s0) {
+            // our block is published; carry on over successors that finished first
+            p = (int)(s0 + ok);
+            __threadfence();
+            while (p < a.cap && ld_acquire_u(&T.ready[p]) == a.epoch) {
+                const int old = atomicCAS(T.published, p, p + 1);
+                if (old != p) break;  // another writer is advancing
+                ++p;
+            }
         }
     }
     *last = ok > 0 ? (int)(s0 + ok - 1) : parent0;
@@ -209,11 +216,12 @@ __device__ int tree_append_many(Ctx& c, const PlanArgs& a, const TreeRef& T, con
 // ---------------------------------------------------------------------------
 // chain validation with appends (extend: n_sub = 1; greedy connect:
 // planner.cpp:66-123). Sub-edges are validated chunk by chunk (NS states of
-// the whole chain at a time); after each chunk every fully validated
-// sub-edge before the first invalid one is appended in order, exactly the
-// nodes the reference's sequential validate/append loop would add.
-// Returns the number of sub-edges appended, or -1 - appended if the tree
-// filled up; the last appended slot in *last.
+// the whole chain at a time) up to the first invalid one; then the leading
+// valid sub-edges' far points are appended as one chained block — exactly
+// the nodes and parents the reference's sequential validate/append loop
+// adds, published in one step instead of one by one. Returns the number of
+// sub-edges appended, or -1 - appended if the tree filled up; the last
+// appended slot in *last.
 // ---------------------------------------------------------------------------
 __device__ long long validate_chain(Ctx& c, const PlanArgs& a, const double* A, const double* B,
                                     long long n_sub, const TreeRef* T, int parent0, int* last,
@@ -221,19 +229,18 @@ __device__ long long validate_chain(Ctx& c, const PlanArgs& a, const double* A, 
                                     unsigned long long& fine_states, bool* stopped) {
     const int n_cc = a.p.n_cc;
     const long long total = n_sub * (long long)n_cc;
-    long long appended = 0;
-    int prev = parent0;
+    long long good = 0;
     *stopped = false;
+    *last = parent0;
     for (long long g0 = 0; g0 < total; g0 += c.NS) {
-        if (done_flag) {
-            if (threadIdx.x == 0) c.ictl[IC_TMP3] = ld_acquire(done_flag);
+        if (done_flag) {  // stop flag (planner.cpp:112)
+            if (threadIdx.x == 0) c.ictl[IC_TMP3] = ld_relaxed(done_flag);
             __syncthreads();
             const int dn = c.ictl[IC_TMP3];
             __syncthreads();
             if (dn != 0) {
                 *stopped = true;
-                *last = prev;
-                return appended;
+                return 0;
             }
         }
         const int cnt = (int)min((long long)c.NS, total - g0);
@@ -247,21 +254,26 @@ __device__ long long validate_chain(Ctx& c, const PlanArgs& a, const double* A, 
         check_chunk(c, cnt, a.p.two_stage != 0, a.p.early_exit != 0, false);
         if (threadIdx.x == 0 && (c.ictl[IC_QN] | c.ictl[IC_PQN])) ++fine_states;
         const int fb = c.ictl[IC_FIRSTBAD];
-        const long long good = (fb != kNoBad) ? (long long)fb : (g0 + cnt) / n_cc;
-        if (good > appended) {
-            const long long k_lo = c.ictl[IC_KLO];
-            const int cntk = (int)(good - appended);
-            const int got = tree_append_many(c, a, *T, c.ends + (appended + 1 - k_lo) * c.dof, cntk,
-                                             prev, &prev);
-            appended += got;
-            if (got < cntk) {
-                *last = prev;
-                __syncthreads();
-                return -1 - appended;
-            }
-        }
+        good = (fb != kNoBad) ? (long long)fb : (g0 + cnt) / n_cc;
         __syncthreads();
         if (fb != kNoBad) break;
+    }
+    long long appended = 0;
+    int prev = parent0;
+    while (appended < good) {
+        const int cntk = (int)min(good - appended, (long long)c.NS + 1);
+        for (int idx = threadIdx.x; idx < cntk * c.dof; idx += c.nthreads) {
+            const int j = idx / c.dof, d = idx - j * c.dof;
+            c.ends[idx] = chain_point(A, B, d, appended + 1 + j, n_sub);
+        }
+        __syncthreads();
+        const int got = tree_append_many(c, a, *T, c.ends, cntk, prev, &prev);
+        appended += got;
+        __syncthreads();
+        if (got < cntk) {
+            *last = prev;
+            return -1 - appended;
+        }
     }
     *last = prev;
     return appended;

@@ -141,7 +141,7 @@ def test_invalid_arguments_raise(gpu):
 
 def test_capacity_exhaustion_fails_cleanly(gpu):
     m = robots.get("panda")
-    probs = load_problems("panda", 30)
+    probs = load_problems("panda")
     kind, pid, s, g = next(p for p in probs if p[0] == "cage")
     scene, _ = make_scene("panda", kind, pid)
     r = planner.plan(m, scene, s, g, PlannerParams(tree_capacity=4))

@@ -14,13 +14,14 @@ m = robots.get(robot)
 scenes = [make_scene(robot, str(k), int(p))[0] for k, p in zip(d["kind"], d["pid"])]
 S, G = d["start"], d["goal"]
 params = PlannerParams(tree_capacity=cap)
-for w in (0, 64, 148, 296, 592):
+sel = list(range(0, len(S), max(1, len(S) // 60)))[:60]
+for w in (0, 32, 64, 148, 296, 592):
     params.workers = w
     walls, devs, st, its = [], [], [], []
-    for i in range(min(60, len(S))):
+    for i in sel:
         r = planner.plan(m, scenes[i], S[i], G[i], params)
         walls.append(r.wall_time_ms); devs.append(r.device_time_ms); st.append(r.status); its.append(r.iterations_total)
-    walls, devs, st = np.array(walls[5:]), np.array(devs[5:]), np.array(st[5:])
+    walls, devs, st = np.array(walls), np.array(devs), np.array(st)
     ok = st == 0
     print(f"{robot} workers={w}: solved {ok.mean():.2f} wall median {np.median(walls[ok]):.3f} p95 {np.percentile(walls[ok],95):.3f} "
           f"dev median {np.median(devs[ok]):.3f} iters med {np.median(its):.0f}", flush=True)
