@@ -64,6 +64,40 @@ def build_lib(force: bool = False, verbose: bool = False) -> Path:
     return LIB
 
 
+REF_INCLUDE = Path("/root/reference/proj/include")
+REF_SRC = Path("/root/reference/proj/src")
+DROPIN_LIB = LIB_DIR / "libprrtc_b200_dropin.so"
+DEMO_BIN = ROOT / "tests" / "cpp" / "bin" / "dropin_demo"
+REF_SOURCES = ["collision", "geometry", "kernels", "kernels_scalar", "kernels_avx2", "kinematics", "nn",
+               "planner", "sampling"]
+
+
+def build_dropin(force: bool = False) -> Path | None:
+    """C++ drop-in prrtc::b200::plan (reference types) + its demo/test binary.
+    Both compile against the reference's headers, so they are built only
+    where /root/reference exists; the outputs travel with the repo snapshot."""
+    if not REF_INCLUDE.is_dir():
+        return None
+    cxx = shutil.which("g++") or "g++"
+    dsrc = PKG / "dropin" / "prrtc_dropin.cpp"
+    deps = [dsrc, PKG / "dropin" / "prrtc_dropin.hpp", ROOT / "include" / "prrtc_b200.h", LIB]
+    flags = ["-std=c++20", "-O2", "-fPIC", f"-I{REF_INCLUDE}", f"-I{ROOT / 'include'}", f"-I{PKG / 'dropin'}"]
+    if force or _stale(DROPIN_LIB, deps):
+        subprocess.run([cxx, *flags, "-shared", "-o", str(DROPIN_LIB), str(dsrc), f"-L{LIB_DIR}",
+                        "-lprrtc_b200", "-Wl,-rpath,$ORIGIN"], check=True)
+    demo = ROOT / "tests" / "cpp" / "dropin_demo.cpp"
+    if REF_SRC.is_dir() and (force or _stale(DEMO_BIN, [demo, DROPIN_LIB])):
+        DEMO_BIN.parent.mkdir(parents=True, exist_ok=True)
+        # reference sources compiled in place (never copied), -mavx2 as the
+        # reference's AVX2 kernels require (SURVEY.md §8c)
+        srcs = [str(REF_SRC / f"{s}.cpp") for s in REF_SOURCES]
+        subprocess.run([cxx, *flags, "-mavx2", "-ffp-contract=off", f"-I{REF_SRC}", "-o", str(DEMO_BIN),
+                        str(demo), *srcs, f"-L{LIB_DIR}", "-lprrtc_b200_dropin", "-lprrtc_b200",
+                        f"-Wl,-rpath,{LIB_DIR}", "-Wl,-rpath,$ORIGIN/../../../paper_2503_06757_b200/lib",
+                        "-lpthread"], check=True)
+    return DROPIN_LIB
+
+
 def build_oracle() -> None:
     """Checker libraries (test infrastructure): oracle/liboracle.so always,
     oracle/_ref/libprrtc_ref.so when the reference sources are present."""
@@ -75,6 +109,7 @@ def build_oracle() -> None:
 
 def main(argv: list[str]) -> int:
     build_lib(force="--force" in argv, verbose="-v" in argv)
+    build_dropin(force="--force" in argv)
     if "--all" in argv:
         build_oracle()
     print(LIB)
