@@ -327,6 +327,22 @@ int prrtc_robot_create(const prrtc_robot_desc* d, int device, prrtc_robot** out)
         for (uint32_t k = d->fine_offset[l]; k < d->fine_offset[l + 1]; ++k) w.push_back((uint32_t)l);
     align4();
     w[RH_WORDS] = (uint32_t)w.size();
+    {   // 3 dof (lerp) + 63 per non-root link + 70 per revolute
+        // + 21 per prismatic + 18 per posed (coarse) sphere
+        unsigned nonroot = 0, rev = 0, pri = 0;
+        double qabs = 0.0;
+        for (int l = 0; l < n; ++l) {
+            nonroot += d->parent[l] >= 0;
+            rev += d->kind[l] == PRRTC_JOINT_REVOLUTE;
+            pri += d->kind[l] == PRRTC_JOINT_PRISMATIC;
+            if (d->kind[l] != PRRTC_JOINT_FIXED)
+                qabs = std::max({qabs, std::abs(d->lo[l]), std::abs(d->hi[l])});
+        }
+        w[RH_FKFLOPS] = 3 * dof + 63 * nonroot + 70 * rev + 21 * pri + 18 * n;
+        // bound on |joint value| for the FP32 NN filter: samples and tree
+        // nodes stay within the limits, endpoints are limit-checked
+        w[RH_QABS] = fbits((float)(qabs * 1.0001 + 1e-6));
+    }
     r->reach = reach_sum;
     for (int l = 0; l < n; ++l) {
         if (d->kind[l] != PRRTC_JOINT_FIXED) {
@@ -553,6 +569,7 @@ struct Workspace {
     unsigned char* d_in = nullptr;
     unsigned char* d_out = nullptr;
     double* d_cfg = nullptr;
+    float* d_cfgf = nullptr;
     int* d_parent = nullptr;
     int* d_dd = nullptr;
     unsigned* d_ready = nullptr;
@@ -572,6 +589,7 @@ struct Workspace {
         cudaFree(d_in);
         cudaFree(d_out);
         cudaFree(d_cfg);
+        cudaFree(d_cfgf);
         cudaFree(d_parent);
         cudaFree(d_dd);
         cudaFree(d_ready);
@@ -599,6 +617,7 @@ struct Workspace {
             cudaMallocHost(&h_out, out_hdr(nn) + 8 * std::min<size_t>(narena, 1 << 16)) != cudaSuccess ||
             cudaMalloc(&d_in, io_bytes) != cudaSuccess || cudaMalloc(&d_out, out_bytes) != cudaSuccess ||
             cudaMalloc(&d_cfg, 8 * nnodes * nd) != cudaSuccess ||
+            cudaMalloc(&d_cfgf, 4 * nnodes * nd) != cudaSuccess ||
             cudaMalloc(&d_parent, 4 * nnodes) != cudaSuccess ||
             cudaMalloc(&d_dd, 4 * nnodes) != cudaSuccess ||
             cudaMalloc(&d_ready, 4 * nnodes) != cudaSuccess) {
@@ -797,6 +816,7 @@ int batch_enqueue(prrtc_batch* b, cudaStream_t st, bool upload) {
     a.n_problems = b->n;
     a.ctl = b->d_ctl;
     a.cfg = ws->d_cfg;
+    a.cfgf = ws->d_cfgf;
     a.parent = ws->d_parent;
     a.ready = ws->d_ready;
     a.dd = ws->d_dd;
@@ -869,8 +889,10 @@ int batch_collect(prrtc_batch* b, prrtc_result* out) {
     const double* arena = reinterpret_cast<const double*>(h + hdr);
     std::vector<double> big;
     if (used > prefix) {
-        big.resize(used);
-        CUDA_TRY(cudaMemcpy(big.data(), b->d_arena, 8 * used, cudaMemcpyDeviceToHost));
+        big.resize(used);  // prefix already on the host; fetch only the rest
+        std::memcpy(big.data(), arena, 8 * prefix);
+        CUDA_TRY(cudaMemcpy(big.data() + prefix, b->d_arena + prefix, 8 * (used - prefix),
+                            cudaMemcpyDeviceToHost));
         arena = big.data();
     }
     float ms = 0.f;
@@ -1106,21 +1128,35 @@ int prrtc_debug_nn(const double* tree, uint32_t count, uint32_t dof, const doubl
     if (rc) return rc;
     cudaSetDevice(device);
     const long long cap = ((long long)count + 31) / 32 * 32;
+    // the planner's layout: FP64 SoA + FP32 SoA copy (the NN filter)
     std::vector<double> soa((size_t)cap * dof, 0.0);
+    std::vector<float> soaf((size_t)cap * dof, 0.0f);
+    double qabs = 0.0;
     for (uint32_t i = 0; i < count; ++i)
-        for (uint32_t d = 0; d < dof; ++d) soa[(size_t)d * cap + i] = tree[(size_t)i * dof + d];
+        for (uint32_t d = 0; d < dof; ++d) {
+            soa[(size_t)d * cap + i] = tree[(size_t)i * dof + d];
+            soaf[(size_t)d * cap + i] = (float)tree[(size_t)i * dof + d];
+            qabs = std::max(qabs, std::abs(tree[(size_t)i * dof + d]));
+        }
+    for (size_t i = 0; i < (size_t)n_queries * dof; ++i) qabs = std::max(qabs, std::abs(q[i]));
     double *ds = nullptr, *dq = nullptr, *dd = nullptr;
+    float* dsf = nullptr;
     uint32_t* di = nullptr;
-    if ((rc = dmalloc(&ds, soa.size())) || (rc = dmalloc(&dq, (size_t)n_queries * dof)) ||
-        (rc = dmalloc(&dd, n_queries)) || (rc = dmalloc(&di, n_queries))) {
+    if ((rc = dmalloc(&ds, soa.size())) || (rc = dmalloc(&dsf, soaf.size())) ||
+        (rc = dmalloc(&dq, (size_t)n_queries * dof)) || (rc = dmalloc(&dd, n_queries)) ||
+        (rc = dmalloc(&di, n_queries))) {
         cudaFree(ds);
+        cudaFree(dsf);
         cudaFree(dq);
         cudaFree(dd);
         return rc;
     }
     cudaMemcpy(ds, soa.data(), 8 * soa.size(), cudaMemcpyHostToDevice);
+    cudaMemcpy(dsf, soaf.data(), 4 * soaf.size(), cudaMemcpyHostToDevice);
     cudaMemcpy(dq, q, 8 * (size_t)n_queries * dof, cudaMemcpyHostToDevice);
-    cudaError_t e = launch_debug_nn(ds, cap, (int)count, (int)dof, dq, (int)n_queries, di, dd, 0);
+    cudaError_t e = launch_debug_nn(ds, dsf, cap, (int)count, (int)dof, (float)(qabs * 1.0001 + 1e-6), dq,
+                                    (int)n_queries, di, dd, 0);
+    cudaFree(dsf);
     if (e == cudaSuccess) e = cudaMemcpy(index, di, 4 * (size_t)n_queries, cudaMemcpyDeviceToHost);
     if (e == cudaSuccess) e = cudaMemcpy(sq_dist, dd, 8 * (size_t)n_queries, cudaMemcpyDeviceToHost);
     cudaFree(ds);

@@ -127,6 +127,53 @@ def _to_result(r: Result, dof: int) -> PlanResult:
     )
 
 
+def _result_dtype() -> np.dtype:
+    """numpy view of prrtc_result (pointer fields as uint64)."""
+    names, formats, offsets = [], [], []
+    for name, ctype in Result._fields_:
+        off = getattr(Result, name).offset
+        if name == "path":
+            fmt = np.uint64
+        elif name == "message":
+            fmt = "S128"
+        elif name == "tree_nodes":
+            fmt = (np.uint64, 2)
+        else:
+            fmt = np.dtype(ctype)
+        names.append(name)
+        formats.append(fmt)
+        offsets.append(off)
+    return np.dtype({"names": names, "formats": formats, "offsets": offsets, "itemsize": C.sizeof(Result)})
+
+
+_RESULT_DTYPE = None
+
+
+class BatchResult:
+    """Array view of a batch's results (no per-problem Python objects):
+    status / cost / iterations_total / device_time_ms / flops arrays and one
+    path array per problem (empty unless solved)."""
+
+    def __init__(self, res, n: int, dof: int):
+        global _RESULT_DTYPE
+        if _RESULT_DTYPE is None:
+            _RESULT_DTYPE = _result_dtype()
+        a = np.frombuffer(res, dtype=_RESULT_DTYPE, count=n)
+        self.status = a["status"].copy()
+        self.cost = a["cost"].copy()
+        self.iterations_total = a["iterations_total"].copy()
+        self.device_time_ms = a["device_time_ms"].copy()
+        self.flops = a["flops"].copy()
+        lens = a["path_len"]
+        self.paths = []
+        for i in range(n):
+            if lens[i]:
+                self.paths.append(np.ctypeslib.as_array(res[i].path, shape=(int(lens[i]) * dof,))
+                                  .reshape(-1, dof).copy())
+            else:
+                self.paths.append(np.zeros((0, dof)))
+
+
 def _cfg(q, dof: int, what: str) -> np.ndarray:
     a = np.ascontiguousarray(np.asarray(q, dtype=np.float64))
     if a.ndim != 1 or a.shape[0] != dof:  # require_dim (types.hpp:16-21)
@@ -160,9 +207,7 @@ def _scene_handles(scenes, n, device):
     return hs, arr
 
 
-def plan_batch(model, scenes, starts, goals, params: PlannerParams | None = None,
-               device: int = 0) -> list[PlanResult]:
-    """n independent problems (one robot, one scene each) in one device launch."""
+def _plan_batch_raw(model, scenes, starts, goals, params, device):
     params = params or PlannerParams()
     rob = device_robot(model, device)
     S = np.ascontiguousarray(np.asarray(starts, dtype=np.float64).reshape(-1, rob.dof))
@@ -172,10 +217,32 @@ def plan_batch(model, scenes, starts, goals, params: PlannerParams | None = None
     p = params.to_c()
     res = (Result * n)()
     check(_lib.load().prrtc_plan_batch(rob.h, arr, n, _dptr(S), _dptr(G), rob.dof, C.byref(p), res))
-    out = [_to_result(res[i], rob.dof) for i in range(n)]
+    return rob, res, n, hs
+
+
+def _free(res, n):
+    lib = _lib.load()
     for i in range(n):
-        _lib.load().prrtc_result_free(C.byref(res[i]))
-    del hs
+        if res[i].path:
+            lib.prrtc_result_free(C.byref(res[i]))
+
+
+def plan_batch(model, scenes, starts, goals, params: PlannerParams | None = None,
+               device: int = 0) -> list[PlanResult]:
+    """n independent problems (one robot, one scene each) in one device launch."""
+    rob, res, n, hs = _plan_batch_raw(model, scenes, starts, goals, params, device)
+    out = [_to_result(res[i], rob.dof) for i in range(n)]
+    _free(res, n)
+    return out
+
+
+def plan_batch_arrays(model, scenes, starts, goals, params: PlannerParams | None = None,
+                      device: int = 0) -> BatchResult:
+    """plan_batch returning arrays (BatchResult) instead of n PlanResult objects.
+    Pass DeviceScene handles (device_scene(s)) to keep scene setup out of the call."""
+    rob, res, n, hs = _plan_batch_raw(model, scenes, starts, goals, params, device)
+    out = BatchResult(res, n, rob.dof)
+    _free(res, n)
     return out
 
 
