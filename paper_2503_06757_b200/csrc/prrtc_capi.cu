@@ -123,7 +123,7 @@ struct prrtc_robot {
     double* d_fine_r64 = nullptr;
     double* d_limits = nullptr;
     double reach = 0.0;           // bound on |posed sphere| (m)
-    mutable std::atomic<int> occ[5] = {};  // planner CTAs per SM, by ns_max / 32
+    mutable std::atomic<int> occ[10] = {};  // planner CTAs per SM, by (ns_max / 32, CTA size)
     RobotArgs args() const {
         RobotArgs r;
         r.words = d_words;
@@ -330,18 +330,12 @@ int prrtc_robot_create(const prrtc_robot_desc* d, int device, prrtc_robot** out)
     {   // 3 dof (lerp) + 63 per non-root link + 70 per revolute
         // + 21 per prismatic + 18 per posed (coarse) sphere
         unsigned nonroot = 0, rev = 0, pri = 0;
-        double qabs = 0.0;
         for (int l = 0; l < n; ++l) {
             nonroot += d->parent[l] >= 0;
             rev += d->kind[l] == PRRTC_JOINT_REVOLUTE;
             pri += d->kind[l] == PRRTC_JOINT_PRISMATIC;
-            if (d->kind[l] != PRRTC_JOINT_FIXED)
-                qabs = std::max({qabs, std::abs(d->lo[l]), std::abs(d->hi[l])});
         }
         w[RH_FKFLOPS] = 3 * dof + 63 * nonroot + 70 * rev + 21 * pri + 18 * n;
-        // bound on |joint value| for the FP32 NN filter: samples and tree
-        // nodes stay within the limits, endpoints are limit-checked
-        w[RH_QABS] = fbits((float)(qabs * 1.0001 + 1e-6));
     }
     r->reach = reach_sum;
     for (int l = 0; l < n; ++l) {
@@ -569,7 +563,6 @@ struct Workspace {
     unsigned char* d_in = nullptr;
     unsigned char* d_out = nullptr;
     double* d_cfg = nullptr;
-    float* d_cfgf = nullptr;
     int* d_parent = nullptr;
     int* d_dd = nullptr;
     unsigned* d_ready = nullptr;
@@ -589,7 +582,6 @@ struct Workspace {
         cudaFree(d_in);
         cudaFree(d_out);
         cudaFree(d_cfg);
-        cudaFree(d_cfgf);
         cudaFree(d_parent);
         cudaFree(d_dd);
         cudaFree(d_ready);
@@ -617,7 +609,6 @@ struct Workspace {
             cudaMallocHost(&h_out, out_hdr(nn) + 8 * std::min<size_t>(narena, 1 << 16)) != cudaSuccess ||
             cudaMalloc(&d_in, io_bytes) != cudaSuccess || cudaMalloc(&d_out, out_bytes) != cudaSuccess ||
             cudaMalloc(&d_cfg, 8 * nnodes * nd) != cudaSuccess ||
-            cudaMalloc(&d_cfgf, 4 * nnodes * nd) != cudaSuccess ||
             cudaMalloc(&d_parent, 4 * nnodes) != cudaSuccess ||
             cudaMalloc(&d_dd, 4 * nnodes) != cudaSuccess ||
             cudaMalloc(&d_ready, 4 * nnodes) != cudaSuccess) {
@@ -677,8 +668,8 @@ int check_params(const prrtc_params* p) {  // planner.cpp:250-252
     if (!(p->delta > 0.0)) return set_err(PRRTC_EINVAL, "plan: delta must be positive");
     if (p->n_cc < 1) return set_err(PRRTC_EINVAL, "plan: n_cc must be >= 1");
     if (p->tree_capacity < 2) return set_err(PRRTC_EINVAL, "plan: tree_capacity too small");
-    if (p->threads_per_cta != 0 && p->threads_per_cta != 128)
-        return set_err(PRRTC_EINVAL, "plan: threads_per_cta must be 0 or 128");
+    if (p->threads_per_cta != 0 && p->threads_per_cta != 128 && p->threads_per_cta != 256)
+        return set_err(PRRTC_EINVAL, "plan: threads_per_cta must be 0, 128 or 256");
     if (p->sampler != PRRTC_SAMPLER_HALTON)
         return set_err(PRRTC_EINVAL, "plan: the device sampler is Halton only (SamplerKind::Uniform is a property-test sampler, sampling.hpp:40-54)");
     return PRRTC_OK;
@@ -721,12 +712,15 @@ int batch_setup(prrtc_batch* b, const prrtc_robot* robot, const prrtc_scene* con
     b->params = *params;
     b->cap = std::max<long long>(2, (long long)(params->tree_capacity / 2));  // planner.cpp:290
     b->stride = (b->cap + 31) / 32 * 32;
-    b->nthreads = 128;
-    b->ns_max = std::max(32, std::min(128, (params->n_cc + 31) / 32 * 32));
-    int occ = robot->occ[b->ns_max / 32].load(std::memory_order_relaxed);
+    b->nthreads = params->threads_per_cta ? (int)params->threads_per_cta : 128;
+    // states per validation chunk: 32 per 128 threads (a connect chain is
+    // validated NS states at a time; longer edges take several chunks)
+    b->ns_max = b->nthreads / 4;
+    const int okey = b->ns_max / 32 + (b->nthreads == 256 ? 5 : 0);
+    int occ = robot->occ[okey].load(std::memory_order_relaxed);
     if (occ == 0) {
         occ = plan_occupancy(robot->args(), b->ns_max, b->nthreads);
-        robot->occ[b->ns_max / 32].store(occ, std::memory_order_relaxed);
+        robot->occ[okey].store(occ, std::memory_order_relaxed);
     }
     const int sms = sm_count(robot->device);
     unsigned workers_eff;
@@ -816,7 +810,6 @@ int batch_enqueue(prrtc_batch* b, cudaStream_t st, bool upload) {
     a.n_problems = b->n;
     a.ctl = b->d_ctl;
     a.cfg = ws->d_cfg;
-    a.cfgf = ws->d_cfgf;
     a.parent = ws->d_parent;
     a.ready = ws->d_ready;
     a.dd = ws->d_dd;
@@ -1128,35 +1121,21 @@ int prrtc_debug_nn(const double* tree, uint32_t count, uint32_t dof, const doubl
     if (rc) return rc;
     cudaSetDevice(device);
     const long long cap = ((long long)count + 31) / 32 * 32;
-    // the planner's layout: FP64 SoA + FP32 SoA copy (the NN filter)
-    std::vector<double> soa((size_t)cap * dof, 0.0);
-    std::vector<float> soaf((size_t)cap * dof, 0.0f);
-    double qabs = 0.0;
+    std::vector<double> soa((size_t)cap * dof, 0.0);  // the planner's SoA tree layout
     for (uint32_t i = 0; i < count; ++i)
-        for (uint32_t d = 0; d < dof; ++d) {
-            soa[(size_t)d * cap + i] = tree[(size_t)i * dof + d];
-            soaf[(size_t)d * cap + i] = (float)tree[(size_t)i * dof + d];
-            qabs = std::max(qabs, std::abs(tree[(size_t)i * dof + d]));
-        }
-    for (size_t i = 0; i < (size_t)n_queries * dof; ++i) qabs = std::max(qabs, std::abs(q[i]));
+        for (uint32_t d = 0; d < dof; ++d) soa[(size_t)d * cap + i] = tree[(size_t)i * dof + d];
     double *ds = nullptr, *dq = nullptr, *dd = nullptr;
-    float* dsf = nullptr;
     uint32_t* di = nullptr;
-    if ((rc = dmalloc(&ds, soa.size())) || (rc = dmalloc(&dsf, soaf.size())) ||
-        (rc = dmalloc(&dq, (size_t)n_queries * dof)) || (rc = dmalloc(&dd, n_queries)) ||
-        (rc = dmalloc(&di, n_queries))) {
+    if ((rc = dmalloc(&ds, soa.size())) || (rc = dmalloc(&dq, (size_t)n_queries * dof)) ||
+        (rc = dmalloc(&dd, n_queries)) || (rc = dmalloc(&di, n_queries))) {
         cudaFree(ds);
-        cudaFree(dsf);
         cudaFree(dq);
         cudaFree(dd);
         return rc;
     }
     cudaMemcpy(ds, soa.data(), 8 * soa.size(), cudaMemcpyHostToDevice);
-    cudaMemcpy(dsf, soaf.data(), 4 * soaf.size(), cudaMemcpyHostToDevice);
     cudaMemcpy(dq, q, 8 * (size_t)n_queries * dof, cudaMemcpyHostToDevice);
-    cudaError_t e = launch_debug_nn(ds, dsf, cap, (int)count, (int)dof, (float)(qabs * 1.0001 + 1e-6), dq,
-                                    (int)n_queries, di, dd, 0);
-    cudaFree(dsf);
+    cudaError_t e = launch_debug_nn(ds, cap, (int)count, (int)dof, dq, (int)n_queries, di, dd, 0);
     if (e == cudaSuccess) e = cudaMemcpy(index, di, 4 * (size_t)n_queries, cudaMemcpyDeviceToHost);
     if (e == cudaSuccess) e = cudaMemcpy(sq_dist, dd, 8 * (size_t)n_queries, cudaMemcpyDeviceToHost);
     cudaFree(ds);

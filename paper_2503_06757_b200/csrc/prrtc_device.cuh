@@ -225,7 +225,6 @@ struct Ctx {
     const double* fine_r64;  // global
     const double* limits;    // global [dof][2]
     unsigned fkflops;        // per-state FK + coarse posing flops
-    float qabs;              // max |joint value| over the limits (NN error bound)
     int nnpar;               // nn_scan buffer parity
     // scene (shared memory copy)
     int ns, nb, nc, P;
@@ -725,10 +724,13 @@ struct NnOut {
     int index;
     double d2;
 };
-// Exact FP64-only scan (the form the FP32-filtered scan below refines to;
-// kept for reference and for trees without an FP32 copy).
-__device__ NnOut nn_scan_exact(Ctx& c, const double* cfg, long long cap, int count, const double* q) {
-    const int tid = threadIdx.x;
+__device__ __noinline__ NnOut nn_scan(Ctx& c, const double* cfg, long long cap, int count,
+                                      const double* q) {
+    __shared__ double s_bd[2][32];
+    __shared__ int s_bi[2][32];
+    const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5, nw = c.nthreads >> 5, dof = c.dof;
+    const int par = c.nnpar;  // double-buffered reduction slots: one barrier per call
+    c.nnpar ^= 1;
     double best = __longlong_as_double(0x7ff0000000000000ll);  // +inf
     int bi = 0x7fffffff;
     const int npairs = (count + 1) >> 1;
@@ -739,12 +741,12 @@ __device__ NnOut nn_scan_exact(Ctx& c, const double* cfg, long long cap, int cou
         const int n0 = pi * 2, pj = pi + c.nthreads, n1 = pj * 2;
         const bool has1 = pj < npairs;
         double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
-        for (int d = 0; d < c.dof; ++d) {
+        for (int d = 0; d < dof; ++d) {
             const double2 v = __ldcg(reinterpret_cast<const double2*>(cfg + d * cap + n0));
-            const double2 w = has1 ? __ldcg(reinterpret_cast<const double2*>(cfg + d * cap + n1)) : v;
+            const double2 u = has1 ? __ldcg(reinterpret_cast<const double2*>(cfg + d * cap + n1)) : v;
             const double qd = q[d];
             const double e0 = __dsub_rn(v.x, qd), e1 = __dsub_rn(v.y, qd);
-            const double e2 = __dsub_rn(w.x, qd), e3 = __dsub_rn(w.y, qd);
+            const double e2 = __dsub_rn(u.x, qd), e3 = __dsub_rn(u.y, qd);
             a0 = __dadd_rn(a0, __dmul_rn(e0, e0));
             a1 = __dadd_rn(a1, __dmul_rn(e1, e1));
             a2 = __dadd_rn(a2, __dmul_rn(e2, e2));
@@ -765,135 +767,6 @@ __device__ NnOut nn_scan_exact(Ctx& c, const double* cfg, long long cap, int cou
         if (has1 && n1 + 1 < count && a3 < best) {
             best = a3;
             bi = n1 + 1;
-        }
-    }
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) {
-        const double ob = __shfl_xor_sync(0xffffffffu, best, o);
-        const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
-        if (ob < best || (ob == best && oi < bi)) {
-            best = ob;
-            bi = oi;
-        }
-    }
-    const int w = tid >> 5, nw = c.nthreads >> 5;
-    if ((tid & 31) == 0) {
-        c.red_d[w] = best;
-        c.red_i[w] = bi;
-    }
-    __syncthreads();
-    if (tid == 0) {
-        double b = c.red_d[0];
-        int i = c.red_i[0];
-        for (int k = 1; k < nw; ++k) {
-            if (c.red_d[k] < b || (c.red_d[k] == b && c.red_i[k] < i)) {
-                b = c.red_d[k];
-                i = c.red_i[k];
-            }
-        }
-        c.red_d[0] = b;
-        c.ictl[IC_TMP0] = i;
-    }
-    __syncthreads();
-    NnOut r{c.ictl[IC_TMP0], c.red_d[0]};
-    __syncthreads();
-    return r;
-}
-
-// ---------------------------------------------------------------------------
-// FP32-filtered exact nearest neighbour (the planner's scan).
-//
-// Pass 1 streams an FP32 SoA copy of the tree (half the bytes of FP64; four
-// nodes per 128-bit load) and keeps, per thread, the smallest and second
-// smallest FP32 key. With mn the CTA-wide FP32 minimum and m a rigorous
-// bound on |key_f32 - key_f64| (inputs rounded to float, FP32 subtraction and
-// FMA accumulation; X = max |joint value|):
-//     m = 8u (2 X sqrt(dof D) + (dof + 2) D),  D = 2 mn,  u = 2^-24,
-// the exact argmin (lowest index on ties) has key_f32 <= mn + m. Every thread
-// whose best is within mn + m evaluates it exactly in FP64 (scalar order,
-// kernels_scalar.cpp:9-16); a thread whose SECOND best is also within the
-// margin re-scans its own nodes exactly. The exact candidates are reduced
-// with ties to the lowest index. Result: identical to nearest_serial with
-// the scalar backend (nn.cpp:22-29).
-// ---------------------------------------------------------------------------
-__device__ __forceinline__ double exact_key(const double* cfg, long long cap, int dof, int n,
-                                            const double* q) {
-    double a = 0.0;
-    for (int d = 0; d < dof; ++d) {
-        const double e = __dsub_rn(__ldcg(cfg + d * cap + n), q[d]);
-        a = __dadd_rn(a, __dmul_rn(e, e));
-    }
-    return a;
-}
-
-__device__ __noinline__ NnOut nn_scan(Ctx& c, const double* cfg, const float* cfgf, long long cap,
-                                      int count, const double* q) {
-    __shared__ float s_mn[2][32];
-    __shared__ double s_bd[2][32];
-    __shared__ int s_bi[2][32];
-    const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5, nw = c.nthreads >> 5;
-    const int par = c.nnpar;
-    c.nnpar ^= 1;
-    const float INF = __int_as_float(0x7f800000);
-    float b1 = INF, b2 = INF;
-    int i1 = -1;
-    const int nquads = (count + 3) >> 2;
-    for (int qi = tid; qi < nquads; qi += c.nthreads) {
-        const int n0 = qi * 4;
-        float a0 = 0.f, a1 = 0.f, a2 = 0.f, a3 = 0.f;
-        for (int d = 0; d < c.dof; ++d) {
-            const float4 v = __ldcg(reinterpret_cast<const float4*>(cfgf + d * cap + n0));
-            const float qd = (float)q[d];
-            const float e0 = v.x - qd, e1 = v.y - qd, e2 = v.z - qd, e3 = v.w - qd;
-            a0 = fmaf(e0, e0, a0);
-            a1 = fmaf(e1, e1, a1);
-            a2 = fmaf(e2, e2, a2);
-            a3 = fmaf(e3, e3, a3);
-        }
-        const float av[4] = {a0, a1, a2, a3};
-#pragma unroll
-        for (int k = 0; k < 4; ++k) {
-            if (n0 + k >= count) break;
-            const float a = av[k];
-            if (a < b1) {
-                b2 = b1;
-                b1 = a;
-                i1 = n0 + k;
-            } else if (a < b2) {
-                b2 = a;
-            }
-        }
-    }
-    float mn = b1;
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) mn = fminf(mn, __shfl_xor_sync(0xffffffffu, mn, o));
-    if (lane == 0) s_mn[par][w] = mn;
-    __syncthreads();
-    mn = s_mn[par][0];
-    for (int k = 1; k < nw; ++k) mn = fminf(mn, s_mn[par][k]);
-    const float D = 2.0f * mn;
-    const float uX = 5.9604645e-8f * c.qabs;
-    const float m = 8.0f * 5.9604645e-8f * (2.0f * c.qabs * sqrtf((float)c.dof * D) + (float)(c.dof + 2) * D) +
-                    8.0f * (float)c.dof * uX * uX + 1e-30f;
-    const float lim = mn + 2.0f * m;
-    double best = __longlong_as_double(0x7ff0000000000000ll);
-    int bi = 0x7fffffff;
-    if (b1 <= lim) {
-        if (b2 <= lim) {  // ambiguous within this thread: exact re-scan of its nodes
-            for (int qi = tid; qi < nquads; qi += c.nthreads) {
-                for (int k = 0; k < 4; ++k) {
-                    const int n = qi * 4 + k;
-                    if (n >= count) break;
-                    const double a = exact_key(cfg, cap, c.dof, n, q);
-                    if (a < best) {
-                        best = a;
-                        bi = n;
-                    }
-                }
-            }
-        } else {
-            best = exact_key(cfg, cap, c.dof, i1, q);
-            bi = i1;
         }
     }
 #pragma unroll

@@ -34,7 +34,6 @@ enum RobotHdr : int {
     RH_OFF_FLINK, // int[S] link of each fine sphere
     RH_FKFLOPS,   // algorithmic FP32 flops of FK + coarse posing per state
     RH_OFF_MAGIC, // uint64[dof] ceil(2^64 / base): exact 32-bit division by the Halton bases
-    RH_QABS,      // float bits: max |joint limit| (FP32 NN filter error bound)
     RH_COUNT = 16
 };
 
@@ -122,7 +121,6 @@ struct PlanArgs {
     int n_problems;
     ProbCtl* ctl;              // [n]
     double* cfg;               // [n][2][dof][cap]
-    float* cfgf;               // [n][2][dof][cap] FP32 copy for the NN filter
     int* parent;               // [n][2][cap]
     unsigned* ready;           // [n][2][cap]
     int* dd;                   // [n][2][cap]

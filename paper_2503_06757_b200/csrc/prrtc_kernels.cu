@@ -114,7 +114,6 @@ __device__ void setup_ctx(Ctx& c, unsigned char* smem, const uint32_t* robot_g, 
     c.tests = 0;
     c.flops = 0;
     c.fkflops = rw[RH_FKFLOPS];
-    c.qabs = __uint_as_float(rw[RH_QABS]);
     c.nnpar = 0;
     c.ns = c.nb = c.nc = c.P = 0;  // scene pointers are wired by load_scene
 }
@@ -151,7 +150,6 @@ __device__ __forceinline__ unsigned char* scene_base(unsigned char* smem, int ro
 // ---------------------------------------------------------------------------
 struct TreeRef {
     double* cfg;       // [dof][cap]
-    float* cfgf;       // [dof][cap]
     int* parent;       // [cap]
     unsigned* ready;   // [cap]
     int* dd;           // [cap]
@@ -163,7 +161,6 @@ __device__ __forceinline__ TreeRef tree_ref(const PlanArgs& a, int prob, int t, 
     TreeRef r;
     const size_t pt = (size_t)prob * 2 + t;
     r.cfg = a.cfg + pt * dof * a.stride;
-    r.cfgf = a.cfgf + pt * dof * a.stride;
     r.parent = a.parent + pt * a.stride;
     r.ready = a.ready + pt * a.stride;
     r.dd = a.dd + pt * a.stride;
@@ -192,7 +189,6 @@ __device__ int tree_append_many(Ctx& c, const PlanArgs& a, const TreeRef& T, con
     for (int idx = tid; idx < ok * dof; idx += c.nthreads) {
         const int j = idx / dof, d = idx - j * dof;
         T.cfg[(size_t)d * a.stride + s0 + j] = pts[idx];
-        T.cfgf[(size_t)d * a.stride + s0 + j] = (float)pts[idx];
     }
     for (int j = tid; j < ok; j += c.nthreads) {
         T.parent[s0 + j] = j == 0 ? parent0 : (int)(s0 + j - 1);
@@ -429,10 +425,7 @@ __device__ bool init_problem(Ctx& c, const PlanArgs& a, int prob, unsigned long 
     // roots
     for (int t = 0; t < 2; ++t) {
         const TreeRef T = tree_ref(a, prob, t, dof);
-        if (tid < dof) {
-            T.cfg[(size_t)tid * a.stride] = (t == 0 ? S : G)[tid];
-            T.cfgf[(size_t)tid * a.stride] = (float)(t == 0 ? S : G)[tid];
-        }
+        if (tid < dof) T.cfg[(size_t)tid * a.stride] = (t == 0 ? S : G)[tid];
         if (tid == 0) {
             T.parent[0] = -1;
             T.dd[0] = 0;
@@ -544,7 +537,8 @@ __device__ void leave_problem(const PlanArgs& a, int prob, int reason_msg) {
     }
 }
 
-__global__ void __launch_bounds__(128, 4) plan_kernel(PlanArgs a) {
+template <int NT, int MINB>
+__global__ void __launch_bounds__(NT, MINB) plan_kernel(PlanArgs a) {
     extern __shared__ __align__(16) unsigned char smem[];
     Ctx c;
     setup_ctx(c, smem, a.robot, reinterpret_cast<const int*>(a.robot)[RH_WORDS], a.fine_r64,
@@ -630,7 +624,7 @@ __global__ void __launch_bounds__(128, 4) plan_kernel(PlanArgs a) {
             }
             __syncthreads();
             // ---- nearest neighbour in the extended tree ----
-            const NnOut nr = nn_scan(c, Ts.cfg, Ts.cfgf, a.stride, snap, smp);
+            const NnOut nr = nn_scan(c, Ts.cfg, a.stride, snap, smp);
             const int nn = nr.index;
             const double d2 = nr.d2;
             if (d2 == 0.0) continue;  // duplicate of an existing node (planner.cpp:320)
@@ -667,7 +661,7 @@ __global__ void __launch_bounds__(128, 4) plan_kernel(PlanArgs a) {
             __syncthreads();
             const int snap_o = c.ictl[IC_TMP2];
             __syncthreads();
-            const NnOut no = nn_scan(c, To.cfg, To.cfgf, a.stride, snap_o, cnew);
+            const NnOut no = nn_scan(c, To.cfg, a.stride, snap_o, cnew);
             const int nno = no.index;
             const double d2o = no.d2;
             bool reached = false;
@@ -725,21 +719,28 @@ __global__ void __launch_bounds__(128, 4) plan_kernel(PlanArgs a) {
     }
 }
 
+// CTA size variants: 128 threads (4 warps, up to 4 CTAs/SM) and 256 threads
+// (8 warps, 2 CTAs/SM: each iteration's parallel phases finish faster).
+using PlanFn = void (*)(PlanArgs);
+static PlanFn plan_fn(int nthreads) {
+    return nthreads == 256 ? plan_kernel<256, 2> : plan_kernel<128, 4>;
+}
+
 cudaError_t launch_plan(const RobotArgs& r, PlanArgs a, int grid, cudaStream_t st) {
     const size_t sm = smem_bytes(r, a.ns_max, a.nthreads);
-    cudaError_t e = cudaFuncSetAttribute(plan_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         (int)sm);
+    const PlanFn fn = plan_fn(a.nthreads);
+    cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
     if (e != cudaSuccess) return e;
-    plan_kernel<<<grid, a.nthreads, sm, st>>>(a);
-    return cudaGetLastError();
+    void* args[] = {&a};
+    return cudaLaunchKernel(reinterpret_cast<const void*>(fn), dim3(grid), dim3(a.nthreads), args, sm, st);
 }
 
 int plan_occupancy(const RobotArgs& r, int ns_max, int nthreads) {
     const size_t sm = smem_bytes(r, ns_max, nthreads);
-    cudaFuncSetAttribute(plan_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+    const PlanFn fn = plan_fn(nthreads);
+    cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
     int n = 0;
-    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, plan_kernel, nthreads, sm) != cudaSuccess)
-        return 1;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, fn, nthreads, sm) != cudaSuccess) return 1;
     return n > 0 ? n : 1;
 }
 
@@ -858,18 +859,17 @@ __global__ void debug_hits_kernel(SceneArgs sa, const float* centers, const doub
     }
 }
 
-__global__ void debug_nn_kernel(const double* soa, const float* soaf, long long cap, int count, int dof,
-                                float qabs, const double* q, int nq, uint32_t* idx, double* d2) {
+__global__ void debug_nn_kernel(const double* soa, long long cap, int count, int dof, const double* q,
+                                int nq, uint32_t* idx, double* d2) {
     __shared__ double qs[kMaxDof];
     Ctx c;
     c.dof = dof;
     c.nthreads = blockDim.x;
-    c.qabs = qabs;
     c.nnpar = 0;
     for (int i = blockIdx.x; i < nq; i += gridDim.x) {
         if (threadIdx.x < dof) qs[threadIdx.x] = q[(size_t)i * dof + threadIdx.x];
         __syncthreads();
-        const NnOut r = nn_scan(c, soa, soaf, cap, count, qs);
+        const NnOut r = nn_scan(c, soa, cap, count, qs);
         if (threadIdx.x == 0) {
             idx[i] = r.index;
             d2[i] = r.d2;
@@ -994,10 +994,10 @@ cudaError_t launch_debug_hits(const SceneArgs& s, const float* centers, const do
     return cudaGetLastError();
 }
 
-cudaError_t launch_debug_nn(const double* soa, const float* soaf, long long cap, int count, int dof,
-                            float qabs, const double* q, int nq, uint32_t* idx, double* d2, cudaStream_t st) {
+cudaError_t launch_debug_nn(const double* soa, long long cap, int count, int dof, const double* q,
+                            int nq, uint32_t* idx, double* d2, cudaStream_t st) {
     const int grid = min(nq, 148 * 8);
-    if (grid > 0) debug_nn_kernel<<<grid, 128, 0, st>>>(soa, soaf, cap, count, dof, qabs, q, nq, idx, d2);
+    if (grid > 0) debug_nn_kernel<<<grid, 128, 0, st>>>(soa, cap, count, dof, q, nq, idx, d2);
     return cudaGetLastError();
 }
 

@@ -39,8 +39,8 @@ cudaError_t launch_debug_fk(const RobotArgs& r, const double* q, int n, float* f
                             float* coarse_out, cudaStream_t st);
 cudaError_t launch_debug_hits(const SceneArgs& s, const float* centers, const double* radii,
                               int n, int n_prims, uint8_t* hits, cudaStream_t st);
-cudaError_t launch_debug_nn(const double* soa, const float* soaf, long long cap, int count, int dof,
-                            float qabs, const double* q, int nq, uint32_t* idx, double* d2, cudaStream_t st);
+cudaError_t launch_debug_nn(const double* soa, long long cap, int count, int dof, const double* q,
+                            int nq, uint32_t* idx, double* d2, cudaStream_t st);
 cudaError_t launch_debug_halton(const uint32_t* bases, const uint64_t* idx, int n, double* out,
                                 cudaStream_t st);
 double measure_fp32_peak(int sms, cudaStream_t st);

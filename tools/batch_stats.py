@@ -12,12 +12,14 @@ from paper_2503_06757_b200.model import PlannerParams, PlanStatus  # noqa: E402
 from paper_2503_06757_b200.scenes import make_scene  # noqa: E402
 
 robot = sys.argv[1] if len(sys.argv) > 1 else "panda"
-budgets = [int(x) for x in (sys.argv[2].split(",") if len(sys.argv) > 2 else ["1", "8", "32"])]
+# configs "budget:threads", e.g. 1:128,32:128,32:256
+configs = [tuple(int(v) for v in (x.split(":") + ["128"])[:2])
+           for x in (sys.argv[2].split(",") if len(sys.argv) > 2 else ["1", "8", "32"])]
 d = np.load(Path(__file__).resolve().parents[1] / "tests" / "golden" / f"problems_{robot}.npz")
 m = robots.get(robot)
 scenes = [make_scene(robot, str(k), int(p))[0] for k, p in zip(d["kind"], d["pid"])]
-for w in budgets:
-    params = PlannerParams(workers=w)
+for w, nt in configs:
+    params = PlannerParams(workers=w, threads_per_cta=nt)
     b = planner.Batch(m, scenes, d["start"], d["goal"], params)
     b.launch()
     b.results()
@@ -30,7 +32,7 @@ for w in budgets:
     dv = np.array([r.device_time_ms for r in res])
     nodes = np.array([sum(r.tree_nodes) for r in res])
     fl = sum(r.flops for r in res)
-    print(f"{robot} budget x{w}: {dt:.2f} ms ({len(res) / dt * 1e3:.0f}/s) solved {st.mean():.3f} "
+    print(f"{robot} budget x{w} threads {nt}: {dt:.2f} ms ({len(res) / dt * 1e3:.0f}/s) solved {st.mean():.3f} "
           f"iters p50/p90/p99/max {np.percentile(it, 50):.0f}/{np.percentile(it, 90):.0f}/"
           f"{np.percentile(it, 99):.0f}/{it.max()} sum {it.sum()} | dev ms p50/p99/max "
           f"{np.median(dv):.3f}/{np.percentile(dv, 99):.3f}/{dv.max():.3f} | nodes p50/max "

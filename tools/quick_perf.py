@@ -13,7 +13,7 @@ d = np.load(Path(__file__).resolve().parents[1] / "tests" / "golden" / f"problem
 m = robots.get(robot)
 scenes = [make_scene(robot, str(k), int(p))[0] for k, p in zip(d["kind"], d["pid"])]
 S, G = d["start"], d["goal"]
-params = PlannerParams(tree_capacity=cap)
+params = PlannerParams(tree_capacity=cap, threads_per_cta=int(sys.argv[3]) if len(sys.argv) > 3 else 0)
 sel = list(range(0, len(S), max(1, len(S) // 60)))[:60]
 for w in (0, 32, 64, 148, 296, 592):
     params.workers = w
