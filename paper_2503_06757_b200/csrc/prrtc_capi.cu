@@ -820,6 +820,7 @@ int batch_enqueue(prrtc_batch* b, cudaStream_t st, bool upload) {
     a.arena_cap = b->arena;
     a.next_problem = b->d_next;
     a.n_done = b->d_ndone;
+    a.trace = reinterpret_cast<unsigned long long*>(ws->d_out + 16);
     a.epoch = ws->epoch;
     a.p.delta = b->params.delta;
     a.p.dd_radius = b->params.dd_radius > 0.0 ? b->params.dd_radius : 4.0 * b->params.delta;
@@ -890,6 +891,19 @@ int batch_collect(prrtc_batch* b, prrtc_result* out) {
     }
     float ms = 0.f;
     cudaEventElapsedTime(&ms, ws->ev0, ws->ev1);
+    if (std::getenv("PRRTC_TRACE")) {  // kernel span vs per-problem span (globaltimer)
+        const auto* tr = reinterpret_cast<const unsigned long long*>(h + 16);
+        const long long k0 = (long long)(0x7fffffffffffffffull - tr[0]), k1 = (long long)tr[1];
+        long long p0 = ctl[0].t_start_ns, p1 = ctl[0].t_end_ns;
+        for (int i = 1; i < b->n; ++i) {
+            p0 = std::min(p0, ctl[i].t_start_ns);
+            p1 = std::max(p1, ctl[i].t_end_ns);
+        }
+        std::fprintf(stderr,
+                     "prrtc trace: events %.3f ms | first CTA -> first init %.3f | inits -> last done %.3f | "
+                     "last done -> last CTA exit %.3f | grid %d x %d\n",
+                     ms, (p0 - k0) * 1e-6, (p1 - p0) * 1e-6, (k1 - p1) * 1e-6, b->grid, b->nthreads);
+    }
     for (int i = 0; i < b->n; ++i) {
         prrtc_result& r = out[i];
         std::memset(&r, 0, sizeof(r));
@@ -984,6 +998,7 @@ int prrtc_plan_batch(const prrtc_robot* robot, const prrtc_scene* const* scenes,
     const double wall =
         std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
     if (n_problems == 1) out[0].wall_time_ms = wall;
+    if (std::getenv("PRRTC_TRACE")) std::fprintf(stderr, "prrtc trace: host wall %.3f ms\n", wall);
     return PRRTC_OK;
 }
 

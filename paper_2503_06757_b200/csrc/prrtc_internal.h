@@ -131,6 +131,7 @@ struct PlanArgs {
     unsigned long long arena_cap;
     int* next_problem;         // unstarted-problem ticket
     int* n_done;               // finished problems (helpers exit when all are done)
+    unsigned long long* trace; // [2]: LLONG_MAX - first CTA start, last CTA exit (globaltimer ns)
     unsigned epoch;
     PlanParamsDev p;
     int ns_max;                // states per validation chunk

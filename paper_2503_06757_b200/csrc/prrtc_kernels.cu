@@ -548,6 +548,7 @@ __global__ void __launch_bounds__(NT, MINB) plan_kernel(PlanArgs a) {
     const int robot_words = reinterpret_cast<const int*>(a.robot)[RH_WORDS];
     unsigned char* sbase = scene_base(smem, robot_words, c.L, dof, c.NS, c.nthreads);
     const double R = a.p.dd_radius, delta = a.p.delta;
+    if (tid == 0 && a.trace) atomicMax(&a.trace[0], 0x7fffffffffffffffull - (unsigned long long)globaltimer());
 
     for (;;) {
         unsigned long long fk_states = 0, fine_states = 0;
@@ -717,6 +718,7 @@ __global__ void __launch_bounds__(NT, MINB) plan_kernel(PlanArgs a) {
         __syncthreads();
         if (a.p.deterministic && a.n_problems == 1) break;
     }
+    if (tid == 0 && a.trace) atomicMax(&a.trace[1], (unsigned long long)globaltimer());
 }
 
 // CTA size variants: 128 threads (4 warps, up to 4 CTAs/SM) and 256 threads
