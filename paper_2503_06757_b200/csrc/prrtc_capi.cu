@@ -658,6 +658,7 @@ struct prrtc_batch {
     int* d_prob_scene = nullptr;
     unsigned long long* d_arena_used = nullptr;
     int *d_next = nullptr, *d_ndone = nullptr;
+    long long* cta_trace = nullptr;  // PRRTC_TRACE only
     ProbCtl* d_ctl = nullptr;
     double* d_arena = nullptr;
 };
@@ -821,6 +822,19 @@ int batch_enqueue(prrtc_batch* b, cudaStream_t st, bool upload) {
     a.next_problem = b->d_next;
     a.n_done = b->d_ndone;
     a.trace = reinterpret_cast<unsigned long long*>(ws->d_out + 16);
+    a.cta_trace = nullptr;
+    if (std::getenv("PRRTC_TRACE")) {
+        static long long* d_ct = nullptr;
+        static int ct_cap = 0;
+        if (ct_cap < b->grid) {
+            cudaFree(d_ct);
+            cudaMalloc(&d_ct, sizeof(long long) * 4 * b->grid);
+            ct_cap = b->grid;
+        }
+        cudaMemsetAsync(d_ct, 0, sizeof(long long) * 4 * b->grid, st);
+        a.cta_trace = d_ct;
+        b->cta_trace = d_ct;
+    }
     a.epoch = ws->epoch;
     a.p.delta = b->params.delta;
     a.p.dd_radius = b->params.dd_radius > 0.0 ? b->params.dd_radius : 4.0 * b->params.delta;
@@ -903,6 +917,25 @@ int batch_collect(prrtc_batch* b, prrtc_result* out) {
                      "prrtc trace: events %.3f ms | first CTA -> first init %.3f | inits -> last done %.3f | "
                      "last done -> last CTA exit %.3f | grid %d x %d\n",
                      ms, (p0 - k0) * 1e-6, (p1 - p0) * 1e-6, (k1 - p1) * 1e-6, b->grid, b->nthreads);
+        if (b->cta_trace) {
+            std::vector<long long> ct(4 * b->grid);
+            cudaMemcpy(ct.data(), b->cta_trace, 8 * ct.size(), cudaMemcpyDeviceToHost);
+            long long max_start = 0, max_leave = 0, max_flush = 0, max_exit = 0;
+            int slow = -1;
+            for (int g = 0; g < b->grid; ++g) {
+                const long long* t = &ct[4 * g];
+                max_start = std::max(max_start, t[3] - k0);
+                if (t[0]) {
+                    if (t[0] - p1 > max_leave) { max_leave = t[0] - p1; slow = g; }
+                    max_flush = std::max(max_flush, t[1] - t[0]);
+                    max_exit = std::max(max_exit, t[2] - t[1]);
+                }
+            }
+            std::fprintf(stderr,
+                         "prrtc trace: latest CTA start +%.3f ms | latest leave after last done %.3f (CTA %d) | "
+                         "max flush+leave %.3f | max leave->exit %.3f\n",
+                         max_start * 1e-6, max_leave * 1e-6, slow, max_flush * 1e-6, max_exit * 1e-6);
+        }
     }
     for (int i = 0; i < b->n; ++i) {
         prrtc_result& r = out[i];

@@ -132,6 +132,7 @@ struct PlanArgs {
     int* next_problem;         // unstarted-problem ticket
     int* n_done;               // finished problems (helpers exit when all are done)
     unsigned long long* trace; // [2]: LLONG_MAX - first CTA start, last CTA exit (globaltimer ns)
+    long long* cta_trace;      // [grid][4]: per-CTA stamps (PRRTC_TRACE only, else null)
     unsigned epoch;
     PlanParamsDev p;
     int ns_max;                // states per validation chunk

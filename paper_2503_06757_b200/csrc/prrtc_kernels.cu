@@ -549,6 +549,7 @@ __global__ void __launch_bounds__(NT, MINB) plan_kernel(PlanArgs a) {
     unsigned char* sbase = scene_base(smem, robot_words, c.L, dof, c.NS, c.nthreads);
     const double R = a.p.dd_radius, delta = a.p.delta;
     if (tid == 0 && a.trace) atomicMax(&a.trace[0], 0x7fffffffffffffffull - (unsigned long long)globaltimer());
+    if (tid == 0 && a.cta_trace) a.cta_trace[blockIdx.x * 4 + 3] = globaltimer();
 
     for (;;) {
         unsigned long long fk_states = 0, fine_states = 0;
@@ -713,12 +714,15 @@ __global__ void __launch_bounds__(NT, MINB) plan_kernel(PlanArgs a) {
             break;
         }
         // ---- leave ----
+        if (tid == 0 && a.cta_trace) a.cta_trace[blockIdx.x * 4 + 0] = globaltimer();
         flush_stats(c, C, fk_states, fine_states);
         if (tid == 0) leave_problem(a, prob, leave_msg);
         __syncthreads();
+        if (tid == 0 && a.cta_trace) a.cta_trace[blockIdx.x * 4 + 1] = globaltimer();
         if (a.p.deterministic && a.n_problems == 1) break;
     }
     if (tid == 0 && a.trace) atomicMax(&a.trace[1], (unsigned long long)globaltimer());
+    if (tid == 0 && a.cta_trace) a.cta_trace[blockIdx.x * 4 + 2] = globaltimer();
 }
 
 // CTA size variants: 128 threads (4 warps, up to 4 CTAs/SM) and 256 threads
