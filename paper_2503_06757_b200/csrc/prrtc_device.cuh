@@ -240,8 +240,8 @@ struct Ctx {
     float* qf;       // [dof][NS]
     int* sgroup;     // [NS] group id, -1 = inactive
     int* sbad;       // [NS]
-    int* queue;      // [kQueueMax]
-    int* pqueue;     // [kQueueMax]
+    unsigned long long* lmask;  // [L][NS] coarse-flagged primitives per (link, state)
+    unsigned long long* pmask;  // [ceil(NP/64)][NS] coarse-flagged self pairs per state
     double* ends;    // [NS + 2][dof] chain points of the chunk
     int* ends_eq;    // [NS + 2] bitwise-equal sub-edge flags
     // CTA scalars
@@ -551,19 +551,22 @@ __device__ void brute_chunk(Ctx& c, StatAcc& acc, int cnt, bool early_exit, bool
 
 // ---------------------------------------------------------------------------
 // validate the chunk's states (qf/sgroup already set): FK + collision.
-// Two-stage (collision.cpp:130-204): padded coarse spheres flag
-// (state, link, primitive) triples and (state, pair) pairs into shared
-// queues; the fine stage re-tests only those. Result: sbad[], IC_FIRSTBAD.
+// Two-stage (collision.cpp:130-204): padded coarse spheres flag primitives
+// per (link, state) into 64-bit masks and self pairs per state into pair
+// masks (collision.cpp:155-183); the fine stage re-tests only what flagged
+// (collision.cpp:189-203): warps over fine spheres / pairs, lanes over
+// states, iterating the set bits. Masks cannot overflow, so no fallback is
+// ever needed. Result: sbad[], IC_FIRSTBAD, IC_QN (= anything flagged).
 // ---------------------------------------------------------------------------
 __device__ __noinline__ void check_chunk(Ctx& c, int cnt, bool two_stage, bool early_exit, bool indep) {
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nw = c.nthreads >> 5;
     const int NS = c.NS;
+    const int PW = (c.NP + 63) >> 6;
     StatAcc acc(c);
     for (int s = tid; s < NS; s += c.nthreads) c.sbad[s] = 0;
+    for (int i = tid; i < (c.L + PW) * NS; i += c.nthreads) c.lmask[i] = 0ull;  // pmask follows lmask
     if (tid == 0) {
         c.ictl[IC_QN] = 0;
-        c.ictl[IC_PQN] = 0;
-        c.ictl[IC_OVF] = 0;
         c.ictl[IC_FIRSTBAD] = kNoBad;
     }
     fk_chunk(c, cnt);  // ends with __syncthreads
@@ -575,6 +578,7 @@ __device__ __noinline__ void check_chunk(Ctx& c, int cnt, bool two_stage, bool e
     // stage 1: units (link, primitive group) over warps, states over lanes
     const int G = (c.P >= 8 && c.L < 2 * nw) ? 2 : 1;
     const int PG = (c.P + G - 1) / G;
+    int flagged = 0;
     for (int u = warp; u < c.L * G; u += nw) {
         const int l = G == 2 ? (u >> 1) : u;
         const int p0 = (u - l * G) * PG, p1 = min(c.P, p0 + PG);
@@ -583,13 +587,12 @@ __device__ __noinline__ void check_chunk(Ctx& c, int cnt, bool two_stage, bool e
         for (int s = lane; s < cnt; s += 32) {
             if (c.sgroup[s] < 0) continue;
             const float* C = c.ccen + (size_t)l * 3 * NS + s;
-            unsigned long long m = coarse_mask(c, C[0], C[NS], C[2 * NS], rc, p0, p1);
+            const unsigned long long m = coarse_mask(c, C[0], C[NS], C[2 * NS], rc, p0, p1);
             acc.t += p1 - p0;
             acc.f += fl;
-            while (m) {
-                const int p = __ffsll((long long)m) - 1;
-                m &= m - 1;
-                push(c.queue, &c.ictl[IC_QN], &c.ictl[IC_OVF], s | (l << 8) | (p << 16));
+            if (m) {
+                atomicOr(&c.lmask[l * NS + s], m);
+                flagged = 1;
             }
         }
     }
@@ -603,50 +606,60 @@ __device__ __noinline__ void check_chunk(Ctx& c, int cnt, bool two_stage, bool e
             const float dx = A[0] - B[0], dy = A[NS] - B[NS], dz = A[2 * NS] - B[2 * NS];
             ++acc.t;
             acc.f += 10;
-            if (fmaf(dx, dx, fmaf(dy, dy, dz * dz)) < rr * rr)
-                push(c.pqueue, &c.ictl[IC_PQN], &c.ictl[IC_OVF], s | (pr << 8));
+            if (fmaf(dx, dx, fmaf(dy, dy, dz * dz)) < rr * rr) {
+                atomicOr(&c.pmask[(pr >> 6) * NS + s], 1ull << (pr & 63));
+                flagged = 1;
+            }
         }
     }
-    __syncthreads();
-    if (c.ictl[IC_OVF]) {  // too many flags: exact brute force for the chunk
-        brute_chunk(c, acc, cnt, early_exit, indep);
-        __syncthreads();
-        return;
-    }
-    const int qn = c.ictl[IC_QN], pqn = c.ictl[IC_PQN];
-    if (qn == 0 && pqn == 0) return;  // nothing flagged: every state free
-    // stage 2a: flagged (state, link, prim) x fine spheres of the link
-    const int mfm = (1 << c.mflog) - 1;
-    for (int it = tid; it < (qn << c.mflog); it += c.nthreads) {
-        const int e = c.queue[it >> c.mflog], k = it & mfm;
-        const int s = e & 0xff, l = (e >> 8) & 0xff, p = e >> 16;
-        if (k >= c.nfine[l] || skip_state(c, s, early_exit, indep)) continue;
-        const int j = c.info[l].w + k;
+    if (!__syncthreads_or(flagged)) return;  // nothing flagged: every state free
+    if (tid == 0) c.ictl[IC_QN] = 1;
+    // stage 2a: fine spheres of flagged links vs the primitives that flagged them
+    for (int j = warp; j < c.S; j += nw) {
+        const int l = c.flink[j];
         const float4 f = c.fine[j];
-        const float3 x = pose_point(c, l, s, f.x, f.y, f.z);
-        ++acc.t;
-        acc.f += 18 + test_flops(c, p);
-        if (fine_vs_prim(c, x, f.w, c.fine_r64[j], p)) mark_bad(c, s);
-    }
-    // stage 2b: flagged (state, pair): fine x fine
-    for (int it = tid; it < (pqn << c.mflog); it += c.nthreads) {
-        const int e = c.pqueue[it >> c.mflog], i = it & mfm;
-        const int s = e & 0xff, pr = e >> 8;
-        const int2 ab = c.pairs[pr];
-        if (i >= c.nfine[ab.x] || skip_state(c, s, early_exit, indep)) continue;
-        const int ja = c.info[ab.x].w + i;
-        const float4 fa = c.fine[ja];
-        const float3 xa = pose_point(c, ab.x, s, fa.x, fa.y, fa.z);
-        const int nb = c.nfine[ab.y], jb0 = c.info[ab.y].w;
-        for (int k = 0; k < nb; ++k) {
-            const float4 fb = c.fine[jb0 + k];
-            const float3 xb = pose_point(c, ab.y, s, fb.x, fb.y, fb.z);
-            ++acc.t;
-            acc.f += 28;
-            if (fine_pair(c, xa, ja, xb, jb0 + k)) {
-                mark_bad(c, s);
-                break;
+        for (int s = lane; s < cnt; s += 32) {
+            unsigned long long m = c.lmask[l * NS + s];
+            if (!m || skip_state(c, s, early_exit, indep)) continue;
+            const float3 x = pose_point(c, l, s, f.x, f.y, f.z);
+            const double rd = c.fine_r64[j];
+            acc.f += 18;
+            while (m) {
+                const int p = __ffsll((long long)m) - 1;
+                m &= m - 1;
+                ++acc.t;
+                acc.f += test_flops(c, p);
+                if (fine_vs_prim(c, x, f.w, rd, p)) {
+                    mark_bad(c, s);
+                    break;
+                }
             }
+        }
+    }
+    // stage 2b: flagged (pair, state): fine x fine (collision.cpp:89-98)
+    for (int pr = warp; pr < c.NP; pr += nw) {
+        const int2 ab = c.pairs[pr];
+        const int na = c.nfine[ab.x], nb = c.nfine[ab.y];
+        const int ja0 = c.info[ab.x].w, jb0 = c.info[ab.y].w;
+        for (int s = lane; s < cnt; s += 32) {
+            if (!((c.pmask[(pr >> 6) * NS + s] >> (pr & 63)) & 1ull) || skip_state(c, s, early_exit, indep))
+                continue;
+            bool hit = false;
+            for (int i = 0; i < na && !hit; ++i) {
+                const float4 fa = c.fine[ja0 + i];
+                const float3 xa = pose_point(c, ab.x, s, fa.x, fa.y, fa.z);
+                for (int k = 0; k < nb; ++k) {
+                    const float4 fb = c.fine[jb0 + k];
+                    const float3 xb = pose_point(c, ab.y, s, fb.x, fb.y, fb.z);
+                    ++acc.t;
+                    acc.f += 28;
+                    if (fine_pair(c, xa, ja0 + i, xb, jb0 + k)) {
+                        hit = true;
+                        break;
+                    }
+                }
+            }
+            if (hit) mark_bad(c, s);
         }
     }
     __syncthreads();

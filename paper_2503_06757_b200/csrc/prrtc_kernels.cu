@@ -25,7 +25,7 @@ using namespace dev;
 // shared memory carve-up (host and device agree through smem_layout)
 // ---------------------------------------------------------------------------
 struct SmemLayout {
-    size_t robot, scene, pose, ccen, qf, sgroup, sbad, queue, pqueue, ictl, dcfg, red_d, red_i,
+    size_t robot, scene, pose, ccen, qf, sgroup, sbad, lmask, ictl, dcfg, red_d, red_i,
         ends, ends_eq, htab, total;
 };
 
@@ -42,8 +42,8 @@ __host__ __device__ inline SmemLayout smem_layout(int robot_words, int L, int do
     s.qf = o;    o = al16(o + 4 * (size_t)dof * NS);
     s.sgroup = o; o = al16(o + 4 * (size_t)NS);
     s.sbad = o;  o = al16(o + 4 * (size_t)NS);
-    s.queue = o; o = al16(o + 4 * (size_t)kQueueMax);
-    s.pqueue = o; o = al16(o + 4 * (size_t)kQueueMax);
+    // lmask [L][NS] then pmask [ceil(NP/64)][NS] (PRRTC_MAX_SELF_PAIRS = 512)
+    s.lmask = o; o = al16(o + 8 * (size_t)(L + 8) * NS);
     s.ictl = o;  o = al16(o + 4 * (size_t)IC_COUNT);
     s.dcfg = o;  o = al16(o + 8 * (size_t)8 * kMaxDof);
     s.red_d = o; o = al16(o + 8 * (size_t)(nthreads / 32));
@@ -92,8 +92,8 @@ __device__ void setup_ctx(Ctx& c, unsigned char* smem, const uint32_t* robot_g, 
     c.qf = reinterpret_cast<float*>(smem + lay.qf);
     c.sgroup = reinterpret_cast<int*>(smem + lay.sgroup);
     c.sbad = reinterpret_cast<int*>(smem + lay.sbad);
-    c.queue = reinterpret_cast<int*>(smem + lay.queue);
-    c.pqueue = reinterpret_cast<int*>(smem + lay.pqueue);
+    c.lmask = reinterpret_cast<unsigned long long*>(smem + lay.lmask);
+    c.pmask = c.lmask + (size_t)c.L * NS;
     c.ictl = reinterpret_cast<int*>(smem + lay.ictl);
     c.dcfg = reinterpret_cast<double*>(smem + lay.dcfg);
     c.red_d = reinterpret_cast<double*>(smem + lay.red_d);
@@ -253,7 +253,7 @@ __device__ long long validate_chain(Ctx& c, const PlanArgs& a, const double* A, 
             c.flops += (unsigned long long)act * c.fkflops;
         }
         check_chunk(c, cnt, a.p.two_stage != 0, a.p.early_exit != 0, false);
-        if (threadIdx.x == 0 && (c.ictl[IC_QN] | c.ictl[IC_PQN])) ++fine_states;
+        if (threadIdx.x == 0 && c.ictl[IC_QN]) ++fine_states;
         const int fb = c.ictl[IC_FIRSTBAD];
         good = (fb != kNoBad) ? (long long)fb : (g0 + cnt) / n_cc;
         __syncthreads();
@@ -479,14 +479,14 @@ __device__ int pick_help(Ctx& c, const PlanArgs& a) {
         }
         if ((tid & 31) == 0) {
             c.red_i[tid >> 5] = bp;
-            c.queue[tid >> 5] = bk;
+            c.sgroup[tid >> 5] = bk;
         }
         __syncthreads();
         if (tid == 0) {
-            int k = c.queue[0], p = c.red_i[0];
+            int k = c.sgroup[0], p = c.red_i[0];
             for (int w = 1; w < c.nthreads / 32; ++w) {
-                if (c.queue[w] < k || (c.queue[w] == k && c.red_i[w] >= 0 && (p < 0 || c.red_i[w] < p))) {
-                    k = c.queue[w];
+                if (c.sgroup[w] < k || (c.sgroup[w] == k && c.red_i[w] >= 0 && (p < 0 || c.red_i[w] < p))) {
+                    k = c.sgroup[w];
                     p = c.red_i[w];
                 }
             }
