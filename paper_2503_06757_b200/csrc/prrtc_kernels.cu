@@ -234,6 +234,10 @@ __device__ long long validate_chain(Ctx& c, const PlanArgs& a, const double* A, 
     *stopped = false;
     *last = parent0;
     for (long long g0 = 0; g0 < total; g0 += c.NS) {
+        if (threadIdx.x == 0 && a.cta_trace) {  // PRRTC_TRACE: phase 5 = validation chunk
+            a.cta_trace[blockIdx.x * 8 + 6] = 5;
+            a.cta_trace[blockIdx.x * 8 + 7] = globaltimer();
+        }
         if (done_flag) {  // stop flag (planner.cpp:112)
             if (threadIdx.x == 0) c.ictl[IC_TMP3] = ld_relaxed(done_flag);
             __syncthreads();
@@ -538,6 +542,16 @@ __device__ void leave_problem(const PlanArgs& a, int prob, int reason_msg) {
 }
 
 template <int NT, int MINB>
+// PRRTC_TRACE: last phase entered + when, and iterations, per CTA
+#define TRACE_PHASE(code)                                                            \
+    do {                                                                             \
+        if (tid == 0 && a.cta_trace) {                                               \
+            a.cta_trace[blockIdx.x * 8 + 6] = (code);                                \
+            a.cta_trace[blockIdx.x * 8 + 7] = globaltimer();                         \
+            if ((code) == 1) a.cta_trace[blockIdx.x * 8 + 5] += 1;                   \
+        }                                                                            \
+    } while (0)
+
 __global__ void __launch_bounds__(NT, MINB) plan_kernel(PlanArgs a) {
     extern __shared__ __align__(16) unsigned char smem[];
     Ctx c;
@@ -549,7 +563,7 @@ __global__ void __launch_bounds__(NT, MINB) plan_kernel(PlanArgs a) {
     unsigned char* sbase = scene_base(smem, robot_words, c.L, dof, c.NS, c.nthreads);
     const double R = a.p.dd_radius, delta = a.p.delta;
     if (tid == 0 && a.trace) atomicMax(&a.trace[0], 0x7fffffffffffffffull - (unsigned long long)globaltimer());
-    if (tid == 0 && a.cta_trace) a.cta_trace[blockIdx.x * 4 + 3] = globaltimer();
+    if (tid == 0 && a.cta_trace) a.cta_trace[blockIdx.x * 8 + 3] = globaltimer();
 
     for (;;) {
         unsigned long long fk_states = 0, fine_states = 0;
@@ -585,6 +599,7 @@ __global__ void __launch_bounds__(NT, MINB) plan_kernel(PlanArgs a) {
         int leave_msg = MSG_NONE;
         for (;;) {
             // ---- iteration header (lead thread) ----
+            TRACE_PHASE(1);
             if (tid == 0) {
                 // one global ticket per iteration is both the budget counter
                 // and the Halton index (no stride-W bias);
@@ -626,6 +641,7 @@ __global__ void __launch_bounds__(NT, MINB) plan_kernel(PlanArgs a) {
             }
             __syncthreads();
             // ---- nearest neighbour in the extended tree ----
+            TRACE_PHASE(2);
             const NnOut nr = nn_scan(c, Ts.cfg, a.stride, snap, smp);
             const int nn = nr.index;
             const double d2 = nr.d2;
@@ -645,6 +661,7 @@ __global__ void __launch_bounds__(NT, MINB) plan_kernel(PlanArgs a) {
             }
             __syncthreads();
             // ---- SIMT edge validation nn -> c_new, then append ----
+            TRACE_PHASE(3);
             int last = nn;
             bool stopped = false;
             const long long ok = validate_chain(c, a, nnc, cnew, 1, &Ts, nn, &last, nullptr,
@@ -659,6 +676,7 @@ __global__ void __launch_bounds__(NT, MINB) plan_kernel(PlanArgs a) {
             }
             const int new_idx = last;
             // ---- greedy connect toward the opposite tree ----
+            TRACE_PHASE(4);
             if (tid == 0) c.ictl[IC_TMP2] = ld_acquire(To.published);
             __syncthreads();
             const int snap_o = c.ictl[IC_TMP2];
@@ -691,6 +709,7 @@ __global__ void __launch_bounds__(NT, MINB) plan_kernel(PlanArgs a) {
             }
             if (!reached) continue;
             // ---- winner (planner.cpp:232-238) ----
+            TRACE_PHASE(6);
             if (tid == 0) c.ictl[IC_TMP6] = (atomicCAS(&C.winner, 0, blockIdx.x + 1) == 0);
             __syncthreads();
             if (c.ictl[IC_TMP6]) {
@@ -714,15 +733,15 @@ __global__ void __launch_bounds__(NT, MINB) plan_kernel(PlanArgs a) {
             break;
         }
         // ---- leave ----
-        if (tid == 0 && a.cta_trace) a.cta_trace[blockIdx.x * 4 + 0] = globaltimer();
+        if (tid == 0 && a.cta_trace) a.cta_trace[blockIdx.x * 8 + 0] = globaltimer();
         flush_stats(c, C, fk_states, fine_states);
         if (tid == 0) leave_problem(a, prob, leave_msg);
         __syncthreads();
-        if (tid == 0 && a.cta_trace) a.cta_trace[blockIdx.x * 4 + 1] = globaltimer();
+        if (tid == 0 && a.cta_trace) a.cta_trace[blockIdx.x * 8 + 1] = globaltimer();
         if (a.p.deterministic && a.n_problems == 1) break;
     }
     if (tid == 0 && a.trace) atomicMax(&a.trace[1], (unsigned long long)globaltimer());
-    if (tid == 0 && a.cta_trace) a.cta_trace[blockIdx.x * 4 + 2] = globaltimer();
+    if (tid == 0 && a.cta_trace) a.cta_trace[blockIdx.x * 8 + 2] = globaltimer();
 }
 
 // CTA size variants: 128 threads (4 warps, up to 4 CTAs/SM) and 256 threads
