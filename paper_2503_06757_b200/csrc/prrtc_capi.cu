@@ -828,10 +828,10 @@ int batch_enqueue(prrtc_batch* b, cudaStream_t st, bool upload) {
         static int ct_cap = 0;
         if (ct_cap < b->grid) {
             cudaFree(d_ct);
-            cudaMalloc(&d_ct, sizeof(long long) * 8 * b->grid);
+            cudaMalloc(&d_ct, sizeof(long long) * 32 * b->grid);
             ct_cap = b->grid;
         }
-        cudaMemsetAsync(d_ct, 0, sizeof(long long) * 8 * b->grid, st);
+        cudaMemsetAsync(d_ct, 0, sizeof(long long) * 32 * b->grid, st);
         a.cta_trace = d_ct;
         b->cta_trace = d_ct;
     }
@@ -918,12 +918,12 @@ int batch_collect(prrtc_batch* b, prrtc_result* out) {
                      "last done -> last CTA exit %.3f | grid %d x %d\n",
                      ms, (p0 - k0) * 1e-6, (p1 - p0) * 1e-6, (k1 - p1) * 1e-6, b->grid, b->nthreads);
         if (b->cta_trace) {
-            std::vector<long long> ct(8 * b->grid);
+            std::vector<long long> ct(32 * b->grid);
             cudaMemcpy(ct.data(), b->cta_trace, 8 * ct.size(), cudaMemcpyDeviceToHost);
             long long max_start = 0, max_leave = 0, max_flush = 0, max_exit = 0;
             int slow = -1;
             for (int g = 0; g < b->grid; ++g) {
-                const long long* t = &ct[8 * g];
+                const long long* t = &ct[32 * g];
                 max_start = std::max(max_start, t[3] - k0);
                 if (t[0]) {
                     if (t[0] - p1 > max_leave) { max_leave = t[0] - p1; slow = g; }
@@ -936,10 +936,16 @@ int batch_collect(prrtc_batch* b, prrtc_result* out) {
                          "max flush+leave %.3f | max leave->exit %.3f\n",
                          max_start * 1e-6, max_leave * 1e-6, slow, max_flush * 1e-6, max_exit * 1e-6);
             if (slow >= 0) {
-                const long long* t = &ct[8 * slow];
+                const long long* t = &ct[32 * slow];
                 std::fprintf(stderr, "prrtc trace: slow CTA %d: iterations %lld, last phase %lld entered %.3f ms "
                                      "before leaving (%.3f ms after last done)\n",
                              slow, t[5], t[6], (t[0] - t[7]) * 1e-6, (t[7] - p1) * 1e-6);
+                std::fprintf(stderr, "prrtc trace: slow CTA events (phase@ms rel. first init):");
+                const long long nev = std::min<long long>(t[4], 12);
+                for (long long e = t[4] - nev; e < t[4]; ++e)
+                    std::fprintf(stderr, " %lld@%.3f", t[8 + 2 * (e % 12)], (t[9 + 2 * (e % 12)] - p0) * 1e-6);
+                std::fprintf(stderr, " | start@%.3f leave@%.3f done@%.3f\n", (t[3] - p0) * 1e-6,
+                             (t[0] - p0) * 1e-6, (p1 - p0) * 1e-6);
             }
         }
     }

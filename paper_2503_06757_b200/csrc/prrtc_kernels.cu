@@ -157,6 +157,20 @@ struct TreeRef {
     int* published;
 };
 
+// PRRTC_TRACE: last phase entered + when, iterations, and a ring of the
+// last 12 (phase, time) events per CTA (slots 8..31)
+__device__ __forceinline__ void trace_phase(const PlanArgs& a, int code) {
+    if (threadIdx.x != 0 || !a.cta_trace) return;
+    long long* t = a.cta_trace + blockIdx.x * 32;
+    const long long now = globaltimer();
+    t[6] = code;
+    t[7] = now;
+    if (code == 1) t[5] += 1;
+    const long long k = t[4]++;
+    t[8 + 2 * (k % 12)] = code;
+    t[9 + 2 * (k % 12)] = now;
+}
+
 __device__ __forceinline__ TreeRef tree_ref(const PlanArgs& a, int prob, int t, int dof) {
     TreeRef r;
     const size_t pt = (size_t)prob * 2 + t;
@@ -234,10 +248,7 @@ __device__ long long validate_chain(Ctx& c, const PlanArgs& a, const double* A, 
     *stopped = false;
     *last = parent0;
     for (long long g0 = 0; g0 < total; g0 += c.NS) {
-        if (threadIdx.x == 0 && a.cta_trace) {  // PRRTC_TRACE: phase 5 = validation chunk
-            a.cta_trace[blockIdx.x * 8 + 6] = 5;
-            a.cta_trace[blockIdx.x * 8 + 7] = globaltimer();
-        }
+        trace_phase(a, 5);  // PRRTC_TRACE: validation chunk
         if (done_flag) {  // stop flag (planner.cpp:112)
             if (threadIdx.x == 0) c.ictl[IC_TMP3] = ld_relaxed(done_flag);
             __syncthreads();
@@ -541,17 +552,9 @@ __device__ void leave_problem(const PlanArgs& a, int prob, int reason_msg) {
     }
 }
 
-template <int NT, int MINB>
-// PRRTC_TRACE: last phase entered + when, and iterations, per CTA
-#define TRACE_PHASE(code)                                                            \
-    do {                                                                             \
-        if (tid == 0 && a.cta_trace) {                                               \
-            a.cta_trace[blockIdx.x * 8 + 6] = (code);                                \
-            a.cta_trace[blockIdx.x * 8 + 7] = globaltimer();                         \
-            if ((code) == 1) a.cta_trace[blockIdx.x * 8 + 5] += 1;                   \
-        }                                                                            \
-    } while (0)
+#define TRACE_PHASE(code) trace_phase(a, code)
 
+template <int NT, int MINB>
 __global__ void __launch_bounds__(NT, MINB) plan_kernel(PlanArgs a) {
     extern __shared__ __align__(16) unsigned char smem[];
     Ctx c;
@@ -563,7 +566,7 @@ __global__ void __launch_bounds__(NT, MINB) plan_kernel(PlanArgs a) {
     unsigned char* sbase = scene_base(smem, robot_words, c.L, dof, c.NS, c.nthreads);
     const double R = a.p.dd_radius, delta = a.p.delta;
     if (tid == 0 && a.trace) atomicMax(&a.trace[0], 0x7fffffffffffffffull - (unsigned long long)globaltimer());
-    if (tid == 0 && a.cta_trace) a.cta_trace[blockIdx.x * 8 + 3] = globaltimer();
+    if (tid == 0 && a.cta_trace) a.cta_trace[blockIdx.x * 32 + 3] = globaltimer();
 
     for (;;) {
         unsigned long long fk_states = 0, fine_states = 0;
@@ -733,15 +736,15 @@ __global__ void __launch_bounds__(NT, MINB) plan_kernel(PlanArgs a) {
             break;
         }
         // ---- leave ----
-        if (tid == 0 && a.cta_trace) a.cta_trace[blockIdx.x * 8 + 0] = globaltimer();
+        if (tid == 0 && a.cta_trace) a.cta_trace[blockIdx.x * 32 + 0] = globaltimer();
         flush_stats(c, C, fk_states, fine_states);
         if (tid == 0) leave_problem(a, prob, leave_msg);
         __syncthreads();
-        if (tid == 0 && a.cta_trace) a.cta_trace[blockIdx.x * 8 + 1] = globaltimer();
+        if (tid == 0 && a.cta_trace) a.cta_trace[blockIdx.x * 32 + 1] = globaltimer();
         if (a.p.deterministic && a.n_problems == 1) break;
     }
     if (tid == 0 && a.trace) atomicMax(&a.trace[1], (unsigned long long)globaltimer());
-    if (tid == 0 && a.cta_trace) a.cta_trace[blockIdx.x * 8 + 2] = globaltimer();
+    if (tid == 0 && a.cta_trace) a.cta_trace[blockIdx.x * 32 + 2] = globaltimer();
 }
 
 // CTA size variants: 128 threads (4 warps, up to 4 CTAs/SM) and 256 threads
