@@ -211,16 +211,30 @@ __device__ int tree_append_many(Ctx& c, const PlanArgs& a, const TreeRef& T, con
     }
     __threadfence();  // data and flags before the publishing CAS
     __syncthreads();
-    if (tid == 0 && ok > 0) {
-        int p = atomicCAS(T.published, (int)s0, (int)(s0 + ok));
-        if (p == s0) {
-            // our block is published; carry on over successors that finished first
-            p = (int)(s0 + ok);
+    if (tid < 32 && ok > 0) {  // warp 0 publishes
+        const int lane = tid;
+        int won = 0;
+        if (lane == 0) won = atomicCAS(T.published, (int)s0, (int)(s0 + ok)) == s0;
+        won = __shfl_sync(0xffffffffu, won, 0);
+        if (won) {
+            // our block is published; carry `published` over the successors
+            // that finished first: 32 ready flags per step, one CAS per run
+            // (a burst of concurrent appends otherwise costs one acquire load +
+            // CAS round trip per slot)
+            int p = (int)(s0 + ok);
             __threadfence();
-            while (p < a.cap && ld_acquire_u(&T.ready[p]) == a.epoch) {
-                const int old = atomicCAS(T.published, p, p + 1);
+            while (p < a.cap) {
+                const long long idx = (long long)p + lane;
+                const bool r = idx < a.cap && ld_acquire_u(&T.ready[idx]) == a.epoch;
+                const unsigned m = __ballot_sync(0xffffffffu, r);
+                const int run = (m == 0xffffffffu) ? 32 : (__ffs(~m) - 1);
+                if (run == 0) break;
+                int old = 0;
+                if (lane == 0) old = atomicCAS(T.published, p, p + run);
+                old = __shfl_sync(0xffffffffu, old, 0);
                 if (old != p) break;  // another writer is advancing
-                ++p;
+                p += run;
+                if (run < 32) break;
             }
         }
     }
