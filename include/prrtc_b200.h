@@ -267,6 +267,14 @@ int prrtc_debug_halton(const uint32_t* bases, const uint64_t* indices, uint32_t 
    index0 .. index0+n-1 against the robot's limits. */
 int prrtc_debug_sample(const prrtc_robot* robot, uint64_t index0, uint32_t n, double* out);
 
+/* clock64 stamps of one 32-state validation chunk in one CTA (latency
+   profiling): [0] kernel start, [7] after setup, [8] after state generation,
+   [1] check start, [2] FK local transforms, [3] FK compose, [4] FK done,
+   [5] coarse stage done, [6] fine env stage done (if reached), [9] chunk done. */
+int prrtc_debug_chunk_profile(const prrtc_robot* robot, const prrtc_scene* scene, const double* from,
+                              const double* to, uint32_t dof, int32_t n_cc, int two_stage,
+                              long long* stamps);
+
 /* ---------------- measurement utility ---------------- */
 /* FP32 FMA-pipe peak of the device in TFLOP/s, measured with an FFMA-chain
    microbenchmark (the roofline denominator of the FK / collision work). */

@@ -127,6 +127,8 @@ SIGNATURES = [
     ("prrtc_debug_nn", C.c_int, [DP, C.c_uint32, C.c_uint32, DP, C.c_uint32, C.c_int, C.POINTER(C.c_uint32), DP]),
     ("prrtc_debug_halton", C.c_int, [C.POINTER(C.c_uint32), C.POINTER(C.c_uint64), C.c_uint32, C.c_int, DP]),
     ("prrtc_debug_sample", C.c_int, [P, C.c_uint64, C.c_uint32, DP]),
+    ("prrtc_debug_chunk_profile", C.c_int, [P, P, DP, DP, C.c_uint32, C.c_int32, C.c_int,
+                                           C.POINTER(C.c_longlong)]),
     ("prrtc_fp32_peak_tflops", C.c_double, [C.c_int]),
 ]
 

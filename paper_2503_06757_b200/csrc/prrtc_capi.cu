@@ -1234,6 +1234,36 @@ int prrtc_debug_halton(const uint32_t* bases, const uint64_t* indices, uint32_t 
     return PRRTC_OK;
 }
 
+int prrtc_debug_chunk_profile(const prrtc_robot* robot, const prrtc_scene* scene, const double* from,
+                              const double* to, uint32_t dof, int32_t n_cc, int two_stage,
+                              long long* stamps) {
+    if (!robot || !scene || !from || !to || !stamps) return set_err(PRRTC_EINVAL, "prrtc_debug_chunk_profile: null argument");
+    if ((int)dof != robot->dof) return set_err(PRRTC_EINVAL, "prrtc_debug_chunk_profile: dimension");
+    int rc = check_device(robot->device);
+    if (rc) return rc;
+    cudaSetDevice(robot->device);
+    double *df = nullptr, *dt = nullptr;
+    uint8_t* dv = nullptr;
+    long long* dp = nullptr;
+    if ((rc = dmalloc(&df, dof)) || (rc = dmalloc(&dt, dof)) || (rc = dmalloc(&dv, 1)) || (rc = dmalloc(&dp, 16))) {
+        cudaFree(df);
+        cudaFree(dt);
+        cudaFree(dv);
+        return rc;
+    }
+    cudaMemcpy(df, from, 8 * dof, cudaMemcpyHostToDevice);
+    cudaMemcpy(dt, to, 8 * dof, cudaMemcpyHostToDevice);
+    cudaMemset(dp, 0, 16 * 8);
+    cudaError_t e = launch_validate_edges(robot->args(), scene->args(), df, dt, 1, n_cc, two_stage, 1, dv, 0, dp);
+    if (e == cudaSuccess) e = cudaMemcpy(stamps, dp, 16 * 8, cudaMemcpyDeviceToHost);
+    cudaFree(df);
+    cudaFree(dt);
+    cudaFree(dv);
+    cudaFree(dp);
+    if (e != cudaSuccess) return set_err(PRRTC_ECUDA, std::string("prrtc_debug_chunk_profile: ") + cudaGetErrorString(e));
+    return PRRTC_OK;
+}
+
 double prrtc_fp32_peak_tflops(int device) {
     if (check_device(device)) return 0.0;
     cudaSetDevice(device);

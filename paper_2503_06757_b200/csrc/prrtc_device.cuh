@@ -226,6 +226,7 @@ struct Ctx {
     const double* limits;    // global [dof][2]
     unsigned fkflops;        // per-state FK + coarse posing flops
     int nnpar;               // nn_scan buffer parity
+    long long* prof;         // per-phase clock64 stamps (debug hook only, else null)
     // scene (shared memory copy)
     int ns, nb, nc, P;
     const float4* sph;
@@ -337,6 +338,7 @@ __device__ __noinline__ void fk_chunk(Ctx& c, int cnt) {
         }
     }
     __syncthreads();
+    if (c.prof && tid == 0) c.prof[2] = clock64();
     // phase B: lanes (s, r), r in 0..3 (r == 3 idle), whole warps iterate
     const int per = c.nthreads / 4;
     for (int sb = 0; sb < cnt; sb += per) {
@@ -371,6 +373,7 @@ __device__ __noinline__ void fk_chunk(Ctx& c, int cnt) {
         }
     }
     __syncthreads();
+    if (c.prof && tid == 0) c.prof[3] = clock64();
     // phase C: coarse centers
     for (int l = warp; l < c.L; l += nw) {
         const float* g = c.geo + l * GEO_STRIDE;
@@ -569,7 +572,9 @@ __device__ __noinline__ void check_chunk(Ctx& c, int cnt, bool two_stage, bool e
         c.ictl[IC_QN] = 0;
         c.ictl[IC_FIRSTBAD] = kNoBad;
     }
+    if (c.prof && tid == 0) c.prof[1] = clock64();
     fk_chunk(c, cnt);  // ends with __syncthreads
+    if (c.prof && tid == 0) c.prof[4] = clock64();
     if (!two_stage) {
         brute_chunk(c, acc, cnt, early_exit, indep);
         __syncthreads();
@@ -612,7 +617,9 @@ __device__ __noinline__ void check_chunk(Ctx& c, int cnt, bool two_stage, bool e
             }
         }
     }
-    if (!__syncthreads_or(flagged)) return;  // nothing flagged: every state free
+    const int any_flag = __syncthreads_or(flagged);
+    if (c.prof && tid == 0) c.prof[5] = clock64();
+    if (!any_flag) return;  // nothing flagged: every state free
     if (tid == 0) c.ictl[IC_QN] = 1;
     // stage 2a: fine spheres of flagged links vs the primitives that flagged them
     for (int j = warp; j < c.S; j += nw) {
@@ -635,6 +642,10 @@ __device__ __noinline__ void check_chunk(Ctx& c, int cnt, bool two_stage, bool e
                 }
             }
         }
+    }
+    if (c.prof) {
+        __syncthreads();
+        if (tid == 0) c.prof[6] = clock64();
     }
     // stage 2b: flagged (pair, state): fine x fine (collision.cpp:89-98)
     for (int pr = warp; pr < c.NP; pr += nw) {

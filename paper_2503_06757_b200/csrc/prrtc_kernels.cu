@@ -115,6 +115,7 @@ __device__ void setup_ctx(Ctx& c, unsigned char* smem, const uint32_t* robot_g, 
     c.flops = 0;
     c.fkflops = rw[RH_FKFLOPS];
     c.nnpar = 0;
+    c.prof = nullptr;
     c.ns = c.nb = c.nc = c.P = 0;  // scene pointers are wired by load_scene
 }
 
@@ -813,11 +814,17 @@ __global__ void __launch_bounds__(128) check_configs_kernel(RobotArgs r, SceneAr
 __global__ void __launch_bounds__(128) validate_edges_kernel(RobotArgs r, SceneArgs sa, const double* from,
                                                               const double* to, int n_edges, int n_cc,
                                                               int two_stage, int early_exit,
-                                                              uint8_t* out, int NS) {
+                                                              uint8_t* out, int NS, long long* prof) {
     extern __shared__ __align__(16) unsigned char smem[];
+    const long long t0 = clock64();
     Ctx c;
     setup_ctx(c, smem, r.words, r.n_words, r.fine_r64, r.limits, NS);
     load_scene(c, scene_base(smem, r.n_words, c.L, c.dof, NS, c.nthreads), sa.words, sa.f64);
+    c.prof = (prof && blockIdx.x == 0) ? prof : nullptr;  // debug hook: phase stamps
+    if (c.prof && threadIdx.x == 0) {
+        c.prof[0] = t0;
+        c.prof[7] = clock64();
+    }
     for (int e = blockIdx.x; e < n_edges; e += gridDim.x) {
         double* A = dc(c, DC_A);
         double* B = dc(c, DC_B);
@@ -830,9 +837,12 @@ __global__ void __launch_bounds__(128) validate_edges_kernel(RobotArgs r, SceneA
         for (long long g0 = 0; g0 < n_cc && !(bad && early_exit); g0 += NS) {
             const int cnt = (int)min((long long)NS, n_cc - g0);
             gen_chain_states(c, A, B, 1, n_cc, g0, cnt);
+            if (c.prof && threadIdx.x == 0) c.prof[8] = clock64();
             check_chunk(c, cnt, two_stage != 0, early_exit != 0, false);
             bad |= c.ictl[IC_FIRSTBAD] != kNoBad;
             __syncthreads();
+            if (c.prof && threadIdx.x == 0) c.prof[9] = clock64();
+            c.prof = nullptr;  // first chunk only
         }
         if (threadIdx.x == 0) out[e] = bad ? 0 : 1;
         __syncthreads();
@@ -1003,7 +1013,7 @@ cudaError_t launch_check_configs(const RobotArgs& r, const SceneArgs& s, const d
 
 cudaError_t launch_validate_edges(const RobotArgs& r, const SceneArgs& s, const double* from,
                                   const double* to, int n_edges, int n_cc, int two_stage,
-                                  int early_exit, uint8_t* out, cudaStream_t st) {
+                                  int early_exit, uint8_t* out, cudaStream_t st, long long* prof) {
     const int NS = chunk_states();
     const size_t sm = smem_bytes(r, NS, 128);
     cudaError_t e = cudaFuncSetAttribute(validate_edges_kernel,
@@ -1012,7 +1022,7 @@ cudaError_t launch_validate_edges(const RobotArgs& r, const SceneArgs& s, const 
     const int grid = (int)min((long long)n_edges, 148LL * 16);
     if (grid > 0)
         validate_edges_kernel<<<grid, 128, sm, st>>>(r, s, from, to, n_edges, n_cc, two_stage,
-                                                     early_exit, out, NS);
+                                                     early_exit, out, NS, prof);
     return cudaGetLastError();
 }
 
