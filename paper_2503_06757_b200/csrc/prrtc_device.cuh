@@ -22,8 +22,8 @@ namespace prrtc_b200 {
 namespace dev {
 
 constexpr int kMaxDof = 32;
-constexpr int kQueueMax = 512;
 constexpr int kNoBad = 0x7fffffff;
+constexpr int kTTab = 128;  // edge-sample fraction table covers n_cc <= 128
 
 // ---------------------------------------------------------------------------
 // memory-model helpers (gpu scope)
@@ -227,6 +227,8 @@ struct Ctx {
     unsigned fkflops;        // per-state FK + coarse posing flops
     int nnpar;               // nn_scan buffer parity
     long long* prof;         // per-phase clock64 stamps (debug hook only, else null)
+    double* ttab;            // [kTTab + 1]: i / ttab_n for i = 0..ttab_n (edge sample fractions)
+    int ttab_n;              // n_cc the table was built for (0 = none)
     // scene (shared memory copy)
     int ns, nb, nc, P;
     const float4* sph;
@@ -339,38 +341,71 @@ __device__ __noinline__ void fk_chunk(Ctx& c, int cnt) {
     }
     __syncthreads();
     if (c.prof && tid == 0) c.prof[2] = clock64();
-    // phase B: lanes (s, r), r in 0..3 (r == 3 idle), whole warps iterate
+    // phase B: lanes (s, r), r in 0..3 (r == 3 idle), whole warps iterate.
+    // Each lane carries its world row of the previous link in registers (the
+    // parent in a chain) and prefetches the next link's local transform, so
+    // one __syncwarp per link orders "all lanes read local l" before "lanes
+    // overwrite their row of link l".
     const int per = c.nthreads / 4;
     for (int sb = 0; sb < cnt; sb += per) {
         const int s = sb + tid / 4, r = tid & 3;
         const bool act = (s < cnt) && (r < 3);
-        for (int l = 0; l < c.L; ++l) {
-            const int par = c.info[l].y;
-            if (par < 0) continue;  // warp-uniform
-            float Rl[9], tl[3];
+        const int rr = r < 3 ? r : 0;
+        float w0 = 0.f, w1 = 0.f, w2 = 0.f, wt = 0.f;  // world row rr of link wl
+        int wl = -1;
+        float Rl[9], tl[3];
+        auto load_local = [&](int l) {
             const float* P = c.pose + (size_t)l * 12 * NS + s;
-            if (act) {
 #pragma unroll
-                for (int k = 0; k < 9; ++k) Rl[k] = P[k * NS];
-                tl[0] = P[9 * NS];
-                tl[1] = P[10 * NS];
-                tl[2] = P[11 * NS];
-            }
-            __syncwarp();
-            if (act) {
-                const float* Q = c.pose + (size_t)par * 12 * NS + s;
-                const float a0 = Q[(3 * r + 0) * NS], a1 = Q[(3 * r + 1) * NS],
-                            a2 = Q[(3 * r + 2) * NS], tp = Q[(9 + r) * NS];
-                float* W = c.pose + (size_t)l * 12 * NS + s;
-#pragma unroll
-                for (int j = 0; j < 3; ++j) {
-                    W[(3 * r + j) * NS] =
-                        __fmaf_rn(a0, Rl[j], __fmaf_rn(a1, Rl[3 + j], __fmul_rn(a2, Rl[6 + j])));
+            for (int k = 0; k < 9; ++k) Rl[k] = act ? P[k * NS] : 0.f;
+            tl[0] = act ? P[9 * NS] : 0.f;
+            tl[1] = act ? P[10 * NS] : 0.f;
+            tl[2] = act ? P[11 * NS] : 0.f;
+        };
+        if (c.L > 0) load_local(0);
+        for (int l = 0; l < c.L; ++l) {
+            const int par = c.info[l].y;  // warp-uniform
+            float n0, n1, n2, nt;
+            if (par < 0) {  // root: world = local
+                n0 = Rl[3 * rr];
+                n1 = Rl[3 * rr + 1];
+                n2 = Rl[3 * rr + 2];
+                nt = tl[rr];
+            } else {
+                float a0, a1, a2, tp;
+                if (par == wl) {
+                    a0 = w0;
+                    a1 = w1;
+                    a2 = w2;
+                    tp = wt;
+                } else {  // branch point: the parent's row was written by this lane
+                    const float* Q = c.pose + (size_t)par * 12 * NS + s;
+                    a0 = act ? Q[(3 * rr + 0) * NS] : 0.f;
+                    a1 = act ? Q[(3 * rr + 1) * NS] : 0.f;
+                    a2 = act ? Q[(3 * rr + 2) * NS] : 0.f;
+                    tp = act ? Q[(9 + rr) * NS] : 0.f;
                 }
-                W[(9 + r) * NS] = __fmaf_rn(a0, tl[0], __fmaf_rn(a1, tl[1], __fmaf_rn(a2, tl[2], tp)));
+                n0 = __fmaf_rn(a0, Rl[0], __fmaf_rn(a1, Rl[3], __fmul_rn(a2, Rl[6])));
+                n1 = __fmaf_rn(a0, Rl[1], __fmaf_rn(a1, Rl[4], __fmul_rn(a2, Rl[7])));
+                n2 = __fmaf_rn(a0, Rl[2], __fmaf_rn(a1, Rl[5], __fmul_rn(a2, Rl[8])));
+                nt = __fmaf_rn(a0, tl[0], __fmaf_rn(a1, tl[1], __fmaf_rn(a2, tl[2], tp)));
             }
-            __syncwarp();
+            __syncwarp();  // every lane has read local l (prefetched last iteration)
+            if (act && par >= 0) {
+                float* W = c.pose + (size_t)l * 12 * NS + s;
+                W[(3 * r + 0) * NS] = n0;
+                W[(3 * r + 1) * NS] = n1;
+                W[(3 * r + 2) * NS] = n2;
+                W[(9 + r) * NS] = nt;
+            }
+            w0 = n0;
+            w1 = n1;
+            w2 = n2;
+            wt = nt;
+            wl = l;
+            if (l + 1 < c.L) load_local(l + 1);  // a different link: no hazard
         }
+        __syncwarp();
     }
     __syncthreads();
     if (c.prof && tid == 0) c.prof[3] = clock64();
@@ -433,6 +468,7 @@ __device__ __forceinline__ unsigned long long coarse_mask(const Ctx& c, float x,
     unsigned long long m = 0;
     const int e1 = min(p1, c.ns), e2 = min(p1, c.ns + c.nb);
     int p = p0;
+#pragma unroll 2
     for (; p < e1; ++p) {
         float d2;
         const float4 s = c.sph[p];
@@ -440,11 +476,13 @@ __device__ __forceinline__ unsigned long long coarse_mask(const Ctx& c, float x,
         const float rr = rc + s.w;
         if (d2 < rr * rr) m |= 1ull << p;
     }
+#pragma unroll 2
     for (; p < e2; ++p) {
         float d2;
         box_d2(x, y, z, c.box + (p - c.ns) * BOX_STRIDE, d2);
         if (d2 < rc * rc) m |= 1ull << p;
     }
+#pragma unroll 2
     for (; p < p1; ++p) {
         float d2;
         const float* C = c.cap + (p - c.ns - c.nb) * CAP_STRIDE;
@@ -484,10 +522,16 @@ __device__ __forceinline__ bool skip_state(const Ctx& c, int s, bool early_exit,
     return c.sgroup[s] >= *(volatile int*)&c.ictl[IC_FIRSTBAD];
 }
 
-__device__ __forceinline__ void push(int* q, int* qn, int* ovf, int val) {
-    const int pos = atomicAdd(qn, 1);
-    if (pos < kQueueMax) q[pos] = val;
-    else *ovf = 1;
+// i / n for i = 0..n (edge_sample's t, collision.cpp:19) tabulated once per
+// CTA with the same IEEE division, so a state costs no FP64 divide.
+__device__ void build_ttab(Ctx& c, int n_cc) {
+    if (n_cc < 1 || n_cc > kTTab) {
+        c.ttab_n = 0;
+        return;
+    }
+    for (int i = threadIdx.x; i <= n_cc; i += c.nthreads) c.ttab[i] = __ddiv_rn((double)i, (double)n_cc);
+    c.ttab_n = n_cc;
+    __syncthreads();
 }
 
 // ---------------------------------------------------------------------------
@@ -656,9 +700,21 @@ __device__ __noinline__ void check_chunk(Ctx& c, int cnt, bool two_stage, bool e
             if (!((c.pmask[(pr >> 6) * NS + s] >> (pr & 63)) & 1ull) || skip_state(c, s, early_exit, indep))
                 continue;
             bool hit = false;
+            // fine spheres of a that cannot reach b's (padded) coarse sphere
+            // cannot hit any fine sphere of b (coarse contains fine,
+            // kinematics.cpp:56-57): skip them before the fine x fine loop
+            const float* CB = c.ccen + (size_t)ab.y * 3 * NS + s;
+            const float cbx = CB[0], cby = CB[NS], cbz = CB[2 * NS];
+            const float rcb = c.geo[ab.y * GEO_STRIDE + 36] + 2.0f * c.cpad;
             for (int i = 0; i < na && !hit; ++i) {
                 const float4 fa = c.fine[ja0 + i];
                 const float3 xa = pose_point(c, ab.x, s, fa.x, fa.y, fa.z);
+                {
+                    const float dx = xa.x - cbx, dy = xa.y - cby, dz = xa.z - cbz;
+                    const float rr = fa.w + rcb;
+                    acc.f += 10;
+                    if (!(fmaf(dx, dx, fmaf(dy, dy, dz * dz)) < rr * rr)) continue;
+                }
                 for (int k = 0; k < nb; ++k) {
                     const float4 fb = c.fine[jb0 + k];
                     const float3 xb = pose_point(c, ab.y, s, fb.x, fb.y, fb.z);
@@ -728,7 +784,7 @@ __device__ void gen_chain_states(Ctx& c, const double* A, const double* B, long 
         if (i == n_cc) {
             for (int d = 0; d < dof; ++d) c.qf[d * c.NS + s] = (float)T[d];
         } else {
-            const double t = __ddiv_rn((double)i, inv_n);
+            const double t = n_cc == c.ttab_n ? c.ttab[i] : __ddiv_rn((double)i, inv_n);
             for (int d = 0; d < dof; ++d) c.qf[d * c.NS + s] = (float)lerp_exact(F[d], T[d], t);
         }
         c.sgroup[s] = (int)k;

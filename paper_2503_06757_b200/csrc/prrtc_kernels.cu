@@ -26,7 +26,7 @@ using namespace dev;
 // ---------------------------------------------------------------------------
 struct SmemLayout {
     size_t robot, scene, pose, ccen, qf, sgroup, sbad, lmask, ictl, dcfg, red_d, red_i,
-        ends, ends_eq, htab, total;
+        ends, ends_eq, htab, ttab, total;
 };
 
 __host__ __device__ inline size_t al16(size_t x) { return (x + 15) & ~size_t(15); }
@@ -51,6 +51,7 @@ __host__ __device__ inline SmemLayout smem_layout(int robot_words, int L, int do
     s.ends = o;  o = al16(o + 8 * (size_t)(NS + 2) * dof);
     s.ends_eq = o; o = al16(o + 4 * (size_t)(NS + 2));
     s.htab = o;  o = al16(o + 8 * (size_t)dof * kHaltonTab);
+    s.ttab = o;  o = al16(o + 8 * (size_t)(kTTab + 1));
     s.total = o;
     return s;
 }
@@ -101,6 +102,8 @@ __device__ void setup_ctx(Ctx& c, unsigned char* smem, const uint32_t* robot_g, 
     c.ends = reinterpret_cast<double*>(smem + lay.ends);
     c.ends_eq = reinterpret_cast<int*>(smem + lay.ends_eq);
     c.htab = reinterpret_cast<double*>(smem + lay.htab);
+    c.ttab = reinterpret_cast<double*>(smem + lay.ttab);
+    c.ttab_n = 0;
     for (int d = tid; d < c.dof; d += c.nthreads) {  // f_k of halton_value (sampling.cpp:12)
         double f = 1.0;
         for (int k = 0; k < kHaltonTab; ++k) {
@@ -579,6 +582,7 @@ __global__ void __launch_bounds__(NT, MINB) plan_kernel(PlanArgs a) {
     const int dof = c.dof;
     const int robot_words = reinterpret_cast<const int*>(a.robot)[RH_WORDS];
     unsigned char* sbase = scene_base(smem, robot_words, c.L, dof, c.NS, c.nthreads);
+    build_ttab(c, a.p.n_cc);
     const double R = a.p.dd_radius, delta = a.p.delta;
     if (tid == 0 && a.trace) atomicMax(&a.trace[0], 0x7fffffffffffffffull - (unsigned long long)globaltimer());
     if (tid == 0 && a.cta_trace) a.cta_trace[blockIdx.x * 32 + 3] = globaltimer();
@@ -820,6 +824,7 @@ __global__ void __launch_bounds__(128) validate_edges_kernel(RobotArgs r, SceneA
     Ctx c;
     setup_ctx(c, smem, r.words, r.n_words, r.fine_r64, r.limits, NS);
     load_scene(c, scene_base(smem, r.n_words, c.L, c.dof, NS, c.nthreads), sa.words, sa.f64);
+    build_ttab(c, n_cc);
     c.prof = (prof && blockIdx.x == 0) ? prof : nullptr;  // debug hook: phase stamps
     if (c.prof && threadIdx.x == 0) {
         c.prof[0] = t0;
