@@ -258,6 +258,33 @@ struct Ctx {
     unsigned long long flops;  // algorithmic FP32 flops
 };
 
+// The Ctx lives in the kernel's local-memory frame, so a pointer read from it
+// is generic: loads through it become LD.E (not LDS) and every store through
+// it may alias the frame, forcing the other fields to be re-read. sh()
+// re-derives the pointer from the dynamic shared-memory symbol, which lets the
+// compiler prove the shared address space (LDS/STS, no aliasing with local
+// memory). Hot routines take their pointers into registers through it once.
+extern __shared__ __align__(16) unsigned char g_dsmem[];
+template <class T>
+__device__ __forceinline__ T* sh(T* p) {
+    // integer offsets in the shared window (no cross-object pointer arithmetic)
+    const unsigned off = (unsigned)__cvta_generic_to_shared(p) - (unsigned)__cvta_generic_to_shared(g_dsmem);
+    return reinterpret_cast<T*>(g_dsmem + off);
+}
+
+// Register-resident view of the scene (shared-memory pointers + scalars).
+struct SceneV {
+    const float4* sph;
+    const float* box;
+    const float* cap;
+    int ns, nb, P;
+    float eps;
+    SceneF64 s64;
+};
+__device__ __forceinline__ SceneV scene_view(const Ctx& c) {
+    return SceneV{sh(c.sph), sh(c.box), sh(c.cap), c.ns, c.nb, c.P, c.eps, c.s64};
+}
+
 // ictl slots
 enum : int {
     IC_QN = 0,      // env queue length
@@ -280,19 +307,22 @@ enum : int {
 // dcfg rows
 enum : int { DC_A = 0, DC_B, DC_SAMPLE, DC_NEW, DC_NN, DC_TARGET, DC_TMP, DC_TMP2 };
 
-__device__ __forceinline__ double* dc(Ctx& c, int row) { return c.dcfg + row * kMaxDof; }
+__device__ __forceinline__ double* dc(Ctx& c, int row) { return sh(c.dcfg) + row * kMaxDof; }
 
 // Posed point R*p + t from a pose stored as [12][NS] column (state s).
 // Explicit fmaf order: identical bits wherever it is used (FK parity).
-__device__ __forceinline__ float3 pose_point(const Ctx& c, int l, int s, float px, float py,
-                                             float pz) {
-    const float* P = c.pose + (size_t)l * 12 * c.NS + s;
-    const int N = c.NS;
+__device__ __forceinline__ float3 pose_pt(const float* pose, int N, int l, int s, float px, float py,
+                                          float pz) {
+    const float* P = pose + l * 12 * N + s;
     float3 o;
     o.x = __fmaf_rn(P[0 * N], px, __fmaf_rn(P[1 * N], py, __fmaf_rn(P[2 * N], pz, P[9 * N])));
     o.y = __fmaf_rn(P[3 * N], px, __fmaf_rn(P[4 * N], py, __fmaf_rn(P[5 * N], pz, P[10 * N])));
     o.z = __fmaf_rn(P[6 * N], px, __fmaf_rn(P[7 * N], py, __fmaf_rn(P[8 * N], pz, P[11 * N])));
     return o;
+}
+__device__ __forceinline__ float3 pose_point(const Ctx& c, int l, int s, float px, float py,
+                                             float pz) {
+    return pose_pt(sh(c.pose), c.NS, l, s, px, py, pz);
 }
 
 // ---------------------------------------------------------------------------
@@ -305,14 +335,20 @@ __device__ __forceinline__ float3 pose_point(const Ctx& c, int l, int s, float p
 // ---------------------------------------------------------------------------
 __device__ __noinline__ void fk_chunk(Ctx& c, int cnt) {
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nw = c.nthreads >> 5;
-    const int NS = c.NS;
-    for (int l = warp; l < c.L; l += nw) {
-        const int4 inf = c.info[l];
-        const float* g = c.geo + l * GEO_STRIDE;
+    const int NS = c.NS, L = c.L, nthreads = c.nthreads;
+    float* const pose = sh(c.pose);
+    const float* const qf = sh(c.qf);
+    const int4* const info = sh(c.info);
+    const float* const geo = sh(c.geo);
+    float* const ccen = sh(c.ccen);
+    long long* const prof = c.prof;
+    for (int l = warp; l < L; l += nw) {
+        const int4 inf = info[l];
+        const float* g = geo + l * GEO_STRIDE;
         for (int s = lane; s < cnt; s += 32) {
-            float* P = c.pose + (size_t)l * 12 * NS + s;
+            float* P = pose + l * 12 * NS + s;
             if (inf.x == PRRTC_JOINT_REVOLUTE) {
-                const float q = c.qf[inf.z * NS + s];
+                const float q = qf[inf.z * NS + s];
                 float sn, cs;
                 sincosf(q, &sn, &cs);
                 const float omc = 1.0f - cs;
@@ -327,7 +363,7 @@ __device__ __noinline__ void fk_chunk(Ctx& c, int cnt) {
 #pragma unroll
                 for (int k = 0; k < 9; ++k) P[k * NS] = g[k];
                 if (inf.x == PRRTC_JOINT_PRISMATIC) {
-                    const float q = c.qf[inf.z * NS + s];
+                    const float q = qf[inf.z * NS + s];
                     P[9 * NS] = __fmaf_rn(g[30], q, g[27]);
                     P[10 * NS] = __fmaf_rn(g[31], q, g[28]);
                     P[11 * NS] = __fmaf_rn(g[32], q, g[29]);
@@ -340,37 +376,38 @@ __device__ __noinline__ void fk_chunk(Ctx& c, int cnt) {
         }
     }
     __syncthreads();
-    if (c.prof && tid == 0) c.prof[2] = clock64();
+    if (prof && tid == 0) prof[2] = clock64();
     // phase B: lanes (s, r), r in 0..3 (r == 3 idle), whole warps iterate.
     // Each lane carries its world row of the previous link in registers (the
     // parent in a chain) and prefetches the next link's local transform, so
     // one __syncwarp per link orders "all lanes read local l" before "lanes
-    // overwrite their row of link l".
-    const int per = c.nthreads / 4;
+    // overwrite their row of link l". Idle lanes read state 0, row 0.
+    const int per = nthreads / 4;
     for (int sb = 0; sb < cnt; sb += per) {
         const int s = sb + tid / 4, r = tid & 3;
         const bool act = (s < cnt) && (r < 3);
-        const int rr = r < 3 ? r : 0;
+        const int sr = act ? s : 0, rr = act ? r : 0;
         float w0 = 0.f, w1 = 0.f, w2 = 0.f, wt = 0.f;  // world row rr of link wl
         int wl = -1;
         float Rl[9], tl[3];
         auto load_local = [&](int l) {
-            const float* P = c.pose + (size_t)l * 12 * NS + s;
+            const float* P = pose + l * 12 * NS + sr;
 #pragma unroll
-            for (int k = 0; k < 9; ++k) Rl[k] = act ? P[k * NS] : 0.f;
-            tl[0] = act ? P[9 * NS] : 0.f;
-            tl[1] = act ? P[10 * NS] : 0.f;
-            tl[2] = act ? P[11 * NS] : 0.f;
+            for (int k = 0; k < 9; ++k) Rl[k] = P[k * NS];
+            tl[0] = P[9 * NS];
+            tl[1] = P[10 * NS];
+            tl[2] = P[11 * NS];
         };
-        if (c.L > 0) load_local(0);
-        for (int l = 0; l < c.L; ++l) {
-            const int par = c.info[l].y;  // warp-uniform
+        if (L > 0) load_local(0);
+        for (int l = 0; l < L; ++l) {
+            const int par = info[l].y;  // warp-uniform
             float n0, n1, n2, nt;
-            if (par < 0) {  // root: world = local
-                n0 = Rl[3 * rr];
-                n1 = Rl[3 * rr + 1];
-                n2 = Rl[3 * rr + 2];
-                nt = tl[rr];
+            if (par < 0) {  // root: world = local, row rr read in place
+                const float* P = pose + l * 12 * NS + sr;
+                n0 = P[(3 * rr + 0) * NS];
+                n1 = P[(3 * rr + 1) * NS];
+                n2 = P[(3 * rr + 2) * NS];
+                nt = P[(9 + rr) * NS];
             } else {
                 float a0, a1, a2, tp;
                 if (par == wl) {
@@ -379,11 +416,11 @@ __device__ __noinline__ void fk_chunk(Ctx& c, int cnt) {
                     a2 = w2;
                     tp = wt;
                 } else {  // branch point: the parent's row was written by this lane
-                    const float* Q = c.pose + (size_t)par * 12 * NS + s;
-                    a0 = act ? Q[(3 * rr + 0) * NS] : 0.f;
-                    a1 = act ? Q[(3 * rr + 1) * NS] : 0.f;
-                    a2 = act ? Q[(3 * rr + 2) * NS] : 0.f;
-                    tp = act ? Q[(9 + rr) * NS] : 0.f;
+                    const float* Q = pose + par * 12 * NS + sr;
+                    a0 = Q[(3 * rr + 0) * NS];
+                    a1 = Q[(3 * rr + 1) * NS];
+                    a2 = Q[(3 * rr + 2) * NS];
+                    tp = Q[(9 + rr) * NS];
                 }
                 n0 = __fmaf_rn(a0, Rl[0], __fmaf_rn(a1, Rl[3], __fmul_rn(a2, Rl[6])));
                 n1 = __fmaf_rn(a0, Rl[1], __fmaf_rn(a1, Rl[4], __fmul_rn(a2, Rl[7])));
@@ -392,7 +429,7 @@ __device__ __noinline__ void fk_chunk(Ctx& c, int cnt) {
             }
             __syncwarp();  // every lane has read local l (prefetched last iteration)
             if (act && par >= 0) {
-                float* W = c.pose + (size_t)l * 12 * NS + s;
+                float* W = pose + l * 12 * NS + s;
                 W[(3 * r + 0) * NS] = n0;
                 W[(3 * r + 1) * NS] = n1;
                 W[(3 * r + 2) * NS] = n2;
@@ -403,18 +440,19 @@ __device__ __noinline__ void fk_chunk(Ctx& c, int cnt) {
             w2 = n2;
             wt = nt;
             wl = l;
-            if (l + 1 < c.L) load_local(l + 1);  // a different link: no hazard
+            if (l + 1 < L) load_local(l + 1);  // a different link: no hazard
         }
         __syncwarp();
     }
     __syncthreads();
-    if (c.prof && tid == 0) c.prof[3] = clock64();
+    if (prof && tid == 0) prof[3] = clock64();
     // phase C: coarse centers
-    for (int l = warp; l < c.L; l += nw) {
-        const float* g = c.geo + l * GEO_STRIDE;
+    for (int l = warp; l < L; l += nw) {
+        const float* g = geo + l * GEO_STRIDE;
+        const float gx = g[33], gy = g[34], gz = g[35];
         for (int s = lane; s < cnt; s += 32) {
-            const float3 o = pose_point(c, l, s, g[33], g[34], g[35]);
-            float* C = c.ccen + (size_t)l * 3 * NS + s;
+            const float3 o = pose_pt(pose, NS, l, s, gx, gy, gz);
+            float* C = ccen + l * 3 * NS + s;
             C[0] = o.x;
             C[NS] = o.y;
             C[2 * NS] = o.z;
@@ -427,51 +465,53 @@ __device__ __noinline__ void fk_chunk(Ctx& c, int cnt) {
 // exact fine-sphere vs primitive (p indexes spheres, boxes, capsules in that
 // order). FP32 with guard band, FP64 exact fallback on the same inputs.
 // ---------------------------------------------------------------------------
-__device__ __forceinline__ bool fine_vs_prim(const Ctx& c, float3 x, float rf, double rd, int p) {
+__device__ __forceinline__ bool fine_vs_prim(const SceneV& v, float3 x, float rf, double rd, int p) {
     float d2, rr;
-    int v;
-    if (p < c.ns) {
-        const float4 s = c.sph[p];
+    int b;
+    if (p < v.ns) {
+        const float4 s = v.sph[p];
         sph_d2(x.x, x.y, x.z, s, d2);
         rr = rf + s.w;
-        v = band(d2, rr, c.eps);
-        if (v >= 0) return v != 0;
-        const double* S = c.s64.s + 4 * p;
-        return sphere_sphere_exact(x.x, x.y, x.z, rd, S[0], S[1], S[2], S[3]);
-    } else if (p < c.ns + c.nb) {
-        const int b = p - c.ns;
-        box_d2(x.x, x.y, x.z, c.box + b * BOX_STRIDE, d2);
-        v = band(d2, rf, c.eps);
-        if (v >= 0) return v != 0;
-        return sphere_box_exact(x.x, x.y, x.z, rd, c.s64.b + BOX_STRIDE * b);
+        b = band(d2, rr, v.eps);
+        if (b >= 0) return b != 0;
+        // the FP64 mirror is global: __ldg pins the address space (a plain
+        // load here was mis-inferred as shared next to the sh() pointers)
+        const double* S = v.s64.s + 4 * p;
+        return sphere_sphere_exact(x.x, x.y, x.z, rd, __ldg(S), __ldg(S + 1), __ldg(S + 2), __ldg(S + 3));
+    } else if (p < v.ns + v.nb) {
+        const int k = p - v.ns;
+        box_d2(x.x, x.y, x.z, v.box + k * BOX_STRIDE, d2);
+        b = band(d2, rf, v.eps);
+        if (b >= 0) return b != 0;
+        return sphere_box_exact(x.x, x.y, x.z, rd, v.s64.b + BOX_STRIDE * k);
     } else {
-        const int k = p - c.ns - c.nb;
-        const float* C = c.cap + k * CAP_STRIDE;
+        const int k = p - v.ns - v.nb;
+        const float* C = v.cap + k * CAP_STRIDE;
         cap_d2(x.x, x.y, x.z, C, d2);
         rr = rf + C[7];
-        v = band(d2, rr, c.eps);
-        if (v >= 0) return v != 0;
-        return sphere_capsule_exact(x.x, x.y, x.z, rd, c.s64.c + CAP_STRIDE * k);
+        b = band(d2, rr, v.eps);
+        if (b >= 0) return b != 0;
+        return sphere_capsule_exact(x.x, x.y, x.z, rd, v.s64.c + CAP_STRIDE * k);
     }
 }
 
 // algorithmic flops of one sphere test (kernels_detail.hpp:17-50 counted:
 // mul/add/sub = 1, FMA = 2): sphere 10, box 27, capsule 22
-__device__ __forceinline__ int test_flops(const Ctx& c, int p) {
-    return p < c.ns ? 10 : (p < c.ns + c.nb ? 27 : 22);
+__device__ __forceinline__ int test_flops(const SceneV& v, int p) {
+    return p < v.ns ? 10 : (p < v.ns + v.nb ? 27 : 22);
 }
 
 // coarse (padded) sphere vs primitives [p0, p1): hit bitmask, FP32 only
 // (conservative: the padding covers FP32 error, so no fine hit is missed)
-__device__ __forceinline__ unsigned long long coarse_mask(const Ctx& c, float x, float y, float z,
+__device__ __forceinline__ unsigned long long coarse_mask(const SceneV& v, float x, float y, float z,
                                                           float rc, int p0, int p1) {
     unsigned long long m = 0;
-    const int e1 = min(p1, c.ns), e2 = min(p1, c.ns + c.nb);
+    const int e1 = min(p1, v.ns), e2 = min(p1, v.ns + v.nb);
     int p = p0;
 #pragma unroll 2
     for (; p < e1; ++p) {
         float d2;
-        const float4 s = c.sph[p];
+        const float4 s = v.sph[p];
         sph_d2(x, y, z, s, d2);
         const float rr = rc + s.w;
         if (d2 < rr * rr) m |= 1ull << p;
@@ -479,13 +519,13 @@ __device__ __forceinline__ unsigned long long coarse_mask(const Ctx& c, float x,
 #pragma unroll 2
     for (; p < e2; ++p) {
         float d2;
-        box_d2(x, y, z, c.box + (p - c.ns) * BOX_STRIDE, d2);
+        box_d2(x, y, z, v.box + (p - v.ns) * BOX_STRIDE, d2);
         if (d2 < rc * rc) m |= 1ull << p;
     }
 #pragma unroll 2
     for (; p < p1; ++p) {
         float d2;
-        const float* C = c.cap + (p - c.ns - c.nb) * CAP_STRIDE;
+        const float* C = v.cap + (p - v.ns - v.nb) * CAP_STRIDE;
         cap_d2(x, y, z, C, d2);
         const float rr = rc + C[7];
         if (d2 < rr * rr) m |= 1ull << p;
@@ -493,33 +533,41 @@ __device__ __forceinline__ unsigned long long coarse_mask(const Ctx& c, float x,
     return m;
 }
 
-__device__ __forceinline__ int range_flops(const Ctx& c, int p0, int p1) {
-    const int e1 = min(p1, c.ns), e2 = min(p1, c.ns + c.nb);
+__device__ __forceinline__ int range_flops(const SceneV& v, int p0, int p1) {
+    const int e1 = min(p1, v.ns), e2 = min(p1, v.ns + v.nb);
     return 10 * max(0, e1 - p0) + 27 * max(0, e2 - max(p0, e1)) + 22 * max(0, p1 - max(p0, e2));
 }
 
 // self pair fine spheres (collision.cpp:89-98 / kernels_detail.hpp:17-23)
-__device__ __forceinline__ bool fine_pair(const Ctx& c, float3 a, int ja, float3 b, int jb) {
+__device__ __forceinline__ bool fine_pair(float eps, const double* fine_r64, float3 a, float ra, int ja,
+                                          float3 b, float rb, int jb) {
     float d2;
-    const float4 fa = c.fine[ja], fb = c.fine[jb];
     sph_d2(a.x, a.y, a.z, make_float4(b.x, b.y, b.z, 0.f), d2);
-    const int v = band(d2, fa.w + fb.w, c.eps);
+    const int v = band(d2, ra + rb, eps);
     if (v >= 0) return v != 0;
-    return sphere_sphere_exact(a.x, a.y, a.z, c.fine_r64[ja], b.x, b.y, b.z, c.fine_r64[jb]);
+    return sphere_sphere_exact(a.x, a.y, a.z, __ldg(fine_r64 + ja), b.x, b.y, b.z, __ldg(fine_r64 + jb));
 }
 
-__device__ __forceinline__ void mark_bad(Ctx& c, int s) {
-    c.sbad[s] = 1;
-    atomicMin(&c.ictl[IC_FIRSTBAD], c.sgroup[s]);
+// Per-chunk state arrays in registers (shared-memory pointers).
+struct ChunkV {
+    int* sbad;
+    int* sgroup;
+    int* ictl;
+};
+__device__ __forceinline__ ChunkV chunk_view(const Ctx& c) { return ChunkV{sh(c.sbad), sh(c.sgroup), sh(c.ictl)}; }
+
+__device__ __forceinline__ void mark_bad(const ChunkV& k, int s) {
+    k.sbad[s] = 1;
+    atomicMin(&k.ictl[IC_FIRSTBAD], k.sgroup[s]);
 }
 
 // skip test for early exit: chain mode skips groups >= first bad (a state
 // of a later or the same sub-edge cannot change the outcome); independent
 // mode skips states already known bad.
-__device__ __forceinline__ bool skip_state(const Ctx& c, int s, bool early_exit, bool indep) {
+__device__ __forceinline__ bool skip_state(const ChunkV& k, int s, bool early_exit, bool indep) {
     if (!early_exit) return false;
-    if (indep) return *(volatile int*)&c.sbad[s] != 0;
-    return c.sgroup[s] >= *(volatile int*)&c.ictl[IC_FIRSTBAD];
+    if (indep) return *(volatile int*)&k.sbad[s] != 0;
+    return k.sgroup[s] >= *(volatile int*)&k.ictl[IC_FIRSTBAD];
 }
 
 // i / n for i = 0..n (edge_sample's t, collision.cpp:19) tabulated once per
@@ -529,7 +577,8 @@ __device__ void build_ttab(Ctx& c, int n_cc) {
         c.ttab_n = 0;
         return;
     }
-    for (int i = threadIdx.x; i <= n_cc; i += c.nthreads) c.ttab[i] = __ddiv_rn((double)i, (double)n_cc);
+    double* tt = sh(c.ttab);
+    for (int i = threadIdx.x; i <= n_cc; i += c.nthreads) tt[i] = __ddiv_rn((double)i, (double)n_cc);
     c.ttab_n = n_cc;
     __syncthreads();
 }
@@ -552,46 +601,56 @@ struct StatAcc {
 
 __device__ void brute_chunk(Ctx& c, StatAcc& acc, int cnt, bool early_exit, bool indep) {
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nw = c.nthreads >> 5;
-    for (int j = warp; j < c.S; j += nw) {
-        const int l = c.flink[j];
-        const float4 f = c.fine[j];
-        const double rd = c.fine_r64[j];
+    const int NS = c.NS, S = c.S, NP = c.NP;
+    const SceneV v = scene_view(c);
+    const ChunkV k = chunk_view(c);
+    const float* const pose = sh(c.pose);
+    const float4* const fine = sh(c.fine);
+    const int* const flink = sh(c.flink);
+    const int4* const info = sh(c.info);
+    const int* const nfine = sh(c.nfine);
+    const int2* const pairs = sh(c.pairs);
+    const double* const fine_r64 = c.fine_r64;
+    for (int j = warp; j < S; j += nw) {
+        const int l = flink[j];
+        const float4 f = fine[j];
+        const double rd = __ldg(fine_r64 + j);
         for (int s = lane; s < cnt; s += 32) {
-            if (c.sgroup[s] < 0 || skip_state(c, s, early_exit, indep)) continue;
-            const float3 x = pose_point(c, l, s, f.x, f.y, f.z);
-            for (int p = 0; p < c.P; ++p) {
+            if (k.sgroup[s] < 0 || skip_state(k, s, early_exit, indep)) continue;
+            const float3 x = pose_pt(pose, NS, l, s, f.x, f.y, f.z);
+            for (int p = 0; p < v.P; ++p) {
                 ++acc.t;
-                acc.f += test_flops(c, p);
-                if (fine_vs_prim(c, x, f.w, rd, p)) {
-                    mark_bad(c, s);
+                acc.f += test_flops(v, p);
+                if (fine_vs_prim(v, x, f.w, rd, p)) {
+                    mark_bad(k, s);
                     if (early_exit) break;
                 }
             }
             acc.f += 18;
         }
     }
-    for (int pr = warp; pr < c.NP; pr += nw) {
-        const int2 ab = c.pairs[pr];
-        const int na = c.nfine[ab.x], nb = c.nfine[ab.y];
-        const int ja0 = c.info[ab.x].w, jb0 = c.info[ab.y].w;
+    for (int pr = warp; pr < NP; pr += nw) {
+        const int2 ab = pairs[pr];
+        const int na = nfine[ab.x], nb = nfine[ab.y];
+        const int ja0 = info[ab.x].w, jb0 = info[ab.y].w;
         for (int s = lane; s < cnt; s += 32) {
-            if (c.sgroup[s] < 0 || skip_state(c, s, early_exit, indep)) continue;
+            if (k.sgroup[s] < 0 || skip_state(k, s, early_exit, indep)) continue;
             bool hit = false;
             for (int i = 0; i < na && !(hit && early_exit); ++i) {
-                const float4 fa = c.fine[ja0 + i];
-                const float3 xa = pose_point(c, ab.x, s, fa.x, fa.y, fa.z);
-                for (int k = 0; k < nb; ++k) {
-                    const float4 fb = c.fine[jb0 + k];
-                    const float3 xb = pose_point(c, ab.y, s, fb.x, fb.y, fb.z);
+                const float4 fa = fine[ja0 + i];
+                const float3 xa = pose_pt(pose, NS, ab.x, s, fa.x, fa.y, fa.z);
+                for (int q = 0; q < nb; ++q) {
+                    const float4 fb = fine[jb0 + q];
+                    const float3 xb = pose_pt(pose, NS, ab.y, s, fb.x, fb.y, fb.z);
                     ++acc.t;
                     acc.f += 28;
-                    if (fine_pair(c, xa, ja0 + i, xb, jb0 + k)) {
+                    if (fine_pair(v.eps, fine_r64, xa, fa.w, ja0 + i, xb, fb.w, jb0 + q)) {
                         hit = true;
                         if (early_exit) break;
                     }
                 }
             }
-            if (hit) mark_bad(c, s);
+            if (hit) mark_bad(k, s);
         }
     }
 }
@@ -607,126 +666,141 @@ __device__ void brute_chunk(Ctx& c, StatAcc& acc, int cnt, bool early_exit, bool
 // ---------------------------------------------------------------------------
 __device__ __noinline__ void check_chunk(Ctx& c, int cnt, bool two_stage, bool early_exit, bool indep) {
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nw = c.nthreads >> 5;
-    const int NS = c.NS;
-    const int PW = (c.NP + 63) >> 6;
+    const int NS = c.NS, L = c.L, NP = c.NP, S = c.S, nthreads = c.nthreads;
+    const int PW = (NP + 63) >> 6;
+    const ChunkV k = chunk_view(c);
+    unsigned long long* const lmask = sh(c.lmask);
+    unsigned long long* const pmask = sh(c.pmask);
+    long long* const prof = c.prof;
     StatAcc acc(c);
-    for (int s = tid; s < NS; s += c.nthreads) c.sbad[s] = 0;
-    for (int i = tid; i < (c.L + PW) * NS; i += c.nthreads) c.lmask[i] = 0ull;  // pmask follows lmask
+    for (int s = tid; s < NS; s += nthreads) k.sbad[s] = 0;
+    for (int i = tid; i < (L + PW) * NS; i += nthreads) lmask[i] = 0ull;  // pmask follows lmask
     if (tid == 0) {
-        c.ictl[IC_QN] = 0;
-        c.ictl[IC_FIRSTBAD] = kNoBad;
+        k.ictl[IC_QN] = 0;
+        k.ictl[IC_FIRSTBAD] = kNoBad;
     }
-    if (c.prof && tid == 0) c.prof[1] = clock64();
+    if (prof && tid == 0) prof[1] = clock64();
     fk_chunk(c, cnt);  // ends with __syncthreads
-    if (c.prof && tid == 0) c.prof[4] = clock64();
+    if (prof && tid == 0) prof[4] = clock64();
     if (!two_stage) {
         brute_chunk(c, acc, cnt, early_exit, indep);
         __syncthreads();
         return;
     }
+    const SceneV v = scene_view(c);
+    const float* const pose = sh(c.pose);
+    const float* const ccen = sh(c.ccen);
+    const float* const geo = sh(c.geo);
+    const float4* const fine = sh(c.fine);
+    const int* const flink = sh(c.flink);
+    const int4* const info = sh(c.info);
+    const int* const nfine = sh(c.nfine);
+    const int2* const pairs = sh(c.pairs);
+    const double* const fine_r64 = c.fine_r64;
+    const float cpad = c.cpad;
     // stage 1: units (link, primitive group) over warps, states over lanes
-    const int G = (c.P >= 8 && c.L < 2 * nw) ? 2 : 1;
-    const int PG = (c.P + G - 1) / G;
+    const int G = (v.P >= 8 && L < 2 * nw) ? 2 : 1;
+    const int PG = (v.P + G - 1) / G;
     int flagged = 0;
-    for (int u = warp; u < c.L * G; u += nw) {
+    for (int u = warp; u < L * G; u += nw) {
         const int l = G == 2 ? (u >> 1) : u;
-        const int p0 = (u - l * G) * PG, p1 = min(c.P, p0 + PG);
-        const float rc = c.geo[l * GEO_STRIDE + 36] + c.cpad;
-        const int fl = range_flops(c, p0, p1);
+        const int p0 = (u - l * G) * PG, p1 = min(v.P, p0 + PG);
+        const float rc = geo[l * GEO_STRIDE + 36] + cpad;
+        const int fl = range_flops(v, p0, p1);
         for (int s = lane; s < cnt; s += 32) {
-            if (c.sgroup[s] < 0) continue;
-            const float* C = c.ccen + (size_t)l * 3 * NS + s;
-            const unsigned long long m = coarse_mask(c, C[0], C[NS], C[2 * NS], rc, p0, p1);
+            if (k.sgroup[s] < 0) continue;
+            const float* C = ccen + l * 3 * NS + s;
+            const unsigned long long m = coarse_mask(v, C[0], C[NS], C[2 * NS], rc, p0, p1);
             acc.t += p1 - p0;
             acc.f += fl;
             if (m) {
-                atomicOr(&c.lmask[l * NS + s], m);
+                atomicOr(&lmask[l * NS + s], m);
                 flagged = 1;
             }
         }
     }
-    for (int pr = warp; pr < c.NP; pr += nw) {
-        const int2 ab = c.pairs[pr];
-        const float rr = c.geo[ab.x * GEO_STRIDE + 36] + c.geo[ab.y * GEO_STRIDE + 36] + 2.0f * c.cpad;
+    for (int pr = warp; pr < NP; pr += nw) {
+        const int2 ab = pairs[pr];
+        const float rr = geo[ab.x * GEO_STRIDE + 36] + geo[ab.y * GEO_STRIDE + 36] + 2.0f * cpad;
         for (int s = lane; s < cnt; s += 32) {
-            if (c.sgroup[s] < 0) continue;
-            const float* A = c.ccen + (size_t)ab.x * 3 * NS + s;
-            const float* B = c.ccen + (size_t)ab.y * 3 * NS + s;
+            if (k.sgroup[s] < 0) continue;
+            const float* A = ccen + ab.x * 3 * NS + s;
+            const float* B = ccen + ab.y * 3 * NS + s;
             const float dx = A[0] - B[0], dy = A[NS] - B[NS], dz = A[2 * NS] - B[2 * NS];
             ++acc.t;
             acc.f += 10;
             if (fmaf(dx, dx, fmaf(dy, dy, dz * dz)) < rr * rr) {
-                atomicOr(&c.pmask[(pr >> 6) * NS + s], 1ull << (pr & 63));
+                atomicOr(&pmask[(pr >> 6) * NS + s], 1ull << (pr & 63));
                 flagged = 1;
             }
         }
     }
     const int any_flag = __syncthreads_or(flagged);
-    if (c.prof && tid == 0) c.prof[5] = clock64();
+    if (prof && tid == 0) prof[5] = clock64();
     if (!any_flag) return;  // nothing flagged: every state free
-    if (tid == 0) c.ictl[IC_QN] = 1;
+    if (tid == 0) k.ictl[IC_QN] = 1;
     // stage 2a: fine spheres of flagged links vs the primitives that flagged them
-    for (int j = warp; j < c.S; j += nw) {
-        const int l = c.flink[j];
-        const float4 f = c.fine[j];
+    for (int j = warp; j < S; j += nw) {
+        const int l = flink[j];
+        const float4 f = fine[j];
         for (int s = lane; s < cnt; s += 32) {
-            unsigned long long m = c.lmask[l * NS + s];
-            if (!m || skip_state(c, s, early_exit, indep)) continue;
-            const float3 x = pose_point(c, l, s, f.x, f.y, f.z);
-            const double rd = c.fine_r64[j];
+            unsigned long long m = lmask[l * NS + s];
+            if (!m || skip_state(k, s, early_exit, indep)) continue;
+            const float3 x = pose_pt(pose, NS, l, s, f.x, f.y, f.z);
+            const double rd = __ldg(fine_r64 + j);
             acc.f += 18;
             while (m) {
                 const int p = __ffsll((long long)m) - 1;
                 m &= m - 1;
                 ++acc.t;
-                acc.f += test_flops(c, p);
-                if (fine_vs_prim(c, x, f.w, rd, p)) {
-                    mark_bad(c, s);
+                acc.f += test_flops(v, p);
+                if (fine_vs_prim(v, x, f.w, rd, p)) {
+                    mark_bad(k, s);
                     break;
                 }
             }
         }
     }
-    if (c.prof) {
+    if (prof) {
         __syncthreads();
-        if (tid == 0) c.prof[6] = clock64();
+        if (tid == 0) prof[6] = clock64();
     }
     // stage 2b: flagged (pair, state): fine x fine (collision.cpp:89-98)
-    for (int pr = warp; pr < c.NP; pr += nw) {
-        const int2 ab = c.pairs[pr];
-        const int na = c.nfine[ab.x], nb = c.nfine[ab.y];
-        const int ja0 = c.info[ab.x].w, jb0 = c.info[ab.y].w;
+    for (int pr = warp; pr < NP; pr += nw) {
+        const int2 ab = pairs[pr];
+        const int na = nfine[ab.x], nb = nfine[ab.y];
+        const int ja0 = info[ab.x].w, jb0 = info[ab.y].w;
+        const float rcb = geo[ab.y * GEO_STRIDE + 36] + 2.0f * cpad;
         for (int s = lane; s < cnt; s += 32) {
-            if (!((c.pmask[(pr >> 6) * NS + s] >> (pr & 63)) & 1ull) || skip_state(c, s, early_exit, indep))
+            if (!((pmask[(pr >> 6) * NS + s] >> (pr & 63)) & 1ull) || skip_state(k, s, early_exit, indep))
                 continue;
             bool hit = false;
             // fine spheres of a that cannot reach b's (padded) coarse sphere
             // cannot hit any fine sphere of b (coarse contains fine,
             // kinematics.cpp:56-57): skip them before the fine x fine loop
-            const float* CB = c.ccen + (size_t)ab.y * 3 * NS + s;
+            const float* CB = ccen + ab.y * 3 * NS + s;
             const float cbx = CB[0], cby = CB[NS], cbz = CB[2 * NS];
-            const float rcb = c.geo[ab.y * GEO_STRIDE + 36] + 2.0f * c.cpad;
             for (int i = 0; i < na && !hit; ++i) {
-                const float4 fa = c.fine[ja0 + i];
-                const float3 xa = pose_point(c, ab.x, s, fa.x, fa.y, fa.z);
+                const float4 fa = fine[ja0 + i];
+                const float3 xa = pose_pt(pose, NS, ab.x, s, fa.x, fa.y, fa.z);
                 {
                     const float dx = xa.x - cbx, dy = xa.y - cby, dz = xa.z - cbz;
                     const float rr = fa.w + rcb;
                     acc.f += 10;
                     if (!(fmaf(dx, dx, fmaf(dy, dy, dz * dz)) < rr * rr)) continue;
                 }
-                for (int k = 0; k < nb; ++k) {
-                    const float4 fb = c.fine[jb0 + k];
-                    const float3 xb = pose_point(c, ab.y, s, fb.x, fb.y, fb.z);
+                for (int q = 0; q < nb; ++q) {
+                    const float4 fb = fine[jb0 + q];
+                    const float3 xb = pose_pt(pose, NS, ab.y, s, fb.x, fb.y, fb.z);
                     ++acc.t;
                     acc.f += 28;
-                    if (fine_pair(c, xa, ja0 + i, xb, jb0 + k)) {
+                    if (fine_pair(v.eps, fine_r64, xa, fa.w, ja0 + i, xb, fb.w, jb0 + q)) {
                         hit = true;
                         break;
                     }
                 }
             }
-            if (hit) mark_bad(c, s);
+            if (hit) mark_bad(k, s);
         }
     }
     __syncthreads();
@@ -748,48 +822,55 @@ __device__ __forceinline__ double chain_point(const double* A, const double* B, 
     return lerp_exact(A[d], B[d], __ddiv_rn((double)k, (double)n));
 }
 
-__device__ void gen_chain_states(Ctx& c, const double* A, const double* B, long long n_sub,
+// Returns the number of active states (each thread owns at most one: NS <= nthreads).
+__device__ int gen_chain_states(Ctx& c, const double* A, const double* B, long long n_sub,
                                  int n_cc, long long g0, int cnt) {
-    const int tid = threadIdx.x, dof = c.dof;
+    const int tid = threadIdx.x, dof = c.dof, NS = c.NS, nthreads = c.nthreads;
+    double* const ends = sh(c.ends);
+    int* const ends_eq = sh(c.ends_eq);
+    int* const sgroup = sh(c.sgroup);
+    float* const qf = sh(c.qf);
+    const double* const ttab = n_cc == c.ttab_n ? sh(c.ttab) : nullptr;
     const long long k_lo = g0 / n_cc;
     const int npts = (int)((g0 + cnt - 1) / n_cc - k_lo) + 2;
-    for (int idx = tid; idx < npts * dof; idx += c.nthreads) {
+    for (int idx = tid; idx < npts * dof; idx += nthreads) {
         const int j = idx / dof, d = idx - j * dof;
-        c.ends[idx] = chain_point(A, B, d, k_lo + j, n_sub);
+        ends[idx] = chain_point(A, B, d, k_lo + j, n_sub);
     }
-    if (tid == 0) c.ictl[IC_KLO] = (int)k_lo;
+    if (tid == 0) sh(c.ictl)[IC_KLO] = (int)k_lo;
     __syncthreads();
-    for (int j = tid; j < npts - 1; j += c.nthreads) {
+    for (int j = tid; j < npts - 1; j += nthreads) {
         bool eq = true;
-        for (int d = 0; d < dof; ++d) eq &= c.ends[j * dof + d] == c.ends[(j + 1) * dof + d];
-        c.ends_eq[j] = eq;
+        for (int d = 0; d < dof; ++d) eq &= ends[j * dof + d] == ends[(j + 1) * dof + d];
+        ends_eq[j] = eq;
     }
     __syncthreads();
-    const double inv_n = (double)n_cc;
-    for (int s = tid; s < c.NS; s += c.nthreads) {
+    int mine = 0;
+    for (int s = tid; s < NS; s += nthreads) {
         if (s >= cnt) {
-            c.sgroup[s] = -1;
+            sgroup[s] = -1;
             continue;
         }
         const long long g = g0 + s;
         const long long k = g / n_cc;
         const int i = (int)(g - k * n_cc) + 1;
         const int j = (int)(k - k_lo);
-        if (c.ends_eq[j] && i != n_cc) {
-            c.sgroup[s] = -1;
+        if (ends_eq[j] && i != n_cc) {
+            sgroup[s] = -1;
             continue;
         }
-        const double* F = c.ends + j * dof;
+        const double* F = ends + j * dof;
         const double* T = F + dof;
         if (i == n_cc) {
-            for (int d = 0; d < dof; ++d) c.qf[d * c.NS + s] = (float)T[d];
+            for (int d = 0; d < dof; ++d) qf[d * NS + s] = (float)T[d];
         } else {
-            const double t = n_cc == c.ttab_n ? c.ttab[i] : __ddiv_rn((double)i, inv_n);
-            for (int d = 0; d < dof; ++d) c.qf[d * c.NS + s] = (float)lerp_exact(F[d], T[d], t);
+            const double t = ttab ? ttab[i] : __ddiv_rn((double)i, (double)n_cc);
+            for (int d = 0; d < dof; ++d) qf[d * NS + s] = (float)lerp_exact(F[d], T[d], t);
         }
-        c.sgroup[s] = (int)k;
+        sgroup[s] = (int)k;
+        ++mine;
     }
-    __syncthreads();
+    return __syncthreads_count(mine);
 }
 
 // ---------------------------------------------------------------------------
@@ -811,6 +892,8 @@ __device__ __noinline__ NnOut nn_scan(Ctx& c, const double* cfg, long long cap, 
     const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5, nw = c.nthreads >> 5, dof = c.dof;
     const int par = c.nnpar;  // double-buffered reduction slots: one barrier per call
     c.nnpar ^= 1;
+    q = sh(q);  // the query lives in the dynamic shared window (every caller)
+
     double best = __longlong_as_double(0x7ff0000000000000ll);  // +inf
     int bi = 0x7fffffff;
     const int npairs = (count + 1) >> 1;

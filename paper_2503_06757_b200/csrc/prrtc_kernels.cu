@@ -107,8 +107,8 @@ __device__ void setup_ctx(Ctx& c, unsigned char* smem, const uint32_t* robot_g, 
     for (int d = tid; d < c.dof; d += c.nthreads) {  // f_k of halton_value (sampling.cpp:12)
         double f = 1.0;
         for (int k = 0; k < kHaltonTab; ++k) {
-            f = __ddiv_rn(f, (double)c.bases[d]);
-            c.htab[d * kHaltonTab + k] = f;
+            f = __ddiv_rn(f, (double)sh(c.bases)[d]);
+            sh(c.htab)[d * kHaltonTab + k] = f;
         }
     }
     __syncthreads();
@@ -200,9 +200,9 @@ __device__ __forceinline__ TreeRef tree_ref(const PlanArgs& a, int prob, int t, 
 __device__ int tree_append_many(Ctx& c, const PlanArgs& a, const TreeRef& T, const double* pts,
                                 int count, int parent0, int* last) {
     const int tid = threadIdx.x, dof = c.dof;
-    if (tid == 0) c.ictl[IC_TMP2] = atomicAdd(T.reserved, count);
+    if (tid == 0) sh(c.ictl)[IC_TMP2] = atomicAdd(T.reserved, count);
     __syncthreads();
-    const long long s0 = c.ictl[IC_TMP2];
+    const long long s0 = sh(c.ictl)[IC_TMP2];
     const int ok = (int)max(0ll, min((long long)count, a.cap - s0));
     for (int idx = tid; idx < ok * dof; idx += c.nthreads) {
         const int j = idx / dof, d = idx - j * dof;
@@ -268,9 +268,9 @@ __device__ long long validate_chain(Ctx& c, const PlanArgs& a, const double* A, 
     for (long long g0 = 0; g0 < total; g0 += c.NS) {
         trace_phase(a, 5);  // PRRTC_TRACE: validation chunk
         if (done_flag) {  // stop flag (planner.cpp:112)
-            if (threadIdx.x == 0) c.ictl[IC_TMP3] = ld_relaxed(done_flag);
+            if (threadIdx.x == 0) sh(c.ictl)[IC_TMP3] = ld_relaxed(done_flag);
             __syncthreads();
-            const int dn = c.ictl[IC_TMP3];
+            const int dn = sh(c.ictl)[IC_TMP3];
             __syncthreads();
             if (dn != 0) {
                 *stopped = true;
@@ -278,16 +278,14 @@ __device__ long long validate_chain(Ctx& c, const PlanArgs& a, const double* A, 
             }
         }
         const int cnt = (int)min((long long)c.NS, total - g0);
-        gen_chain_states(c, A, B, n_sub, n_cc, g0, cnt);
+        const int act = gen_chain_states(c, A, B, n_sub, n_cc, g0, cnt);
         if (threadIdx.x == 0) {
-            int act = 0;
-            for (int s = 0; s < cnt; ++s) act += (c.sgroup[s] >= 0);
             fk_states += act;
             c.flops += (unsigned long long)act * c.fkflops;
         }
         check_chunk(c, cnt, a.p.two_stage != 0, a.p.early_exit != 0, false);
-        if (threadIdx.x == 0 && c.ictl[IC_QN]) ++fine_states;
-        const int fb = c.ictl[IC_FIRSTBAD];
+        if (threadIdx.x == 0 && sh(c.ictl)[IC_QN]) ++fine_states;
+        const int fb = sh(c.ictl)[IC_FIRSTBAD];
         good = (fb != kNoBad) ? (long long)fb : (g0 + cnt) / n_cc;
         __syncthreads();
         if (fb != kNoBad) break;
@@ -298,10 +296,10 @@ __device__ long long validate_chain(Ctx& c, const PlanArgs& a, const double* A, 
         const int cntk = (int)min(good - appended, (long long)c.NS + 1);
         for (int idx = threadIdx.x; idx < cntk * c.dof; idx += c.nthreads) {
             const int j = idx / c.dof, d = idx - j * c.dof;
-            c.ends[idx] = chain_point(A, B, d, appended + 1 + j, n_sub);
+            sh(c.ends)[idx] = chain_point(A, B, d, appended + 1 + j, n_sub);
         }
         __syncthreads();
-        const int got = tree_append_many(c, a, *T, c.ends, cntk, prev, &prev);
+        const int got = tree_append_many(c, a, *T, sh(c.ends), cntk, prev, &prev);
         appended += got;
         __syncthreads();
         if (got < cntk) {
@@ -330,9 +328,9 @@ __device__ void assemble_path(Ctx& c, const PlanArgs& a, int prob, int meet_a, i
         const int len = la + lb - 1;
         const unsigned long long need = (unsigned long long)len * dof;
         const unsigned long long off = atomicAdd(a.arena_used, need);
-        c.ictl[IC_TMP4] = len;
+        sh(c.ictl)[IC_TMP4] = len;
         if (off + need > a.arena_cap || len > ib_cap) {
-            c.ictl[IC_TMP4] = -1;
+            sh(c.ictl)[IC_TMP4] = -1;
         } else {
             a.ctl[prob].path_off = off;
             int pos = la - 1;
@@ -347,7 +345,7 @@ __device__ void assemble_path(Ctx& c, const PlanArgs& a, int prob, int meet_a, i
         }
     }
     __syncthreads();
-    const int len = c.ictl[IC_TMP4];
+    const int len = sh(c.ictl)[IC_TMP4];
     if (len < 0) return;
     const unsigned long long off = a.ctl[prob].path_off;
     for (int e = tid; e < len * dof; e += c.nthreads) {
@@ -399,9 +397,9 @@ __device__ bool init_problem(Ctx& c, const PlanArgs& a, int prob, unsigned long 
     __syncthreads();
     // states: 0 = start, 1 = goal (independent, early exit per state)
     for (int s = tid; s < c.NS; s += c.nthreads) {
-        c.sgroup[s] = s < 2 ? s : -1;
+        sh(c.sgroup)[s] = s < 2 ? s : -1;
         if (s < 2) {
-            for (int d = 0; d < dof; ++d) c.qf[d * c.NS + s] = (float)(s == 0 ? S[d] : G[d]);
+            for (int d = 0; d < dof; ++d) sh(c.qf)[d * c.NS + s] = (float)(s == 0 ? S[d] : G[d]);
         }
     }
     __syncthreads();
@@ -417,17 +415,17 @@ __device__ bool init_problem(Ctx& c, const PlanArgs& a, int prob, unsigned long 
             gl &= !(G[d] < lo || G[d] > hi);
         }
         int verdict = 0;
-        if (!sl || c.sbad[0]) verdict = 1;
-        else if (!gl || c.sbad[1]) verdict = 2;
+        if (!sl || sh(c.sbad)[0]) verdict = 1;
+        else if (!gl || sh(c.sbad)[1]) verdict = 2;
         else {
             bool eq = true;
             for (int d = 0; d < dof; ++d) eq &= (S[d] == G[d]);
             if (eq) verdict = 3;
         }
-        c.ictl[IC_TMP5] = verdict;
+        sh(c.ictl)[IC_TMP5] = verdict;
     }
     __syncthreads();
-    const int verdict = c.ictl[IC_TMP5];
+    const int verdict = sh(c.ictl)[IC_TMP5];
     if (verdict == 1 || verdict == 2) {
         if (tid == 0) {
             C.started = 1;
@@ -483,9 +481,9 @@ __device__ int pick_help(Ctx& c, const PlanArgs& a) {
     // problems are finished
     for (int attempt = 0;; ++attempt) {
         if (attempt > 0) {
-            if (tid == 0) c.ictl[IC_TMP1] = ld_acquire(a.n_done);
+            if (tid == 0) sh(c.ictl)[IC_TMP1] = ld_acquire(a.n_done);
             __syncthreads();
-            const bool all_done = c.ictl[IC_TMP1] >= a.n_problems;
+            const bool all_done = sh(c.ictl)[IC_TMP1] >= a.n_problems;
             __syncthreads();
             if (all_done) return -1;
             __nanosleep(200);
@@ -511,16 +509,16 @@ __device__ int pick_help(Ctx& c, const PlanArgs& a) {
             }
         }
         if ((tid & 31) == 0) {
-            c.red_i[tid >> 5] = bp;
-            c.sgroup[tid >> 5] = bk;
+            sh(c.red_i)[tid >> 5] = bp;
+            sh(c.sgroup)[tid >> 5] = bk;
         }
         __syncthreads();
         if (tid == 0) {
-            int k = c.sgroup[0], p = c.red_i[0];
+            int k = sh(c.sgroup)[0], p = sh(c.red_i)[0];
             for (int w = 1; w < c.nthreads / 32; ++w) {
-                if (c.sgroup[w] < k || (c.sgroup[w] == k && c.red_i[w] >= 0 && (p < 0 || c.red_i[w] < p))) {
-                    k = c.sgroup[w];
-                    p = c.red_i[w];
+                if (sh(c.sgroup)[w] < k || (sh(c.sgroup)[w] == k && sh(c.red_i)[w] >= 0 && (p < 0 || sh(c.red_i)[w] < p))) {
+                    k = sh(c.sgroup)[w];
+                    p = sh(c.red_i)[w];
                 }
             }
             if (p >= 0) {
@@ -530,10 +528,10 @@ __device__ int pick_help(Ctx& c, const PlanArgs& a) {
                     p = -2;  // raced with completion: rescan
                 }
             }
-            c.ictl[IC_TMP1] = p;
+            sh(c.ictl)[IC_TMP1] = p;
         }
         __syncthreads();
-        const int p = c.ictl[IC_TMP1];
+        const int p = sh(c.ictl)[IC_TMP1];
         __syncthreads();
         if (p >= 0) return p;
     }
@@ -593,9 +591,9 @@ __global__ void __launch_bounds__(NT, MINB) plan_kernel(PlanArgs a) {
         int prob = -1;
         // unstarted problems first: claim, stage its scene, initialise
         for (;;) {
-            if (tid == 0) c.ictl[IC_TMP1] = atomicAdd(a.next_problem, 1);
+            if (tid == 0) sh(c.ictl)[IC_TMP1] = atomicAdd(a.next_problem, 1);
             __syncthreads();
-            const int p = c.ictl[IC_TMP1];
+            const int p = sh(c.ictl)[IC_TMP1];
             __syncthreads();
             if (p >= a.n_problems) break;
             const int si = a.prob_scene[p];
@@ -638,27 +636,27 @@ __global__ void __launch_bounds__(NT, MINB) plan_kernel(PlanArgs a) {
                 const unsigned long long hidx = 1ull + a.p.seed + (a.p.deterministic ? local_iter : it);
                 const int snap = from_start ? la : lb;
                 ++local_iter;
-                c.ictl[IC_TMP0] = leave;
-                c.ictl[IC_TMP1] = from_start;
-                c.ictl[IC_TMP2] = snap;
-                reinterpret_cast<unsigned long long*>(c.red_d)[0] = hidx;
+                sh(c.ictl)[IC_TMP0] = leave;
+                sh(c.ictl)[IC_TMP1] = from_start;
+                sh(c.ictl)[IC_TMP2] = snap;
+                reinterpret_cast<unsigned long long*>(sh(c.red_d))[0] = hidx;
             }
             __syncthreads();
-            const int leave = c.ictl[IC_TMP0];
+            const int leave = sh(c.ictl)[IC_TMP0];
             if (leave) {
                 leave_msg = leave == 2 ? MSG_BUDGET : MSG_NONE;
                 break;
             }
-            const int ts = c.ictl[IC_TMP1] ? 0 : 1;
-            const int snap = c.ictl[IC_TMP2];
-            const unsigned long long hidx = reinterpret_cast<unsigned long long*>(c.red_d)[0];
+            const int ts = sh(c.ictl)[IC_TMP1] ? 0 : 1;
+            const int snap = sh(c.ictl)[IC_TMP2];
+            const unsigned long long hidx = reinterpret_cast<unsigned long long*>(sh(c.red_d))[0];
             __syncthreads();
             const TreeRef Ts = tree_ref(a, prob, ts, dof);
             const TreeRef To = tree_ref(a, prob, 1 - ts, dof);
             // ---- sample (sampling.cpp:39-51), one thread per dimension ----
             double* smp = dc(c, DC_SAMPLE);
             if (tid < dof) {
-                smp[tid] = sample_dim(halton_tab(c.bases[tid], c.magic[tid], c.htab + tid * kHaltonTab, hidx),
+                smp[tid] = sample_dim(halton_tab(sh(c.bases)[tid], sh(c.magic)[tid], sh(c.htab) + tid * kHaltonTab, hidx),
                                       c.limits[2 * tid], c.limits[2 * tid + 1]);
             }
             __syncthreads();
@@ -699,9 +697,9 @@ __global__ void __launch_bounds__(NT, MINB) plan_kernel(PlanArgs a) {
             const int new_idx = last;
             // ---- greedy connect toward the opposite tree ----
             TRACE_PHASE(4);
-            if (tid == 0) c.ictl[IC_TMP2] = ld_acquire(To.published);
+            if (tid == 0) sh(c.ictl)[IC_TMP2] = ld_acquire(To.published);
             __syncthreads();
-            const int snap_o = c.ictl[IC_TMP2];
+            const int snap_o = sh(c.ictl)[IC_TMP2];
             __syncthreads();
             const NnOut no = nn_scan(c, To.cfg, a.stride, snap_o, cnew);
             const int nno = no.index;
@@ -732,9 +730,9 @@ __global__ void __launch_bounds__(NT, MINB) plan_kernel(PlanArgs a) {
             if (!reached) continue;
             // ---- winner (planner.cpp:232-238) ----
             TRACE_PHASE(6);
-            if (tid == 0) c.ictl[IC_TMP6] = (atomicCAS(&C.winner, 0, blockIdx.x + 1) == 0);
+            if (tid == 0) sh(c.ictl)[IC_TMP6] = (atomicCAS(&C.winner, 0, blockIdx.x + 1) == 0);
             __syncthreads();
-            if (c.ictl[IC_TMP6]) {
+            if (sh(c.ictl)[IC_TMP6]) {
                 const int meet_a = ts == 0 ? meet_self : nno;
                 const int meet_b = ts == 0 ? nno : meet_self;
                 if (tid == 0) {
@@ -743,10 +741,10 @@ __global__ void __launch_bounds__(NT, MINB) plan_kernel(PlanArgs a) {
                 }
                 assemble_path(c, a, prob, meet_a, meet_b);
                 if (tid == 0) {
-                    if (c.ictl[IC_TMP4] < 0) {
+                    if (sh(c.ictl)[IC_TMP4] < 0) {
                         finish_problem(a, prob, DONE_FAILED, MSG_ARENA);
                     } else {
-                        C.path_len = c.ictl[IC_TMP4];
+                        C.path_len = sh(c.ictl)[IC_TMP4];
                         __threadfence();
                         finish_problem(a, prob, DONE_SOLVED, MSG_NONE);
                     }
@@ -804,13 +802,13 @@ __global__ void __launch_bounds__(128) check_configs_kernel(RobotArgs r, SceneAr
     for (long long base = (long long)blockIdx.x * NS; base < n; base += (long long)gridDim.x * NS) {
         const int cnt = (int)min((long long)NS, n - base);
         for (int s = threadIdx.x; s < NS; s += c.nthreads) {
-            c.sgroup[s] = s < cnt ? s : -1;
+            sh(c.sgroup)[s] = s < cnt ? s : -1;
             if (s < cnt)
-                for (int d = 0; d < c.dof; ++d) c.qf[d * NS + s] = (float)q[(base + s) * c.dof + d];
+                for (int d = 0; d < c.dof; ++d) sh(c.qf)[d * NS + s] = (float)q[(base + s) * c.dof + d];
         }
         __syncthreads();
         check_chunk(c, cnt, two_stage != 0, true, true);
-        for (int s = threadIdx.x; s < cnt; s += c.nthreads) out[base + s] = c.sbad[s] ? 0 : 1;
+        for (int s = threadIdx.x; s < cnt; s += c.nthreads) out[base + s] = sh(c.sbad)[s] ? 0 : 1;
         __syncthreads();
     }
 }
@@ -844,7 +842,7 @@ __global__ void __launch_bounds__(128) validate_edges_kernel(RobotArgs r, SceneA
             gen_chain_states(c, A, B, 1, n_cc, g0, cnt);
             if (c.prof && threadIdx.x == 0) c.prof[8] = clock64();
             check_chunk(c, cnt, two_stage != 0, early_exit != 0, false);
-            bad |= c.ictl[IC_FIRSTBAD] != kNoBad;
+            bad |= sh(c.ictl)[IC_FIRSTBAD] != kNoBad;
             __syncthreads();
             if (c.prof && threadIdx.x == 0) c.prof[9] = clock64();
             c.prof = nullptr;  // first chunk only
@@ -863,7 +861,7 @@ __global__ void __launch_bounds__(128) debug_fk_kernel(RobotArgs r, const double
         const int cnt = (int)min((long long)NS, n - base);
         for (int s = threadIdx.x; s < NS; s += c.nthreads) {
             if (s < cnt)
-                for (int d = 0; d < c.dof; ++d) c.qf[d * NS + s] = (float)q[(base + s) * c.dof + d];
+                for (int d = 0; d < c.dof; ++d) sh(c.qf)[d * NS + s] = (float)q[(base + s) * c.dof + d];
         }
         __syncthreads();
         fk_chunk(c, cnt);
@@ -882,7 +880,7 @@ __global__ void __launch_bounds__(128) debug_fk_kernel(RobotArgs r, const double
             for (int it = threadIdx.x; it < cnt * c.L; it += c.nthreads) {
                 const int s = it % cnt, l = it / cnt;
                 float* o = coarse_out + ((base + s) * c.L + l) * 3;
-                const float* C = c.ccen + (size_t)l * 3 * NS + s;
+                const float* C = sh(c.ccen) + (size_t)l * 3 * NS + s;
                 o[0] = C[0];
                 o[1] = C[NS];
                 o[2] = C[2 * NS];
@@ -898,27 +896,28 @@ __global__ void debug_hits_kernel(SceneArgs sa, const float* centers, const doub
     const int words = sa.words[SH_WORDS];
     for (int i = threadIdx.x; i < words; i += blockDim.x) sw[i] = sa.words[i];
     __syncthreads();
-    Ctx c;
-    c.ns = sw[SH_NS];
-    c.nb = sw[SH_NB];
-    c.nc = sw[SH_NC];
-    c.P = c.ns + c.nb + c.nc;
-    c.sph = reinterpret_cast<const float4*>(sw + sw[SH_OFF_S]);
-    c.box = reinterpret_cast<const float*>(sw + sw[SH_OFF_B]);
-    c.cap = reinterpret_cast<const float*>(sw + sw[SH_OFF_C]);
-    c.eps = __uint_as_float(sw[SH_EPS]);
-    c.s64 = sa.f64;
+    // static shared memory: the view is built directly (sh() is for the
+    // dynamic window only)
+    SceneV v;
+    v.ns = sw[SH_NS];
+    v.nb = sw[SH_NB];
+    v.P = v.ns + v.nb + sw[SH_NC];
+    v.sph = reinterpret_cast<const float4*>(sw + sw[SH_OFF_S]);
+    v.box = reinterpret_cast<const float*>(sw + sw[SH_OFF_B]);
+    v.cap = reinterpret_cast<const float*>(sw + sw[SH_OFF_C]);
+    v.eps = __uint_as_float(sw[SH_EPS]);
+    v.s64 = sa.f64;
     for (long long it = blockIdx.x * (long long)blockDim.x + threadIdx.x; it < (long long)n * n_prims;
          it += (long long)gridDim.x * blockDim.x) {
         const int i = (int)(it / n_prims), p = (int)(it % n_prims);
         const float3 x = make_float3(centers[3 * i], centers[3 * i + 1], centers[3 * i + 2]);
-        hits[it] = fine_vs_prim(c, x, (float)radii[i], radii[i], p) ? 1 : 0;
+        hits[it] = fine_vs_prim(v, x, (float)radii[i], radii[i], p) ? 1 : 0;
     }
 }
 
 __global__ void debug_nn_kernel(const double* soa, long long cap, int count, int dof, const double* q,
                                 int nq, uint32_t* idx, double* d2) {
-    __shared__ double qs[kMaxDof];
+    double* qs = reinterpret_cast<double*>(g_dsmem);  // [kMaxDof], dynamic window (nn_scan uses sh())
     Ctx c;
     c.dof = dof;
     c.nthreads = blockDim.x;
@@ -1054,7 +1053,7 @@ cudaError_t launch_debug_hits(const SceneArgs& s, const float* centers, const do
 cudaError_t launch_debug_nn(const double* soa, long long cap, int count, int dof, const double* q,
                             int nq, uint32_t* idx, double* d2, cudaStream_t st) {
     const int grid = min(nq, 148 * 8);
-    if (grid > 0) debug_nn_kernel<<<grid, 128, 0, st>>>(soa, cap, count, dof, q, nq, idx, d2);
+    if (grid > 0) debug_nn_kernel<<<grid, 128, 8 * kMaxDof, st>>>(soa, cap, count, dof, q, nq, idx, d2);
     return cudaGetLastError();
 }
 
