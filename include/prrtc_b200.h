@@ -182,6 +182,9 @@ int prrtc_api_version(void);
 int prrtc_last_error(char* buf, size_t len);
 /* Number of usable devices, or a negative error. */
 int prrtc_device_count(void);
+/* CTAs prrtc_plan puts on one problem for params.workers == 0 (the analogue of
+ * the reference's hardware_concurrency default, planner.cpp:287-288); or an error. */
+int prrtc_default_workers(int device);
 void prrtc_params_default(prrtc_params* p);
 
 /* ---------------- setup (untimed) ---------------- */

@@ -177,6 +177,14 @@ int prrtc_device_count(void) {
     return ok;
 }
 
+int prrtc_default_workers(int device) {
+    int rc = check_device(device);
+    if (rc) return rc;
+    int n = 0;
+    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, device);
+    return 2 * (n > 0 ? n : 1);
+}
+
 void prrtc_params_default(prrtc_params* p) {  // planner.hpp:21-40
     std::memset(p, 0, sizeof(*p));
     p->delta = 0.5;

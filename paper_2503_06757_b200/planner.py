@@ -369,3 +369,11 @@ def debug_sample(model, index0: int, n: int, device: int = 0) -> np.ndarray:
 
 def device_count() -> int:
     return _lib.load().prrtc_device_count()
+
+
+def default_workers(device: int = 0) -> int:
+    """CTAs prrtc_plan uses on one problem when params.workers == 0."""
+    lib = _lib.load()
+    n = lib.prrtc_default_workers(device)
+    check(min(n, 0))
+    return n
