@@ -353,6 +353,16 @@ int prrtc_robot_create(const prrtc_robot_desc* d, int device, prrtc_robot** out)
             if (d->kind[l] == PRRTC_JOINT_PRISMATIC) r->reach += std::max(std::abs(d->lo[l]), std::abs(d->hi[l]));
         }
     }
+    // Halton reciprocal powers f_k = (((1/b)/b).../b) (halton_value's f /= b,
+    // sampling.cpp:12) after the [dof][2] limits: the same IEEE divisions as
+    // on the device, read through the read-only path by the sampler
+    for (unsigned b : first_primes(dof)) {
+        double f = 1.0;
+        for (int k = 0; k < HALTON_TAB; ++k) {
+            f = f / (double)b;
+            r->limits.push_back(f);
+        }
+    }
     r->fine_r64.resize(S);
     for (uint32_t k = 0; k < S; ++k) r->fine_r64[k] = d->fine[4 * k + 3];
 
@@ -389,7 +399,7 @@ int prrtc_robot_dof(const prrtc_robot* r) { return r ? r->dof : PRRTC_EINVAL; }
 int prrtc_robot_fine_count(const prrtc_robot* r) { return r ? r->n_fine : PRRTC_EINVAL; }
 int prrtc_robot_limits(const prrtc_robot* r, double* lim) {
     if (!r || !lim) return PRRTC_EINVAL;
-    std::copy(r->limits.begin(), r->limits.end(), lim);
+    std::copy(r->limits.begin(), r->limits.begin() + 2 * r->dof, lim);  // [dof][2]; the Halton table follows
     return PRRTC_OK;
 }
 
@@ -836,14 +846,15 @@ int batch_enqueue(prrtc_batch* b, cudaStream_t st, bool upload) {
         static int ct_cap = 0;
         if (ct_cap < b->grid) {
             cudaFree(d_ct);
-            cudaMalloc(&d_ct, sizeof(long long) * 32 * b->grid);
+            cudaMalloc(&d_ct, sizeof(long long) * 64 * b->grid);
             ct_cap = b->grid;
         }
-        cudaMemsetAsync(d_ct, 0, sizeof(long long) * 32 * b->grid, st);
+        cudaMemsetAsync(d_ct, 0, sizeof(long long) * 64 * b->grid, st);
         a.cta_trace = d_ct;
         b->cta_trace = d_ct;
     }
     a.epoch = ws->epoch;
+    a.dbg = std::getenv("PRRTC_DEBUG_FLAGS") ? (unsigned)std::atoi(std::getenv("PRRTC_DEBUG_FLAGS")) : 0u;
     a.p.delta = b->params.delta;
     a.p.dd_radius = b->params.dd_radius > 0.0 ? b->params.dd_radius : 4.0 * b->params.delta;
     a.p.n_cc = b->params.n_cc;
@@ -926,12 +937,29 @@ int batch_collect(prrtc_batch* b, prrtc_result* out) {
                      "last done -> last CTA exit %.3f | grid %d x %d\n",
                      ms, (p0 - k0) * 1e-6, (p1 - p0) * 1e-6, (k1 - p1) * 1e-6, b->grid, b->nthreads);
         if (b->cta_trace) {
-            std::vector<long long> ct(32 * b->grid);
+            std::vector<long long> ct(64 * b->grid);
             cudaMemcpy(ct.data(), b->cta_trace, 8 * ct.size(), cudaMemcpyDeviceToHost);
+            {  // per-phase SM cycles summed over CTAs (kernels.cu trace_phase codes)
+                static const char* names[16] = {"-", "header", "nn_extend", "dd+steer", "nn_connect", "fk+collide",
+                                                 "winner", "sample", "append", "chain_book", "leave", "", "", "",
+                                                 "", ""};
+                double cyc[16] = {0}, cnt[16] = {0}, tot = 0;
+                for (int g = 0; g < b->grid; ++g)
+                    for (int k = 0; k < 16; ++k) {
+                        cyc[k] += (double)ct[64 * g + 32 + k];
+                        cnt[k] += (double)ct[64 * g + 48 + k];
+                    }
+                for (int k = 0; k < 16; ++k) tot += cyc[k];
+                std::fprintf(stderr, "prrtc phases (share of CTA cycles, mean cycles/entry):");
+                for (int k = 1; k < 16; ++k)
+                    if (cnt[k] > 0)
+                        std::fprintf(stderr, " %s %.1f%% %.0f", names[k], 100.0 * cyc[k] / tot, cyc[k] / cnt[k]);
+                std::fprintf(stderr, "\n");
+            }
             long long max_start = 0, max_leave = 0, max_flush = 0, max_exit = 0;
             int slow = -1;
             for (int g = 0; g < b->grid; ++g) {
-                const long long* t = &ct[32 * g];
+                const long long* t = &ct[64 * g];
                 max_start = std::max(max_start, t[3] - k0);
                 if (t[0]) {
                     if (t[0] - p1 > max_leave) { max_leave = t[0] - p1; slow = g; }
@@ -944,14 +972,14 @@ int batch_collect(prrtc_batch* b, prrtc_result* out) {
                          "max flush+leave %.3f | max leave->exit %.3f\n",
                          max_start * 1e-6, max_leave * 1e-6, slow, max_flush * 1e-6, max_exit * 1e-6);
             if (slow >= 0) {
-                const long long* t = &ct[32 * slow];
+                const long long* t = &ct[64 * slow];
                 std::fprintf(stderr, "prrtc trace: slow CTA %d: iterations %lld, last phase %lld entered %.3f ms "
                                      "before leaving (%.3f ms after last done)\n",
                              slow, t[5], t[6], (t[0] - t[7]) * 1e-6, (t[7] - p1) * 1e-6);
                 std::fprintf(stderr, "prrtc trace: slow CTA events (phase@ms rel. first init):");
-                const long long nev = std::min<long long>(t[4], 12);
+                const long long nev = std::min<long long>(t[4], 11);
                 for (long long e = t[4] - nev; e < t[4]; ++e)
-                    std::fprintf(stderr, " %lld@%.3f", t[8 + 2 * (e % 12)], (t[9 + 2 * (e % 12)] - p0) * 1e-6);
+                    std::fprintf(stderr, " %lld@%.3f", t[8 + 2 * (e % 11)], (t[9 + 2 * (e % 11)] - p0) * 1e-6);
                 std::fprintf(stderr, " | start@%.3f leave@%.3f done@%.3f\n", (t[3] - p0) * 1e-6,
                              (t[0] - p0) * 1e-6, (p1 - p0) * 1e-6);
             }
@@ -978,7 +1006,7 @@ int batch_collect(prrtc_batch* b, prrtc_result* out) {
         // per-problem device time (globaltimer: initialisation -> finish)
         r.device_time_ms = (C.t_end_ns > C.t_start_ns) ? (C.t_end_ns - C.t_start_ns) * 1e-6 : 0.0;
         r.wall_time_ms = ms;  // launch time; prrtc_plan overwrites with the host wall clock
-        r.iterations_total = C.iters < b->budget ? C.iters : b->budget;
+        r.iterations_total = C.iters_used;
         r.sphere_tests = C.sphere_tests;
         r.fk_calls = C.fk_calls;
         r.fine_stage_entries = C.fine_entries;

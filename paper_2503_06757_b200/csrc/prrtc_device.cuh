@@ -92,7 +92,7 @@ __device__ __forceinline__ double halton_exact(unsigned base, unsigned long long
 // division done by multiply-high with M = ceil(2^64 / b) (exact for 32-bit
 // indices): bit-identical to halton_exact, without the per-digit FP64 and
 // integer divides.
-constexpr int kHaltonTab = 40;
+constexpr int kHaltonTab = HALTON_TAB;
 __device__ __forceinline__ double halton_tab(unsigned base, unsigned long long magic, const double* ftab,
                                              unsigned long long index) {
     if (index >> 32) return halton_exact(base, index);
@@ -220,7 +220,7 @@ struct Ctx {
     const int2* pairs;     // [NP]
     const unsigned* bases; // [dof]
     const unsigned long long* magic;  // [dof] ceil(2^64 / base)
-    double* htab;          // [dof][kHaltonTab] Halton reciprocal powers
+    const double* htab;    // [dof][kHaltonTab] Halton reciprocal powers (global, after limits)
     const int* flink;      // [S] link of each fine sphere
     const double* fine_r64;  // global
     const double* limits;    // global [dof][2]
@@ -250,6 +250,7 @@ struct Ctx {
     // CTA scalars
     int* ictl;       // [32] misc ints
     double* dcfg;    // [8][kMaxDof] scratch configs
+    double* sbuf;    // [nthreads] Halton samples of the CTA's current ticket block
     double* red_d;   // [nwarps]
     int* red_i;      // [nwarps]
     int nthreads;
@@ -301,6 +302,9 @@ enum : int {
     IC_TMP6,
     IC_TMP7,
     IC_KLO,         // first chain point held in `ends`
+    IC_KNOWN0,      // per tree: published prefix this CTA holds acquire-ordered (or wrote itself);
+    IC_KNOWN1,      //   a snapshot within it needs no fence (thread 0 only)
+    IC_DIRTY,       // the CTA stored tree data since its last fence: L1 may hold stale lines
     IC_COUNT = 32
 };
 
@@ -876,8 +880,11 @@ __device__ int gen_chain_states(Ctx& c, const double* A, const double* B, long l
 // ---------------------------------------------------------------------------
 // nearest neighbour over the published prefix of a tree (nn.cpp:22-29,
 // kernels_scalar.cpp:9-37): exact FP64 keys in the scalar summation order
-// over SoA rows, 128-bit loads (two nodes per load, L1-bypassing .cg since
-// slots become visible while the kernel runs), per-thread strict-< argmin
+// over SoA rows, 128-bit loads (two nodes per load; plain L1-allocating
+// loads: every slot below the snapshot was released before the caller's
+// acquire of `published`, which also invalidates stale L1 lines, so the
+// follow-up reads of the winner's config and dynamic-domain flag — both
+// prefetched into L1 here — hit L1), per-thread strict-< argmin
 // over increasing indices, then warp-shuffle and cross-warp argmin with ties
 // to the lowest index. Returned to every thread.
 // ---------------------------------------------------------------------------
@@ -886,7 +893,7 @@ struct NnOut {
     double d2;
 };
 __device__ __noinline__ NnOut nn_scan(Ctx& c, const double* cfg, long long cap, int count,
-                                      const double* q) {
+                                      const double* q, const int* ddf = nullptr) {
     __shared__ double s_bd[2][32];
     __shared__ int s_bi[2][32];
     const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5, nw = c.nthreads >> 5, dof = c.dof;
@@ -897,23 +904,30 @@ __device__ __noinline__ NnOut nn_scan(Ctx& c, const double* cfg, long long cap, 
     double best = __longlong_as_double(0x7ff0000000000000ll);  // +inf
     int bi = 0x7fffffff;
     const int npairs = (count + 1) >> 1;
-    // two node pairs (4 nodes) per thread per step: 2 x 128-bit loads per
-    // dimension in flight; candidates visited in increasing index order so
-    // strict < keeps the lowest index (kernels_scalar.cpp:30-34)
-    for (int pi = tid; pi < npairs; pi += 2 * c.nthreads) {
-        const int n0 = pi * 2, pj = pi + c.nthreads, n1 = pj * 2;
-        const bool has1 = pj < npairs;
-        double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
-        for (int d = 0; d < dof; ++d) {
-            const double2 v = __ldcg(reinterpret_cast<const double2*>(cfg + d * cap + n0));
-            const double2 u = has1 ? __ldcg(reinterpret_cast<const double2*>(cfg + d * cap + n1)) : v;
-            const double qd = q[d];
-            const double e0 = __dsub_rn(v.x, qd), e1 = __dsub_rn(v.y, qd);
-            const double e2 = __dsub_rn(u.x, qd), e3 = __dsub_rn(u.y, qd);
-            a0 = __dadd_rn(a0, __dmul_rn(e0, e0));
-            a1 = __dadd_rn(a1, __dmul_rn(e1, e1));
-            a2 = __dadd_rn(a2, __dmul_rn(e2, e2));
-            a3 = __dadd_rn(a3, __dmul_rn(e3, e3));
+    // one node pair per thread per step (128-bit load per dimension); the
+    // dimensions' loads are issued 8 at a time before any is consumed, so a
+    // step costs one L2 round trip per 8 dimensions instead of one per
+    // dimension. Candidates are visited in increasing index order per
+    // thread, so strict < keeps the lowest index (kernels_scalar.cpp:30-34);
+    // keys accumulate in the scalar order d = 0, 1, ... (bit-exact).
+    for (int pi = tid; pi < npairs; pi += c.nthreads) {
+        const int n0 = pi * 2;
+        double a0 = 0.0, a1 = 0.0;
+        if (ddf) asm volatile("prefetch.global.L1 [%0];" ::"l"(ddf + n0));
+        for (int d0 = 0; d0 < dof; d0 += 8) {
+            double2 v[8];
+#pragma unroll
+            for (int j = 0; j < 8; ++j)
+                if (d0 + j < dof) v[j] = *reinterpret_cast<const double2*>(cfg + (d0 + j) * cap + n0);
+#pragma unroll
+            for (int j = 0; j < 8; ++j) {
+                if (d0 + j < dof) {
+                    const double qd = q[d0 + j];
+                    const double e0 = __dsub_rn(v[j].x, qd), e1 = __dsub_rn(v[j].y, qd);
+                    a0 = __dadd_rn(a0, __dmul_rn(e0, e0));
+                    a1 = __dadd_rn(a1, __dmul_rn(e1, e1));
+                }
+            }
         }
         if (a0 < best) {
             best = a0;
@@ -922,14 +936,6 @@ __device__ __noinline__ NnOut nn_scan(Ctx& c, const double* cfg, long long cap, 
         if (n0 + 1 < count && a1 < best) {
             best = a1;
             bi = n0 + 1;
-        }
-        if (has1 && a2 < best) {
-            best = a2;
-            bi = n1;
-        }
-        if (has1 && n1 + 1 < count && a3 < best) {
-            best = a3;
-            bi = n1 + 1;
         }
     }
 #pragma unroll

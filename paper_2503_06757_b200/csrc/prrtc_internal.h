@@ -81,7 +81,7 @@ struct ProbCtl {
     int active;       // CTAs currently working on it
     int reserved[2];  // tree slot reservation counters
     int published[2]; // fully-ready prefix lengths
-    unsigned long long halton_ticket;
+    unsigned long long iters_used;  // iterations actually run (tickets are claimed in blocks)
     unsigned long long iters;
     unsigned long long sphere_tests;
     unsigned long long fk_calls;
@@ -109,6 +109,10 @@ struct PlanParamsDev {
     unsigned long long seed;
 };
 
+// Halton reciprocal-power table length per dimension: stored after the
+// [dof][2] limits in the robot's device buffer (prrtc_robot_create).
+constexpr int HALTON_TAB = 40;
+
 struct PlanArgs {
     const uint32_t* robot;     // packed robot words
     const double* fine_r64;    // [S]
@@ -134,6 +138,7 @@ struct PlanArgs {
     unsigned long long* trace; // [2]: LLONG_MAX - first CTA start, last CTA exit (globaltimer ns)
     long long* cta_trace;      // [grid][4]: per-CTA stamps (PRRTC_TRACE only, else null)
     unsigned epoch;
+    unsigned dbg;              // PRRTC_DEBUG_FLAGS (development switches, 0 in production)
     PlanParamsDev p;
     int ns_max;                // states per validation chunk
     int nthreads;

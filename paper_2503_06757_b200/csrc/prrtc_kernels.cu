@@ -26,7 +26,7 @@ using namespace dev;
 // ---------------------------------------------------------------------------
 struct SmemLayout {
     size_t robot, scene, pose, ccen, qf, sgroup, sbad, lmask, ictl, dcfg, red_d, red_i,
-        ends, ends_eq, htab, ttab, total;
+        ends, ends_eq, ttab, sbuf, total;
 };
 
 __host__ __device__ inline size_t al16(size_t x) { return (x + 15) & ~size_t(15); }
@@ -50,8 +50,8 @@ __host__ __device__ inline SmemLayout smem_layout(int robot_words, int L, int do
     s.red_i = o; o = al16(o + 4 * (size_t)(nthreads / 32));
     s.ends = o;  o = al16(o + 8 * (size_t)(NS + 2) * dof);
     s.ends_eq = o; o = al16(o + 4 * (size_t)(NS + 2));
-    s.htab = o;  o = al16(o + 8 * (size_t)dof * kHaltonTab);
     s.ttab = o;  o = al16(o + 8 * (size_t)(kTTab + 1));
+    s.sbuf = o;  o = al16(o + 8 * (size_t)nthreads);
     s.total = o;
     return s;
 }
@@ -101,17 +101,10 @@ __device__ void setup_ctx(Ctx& c, unsigned char* smem, const uint32_t* robot_g, 
     c.red_i = reinterpret_cast<int*>(smem + lay.red_i);
     c.ends = reinterpret_cast<double*>(smem + lay.ends);
     c.ends_eq = reinterpret_cast<int*>(smem + lay.ends_eq);
-    c.htab = reinterpret_cast<double*>(smem + lay.htab);
+    c.htab = limits + 2 * c.dof;
     c.ttab = reinterpret_cast<double*>(smem + lay.ttab);
+    c.sbuf = reinterpret_cast<double*>(smem + lay.sbuf);
     c.ttab_n = 0;
-    for (int d = tid; d < c.dof; d += c.nthreads) {  // f_k of halton_value (sampling.cpp:12)
-        double f = 1.0;
-        for (int k = 0; k < kHaltonTab; ++k) {
-            f = __ddiv_rn(f, (double)sh(c.bases)[d]);
-            sh(c.htab)[d * kHaltonTab + k] = f;
-        }
-    }
-    __syncthreads();
     c.nslog = 31 - __clz(NS);
     c.mflog = c.MF > 1 ? 32 - __clz(c.MF - 1) : 0;
     c.tests = 0;
@@ -159,20 +152,36 @@ struct TreeRef {
     int* dd;           // [cap]
     int* reserved;
     int* published;
+    int which;         // 0 start tree, 1 goal tree
 };
 
 // PRRTC_TRACE: last phase entered + when, iterations, and a ring of the
-// last 12 (phase, time) events per CTA (slots 8..31)
+// last 11 (phase, time) events per CTA (slots 8..29); slots 32..47 sum the
+// SM cycles spent in each phase code, 48..63 count the entries (a phase
+// lasts until the next marker). Codes: 1 header, 2 NN (extend), 3 dynamic
+// domain + steer, 4 NN (connect), 5 validation chunk, 6 winner/assembly,
+// 7 sample, 8 append, 9 chain states + FK + collision bookkeeping, 10 leave.
+// The row lives in shared memory while the CTA runs (global read-modify-
+// writes would cost an L2 round trip per marker) and is copied out at exit.
+constexpr int kTraceStride = 64;
+__shared__ long long g_trace[kTraceStride];
 __device__ __forceinline__ void trace_phase(const PlanArgs& a, int code) {
     if (threadIdx.x != 0 || !a.cta_trace) return;
-    long long* t = a.cta_trace + blockIdx.x * 32;
+    long long* t = g_trace;
     const long long now = globaltimer();
+    const long long cyc = clock64();
+    const int prev = (int)t[6];
+    if (prev > 0 && prev < 16) {
+        t[32 + prev] += cyc - t[30];  // slot 30: clock64 of the last marker
+        t[48 + prev] += 1;
+    }
+    t[30] = cyc;
     t[6] = code;
     t[7] = now;
     if (code == 1) t[5] += 1;
     const long long k = t[4]++;
-    t[8 + 2 * (k % 12)] = code;
-    t[9 + 2 * (k % 12)] = now;
+    t[8 + 2 * (k % 11)] = code;
+    t[9 + 2 * (k % 11)] = now;
 }
 
 __device__ __forceinline__ TreeRef tree_ref(const PlanArgs& a, int prob, int t, int dof) {
@@ -184,6 +193,7 @@ __device__ __forceinline__ TreeRef tree_ref(const PlanArgs& a, int prob, int t, 
     r.dd = a.dd + pt * a.stride;
     r.reserved = &a.ctl[prob].reserved[t];
     r.published = &a.ctl[prob].published[t];
+    r.which = t;
     return r;
 }
 
@@ -218,7 +228,14 @@ __device__ int tree_append_many(Ctx& c, const PlanArgs& a, const TreeRef& T, con
     if (tid < 32 && ok > 0) {  // warp 0 publishes
         const int lane = tid;
         int won = 0;
-        if (lane == 0) won = atomicCAS(T.published, (int)s0, (int)(s0 + ok)) == s0;
+        if (lane == 0) {
+            won = atomicCAS(T.published, (int)s0, (int)(s0 + ok)) == s0;
+            // a block that starts at the CTA's known prefix extends it: the
+            // new nodes are its own writes
+            int* known = sh(c.ictl) + IC_KNOWN0 + T.which;
+            if (won && *known == (int)s0) *known = (int)(s0 + ok);
+            sh(c.ictl)[IC_DIRTY] = 1;
+        }
         won = __shfl_sync(0xffffffffu, won, 0);
         if (won) {
             // our block is published; carry `published` over the successors
@@ -226,19 +243,25 @@ __device__ int tree_append_many(Ctx& c, const PlanArgs& a, const TreeRef& T, con
             // (a burst of concurrent appends otherwise costs one acquire load +
             // CAS round trip per slot)
             int p = (int)(s0 + ok);
-            __threadfence();
             while (p < a.cap) {
+                // store->load (Dekker) ordering against a successor that set
+                // its flags and then failed its CAS: our last CAS must be
+                // visible before we read its flags (it fenced the other way
+                // round). After every successful CAS the flags are read
+                // again: a successor whose CAS lost to that one is only seen
+                // here (stopping early would strand its block)
+                __threadfence();
                 const long long idx = (long long)p + lane;
                 const bool r = idx < a.cap && ld_acquire_u(&T.ready[idx]) == a.epoch;
                 const unsigned m = __ballot_sync(0xffffffffu, r);
                 const int run = (m == 0xffffffffu) ? 32 : (__ffs(~m) - 1);
                 if (run == 0) break;
                 int old = 0;
+                fence_acq_rel();  // release for the carried slots (acquired through their flags)
                 if (lane == 0) old = atomicCAS(T.published, p, p + run);
                 old = __shfl_sync(0xffffffffu, old, 0);
                 if (old != p) break;  // another writer is advancing
                 p += run;
-                if (run < 32) break;
             }
         }
     }
@@ -266,7 +289,7 @@ __device__ long long validate_chain(Ctx& c, const PlanArgs& a, const double* A, 
     *stopped = false;
     *last = parent0;
     for (long long g0 = 0; g0 < total; g0 += c.NS) {
-        trace_phase(a, 5);  // PRRTC_TRACE: validation chunk
+        trace_phase(a, 9);  // PRRTC_TRACE: chain states
         if (done_flag) {  // stop flag (planner.cpp:112)
             if (threadIdx.x == 0) sh(c.ictl)[IC_TMP3] = ld_relaxed(done_flag);
             __syncthreads();
@@ -283,7 +306,9 @@ __device__ long long validate_chain(Ctx& c, const PlanArgs& a, const double* A, 
             fk_states += act;
             c.flops += (unsigned long long)act * c.fkflops;
         }
+        trace_phase(a, 5);  // FK + collision
         check_chunk(c, cnt, a.p.two_stage != 0, a.p.early_exit != 0, false);
+        trace_phase(a, 9);
         if (threadIdx.x == 0 && sh(c.ictl)[IC_QN]) ++fine_states;
         const int fb = sh(c.ictl)[IC_FIRSTBAD];
         good = (fb != kNoBad) ? (long long)fb : (g0 + cnt) / n_cc;
@@ -292,6 +317,7 @@ __device__ long long validate_chain(Ctx& c, const PlanArgs& a, const double* A, 
     }
     long long appended = 0;
     int prev = parent0;
+    trace_phase(a, 8);  // append
     while (appended < good) {
         const int cntk = (int)min(good - appended, (long long)c.NS + 1);
         for (int idx = threadIdx.x; idx < cntk * c.dof; idx += c.nthreads) {
@@ -583,7 +609,10 @@ __global__ void __launch_bounds__(NT, MINB) plan_kernel(PlanArgs a) {
     build_ttab(c, a.p.n_cc);
     const double R = a.p.dd_radius, delta = a.p.delta;
     if (tid == 0 && a.trace) atomicMax(&a.trace[0], 0x7fffffffffffffffull - (unsigned long long)globaltimer());
-    if (tid == 0 && a.cta_trace) a.cta_trace[blockIdx.x * 32 + 3] = globaltimer();
+    if (tid == 0 && a.cta_trace) {
+        for (int k = 0; k < kTraceStride; ++k) g_trace[k] = 0;
+        g_trace[3] = globaltimer();
+    }
 
     for (;;) {
         unsigned long long fk_states = 0, fine_states = 0;
@@ -615,31 +644,60 @@ __global__ void __launch_bounds__(NT, MINB) plan_kernel(PlanArgs a) {
             load_scene(c, sbase, a.scene_words[si], a.scene_f64[si]);
         }
         ProbCtl& C = a.ctl[prob];
+        if (tid == 0) {  // the roots: written by this CTA, or acquired through `started` (pick_help)
+            sh(c.ictl)[IC_KNOWN0] = 1;
+            sh(c.ictl)[IC_KNOWN1] = 1;
+            sh(c.ictl)[IC_DIRTY] = 1;
+        }
         unsigned long long local_iter = 0;
+        // Halton tickets are claimed in blocks of kblk (one atomic per block,
+        // every ticket still used once, in order within the CTA); the block's
+        // samples are computed by all threads at once into sbuf
+        const int kblk = max(1, min(32, c.nthreads / dof));
+        unsigned long long tk_base = 0, tk_pos = 0, tk_cnt = 0, used = 0;  // thread 0's copy
         int leave_msg = MSG_NONE;
         for (;;) {
             // ---- iteration header (lead thread) ----
             TRACE_PHASE(1);
             if (tid == 0) {
-                // one global ticket per iteration is both the budget counter
-                // and the Halton index (no stride-W bias);
-                // the four accesses are issued back to back, then one fence
-                // gives the published snapshot acquire semantics
+                // the done flag and both published counts are read back to
+                // back (relaxed done, acquire counts)
                 const int dn = ld_relaxed(&C.done);
-                const unsigned long long it = atomicAdd(&C.iters, 1ull);
+                int refill = 0;
+                if (tk_pos == tk_cnt) {
+                    tk_base = a.p.deterministic ? tk_base + tk_cnt : atomicAdd(&C.iters, (unsigned long long)kblk);
+                    tk_pos = 0;
+                    tk_cnt = kblk;
+                    refill = 1;
+                }
+                const unsigned long long it = tk_base + tk_pos;
                 const int la = ld_relaxed(&C.published[0]);
                 const int lb = ld_relaxed(&C.published[1]);
-                fence_acq_rel();
+                // a snapshot beyond what the CTA already holds needs acquire
+                // ordering (fence after the relaxed reads) before plain loads
+                // of the new slots; a CTA working alone never pays it
+                // (the fence also drops the SM's L1 lines, so after the CTA's
+                // own tree stores — appends, dynamic-domain flags — it is
+                // taken once to keep later plain loads from stale lines)
+                int* known = sh(c.ictl) + IC_KNOWN0;
+                if (la > known[0] || lb > known[1] || sh(c.ictl)[IC_DIRTY] || (a.dbg & 1)) {
+                    fence_acq_rel();
+                    known[0] = max(known[0], la);
+                    known[1] = max(known[1], lb);
+                    sh(c.ictl)[IC_DIRTY] = 0;
+                }
                 const int leave = dn != DONE_RUNNING ? 1 : (it >= a.p.budget ? 2 : 0);
                 // extend_start_tree (planner.hpp:62-65)
                 const int from_start = a.p.balance ? (la <= lb) : ((local_iter & 1) == 0);
-                const unsigned long long hidx = 1ull + a.p.seed + (a.p.deterministic ? local_iter : it);
                 const int snap = from_start ? la : lb;
                 ++local_iter;
+                used += leave == 0;
                 sh(c.ictl)[IC_TMP0] = leave;
                 sh(c.ictl)[IC_TMP1] = from_start;
                 sh(c.ictl)[IC_TMP2] = snap;
-                reinterpret_cast<unsigned long long*>(sh(c.red_d))[0] = hidx;
+                sh(c.ictl)[IC_TMP3] = refill;
+                sh(c.ictl)[IC_TMP4] = (int)tk_pos++;
+                reinterpret_cast<unsigned long long*>(sh(c.red_d))[0] = tk_base;
             }
             __syncthreads();
             const int leave = sh(c.ictl)[IC_TMP0];
@@ -649,45 +707,58 @@ __global__ void __launch_bounds__(NT, MINB) plan_kernel(PlanArgs a) {
             }
             const int ts = sh(c.ictl)[IC_TMP1] ? 0 : 1;
             const int snap = sh(c.ictl)[IC_TMP2];
-            const unsigned long long hidx = reinterpret_cast<unsigned long long*>(sh(c.red_d))[0];
-            __syncthreads();
+            const int refill = sh(c.ictl)[IC_TMP3];
+            const int slot = sh(c.ictl)[IC_TMP4];
             const TreeRef Ts = tree_ref(a, prob, ts, dof);
             const TreeRef To = tree_ref(a, prob, 1 - ts, dof);
-            // ---- sample (sampling.cpp:39-51), one thread per dimension ----
-            double* smp = dc(c, DC_SAMPLE);
-            if (tid < dof) {
-                smp[tid] = sample_dim(halton_tab(sh(c.bases)[tid], sh(c.magic)[tid], sh(c.htab) + tid * kHaltonTab, hidx),
-                                      c.limits[2 * tid], c.limits[2 * tid + 1]);
+            // ---- sample (sampling.cpp:39-51): a whole ticket block at once,
+            // one thread per (ticket, dimension), Halton index 1 + seed + ticket
+            if (refill) {
+                TRACE_PHASE(7);
+                const unsigned long long base = reinterpret_cast<unsigned long long*>(sh(c.red_d))[0];
+                __syncthreads();  // header scalars read before they are reused
+                if (tid < kblk * dof) {
+                    const int k = tid / dof, d = tid - k * dof;
+                    sh(c.sbuf)[tid] = sample_dim(halton_tab(sh(c.bases)[d], sh(c.magic)[d], c.htab + d * kHaltonTab,
+                                                            1ull + a.p.seed + base + k),
+                                                 __ldg(c.limits + 2 * d), __ldg(c.limits + 2 * d + 1));
+                }
             }
             __syncthreads();
+            const double* smp = sh(c.sbuf) + slot * dof;
             // ---- nearest neighbour in the extended tree ----
             TRACE_PHASE(2);
-            const NnOut nr = nn_scan(c, Ts.cfg, a.stride, snap, smp);
+            const NnOut nr = nn_scan(c, Ts.cfg, a.stride, snap, smp, a.p.dynamic_domain ? Ts.dd : nullptr);
             const int nn = nr.index;
             const double d2 = nr.d2;
             if (d2 == 0.0) continue;  // duplicate of an existing node (planner.cpp:320)
+            TRACE_PHASE(3);
             const double dist = __dsqrt_rn(d2);
+            // the nearest node's config and dynamic-domain flag are loaded
+            // together (one L2 round trip), before the accept decision
+            const double v = tid < dof ? Ts.cfg[(size_t)tid * a.stride + nn] : 0.0;
             if (a.p.dynamic_domain) {  // DynamicDomain::accept (sampling.hpp:61-75)
-                const int has = __ldcg(&Ts.dd[nn]);  // one broadcast load, no barrier
+                const int has = Ts.dd[nn];  // one broadcast load (L1: prefetched by the scan)
                 if (__syncthreads_or(has) && !(dist <= R)) continue;
             }
             // ---- steer (planner.cpp:48-64) ----
             double* nnc = dc(c, DC_NN);
             double* cnew = dc(c, DC_NEW);
             if (tid < dof) {
-                const double v = __ldcg(&Ts.cfg[(size_t)tid * a.stride + nn]);
                 nnc[tid] = v;
                 cnew[tid] = dist <= delta ? smp[tid] : lerp_exact(v, smp[tid], __ddiv_rn(delta, dist));
             }
             __syncthreads();
             // ---- SIMT edge validation nn -> c_new, then append ----
-            TRACE_PHASE(3);
             int last = nn;
             bool stopped = false;
             const long long ok = validate_chain(c, a, nnc, cnew, 1, &Ts, nn, &last, nullptr,
                                                 fk_states, fine_states, &stopped);
             if (ok == 0) {
-                if (a.p.dynamic_domain && tid == 0) Ts.dd[nn] = 1;  // record_failure
+                if (a.p.dynamic_domain && tid == 0) {  // record_failure
+                    Ts.dd[nn] = 1;
+                    sh(c.ictl)[IC_DIRTY] = 1;
+                }
                 continue;
             }
             if (ok < 0) {
@@ -697,7 +768,15 @@ __global__ void __launch_bounds__(NT, MINB) plan_kernel(PlanArgs a) {
             const int new_idx = last;
             // ---- greedy connect toward the opposite tree ----
             TRACE_PHASE(4);
-            if (tid == 0) sh(c.ictl)[IC_TMP2] = ld_acquire(To.published);
+            if (tid == 0) {
+                const int po = ld_relaxed(To.published);
+                int* known = sh(c.ictl) + IC_KNOWN0 + To.which;
+                if (po > *known || (a.dbg & 1)) {
+                    fence_acq_rel();
+                    *known = po;
+                }
+                sh(c.ictl)[IC_TMP2] = po;
+            }
             __syncthreads();
             const int snap_o = sh(c.ictl)[IC_TMP2];
             __syncthreads();
@@ -714,7 +793,7 @@ __global__ void __launch_bounds__(NT, MINB) plan_kernel(PlanArgs a) {
                 double* tgt = dc(c, DC_TARGET);
                 double* A = dc(c, DC_A);
                 if (tid < dof) {
-                    tgt[tid] = __ldcg(&To.cfg[(size_t)tid * a.stride + nno]);
+                    tgt[tid] = To.cfg[(size_t)tid * a.stride + nno];
                     A[tid] = cnew[tid];
                 }
                 __syncthreads();
@@ -753,22 +832,33 @@ __global__ void __launch_bounds__(NT, MINB) plan_kernel(PlanArgs a) {
             break;
         }
         // ---- leave ----
-        if (tid == 0 && a.cta_trace) a.cta_trace[blockIdx.x * 32 + 0] = globaltimer();
+        TRACE_PHASE(10);
+        if (tid == 0 && used) atomicAdd(&C.iters_used, used);
+        if (tid == 0 && a.cta_trace) g_trace[0] = globaltimer();
         flush_stats(c, C, fk_states, fine_states);
         if (tid == 0) leave_problem(a, prob, leave_msg);
         __syncthreads();
-        if (tid == 0 && a.cta_trace) a.cta_trace[blockIdx.x * 32 + 1] = globaltimer();
+        if (tid == 0 && a.cta_trace) g_trace[1] = globaltimer();
         if (a.p.deterministic && a.n_problems == 1) break;
     }
     if (tid == 0 && a.trace) atomicMax(&a.trace[1], (unsigned long long)globaltimer());
-    if (tid == 0 && a.cta_trace) a.cta_trace[blockIdx.x * 32 + 2] = globaltimer();
+    if (tid == 0 && a.cta_trace) {
+        TRACE_PHASE(0);  // close the last phase
+        g_trace[2] = globaltimer();
+        for (int k = 0; k < kTraceStride; ++k) a.cta_trace[blockIdx.x * kTraceStride + k] = g_trace[k];
+    }
 }
 
 // CTA size variants: 128 threads (4 warps, up to 4 CTAs/SM) and 256 threads
 // (8 warps, 2 CTAs/SM: each iteration's parallel phases finish faster).
 using PlanFn = void (*)(PlanArgs);
 static PlanFn plan_fn(int nthreads) {
-    return nthreads == 256 ? plan_kernel<256, 2> : plan_kernel<128, 4>;
+    if (nthreads == 256) return plan_kernel<256, 2>;
+    static const int minb = [] {
+        const char* e = getenv("PRRTC_PLAN_MINB");
+        return e ? atoi(e) : 4;
+    }();
+    return minb == 6 ? plan_kernel<128, 6> : (minb == 5 ? plan_kernel<128, 5> : plan_kernel<128, 4>);
 }
 
 cudaError_t launch_plan(const RobotArgs& r, PlanArgs a, int grid, cudaStream_t st) {
@@ -957,7 +1047,10 @@ __global__ void debug_sample_kernel(RobotArgs r, uint64_t index0, int n, double*
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= n * dof) return;
     const int k = i / dof, d = i % dof;
-    out[i] = sample_dim(halton_planner(bases[d], index0 + k), r.limits[2 * d], r.limits[2 * d + 1]);
+    // the planner's own path: host-built reciprocal table after the limits
+    const double* ftab = r.limits + 2 * dof + d * kHaltonTab;
+    out[i] = sample_dim(halton_tab(bases[d], ~0ull / bases[d] + 1, ftab, index0 + k), r.limits[2 * d],
+                        r.limits[2 * d + 1]);
 }
 
 // FP32 FFMA-chain microbenchmark: the roofline denominator for the FK /

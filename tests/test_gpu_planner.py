@@ -49,7 +49,7 @@ def check_path(oracle, m, scene, res, start, goal, params):
 @pytest.mark.parametrize("robot", ["panda", "fetch", "baxter"])
 def test_plan_paths_revalidate(gpu, oracle, robot):
     m = robots.get(robot)
-    params = PlannerParams(tree_capacity=20000)
+    params = PlannerParams()  # reference defaults (tree_capacity 200000, planner.hpp:21-40)
     probs = load_problems(robot, 24)
     solved = solved_ref = 0
     for kind, pid, s, g in probs:
@@ -59,7 +59,7 @@ def test_plan_paths_revalidate(gpu, oracle, robot):
         if r.status == PlanStatus.Solved:
             solved += 1
             check_path(oracle, m, scene, r, s, g, params)
-        ref = oracle.plan(m, scene, s, g, PlannerParams(workers=1, tree_capacity=20000))
+        ref = oracle.plan(m, scene, s, g, PlannerParams(workers=1))
         solved_ref += ref.status == PlanStatus.Solved
     assert solved >= solved_ref
 
