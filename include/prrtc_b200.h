@@ -263,6 +263,11 @@ int prrtc_debug_sphere_hits(const prrtc_scene* scene, const float* centers,
    the lowest index. */
 int prrtc_debug_nn(const double* tree, uint32_t count, uint32_t dof, const double* q,
                    uint32_t n_queries, int device, uint32_t* index, double* sq_dist);
+/* The planner's multi-sample NN pass: queries evaluated `group` (1..32) at a
+   time against the same tree, as the planner evaluates the samples of a
+   Halton ticket block; group 0 = prrtc_debug_nn. */
+int prrtc_debug_nn_multi(const double* tree, uint32_t count, uint32_t dof, const double* q,
+                         uint32_t n_queries, uint32_t group, int device, uint32_t* index, double* sq_dist);
 /* Device Halton values (reference halton_value, sampling.cpp:8-18). */
 int prrtc_debug_halton(const uint32_t* bases, const uint64_t* indices, uint32_t n, int device,
                        double* out);

@@ -126,6 +126,8 @@ SIGNATURES = [
     ("prrtc_debug_fk", C.c_int, [P, DP, C.c_uint32, C.c_uint32, FP, FP]),
     ("prrtc_debug_sphere_hits", C.c_int, [P, FP, DP, C.c_uint32, U8P]),
     ("prrtc_debug_nn", C.c_int, [DP, C.c_uint32, C.c_uint32, DP, C.c_uint32, C.c_int, C.POINTER(C.c_uint32), DP]),
+    ("prrtc_debug_nn_multi", C.c_int, [DP, C.c_uint32, C.c_uint32, DP, C.c_uint32, C.c_uint32, C.c_int,
+                                       C.POINTER(C.c_uint32), DP]),
     ("prrtc_debug_halton", C.c_int, [C.POINTER(C.c_uint32), C.POINTER(C.c_uint64), C.c_uint32, C.c_int, DP]),
     ("prrtc_debug_sample", C.c_int, [P, C.c_uint64, C.c_uint32, DP]),
     ("prrtc_debug_chunk_profile", C.c_int, [P, P, DP, DP, C.c_uint32, C.c_int32, C.c_int,

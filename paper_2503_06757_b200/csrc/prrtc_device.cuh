@@ -251,6 +251,9 @@ struct Ctx {
     int* ictl;       // [32] misc ints
     double* dcfg;    // [8][kMaxDof] scratch configs
     double* sbuf;    // [nthreads] Halton samples of the CTA's current ticket block
+    double* mnn_d;   // [32] multi-sample NN: squared distance per evaluated sample
+    int* mnn_i;      // [32]                  nearest index per evaluated sample
+    int* mnn_ok;     // [32]                  accepted (not duplicate, inside its dynamic domain)
     double* red_d;   // [nwarps]
     int* red_i;      // [nwarps]
     int nthreads;
@@ -330,136 +333,102 @@ __device__ __forceinline__ float3 pose_point(const Ctx& c, int l, int s, float p
 }
 
 // ---------------------------------------------------------------------------
-// forward kinematics for the chunk's states (kinematics.cpp:92-103), FP32
-//   phase A: warps split links, lanes states -> local transform
-//            origin_tf * motion(q) (Rodrigues folded: cos M1 + sin M2 +
-//            (1 - cos) M3, see prrtc_internal.h)
-//   phase B: 3 lanes per state compose world = parent * local row by row
-//   phase C: warps split links, lanes states -> posed coarse centers
+// forward kinematics for the chunk's states (kinematics.cpp:92-103), FP32,
+// one pass: row r of world_l = row r of world_parent * local_l depends only
+// on row r of the parent, so warps take (row, 32-state group) tasks and
+// every lane walks its state's chain link by link in registers:
+//   local_l = origin_tf * motion(q) (Rodrigues folded: cos M1 + sin M2 +
+//             (1 - cos) M3, see prrtc_internal.h; recomputed by each of the
+//             three row lanes of a state instead of staged through smem)
+//   row r of world_l, stored to pose[l][3r..3r+2 | 9+r][s]
+//   coordinate r of the posed coarse centre, stored to ccen[l][r][s]
+// State is the fastest smem index: every access is conflict-free. A branch
+// point (parent != previous link) reads the parent row this lane stored.
 // ---------------------------------------------------------------------------
+__device__ __forceinline__ void sincos_joint(float q, float* sn, float* cs) {
+    // |q| within a few turns (joint limits): 2-constant Cody-Waite reduction
+    // to [-pi, pi], then the SFU pair (abs error ~2^-21 there; FK stays well
+    // inside the 1e-5 m sphere-centre tolerance)
+    const float k = rintf(q * 0.15915494309189535f);
+    const float r = __fmaf_rn(-k, 6.28318548202514648f, __fmaf_rn(-k, -1.7484555314695172e-7f, q));
+    __sincosf(r, sn, cs);
+}
+
 __device__ __noinline__ void fk_chunk(Ctx& c, int cnt) {
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nw = c.nthreads >> 5;
-    const int NS = c.NS, L = c.L, nthreads = c.nthreads;
+    const int NS = c.NS, L = c.L;
     float* const pose = sh(c.pose);
     const float* const qf = sh(c.qf);
     const int4* const info = sh(c.info);
     const float* const geo = sh(c.geo);
     float* const ccen = sh(c.ccen);
-    long long* const prof = c.prof;
-    for (int l = warp; l < L; l += nw) {
-        const int4 inf = info[l];
-        const float* g = geo + l * GEO_STRIDE;
-        for (int s = lane; s < cnt; s += 32) {
-            float* P = pose + l * 12 * NS + s;
+    const int groups = (cnt + 31) >> 5;
+    for (int task = warp; task < 3 * groups; task += nw) {
+        const int r = task % 3;
+        const int s = (task / 3) * 32 + lane;
+        const bool act = s < cnt;
+        const int sr = act ? s : 0;
+        float w0 = 0.f, w1 = 0.f, w2 = 0.f, wt = 0.f;  // row r of the previous link's world pose
+        for (int l = 0; l < L; ++l) {
+            const int4 inf = info[l];  // warp-uniform
+            const float* g = geo + l * GEO_STRIDE;
+            float R[9], t0, t1, t2;
             if (inf.x == PRRTC_JOINT_REVOLUTE) {
-                const float q = qf[inf.z * NS + s];
                 float sn, cs;
-                sincosf(q, &sn, &cs);
+                sincos_joint(qf[inf.z * NS + sr], &sn, &cs);
                 const float omc = 1.0f - cs;
 #pragma unroll
-                for (int k = 0; k < 9; ++k) {
-                    P[k * NS] = __fmaf_rn(cs, g[k], __fmaf_rn(sn, g[9 + k], __fmul_rn(omc, g[18 + k])));
-                }
-                P[9 * NS] = g[27];
-                P[10 * NS] = g[28];
-                P[11 * NS] = g[29];
+                for (int k = 0; k < 9; ++k) R[k] = __fmaf_rn(cs, g[k], __fmaf_rn(sn, g[9 + k], __fmul_rn(omc, g[18 + k])));
+                t0 = g[27];
+                t1 = g[28];
+                t2 = g[29];
             } else {
 #pragma unroll
-                for (int k = 0; k < 9; ++k) P[k * NS] = g[k];
+                for (int k = 0; k < 9; ++k) R[k] = g[k];
                 if (inf.x == PRRTC_JOINT_PRISMATIC) {
-                    const float q = qf[inf.z * NS + s];
-                    P[9 * NS] = __fmaf_rn(g[30], q, g[27]);
-                    P[10 * NS] = __fmaf_rn(g[31], q, g[28]);
-                    P[11 * NS] = __fmaf_rn(g[32], q, g[29]);
+                    const float q = qf[inf.z * NS + sr];
+                    t0 = __fmaf_rn(g[30], q, g[27]);
+                    t1 = __fmaf_rn(g[31], q, g[28]);
+                    t2 = __fmaf_rn(g[32], q, g[29]);
                 } else {
-                    P[9 * NS] = g[27];
-                    P[10 * NS] = g[28];
-                    P[11 * NS] = g[29];
+                    t0 = g[27];
+                    t1 = g[28];
+                    t2 = g[29];
                 }
             }
-        }
-    }
-    __syncthreads();
-    if (prof && tid == 0) prof[2] = clock64();
-    // phase B: lanes (s, r), r in 0..3 (r == 3 idle), whole warps iterate.
-    // Each lane carries its world row of the previous link in registers (the
-    // parent in a chain) and prefetches the next link's local transform, so
-    // one __syncwarp per link orders "all lanes read local l" before "lanes
-    // overwrite their row of link l". Idle lanes read state 0, row 0.
-    const int per = nthreads / 4;
-    for (int sb = 0; sb < cnt; sb += per) {
-        const int s = sb + tid / 4, r = tid & 3;
-        const bool act = (s < cnt) && (r < 3);
-        const int sr = act ? s : 0, rr = act ? r : 0;
-        float w0 = 0.f, w1 = 0.f, w2 = 0.f, wt = 0.f;  // world row rr of link wl
-        int wl = -1;
-        float Rl[9], tl[3];
-        auto load_local = [&](int l) {
-            const float* P = pose + l * 12 * NS + sr;
-#pragma unroll
-            for (int k = 0; k < 9; ++k) Rl[k] = P[k * NS];
-            tl[0] = P[9 * NS];
-            tl[1] = P[10 * NS];
-            tl[2] = P[11 * NS];
-        };
-        if (L > 0) load_local(0);
-        for (int l = 0; l < L; ++l) {
-            const int par = info[l].y;  // warp-uniform
             float n0, n1, n2, nt;
-            if (par < 0) {  // root: world = local, row rr read in place
-                const float* P = pose + l * 12 * NS + sr;
-                n0 = P[(3 * rr + 0) * NS];
-                n1 = P[(3 * rr + 1) * NS];
-                n2 = P[(3 * rr + 2) * NS];
-                nt = P[(9 + rr) * NS];
+            if (inf.y < 0) {  // root: world = local
+                n0 = R[3 * r + 0];
+                n1 = R[3 * r + 1];
+                n2 = R[3 * r + 2];
+                nt = r == 0 ? t0 : (r == 1 ? t1 : t2);
             } else {
-                float a0, a1, a2, tp;
-                if (par == wl) {
-                    a0 = w0;
-                    a1 = w1;
-                    a2 = w2;
-                    tp = wt;
-                } else {  // branch point: the parent's row was written by this lane
-                    const float* Q = pose + par * 12 * NS + sr;
-                    a0 = Q[(3 * rr + 0) * NS];
-                    a1 = Q[(3 * rr + 1) * NS];
-                    a2 = Q[(3 * rr + 2) * NS];
-                    tp = Q[(9 + rr) * NS];
+                float a0 = w0, a1 = w1, a2 = w2, tp = wt;
+                if (inf.y != l - 1) {  // branch point: the parent row this lane stored
+                    const float* Q = pose + inf.y * 12 * NS + sr;
+                    a0 = Q[(3 * r + 0) * NS];
+                    a1 = Q[(3 * r + 1) * NS];
+                    a2 = Q[(3 * r + 2) * NS];
+                    tp = Q[(9 + r) * NS];
                 }
-                n0 = __fmaf_rn(a0, Rl[0], __fmaf_rn(a1, Rl[3], __fmul_rn(a2, Rl[6])));
-                n1 = __fmaf_rn(a0, Rl[1], __fmaf_rn(a1, Rl[4], __fmul_rn(a2, Rl[7])));
-                n2 = __fmaf_rn(a0, Rl[2], __fmaf_rn(a1, Rl[5], __fmul_rn(a2, Rl[8])));
-                nt = __fmaf_rn(a0, tl[0], __fmaf_rn(a1, tl[1], __fmaf_rn(a2, tl[2], tp)));
+                n0 = __fmaf_rn(a0, R[0], __fmaf_rn(a1, R[3], __fmul_rn(a2, R[6])));
+                n1 = __fmaf_rn(a0, R[1], __fmaf_rn(a1, R[4], __fmul_rn(a2, R[7])));
+                n2 = __fmaf_rn(a0, R[2], __fmaf_rn(a1, R[5], __fmul_rn(a2, R[8])));
+                nt = __fmaf_rn(a0, t0, __fmaf_rn(a1, t1, __fmaf_rn(a2, t2, tp)));
             }
-            __syncwarp();  // every lane has read local l (prefetched last iteration)
-            if (act && par >= 0) {
+            if (act) {
                 float* W = pose + l * 12 * NS + s;
                 W[(3 * r + 0) * NS] = n0;
                 W[(3 * r + 1) * NS] = n1;
                 W[(3 * r + 2) * NS] = n2;
                 W[(9 + r) * NS] = nt;
+                // coordinate r of the coarse centre: same expression as pose_pt
+                ccen[l * 3 * NS + r * NS + s] = __fmaf_rn(n0, g[33], __fmaf_rn(n1, g[34], __fmaf_rn(n2, g[35], nt)));
             }
             w0 = n0;
             w1 = n1;
             w2 = n2;
             wt = nt;
-            wl = l;
-            if (l + 1 < L) load_local(l + 1);  // a different link: no hazard
-        }
-        __syncwarp();
-    }
-    __syncthreads();
-    if (prof && tid == 0) prof[3] = clock64();
-    // phase C: coarse centers
-    for (int l = warp; l < L; l += nw) {
-        const float* g = geo + l * GEO_STRIDE;
-        const float gx = g[33], gy = g[34], gz = g[35];
-        for (int s = lane; s < cnt; s += 32) {
-            const float3 o = pose_pt(pose, NS, l, s, gx, gy, gz);
-            float* C = ccen + l * 3 * NS + s;
-            C[0] = o.x;
-            C[NS] = o.y;
-            C[2 * NS] = o.z;
         }
     }
     __syncthreads();
@@ -512,7 +481,7 @@ __device__ __forceinline__ unsigned long long coarse_mask(const SceneV& v, float
     unsigned long long m = 0;
     const int e1 = min(p1, v.ns), e2 = min(p1, v.ns + v.nb);
     int p = p0;
-#pragma unroll 2
+#pragma unroll 4
     for (; p < e1; ++p) {
         float d2;
         const float4 s = v.sph[p];
@@ -520,13 +489,13 @@ __device__ __forceinline__ unsigned long long coarse_mask(const SceneV& v, float
         const float rr = rc + s.w;
         if (d2 < rr * rr) m |= 1ull << p;
     }
-#pragma unroll 2
+#pragma unroll 4
     for (; p < e2; ++p) {
         float d2;
         box_d2(x, y, z, v.box + (p - v.ns) * BOX_STRIDE, d2);
         if (d2 < rc * rc) m |= 1ull << p;
     }
-#pragma unroll 2
+#pragma unroll 4
     for (; p < p1; ++p) {
         float d2;
         const float* C = v.cap + (p - v.ns - v.nb) * CAP_STRIDE;
@@ -702,24 +671,29 @@ __device__ __noinline__ void check_chunk(Ctx& c, int cnt, bool two_stage, bool e
     const int2* const pairs = sh(c.pairs);
     const double* const fine_r64 = c.fine_r64;
     const float cpad = c.cpad;
-    // stage 1: units (link, primitive group) over warps, states over lanes
-    const int G = (v.P >= 8 && L < 2 * nw) ? 2 : 1;
-    const int PG = (v.P + G - 1) / G;
+    // stage 1: the L x P (link, primitive) tests split into nw equal
+    // contiguous ranges, one per warp (a warp walks its links' primitive
+    // sub-ranges), states over lanes
     int flagged = 0;
-    for (int u = warp; u < L * G; u += nw) {
-        const int l = G == 2 ? (u >> 1) : u;
-        const int p0 = (u - l * G) * PG, p1 = min(v.P, p0 + PG);
-        const float rc = geo[l * GEO_STRIDE + 36] + cpad;
-        const int fl = range_flops(v, p0, p1);
-        for (int s = lane; s < cnt; s += 32) {
-            if (k.sgroup[s] < 0) continue;
-            const float* C = ccen + l * 3 * NS + s;
-            const unsigned long long m = coarse_mask(v, C[0], C[NS], C[2 * NS], rc, p0, p1);
-            acc.t += p1 - p0;
-            acc.f += fl;
-            if (m) {
-                atomicOr(&lmask[l * NS + s], m);
-                flagged = 1;
+    {
+        const int T = L * v.P;
+        const int lo = (int)((long long)T * warp / nw), hi = (int)((long long)T * (warp + 1) / nw);
+        for (int i = lo; i < hi;) {
+            const int l = i / v.P;
+            const int p0 = i - l * v.P, p1 = min(v.P, p0 + (hi - i));
+            i += p1 - p0;
+            const float rc = geo[l * GEO_STRIDE + 36] + cpad;
+            const int fl = range_flops(v, p0, p1);
+            for (int s = lane; s < cnt; s += 32) {
+                if (k.sgroup[s] < 0) continue;
+                const float* C = ccen + l * 3 * NS + s;
+                const unsigned long long m = coarse_mask(v, C[0], C[NS], C[2 * NS], rc, p0, p1);
+                acc.t += p1 - p0;
+                acc.f += fl;
+                if (m) {
+                    atomicOr(&lmask[l * NS + s], m);
+                    flagged = 1;
+                }
             }
         }
     }
@@ -961,6 +935,98 @@ __device__ __noinline__ NnOut nn_scan(Ctx& c, const double* cfg, long long cap, 
         }
     }
     return NnOut{i, b};
+}
+
+// ---------------------------------------------------------------------------
+// nearest neighbours of m <= 32 samples over the same published prefix, in
+// one pass: g = nthreads / next_pow2(m) threads per sample stride the node
+// pairs exactly like nn_scan (same loads, same FP64 keys, strict < over
+// increasing indices per thread), then a segmented shuffle argmin (ties to
+// the lowest index) — or, for g > 32, the cross-warp step. Results for
+// sample j land in mnn_d[j] / mnn_i[j]; ends with a barrier.
+// ---------------------------------------------------------------------------
+__device__ __noinline__ void nn_scan_multi(Ctx& c, const double* cfg, long long cap, int count,
+                                           const double* Q, int m, const int* ddf) {
+    __shared__ double s_md[32];
+    __shared__ int s_mi[32];
+    const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5, dof = c.dof, nt = c.nthreads;
+    Q = sh(Q);
+    double* const out_d = sh(c.mnn_d);
+    int* const out_i = sh(c.mnn_i);
+    int mp = 1;
+    while (mp < m) mp <<= 1;
+    const int g = nt / mp;  // threads per sample (power of two)
+    const int j = tid / g, sub = tid - j * g;
+    double best = __longlong_as_double(0x7ff0000000000000ll);  // +inf
+    int bi = 0x7fffffff;
+    const int npairs = (count + 1) >> 1;
+    if (j < m) {
+        const double* q = Q + j * dof;
+        for (int pi = sub; pi < npairs; pi += g) {
+            const int n0 = pi * 2;
+            double a0 = 0.0, a1 = 0.0;
+            if (ddf) asm volatile("prefetch.global.L1 [%0];" ::"l"(ddf + n0));
+            for (int d0 = 0; d0 < dof; d0 += 8) {
+                double2 v[8];
+#pragma unroll
+                for (int k = 0; k < 8; ++k)
+                    if (d0 + k < dof) v[k] = *reinterpret_cast<const double2*>(cfg + (d0 + k) * cap + n0);
+#pragma unroll
+                for (int k = 0; k < 8; ++k) {
+                    if (d0 + k < dof) {
+                        const double qd = q[d0 + k];
+                        const double e0 = __dsub_rn(v[k].x, qd), e1 = __dsub_rn(v[k].y, qd);
+                        a0 = __dadd_rn(a0, __dmul_rn(e0, e0));
+                        a1 = __dadd_rn(a1, __dmul_rn(e1, e1));
+                    }
+                }
+            }
+            if (a0 < best) {
+                best = a0;
+                bi = n0;
+            }
+            if (n0 + 1 < count && a1 < best) {
+                best = a1;
+                bi = n0 + 1;
+            }
+        }
+    }
+    for (int o = min(g, 32) >> 1; o > 0; o >>= 1) {
+        const double ob = __shfl_xor_sync(0xffffffffu, best, o);
+        const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
+        if (ob < best || (ob == best && oi < bi)) {
+            best = ob;
+            bi = oi;
+        }
+    }
+    if (g <= 32) {
+        if (sub == 0 && j < m) {
+            out_d[j] = best;
+            out_i[j] = bi;
+        }
+    } else {
+        if (lane == 0) {
+            s_md[w] = best;
+            s_mi[w] = bi;
+        }
+        __syncthreads();
+        const int wpg = g >> 5;  // warps per sample
+        if (tid < m) {
+            double b = s_md[tid * wpg];
+            int i = s_mi[tid * wpg];
+            for (int k = 1; k < wpg; ++k) {
+                const double ob = s_md[tid * wpg + k];
+                const int oi = s_mi[tid * wpg + k];
+                if (ob < b || (ob == b && oi < i)) {
+                    b = ob;
+                    i = oi;
+                }
+            }
+            out_d[tid] = b;
+            out_i[tid] = i;
+        }
+    }
+    __syncthreads();
 }
 
 }  // namespace dev

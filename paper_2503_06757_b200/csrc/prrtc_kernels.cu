@@ -26,7 +26,7 @@ using namespace dev;
 // ---------------------------------------------------------------------------
 struct SmemLayout {
     size_t robot, scene, pose, ccen, qf, sgroup, sbad, lmask, ictl, dcfg, red_d, red_i,
-        ends, ends_eq, ttab, sbuf, total;
+        ends, ends_eq, ttab, sbuf, mnn, total;
 };
 
 __host__ __device__ inline size_t al16(size_t x) { return (x + 15) & ~size_t(15); }
@@ -52,6 +52,7 @@ __host__ __device__ inline SmemLayout smem_layout(int robot_words, int L, int do
     s.ends_eq = o; o = al16(o + 4 * (size_t)(NS + 2));
     s.ttab = o;  o = al16(o + 8 * (size_t)(kTTab + 1));
     s.sbuf = o;  o = al16(o + 8 * (size_t)nthreads);
+    s.mnn = o;   o = al16(o + (8 + 4 + 4) * 32);
     s.total = o;
     return s;
 }
@@ -104,6 +105,9 @@ __device__ void setup_ctx(Ctx& c, unsigned char* smem, const uint32_t* robot_g, 
     c.htab = limits + 2 * c.dof;
     c.ttab = reinterpret_cast<double*>(smem + lay.ttab);
     c.sbuf = reinterpret_cast<double*>(smem + lay.sbuf);
+    c.mnn_d = reinterpret_cast<double*>(smem + lay.mnn);
+    c.mnn_i = reinterpret_cast<int*>(smem + lay.mnn + 8 * 32);
+    c.mnn_ok = reinterpret_cast<int*>(smem + lay.mnn + 12 * 32);
     c.ttab_n = 0;
     c.nslog = 31 - __clz(NS);
     c.mflog = c.MF > 1 ? 32 - __clz(c.MF - 1) : 0;
@@ -696,6 +700,10 @@ __global__ void __launch_bounds__(NT, MINB) plan_kernel(PlanArgs a) {
                 sh(c.ictl)[IC_TMP1] = from_start;
                 sh(c.ictl)[IC_TMP2] = snap;
                 sh(c.ictl)[IC_TMP3] = refill;
+                // tickets of the block from this one on that are within the
+                // budget: the samples a multi-sample NN pass may consume
+                const unsigned long long rem = tk_cnt - tk_pos;
+                sh(c.ictl)[IC_TMP5] = (int)(it < a.p.budget ? min(rem, a.p.budget - it) : 1ull);
                 sh(c.ictl)[IC_TMP4] = (int)tk_pos++;
                 reinterpret_cast<unsigned long long*>(sh(c.red_d))[0] = tk_base;
             }
@@ -725,22 +733,42 @@ __global__ void __launch_bounds__(NT, MINB) plan_kernel(PlanArgs a) {
                 }
             }
             __syncthreads();
-            const double* smp = sh(c.sbuf) + slot * dof;
-            // ---- nearest neighbour in the extended tree ----
+            // ---- nearest neighbour(s) in the extended tree ----
+            // While the tree is unchanged the samples of the block that the
+            // sequential loop would draw next meet the same snapshot, so
+            // (balanced mode: the extended tree does not alternate) up to 32
+            // of them are evaluated in one pass, bounded to ~8 node pairs per
+            // thread; the loop then continues with the first accepted one and
+            // the rejected ones count as iterations — the same outcome as
+            // one NN scan and accept test per iteration (planner.cpp:216-219).
             TRACE_PHASE(2);
-            const NnOut nr = nn_scan(c, Ts.cfg, a.stride, snap, smp, a.p.dynamic_domain ? Ts.dd : nullptr);
-            const int nn = nr.index;
-            const double d2 = nr.d2;
-            if (d2 == 0.0) continue;  // duplicate of an existing node (planner.cpp:320)
+            int m = 1;
+            if (a.p.balance) m = max(1, min(sh(c.ictl)[IC_TMP5], 2048 / max(1, snap)));
+            nn_scan_multi(c, Ts.cfg, a.stride, snap, sh(c.sbuf) + slot * dof, m,
+                          a.p.dynamic_domain ? Ts.dd : nullptr);
             TRACE_PHASE(3);
-            const double dist = __dsqrt_rn(d2);
-            // the nearest node's config and dynamic-domain flag are loaded
-            // together (one L2 round trip), before the accept decision
-            const double v = tid < dof ? Ts.cfg[(size_t)tid * a.stride + nn] : 0.0;
-            if (a.p.dynamic_domain) {  // DynamicDomain::accept (sampling.hpp:61-75)
-                const int has = Ts.dd[nn];  // one broadcast load (L1: prefetched by the scan)
-                if (__syncthreads_or(has) && !(dist <= R)) continue;
+            if (tid < m) {  // duplicate (planner.cpp:218) / DynamicDomain::accept (sampling.hpp:61-75)
+                const double d2j = sh(c.mnn_d)[tid];
+                int okj = d2j != 0.0;
+                if (okj && a.p.dynamic_domain && Ts.dd[sh(c.mnn_i)[tid]] && !(__dsqrt_rn(d2j) <= R)) okj = 0;
+                sh(c.mnn_ok)[tid] = okj;
             }
+            __syncthreads();
+            unsigned okm = 0;
+            for (int k = 0; k < m; ++k) okm |= (unsigned)sh(c.mnn_ok)[k] << k;
+            const int first = okm ? __ffs(okm) - 1 : m;
+            if (tid == 0) {  // the rejected samples before `first` were iterations too
+                const int extra = (first < m ? first + 1 : m) - 1;
+                tk_pos += extra;
+                used += extra;
+                local_iter += extra;
+            }
+            if (first == m) continue;
+            const double* smp = sh(c.sbuf) + (slot + first) * dof;
+            const int nn = sh(c.mnn_i)[first];
+            const double d2 = sh(c.mnn_d)[first];
+            const double dist = __dsqrt_rn(d2);
+            const double v = tid < dof ? Ts.cfg[(size_t)tid * a.stride + nn] : 0.0;  // L1: the scan read it
             // ---- steer (planner.cpp:48-64) ----
             double* nnc = dc(c, DC_NN);
             double* cnew = dc(c, DC_NEW);
@@ -1024,6 +1052,29 @@ __global__ void debug_nn_kernel(const double* soa, long long cap, int count, int
     }
 }
 
+// nn_scan_multi over groups of `group` queries (the planner's multi-sample
+// pass): the parity tests run it against the reference's nearest_serial
+__global__ void debug_nn_multi_kernel(const double* soa, long long cap, int count, int dof, const double* q,
+                                      int nq, int group, uint32_t* idx, double* d2) {
+    double* qs = reinterpret_cast<double*>(g_dsmem);  // [32][kMaxDof]
+    Ctx c;
+    c.dof = dof;
+    c.nthreads = blockDim.x;
+    c.mnn_d = qs + 32 * kMaxDof;
+    c.mnn_i = reinterpret_cast<int*>(c.mnn_d + 32);
+    for (int b = blockIdx.x * group; b < nq; b += gridDim.x * group) {
+        const int m = min(group, nq - b);
+        for (int k = threadIdx.x; k < m * dof; k += blockDim.x) qs[k] = q[(size_t)b * dof + k];
+        __syncthreads();
+        nn_scan_multi(c, soa, cap, count, qs, m, nullptr);
+        if (threadIdx.x < m) {
+            idx[b + threadIdx.x] = sh(c.mnn_i)[threadIdx.x];
+            d2[b + threadIdx.x] = sh(c.mnn_d)[threadIdx.x];
+        }
+        __syncthreads();
+    }
+}
+
 // planner's Halton path: reciprocal-power table + multiply-high digits
 __device__ double halton_planner(unsigned base, unsigned long long index) {
     double ftab[kHaltonTab];
@@ -1147,6 +1198,15 @@ cudaError_t launch_debug_nn(const double* soa, long long cap, int count, int dof
                             int nq, uint32_t* idx, double* d2, cudaStream_t st) {
     const int grid = min(nq, 148 * 8);
     if (grid > 0) debug_nn_kernel<<<grid, 128, 8 * kMaxDof, st>>>(soa, cap, count, dof, q, nq, idx, d2);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_debug_nn_multi(const double* soa, long long cap, int count, int dof, const double* q,
+                                  int nq, int group, uint32_t* idx, double* d2, cudaStream_t st) {
+    const int grid = min((nq + group - 1) / group, 148 * 8);
+    if (grid > 0)
+        debug_nn_multi_kernel<<<grid, 128, 8 * 32 * kMaxDof + 8 * 32 + 4 * 32, st>>>(soa, cap, count, dof, q, nq,
+                                                                                       group, idx, d2);
     return cudaGetLastError();
 }
 

@@ -42,6 +42,8 @@ cudaError_t launch_debug_hits(const SceneArgs& s, const float* centers, const do
                               int n, int n_prims, uint8_t* hits, cudaStream_t st);
 cudaError_t launch_debug_nn(const double* soa, long long cap, int count, int dof, const double* q,
                             int nq, uint32_t* idx, double* d2, cudaStream_t st);
+cudaError_t launch_debug_nn_multi(const double* soa, long long cap, int count, int dof, const double* q,
+                                  int nq, int group, uint32_t* idx, double* d2, cudaStream_t st);
 cudaError_t launch_debug_halton(const uint32_t* bases, const uint64_t* idx, int n, double* out,
                                 cudaStream_t st);
 double measure_fp32_peak(int sms, cudaStream_t st);

@@ -339,14 +339,15 @@ def debug_sphere_hits(scene, centers, radii, device: int = 0) -> np.ndarray:
     return out.astype(bool)
 
 
-def debug_nn(tree, q, device: int = 0):
-    """Device nearest neighbour: (index[nq], squared distance[nq])."""
+def debug_nn(tree, q, device: int = 0, group: int = 0):
+    """Device nearest neighbour: (index[nq], squared distance[nq]); group > 0
+    runs the planner's multi-sample pass on `group` queries at a time."""
     T = np.ascontiguousarray(np.asarray(tree, dtype=np.float64))
     Q = np.ascontiguousarray(np.asarray(q, dtype=np.float64).reshape(-1, T.shape[1]))
     idx = np.zeros(Q.shape[0], dtype=np.uint32)
     d2 = np.zeros(Q.shape[0], dtype=np.float64)
-    check(_lib.load().prrtc_debug_nn(_dptr(T), T.shape[0], T.shape[1], _dptr(Q), Q.shape[0], device,
-                                     idx.ctypes.data_as(C.POINTER(C.c_uint32)), _dptr(d2)))
+    check(_lib.load().prrtc_debug_nn_multi(_dptr(T), T.shape[0], T.shape[1], _dptr(Q), Q.shape[0], group, device,
+                                           idx.ctypes.data_as(C.POINTER(C.c_uint32)), _dptr(d2)))
     return idx, d2
 
 

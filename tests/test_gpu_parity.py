@@ -172,25 +172,27 @@ def test_nn_exact_with_ties(gpu, oracle):
             q = rng.uniform(-3, 3, (8, dof))
             q[0] = tree[min(1, count - 1)]  # zero distance, first index wins
             q[1] = tree[count // 2]
-            idx, d2 = planner.debug_nn(tree, q)
-            for i in range(len(q)):
-                ri, rd = oracle.nearest_serial(tree, q[i])
-                assert idx[i] == ri, (dof, count, i)
-                assert d2[i] == oracle.sq_distance(tree[ri], q[i])
+            for group in (0, 1, 2, 3, 5, 8):  # single scan, and the planner's multi-sample pass
+                idx, d2 = planner.debug_nn(tree, q, group=group)
+                for i in range(len(q)):
+                    ri, rd = oracle.nearest_serial(tree, q[i])
+                    assert idx[i] == ri, (dof, count, i, group)
+                    assert d2[i] == oracle.sq_distance(tree[ri], q[i])
     # near-ties below FP32 resolution: the FP32 filter must hand them to the
     # exact FP64 refinement (several candidates per thread included)
     for dof in (7, 14):
-        q = rng.uniform(-2, 2, (16, dof))
+        q = rng.uniform(-2, 2, (32, dof))
         for count in (64, 1000, 5000):
             d = rng.normal(size=(count, dof))
             d /= np.linalg.norm(d, axis=1, keepdims=True)
             r = 0.7 + rng.integers(0, 3, count)[:, None] * 1e-12 + rng.uniform(0, 1e-9, (count, 1))
             tree = q[0] + d * r
-            idx, d2 = planner.debug_nn(tree, q)
-            for i in range(len(q)):
-                ri, _ = oracle.nearest_serial(tree, q[i])
-                assert idx[i] == ri, (dof, count, i)
-                assert d2[i] == oracle.sq_distance(tree[ri], q[i])
+            for group in (0, 16, 18, 32):
+                idx, d2 = planner.debug_nn(tree, q, group=group)
+                for i in range(len(q)):
+                    ri, _ = oracle.nearest_serial(tree, q[i])
+                    assert idx[i] == ri, (dof, count, i, group)
+                    assert d2[i] == oracle.sq_distance(tree[ri], q[i])
     # distances (2, 1, 1) -> first distance-1 index
     tree = np.array([[2.0, 0.0], [1.0, 0.0], [-1.0, 0.0]])
     idx, _ = planner.debug_nn(tree, np.zeros((1, 2)))
