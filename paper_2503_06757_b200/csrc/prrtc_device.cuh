@@ -225,7 +225,6 @@ struct Ctx {
     const double* fine_r64;  // global
     const double* limits;    // global [dof][2]
     unsigned fkflops;        // per-state FK + coarse posing flops
-    int nnpar;               // nn_scan buffer parity
     long long* prof;         // per-phase clock64 stamps (debug hook only, else null)
     double* ttab;            // [kTTab + 1]: i / ttab_n for i = 0..ttab_n (edge sample fractions)
     int ttab_n;              // n_cc the table was built for (0 = none)
@@ -257,10 +256,16 @@ struct Ctx {
     double* red_d;   // [nwarps]
     int* red_i;      // [nwarps]
     int nthreads;
-    // stats (per-thread accumulators)
-    unsigned long long tests;
-    unsigned long long flops;  // algorithmic FP32 flops
+    // stats: per-thread slots [nthreads][2] in shared memory (sphere tests,
+    // algorithmic FP32 flops), summed when a CTA leaves a problem
+    unsigned long long* stat;
 };
+
+// The planner keeps its Ctx in shared memory (plan_kernel): every field is
+// CTA-uniform, so reads are broadcast LDS instead of local-memory loads that
+// the acquire fences' L1 invalidations would send to L2. The helpers below
+// that fill it write through thread 0 only in that case (ctx_writer).
+__device__ __forceinline__ bool ctx_writer(const Ctx& c) { return !__isShared(&c) || threadIdx.x == 0; }
 
 // The Ctx lives in the kernel's local-memory frame, so a pointer read from it
 // is generic: loads through it become LD.E (not LDS) and every store through
@@ -546,13 +551,13 @@ __device__ __forceinline__ bool skip_state(const ChunkV& k, int s, bool early_ex
 // i / n for i = 0..n (edge_sample's t, collision.cpp:19) tabulated once per
 // CTA with the same IEEE division, so a state costs no FP64 divide.
 __device__ void build_ttab(Ctx& c, int n_cc) {
-    if (n_cc < 1 || n_cc > kTTab) {
-        c.ttab_n = 0;
-        return;
+    const bool ok = n_cc >= 1 && n_cc <= kTTab;
+    if (ok) {
+        double* tt = sh(c.ttab);
+        for (int i = threadIdx.x; i <= n_cc; i += c.nthreads) tt[i] = __ddiv_rn((double)i, (double)n_cc);
     }
-    double* tt = sh(c.ttab);
-    for (int i = threadIdx.x; i <= n_cc; i += c.nthreads) tt[i] = __ddiv_rn((double)i, (double)n_cc);
-    c.ttab_n = n_cc;
+    __syncthreads();  // every reader of ttab_n is past here before it changes
+    if (ctx_writer(c)) c.ttab_n = ok ? n_cc : 0;
     __syncthreads();
 }
 
@@ -567,8 +572,9 @@ struct StatAcc {
     unsigned long long t = 0, f = 0;
     __device__ explicit StatAcc(Ctx& cc) : c(cc) {}
     __device__ ~StatAcc() {
-        c.tests += t;
-        c.flops += f;
+        unsigned long long* st = sh(c.stat) + 2 * threadIdx.x;
+        st[0] += t;
+        st[1] += f;
     }
 };
 
@@ -867,12 +873,12 @@ struct NnOut {
     double d2;
 };
 __device__ __noinline__ NnOut nn_scan(Ctx& c, const double* cfg, long long cap, int count,
-                                      const double* q, const int* ddf = nullptr) {
+                                      const double* q, int par, const int* ddf = nullptr) {
+    // par: the caller alternates 0/1 between calls (double-buffered
+    // reduction slots: one barrier per call)
     __shared__ double s_bd[2][32];
     __shared__ int s_bi[2][32];
     const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5, nw = c.nthreads >> 5, dof = c.dof;
-    const int par = c.nnpar;  // double-buffered reduction slots: one barrier per call
-    c.nnpar ^= 1;
     q = sh(q);  // the query lives in the dynamic shared window (every caller)
 
     double best = __longlong_as_double(0x7ff0000000000000ll);  // +inf

@@ -26,7 +26,7 @@ using namespace dev;
 // ---------------------------------------------------------------------------
 struct SmemLayout {
     size_t robot, scene, pose, ccen, qf, sgroup, sbad, lmask, ictl, dcfg, red_d, red_i,
-        ends, ends_eq, ttab, sbuf, mnn, total;
+        ends, ends_eq, ttab, sbuf, mnn, stat, total;
 };
 
 __host__ __device__ inline size_t al16(size_t x) { return (x + 15) & ~size_t(15); }
@@ -53,6 +53,7 @@ __host__ __device__ inline SmemLayout smem_layout(int robot_words, int L, int do
     s.ttab = o;  o = al16(o + 8 * (size_t)(kTTab + 1));
     s.sbuf = o;  o = al16(o + 8 * (size_t)nthreads);
     s.mnn = o;   o = al16(o + (8 + 4 + 4) * 32);
+    s.stat = o;  o = al16(o + 16 * (size_t)nthreads);
     s.total = o;
     return s;
 }
@@ -64,59 +65,63 @@ size_t smem_bytes(const RobotArgs& r, int ns_max, int nthreads) {
 // Copies the packed robot into shared memory and wires the context.
 __device__ void setup_ctx(Ctx& c, unsigned char* smem, const uint32_t* robot_g, int robot_words,
                           const double* fine_r64, const double* limits, int NS) {
-    const int tid = threadIdx.x;
-    c.nthreads = blockDim.x;
+    const int tid = threadIdx.x, nthreads = blockDim.x;
     uint32_t* rw = reinterpret_cast<uint32_t*>(smem);
     // 16-byte vector copy (buffer padded to a multiple of 4 words on host)
-    for (int i = tid; i < robot_words / 4; i += c.nthreads) {
+    for (int i = tid; i < robot_words / 4; i += nthreads) {
         reinterpret_cast<uint4*>(rw)[i] = __ldg(reinterpret_cast<const uint4*>(robot_g) + i);
     }
     __syncthreads();
-    c.L = rw[RH_NLINKS];
-    c.dof = rw[RH_DOF];
-    c.S = rw[RH_NFINE];
-    c.NP = rw[RH_NPAIRS];
-    c.MF = rw[RH_MAXFINE];
-    c.info = reinterpret_cast<const int4*>(rw + rw[RH_OFF_INFO]);
-    c.nfine = reinterpret_cast<const int*>(rw + rw[RH_OFF_NFINE]);
-    c.geo = reinterpret_cast<const float*>(rw + rw[RH_OFF_GEO]);
-    c.fine = reinterpret_cast<const float4*>(rw + rw[RH_OFF_FINE]);
-    c.pairs = reinterpret_cast<const int2*>(rw + rw[RH_OFF_PAIRS]);
-    c.bases = rw + rw[RH_OFF_BASES];
-    c.magic = reinterpret_cast<const unsigned long long*>(rw + rw[RH_OFF_MAGIC]);
-    c.flink = reinterpret_cast<const int*>(rw + rw[RH_OFF_FLINK]);
-    c.fine_r64 = fine_r64;
-    c.limits = limits;
-    c.NS = NS;
-    const SmemLayout lay = smem_layout(robot_words, c.L, c.dof, NS, c.nthreads);
-    c.pose = reinterpret_cast<float*>(smem + lay.pose);
-    c.ccen = reinterpret_cast<float*>(smem + lay.ccen);
-    c.qf = reinterpret_cast<float*>(smem + lay.qf);
-    c.sgroup = reinterpret_cast<int*>(smem + lay.sgroup);
-    c.sbad = reinterpret_cast<int*>(smem + lay.sbad);
-    c.lmask = reinterpret_cast<unsigned long long*>(smem + lay.lmask);
-    c.pmask = c.lmask + (size_t)c.L * NS;
-    c.ictl = reinterpret_cast<int*>(smem + lay.ictl);
-    c.dcfg = reinterpret_cast<double*>(smem + lay.dcfg);
-    c.red_d = reinterpret_cast<double*>(smem + lay.red_d);
-    c.red_i = reinterpret_cast<int*>(smem + lay.red_i);
-    c.ends = reinterpret_cast<double*>(smem + lay.ends);
-    c.ends_eq = reinterpret_cast<int*>(smem + lay.ends_eq);
-    c.htab = limits + 2 * c.dof;
-    c.ttab = reinterpret_cast<double*>(smem + lay.ttab);
-    c.sbuf = reinterpret_cast<double*>(smem + lay.sbuf);
-    c.mnn_d = reinterpret_cast<double*>(smem + lay.mnn);
-    c.mnn_i = reinterpret_cast<int*>(smem + lay.mnn + 8 * 32);
-    c.mnn_ok = reinterpret_cast<int*>(smem + lay.mnn + 12 * 32);
-    c.ttab_n = 0;
-    c.nslog = 31 - __clz(NS);
-    c.mflog = c.MF > 1 ? 32 - __clz(c.MF - 1) : 0;
-    c.tests = 0;
-    c.flops = 0;
-    c.fkflops = rw[RH_FKFLOPS];
-    c.nnpar = 0;
-    c.prof = nullptr;
-    c.ns = c.nb = c.nc = c.P = 0;  // scene pointers are wired by load_scene
+    const SmemLayout lay = smem_layout(robot_words, rw[RH_NLINKS], rw[RH_DOF], NS, nthreads);
+    unsigned long long* stat = reinterpret_cast<unsigned long long*>(smem + lay.stat);
+    stat[2 * tid] = 0;
+    stat[2 * tid + 1] = 0;
+    if (ctx_writer(c)) {
+        c.nthreads = nthreads;
+        c.L = rw[RH_NLINKS];
+        c.dof = rw[RH_DOF];
+        c.S = rw[RH_NFINE];
+        c.NP = rw[RH_NPAIRS];
+        c.MF = rw[RH_MAXFINE];
+        c.info = reinterpret_cast<const int4*>(rw + rw[RH_OFF_INFO]);
+        c.nfine = reinterpret_cast<const int*>(rw + rw[RH_OFF_NFINE]);
+        c.geo = reinterpret_cast<const float*>(rw + rw[RH_OFF_GEO]);
+        c.fine = reinterpret_cast<const float4*>(rw + rw[RH_OFF_FINE]);
+        c.pairs = reinterpret_cast<const int2*>(rw + rw[RH_OFF_PAIRS]);
+        c.bases = rw + rw[RH_OFF_BASES];
+        c.magic = reinterpret_cast<const unsigned long long*>(rw + rw[RH_OFF_MAGIC]);
+        c.flink = reinterpret_cast<const int*>(rw + rw[RH_OFF_FLINK]);
+        c.fine_r64 = fine_r64;
+        c.limits = limits;
+        c.NS = NS;
+        c.pose = reinterpret_cast<float*>(smem + lay.pose);
+        c.ccen = reinterpret_cast<float*>(smem + lay.ccen);
+        c.qf = reinterpret_cast<float*>(smem + lay.qf);
+        c.sgroup = reinterpret_cast<int*>(smem + lay.sgroup);
+        c.sbad = reinterpret_cast<int*>(smem + lay.sbad);
+        c.lmask = reinterpret_cast<unsigned long long*>(smem + lay.lmask);
+        c.pmask = c.lmask + (size_t)c.L * NS;
+        c.ictl = reinterpret_cast<int*>(smem + lay.ictl);
+        c.dcfg = reinterpret_cast<double*>(smem + lay.dcfg);
+        c.red_d = reinterpret_cast<double*>(smem + lay.red_d);
+        c.red_i = reinterpret_cast<int*>(smem + lay.red_i);
+        c.ends = reinterpret_cast<double*>(smem + lay.ends);
+        c.ends_eq = reinterpret_cast<int*>(smem + lay.ends_eq);
+        c.htab = limits + 2 * c.dof;
+        c.ttab = reinterpret_cast<double*>(smem + lay.ttab);
+        c.sbuf = reinterpret_cast<double*>(smem + lay.sbuf);
+        c.mnn_d = reinterpret_cast<double*>(smem + lay.mnn);
+        c.mnn_i = reinterpret_cast<int*>(smem + lay.mnn + 8 * 32);
+        c.mnn_ok = reinterpret_cast<int*>(smem + lay.mnn + 12 * 32);
+        c.stat = stat;
+        c.ttab_n = 0;
+        c.nslog = 31 - __clz(NS);
+        c.mflog = c.MF > 1 ? 32 - __clz(c.MF - 1) : 0;
+        c.fkflops = rw[RH_FKFLOPS];
+        c.prof = nullptr;
+        c.ns = c.nb = c.nc = c.P = 0;  // scene pointers are wired by load_scene
+    }
+    __syncthreads();
 }
 
 // Stages one scene's primitives in shared memory (the full
@@ -127,16 +132,19 @@ __device__ void load_scene(Ctx& c, unsigned char* sbase, const uint32_t* scene_g
     const int words = __ldg(scene_g + SH_WORDS);
     for (int i = threadIdx.x; i < words; i += c.nthreads) sw[i] = __ldg(scene_g + i);
     __syncthreads();
-    c.ns = sw[SH_NS];
-    c.nb = sw[SH_NB];
-    c.nc = sw[SH_NC];
-    c.P = c.ns + c.nb + c.nc;
-    c.sph = reinterpret_cast<const float4*>(sw + sw[SH_OFF_S]);
-    c.box = reinterpret_cast<const float*>(sw + sw[SH_OFF_B]);
-    c.cap = reinterpret_cast<const float*>(sw + sw[SH_OFF_C]);
-    c.eps = __uint_as_float(sw[SH_EPS]);
-    c.cpad = __uint_as_float(sw[SH_CPAD]);
-    c.s64 = f64;
+    if (ctx_writer(c)) {
+        c.ns = sw[SH_NS];
+        c.nb = sw[SH_NB];
+        c.nc = sw[SH_NC];
+        c.P = c.ns + c.nb + c.nc;
+        c.sph = reinterpret_cast<const float4*>(sw + sw[SH_OFF_S]);
+        c.box = reinterpret_cast<const float*>(sw + sw[SH_OFF_B]);
+        c.cap = reinterpret_cast<const float*>(sw + sw[SH_OFF_C]);
+        c.eps = __uint_as_float(sw[SH_EPS]);
+        c.cpad = __uint_as_float(sw[SH_CPAD]);
+        c.s64 = f64;
+    }
+    __syncthreads();
 }
 
 // the scene words live right after the robot in shared memory; load_scene
@@ -308,7 +316,7 @@ __device__ long long validate_chain(Ctx& c, const PlanArgs& a, const double* A, 
         const int act = gen_chain_states(c, A, B, n_sub, n_cc, g0, cnt);
         if (threadIdx.x == 0) {
             fk_states += act;
-            c.flops += (unsigned long long)act * c.fkflops;
+            sh(c.stat)[1] += (unsigned long long)act * c.fkflops;  // thread 0's flop slot
         }
         trace_phase(a, 5);  // FK + collision
         check_chunk(c, cnt, a.p.two_stage != 0, a.p.early_exit != 0, false);
@@ -436,7 +444,7 @@ __device__ bool init_problem(Ctx& c, const PlanArgs& a, int prob, unsigned long 
     check_chunk(c, 2, a.p.two_stage != 0, a.p.early_exit != 0, true);
     if (tid == 0) {
         fk_states += 2;
-        c.flops += 2ull * c.fkflops;
+        sh(c.stat)[1] += 2ull * c.fkflops;  // thread 0's flop slot
         // within_limits (planner.cpp:25-31): inclusive bounds
         bool sl = true, gl = true;
         for (int d = 0; d < dof; ++d) {
@@ -570,18 +578,20 @@ __device__ int pick_help(Ctx& c, const PlanArgs& a) {
 // CheckStats counters (collision.hpp:17-25), reduced per warp then per CTA.
 __device__ void flush_stats(Ctx& c, ProbCtl& C, unsigned long long& fk_states,
                             unsigned long long& fine_states) {
+    unsigned long long* st = sh(c.stat) + 2 * threadIdx.x;
+    unsigned long long tests = st[0], flops = st[1];
+    st[0] = 0;
+    st[1] = 0;
     for (int o = 16; o > 0; o >>= 1) {
-        c.tests += __shfl_xor_sync(0xffffffffu, c.tests, o);
-        c.flops += __shfl_xor_sync(0xffffffffu, c.flops, o);
+        tests += __shfl_xor_sync(0xffffffffu, tests, o);
+        flops += __shfl_xor_sync(0xffffffffu, flops, o);
     }
-    if ((threadIdx.x & 31) == 0 && c.tests) atomicAdd(&C.sphere_tests, c.tests);
-    if ((threadIdx.x & 31) == 0 && c.flops) atomicAdd(&C.flops, c.flops);
+    if ((threadIdx.x & 31) == 0 && tests) atomicAdd(&C.sphere_tests, tests);
+    if ((threadIdx.x & 31) == 0 && flops) atomicAdd(&C.flops, flops);
     if (threadIdx.x == 0) {
         if (fk_states) atomicAdd(&C.fk_calls, fk_states);
         if (fine_states) atomicAdd(&C.fine_entries, fine_states);
     }
-    c.tests = 0;
-    c.flops = 0;
     fk_states = 0;
     fine_states = 0;
 }
@@ -600,10 +610,12 @@ __device__ void leave_problem(const PlanArgs& a, int prob, int reason_msg) {
 
 #define TRACE_PHASE(code) trace_phase(a, code)
 
+__shared__ Ctx g_ctx;  // the planner's CTA context (see ctx_writer)
+
 template <int NT, int MINB>
 __global__ void __launch_bounds__(NT, MINB) plan_kernel(PlanArgs a) {
     extern __shared__ __align__(16) unsigned char smem[];
-    Ctx c;
+    Ctx& c = g_ctx;
     setup_ctx(c, smem, a.robot, reinterpret_cast<const int*>(a.robot)[RH_WORDS], a.fine_r64,
               a.limits, a.ns_max);
     const int tid = threadIdx.x;
@@ -612,6 +624,7 @@ __global__ void __launch_bounds__(NT, MINB) plan_kernel(PlanArgs a) {
     unsigned char* sbase = scene_base(smem, robot_words, c.L, dof, c.NS, c.nthreads);
     build_ttab(c, a.p.n_cc);
     const double R = a.p.dd_radius, delta = a.p.delta;
+    int nnpar = 0;  // nn_scan's double-buffered reduction slot
     if (tid == 0 && a.trace) atomicMax(&a.trace[0], 0x7fffffffffffffffull - (unsigned long long)globaltimer());
     if (tid == 0 && a.cta_trace) {
         for (int k = 0; k < kTraceStride; ++k) g_trace[k] = 0;
@@ -620,7 +633,6 @@ __global__ void __launch_bounds__(NT, MINB) plan_kernel(PlanArgs a) {
 
     for (;;) {
         unsigned long long fk_states = 0, fine_states = 0;
-        c.tests = 0;
         int prob = -1;
         // unstarted problems first: claim, stage its scene, initialise
         for (;;) {
@@ -754,8 +766,7 @@ __global__ void __launch_bounds__(NT, MINB) plan_kernel(PlanArgs a) {
                 sh(c.mnn_ok)[tid] = okj;
             }
             __syncthreads();
-            unsigned okm = 0;
-            for (int k = 0; k < m; ++k) okm |= (unsigned)sh(c.mnn_ok)[k] << k;
+            const unsigned okm = __ballot_sync(0xffffffffu, (tid & 31) < m && sh(c.mnn_ok)[tid & 31]);
             const int first = okm ? __ffs(okm) - 1 : m;
             if (tid == 0) {  // the rejected samples before `first` were iterations too
                 const int extra = (first < m ? first + 1 : m) - 1;
@@ -808,7 +819,8 @@ __global__ void __launch_bounds__(NT, MINB) plan_kernel(PlanArgs a) {
             __syncthreads();
             const int snap_o = sh(c.ictl)[IC_TMP2];
             __syncthreads();
-            const NnOut no = nn_scan(c, To.cfg, a.stride, snap_o, cnew);
+            const NnOut no = nn_scan(c, To.cfg, a.stride, snap_o, cnew, nnpar);
+            nnpar ^= 1;
             const int nno = no.index;
             const double d2o = no.d2;
             bool reached = false;
@@ -1039,11 +1051,12 @@ __global__ void debug_nn_kernel(const double* soa, long long cap, int count, int
     Ctx c;
     c.dof = dof;
     c.nthreads = blockDim.x;
-    c.nnpar = 0;
+    int par = 0;
     for (int i = blockIdx.x; i < nq; i += gridDim.x) {
         if (threadIdx.x < dof) qs[threadIdx.x] = q[(size_t)i * dof + threadIdx.x];
         __syncthreads();
-        const NnOut r = nn_scan(c, soa, cap, count, qs);
+        const NnOut r = nn_scan(c, soa, cap, count, qs, par);
+        par ^= 1;
         if (threadIdx.x == 0) {
             idx[i] = r.index;
             d2[i] = r.d2;
