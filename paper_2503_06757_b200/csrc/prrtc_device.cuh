@@ -486,7 +486,7 @@ __device__ __forceinline__ unsigned long long coarse_mask(const SceneV& v, float
     unsigned long long m = 0;
     const int e1 = min(p1, v.ns), e2 = min(p1, v.ns + v.nb);
     int p = p0;
-#pragma unroll 4
+#pragma unroll 2
     for (; p < e1; ++p) {
         float d2;
         const float4 s = v.sph[p];
@@ -494,13 +494,13 @@ __device__ __forceinline__ unsigned long long coarse_mask(const SceneV& v, float
         const float rr = rc + s.w;
         if (d2 < rr * rr) m |= 1ull << p;
     }
-#pragma unroll 4
+#pragma unroll 2
     for (; p < e2; ++p) {
         float d2;
         box_d2(x, y, z, v.box + (p - v.ns) * BOX_STRIDE, d2);
         if (d2 < rc * rc) m |= 1ull << p;
     }
-#pragma unroll 4
+#pragma unroll 2
     for (; p < p1; ++p) {
         float d2;
         const float* C = v.cap + (p - v.ns - v.nb) * CAP_STRIDE;
@@ -799,27 +799,32 @@ __device__ __noinline__ void check_chunk(Ctx& c, int cnt, bool two_stage, bool e
 // computed once into `ends` (each is a full lerp with one FP64 division)
 // and reused by the states and by the appends.
 // ---------------------------------------------------------------------------
-__device__ __forceinline__ double chain_point(const double* A, const double* B, int d, long long k,
-                                              long long n) {
+__device__ __noinline__ double chain_point(const double* A, const double* B, int d, long long k,
+                                           long long n) {
     if (k == 0) return A[d];
     if (k >= n) return B[d];
     return lerp_exact(A[d], B[d], __ddiv_rn((double)k, (double)n));
 }
 
 // Returns the number of active states (each thread owns at most one: NS <= nthreads).
-__device__ int gen_chain_states(Ctx& c, const double* A, const double* B, long long n_sub,
-                                 int n_cc, long long g0, int cnt) {
+__device__ __noinline__ double frac_div(int i, int n) { return __ddiv_rn((double)i, (double)n); }
+
+// Chain indices are 32-bit: a chain holds n_sub * n_cc < 2^30 states (the
+// caller rejects longer ones; joint limits bound n_sub to a few dozen).
+__device__ __noinline__ int gen_chain_states(Ctx& c, const double* A, const double* B, long long n_sub,
+                                 int n_cc, long long g0l, int cnt) {
     const int tid = threadIdx.x, dof = c.dof, NS = c.NS, nthreads = c.nthreads;
     double* const ends = sh(c.ends);
     int* const ends_eq = sh(c.ends_eq);
     int* const sgroup = sh(c.sgroup);
     float* const qf = sh(c.qf);
     const double* const ttab = n_cc == c.ttab_n ? sh(c.ttab) : nullptr;
-    const long long k_lo = g0 / n_cc;
-    const int npts = (int)((g0 + cnt - 1) / n_cc - k_lo) + 2;
+    const unsigned ncc = (unsigned)n_cc, g0 = (unsigned)g0l;
+    const unsigned k_lo = g0 / ncc;
+    const int npts = (int)((g0 + cnt - 1) / ncc - k_lo) + 2;
     for (int idx = tid; idx < npts * dof; idx += nthreads) {
         const int j = idx / dof, d = idx - j * dof;
-        ends[idx] = chain_point(A, B, d, k_lo + j, n_sub);
+        ends[idx] = chain_point(A, B, d, (long long)(k_lo + j), n_sub);
     }
     if (tid == 0) sh(c.ictl)[IC_KLO] = (int)k_lo;
     __syncthreads();
@@ -835,9 +840,9 @@ __device__ int gen_chain_states(Ctx& c, const double* A, const double* B, long l
             sgroup[s] = -1;
             continue;
         }
-        const long long g = g0 + s;
-        const long long k = g / n_cc;
-        const int i = (int)(g - k * n_cc) + 1;
+        const unsigned g = g0 + s;
+        const unsigned k = g / ncc;
+        const int i = (int)(g - k * ncc) + 1;
         const int j = (int)(k - k_lo);
         if (ends_eq[j] && i != n_cc) {
             sgroup[s] = -1;
@@ -848,7 +853,7 @@ __device__ int gen_chain_states(Ctx& c, const double* A, const double* B, long l
         if (i == n_cc) {
             for (int d = 0; d < dof; ++d) qf[d * NS + s] = (float)T[d];
         } else {
-            const double t = ttab ? ttab[i] : __ddiv_rn((double)i, (double)n_cc);
+            const double t = ttab ? ttab[i] : frac_div(i, n_cc);
             for (int d = 0; d < dof; ++d) qf[d * NS + s] = (float)lerp_exact(F[d], T[d], t);
         }
         sgroup[s] = (int)k;

@@ -177,8 +177,13 @@ struct TreeRef {
 // writes would cost an L2 round trip per marker) and is copied out at exit.
 constexpr int kTraceStride = 64;
 __shared__ long long g_trace[kTraceStride];
+__device__ __noinline__ void trace_phase_rec(int code);
 __device__ __forceinline__ void trace_phase(const PlanArgs& a, int code) {
-    if (threadIdx.x != 0 || !a.cta_trace) return;
+    // out of line: ten call sites of the recorder would otherwise bloat the
+    // hot loop's instruction footprint even with tracing off
+    if (threadIdx.x == 0 && a.cta_trace) trace_phase_rec(code);
+}
+__device__ __noinline__ void trace_phase_rec(int code) {
     long long* t = g_trace;
     const long long now = globaltimer();
     const long long cyc = clock64();
@@ -300,6 +305,7 @@ __device__ long long validate_chain(Ctx& c, const PlanArgs& a, const double* A, 
     long long good = 0;
     *stopped = false;
     *last = parent0;
+    if (total >= (1ll << 30)) return 0;  // beyond the 32-bit chain indexing: never valid (see gen_chain_states)
     for (long long g0 = 0; g0 < total; g0 += c.NS) {
         trace_phase(a, 9);  // PRRTC_TRACE: chain states
         if (done_flag) {  // stop flag (planner.cpp:112)
@@ -624,7 +630,6 @@ __global__ void __launch_bounds__(NT, MINB) plan_kernel(PlanArgs a) {
     unsigned char* sbase = scene_base(smem, robot_words, c.L, dof, c.NS, c.nthreads);
     build_ttab(c, a.p.n_cc);
     const double R = a.p.dd_radius, delta = a.p.delta;
-    int nnpar = 0;  // nn_scan's double-buffered reduction slot
     if (tid == 0 && a.trace) atomicMax(&a.trace[0], 0x7fffffffffffffffull - (unsigned long long)globaltimer());
     if (tid == 0 && a.cta_trace) {
         for (int k = 0; k < kTraceStride; ++k) g_trace[k] = 0;
@@ -819,10 +824,9 @@ __global__ void __launch_bounds__(NT, MINB) plan_kernel(PlanArgs a) {
             __syncthreads();
             const int snap_o = sh(c.ictl)[IC_TMP2];
             __syncthreads();
-            const NnOut no = nn_scan(c, To.cfg, a.stride, snap_o, cnew, nnpar);
-            nnpar ^= 1;
-            const int nno = no.index;
-            const double d2o = no.d2;
+            nn_scan_multi(c, To.cfg, a.stride, snap_o, cnew, 1, nullptr);
+            const int nno = sh(c.mnn_i)[0];
+            const double d2o = sh(c.mnn_d)[0];
             bool reached = false;
             int meet_self = new_idx;
             if (d2o == 0.0) {
