@@ -146,7 +146,10 @@ typedef struct prrtc_params {
     uint32_t ctas_per_sm;          /* 0 = as many as co-reside */
     uint32_t deterministic;        /* 1 = single CTA, Halton stride 1: replays
                                       the reference's workers=1 mode */
-    uint32_t _reserved;
+    uint32_t validate_path;        /* 1 = re-validate every returned path on the device
+                                      at 4*n_cc states per edge, fine spheres only, no
+                                      early exit, by a second kernel on the
+                                      same stream (result: prrtc_result.path_check) */
 } prrtc_params;
 
 /* Result of one planning problem: reference PlanResult (planner.hpp:42-51). */
@@ -168,7 +171,7 @@ typedef struct prrtc_result {
                                     (SURVEY.md §8d), for the roofline */
     uint64_t tree_nodes[2];      /* published nodes in start/goal tree */
     int32_t solving_worker;      /* CTA that connected the trees, -1 if none */
-    uint32_t _pad2;
+    uint32_t path_check;         /* validate_path: 0 not checked, 1 valid, 2 invalid */
     char message[128];
 } prrtc_result;
 

@@ -68,7 +68,7 @@ class Params(C.Structure):
         ("threads_per_cta", C.c_uint32),
         ("ctas_per_sm", C.c_uint32),
         ("deterministic", C.c_uint32),
-        ("_reserved", C.c_uint32),
+        ("validate_path", C.c_uint32),
     ]
 
 
@@ -89,7 +89,7 @@ class Result(C.Structure):
         ("flops", C.c_uint64),
         ("tree_nodes", C.c_uint64 * 2),
         ("solving_worker", C.c_int32),
-        ("_pad2", C.c_uint32),
+        ("path_check", C.c_uint32),
         ("message", C.c_char * 128),
     ]
 

@@ -584,6 +584,7 @@ struct Workspace {
     int* d_parent = nullptr;
     int* d_dd = nullptr;
     unsigned* d_ready = nullptr;
+    int* d_vprefix = nullptr;  // [n + 1] path-edge prefix (validate_path)
     cudaEvent_t ev0 = nullptr, ev1 = nullptr;
     cudaStream_t stream = nullptr;
 
@@ -603,6 +604,7 @@ struct Workspace {
         cudaFree(d_parent);
         cudaFree(d_dd);
         cudaFree(d_ready);
+        cudaFree(d_vprefix);
         if (ev0) cudaEventDestroy(ev0);
         if (ev1) cudaEventDestroy(ev1);
         if (stream) cudaStreamDestroy(stream);
@@ -629,7 +631,8 @@ struct Workspace {
             cudaMalloc(&d_cfg, 8 * nnodes * nd) != cudaSuccess ||
             cudaMalloc(&d_parent, 4 * nnodes) != cudaSuccess ||
             cudaMalloc(&d_dd, 4 * nnodes) != cudaSuccess ||
-            cudaMalloc(&d_ready, 4 * nnodes) != cudaSuccess) {
+            cudaMalloc(&d_ready, 4 * nnodes) != cudaSuccess ||
+            cudaMalloc(&d_vprefix, 4 * (nn + 1)) != cudaSuccess) {
             release();
             return set_err(PRRTC_ENOMEM, "plan: device workspace allocation failed (" +
                                              std::to_string((8 * nd + 12) * nnodes) + " bytes of trees)");
@@ -870,6 +873,8 @@ int batch_enqueue(prrtc_batch* b, cudaStream_t st, bool upload) {
     CUDA_TRY(cudaEventRecord(ws->ev0, st));
     CUDA_TRY(launch_plan(b->robot->args(), a, b->grid, st));
     CUDA_TRY(cudaEventRecord(ws->ev1, st));
+    if (b->params.validate_path)  // stream-ordered after the planner, outside its timing
+        CUDA_TRY(launch_validate_paths(b->robot->args(), a, ws->d_vprefix, 4 * sm_count(b->device), st));
     b->launches = 1;
     return PRRTC_OK;
 }
@@ -1014,6 +1019,7 @@ int batch_collect(prrtc_batch* b, prrtc_result* out) {
         r.tree_nodes[0] = (uint64_t)std::max(0, C.published[0]);
         r.tree_nodes[1] = (uint64_t)std::max(0, C.published[1]);
         r.solving_worker = C.winner - 1;
+        if (b->params.validate_path && r.status == PRRTC_SOLVED) r.path_check = C.path_bad ? 2 : 1;
     }
     return PRRTC_OK;
 }

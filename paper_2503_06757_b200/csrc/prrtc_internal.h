@@ -93,6 +93,8 @@ struct ProbCtl {
     int msg;          // 0 none, 1 start infeasible, 2 goal infeasible, 3 capacity, 4 budget, 5 path arena
     long long t_start_ns;
     long long t_end_ns;
+    int path_bad;     // validate_paths_kernel: some edge of the returned path collides
+    int _pad;
 };
 static_assert(sizeof(ProbCtl) <= 128, "ProbCtl must fit 128 bytes");
 

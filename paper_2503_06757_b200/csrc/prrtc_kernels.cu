@@ -893,6 +893,88 @@ __global__ void __launch_bounds__(NT, MINB) plan_kernel(PlanArgs a) {
     }
 }
 
+// ---------------------------------------------------------------------------
+// device re-validation of the returned paths (SURVEY.md §8f
+// rank 1): every edge of every solved problem's path (already in the arena)
+// is checked at 4 * n_cc states, fine spheres only, no early exit — the
+// reference's soundness criterion — by a second kernel on the planner's
+// stream. path_edges_scan_kernel lays the edges out (exclusive prefix over
+// problems, one CTA); validate_paths_kernel takes edges grid-stride, finds
+// the problem by binary search and ORs a collision into ctl[p].path_bad.
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(1024) path_edges_scan_kernel(const ProbCtl* ctl, int n, int* prefix) {
+    __shared__ int part[1024];
+    const int tid = threadIdx.x, per = (n + 1023) / 1024;
+    const int b0 = min(n, tid * per), b1 = min(n, b0 + per);
+    int sum = 0;
+    for (int p = b0; p < b1; ++p) sum += (ctl[p].done == 1 && ctl[p].path_len > 1) ? ctl[p].path_len - 1 : 0;
+    part[tid] = sum;
+    __syncthreads();
+    for (int o = 1; o < 1024; o <<= 1) {  // inclusive Hillis-Steele scan
+        const int v = tid >= o ? part[tid - o] : 0;
+        __syncthreads();
+        part[tid] += v;
+        __syncthreads();
+    }
+    int run = tid ? part[tid - 1] : 0;
+    for (int p = b0; p < b1; ++p) {
+        prefix[p] = run;
+        run += (ctl[p].done == 1 && ctl[p].path_len > 1) ? ctl[p].path_len - 1 : 0;
+    }
+    if (tid == 1023) prefix[n] = part[1023];
+}
+
+__global__ void __launch_bounds__(128) validate_paths_kernel(PlanArgs a, const int* prefix, int n_cc4) {
+    extern __shared__ __align__(16) unsigned char smem[];
+    Ctx c;
+    setup_ctx(c, smem, a.robot, reinterpret_cast<const int*>(a.robot)[RH_WORDS], a.fine_r64, a.limits,
+              a.ns_max);
+    unsigned char* sbase = scene_base(smem, reinterpret_cast<const int*>(a.robot)[RH_WORDS], c.L, c.dof,
+                                      c.NS, c.nthreads);
+    const int total = prefix[a.n_problems];
+    int cur_scene = -1;
+    for (int E = blockIdx.x; E < total; E += gridDim.x) {
+        int lo = 0, hi = a.n_problems - 1;  // last p with prefix[p] <= E
+        while (lo < hi) {
+            const int mid = (lo + hi + 1) >> 1;
+            if (prefix[mid] <= E) lo = mid;
+            else hi = mid - 1;
+        }
+        const int p = lo, e = E - prefix[p];
+        const int si = a.prob_scene[p];
+        if (si != cur_scene) {
+            load_scene(c, sbase, a.scene_words[si], a.scene_f64[si]);
+            cur_scene = si;
+        }
+        const double* A = a.arena + a.ctl[p].path_off + (size_t)e * c.dof;
+        double* sa = dc(c, DC_A);
+        double* sb = dc(c, DC_B);
+        if (threadIdx.x < c.dof) {
+            sa[threadIdx.x] = A[threadIdx.x];
+            sb[threadIdx.x] = A[c.dof + threadIdx.x];
+        }
+        __syncthreads();
+        int bad = 0;
+        for (int g0 = 0; g0 < n_cc4; g0 += c.NS) {
+            const int cnt = min(c.NS, n_cc4 - g0);
+            gen_chain_states(c, sa, sb, 1, n_cc4, g0, cnt);
+            check_chunk(c, cnt, false, false, false);
+            bad |= sh(c.ictl)[IC_FIRSTBAD] != kNoBad;
+            __syncthreads();
+        }
+        if (threadIdx.x == 0 && bad) atomicOr(&a.ctl[p].path_bad, 1);
+    }
+}
+
+cudaError_t launch_validate_paths(const RobotArgs& r, const PlanArgs& a, int* prefix, int grid, cudaStream_t st) {
+    path_edges_scan_kernel<<<1, 1024, 0, st>>>(a.ctl, a.n_problems, prefix);
+    const size_t sm = smem_bytes(r, a.ns_max, 128);
+    cudaError_t e = cudaFuncSetAttribute(validate_paths_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+    if (e != cudaSuccess) return e;
+    validate_paths_kernel<<<grid, 128, sm, st>>>(a, prefix, 4 * a.p.n_cc);
+    return cudaGetLastError();
+}
+
 // CTA size variants: 128 threads (4 warps, up to 4 CTAs/SM) and 256 threads
 // (8 warps, 2 CTAs/SM: each iteration's parallel phases finish faster).
 using PlanFn = void (*)(PlanArgs);

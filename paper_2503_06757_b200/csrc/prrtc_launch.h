@@ -27,6 +27,9 @@ size_t smem_bytes(const RobotArgs& r, int ns_max, int nthreads);
 
 // Persistent planner: grid CTAs solve a.n_problems problems.
 cudaError_t launch_plan(const RobotArgs& r, PlanArgs a, int grid, cudaStream_t st);
+// Device re-validation of the solved problems' paths (after launch_plan on
+// the same stream): prefix = [n_problems + 1] ints of scratch.
+cudaError_t launch_validate_paths(const RobotArgs& r, const PlanArgs& a, int* prefix, int grid, cudaStream_t st);
 // Max co-resident planner CTAs per SM for this configuration.
 int plan_occupancy(const RobotArgs& r, int ns_max, int nthreads);
 

@@ -209,6 +209,7 @@ class PlannerParams:  # planner.hpp:21-40 (+ device knobs)
     threads_per_cta: int = 0
     ctas_per_sm: int = 0
     deterministic: bool = False
+    validate_path: bool = False  # device re-validation of returned paths
 
     def resolved_dd_radius(self) -> float:
         return self.dd_radius if self.dd_radius > 0.0 else 4.0 * self.delta
@@ -233,6 +234,7 @@ class PlannerParams:  # planner.hpp:21-40 (+ device knobs)
         p.threads_per_cta = self.threads_per_cta
         p.ctas_per_sm = self.ctas_per_sm
         p.deterministic = int(self.deterministic)
+        p.validate_path = int(self.validate_path)
         return p
 
 
@@ -256,3 +258,4 @@ class PlanResult:  # planner.hpp:42-51
     device_time_ms: float = 0.0
     tree_nodes: tuple = (0, 0)
     flops: int = 0
+    path_check: int = 0  # validate_path: 0 not checked, 1 valid, 2 invalid

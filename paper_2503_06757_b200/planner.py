@@ -124,6 +124,7 @@ def _to_result(r: Result, dof: int) -> PlanResult:
         device_time_ms=r.device_time_ms,
         tree_nodes=(int(r.tree_nodes[0]), int(r.tree_nodes[1])),
         flops=int(r.flops),
+        path_check=int(r.path_check),
     )
 
 
@@ -164,6 +165,7 @@ class BatchResult:
         self.iterations_total = a["iterations_total"].copy()
         self.device_time_ms = a["device_time_ms"].copy()
         self.flops = a["flops"].copy()
+        self.path_check = a["path_check"].copy()
         lens = a["path_len"]
         self.paths = []
         for i in range(n):
