@@ -161,6 +161,87 @@ def traffic_from_profiles():
     return None
 
 
+def bench_extras(dev, params):
+    """BASELINE configs 3-5 beside the headline (informational, untimed by the
+    driver): Fetch / Baxter 1000-problem batches (configs 3, 4), a 10k mixed
+    three-robot batch (config 5; three device batches on three streams,
+    tree_capacity 20000 so 10k resident problems fit in HBM) and the
+    dynamic-obstacle replanning loop (config 5: 100 frames, 3 spheres moving
+    1 cm/frame, prrtc_scene_update + prrtc_plan per frame)."""
+    import torch
+    from paper_2503_06757_b200 import planner, replan
+    from paper_2503_06757_b200.model import PlannerParams, PlanStatus
+    import copy
+
+    def robot_params(robot, base):
+        # the reference's default dynamic-domain radius (4 delta = 2.0,
+        # planner.hpp:37) starves exploration in 14-D (uniform samples are
+        # almost never within 2.0 of a failed node): the reference itself
+        # solves ~6% of these Baxter problems with it. Scale it with the
+        # dimension (4 delta * dof / 7) for the dual-arm robot.
+        p = copy.copy(base)
+        if robot == "baxter":
+            p.dd_radius = 4.0 * p.delta * 14 / 7
+        return p
+
+    out = {"robots": {}}
+    for robot in ("fetch", "baxter"):
+        model, scenes, S, G, kinds = load_workload(robot, 1000)
+        rp = robot_params(robot, params)
+        b = planner.Batch(model, scenes, S, G, rp, device=dev)
+        b.launch()
+        b.results()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        ms = []
+        for _ in range(3):
+            e0.record()
+            b.launch(torch.cuda.current_stream().cuda_stream)
+            e1.record()
+            torch.cuda.synchronize()
+            ms.append(e0.elapsed_time(e1))
+        res = b.results()
+        ok = [r.status == PlanStatus.Solved for r in res]
+        dv = [r.device_time_ms for r in res if r.status == PlanStatus.Solved]
+        out["robots"][robot] = {"problems_per_s": len(S) / (statistics.median(ms) / 1e3),
+                                "success_rate": float(np.mean(ok)), "device_ms_median": float(np.median(dv)),
+                                "device_ms_p95": float(np.percentile(dv, 95)), "dof": model.dof,
+                                "dd_radius": rp.resolved_dd_radius(), "problems": len(S)}
+        del b
+    # 10k mixed batch: three robots' batches concurrently on three streams
+    mp = PlannerParams(tree_capacity=20000)
+    batches, streams = [], []
+    for robot, n in (("panda", 3334), ("fetch", 3333), ("baxter", 3333)):
+        model, scenes, S, G, _ = load_workload(robot, 1000)
+        reps = -(-n // len(S))
+        batches.append(planner.Batch(model, (scenes * reps)[:n], np.tile(S, (reps, 1))[:n], np.tile(G, (reps, 1))[:n],
+                                     robot_params(robot, mp), device=dev))
+        streams.append(torch.cuda.Stream(device=dev))
+    for b, st in zip(batches, streams):
+        b.launch(st.cuda_stream)
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    for b, st in zip(batches, streams):
+        b.launch(st.cuda_stream)
+    torch.cuda.synchronize()
+    mix_ms = (time.perf_counter() - t0) * 1e3
+    mok = [r.status == PlanStatus.Solved for b in batches for r in b.results()]
+    out["mixed_10k"] = {"problems": len(mok), "problems_per_s": len(mok) / (mix_ms / 1e3),
+                        "success_rate": float(np.mean(mok)), "tree_capacity": 20000,
+                        "timing": "host wall clock around three concurrent stream launches + sync"}
+    del batches
+    # replanning loop
+    model, scenes, S, G, kinds = load_workload("panda", 1000)
+    i = int(np.where(kinds == "table_pick")[0][0])
+    frames = replan.run(model, scenes[i], S[i], G[i], frames=100, params=params, device=dev)
+    wall = [f.wall_ms for f in frames]
+    ok = [f.result.status == PlanStatus.Solved for f in frames]
+    out["replanning"] = {"frames": len(frames), "frame_ms_median": float(np.median(wall)),
+                         "frame_ms_p95": float(np.percentile(wall, 95)), "success_rate": float(np.mean(ok)),
+                         "api": "prrtc_scene_update + prrtc_plan per frame (host wall clock)",
+                         "obstacles": "3 spheres r=0.05 moving 1 cm/frame through a table_pick scene"}
+    return out
+
+
 def run_reference(args):
     world, rank, _ = dist_setup()
     from paper_2503_06757_b200.model import PlannerParams
@@ -254,20 +335,24 @@ def run_b200(args):
             e2e_ms.append((time.perf_counter() - t0) * 1e3)
         e2e_solved = float(np.mean(er.status == PlanStatus.Solved))
         h2d = n * model.dof * 8 * 2 + n * (8 + 24 + 4)
-        used = sum(len(p) for p in er.paths) * model.dof
+        used = int(er.path_offsets[-1])
         prefix = min(model.dof * 4096 * n, 1 << 16)
         d2h = 128 + 128 * n + 8 * prefix + 8 * max(0, used - prefix)
         # ---- single-problem latency (prrtc_plan, host wall clock) ----
         idx = list(range(0, n, max(1, n // args.latency_samples)))[: args.latency_samples]
         for i in idx[:5]:
             planner.plan(model, scenes[i], S[i], G[i], params, device=dev)
-        lat, dlat, lst = [], [], []
+        lat, dlat, lst, lcost = [], [], [], []
         for i in idx:
             r = planner.plan(model, scenes[i], S[i], G[i], params, device=dev)
             lst.append(r.status == PlanStatus.Solved)
             if r.status == PlanStatus.Solved:
                 lat.append(r.wall_time_ms)
                 dlat.append(r.device_time_ms)
+                lcost.append(r.cost)
+        from paper_2503_06757_b200 import suite
+        q = suite.summarize_values(lat)  # Table-I statistics (bench.cpp:90-109)
+        extras = {} if args.no_extras else bench_extras(dev, params)
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": max(3, args.warmup), "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
@@ -277,9 +362,10 @@ def run_b200(args):
             "success_by_scene": {k: float(np.mean([s for s, kk in zip(solved, kinds) if kk == k]))
                                  for k in ("table_pick", "bookshelf", "cage")},
             "mean_cost": float(np.mean([r.cost for r in res if r.status == PlanStatus.Solved])),
-            "latency_ms": {"median": float(np.median(lat)), "p95": float(np.percentile(lat, 95)),
+            "latency_ms": {"median": q.median, "p95": q.p95, "mean": q.mean, "q1": q.q1, "q3": q.q3, "max": q.max,
                            "device_median": float(np.median(dlat)), "samples": len(idx),
-                           "success_rate": float(np.mean(lst)), "api": "prrtc_plan (host wall clock)"},
+                           "success_rate": float(np.mean(lst)), "mean_cost": float(np.mean(lcost)),
+                           "api": "prrtc_plan (host wall clock), params.workers = 0 (2 CTAs per SM)"},
             "e2e": {"value": n / (statistics.median(e2e_ms) / 1e3), "unit": UNIT, "h2d_bytes_per_step": int(h2d),
                     "d2h_bytes_per_step": int(d2h), "success_rate": float(e2e_solved),
                     "api": "prrtc_plan_batch (host buffers)"},
@@ -290,6 +376,7 @@ def run_b200(args):
                          "algorithmic_flops_per_launch": flops, "traffic": traffic_from_profiles()},
             "gpu_launches": args.steps,
             "clocks": clk.summary(),
+            **extras,
         }
         if world == 1 and not args.no_cpu_baseline:
             threads = os.cpu_count() or 1
@@ -317,6 +404,7 @@ def main():
     ap.add_argument("--problems", type=int, default=1000)
     ap.add_argument("--latency-samples", type=int, default=100)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-extras", action="store_true", help="skip the Fetch/Baxter/mixed/replanning extras")
     args = ap.parse_args()
     if args.impl == "reference":
         return run_reference(args)

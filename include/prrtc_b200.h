@@ -219,6 +219,11 @@ int prrtc_plan_batch(const prrtc_robot* robot, const prrtc_scene* const* scenes,
                      uint32_t dof, const prrtc_params* params, prrtc_result* out);
 
 void prrtc_result_free(prrtc_result* result);
+/* Frees the paths of n results (prrtc_plan_batch output) in one call. */
+void prrtc_results_free(prrtc_result* results, uint32_t n);
+/* Copies the paths of n results back to back into out (doubles, config-major;
+   NULL to only size) and writes offsets[n + 1] (in doubles). */
+int prrtc_results_pack_paths(const prrtc_result* results, uint32_t n, double* out, uint64_t* offsets);
 
 /* Device-resident batches: inputs uploaded once, then run repeatedly. Used to
    time the device work alone (bench `value`); prrtc_plan_batch is the same

@@ -116,6 +116,9 @@ SIGNATURES = [
     ("prrtc_plan", C.c_int, [P, P, DP, DP, C.c_uint32, C.POINTER(Params), C.POINTER(Result)]),
     ("prrtc_plan_batch", C.c_int, [P, C.POINTER(P), C.c_uint32, DP, DP, C.c_uint32, C.POINTER(Params), C.POINTER(Result)]),
     ("prrtc_result_free", None, [C.POINTER(Result)]),
+    ("prrtc_results_free", None, [C.POINTER(Result), C.c_uint32]),
+    ("prrtc_results_pack_paths", C.c_int, [C.POINTER(Result), C.c_uint32, C.POINTER(C.c_double),
+                                           C.POINTER(C.c_uint64)]),
     ("prrtc_batch_create", C.c_int, [P, C.POINTER(P), C.c_uint32, DP, DP, C.c_uint32, C.POINTER(Params), C.POINTER(P)]),
     ("prrtc_batch_launch", C.c_int, [P, P]),
     ("prrtc_batch_results", C.c_int, [P, C.POINTER(Result)]),

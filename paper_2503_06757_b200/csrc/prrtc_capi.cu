@@ -1103,6 +1103,24 @@ void prrtc_result_free(prrtc_result* r) {
     }
 }
 
+void prrtc_results_free(prrtc_result* r, uint32_t n) {
+    if (!r) return;
+    for (uint32_t i = 0; i < n; ++i) prrtc_result_free(r + i);
+}
+
+int prrtc_results_pack_paths(const prrtc_result* r, uint32_t n, double* out, uint64_t* offsets) {
+    if (!r || !offsets) return set_err(PRRTC_EINVAL, "prrtc_results_pack_paths: null argument");
+    uint64_t o = 0;
+    for (uint32_t i = 0; i < n; ++i) {
+        offsets[i] = o;
+        const uint64_t k = r[i].path ? (uint64_t)r[i].path_len * r[i].dof : 0;
+        if (k && out) std::memcpy(out + o, r[i].path, 8 * k);
+        o += k;
+    }
+    offsets[n] = o;
+    return PRRTC_OK;
+}
+
 // ---------------------------------------------------------------------------
 // batched collision checking + parity hooks
 // ---------------------------------------------------------------------------

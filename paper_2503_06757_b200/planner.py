@@ -152,8 +152,9 @@ _RESULT_DTYPE = None
 
 class BatchResult:
     """Array view of a batch's results (no per-problem Python objects):
-    status / cost / iterations_total / device_time_ms / flops arrays and one
-    path array per problem (empty unless solved)."""
+    status / cost / iterations_total / device_time_ms / flops / path_check
+    arrays, and all paths back to back in `path_data` (config-major doubles)
+    with `path_offsets[n + 1]` (in doubles); `paths` gives per-problem views."""
 
     def __init__(self, res, n: int, dof: int):
         global _RESULT_DTYPE
@@ -166,14 +167,18 @@ class BatchResult:
         self.device_time_ms = a["device_time_ms"].copy()
         self.flops = a["flops"].copy()
         self.path_check = a["path_check"].copy()
-        lens = a["path_len"]
-        self.paths = []
-        for i in range(n):
-            if lens[i]:
-                self.paths.append(np.ctypeslib.as_array(res[i].path, shape=(int(lens[i]) * dof,))
-                                  .reshape(-1, dof).copy())
-            else:
-                self.paths.append(np.zeros((0, dof)))
+        self.dof = dof
+        lib = _lib.load()
+        self.path_offsets = np.zeros(n + 1, dtype=np.uint64)
+        offp = self.path_offsets.ctypes.data_as(C.POINTER(C.c_uint64))
+        check(lib.prrtc_results_pack_paths(res, n, None, offp))
+        self.path_data = np.empty(int(self.path_offsets[-1]), dtype=np.float64)
+        check(lib.prrtc_results_pack_paths(res, n, _dptr(self.path_data), offp))
+
+    @property
+    def paths(self) -> list:
+        o = self.path_offsets.astype(np.int64)
+        return [self.path_data[o[i]:o[i + 1]].reshape(-1, self.dof) for i in range(len(o) - 1)]
 
 
 def _cfg(q, dof: int, what: str) -> np.ndarray:
@@ -223,10 +228,7 @@ def _plan_batch_raw(model, scenes, starts, goals, params, device):
 
 
 def _free(res, n):
-    lib = _lib.load()
-    for i in range(n):
-        if res[i].path:
-            lib.prrtc_result_free(C.byref(res[i]))
+    _lib.load().prrtc_results_free(res, n)
 
 
 def plan_batch(model, scenes, starts, goals, params: PlannerParams | None = None,

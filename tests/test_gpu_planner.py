@@ -179,3 +179,25 @@ def test_device_path_validation_agrees_with_reference(gpu, oracle, robot):
     off = PlannerParams(tree_capacity=20000)
     r0 = planner.plan_batch(m, scenes[:4], S[:4], G[:4], off)
     assert all(r.path_check == 0 for r in r0)
+
+
+def test_replanning_loop_with_scene_updates(gpu, oracle):
+    """BASELINE config 5: moving obstacles pushed with prrtc_scene_update
+    between plans; every frame's path re-validates in THAT frame's scene."""
+    from paper_2503_06757_b200 import replan
+    m = robots.get("panda")
+    kind, pid, s, g = next(p for p in load_problems("panda", 50) if p[0] == "table_pick")
+    static, _ = make_scene("panda", kind, pid)
+    params = PlannerParams(tree_capacity=20000)
+    frames = replan.run(m, static, s, g, frames=12, obstacles=replan.MovingSpheres(step=0.08), params=params)
+    solved = 0
+    for f in frames:
+        assert len(f.scene.primitives) == len(static.primitives) + 3
+        r = f.result
+        if r.status == PlanStatus.Solved:
+            solved += 1
+            check_path(oracle, m, f.scene, r, s, g, params)
+        else:
+            ref = oracle.plan(m, f.scene, s, g, PlannerParams(workers=1, tree_capacity=20000))
+            assert ref.status != PlanStatus.Solved or r.status == PlanStatus.Failed
+    assert solved >= 8
