@@ -172,21 +172,30 @@ __device__ __forceinline__ void sph_d2(float px, float py, float pz, float4 s, f
     const float dx = px - s.x, dy = py - s.y, dz = pz - s.z;
     d2 = fmaf(dx, dx, fmaf(dy, dy, dz * dz));
 }
+// Primitive records are 16-byte aligned in shared memory (scene words:
+// 12-word header, float4 spheres, 16-float boxes, 8-float capsules), so each
+// is fetched with 128-bit loads (2 / 4 LDS.128 instead of 8 / 15 LDS.32).
 __device__ __forceinline__ void cap_d2(float px, float py, float pz, const float* c, float& d2) {
-    const float pax = px - c[0], pay = py - c[1], paz = pz - c[2];
-    float t = fmaf(pax, c[3], fmaf(pay, c[4], paz * c[5])) * c[6];
+    const float4 c0 = reinterpret_cast<const float4*>(c)[0];  // a.xyz, ab.x
+    const float4 c1 = reinterpret_cast<const float4*>(c)[1];  // ab.yz, 1/|ab|^2, r
+    const float pax = px - c0.x, pay = py - c0.y, paz = pz - c0.z;
+    float t = fmaf(pax, c0.w, fmaf(pay, c1.x, paz * c1.y)) * c1.z;
     t = fminf(fmaxf(t, 0.0f), 1.0f);
-    const float dx = fmaf(-t, c[3], pax), dy = fmaf(-t, c[4], pay), dz = fmaf(-t, c[5], paz);
+    const float dx = fmaf(-t, c0.w, pax), dy = fmaf(-t, c1.x, pay), dz = fmaf(-t, c1.y, paz);
     d2 = fmaf(dx, dx, fmaf(dy, dy, dz * dz));
 }
 __device__ __forceinline__ void box_d2(float px, float py, float pz, const float* b, float& d2) {
-    const float wx = px - b[9], wy = py - b[10], wz = pz - b[11];
-    const float lx = fmaf(b[0], wx, fmaf(b[1], wy, b[2] * wz));
-    const float ly = fmaf(b[3], wx, fmaf(b[4], wy, b[5] * wz));
-    const float lz = fmaf(b[6], wx, fmaf(b[7], wy, b[8] * wz));
-    const float dx = lx - fminf(fmaxf(lx, -b[12]), b[12]);
-    const float dy = ly - fminf(fmaxf(ly, -b[13]), b[13]);
-    const float dz = lz - fminf(fmaxf(lz, -b[14]), b[14]);
+    const float4 b0 = reinterpret_cast<const float4*>(b)[0];  // M00 M01 M02 M10
+    const float4 b1 = reinterpret_cast<const float4*>(b)[1];  // M11 M12 M20 M21
+    const float4 b2 = reinterpret_cast<const float4*>(b)[2];  // M22 tx ty tz
+    const float4 b3 = reinterpret_cast<const float4*>(b)[3];  // hx hy hz -
+    const float wx = px - b2.y, wy = py - b2.z, wz = pz - b2.w;
+    const float lx = fmaf(b0.x, wx, fmaf(b0.y, wy, b0.z * wz));
+    const float ly = fmaf(b0.w, wx, fmaf(b1.x, wy, b1.y * wz));
+    const float lz = fmaf(b1.z, wx, fmaf(b1.w, wy, b2.x * wz));
+    const float dx = lx - fminf(fmaxf(lx, -b3.x), b3.x);
+    const float dy = ly - fminf(fmaxf(ly, -b3.y), b3.y);
+    const float dz = lz - fminf(fmaxf(lz, -b3.z), b3.z);
     d2 = fmaf(dx, dx, fmaf(dy, dy, dz * dz));
 }
 
@@ -376,7 +385,10 @@ __device__ __noinline__ void fk_chunk(Ctx& c, int cnt) {
         float w0 = 0.f, w1 = 0.f, w2 = 0.f, wt = 0.f;  // row r of the previous link's world pose
         for (int l = 0; l < L; ++l) {
             const int4 inf = info[l];  // warp-uniform
-            const float* g = geo + l * GEO_STRIDE;
+            float g[36];  // the link's geometry record, 9 x 128-bit broadcast loads
+#pragma unroll
+            for (int k = 0; k < 9; ++k)
+                reinterpret_cast<float4*>(g)[k] = reinterpret_cast<const float4*>(geo + l * GEO_STRIDE)[k];
             float R[9], t0, t1, t2;
             if (inf.x == PRRTC_JOINT_REVOLUTE) {
                 float sn, cs;
