@@ -832,6 +832,25 @@ __device__ __noinline__ int gen_chain_states(Ctx& c, const double* A, const doub
     float* const qf = sh(c.qf);
     const double* const ttab = n_cc == c.ttab_n ? sh(c.ttab) : nullptr;
     const unsigned ncc = (unsigned)n_cc, g0 = (unsigned)g0l;
+    if (n_sub == 1) {
+        // a single edge (extend, path checks): states straight from A and B,
+        // one (state, dimension) item per thread, no chain-point staging
+        const double* As = sh(A);
+        const double* Bs = sh(B);
+        bool eq = true;  // bitwise-equal edge: one check of the far end (collision.cpp:215)
+        for (int d = 0; d < dof; ++d) eq &= As[d] == Bs[d];
+        for (int idx = tid; idx < dof * NS; idx += nthreads) {
+            const int d = idx >> c.nslog, s = idx & (NS - 1);
+            const int i = (int)g0 + s + 1;
+            const bool act = s < cnt && !(eq && i != n_cc);
+            if (d == 0) sgroup[s] = act ? 0 : -1;
+            if (!act) continue;
+            qf[idx] = i == n_cc ? (float)Bs[d]
+                                : (float)lerp_exact(As[d], Bs[d], ttab ? ttab[i] : frac_div(i, n_cc));
+        }
+        __syncthreads();
+        return eq ? ((int)g0 + cnt == n_cc ? 1 : 0) : cnt;
+    }
     const unsigned k_lo = g0 / ncc;
     const int npts = (int)((g0 + cnt - 1) / ncc - k_lo) + 2;
     for (int idx = tid; idx < npts * dof; idx += nthreads) {
