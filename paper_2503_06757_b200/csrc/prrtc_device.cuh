@@ -987,8 +987,13 @@ __device__ __noinline__ NnOut nn_scan(Ctx& c, const double* cfg, long long cap, 
 // the lowest index) — or, for g > 32, the cross-warp step. Results for
 // sample j land in mnn_d[j] / mnn_i[j]; ends with a barrier.
 // ---------------------------------------------------------------------------
+// With `accept` set, the reducing thread of sample j also evaluates the
+// planner's acceptance right away (duplicate, planner.cpp:218; dynamic
+// domain with radius R when ddf is given, sampling.hpp:61-75) into
+// mnn_ok[j], saving the caller a pass and a barrier.
 __device__ __noinline__ void nn_scan_multi(Ctx& c, const double* cfg, long long cap, int count,
-                                           const double* Q, int m, const int* ddf) {
+                                           const double* Q, int m, const int* ddf, bool accept = false,
+                                           double R = 0.0) {
     __shared__ double s_md[32];
     __shared__ int s_mi[32];
     const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5, dof = c.dof, nt = c.nthreads;
@@ -1045,6 +1050,7 @@ __device__ __noinline__ void nn_scan_multi(Ctx& c, const double* cfg, long long 
         if (sub == 0 && j < m) {
             out_d[j] = best;
             out_i[j] = bi;
+            if (accept) sh(c.mnn_ok)[j] = best != 0.0 && !(ddf && ddf[bi] && !(__dsqrt_rn(best) <= R));
         }
     } else {
         if (lane == 0) {
@@ -1066,6 +1072,7 @@ __device__ __noinline__ void nn_scan_multi(Ctx& c, const double* cfg, long long 
             }
             out_d[tid] = b;
             out_i[tid] = i;
+            if (accept) sh(c.mnn_ok)[tid] = b != 0.0 && !(ddf && ddf[i] && !(__dsqrt_rn(b) <= R));
         }
     }
     __syncthreads();

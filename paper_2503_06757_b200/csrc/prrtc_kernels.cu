@@ -535,7 +535,9 @@ __device__ int pick_help(Ctx& c, const PlanArgs& a) {
         int bk = 0x7fffffff, bp = -1;
         for (int q = tid; q < a.n_problems; q += c.nthreads) {
             const ProbCtl& C = a.ctl[q];
-            if (ld_acquire(&C.started) == 1 && ld_acquire(&C.done) == DONE_RUNNING &&
+            // relaxed scan (an acquire per problem would invalidate L1 a
+            // thousand times); the chosen problem is acquired below
+            if (ld_relaxed(&C.started) == 1 && ld_relaxed(&C.done) == DONE_RUNNING &&
                 __ldcg(&C.iters) < a.p.budget) {
                 const int k = __ldcg(&C.active);
                 if (k < bk) {
@@ -567,6 +569,7 @@ __device__ int pick_help(Ctx& c, const PlanArgs& a) {
             }
             if (p >= 0) {
                 atomicAdd(&a.ctl[p].active, 1);
+                ld_acquire(&a.ctl[p].started);  // the roots are visible from here on
                 if (ld_acquire(&a.ctl[p].done) != DONE_RUNNING) {
                     atomicSub(&a.ctl[p].active, 1);
                     p = -2;  // raced with completion: rescan
@@ -761,16 +764,11 @@ __global__ void __launch_bounds__(NT, MINB) plan_kernel(PlanArgs a) {
             TRACE_PHASE(2);
             int m = 1;
             if (a.p.balance) m = max(1, min(sh(c.ictl)[IC_TMP5], 2048 / max(1, snap)));
+            // (the scan also evaluates each sample's acceptance: duplicate,
+            // planner.cpp:218 / DynamicDomain::accept, sampling.hpp:61-75)
             nn_scan_multi(c, Ts.cfg, a.stride, snap, sh(c.sbuf) + slot * dof, m,
-                          a.p.dynamic_domain ? Ts.dd : nullptr);
+                          a.p.dynamic_domain ? Ts.dd : nullptr, true, R);
             TRACE_PHASE(3);
-            if (tid < m) {  // duplicate (planner.cpp:218) / DynamicDomain::accept (sampling.hpp:61-75)
-                const double d2j = sh(c.mnn_d)[tid];
-                int okj = d2j != 0.0;
-                if (okj && a.p.dynamic_domain && Ts.dd[sh(c.mnn_i)[tid]] && !(__dsqrt_rn(d2j) <= R)) okj = 0;
-                sh(c.mnn_ok)[tid] = okj;
-            }
-            __syncthreads();
             const unsigned okm = __ballot_sync(0xffffffffu, (tid & 31) < m && sh(c.mnn_ok)[tid & 31]);
             const int first = okm ? __ffs(okm) - 1 : m;
             if (tid == 0) {  // the rejected samples before `first` were iterations too
