@@ -485,6 +485,14 @@ __device__ __forceinline__ bool fine_vs_prim(const SceneV& v, float3 x, float rf
     }
 }
 
+// 64-bit OR into shared memory as two native 32-bit ATOMS.OR (the 64-bit
+// form compiles to a CAS spin loop)
+__device__ __forceinline__ void or64_shared(unsigned long long* p, unsigned long long v) {
+    unsigned* w = reinterpret_cast<unsigned*>(p);
+    if ((unsigned)v) atomicOr(w, (unsigned)v);
+    if ((unsigned)(v >> 32)) atomicOr(w + 1, (unsigned)(v >> 32));
+}
+
 // algorithmic flops of one sphere test (kernels_detail.hpp:17-50 counted:
 // mul/add/sub = 1, FMA = 2): sphere 10, box 27, capsule 22
 __device__ __forceinline__ int test_flops(const SceneV& v, int p) {
@@ -709,7 +717,7 @@ __device__ __noinline__ void check_chunk(Ctx& c, int cnt, bool two_stage, bool e
                 acc.t += p1 - p0;
                 acc.f += fl;
                 if (m) {
-                    atomicOr(&lmask[l * NS + s], m);
+                    or64_shared(&lmask[l * NS + s], m);
                     flagged = 1;
                 }
             }
@@ -726,7 +734,7 @@ __device__ __noinline__ void check_chunk(Ctx& c, int cnt, bool two_stage, bool e
             ++acc.t;
             acc.f += 10;
             if (fmaf(dx, dx, fmaf(dy, dy, dz * dz)) < rr * rr) {
-                atomicOr(&pmask[(pr >> 6) * NS + s], 1ull << (pr & 63));
+                or64_shared(&pmask[(pr >> 6) * NS + s], 1ull << (pr & 63));
                 flagged = 1;
             }
         }
