@@ -333,6 +333,15 @@ int prrtc_robot_create(const prrtc_robot_desc* d, int device, prrtc_robot** out)
     w[RH_OFF_FLINK] = (uint32_t)w.size();
     for (int l = 0; l < n; ++l)
         for (uint32_t k = d->fine_offset[l]; k < d->fine_offset[l + 1]; ++k) w.push_back((uint32_t)l);
+    if (w.size() % 2) w.push_back(0);
+    w[RH_OFF_FUNITS] = (uint32_t)w.size();
+    uint32_t nunits = 0;
+    for (int l = 0; l < n; ++l)
+        for (uint32_t k = d->fine_offset[l]; k < d->fine_offset[l + 1]; k += 3, ++nunits) {
+            w.push_back((uint32_t)l);
+            w.push_back(k | (std::min<uint32_t>(3, d->fine_offset[l + 1] - k) << 16));
+        }
+    w[RH_NFUNITS] = nunits;
     align4();
     w[RH_WORDS] = (uint32_t)w.size();
     {   // 3 dof (lerp) + 63 per non-root link + 70 per revolute

@@ -231,6 +231,8 @@ struct Ctx {
     const unsigned long long* magic;  // [dof] ceil(2^64 / base)
     const double* htab;    // [dof][kHaltonTab] Halton reciprocal powers (global, after limits)
     const int* flink;      // [S] link of each fine sphere
+    const int2* funits;    // [NFU] fine-stage units: (link, first sphere | count << 16)
+    int NFU;
     const double* fine_r64;  // global
     const double* limits;    // global [dof][2]
     unsigned fkflops;        // per-state FK + coarse posing flops
@@ -274,6 +276,7 @@ struct Ctx {
 // CTA-uniform, so reads are broadcast LDS instead of local-memory loads that
 // the acquire fences' L1 invalidations would send to L2. The helpers below
 // that fill it write through thread 0 only in that case (ctx_writer).
+__device__ int g_dbg_chunk;  // TEMP experiment switch
 __device__ __forceinline__ bool ctx_writer(const Ctx& c) { return !__isShared(&c) || threadIdx.x == 0; }
 
 // The Ctx lives in the kernel's local-memory frame, so a pointer read from it
@@ -344,6 +347,26 @@ __device__ __forceinline__ float3 pose_pt(const float* pose, int N, int l, int s
 __device__ __forceinline__ float3 pose_point(const Ctx& c, int l, int s, float px, float py,
                                              float pz) {
     return pose_pt(sh(c.pose), c.NS, l, s, px, py, pz);
+}
+
+// A link pose (3x4) of one state held in registers, applied with the same
+// fmaf order as pose_pt (identical bits).
+struct PoseR {
+    float m[12];
+};
+__device__ __forceinline__ PoseR pose_load(const float* pose, int N, int l, int s) {
+    const float* P = pose + l * 12 * N + s;
+    PoseR r;
+#pragma unroll
+    for (int k = 0; k < 12; ++k) r.m[k] = P[k * N];
+    return r;
+}
+__device__ __forceinline__ float3 pose_apply(const PoseR& P, float px, float py, float pz) {
+    float3 o;
+    o.x = __fmaf_rn(P.m[0], px, __fmaf_rn(P.m[1], py, __fmaf_rn(P.m[2], pz, P.m[9])));
+    o.y = __fmaf_rn(P.m[3], px, __fmaf_rn(P.m[4], py, __fmaf_rn(P.m[5], pz, P.m[10])));
+    o.z = __fmaf_rn(P.m[6], px, __fmaf_rn(P.m[7], py, __fmaf_rn(P.m[8], pz, P.m[11])));
+    return o;
 }
 
 // ---------------------------------------------------------------------------
@@ -635,12 +658,13 @@ __device__ void brute_chunk(Ctx& c, StatAcc& acc, int cnt, bool early_exit, bool
         for (int s = lane; s < cnt; s += 32) {
             if (k.sgroup[s] < 0 || skip_state(k, s, early_exit, indep)) continue;
             bool hit = false;
+            const PoseR PA = pose_load(pose, NS, ab.x, s), PB = pose_load(pose, NS, ab.y, s);
             for (int i = 0; i < na && !(hit && early_exit); ++i) {
                 const float4 fa = fine[ja0 + i];
-                const float3 xa = pose_pt(pose, NS, ab.x, s, fa.x, fa.y, fa.z);
+                const float3 xa = pose_apply(PA, fa.x, fa.y, fa.z);
                 for (int q = 0; q < nb; ++q) {
                     const float4 fb = fine[jb0 + q];
-                    const float3 xb = pose_pt(pose, NS, ab.y, s, fb.x, fb.y, fb.z);
+                    const float3 xb = pose_apply(PB, fb.x, fb.y, fb.z);
                     ++acc.t;
                     acc.f += 28;
                     if (fine_pair(v.eps, fine_r64, xa, fa.w, ja0 + i, xb, fb.w, jb0 + q)) {
@@ -665,7 +689,7 @@ __device__ void brute_chunk(Ctx& c, StatAcc& acc, int cnt, bool early_exit, bool
 // ---------------------------------------------------------------------------
 __device__ __noinline__ void check_chunk(Ctx& c, int cnt, bool two_stage, bool early_exit, bool indep) {
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nw = c.nthreads >> 5;
-    const int NS = c.NS, L = c.L, NP = c.NP, S = c.S, nthreads = c.nthreads;
+    const int NS = c.NS, L = c.L, NP = c.NP, nthreads = c.nthreads;
     const int PW = (NP + 63) >> 6;
     const ChunkV k = chunk_view(c);
     unsigned long long* const lmask = sh(c.lmask);
@@ -701,7 +725,7 @@ __device__ __noinline__ void check_chunk(Ctx& c, int cnt, bool two_stage, bool e
     // contiguous ranges, one per warp (a warp walks its links' primitive
     // sub-ranges), states over lanes
     int flagged = 0;
-    {
+    if (!(g_dbg_chunk & 32)) {
         const int T = L * v.P;
         const int lo = (int)((long long)T * warp / nw), hi = (int)((long long)T * (warp + 1) / nw);
         for (int i = lo; i < hi;) {
@@ -723,44 +747,68 @@ __device__ __noinline__ void check_chunk(Ctx& c, int cnt, bool two_stage, bool e
             }
         }
     }
-    for (int pr = warp; pr < NP; pr += nw) {
-        const int2 ab = pairs[pr];
-        const float rr = geo[ab.x * GEO_STRIDE + 36] + geo[ab.y * GEO_STRIDE + 36] + 2.0f * cpad;
-        for (int s = lane; s < cnt; s += 32) {
-            if (k.sgroup[s] < 0) continue;
+    // coarse self pairs (collision.cpp:174-183): pairs over warps, states
+    // over lanes; a lane collects its state's pair bits of each 64-pair word
+    // in a register and ORs them once
+    for (int s = lane; s < cnt; s += 32) {
+        if (k.sgroup[s] < 0) continue;
+        unsigned long long pm = 0;
+        int blk = warp >> 6;
+        for (int pr = warp; pr < NP; pr += nw) {
+            if ((pr >> 6) != blk) {
+                if (pm) or64_shared(&pmask[blk * NS + s], pm);
+                flagged |= pm != 0;
+                pm = 0;
+                blk = pr >> 6;
+            }
+            const int2 ab = pairs[pr];
+            const float rr = geo[ab.x * GEO_STRIDE + 36] + geo[ab.y * GEO_STRIDE + 36] + 2.0f * cpad;
             const float* A = ccen + ab.x * 3 * NS + s;
             const float* B = ccen + ab.y * 3 * NS + s;
             const float dx = A[0] - B[0], dy = A[NS] - B[NS], dz = A[2 * NS] - B[2 * NS];
             ++acc.t;
             acc.f += 10;
-            if (fmaf(dx, dx, fmaf(dy, dy, dz * dz)) < rr * rr) {
-                or64_shared(&pmask[(pr >> 6) * NS + s], 1ull << (pr & 63));
-                flagged = 1;
-            }
+            if (fmaf(dx, dx, fmaf(dy, dy, dz * dz)) < rr * rr) pm |= 1ull << (pr & 63);
         }
+        if (pm) or64_shared(&pmask[blk * NS + s], pm);
+        flagged |= pm != 0;
     }
     const int any_flag = __syncthreads_or(flagged);
     if (prof && tid == 0) prof[5] = clock64();
     if (!any_flag) return;  // nothing flagged: every state free
     if (tid == 0) k.ictl[IC_QN] = 1;
-    // stage 2a: fine spheres of flagged links vs the primitives that flagged them
-    for (int j = warp; j < S; j += nw) {
-        const int l = flink[j];
-        const float4 f = fine[j];
-        for (int s = lane; s < cnt; s += 32) {
-            unsigned long long m = lmask[l * NS + s];
-            if (!m || skip_state(k, s, early_exit, indep)) continue;
-            const float3 x = pose_pt(pose, NS, l, s, f.x, f.y, f.z);
-            const double rd = __ldg(fine_r64 + j);
-            acc.f += 18;
-            while (m) {
-                const int p = __ffsll((long long)m) - 1;
-                m &= m - 1;
-                ++acc.t;
-                acc.f += test_flops(v, p);
-                if (fine_vs_prim(v, x, f.w, rd, p)) {
-                    mark_bad(k, s);
-                    break;
+    // stage 2a: fine spheres of flagged links vs the primitives that flagged
+    // them. Work units of up to three consecutive fine spheres of one link
+    // (host-built) over warps, states over lanes: an unflagged (link, state)
+    // costs one mask read per unit, a flagged one loads the link pose into
+    // registers once for the unit's spheres; small units keep warps balanced
+    // when one link collects most of the flags.
+    {
+        const int2* const funits = sh(c.funits);
+        for (int u = warp; u < c.NFU; u += nw) {
+            const int2 un = funits[u];
+            const int l = un.x, j0 = un.y & 0xffff, j1 = j0 + (un.y >> 16);
+            for (int s = lane; s < cnt; s += 32) {
+                const unsigned long long m0 = lmask[l * NS + s];
+                if (!m0 || skip_state(k, s, early_exit, indep)) continue;
+                const PoseR P = pose_load(pose, NS, l, s);
+                for (int j = j0; j < j1; ++j) {
+                    if (skip_state(k, s, early_exit, indep)) break;
+                    const float4 f = fine[j];
+                    const float3 x = pose_apply(P, f.x, f.y, f.z);
+                    const double rd = __ldg(fine_r64 + j);
+                    acc.f += 18;
+                    unsigned long long m = m0;
+                    while (m) {
+                        const int p = __ffsll((long long)m) - 1;
+                        m &= m - 1;
+                        ++acc.t;
+                        acc.f += test_flops(v, p);
+                        if (fine_vs_prim(v, x, f.w, rd, p)) {
+                            mark_bad(k, s);
+                            break;
+                        }
+                    }
                 }
             }
         }
@@ -784,9 +832,10 @@ __device__ __noinline__ void check_chunk(Ctx& c, int cnt, bool two_stage, bool e
             // kinematics.cpp:56-57): skip them before the fine x fine loop
             const float* CB = ccen + ab.y * 3 * NS + s;
             const float cbx = CB[0], cby = CB[NS], cbz = CB[2 * NS];
+            const PoseR PA = pose_load(pose, NS, ab.x, s), PB = pose_load(pose, NS, ab.y, s);
             for (int i = 0; i < na && !hit; ++i) {
                 const float4 fa = fine[ja0 + i];
-                const float3 xa = pose_pt(pose, NS, ab.x, s, fa.x, fa.y, fa.z);
+                const float3 xa = pose_apply(PA, fa.x, fa.y, fa.z);
                 {
                     const float dx = xa.x - cbx, dy = xa.y - cby, dz = xa.z - cbz;
                     const float rr = fa.w + rcb;
@@ -795,7 +844,7 @@ __device__ __noinline__ void check_chunk(Ctx& c, int cnt, bool two_stage, bool e
                 }
                 for (int q = 0; q < nb; ++q) {
                     const float4 fb = fine[jb0 + q];
-                    const float3 xb = pose_pt(pose, NS, ab.y, s, fb.x, fb.y, fb.z);
+                    const float3 xb = pose_apply(PB, fb.x, fb.y, fb.z);
                     ++acc.t;
                     acc.f += 28;
                     if (fine_pair(v.eps, fine_r64, xa, fa.w, ja0 + i, xb, fb.w, jb0 + q)) {

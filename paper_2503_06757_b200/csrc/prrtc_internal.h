@@ -34,6 +34,8 @@ enum RobotHdr : int {
     RH_OFF_FLINK, // int[S] link of each fine sphere
     RH_FKFLOPS,   // algorithmic FP32 flops of FK + coarse posing per state
     RH_OFF_MAGIC, // uint64[dof] ceil(2^64 / base): exact 32-bit division by the Halton bases
+    RH_OFF_FUNITS, // int2[n]: fine-stage work units (link, first sphere | count << 16), <= 3 spheres each
+    RH_NFUNITS,
     RH_COUNT = 16
 };
 

@@ -91,6 +91,8 @@ __device__ void setup_ctx(Ctx& c, unsigned char* smem, const uint32_t* robot_g, 
         c.bases = rw + rw[RH_OFF_BASES];
         c.magic = reinterpret_cast<const unsigned long long*>(rw + rw[RH_OFF_MAGIC]);
         c.flink = reinterpret_cast<const int*>(rw + rw[RH_OFF_FLINK]);
+        c.funits = reinterpret_cast<const int2*>(rw + rw[RH_OFF_FUNITS]);
+        c.NFU = rw[RH_NFUNITS];
         c.fine_r64 = fine_r64;
         c.limits = limits;
         c.NS = NS;
@@ -1261,6 +1263,10 @@ cudaError_t launch_validate_edges(const RobotArgs& r, const SceneArgs& s, const 
                                   int early_exit, uint8_t* out, cudaStream_t st, long long* prof) {
     const int NS = chunk_states();
     const size_t sm = smem_bytes(r, NS, 128);
+    {
+        const int dbg = getenv("PRRTC_CHUNK_DBG") ? atoi(getenv("PRRTC_CHUNK_DBG")) : 0;
+        cudaMemcpyToSymbol(g_dbg_chunk, &dbg, sizeof dbg);
+    }
     cudaError_t e = cudaFuncSetAttribute(validate_edges_kernel,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
     if (e != cudaSuccess) return e;
