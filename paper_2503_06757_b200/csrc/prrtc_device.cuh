@@ -276,7 +276,6 @@ struct Ctx {
 // CTA-uniform, so reads are broadcast LDS instead of local-memory loads that
 // the acquire fences' L1 invalidations would send to L2. The helpers below
 // that fill it write through thread 0 only in that case (ctx_writer).
-__device__ int g_dbg_chunk;  // TEMP experiment switch
 __device__ __forceinline__ bool ctx_writer(const Ctx& c) { return !__isShared(&c) || threadIdx.x == 0; }
 
 // The Ctx lives in the kernel's local-memory frame, so a pointer read from it
@@ -725,7 +724,7 @@ __device__ __noinline__ void check_chunk(Ctx& c, int cnt, bool two_stage, bool e
     // contiguous ranges, one per warp (a warp walks its links' primitive
     // sub-ranges), states over lanes
     int flagged = 0;
-    if (!(g_dbg_chunk & 32)) {
+    {
         const int T = L * v.P;
         const int lo = (int)((long long)T * warp / nw), hi = (int)((long long)T * (warp + 1) / nw);
         for (int i = lo; i < hi;) {

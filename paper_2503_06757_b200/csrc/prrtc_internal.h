@@ -142,7 +142,7 @@ struct PlanArgs {
     unsigned long long* trace; // [2]: LLONG_MAX - first CTA start, last CTA exit (globaltimer ns)
     long long* cta_trace;      // [grid][4]: per-CTA stamps (PRRTC_TRACE only, else null)
     unsigned epoch;
-    unsigned dbg;              // PRRTC_DEBUG_FLAGS (development switches, 0 in production)
+    unsigned dbg;              // PRRTC_DEBUG_FLAGS: bit 0 = fence at every snapshot (protocol check; 0 in production)
     PlanParamsDev p;
     int ns_max;                // states per validation chunk
     int nthreads;

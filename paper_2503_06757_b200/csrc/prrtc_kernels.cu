@@ -1263,10 +1263,6 @@ cudaError_t launch_validate_edges(const RobotArgs& r, const SceneArgs& s, const 
                                   int early_exit, uint8_t* out, cudaStream_t st, long long* prof) {
     const int NS = chunk_states();
     const size_t sm = smem_bytes(r, NS, 128);
-    {
-        const int dbg = getenv("PRRTC_CHUNK_DBG") ? atoi(getenv("PRRTC_CHUNK_DBG")) : 0;
-        cudaMemcpyToSymbol(g_dbg_chunk, &dbg, sizeof dbg);
-    }
     cudaError_t e = cudaFuncSetAttribute(validate_edges_kernel,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
     if (e != cudaSuccess) return e;
