@@ -229,7 +229,7 @@ struct Ctx {
     const int2* pairs;     // [NP]
     const unsigned* bases; // [dof]
     const unsigned long long* magic;  // [dof] ceil(2^64 / base)
-    const double* htab;    // [dof][kHaltonTab] Halton reciprocal powers (global, after limits)
+    const double* htab;    // [dof][kHaltonTab] Halton reciprocal powers (shared copy of the host table)
     const int* flink;      // [S] link of each fine sphere
     const int2* funits;    // [NFU] fine-stage units: (link, first sphere | count << 16)
     int NFU;

@@ -26,7 +26,7 @@ using namespace dev;
 // ---------------------------------------------------------------------------
 struct SmemLayout {
     size_t robot, scene, pose, ccen, qf, sgroup, sbad, lmask, ictl, dcfg, red_d, red_i,
-        ends, ends_eq, ttab, sbuf, mnn, stat, total;
+        ends, ends_eq, ttab, sbuf, mnn, stat, htab, total;
 };
 
 __host__ __device__ inline size_t al16(size_t x) { return (x + 15) & ~size_t(15); }
@@ -54,6 +54,7 @@ __host__ __device__ inline SmemLayout smem_layout(int robot_words, int L, int do
     s.sbuf = o;  o = al16(o + 8 * (size_t)nthreads);
     s.mnn = o;   o = al16(o + (8 + 4 + 4) * 32);
     s.stat = o;  o = al16(o + 16 * (size_t)nthreads);
+    s.htab = o;  o = al16(o + 8 * (size_t)dof * (kHaltonTab + 2));  // + the [dof][2] limits
     s.total = o;
     return s;
 }
@@ -76,6 +77,11 @@ __device__ void setup_ctx(Ctx& c, unsigned char* smem, const uint32_t* robot_g, 
     unsigned long long* stat = reinterpret_cast<unsigned long long*>(smem + lay.stat);
     stat[2 * tid] = 0;
     stat[2 * tid + 1] = 0;
+    // Halton reciprocal table (host-built, after the limits) staged in shared
+    // memory: the sampler reads it per digit, and global reads would often
+    // miss the L1 the tree protocol's acquires keep invalidating
+    double* htab = reinterpret_cast<double*>(smem + lay.htab);
+    for (int i = tid; i < (int)rw[RH_DOF] * (kHaltonTab + 2); i += nthreads) htab[i] = limits[i];
     if (ctx_writer(c)) {
         c.nthreads = nthreads;
         c.L = rw[RH_NLINKS];
@@ -94,7 +100,7 @@ __device__ void setup_ctx(Ctx& c, unsigned char* smem, const uint32_t* robot_g, 
         c.funits = reinterpret_cast<const int2*>(rw + rw[RH_OFF_FUNITS]);
         c.NFU = rw[RH_NFUNITS];
         c.fine_r64 = fine_r64;
-        c.limits = limits;
+        c.limits = htab;  // shared copy: [dof][2] limits, then the Halton table
         c.NS = NS;
         c.pose = reinterpret_cast<float*>(smem + lay.pose);
         c.ccen = reinterpret_cast<float*>(smem + lay.ccen);
@@ -109,7 +115,7 @@ __device__ void setup_ctx(Ctx& c, unsigned char* smem, const uint32_t* robot_g, 
         c.red_i = reinterpret_cast<int*>(smem + lay.red_i);
         c.ends = reinterpret_cast<double*>(smem + lay.ends);
         c.ends_eq = reinterpret_cast<int*>(smem + lay.ends_eq);
-        c.htab = limits + 2 * c.dof;
+        c.htab = htab + 2 * c.dof;
         c.ttab = reinterpret_cast<double*>(smem + lay.ttab);
         c.sbuf = reinterpret_cast<double*>(smem + lay.sbuf);
         c.mnn_d = reinterpret_cast<double*>(smem + lay.mnn);
@@ -749,9 +755,9 @@ __global__ void __launch_bounds__(NT, MINB) plan_kernel(PlanArgs a) {
                 __syncthreads();  // header scalars read before they are reused
                 if (tid < kblk * dof) {
                     const int k = tid / dof, d = tid - k * dof;
-                    sh(c.sbuf)[tid] = sample_dim(halton_tab(sh(c.bases)[d], sh(c.magic)[d], c.htab + d * kHaltonTab,
+                    sh(c.sbuf)[tid] = sample_dim(halton_tab(sh(c.bases)[d], sh(c.magic)[d], sh(c.htab) + d * kHaltonTab,
                                                             1ull + a.p.seed + base + k),
-                                                 __ldg(c.limits + 2 * d), __ldg(c.limits + 2 * d + 1));
+                                                 sh(c.limits)[2 * d], sh(c.limits)[2 * d + 1]);
                 }
             }
             __syncthreads();
