@@ -541,17 +541,17 @@ __device__ int pick_help(Ctx& c, const PlanArgs& a) {
             __nanosleep(200);
         }
         int bk = 0x7fffffff, bp = -1;
+        // an L2 scan of every problem's (started, done, winner, active) word
+        // and ticket count, two independent 16 / 8-byte loads per problem so
+        // they pipeline (a hint only: the chosen problem is acquired below;
+        // an acquire per problem would invalidate L1 a thousand times)
         for (int q = tid; q < a.n_problems; q += c.nthreads) {
             const ProbCtl& C = a.ctl[q];
-            // relaxed scan (an acquire per problem would invalidate L1 a
-            // thousand times); the chosen problem is acquired below
-            if (ld_relaxed(&C.started) == 1 && ld_relaxed(&C.done) == DONE_RUNNING &&
-                __ldcg(&C.iters) < a.p.budget) {
-                const int k = __ldcg(&C.active);
-                if (k < bk) {
-                    bk = k;
-                    bp = q;
-                }
+            const int4 hdr = __ldcg(reinterpret_cast<const int4*>(&C));  // started, done, winner, active
+            const unsigned long long it = __ldcg(&C.iters);
+            if (hdr.x == 1 && hdr.y == DONE_RUNNING && it < a.p.budget && hdr.w < bk) {
+                bk = hdr.w;
+                bp = q;
             }
         }
         for (int o = 16; o > 0; o >>= 1) {
