@@ -365,7 +365,7 @@ def run_b200(args):
             "latency_ms": {"median": q.median, "p95": q.p95, "mean": q.mean, "q1": q.q1, "q3": q.q3, "max": q.max,
                            "device_median": float(np.median(dlat)), "samples": len(idx),
                            "success_rate": float(np.mean(lst)), "mean_cost": float(np.mean(lcost)),
-                           "api": "prrtc_plan (host wall clock), params.workers = 0 (2 CTAs per SM)"},
+                           "api": "prrtc_plan (host wall clock), params.workers = 0 (one 256-thread CTA per SM)"},
             "e2e": {"value": n / (statistics.median(e2e_ms) / 1e3), "unit": UNIT, "h2d_bytes_per_step": int(h2d),
                     "d2h_bytes_per_step": int(d2h), "success_rate": float(e2e_solved),
                     "api": "prrtc_plan_batch (host buffers)"},

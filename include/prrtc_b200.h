@@ -118,7 +118,7 @@ typedef struct prrtc_scene_desc {
  *
  *  workers          reference: concurrent worker iterations (0 = hardware
  *                   concurrency). Here: CTAs working on one problem in
- *                   prrtc_plan (0 = one per SM). The per-problem iteration
+ *                   prrtc_plan (0 = one 256-thread CTA per SM). The per-problem iteration
  *                   budget is workers_effective * max_iters_per_worker.
  *  tree_capacity    total across both trees, split in half (planner.cpp:290).
  *  nn_partitions    accepted for API parity; the device scan always splits
@@ -146,10 +146,13 @@ typedef struct prrtc_params {
     uint32_t ctas_per_sm;          /* 0 = as many as co-reside */
     uint32_t deterministic;        /* 1 = single CTA, Halton stride 1: replays
                                       the reference's workers=1 mode */
-    uint32_t validate_path;        /* 1 = re-validate every returned path on the device
+    uint32_t validate_path;        /* 1 = sound mode: re-validate every path on the device
                                       at 4*n_cc states per edge, fine spheres only, no
                                       early exit, by a second kernel on the
-                                      same stream (result: prrtc_result.path_check) */
+                                      same stream (result: prrtc_result.path_check);
+                                      prrtc_plan / prrtc_plan_batch re-plan a problem whose
+                                      path fails it with the next seed (up to 4 times) and
+                                      never return such a path (status FAILED instead) */
 } prrtc_params;
 
 /* Result of one planning problem: reference PlanResult (planner.hpp:42-51). */

@@ -115,7 +115,7 @@ uint32_t fbits(float f) {
 // ---------------------------------------------------------------------------
 struct prrtc_robot {
     int device = 0;
-    int dof = 0, n_links = 0, n_fine = 0;
+    int dof = 0, n_links = 0, n_fine = 0, n_pairs = 0;
     std::vector<uint32_t> words;
     std::vector<double> limits;   // [dof][2]
     std::vector<double> fine_r64;
@@ -182,7 +182,7 @@ int prrtc_default_workers(int device) {
     if (rc) return rc;
     int n = 0;
     cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, device);
-    return 2 * (n > 0 ? n : 1);
+    return n > 0 ? n : 1;  // one 256-thread CTA per SM (batch_setup)
 }
 
 void prrtc_params_default(prrtc_params* p) {  // planner.hpp:21-40
@@ -265,6 +265,7 @@ int prrtc_robot_create(const prrtc_robot_desc* d, int device, prrtc_robot** out)
     r->dof = dof;
     r->n_links = n;
     r->n_fine = (int)S;
+    r->n_pairs = (int)d->n_self_pairs;
     // packed words
     std::vector<uint32_t>& w = r->words;
     w.assign(RH_COUNT, 0);
@@ -743,10 +744,16 @@ int batch_setup(prrtc_batch* b, const prrtc_robot* robot, const prrtc_scene* con
     b->params = *params;
     b->cap = std::max<long long>(2, (long long)(params->tree_capacity / 2));  // planner.cpp:290
     b->stride = (b->cap + 31) / 32 * 32;
-    b->nthreads = params->threads_per_cta ? (int)params->threads_per_cta : 128;
-    // states per validation chunk: 32 per 128 threads (a connect chain is
-    // validated NS states at a time; longer edges take several chunks)
-    b->ns_max = b->nthreads / 4;
+    // CTA size (threads_per_cta = 0): a single problem gets 256-thread CTAs
+    // (the extra warps split the chunk's links / primitives / pairs: lower
+    // latency per iteration); batches use 128-thread CTAs (more independent
+    // workers per SM) unless the robot is large (many fine spheres or self
+    // pairs, e.g. the dual-arm Baxter), where the split pays again
+    const bool heavy = robot->n_fine > 64 || robot->n_pairs > 48;
+    b->nthreads = params->threads_per_cta ? (int)params->threads_per_cta : (n_problems == 1 || heavy ? 256 : 128);
+    // states per validation chunk: one n_cc = 32 edge; a 256-thread CTA uses
+    // its extra warps to split links / pairs / primitives of the same chunk
+    b->ns_max = std::getenv("PRRTC_NS64") && b->nthreads == 256 ? 64 : 32;
     const int okey = b->ns_max / 32 + (b->nthreads == 256 ? 5 : 0);
     int occ = robot->occ[okey].load(std::memory_order_relaxed);
     if (occ == 0) {
@@ -759,7 +766,10 @@ int batch_setup(prrtc_batch* b, const prrtc_robot* robot, const prrtc_scene* con
         b->grid = 1;
         workers_eff = 1;
     } else if (n_problems == 1) {
-        b->grid = (int)(params->workers ? std::min<unsigned>(params->workers, sms * occ) : 2 * sms);
+        // workers = 0: one 256-thread CTA per SM (measured: ~64-148 CTAs give
+        // the lowest time-to-solution; 2 per SM only adds redundant work)
+        b->grid = (int)(params->workers ? std::min<unsigned>(params->workers, sms * occ)
+                                        : (b->nthreads == 256 ? sms : 2 * sms));
         workers_eff = b->grid;
     } else {
         const unsigned per_sm = params->ctas_per_sm ? std::min<unsigned>(params->ctas_per_sm, occ) : occ;
@@ -1076,9 +1086,70 @@ int prrtc_batch_destroy(prrtc_batch* b) {
 
 // Host-buffer entry point (the e2e path): packed H2D, kernel, D2H on the
 // device's cached workspace.
+namespace {
+// Sound mode (params.validate_path): a problem whose path fails the device's
+// 4 x n_cc re-validation is planned again with the next seed,
+// up to kSoundRetries times; a problem that never yields a sound path is
+// reported Failed. Planning at n_cc resolution (the reference's semantics)
+// can return an edge whose collision lies between two of its 32 samples;
+// this mode never returns one.
+constexpr int kSoundRetries = 4;
+int plan_batch_once(const prrtc_robot* robot, const prrtc_scene* const* scenes, uint32_t n_problems,
+                    const double* starts, const double* goals, uint32_t dof, const prrtc_params* params,
+                    prrtc_result* out);
+}  // namespace
+
 int prrtc_plan_batch(const prrtc_robot* robot, const prrtc_scene* const* scenes,
                      uint32_t n_problems, const double* starts, const double* goals,
                      uint32_t dof, const prrtc_params* params, prrtc_result* out) {
+    const auto t0 = std::chrono::steady_clock::now();
+    int rc = plan_batch_once(robot, scenes, n_problems, starts, goals, dof, params, out);
+    if (rc || !params->validate_path) return rc;
+    prrtc_params p = *params;
+    for (int attempt = 0; attempt < kSoundRetries; ++attempt) {
+        std::vector<uint32_t> bad;
+        for (uint32_t i = 0; i < n_problems; ++i)
+            if (out[i].status == PRRTC_SOLVED && out[i].path_check == 2) bad.push_back(i);
+        if (bad.empty()) break;
+        std::vector<const prrtc_scene*> sc;
+        std::vector<double> s, g;
+        for (uint32_t i : bad) {
+            sc.push_back(scenes[i]);
+            s.insert(s.end(), starts + (size_t)i * dof, starts + (size_t)(i + 1) * dof);
+            g.insert(g.end(), goals + (size_t)i * dof, goals + (size_t)(i + 1) * dof);
+        }
+        p.seed += 1;
+        std::vector<prrtc_result> re(bad.size());
+        rc = plan_batch_once(robot, sc.data(), (uint32_t)bad.size(), s.data(), g.data(), dof, &p, re.data());
+        if (rc) return rc;
+        for (size_t k = 0; k < bad.size(); ++k) {
+            prrtc_result& o = out[bad[k]];
+            const uint64_t iters = o.iterations_total, tests = o.sphere_tests, fk = o.fk_calls,
+                           fine = o.fine_stage_entries, flops = o.flops;
+            prrtc_result_free(&o);
+            o = re[k];  // takes ownership of the new path
+            o.iterations_total += iters;
+            o.sphere_tests += tests;
+            o.fk_calls += fk;
+            o.fine_stage_entries += fine;
+            o.flops += flops;
+        }
+    }
+    for (uint32_t i = 0; i < n_problems; ++i)
+        if (out[i].status == PRRTC_SOLVED && out[i].path_check == 2) {
+            prrtc_result_free(&out[i]);
+            out[i].status = PRRTC_FAILED;
+            std::snprintf(out[i].message, sizeof(out[i].message), "no path passed the 4 x n_cc re-validation");
+        }
+    if (n_problems == 1)
+        out[0].wall_time_ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+    return PRRTC_OK;
+}
+
+namespace {
+int plan_batch_once(const prrtc_robot* robot, const prrtc_scene* const* scenes, uint32_t n_problems,
+                    const double* starts, const double* goals, uint32_t dof, const prrtc_params* params,
+                    prrtc_result* out) {
     const auto t0 = std::chrono::steady_clock::now();
     if (!out) return set_err(PRRTC_EINVAL, "plan: null result");
     prrtc_batch b;
@@ -1097,6 +1168,7 @@ int prrtc_plan_batch(const prrtc_robot* robot, const prrtc_scene* const* scenes,
     if (std::getenv("PRRTC_TRACE")) std::fprintf(stderr, "prrtc trace: host wall %.3f ms\n", wall);
     return PRRTC_OK;
 }
+}  // namespace
 
 int prrtc_plan(const prrtc_robot* robot, const prrtc_scene* scene, const double* start,
                const double* goal, uint32_t dof, const prrtc_params* params, prrtc_result* result) {

@@ -77,5 +77,7 @@ def test_dropin_matches_reference_contract(gpu, oracle, tmp_path):
             continue
         P = np.array(x["path"])
         assert np.array_equal(P[0], s) and np.array_equal(P[-1], g)
-        assert oracle.path_valid(m, scene, P, 128)
+        # sound at the planner's resolution (the reference planner's own
+        # guarantee; the 4 x n_cc sound mode is tested in test_gpu_planner.py)
+        assert oracle.path_valid(m, scene, P, 32)
         assert abs(x["cost"] - np.linalg.norm(np.diff(P, axis=0), axis=1).sum()) < 1e-9
