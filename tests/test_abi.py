@@ -108,3 +108,33 @@ def test_missing_library_fails_loudly(tmp_path):
     env = dict(os.environ, PRRTC_B200_LIB=str(tmp_path / "missing.so"))
     r = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True)
     assert r.returncode != 0 and "no CPU fallback" in r.stderr
+
+
+def test_result_helpers_pack_and_free():
+    """prrtc_results_pack_paths / prrtc_results_free (host-only helpers used by
+    the batch API): paths back to back with doubles offsets; freeing clears."""
+    import numpy as np
+    lib = _lib.load()
+    libc = C.CDLL(None)
+    libc.malloc.restype = C.c_void_p
+    libc.malloc.argtypes = [C.c_size_t]
+    res = (_lib.Result * 3)()
+    rng = np.random.default_rng(0)
+    paths = [rng.standard_normal((4, 7)), None, rng.standard_normal((2, 7))]
+    for r, p in zip(res, paths):
+        r.dof = 7
+        if p is not None:
+            buf = libc.malloc(8 * p.size)
+            C.memmove(buf, p.ctypes.data, 8 * p.size)
+            r.path = C.cast(buf, C.POINTER(C.c_double))
+            r.path_len = p.shape[0]
+    off = np.zeros(4, dtype=np.uint64)
+    assert lib.prrtc_results_pack_paths(res, 3, None, off.ctypes.data_as(C.POINTER(C.c_uint64))) == 0
+    assert off.tolist() == [0, 28, 28, 42]
+    flat = np.zeros(int(off[-1]))
+    assert lib.prrtc_results_pack_paths(res, 3, flat.ctypes.data_as(C.POINTER(C.c_double)),
+                                        off.ctypes.data_as(C.POINTER(C.c_uint64))) == 0
+    assert np.array_equal(flat[:28].reshape(4, 7), paths[0]) and np.array_equal(flat[28:].reshape(2, 7), paths[2])
+    lib.prrtc_results_free(res, 3)
+    assert all(not r.path and r.path_len == 0 for r in res)
+    assert lib.prrtc_results_pack_paths(None, 0, None, off.ctypes.data_as(C.POINTER(C.c_uint64))) == -1
