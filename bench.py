@@ -279,13 +279,13 @@ def run_reference(args):
 
 
 def run_b200(args):
-    world, rank, local = dist_setup()
     import torch
+    torch.cuda.set_device(int(os.environ.get("LOCAL_RANK", "0")))  # before NCCL init: one GPU per rank
+    world, rank, local = dist_setup()
     from paper_2503_06757_b200 import _lib, planner
     from paper_2503_06757_b200.model import PlannerParams, PlanStatus
     from paper_2503_06757_b200.planner import Batch
 
-    torch.cuda.set_device(local)
     dev = local
     model, scenes, S, G, kinds = load_workload(args.robot, args.problems)
     n = len(S)
