@@ -324,6 +324,7 @@ enum : int {
     IC_KNOWN0,      // per tree: published prefix this CTA holds acquire-ordered (or wrote itself);
     IC_KNOWN1,      //   a snapshot within it needs no fence (thread 0 only)
     IC_DIRTY,       // the CTA stored tree data since its last fence: L1 may hold stale lines
+    IC_STOP,        // the problem's done flag as sampled by gen_chain_states (planner.cpp:112)
     IC_COUNT = 32
 };
 
@@ -879,9 +880,13 @@ __device__ __noinline__ double frac_div(int i, int n) { return __ddiv_rn((double
 
 // Chain indices are 32-bit: a chain holds n_sub * n_cc < 2^30 states (the
 // caller rejects longer ones; joint limits bound n_sub to a few dozen).
+// stop_flag (nullable): thread 0 issues a relaxed load of it on entry and
+// publishes the value in ictl[IC_STOP] just before the final barrier, so the
+// caller can abandon the chunk without a barrier pair of its own.
 __device__ __noinline__ int gen_chain_states(Ctx& c, const double* A, const double* B, long long n_sub,
-                                 int n_cc, long long g0l, int cnt) {
+                                 int n_cc, long long g0l, int cnt, const int* stop_flag) {
     const int tid = threadIdx.x, dof = c.dof, NS = c.NS, nthreads = c.nthreads;
+    const int stop = (stop_flag && tid == 0) ? ld_relaxed(stop_flag) : 0;
     double* const ends = sh(c.ends);
     int* const ends_eq = sh(c.ends_eq);
     int* const sgroup = sh(c.sgroup);
@@ -904,6 +909,7 @@ __device__ __noinline__ int gen_chain_states(Ctx& c, const double* A, const doub
             qf[idx] = i == n_cc ? (float)Bs[d]
                                 : (float)lerp_exact(As[d], Bs[d], ttab ? ttab[i] : frac_div(i, n_cc));
         }
+        if (tid == 0) sh(c.ictl)[IC_STOP] = stop;
         __syncthreads();
         return eq ? ((int)g0 + cnt == n_cc ? 1 : 0) : cnt;
     }
@@ -946,6 +952,7 @@ __device__ __noinline__ int gen_chain_states(Ctx& c, const double* A, const doub
         sgroup[s] = (int)k;
         ++mine;
     }
+    if (tid == 0) sh(c.ictl)[IC_STOP] = stop;
     return __syncthreads_count(mine);
 }
 

@@ -316,18 +316,12 @@ __device__ long long validate_chain(Ctx& c, const PlanArgs& a, const double* A, 
     if (total >= (1ll << 30)) return 0;  // beyond the 32-bit chain indexing: never valid (see gen_chain_states)
     for (long long g0 = 0; g0 < total; g0 += c.NS) {
         trace_phase(a, 9);  // PRRTC_TRACE: chain states
-        if (done_flag) {  // stop flag (planner.cpp:112)
-            if (threadIdx.x == 0) sh(c.ictl)[IC_TMP3] = ld_relaxed(done_flag);
-            __syncthreads();
-            const int dn = sh(c.ictl)[IC_TMP3];
-            __syncthreads();
-            if (dn != 0) {
-                *stopped = true;
-                return 0;
-            }
-        }
         const int cnt = (int)min((long long)c.NS, total - g0);
-        const int act = gen_chain_states(c, A, B, n_sub, n_cc, g0, cnt);
+        const int act = gen_chain_states(c, A, B, n_sub, n_cc, g0, cnt, done_flag);
+        if (done_flag && sh(c.ictl)[IC_STOP] != 0) {  // stop flag (planner.cpp:112): not running
+            *stopped = true;
+            return 0;
+        }
         if (threadIdx.x == 0) {
             fk_states += act;
             sh(c.stat)[1] += (unsigned long long)act * c.fkflops;  // thread 0's flop slot
@@ -963,7 +957,7 @@ __global__ void __launch_bounds__(128) validate_paths_kernel(PlanArgs a, const i
         int bad = 0;
         for (int g0 = 0; g0 < n_cc4; g0 += c.NS) {
             const int cnt = min(c.NS, n_cc4 - g0);
-            gen_chain_states(c, sa, sb, 1, n_cc4, g0, cnt);
+            gen_chain_states(c, sa, sb, 1, n_cc4, g0, cnt, nullptr);
             check_chunk(c, cnt, false, false, false);
             bad |= sh(c.ictl)[IC_FIRSTBAD] != kNoBad;
             __syncthreads();
@@ -1061,7 +1055,7 @@ __global__ void __launch_bounds__(128) validate_edges_kernel(RobotArgs r, SceneA
         bool bad = false;
         for (long long g0 = 0; g0 < n_cc && !(bad && early_exit); g0 += NS) {
             const int cnt = (int)min((long long)NS, n_cc - g0);
-            gen_chain_states(c, A, B, 1, n_cc, g0, cnt);
+            gen_chain_states(c, A, B, 1, n_cc, g0, cnt, nullptr);
             if (c.prof && threadIdx.x == 0) c.prof[8] = clock64();
             check_chunk(c, cnt, two_stage != 0, early_exit != 0, false);
             bad |= sh(c.ictl)[IC_FIRSTBAD] != kNoBad;
