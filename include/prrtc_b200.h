@@ -110,6 +110,11 @@ typedef struct prrtc_scene_desc {
     const double* boxes;     /* [n*10] qw,qx,qy,qz, tx,ty,tz, hx,hy,hz */
     uint32_t n_capsules;
     const double* capsules;  /* [n*7]  ax,ay,az, bx,by,bz, r */
+    /* Extension (BASELINE config 4; the reference has no cylinder primitive,
+       geometry.hpp:35, so its verdicts are pinned to the C restatement only):
+       solid cylinders about the pose's local z axis. */
+    uint32_t n_cylinders;
+    const double* cylinders; /* [n*9]  qw,qx,qy,qz, tx,ty,tz, radius, half_length */
 } prrtc_scene_desc;
 
 /*

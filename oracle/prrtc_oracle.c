@@ -248,22 +248,38 @@ int orc_fk_spheres(void* rp, const double* q, int level, double* out) {
 
 /* ---------------- scene (geometry.hpp/.cpp) ---------------- */
 typedef struct {
-    int ns, nb, nc;
+    int ns, nb, nc, ny;
     double* s;  /* [ns][4] */
     double* b;  /* [nb][15]: world->box rotation m[9], t[3], h[3] (SceneIndex) */
     double* c;  /* [nc][8]: a[3], ab[3], inv_ab2, r */
+    double* y;  /* [ny][14]: world->cylinder rotation m[9], t[3], r, h — EXTENSION, no
+                   reference counterpart (geometry.hpp:35); parity unpinned */
 } SceneI;
 
 void orc_scene_destroy(void* p) {
     SceneI* s = (SceneI*)p;
     if (!s) return;
-    free(s->s); free(s->b); free(s->c); free(s);
+    free(s->s); free(s->b); free(s->c); free(s->y); free(s);
 }
 
 /* Scene::validate (geometry.cpp:10-39) + SceneIndex (geometry.cpp:68-99) */
 void* orc_scene_create(const prrtc_scene_desc* d) {
     SceneI* s = (SceneI*)calloc(1, sizeof(SceneI));
     s->ns = d->n_spheres; s->nb = d->n_boxes; s->nc = d->n_capsules;
+    s->ny = d->cylinders ? (int)d->n_cylinders : 0;
+    s->y = malloc(sizeof(double) * 14 * (s->ny + 1));
+    for (int i = 0; i < s->ny; ++i) {
+        const double* p = d->cylinders + 9 * i;
+        if (!(p[7] > 0.0) || !(p[8] > 0.0)) { fail("scene cylinder radius and half_length must be positive"); orc_scene_destroy(s); return NULL; }
+        const double qn = sqrt(p[0] * p[0] + p[1] * p[1] + p[2] * p[2] + p[3] * p[3]);
+        if (fabs(qn - 1.0) > 1e-6) { fail("scene cylinder pose.quaternion norm deviates from 1 by more than 1e-6"); orc_scene_destroy(s); return NULL; }
+        M3 R = quat_mat(p);
+        M3 rt = m3_T(&R);
+        for (int k = 0; k < 9; ++k) s->y[14 * i + k] = rt.m[k];
+        for (int k = 0; k < 3; ++k) s->y[14 * i + 9 + k] = p[4 + k];
+        s->y[14 * i + 12] = p[7];
+        s->y[14 * i + 13] = p[8];
+    }
     s->s = malloc(sizeof(double) * 4 * (s->ns + 1));
     s->b = malloc(sizeof(double) * 15 * (s->nb + 1));
     s->c = malloc(sizeof(double) * 8 * (s->nc + 1));
@@ -333,7 +349,25 @@ static int sphere_box_hit(double px, double py, double pz, double pr, const doub
     return d2 < pr * pr;
 }
 
-/* sphere_vs_primitive (geometry.cpp:41-66), primitive order spheres, boxes, capsules */
+/* Cylinder EXTENSION (the reference has none, geometry.hpp:35): solid
+   cylinder about its local z axis; the same operation order as the device's
+   sphere_cylinder_exact (paper_2503_06757_b200/csrc/prrtc_device.cuh). */
+static int sphere_cylinder_hit(double px, double py, double pz, double pr, const double* y) {
+    const double wx = px - y[9], wy = py - y[10], wz = pz - y[11];
+    const double lx = y[0] * wx + y[1] * wy + y[2] * wz;
+    const double ly = y[3] * wx + y[4] * wy + y[5] * wz;
+    const double lz = y[6] * wx + y[7] * wy + y[8] * wz;
+    const double rho = sqrt(lx * lx + ly * ly);
+    double er = rho - y[12];
+    if (er < 0.0) er = 0.0;
+    double ez = fabs(lz) - y[13];
+    if (ez < 0.0) ez = 0.0;
+    const double d2 = er * er + ez * ez;
+    return d2 < pr * pr;
+}
+
+/* sphere_vs_primitive (geometry.cpp:41-66), primitive order spheres, boxes,
+   capsules (+ cylinders, extension) */
 int orc_sphere_hits(void* sp, double x, double y, double z, double r, uint8_t* hits) {
     const SceneI* s = (const SceneI*)sp;
     int any = 0, k = 0;
@@ -348,6 +382,10 @@ int orc_sphere_hits(void* sp, double x, double y, double z, double r, uint8_t* h
     }
     for (int i = 0; i < s->nc; ++i, ++k) {
         hits[k] = (uint8_t)sphere_capsule_hit(x, y, z, r, s->c + 8 * i);
+        any |= hits[k];
+    }
+    for (int i = 0; i < s->ny; ++i, ++k) {
+        hits[k] = (uint8_t)sphere_cylinder_hit(x, y, z, r, s->y + 14 * i);
         any |= hits[k];
     }
     return any;
@@ -380,7 +418,7 @@ static void checker_init(Checker* c, const Robot* r, const SceneI* s) {
     c->cc = malloc(sizeof(V3) * r->L);
     c->fp = malloc(sizeof(V3) * (r->S + 1));
     c->fine_posed = malloc(r->L);
-    c->flag = malloc((size_t)r->L * (s->ns + s->nb + s->nc + 1));
+    c->flag = malloc((size_t)r->L * (s->ns + s->nb + s->nc + s->ny + 1));
     c->flagged_links = malloc(sizeof(int) * r->L);
     c->flagged_pairs = malloc(sizeof(int) * (r->NP + 1));
     c->sample = malloc(sizeof(double) * (r->dof + 1));
@@ -416,7 +454,7 @@ static int fine_pair_collides(Checker* c, int li, int lj, Stats* st) {
 static int check_brute(Checker* c, Stats* st, int early_exit) {
     const Robot* r = c->r;
     const SceneI* S = c->s;
-    const int P = S->ns + S->nb + S->nc;
+    const int P = S->ns + S->nb + S->nc + S->ny;
     int colliding = 0;
     for (int l = 0; l < r->L && !(colliding && early_exit); ++l) {
         posed_fine(c, l);
@@ -428,6 +466,7 @@ static int check_brute(Checker* c, Stats* st, int early_exit) {
                 hit = sphere_sphere_hit(S->s[4 * i], S->s[4 * i + 1], S->s[4 * i + 2], S->s[4 * i + 3], x.x, x.y, x.z, r->fr[k]);
             for (int i = 0; i < S->nc && !hit; ++i) hit = sphere_capsule_hit(x.x, x.y, x.z, r->fr[k], S->c + 8 * i);
             for (int i = 0; i < S->nb && !hit; ++i) hit = sphere_box_hit(x.x, x.y, x.z, r->fr[k], S->b + 15 * i);
+            for (int i = 0; i < S->ny && !hit; ++i) hit = sphere_cylinder_hit(x.x, x.y, x.z, r->fr[k], S->y + 14 * i);
             if (hit) {
                 colliding = 1;
                 if (early_exit) break;
@@ -447,7 +486,7 @@ static int check_config(Checker* c, const double* q, Stats* st, int two_stage, i
     st->fk_calls += 1;
     memset(c->fine_posed, 0, r->L);
     if (!two_stage) return check_brute(c, st, early_exit);
-    const int P = S->ns + S->nb + S->nc;
+    const int P = S->ns + S->nb + S->nc + S->ny;
     for (int l = 0; l < r->L; ++l) c->cc[l] = tf_apply(&c->poses[l], r->cc[l]);
     int nfl = 0, nfp = 0;
     for (int l = 0; l < r->L; ++l) {
@@ -468,6 +507,10 @@ static int check_config(Checker* c, const double* q, Stats* st, int two_stage, i
         for (int i = 0; i < S->nb; ++i) {
             f[S->ns + S->nc + i] = (uint8_t)sphere_box_hit(x.x, x.y, x.z, r->cr[l], S->b + 15 * i);
             any |= f[S->ns + S->nc + i];
+        }
+        for (int i = 0; i < S->ny; ++i) {  /* cylinder extension */
+            f[S->ns + S->nc + S->nb + i] = (uint8_t)sphere_cylinder_hit(x.x, x.y, x.z, r->cr[l], S->y + 14 * i);
+            any |= f[S->ns + S->nc + S->nb + i];
         }
         if (any) c->flagged_links[nfl++] = l;
     }
@@ -505,6 +548,12 @@ static int check_config(Checker* c, const double* q, Stats* st, int two_stage, i
             st->tests += n;
             for (int k = r->foff[l]; k < r->foff[l + 1] && !hit; ++k)
                 hit = sphere_box_hit(c->fp[k].x, c->fp[k].y, c->fp[k].z, r->fr[k], S->b + 15 * i);
+        }
+        for (int i = 0; i < S->ny && !hit; ++i) {
+            if (!f[S->ns + S->nc + S->nb + i]) continue;
+            st->tests += n;
+            for (int k = r->foff[l]; k < r->foff[l + 1] && !hit; ++k)
+                hit = sphere_cylinder_hit(c->fp[k].x, c->fp[k].y, c->fp[k].z, r->fr[k], S->y + 14 * i);
         }
         if (hit) {
             colliding = 1;

@@ -97,6 +97,10 @@ int ref_robot_dof(void* r) { return static_cast<RobotModel*>(r)->dof; }
 
 // Scene (geometry.hpp:37-46); primitive order: spheres, boxes, capsules.
 void* ref_scene_create(const prrtc_scene_desc* d) {
+    if (d->cylinders && d->n_cylinders) {  // the reference has no cylinder (geometry.hpp:35)
+        g_err = "the reference scene has no cylinder primitive (geometry.hpp:35)";
+        return nullptr;
+    }
     try {
         auto* s = new Scene();
         s->name = "scene";

@@ -45,6 +45,8 @@ class SceneDesc(C.Structure):
         ("boxes", C.POINTER(C.c_double)),
         ("n_capsules", C.c_uint32),
         ("capsules", C.POINTER(C.c_double)),
+        ("n_cylinders", C.c_uint32),
+        ("cylinders", C.POINTER(C.c_double)),
     ]
 
 

@@ -140,8 +140,8 @@ struct prrtc_robot {
 struct prrtc_scene {
     int device = 0;
     std::vector<uint32_t> words;
-    std::vector<double> f64;  // spheres, boxes, capsules
-    int ns = 0, nb = 0, nc = 0;
+    std::vector<double> f64;  // spheres, boxes, capsules, cylinders
+    int ns = 0, nb = 0, nc = 0, ny = 0;
     double extent = 0.0;
     uint32_t* d_words = nullptr;
     double* d_f64 = nullptr;
@@ -151,6 +151,7 @@ struct prrtc_scene {
         s.f64.s = d_f64;
         s.f64.b = d_f64 + 4 * ns;
         s.f64.c = d_f64 + 4 * ns + BOX_STRIDE * nb;
+        s.f64.y = d_f64 + 4 * ns + BOX_STRIDE * nb + CAP_STRIDE * nc;
         return s;
     }
 };
@@ -415,7 +416,8 @@ int prrtc_robot_limits(const prrtc_robot* r, double* lim) {
 
 // ---- scene: Scene::validate (geometry.cpp:10-39) + SceneIndex layout ----
 static int build_scene(const prrtc_scene_desc* d, prrtc_scene* s) {
-    const uint32_t P = d->n_spheres + d->n_boxes + d->n_capsules;
+    const uint32_t ny = d->cylinders ? d->n_cylinders : 0;
+    const uint32_t P = d->n_spheres + d->n_boxes + d->n_capsules + ny;
     if (P > PRRTC_MAX_PRIMS) return set_err(PRRTC_EINVAL, "scene: more than PRRTC_MAX_PRIMS primitives");
     int idx = 0;
     auto where = [&](int i) { return std::string("scene primitives[") + std::to_string(i) + "]"; };
@@ -431,10 +433,19 @@ static int build_scene(const prrtc_scene_desc* d, prrtc_scene* s) {
     }
     for (uint32_t i = 0; i < d->n_capsules; ++i, ++idx)
         if (!(d->capsules[7 * i + 6] > 0.0)) return set_err(PRRTC_EINVAL, where(idx) + ".radius: must be positive");
+    for (uint32_t i = 0; i < ny; ++i, ++idx) {  // cylinder extension, validated like boxes / capsules
+        const double* y = d->cylinders + 9 * i;
+        if (!(y[7] > 0.0)) return set_err(PRRTC_EINVAL, where(idx) + ".radius: must be positive");
+        if (!(y[8] > 0.0)) return set_err(PRRTC_EINVAL, where(idx) + ".half_length: must be positive");
+        const double qn = std::sqrt(y[0] * y[0] + y[1] * y[1] + y[2] * y[2] + y[3] * y[3]);
+        if (std::abs(qn - 1.0) > 1e-6)
+            return set_err(PRRTC_EINVAL, where(idx) + ".pose.quaternion: norm deviates from 1 by more than 1e-6");
+    }
 
     s->ns = d->n_spheres;
     s->nb = d->n_boxes;
     s->nc = d->n_capsules;
+    s->ny = ny;
     std::vector<uint32_t>& w = s->words;
     std::vector<double>& f = s->f64;
     w.assign(SH_COUNT, 0);
@@ -483,6 +494,25 @@ static int build_scene(const prrtc_scene_desc* d, prrtc_scene* s) {
             f.push_back(v[k]);
         }
         for (int k = 0; k < 6; ++k) upd(std::abs(c[k]) + c[6]);
+    }
+    w[SH_NY] = s->ny;
+    w[SH_OFF_Y] = (uint32_t)w.size();
+    for (int i = 0; i < s->ny; ++i) {
+        const double* y = d->cylinders + 9 * i;
+        // like a box: world-to-cylinder rotation R^T, t, then radius, half length
+        const M3 rt = transposed(quat_to_mat3(y[0], y[1], y[2], y[3]));
+        double v[CYL_STRIDE] = {0};
+        for (int k = 0; k < 9; ++k) v[k] = rt.m[k];
+        for (int k = 0; k < 3; ++k) {
+            v[9 + k] = y[4 + k];
+            upd(std::abs(y[4 + k]) + y[7] + y[8]);
+        }
+        v[12] = y[7];
+        v[13] = y[8];
+        for (int k = 0; k < CYL_STRIDE; ++k) {
+            w.push_back(fbits((float)v[k]));
+            f.push_back(v[k]);
+        }
     }
     while (w.size() % 4) w.push_back(0);
     w[SH_WORDS] = (uint32_t)w.size();
@@ -549,6 +579,7 @@ int prrtc_scene_update(prrtc_scene* s, const prrtc_scene_desc* d) {
     s->ns = tmp.ns;
     s->nb = tmp.nb;
     s->nc = tmp.nc;
+    s->ny = tmp.ny;
     s->extent = tmp.extent;
     finish_scene_words(s, kDefaultReach);
     return upload_scene(s);
@@ -1293,7 +1324,7 @@ int prrtc_debug_sphere_hits(const prrtc_scene* scene, const float* centers, cons
     int rc = check_device(scene->device);
     if (rc) return rc;
     cudaSetDevice(scene->device);
-    const int P = scene->ns + scene->nb + scene->nc;
+    const int P = scene->ns + scene->nb + scene->nc + scene->ny;
     float* dcn = nullptr;
     double* dr = nullptr;
     uint8_t* dh = nullptr;

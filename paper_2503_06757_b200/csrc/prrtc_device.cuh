@@ -164,6 +164,25 @@ __device__ __noinline__ bool sphere_box_exact(double px, double py, double pz, d
     return d2 < __dmul_rn(pr, pr);
 }
 
+// Cylinder extension (no reference counterpart; restated bit-for-bit in
+// oracle/prrtc_oracle.c sphere_cylinder_hit): local coordinates like the box
+// test, radial excess max(rho - r, 0), axial excess max(|z| - h, 0),
+// d2 = er^2 + ez^2 < pr^2, in this exact operation order.
+__device__ __noinline__ bool sphere_cylinder_exact(double px, double py, double pz, double pr,
+                                                   const double* y /* m[9], t[3], r, h */) {
+    const double wx = __dsub_rn(px, y[9]), wy = __dsub_rn(py, y[10]), wz = __dsub_rn(pz, y[11]);
+    const double lx = __dadd_rn(__dadd_rn(__dmul_rn(y[0], wx), __dmul_rn(y[1], wy)), __dmul_rn(y[2], wz));
+    const double ly = __dadd_rn(__dadd_rn(__dmul_rn(y[3], wx), __dmul_rn(y[4], wy)), __dmul_rn(y[5], wz));
+    const double lz = __dadd_rn(__dadd_rn(__dmul_rn(y[6], wx), __dmul_rn(y[7], wy)), __dmul_rn(y[8], wz));
+    const double rho = __dsqrt_rn(__dadd_rn(__dmul_rn(lx, lx), __dmul_rn(ly, ly)));
+    double er = __dsub_rn(rho, y[12]);
+    if (er < 0.0) er = 0.0;
+    double ez = __dsub_rn(fabs(lz), y[13]);
+    if (ez < 0.0) ez = 0.0;
+    const double d2 = __dadd_rn(__dmul_rn(er, er), __dmul_rn(ez, ez));
+    return d2 < __dmul_rn(pr, pr);
+}
+
 // ---------------------------------------------------------------------------
 // FP32 fast predicates. Each returns the squared distance d2 and the
 // combined radius rr of the test "d2 < rr*rr" evaluated in FP32.
@@ -197,6 +216,19 @@ __device__ __forceinline__ void box_d2(float px, float py, float pz, const float
     const float dy = ly - fminf(fmaxf(ly, -b3.y), b3.y);
     const float dz = lz - fminf(fmaxf(lz, -b3.z), b3.z);
     d2 = fmaf(dx, dx, fmaf(dy, dy, dz * dz));
+}
+__device__ __forceinline__ void cyl_d2(float px, float py, float pz, const float* y, float& d2) {
+    const float4 y0 = reinterpret_cast<const float4*>(y)[0];  // M00 M01 M02 M10
+    const float4 y1 = reinterpret_cast<const float4*>(y)[1];  // M11 M12 M20 M21
+    const float4 y2 = reinterpret_cast<const float4*>(y)[2];  // M22 tx ty tz
+    const float4 y3 = reinterpret_cast<const float4*>(y)[3];  // r h - -
+    const float wx = px - y2.y, wy = py - y2.z, wz = pz - y2.w;
+    const float lx = fmaf(y0.x, wx, fmaf(y0.y, wy, y0.z * wz));
+    const float ly = fmaf(y0.w, wx, fmaf(y1.x, wy, y1.y * wz));
+    const float lz = fmaf(y1.z, wx, fmaf(y1.w, wy, y2.x * wz));
+    const float er = fmaxf(sqrtf(fmaf(lx, lx, ly * ly)) - y3.x, 0.0f);
+    const float ez = fmaxf(fabsf(lz) - y3.y, 0.0f);
+    d2 = fmaf(er, er, ez * ez);
 }
 
 // Guard band: returns 1 = certainly hit, 0 = certainly free, -1 = undecided
@@ -240,10 +272,11 @@ struct Ctx {
     double* ttab;            // [kTTab + 1]: i / ttab_n for i = 0..ttab_n (edge sample fractions)
     int ttab_n;              // n_cc the table was built for (0 = none)
     // scene (shared memory copy)
-    int ns, nb, nc, P;
+    int ns, nb, nc, ny, P;
     const float4* sph;
     const float* box;
     const float* cap;
+    const float* cyl;
     float eps, cpad;
     SceneF64 s64;  // global FP64 mirror
     // per-chunk buffers
@@ -297,12 +330,13 @@ struct SceneV {
     const float4* sph;
     const float* box;
     const float* cap;
-    int ns, nb, P;
+    const float* cyl;
+    int ns, nb, nsbc, P;  // primitive order: spheres [0, ns), boxes, capsules, cylinders [nsbc, P)
     float eps;
     SceneF64 s64;
 };
 __device__ __forceinline__ SceneV scene_view(const Ctx& c) {
-    return SceneV{sh(c.sph), sh(c.box), sh(c.cap), c.ns, c.nb, c.P, c.eps, c.s64};
+    return SceneV{sh(c.sph), sh(c.box), sh(c.cap), sh(c.cyl), c.ns, c.nb, c.ns + c.nb + c.nc, c.P, c.eps, c.s64};
 }
 
 // ictl slots
@@ -497,7 +531,7 @@ __device__ __forceinline__ bool fine_vs_prim(const SceneV& v, float3 x, float rf
         b = band(d2, rf, v.eps);
         if (b >= 0) return b != 0;
         return sphere_box_exact(x.x, x.y, x.z, rd, v.s64.b + BOX_STRIDE * k);
-    } else {
+    } else if (p < v.nsbc) {
         const int k = p - v.ns - v.nb;
         const float* C = v.cap + k * CAP_STRIDE;
         cap_d2(x.x, x.y, x.z, C, d2);
@@ -505,6 +539,12 @@ __device__ __forceinline__ bool fine_vs_prim(const SceneV& v, float3 x, float rf
         b = band(d2, rr, v.eps);
         if (b >= 0) return b != 0;
         return sphere_capsule_exact(x.x, x.y, x.z, rd, v.s64.c + CAP_STRIDE * k);
+    } else {
+        const int k = p - v.nsbc;
+        cyl_d2(x.x, x.y, x.z, v.cyl + k * CYL_STRIDE, d2);
+        b = band(d2, rf, v.eps);
+        if (b >= 0) return b != 0;
+        return sphere_cylinder_exact(x.x, x.y, x.z, rd, v.s64.y + CYL_STRIDE * k);
     }
 }
 
@@ -519,7 +559,7 @@ __device__ __forceinline__ void or64_shared(unsigned long long* p, unsigned long
 // algorithmic flops of one sphere test (kernels_detail.hpp:17-50 counted:
 // mul/add/sub = 1, FMA = 2): sphere 10, box 27, capsule 22
 __device__ __forceinline__ int test_flops(const SceneV& v, int p) {
-    return p < v.ns ? 10 : (p < v.ns + v.nb ? 27 : 22);
+    return p < v.ns ? 10 : (p < v.ns + v.nb ? 27 : (p < v.nsbc ? 22 : 26));
 }
 
 // coarse (padded) sphere vs primitives [p0, p1): hit bitmask, FP32 only
@@ -543,20 +583,27 @@ __device__ __forceinline__ unsigned long long coarse_mask(const SceneV& v, float
         box_d2(x, y, z, v.box + (p - v.ns) * BOX_STRIDE, d2);
         if (d2 < rc * rc) m |= 1ull << p;
     }
+    const int e3 = min(p1, v.nsbc);
 #pragma unroll 2
-    for (; p < p1; ++p) {
+    for (; p < e3; ++p) {
         float d2;
         const float* C = v.cap + (p - v.ns - v.nb) * CAP_STRIDE;
         cap_d2(x, y, z, C, d2);
         const float rr = rc + C[7];
         if (d2 < rr * rr) m |= 1ull << p;
     }
+    for (; p < p1; ++p) {  // cylinders (extension)
+        float d2;
+        cyl_d2(x, y, z, v.cyl + (p - v.nsbc) * CYL_STRIDE, d2);
+        if (d2 < rc * rc) m |= 1ull << p;
+    }
     return m;
 }
 
 __device__ __forceinline__ int range_flops(const SceneV& v, int p0, int p1) {
-    const int e1 = min(p1, v.ns), e2 = min(p1, v.ns + v.nb);
-    return 10 * max(0, e1 - p0) + 27 * max(0, e2 - max(p0, e1)) + 22 * max(0, p1 - max(p0, e2));
+    const int e1 = min(p1, v.ns), e2 = min(p1, v.ns + v.nb), e3 = min(p1, v.nsbc);
+    return 10 * max(0, e1 - p0) + 27 * max(0, e2 - max(p0, e1)) + 22 * max(0, e3 - max(p0, e2)) +
+           26 * max(0, p1 - max(p0, e3));
 }
 
 // self pair fine spheres (collision.cpp:89-98 / kernels_detail.hpp:17-23)

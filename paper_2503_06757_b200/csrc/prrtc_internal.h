@@ -62,10 +62,13 @@ enum SceneHdr : int {
     SH_OFF_C,  // float[nc][8]: a(3), ab(3), inv_ab2, r
     SH_EPS,    // float bits: guard band (m)
     SH_CPAD,   // float bits: coarse padding (m)
+    SH_NY,     // cylinders (extension)
+    SH_OFF_Y,  // float[ny][16]: M(world->cylinder, 9), t(3), r, h, pad
     SH_COUNT = 12
 };
 constexpr int BOX_STRIDE = 16;
 constexpr int CAP_STRIDE = 8;
+constexpr int CYL_STRIDE = 16;
 constexpr int SCENE_MAX_WORDS = SH_COUNT + 16 * 64 + 4;  // ≤ PRRTC_MAX_PRIMS boxes
 
 // FP64 mirror: spheres [ns][4], boxes [nb][16], capsules [nc][8], same order.
@@ -73,6 +76,7 @@ struct SceneF64 {
     const double* s;
     const double* b;
     const double* c;
+    const double* y;  // cylinders: m[9], t[3], r, h (CYL_STRIDE)
 };
 
 // ---- per-problem control block ----

@@ -127,7 +127,7 @@ __device__ void setup_ctx(Ctx& c, unsigned char* smem, const uint32_t* robot_g, 
         c.mflog = c.MF > 1 ? 32 - __clz(c.MF - 1) : 0;
         c.fkflops = rw[RH_FKFLOPS];
         c.prof = nullptr;
-        c.ns = c.nb = c.nc = c.P = 0;  // scene pointers are wired by load_scene
+        c.ns = c.nb = c.nc = c.ny = c.P = 0;  // scene pointers are wired by load_scene
     }
     __syncthreads();
 }
@@ -144,10 +144,12 @@ __device__ void load_scene(Ctx& c, unsigned char* sbase, const uint32_t* scene_g
         c.ns = sw[SH_NS];
         c.nb = sw[SH_NB];
         c.nc = sw[SH_NC];
-        c.P = c.ns + c.nb + c.nc;
+        c.ny = sw[SH_NY];
+        c.P = c.ns + c.nb + c.nc + c.ny;
         c.sph = reinterpret_cast<const float4*>(sw + sw[SH_OFF_S]);
         c.box = reinterpret_cast<const float*>(sw + sw[SH_OFF_B]);
         c.cap = reinterpret_cast<const float*>(sw + sw[SH_OFF_C]);
+        c.cyl = reinterpret_cast<const float*>(sw + sw[SH_OFF_Y]);
         c.eps = __uint_as_float(sw[SH_EPS]);
         c.cpad = __uint_as_float(sw[SH_CPAD]);
         c.s64 = f64;
@@ -1117,10 +1119,12 @@ __global__ void debug_hits_kernel(SceneArgs sa, const float* centers, const doub
     SceneV v;
     v.ns = sw[SH_NS];
     v.nb = sw[SH_NB];
-    v.P = v.ns + v.nb + sw[SH_NC];
+    v.nsbc = v.ns + v.nb + sw[SH_NC];
+    v.P = v.nsbc + sw[SH_NY];
     v.sph = reinterpret_cast<const float4*>(sw + sw[SH_OFF_S]);
     v.box = reinterpret_cast<const float*>(sw + sw[SH_OFF_B]);
     v.cap = reinterpret_cast<const float*>(sw + sw[SH_OFF_C]);
+    v.cyl = reinterpret_cast<const float*>(sw + sw[SH_OFF_Y]);
     v.eps = __uint_as_float(sw[SH_EPS]);
     v.s64 = sa.f64;
     for (long long it = blockIdx.x * (long long)blockDim.x + threadIdx.x; it < (long long)n * n_prims;

@@ -158,6 +158,17 @@ class CapsulePrim:  # geometry.hpp:27-33
 
 
 @dataclass
+class CylinderPrim:
+    """Extension (BASELINE config 4): a solid cylinder about the local z axis
+    of its pose. The reference has no cylinder primitive (geometry.hpp:35);
+    verdicts are pinned to the C restatement (oracle/prrtc_oracle.c)."""
+    quat: tuple
+    translation: tuple
+    radius: float
+    half_length: float
+
+
+@dataclass
 class Scene:  # geometry.hpp:37-46
     name: str
     primitives: list = field(default_factory=list)
@@ -168,24 +179,31 @@ class Scene:  # geometry.hpp:37-46
         c = [p for p in self.primitives if isinstance(p, CapsulePrim)]
         return s, b, c
 
+    def cylinders(self) -> list:
+        return [p for p in self.primitives if isinstance(p, CylinderPrim)]
+
     def ordered(self) -> list:
-        """Primitive order used by every per-primitive output: spheres, boxes, capsules."""
+        """Primitive order used by every per-primitive output: spheres, boxes,
+        capsules, then cylinders."""
         s, b, c = self.grouped()
-        return s + b + c
+        return s + b + c + self.cylinders()
 
     def to_desc(self):
         from ._lib import SceneDesc
         s, b, c = self.grouped()
+        y = self.cylinders()
         keep = {}
         sv = [v for p in s for v in (*p.center, p.radius)]
         bv = [v for p in b for v in (*p.quat, *p.translation, *p.half_extents)]
         cv = [v for p in c for v in (*p.a, *p.b, p.radius)]
+        yv = [v for p in y for v in (*p.quat, *p.translation, p.radius, p.half_length)]
         d = SceneDesc()
-        d.n_spheres, d.n_boxes, d.n_capsules = len(s), len(b), len(c)
+        d.n_spheres, d.n_boxes, d.n_capsules, d.n_cylinders = len(s), len(b), len(c), len(y)
         keep["s"] = (C.c_double * max(1, len(sv)))(*sv)
         keep["b"] = (C.c_double * max(1, len(bv)))(*bv)
         keep["c"] = (C.c_double * max(1, len(cv)))(*cv)
-        d.spheres, d.boxes, d.capsules = keep["s"], keep["b"], keep["c"]
+        keep["y"] = (C.c_double * max(1, len(yv)))(*yv)
+        d.spheres, d.boxes, d.capsules, d.cylinders = keep["s"], keep["b"], keep["c"], keep["y"]
         return d, keep
 
 

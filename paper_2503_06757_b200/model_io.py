@@ -670,6 +670,9 @@ def scene_to_json(scene: Scene) -> dict:
         elif isinstance(p, CapsulePrim):
             prims.append({"kind": "capsule", "a": _vec3_to(p.a), "b": _vec3_to(p.b),
                           "radius": float(p.radius)})
+        elif not isinstance(p, BoxPrim):
+            raise IoError(f"scene '{scene.name}': the reference scene format has no "
+                          f"{type(p).__name__} primitive (geometry.hpp:35)")
         else:
             prims.append({"kind": "box", "pose": _pose_to(p.quat, p.translation),
                           "half_extents": _vec3_to(p.half_extents)})

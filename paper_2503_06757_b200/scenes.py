@@ -26,7 +26,7 @@ from dataclasses import dataclass
 
 import numpy as np
 
-from .model import BoxPrim, CapsulePrim, Scene, SpherePrim
+from .model import BoxPrim, CapsulePrim, CylinderPrim, Scene, SpherePrim
 
 KINDS = ("table_pick", "bookshelf", "cage")
 
@@ -195,10 +195,24 @@ def cage(frame: Frame, rng):
 GENERATORS = {"table_pick": table_pick, "bookshelf": bookshelf, "cage": cage}
 
 
-def make_scene(robot: str, kind: str, problem_id: int) -> tuple[Scene, list[GoalRegion]]:
+def make_scene(robot: str, kind: str, problem_id: int, cylinders: bool = False) -> tuple[Scene, list[GoalRegion]]:
+    """cylinders=True: the upright objects become true solid cylinders (the
+    primitive extension, BASELINE config 4) instead of capsules."""
     rng = np.random.default_rng(1000 + int(problem_id))
     prims, regions = GENERATORS[kind](FRAMES[robot], rng)
-    return Scene(f"{robot}_{kind}_{problem_id}", prims), regions
+    if cylinders:
+        prims = [as_cylinder(p) for p in prims]
+    return Scene(f"{robot}_{kind}_{problem_id}" + ("_cyl" if cylinders else ""), prims), regions
+
+
+def as_cylinder(p):
+    """An upright capsule (a, b share x, y) -> the solid cylinder spanning the
+    same height (its caps' extent) with the same radius; other primitives
+    unchanged."""
+    if not isinstance(p, CapsulePrim) or p.a[0] != p.b[0] or p.a[1] != p.b[1]:
+        return p
+    lo, hi = min(p.a[2], p.b[2]) - p.radius, max(p.a[2], p.b[2]) + p.radius
+    return CylinderPrim((1.0, 0.0, 0.0, 0.0), (p.a[0], p.a[1], 0.5 * (lo + hi)), p.radius, 0.5 * (hi - lo))
 
 
 def kind_for(problem_id: int, n_problems: int) -> str:
