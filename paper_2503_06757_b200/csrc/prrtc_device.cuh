@@ -512,6 +512,28 @@ __device__ __noinline__ void fk_chunk(Ctx& c, int cnt) {
 // exact fine-sphere vs primitive (p indexes spheres, boxes, capsules in that
 // order). FP32 with guard band, FP64 exact fallback on the same inputs.
 // ---------------------------------------------------------------------------
+// cylinder extension, out of line: scenes without cylinders (every bench
+// scene) keep the hot loop's instruction footprint
+// (scalars and pointers by value: no local-memory copy of the scene view)
+__device__ __noinline__ bool fine_vs_cyl(const float* cyl, const double* y64, float eps, float3 x, float rf,
+                                         double rd) {
+    float d2;
+    cyl_d2(x.x, x.y, x.z, cyl, d2);
+    const int b = band(d2, rf, eps);
+    if (b >= 0) return b != 0;
+    return sphere_cylinder_exact(x.x, x.y, x.z, rd, y64);
+}
+__device__ __noinline__ unsigned long long coarse_mask_cyl(const float* cyl, int nsbc, float x, float y, float z,
+                                                           float rc, int p0, int p1) {
+    unsigned long long m = 0;
+    for (int p = p0; p < p1; ++p) {
+        float d2;
+        cyl_d2(x, y, z, cyl + (p - nsbc) * CYL_STRIDE, d2);
+        if (d2 < rc * rc) m |= 1ull << p;
+    }
+    return m;
+}
+
 __device__ __forceinline__ bool fine_vs_prim(const SceneV& v, float3 x, float rf, double rd, int p) {
     float d2, rr;
     int b;
@@ -541,10 +563,7 @@ __device__ __forceinline__ bool fine_vs_prim(const SceneV& v, float3 x, float rf
         return sphere_capsule_exact(x.x, x.y, x.z, rd, v.s64.c + CAP_STRIDE * k);
     } else {
         const int k = p - v.nsbc;
-        cyl_d2(x.x, x.y, x.z, v.cyl + k * CYL_STRIDE, d2);
-        b = band(d2, rf, v.eps);
-        if (b >= 0) return b != 0;
-        return sphere_cylinder_exact(x.x, x.y, x.z, rd, v.s64.y + CYL_STRIDE * k);
+        return fine_vs_cyl(v.cyl + k * CYL_STRIDE, v.s64.y + CYL_STRIDE * k, v.eps, x, rf, rd);
     }
 }
 
@@ -592,11 +611,7 @@ __device__ __forceinline__ unsigned long long coarse_mask(const SceneV& v, float
         const float rr = rc + C[7];
         if (d2 < rr * rr) m |= 1ull << p;
     }
-    for (; p < p1; ++p) {  // cylinders (extension)
-        float d2;
-        cyl_d2(x, y, z, v.cyl + (p - v.nsbc) * CYL_STRIDE, d2);
-        if (d2 < rc * rc) m |= 1ull << p;
-    }
+    if (p < p1) m |= coarse_mask_cyl(v.cyl, v.nsbc, x, y, z, rc, p, p1);  // cylinders (extension)
     return m;
 }
 
