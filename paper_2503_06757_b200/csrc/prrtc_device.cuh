@@ -788,11 +788,11 @@ __device__ __noinline__ void check_chunk(Ctx& c, int cnt, bool two_stage, bool e
     // sub-ranges), states over lanes
     int flagged = 0;
     {
-        const int T = L * v.P;
-        const int lo = (int)((long long)T * warp / nw), hi = (int)((long long)T * (warp + 1) / nw);
-        for (int i = lo; i < hi;) {
-            const int l = i / v.P;
-            const int p0 = i - l * v.P, p1 = min(v.P, p0 + (hi - i));
+        const int T = L * v.P, nwlog = 31 - __clz(nw);  // nw: 4 or 8
+        const int lo = (T * warp) >> nwlog, hi = (T * (warp + 1)) >> nwlog;
+        int l = v.P ? lo / v.P : 0, p0 = lo - l * v.P;  // one division per warp, then walk
+        for (int i = lo; i < hi; ++l, p0 = 0) {
+            const int p1 = min(v.P, p0 + (hi - i));
             i += p1 - p0;
             const float rc = geo[l * GEO_STRIDE + 36] + cpad;
             const int fl = range_flops(v, p0, p1);
@@ -1125,10 +1125,11 @@ __device__ __noinline__ void nn_scan_multi(Ctx& c, const double* cfg, long long 
     Q = sh(Q);
     double* const out_d = sh(c.mnn_d);
     int* const out_i = sh(c.mnn_i);
-    int mp = 1;
-    while (mp < m) mp <<= 1;
-    const int g = nt / mp;  // threads per sample (power of two)
-    const int j = tid / g, sub = tid - j * g;
+    int mplog = 0;
+    while ((1 << mplog) < m) ++mplog;
+    const int glog = (31 - __clz(nt)) - mplog;  // threads per sample g = nt / next_pow2(m) (a power of two)
+    const int g = 1 << glog;
+    const int j = tid >> glog, sub = tid & (g - 1);
     double best = __longlong_as_double(0x7ff0000000000000ll);  // +inf
     int bi = 0x7fffffff;
     const int npairs = (count + 1) >> 1;
