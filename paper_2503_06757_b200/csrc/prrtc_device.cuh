@@ -357,7 +357,7 @@ enum : int {
     IC_KLO,         // first chain point held in `ends`
     IC_KNOWN0,      // per tree: published prefix this CTA holds acquire-ordered (or wrote itself);
     IC_KNOWN1,      //   a snapshot within it needs no fence (thread 0 only)
-    IC_DIRTY,       // the CTA stored tree data since its last fence: L1 may hold stale lines
+    IC_DIRTY,       // force a fence at the next header (set when the CTA joins a problem)
     IC_STOP,        // the problem's done flag as sampled by gen_chain_states (planner.cpp:112)
     IC_COUNT = 32
 };

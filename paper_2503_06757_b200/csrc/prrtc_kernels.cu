@@ -261,7 +261,6 @@ __device__ int tree_append_many(Ctx& c, const PlanArgs& a, const TreeRef& T, con
             // new nodes are its own writes
             int* known = sh(c.ictl) + IC_KNOWN0 + T.which;
             if (won && *known == (int)s0) *known = (int)(s0 + ok);
-            sh(c.ictl)[IC_DIRTY] = 1;
         }
         won = __shfl_sync(0xffffffffu, won, 0);
         if (won) {
@@ -702,11 +701,12 @@ __global__ void __launch_bounds__(NT, MINB) plan_kernel(PlanArgs a) {
                 const int la = ld_relaxed(&C.published[0]);
                 const int lb = ld_relaxed(&C.published[1]);
                 // a snapshot beyond what the CTA already holds needs acquire
-                // ordering (fence after the relaxed reads) before plain loads
-                // of the new slots; a CTA working alone never pays it
-                // (the fence also drops the SM's L1 lines, so after the CTA's
-                // own tree stores — appends, dynamic-domain flags — it is
-                // taken once to keep later plain loads from stale lines)
+                // ordering (fence after the relaxed reads, which also drops
+                // the SM's L1 lines) before plain loads of the new slots; a
+                // CTA working alone never pays it — its own stores are
+                // coherent with its SM's L1 (program order), so its own
+                // appends and dynamic-domain flags need no fence (IC_DIRTY
+                // only forces one when the CTA joins a problem)
                 int* known = sh(c.ictl) + IC_KNOWN0;
                 if (la > known[0] || lb > known[1] || sh(c.ictl)[IC_DIRTY] || (a.dbg & 1)) {
                     fence_acq_rel();
@@ -801,10 +801,7 @@ __global__ void __launch_bounds__(NT, MINB) plan_kernel(PlanArgs a) {
             const long long ok = validate_chain(c, a, nnc, cnew, 1, &Ts, nn, &last, nullptr,
                                                 fk_states, fine_states, &stopped);
             if (ok == 0) {
-                if (a.p.dynamic_domain && tid == 0) {  // record_failure
-                    Ts.dd[nn] = 1;
-                    sh(c.ictl)[IC_DIRTY] = 1;
-                }
+                if (a.p.dynamic_domain && tid == 0) Ts.dd[nn] = 1;  // record_failure
                 continue;
             }
             if (ok < 0) {
