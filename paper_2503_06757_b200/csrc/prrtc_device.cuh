@@ -434,6 +434,24 @@ __device__ __noinline__ void fk_chunk(Ctx& c, int cnt) {
     const float* const geo = sh(c.geo);
     float* const ccen = sh(c.ccen);
     const int groups = (cnt + 31) >> 5;
+    {
+        // the warps FK leaves idle (all warps if none is) reset the chunk's
+        // verdict state and flag masks meanwhile; check_chunk's stages read
+        // them after the closing barrier
+        const int busy = 3 * groups < nw ? 3 * groups * 32 : 0;
+        if (tid >= busy) {
+            const int PW = (c.NP + 63) >> 6, t0 = tid - busy, nt = c.nthreads - busy;
+            int* const sbad = sh(c.sbad);
+            unsigned long long* const lmask = sh(c.lmask);
+            for (int s = t0; s < NS; s += nt) sbad[s] = 0;
+            for (int i = t0; i < (L + PW) * NS; i += nt) lmask[i] = 0ull;  // pmask follows lmask
+            if (t0 == 0) {
+                sh(c.ictl)[IC_QN] = 0;
+                sh(c.ictl)[IC_FIRSTBAD] = kNoBad;
+            }
+        }
+        if (!busy) __syncthreads();  // no idle warp: the reset precedes FK
+    }
     for (int task = warp; task < 3 * groups; task += nw) {
         const int r = task % 3;
         const int s = (task / 3) * 32 + lane;
@@ -751,21 +769,14 @@ __device__ void brute_chunk(Ctx& c, StatAcc& acc, int cnt, bool early_exit, bool
 // ---------------------------------------------------------------------------
 __device__ __noinline__ void check_chunk(Ctx& c, int cnt, bool two_stage, bool early_exit, bool indep) {
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nw = c.nthreads >> 5;
-    const int NS = c.NS, L = c.L, NP = c.NP, nthreads = c.nthreads;
-    const int PW = (NP + 63) >> 6;
+    const int NS = c.NS, L = c.L, NP = c.NP;
     const ChunkV k = chunk_view(c);
     unsigned long long* const lmask = sh(c.lmask);
     unsigned long long* const pmask = sh(c.pmask);
     long long* const prof = c.prof;
     StatAcc acc(c);
-    for (int s = tid; s < NS; s += nthreads) k.sbad[s] = 0;
-    for (int i = tid; i < (L + PW) * NS; i += nthreads) lmask[i] = 0ull;  // pmask follows lmask
-    if (tid == 0) {
-        k.ictl[IC_QN] = 0;
-        k.ictl[IC_FIRSTBAD] = kNoBad;
-    }
     if (prof && tid == 0) prof[1] = clock64();
-    fk_chunk(c, cnt);  // ends with __syncthreads
+    fk_chunk(c, cnt);  // also resets sbad / lmask / pmask / IC_QN / IC_FIRSTBAD; ends with __syncthreads
     if (prof && tid == 0) prof[4] = clock64();
     if (!two_stage) {
         brute_chunk(c, acc, cnt, early_exit, indep);
