@@ -331,9 +331,10 @@ __device__ long long validate_chain(Ctx& c, const PlanArgs& a, const double* A, 
         check_chunk(c, cnt, a.p.two_stage != 0, a.p.early_exit != 0, false);
         trace_phase(a, 9);
         if (threadIdx.x == 0 && sh(c.ictl)[IC_QN]) ++fine_states;
+        // (IC_FIRSTBAD is next reset inside the next chunk's FK, after the
+        // state-generation barrier: every thread has read it by then)
         const int fb = sh(c.ictl)[IC_FIRSTBAD];
         good = (fb != kNoBad) ? (long long)fb : (g0 + cnt) / n_cc;
-        __syncthreads();
         if (fb != kNoBad) break;
     }
     long long appended = 0;
@@ -341,14 +342,19 @@ __device__ long long validate_chain(Ctx& c, const PlanArgs& a, const double* A, 
     trace_phase(a, 8);  // append
     while (appended < good) {
         const int cntk = (int)min(good - appended, (long long)c.NS + 1);
-        for (int idx = threadIdx.x; idx < cntk * c.dof; idx += c.nthreads) {
-            const int j = idx / c.dof, d = idx - j * c.dof;
-            sh(c.ends)[idx] = chain_point(A, B, d, appended + 1 + j, n_sub);
+        const double* pts = B;  // a single edge appends its far end as is (collision.cpp:19)
+        if (n_sub > 1) {
+            for (int idx = threadIdx.x; idx < cntk * c.dof; idx += c.nthreads) {
+                const int j = idx / c.dof, d = idx - j * c.dof;
+                sh(c.ends)[idx] = chain_point(A, B, d, appended + 1 + j, n_sub);
+            }
+            __syncthreads();
+            pts = sh(c.ends);
         }
-        __syncthreads();
-        const int got = tree_append_many(c, a, *T, sh(c.ends), cntk, prev, &prev);
+        // (tree_append_many reads pts and the shared scalars before its own
+        // barriers, so the next round may overwrite them right away)
+        const int got = tree_append_many(c, a, *T, pts, cntk, prev, &prev);
         appended += got;
-        __syncthreads();
         if (got < cntk) {
             *last = prev;
             return -1 - appended;
