@@ -293,7 +293,7 @@ struct Ctx {
     // CTA scalars
     int* ictl;       // [32] misc ints
     double* dcfg;    // [8][kMaxDof] scratch configs
-    double* sbuf;    // [nthreads] Halton samples of the CTA's current ticket block
+    double* sbuf;    // [32][dof] Halton samples of the CTA's current ticket block
     double* mnn_d;   // [32] multi-sample NN: squared distance per evaluated sample
     int* mnn_i;      // [32]                  nearest index per evaluated sample
     int* mnn_ok;     // [32]                  accepted (not duplicate, inside its dynamic domain)

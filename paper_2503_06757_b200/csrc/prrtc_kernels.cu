@@ -51,7 +51,7 @@ __host__ __device__ inline SmemLayout smem_layout(int robot_words, int L, int do
     s.ends = o;  o = al16(o + 8 * (size_t)(NS + 2) * dof);
     s.ends_eq = o; o = al16(o + 4 * (size_t)(NS + 2));
     s.ttab = o;  o = al16(o + 8 * (size_t)(kTTab + 1));
-    s.sbuf = o;  o = al16(o + 8 * (size_t)nthreads);
+    s.sbuf = o;  o = al16(o + 8 * (size_t)32 * dof);  // one ticket block of 32 samples
     s.mnn = o;   o = al16(o + (8 + 4 + 4) * 32);
     s.stat = o;  o = al16(o + 16 * (size_t)nthreads);
     s.htab = o;  o = al16(o + 8 * (size_t)dof * (kHaltonTab + 2));  // + the [dof][2] limits
@@ -686,7 +686,7 @@ __global__ void __launch_bounds__(NT, MINB) plan_kernel(PlanArgs a) {
         // Halton tickets are claimed in blocks of kblk (one atomic per block,
         // every ticket still used once, in order within the CTA); the block's
         // samples are computed by all threads at once into sbuf
-        const int kblk = max(1, min(32, c.nthreads / dof));
+        const int kblk = 32;
         unsigned long long tk_base = 0, tk_pos = 0, tk_cnt = 0, used = 0;  // thread 0's copy
         int leave_msg = MSG_NONE;
         for (;;) {
@@ -755,9 +755,9 @@ __global__ void __launch_bounds__(NT, MINB) plan_kernel(PlanArgs a) {
                 TRACE_PHASE(7);
                 const unsigned long long base = reinterpret_cast<unsigned long long*>(sh(c.red_d))[0];
                 __syncthreads();  // header scalars read before they are reused
-                if (tid < kblk * dof) {
-                    const int k = tid / dof, d = tid - k * dof;
-                    sh(c.sbuf)[tid] = sample_dim(halton_tab(sh(c.bases)[d], sh(c.magic)[d], sh(c.htab) + d * kHaltonTab,
+                for (int j = tid; j < kblk * dof; j += c.nthreads) {
+                    const int k = j / dof, d = j - k * dof;
+                    sh(c.sbuf)[j] = sample_dim(halton_tab(sh(c.bases)[d], sh(c.magic)[d], sh(c.htab) + d * kHaltonTab,
                                                             1ull + a.p.seed + base + k),
                                                  sh(c.limits)[2 * d], sh(c.limits)[2 * d + 1]);
                 }
