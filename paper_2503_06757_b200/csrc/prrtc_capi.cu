@@ -600,11 +600,16 @@ int prrtc_scene_destroy(prrtc_scene* s) {
 // planning workspace and batches
 //
 // A workspace owns every device buffer a launch needs, laid out so one call
-// costs one packed H2D copy, one memset, one kernel and one D2H copy:
+// costs one packed H2D copy, one kernel and one D2H copy:
 //   io   (pinned host) : starts | goals | scene-word ptrs | scene-f64 ptrs | prob_scene
-//   d_in (device)      : same layout
-//   d_out (device)     : [hdr 128 B: arena_used u64, next_problem, n_done]
+//                        | pad to 128 B | zeroed out-header for n problems
+//   d_in (device)      : the same layout, then the path arena right after
+//                        the out-header: d_out = d_in + out_offset(n) is
+//                        [hdr 128 B: arena_used u64, next_problem, n_done]
 //                        [ProbCtl x n][path arena]
+// so the inputs and the zeroed controls go up in one copy, and the controls
+// and paths come back in one. (A persistent prrtc_batch uploads its inputs
+// once and zeroes the out-header with a memset per launch.)
 //   trees              : cfg [n][2][dof][stride], parent/ready/dd [n][2][stride]
 // Workspaces grow monotonically and are cached per device for prrtc_plan /
 // prrtc_plan_batch (allocation is setup, not part of a plan call).
@@ -619,8 +624,10 @@ struct Workspace {
     size_t io_bytes = 0;
     void* h_out = nullptr;
     size_t out_bytes = 0;
-    unsigned char* d_in = nullptr;
-    unsigned char* d_out = nullptr;
+    size_t h_out_arena = 0;  // arena doubles h_out holds past the header
+    double path_hint = 0.0;  // recent arena doubles used per problem (sizes the D2H prefix)
+    uint64_t last_h2d = 0, last_d2h = 0;  // bytes copied by the last plan call
+    unsigned char* d_in = nullptr;  // inputs, then the out-header and arena (see above)
     double* d_cfg = nullptr;
     int* d_parent = nullptr;
     int* d_dd = nullptr;
@@ -640,7 +647,6 @@ struct Workspace {
         cudaFreeHost(h_io);
         cudaFreeHost(h_out);
         cudaFree(d_in);
-        cudaFree(d_out);
         cudaFree(d_cfg);
         cudaFree(d_parent);
         cudaFree(d_dd);
@@ -650,6 +656,17 @@ struct Workspace {
         if (ev1) cudaEventDestroy(ev1);
         if (stream) cudaStreamDestroy(stream);
         *this = Workspace();
+    }
+
+    // Grow the pinned result buffer to hold `need` arena doubles past the header.
+    void grow_h_out(size_t need) {
+        if (need <= h_out_arena) return;
+        need = std::min(arena_cap, std::max(need, 2 * h_out_arena));
+        void* h = nullptr;
+        if (cudaMallocHost(&h, out_hdr(n_cap) + 8 * need) != cudaSuccess) return;  // keep the old one
+        cudaFreeHost(h_out);
+        h_out = h;
+        h_out_arena = need;
     }
     ~Workspace() { release(); }
 
@@ -666,9 +683,9 @@ struct Workspace {
         cudaSetDevice(dev);
         io_bytes = in_bytes(nn, nd);
         out_bytes = out_hdr(nn) + 8 * narena;
-        if (cudaMallocHost(&h_io, io_bytes) != cudaSuccess ||
-            cudaMallocHost(&h_out, out_hdr(nn) + 8 * std::min<size_t>(narena, 1 << 16)) != cudaSuccess ||
-            cudaMalloc(&d_in, io_bytes) != cudaSuccess || cudaMalloc(&d_out, out_bytes) != cudaSuccess ||
+        if (cudaMallocHost(&h_io, io_bytes + 128 + out_hdr(nn)) != cudaSuccess ||
+            cudaMallocHost(&h_out, out_hdr(nn) + 8 * (h_out_arena = std::min<size_t>(narena, 1 << 16))) != cudaSuccess ||
+            cudaMalloc(&d_in, io_bytes + 128 + out_bytes) != cudaSuccess ||
             cudaMalloc(&d_cfg, 8 * nnodes * nd) != cudaSuccess ||
             cudaMalloc(&d_parent, 4 * nnodes) != cudaSuccess ||
             cudaMalloc(&d_dd, 4 * nnodes) != cudaSuccess ||
@@ -713,6 +730,8 @@ struct prrtc_batch {
     unsigned long long budget = 0, arena = 0;
     cudaStream_t last_stream = 0;
     int launches = 0;
+    unsigned char* d_out = nullptr;  // ws->d_in + out_offset: out-header, controls, arena
+    bool timed = true;  // bracket the kernel with events (batch results report the kernel time)
     // device views into ws->d_in / d_out
     double *d_starts = nullptr, *d_goals = nullptr;
     const uint32_t** d_scene_words = nullptr;
@@ -819,6 +838,14 @@ int batch_setup(prrtc_batch* b, const prrtc_robot* robot, const prrtc_scene* con
 }
 
 // Binds the batch to a workspace and stages the inputs into its pinned buffer.
+size_t io_used(const prrtc_batch* b) {
+    const size_t n = b->n, dof = b->dof;
+    return 8 * 2 * n * dof + sizeof(void*) * n + sizeof(SceneF64) * n + 4 * n;
+}
+
+// offset of the out-header in the device block (and of its zeroed image in h_io)
+size_t out_offset(const prrtc_batch* b) { return (io_used(b) + 127) / 128 * 128; }
+
 int batch_bind(prrtc_batch* b, Workspace* ws, const prrtc_scene* const* scenes, const double* starts,
                const double* goals) {
     int rc = ws->reserve(b->device, b->n, b->dof, b->stride, b->arena);
@@ -849,27 +876,30 @@ int batch_bind(prrtc_batch* b, Workspace* ws, const prrtc_scene* const* scenes, 
         sf[i] = sa.f64;
         ps[i] = (int)i;
     }
-    b->d_arena_used = reinterpret_cast<unsigned long long*>(ws->d_out);
-    b->d_next = reinterpret_cast<int*>(ws->d_out + 8);
-    b->d_ndone = reinterpret_cast<int*>(ws->d_out + 12);
-    b->d_ctl = reinterpret_cast<ProbCtl*>(ws->d_out + 128);
-    b->d_arena = reinterpret_cast<double*>(ws->d_out + Workspace::out_hdr(n));
+    std::memset(h + out_offset(b), 0, Workspace::out_hdr(n));  // the zeroed controls ride the upload
+    b->d_out = d + out_offset(b);
+    b->d_arena_used = reinterpret_cast<unsigned long long*>(b->d_out);
+    b->d_next = reinterpret_cast<int*>(b->d_out + 8);
+    b->d_ndone = reinterpret_cast<int*>(b->d_out + 12);
+    b->d_ctl = reinterpret_cast<ProbCtl*>(b->d_out + 128);
+    b->d_arena = reinterpret_cast<double*>(b->d_out + Workspace::out_hdr(n));
     return PRRTC_OK;
 }
 
-size_t io_used(const prrtc_batch* b) {
-    const size_t n = b->n, dof = b->dof;
-    return 8 * 2 * n * dof + sizeof(void*) * n + sizeof(SceneF64) * n + 4 * n;
-}
 
 // Enqueues: inputs H2D (optional), header memset, the planner kernel.
 int batch_enqueue(prrtc_batch* b, cudaStream_t st, bool upload) {
+    const auto q0 = std::chrono::steady_clock::now();
     Workspace* ws = b->ws;
     cudaSetDevice(b->device);
     b->last_stream = st;
     if (++ws->epoch == 0) ++ws->epoch;
-    if (upload) CUDA_TRY(cudaMemcpyAsync(ws->d_in, ws->h_io, io_used(b), cudaMemcpyHostToDevice, st));
-    CUDA_TRY(cudaMemsetAsync(ws->d_out, 0, Workspace::out_hdr(b->n), st));
+    const size_t up = out_offset(b) + Workspace::out_hdr(b->n);
+    ws->last_h2d = upload ? up : 0;
+    if (upload)  // inputs + zeroed out-header in one copy
+        CUDA_TRY(cudaMemcpyAsync(ws->d_in, ws->h_io, up, cudaMemcpyHostToDevice, st));
+    else
+        CUDA_TRY(cudaMemsetAsync(b->d_out, 0, Workspace::out_hdr(b->n), st));
     PlanArgs a{};
     a.robot = b->robot->d_words;
     a.fine_r64 = b->robot->d_fine_r64;
@@ -892,7 +922,7 @@ int batch_enqueue(prrtc_batch* b, cudaStream_t st, bool upload) {
     a.arena_cap = b->arena;
     a.next_problem = b->d_next;
     a.n_done = b->d_ndone;
-    a.trace = reinterpret_cast<unsigned long long*>(ws->d_out + 16);
+    a.trace = reinterpret_cast<unsigned long long*>(b->d_out + 16);
     a.cta_trace = nullptr;
     if (std::getenv("PRRTC_TRACE")) {
         static long long* d_ct = nullptr;
@@ -920,9 +950,17 @@ int batch_enqueue(prrtc_batch* b, cudaStream_t st, bool upload) {
     a.p.seed = b->params.seed;
     a.ns_max = b->ns_max;
     a.nthreads = b->nthreads;
-    CUDA_TRY(cudaEventRecord(ws->ev0, st));
+    const auto e0 = std::chrono::steady_clock::now();
+    if (b->timed) CUDA_TRY(cudaEventRecord(ws->ev0, st));
+    const auto e1 = std::chrono::steady_clock::now();
     CUDA_TRY(launch_plan(b->robot->args(), a, b->grid, st));
-    CUDA_TRY(cudaEventRecord(ws->ev1, st));
+    const auto e2 = std::chrono::steady_clock::now();
+    if (b->timed) CUDA_TRY(cudaEventRecord(ws->ev1, st));
+    if (std::getenv("PRRTC_HOST_TRACE")) {
+        auto us = [](auto x, auto y) { return std::chrono::duration<double, std::micro>(y - x).count(); };
+        std::fprintf(stderr, "prrtc enqueue: copies %.1f ev0 %.1f launch %.1f ev1 %.1f us\n", us(q0, e0),
+                     us(e0, e1), us(e1, e2), us(e2, std::chrono::steady_clock::now()));
+    }
     if (b->params.validate_path)  // stream-ordered after the planner, outside its timing
         CUDA_TRY(launch_validate_paths(b->robot->args(), a, ws->d_vprefix, 4 * sm_count(b->device), st));
     b->launches = 1;
@@ -955,30 +993,45 @@ double path_cost(const double* path, uint32_t len, uint32_t dof) {
 }
 
 // Copies the header, controls and used arena back and fills out[].
+std::chrono::steady_clock::time_point g_sync_time;  // PRRTC_HOST_TRACE
+
 int batch_collect(prrtc_batch* b, prrtc_result* out) {
     Workspace* ws = b->ws;
     cudaSetDevice(b->device);
     const size_t hdr = Workspace::out_hdr(b->n);
-    // one D2H of header + controls + an arena prefix; a second one only when
-    // the paths overflow the prefix
-    const size_t prefix = std::min<size_t>(b->arena, 1 << 16);
-    CUDA_TRY(cudaMemcpyAsync(ws->h_out, ws->d_out, hdr + 8 * prefix, cudaMemcpyDeviceToHost, b->last_stream));
+    // one D2H of header + controls + an arena prefix sized from the paths of
+    // recent calls (a single problem reads back a few KB, not the whole
+    // arena); a second copy only when the paths overflow the prefix
+    size_t prefix = std::min<size_t>(b->arena, 1 << 16);
+    if (ws->path_hint > 0.0) {
+        const size_t want = (size_t)(1.5 * ws->path_hint * b->n) + 64 * (size_t)b->dof;
+        ws->grow_h_out(std::min<size_t>(want, b->arena));
+        prefix = std::min({(size_t)b->arena, want, ws->h_out_arena});
+    }
+    ws->last_d2h = hdr + 8 * prefix;
+    CUDA_TRY(cudaMemcpyAsync(ws->h_out, b->d_out, hdr + 8 * prefix, cudaMemcpyDeviceToHost, b->last_stream));
     CUDA_TRY(cudaStreamSynchronize(b->last_stream));
+    g_sync_time = std::chrono::steady_clock::now();
     const unsigned char* h = static_cast<const unsigned char*>(ws->h_out);
     unsigned long long used = *reinterpret_cast<const unsigned long long*>(h);
     used = std::min<unsigned long long>(used, b->arena);
+    {
+        const double per = (double)used / b->n;
+        ws->path_hint = per >= ws->path_hint ? per : 0.9 * ws->path_hint + 0.1 * per;
+    }
     const ProbCtl* ctl = reinterpret_cast<const ProbCtl*>(h + 128);
     const double* arena = reinterpret_cast<const double*>(h + hdr);
     std::vector<double> big;
     if (used > prefix) {
         big.resize(used);  // prefix already on the host; fetch only the rest
+        ws->last_d2h += 8 * (used - prefix);
         std::memcpy(big.data(), arena, 8 * prefix);
         CUDA_TRY(cudaMemcpy(big.data() + prefix, b->d_arena + prefix, 8 * (used - prefix),
                             cudaMemcpyDeviceToHost));
         arena = big.data();
     }
     float ms = 0.f;
-    cudaEventElapsedTime(&ms, ws->ev0, ws->ev1);
+    if (b->timed) cudaEventElapsedTime(&ms, ws->ev0, ws->ev1);
     if (std::getenv("PRRTC_TRACE")) {  // kernel span vs per-problem span (globaltimer)
         const auto* tr = reinterpret_cast<const unsigned long long*>(h + 16);
         const long long k0 = (long long)(0x7fffffffffffffffull - tr[0]), k1 = (long long)tr[1];
@@ -1189,17 +1242,39 @@ int plan_batch_once(const prrtc_robot* robot, const prrtc_scene* const* scenes, 
     if (b.device < 0 || b.device >= 64) return set_err(PRRTC_ENODEV, "device ordinal out of range");
     std::lock_guard<std::mutex> lk(g_ws_mu[b.device]);
     Workspace& ws = g_ws[b.device];
+    // a single problem reports the host wall clock: no kernel events
+    b.timed = n_problems > 1 || std::getenv("PRRTC_TRACE") || std::getenv("PRRTC_HOST_TRACE");
+    const auto t1 = std::chrono::steady_clock::now();
     rc = batch_bind(&b, &ws, scenes, starts, goals);
+    const auto t2 = std::chrono::steady_clock::now();
     if (!rc) rc = batch_enqueue(&b, ws.stream, true);
+    const auto t3 = std::chrono::steady_clock::now();
     if (!rc) rc = batch_collect(&b, out);
     if (rc) return rc;
-    const double wall =
-        std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+    const auto t4 = std::chrono::steady_clock::now();
+    const double wall = std::chrono::duration<double, std::milli>(t4 - t0).count();
+    if (std::getenv("PRRTC_HOST_TRACE")) {
+        auto us = [](auto x, auto y) { return std::chrono::duration<double, std::micro>(y - x).count(); };
+        float ev = 0.f;
+        cudaEventElapsedTime(&ev, ws.ev0, ws.ev1);
+        std::fprintf(stderr,
+                     "prrtc host: setup %.1f bind %.1f enqueue %.1f wait+d2h %.1f fill %.1f us | kernel %.1f problem %.1f us\n",
+                     us(t0, t1), us(t1, t2), us(t2, t3), us(t3, g_sync_time), us(g_sync_time, t4), ev * 1e3,
+                     out[0].device_time_ms * 1e3);
+    }
     if (n_problems == 1) out[0].wall_time_ms = wall;
     if (std::getenv("PRRTC_TRACE")) std::fprintf(stderr, "prrtc trace: host wall %.3f ms\n", wall);
     return PRRTC_OK;
 }
 }  // namespace
+
+int prrtc_last_transfer_bytes(int device, uint64_t* h2d, uint64_t* d2h) {
+    if (device < 0 || device >= 64) return set_err(PRRTC_ENODEV, "device ordinal out of range");
+    std::lock_guard<std::mutex> lk(g_ws_mu[device]);
+    if (h2d) *h2d = g_ws[device].last_h2d;
+    if (d2h) *d2h = g_ws[device].last_d2h;
+    return PRRTC_OK;
+}
 
 int prrtc_plan(const prrtc_robot* robot, const prrtc_scene* scene, const double* start,
                const double* goal, uint32_t dof, const prrtc_params* params, prrtc_result* result) {

@@ -767,7 +767,12 @@ __device__ void brute_chunk(Ctx& c, StatAcc& acc, int cnt, bool early_exit, bool
 // states, iterating the set bits. Masks cannot overflow, so no fallback is
 // ever needed. Result: sbad[], IC_FIRSTBAD, IC_QN (= anything flagged).
 // ---------------------------------------------------------------------------
-__device__ __noinline__ void check_chunk(Ctx& c, int cnt, bool two_stage, bool early_exit, bool indep) {
+// stop_flag (nullable): thread 0 samples it once the poses are built and
+// publishes it in ictl[IC_STOP] at the stage-1 barrier (or the brute-force
+// path's final one), for callers that abandon the chain when the problem
+// has been settled meanwhile; the load's latency hides behind stage 1.
+__device__ __noinline__ void check_chunk(Ctx& c, int cnt, bool two_stage, bool early_exit, bool indep,
+                                         const int* stop_flag = nullptr) {
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nw = c.nthreads >> 5;
     const int NS = c.NS, L = c.L, NP = c.NP;
     const ChunkV k = chunk_view(c);
@@ -778,8 +783,10 @@ __device__ __noinline__ void check_chunk(Ctx& c, int cnt, bool two_stage, bool e
     if (prof && tid == 0) prof[1] = clock64();
     fk_chunk(c, cnt);  // also resets sbad / lmask / pmask / IC_QN / IC_FIRSTBAD; ends with __syncthreads
     if (prof && tid == 0) prof[4] = clock64();
+    const int stop = (stop_flag && tid == 0) ? ld_relaxed(stop_flag) : 0;
     if (!two_stage) {
         brute_chunk(c, acc, cnt, early_exit, indep);
+        if (stop_flag && tid == 0) k.ictl[IC_STOP] = stop;
         __syncthreads();
         return;
     }
@@ -846,6 +853,7 @@ __device__ __noinline__ void check_chunk(Ctx& c, int cnt, bool two_stage, bool e
         if (pm) or64_shared(&pmask[blk * NS + s], pm);
         flagged |= pm != 0;
     }
+    if (stop_flag && tid == 0) k.ictl[IC_STOP] = stop;
     const int any_flag = __syncthreads_or(flagged);
     if (prof && tid == 0) prof[5] = clock64();
     if (!any_flag) return;  // nothing flagged: every state free

@@ -13,6 +13,10 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <map>
+#include <mutex>
+#include <utility>
+
 #include "prrtc_b200.h"
 #include "prrtc_device.cuh"
 #include "prrtc_launch.h"
@@ -328,8 +332,12 @@ __device__ long long validate_chain(Ctx& c, const PlanArgs& a, const double* A, 
             sh(c.stat)[1] += (unsigned long long)act * c.fkflops;  // thread 0's flop slot
         }
         trace_phase(a, 5);  // FK + collision
-        check_chunk(c, cnt, a.p.two_stage != 0, a.p.early_exit != 0, false);
+        check_chunk(c, cnt, a.p.two_stage != 0, a.p.early_exit != 0, false, done_flag);
         trace_phase(a, 9);
+        if (done_flag && sh(c.ictl)[IC_STOP] != 0) {  // settled while this chunk was checked
+            *stopped = true;
+            return 0;
+        }
         if (threadIdx.x == 0 && sh(c.ictl)[IC_QN]) ++fine_states;
         // (IC_FIRSTBAD is next reset inside the next chunk's FK, after the
         // state-generation barrier: every thread has read it by then)
@@ -804,8 +812,12 @@ __global__ void __launch_bounds__(NT, MINB) plan_kernel(PlanArgs a) {
             // ---- SIMT edge validation nn -> c_new, then append ----
             int last = nn;
             bool stopped = false;
-            const long long ok = validate_chain(c, a, nnc, cnew, 1, &Ts, nn, &last, nullptr,
+            // (the done flag is sampled here too: a CTA still extending when
+            // another one solved the problem leaves at the next chunk
+            // instead of finishing the iteration — the result is settled)
+            const long long ok = validate_chain(c, a, nnc, cnew, 1, &Ts, nn, &last, &C.done,
                                                 fk_states, fine_states, &stopped);
+            if (stopped) continue;  // the header sees the done flag and leaves
             if (ok == 0) {
                 if (a.p.dynamic_domain && tid == 0) Ts.dd[nn] = 1;  // record_failure
                 continue;
@@ -819,6 +831,7 @@ __global__ void __launch_bounds__(NT, MINB) plan_kernel(PlanArgs a) {
             TRACE_PHASE(4);
             if (tid == 0) {
                 const int po = ld_relaxed(To.published);
+                sh(c.ictl)[IC_TMP3] = ld_relaxed(&C.done);  // settled meanwhile: skip the connect
                 int* known = sh(c.ictl) + IC_KNOWN0 + To.which;
                 if (po > *known || (a.dbg & 1)) {
                     fence_acq_rel();
@@ -828,7 +841,9 @@ __global__ void __launch_bounds__(NT, MINB) plan_kernel(PlanArgs a) {
             }
             __syncthreads();
             const int snap_o = sh(c.ictl)[IC_TMP2];
+            const int settled = sh(c.ictl)[IC_TMP3];
             __syncthreads();
+            if (settled != DONE_RUNNING) continue;  // the header leaves
             nn_scan_multi(c, To.cfg, a.stride, snap_o, cnew, 1, nullptr);
             const int nno = sh(c.mnn_i)[0];
             const double d2o = sh(c.mnn_d)[0];
@@ -971,10 +986,26 @@ __global__ void __launch_bounds__(128) validate_paths_kernel(PlanArgs a, const i
     }
 }
 
+// cudaFuncSetAttribute costs microseconds per call: raise the dynamic shared
+// memory limit of a (kernel, device) only when a launch needs more than it
+// was last set to
+cudaError_t raise_smem_limit(const void* fn, int sm) {
+    static std::mutex mu;
+    static std::map<std::pair<const void*, int>, int> set;
+    int dev = 0;
+    cudaGetDevice(&dev);
+    std::lock_guard<std::mutex> lk(mu);
+    int& cur = set[{fn, dev}];
+    if (sm <= cur) return cudaSuccess;
+    const cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, sm);
+    if (e == cudaSuccess) cur = sm;
+    return e;
+}
+
 cudaError_t launch_validate_paths(const RobotArgs& r, const PlanArgs& a, int* prefix, int grid, cudaStream_t st) {
     path_edges_scan_kernel<<<1, 1024, 0, st>>>(a.ctl, a.n_problems, prefix);
     const size_t sm = smem_bytes(r, a.ns_max, 128);
-    cudaError_t e = cudaFuncSetAttribute(validate_paths_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+    cudaError_t e = raise_smem_limit(reinterpret_cast<const void*>(validate_paths_kernel), (int)sm);
     if (e != cudaSuccess) return e;
     validate_paths_kernel<<<grid, 128, sm, st>>>(a, prefix, 4 * a.p.n_cc);
     return cudaGetLastError();
@@ -995,7 +1026,7 @@ static PlanFn plan_fn(int nthreads) {
 cudaError_t launch_plan(const RobotArgs& r, PlanArgs a, int grid, cudaStream_t st) {
     const size_t sm = smem_bytes(r, a.ns_max, a.nthreads);
     const PlanFn fn = plan_fn(a.nthreads);
-    cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+    cudaError_t e = raise_smem_limit(reinterpret_cast<const void*>(fn), (int)sm);
     if (e != cudaSuccess) return e;
     void* args[] = {&a};
     return cudaLaunchKernel(reinterpret_cast<const void*>(fn), dim3(grid), dim3(a.nthreads), args, sm, st);
@@ -1004,7 +1035,7 @@ cudaError_t launch_plan(const RobotArgs& r, PlanArgs a, int grid, cudaStream_t s
 int plan_occupancy(const RobotArgs& r, int ns_max, int nthreads) {
     const size_t sm = smem_bytes(r, ns_max, nthreads);
     const PlanFn fn = plan_fn(nthreads);
-    cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+    raise_smem_limit(reinterpret_cast<const void*>(fn), (int)sm);
     int n = 0;
     if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, fn, nthreads, sm) != cudaSuccess) return 1;
     return n > 0 ? n : 1;
@@ -1257,8 +1288,7 @@ cudaError_t launch_check_configs(const RobotArgs& r, const SceneArgs& s, const d
                                  int two_stage, uint8_t* out, cudaStream_t st) {
     const int NS = chunk_states();
     const size_t sm = smem_bytes(r, NS, 128);
-    cudaError_t e = cudaFuncSetAttribute(check_configs_kernel,
-                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+    cudaError_t e = raise_smem_limit(reinterpret_cast<const void*>(check_configs_kernel), (int)sm);
     if (e != cudaSuccess) return e;
     const int grid = (int)min((long long)(n + NS - 1) / NS, 148LL * 16);
     if (grid > 0) check_configs_kernel<<<grid, 128, sm, st>>>(r, s, q, n, two_stage, out, NS);
@@ -1270,8 +1300,7 @@ cudaError_t launch_validate_edges(const RobotArgs& r, const SceneArgs& s, const 
                                   int early_exit, uint8_t* out, cudaStream_t st, long long* prof) {
     const int NS = chunk_states();
     const size_t sm = smem_bytes(r, NS, 128);
-    cudaError_t e = cudaFuncSetAttribute(validate_edges_kernel,
-                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+    cudaError_t e = raise_smem_limit(reinterpret_cast<const void*>(validate_edges_kernel), (int)sm);
     if (e != cudaSuccess) return e;
     const int grid = (int)min((long long)n_edges, 148LL * 16);
     if (grid > 0)
@@ -1284,8 +1313,7 @@ cudaError_t launch_debug_fk(const RobotArgs& r, const double* q, int n, float* f
                             float* coarse_out, cudaStream_t st) {
     const int NS = chunk_states();
     const size_t sm = smem_bytes(r, NS, 128);
-    cudaError_t e = cudaFuncSetAttribute(debug_fk_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         (int)sm);
+    cudaError_t e = raise_smem_limit(reinterpret_cast<const void*>(debug_fk_kernel), (int)sm);
     if (e != cudaSuccess) return e;
     const int grid = (int)min((long long)(n + NS - 1) / NS, 148LL * 16);
     if (grid > 0) debug_fk_kernel<<<grid, 128, sm, st>>>(r, q, n, fine_out, coarse_out, NS);

@@ -204,7 +204,28 @@ def plan(model, scene, start, goal, params: PlannerParams | None = None, device:
         _lib.load().prrtc_result_free(C.byref(r))
 
 
+class SceneSet:
+    """Per-problem scene handles packed once for repeated batch calls (setup,
+    like device_scene): plan_batch* accepts it in place of a scene list."""
+
+    def __init__(self, scenes, device: int = 0):
+        self.device = device
+        self.hs = [device_scene(s, device) for s in scenes]
+        self.arr = (C.c_void_p * len(self.hs))(*[h.h.value for h in self.hs])
+
+    def __len__(self) -> int:
+        return len(self.hs)
+
+
+def device_scenes(scenes, device: int = 0) -> SceneSet:
+    return SceneSet(scenes, device)
+
+
 def _scene_handles(scenes, n, device):
+    if isinstance(scenes, SceneSet):
+        if len(scenes) != n or scenes.device != device:
+            raise ValueError("plan_batch: SceneSet must hold one scene per problem on the same device")
+        return scenes.hs, scenes.arr
     if isinstance(scenes, (Scene, DeviceScene)):
         scenes = [scenes] * n
     if len(scenes) != n:

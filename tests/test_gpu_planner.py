@@ -201,6 +201,14 @@ def test_device_path_validation_agrees_with_reference(gpu, oracle, robot):
     assert r1.status != PlanStatus.Solved or r1.path_check == 1
     ba = planner.plan_batch_arrays(m, scenes[:8], S[:8], G[:8], params)
     assert all(c == 1 for c, st in zip(ba.path_check, ba.status) if st == PlanStatus.Solved)
+    # pre-packed scene handles (SceneSet) give the same results as the list
+    bs = planner.plan_batch_arrays(m, planner.device_scenes(scenes[:8]), S[:8], G[:8],
+                                   PlannerParams(tree_capacity=20000, validate_path=True, deterministic=True))
+    bl = planner.plan_batch_arrays(m, scenes[:8], S[:8], G[:8],
+                                   PlannerParams(tree_capacity=20000, validate_path=True, deterministic=True))
+    assert (bs.status == bl.status).all() and np.array_equal(bs.path_data, bl.path_data)
+    with pytest.raises(ValueError):
+        planner.plan_batch_arrays(m, planner.device_scenes(scenes[:4]), S[:8], G[:8], params)
     # off by default: nothing is checked
     off = PlannerParams(tree_capacity=20000)
     r0 = planner.plan_batch(m, scenes[:4], S[:4], G[:4], off)
