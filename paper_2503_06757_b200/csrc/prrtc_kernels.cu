@@ -1075,10 +1075,35 @@ __global__ void __launch_bounds__(128) validate_edges_kernel(RobotArgs r, SceneA
     setup_ctx(c, smem, r.words, r.n_words, r.fine_r64, r.limits, NS);
     load_scene(c, scene_base(smem, r.n_words, c.L, c.dof, NS, c.nthreads), sa.words, sa.f64);
     build_ttab(c, n_cc);
-    c.prof = (prof && blockIdx.x == 0) ? prof : nullptr;  // debug hook: phase stamps
-    if (c.prof && threadIdx.x == 0) {
-        c.prof[0] = t0;
-        c.prof[7] = clock64();
+    c.prof = nullptr;
+    if (prof && blockIdx.x == 0) {
+        // debug hook: phase stamps of the first chunk, warm: the chunk is
+        // checked three times untimed (instruction cache, robot and scene
+        // lines), then once with stamps
+        long long* p = prof;
+        prof = nullptr;
+        for (int rep = 0; rep < 4; ++rep) {
+            double* A = dc(c, DC_A);
+            double* B = dc(c, DC_B);
+            if (threadIdx.x < c.dof) {
+                A[threadIdx.x] = from[threadIdx.x];
+                B[threadIdx.x] = to[threadIdx.x];
+            }
+            __syncthreads();
+            if (rep == 3) {
+                c.prof = p;
+                if (threadIdx.x == 0) {
+                    p[0] = t0;
+                    p[7] = clock64();
+                }
+            }
+            gen_chain_states(c, A, B, 1, n_cc, 0, (int)min((long long)NS, (long long)n_cc), nullptr);
+            if (c.prof && threadIdx.x == 0) c.prof[8] = clock64();
+            check_chunk(c, (int)min((long long)NS, (long long)n_cc), two_stage != 0, early_exit != 0, false);
+            __syncthreads();
+            if (c.prof && threadIdx.x == 0) c.prof[9] = clock64();
+            c.prof = nullptr;
+        }
     }
     for (int e = blockIdx.x; e < n_edges; e += gridDim.x) {
         double* A = dc(c, DC_A);
@@ -1092,12 +1117,9 @@ __global__ void __launch_bounds__(128) validate_edges_kernel(RobotArgs r, SceneA
         for (long long g0 = 0; g0 < n_cc && !(bad && early_exit); g0 += NS) {
             const int cnt = (int)min((long long)NS, n_cc - g0);
             gen_chain_states(c, A, B, 1, n_cc, g0, cnt, nullptr);
-            if (c.prof && threadIdx.x == 0) c.prof[8] = clock64();
             check_chunk(c, cnt, two_stage != 0, early_exit != 0, false);
             bad |= sh(c.ictl)[IC_FIRSTBAD] != kNoBad;
             __syncthreads();
-            if (c.prof && threadIdx.x == 0) c.prof[9] = clock64();
-            c.prof = nullptr;  // first chunk only
         }
         if (threadIdx.x == 0) out[e] = bad ? 0 : 1;
         __syncthreads();
