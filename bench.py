@@ -161,6 +161,54 @@ def traffic_from_profiles():
     return None
 
 
+def microbench(model, scenes, S, G, dev, fp32_peak):
+    """SURVEY.md §8(d) roofline microbenchmarks of the two kernels inside the
+    planner: the collision path (prrtc_validate_edges' kernel) in dense mode
+    (two_stage off, early_exit off: every test executed, the unambiguous
+    FP32-pipe figure) and in the production two-stage mode, and the NN scan
+    (FP64 SoA tree, 100k nodes = one tree at the default capacity) against the
+    measured L2 read bandwidth. Device-resident inputs, CUDA events."""
+    import ctypes
+    from paper_2503_06757_b200 import _lib, planner
+    lib = _lib.load()
+    rob = planner.device_robot(model, dev)
+    out = {}
+    n_edges, n_cc, delta = 4096, 32, 0.5
+    k = np.arange(n_edges) % len(S)
+    A = np.ascontiguousarray(S[k])
+    d = G[k] - A
+    B = np.ascontiguousarray(A + d * np.minimum(1.0, delta / np.linalg.norm(d, axis=1))[:, None])
+    sc = planner.device_scene(scenes[len(scenes) // 2], dev)  # a bookshelf scene
+    dp = lambda a: a.ctypes.data_as(ctypes.POINTER(ctypes.c_double))  # noqa: E731
+    for name, two, early in (("collision_dense", 0, 0), ("collision_two_stage", 1, 1)):
+        ms, fl, te = ctypes.c_double(), ctypes.c_double(), ctypes.c_double()
+        _lib.check(lib.prrtc_bench_validate_edges(rob.h, sc.h, dp(A), dp(B), n_edges, model.dof, n_cc, two, early, 5,
+                                                  ctypes.byref(ms), ctypes.byref(fl), ctypes.byref(te)))
+        states = n_edges * n_cc
+        tf = fl.value / (ms.value * 1e-3) / 1e12
+        out[name] = {"kernel": "validate_edges_kernel", "edges": n_edges, "states": states, "ms": ms.value,
+                     "states_per_s": states / (ms.value * 1e-3), "flops_per_state": fl.value / states,
+                     "tests_per_state": te.value / states, "achieved_tflops": tf,
+                     "frac_fp32_peak": tf / fp32_peak if fp32_peak else None,
+                     "mode": f"two_stage={two} early_exit={early}"}
+    l2 = lib.prrtc_l2_peak_gbs(dev)
+    rng = np.random.default_rng(7)
+    lim = model.limits()
+    T = np.ascontiguousarray(rng.uniform(lim[:, 0], lim[:, 1], size=(100000, model.dof)))
+    Q = np.ascontiguousarray(rng.uniform(lim[:, 0], lim[:, 1], size=(2048, model.dof)))
+    for g in (1, 32):
+        ms = ctypes.c_double()
+        _lib.check(lib.prrtc_bench_nn(dp(T), T.shape[0], model.dof, dp(Q), Q.shape[0], g, dev, 3, ctypes.byref(ms)))
+        gbs = Q.shape[0] * T.shape[0] * model.dof * 8 / (ms.value * 1e-3) / 1e9
+        out[f"nn_group{g}"] = {"kernel": "debug_nn_multi_kernel (the planner's nn_scan_multi)", "tree_nodes": T.shape[0],
+                               "queries": Q.shape[0], "queries_per_pass": g, "ms": ms.value,
+                               "algorithmic_gbs": gbs, "frac_l2_peak": gbs / l2 if l2 else None,
+                               "bytes_per_query": T.shape[0] * model.dof * 8}
+    out["l2_peak_gbs"] = l2
+    out["fp32_peak_tflops"] = fp32_peak
+    return out
+
+
 def bench_extras(dev, params):
     """BASELINE configs 3-5 beside the headline (informational, untimed by the
     driver): Fetch / Baxter 1000-problem batches (configs 3, 4), a 10k mixed
@@ -354,6 +402,7 @@ def run_b200(args):
         from paper_2503_06757_b200 import suite
         q = suite.summarize_values(lat)  # Table-I statistics (bench.cpp:90-109)
         extras = {} if args.no_extras else bench_extras(dev, params)
+        micro = microbench(model, scenes, S, G, dev, peak)
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": max(3, args.warmup), "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
@@ -375,6 +424,7 @@ def run_b200(args):
                          "peak_source": "measured FFMA-chain microbenchmark (prrtc_fp32_peak_tflops); "
                                         "MEASURED_PEAKS.json has no FP32 figure",
                          "algorithmic_flops_per_launch": flops, "traffic": traffic_from_profiles()},
+            "microbench": micro,
             "gpu_launches": args.steps,
             "clocks": clk.summary(),
             **extras,

@@ -306,6 +306,23 @@ int prrtc_debug_chunk_profile(const prrtc_robot* robot, const prrtc_scene* scene
 /* FP32 FMA-pipe peak of the device in TFLOP/s, measured with an FFMA-chain
    microbenchmark (the roofline denominator of the FK / collision work). */
 double prrtc_fp32_peak_tflops(int device);
+/* L2 read bandwidth of the device in GB/s (float4 streaming over a 32 MiB
+   L2-resident buffer from 4 CTAs per SM): the NN scan's roofline denominator. */
+double prrtc_l2_peak_gbs(int device);
+/* Roofline microbenchmark of the collision path: the
+   prrtc_validate_edges kernel over n_edges device-resident edges, `reps`
+   timed launches after a warm-up (CUDA events). ms = mean per launch; flops /
+   tests = algorithmic FLOPs and sphere tests of one launch (device counters;
+   NULL to skip). Dense mode = two_stage 0, early_exit 0. */
+int prrtc_bench_validate_edges(const prrtc_robot* robot, const prrtc_scene* scene, const double* from,
+                               const double* to, uint32_t n_edges, uint32_t dof, int32_t n_cc, int two_stage,
+                               int early_exit, int reps, double* ms, double* flops, double* tests);
+/* NN scan throughput: n_queries queries over a count-node tree (AoS input,
+   scanned in the planner's SoA FP64 layout), `group` queries per pass (the
+   planner's multi-sample pass; 1 = one query per pass), `reps` timed
+   launches. Algorithmic bytes per query = count * dof * 8. */
+int prrtc_bench_nn(const double* tree, uint32_t count, uint32_t dof, const double* q, uint32_t n_queries,
+                   uint32_t group, int device, int reps, double* ms);
 
 #ifdef __cplusplus
 }

@@ -1525,6 +1525,114 @@ double prrtc_fp32_peak_tflops(int device) {
     return measure_fp32_peak(sm_count(device), 0);
 }
 
+double prrtc_l2_peak_gbs(int device) {
+    if (check_device(device)) return 0.0;
+    cudaSetDevice(device);
+    return measure_l2_gbs(sm_count(device), 0);
+}
+
+}  // extern "C"
+
+namespace {
+// mean ms per launch of `launch` over `reps` launches after one warm-up (CUDA events, stream 0)
+template <class F>
+cudaError_t time_launches(F launch, int reps, double* ms) {
+    cudaEvent_t e0, e1;
+    cudaEventCreate(&e0);
+    cudaEventCreate(&e1);
+    cudaError_t e = launch();
+    if (e == cudaSuccess) e = cudaDeviceSynchronize();
+    if (e == cudaSuccess) e = cudaEventRecord(e0, 0);
+    for (int r = 0; r < reps && e == cudaSuccess; ++r) e = launch();
+    if (e == cudaSuccess) e = cudaEventRecord(e1, 0);
+    if (e == cudaSuccess) e = cudaEventSynchronize(e1);
+    float t = 0.f;
+    if (e == cudaSuccess) e = cudaEventElapsedTime(&t, e0, e1);
+    *ms = t / reps;
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    return e;
+}
+}  // namespace
+
+extern "C" {
+
+int prrtc_bench_validate_edges(const prrtc_robot* robot, const prrtc_scene* scene, const double* from,
+                               const double* to, uint32_t n_edges, uint32_t dof, int32_t n_cc, int two_stage,
+                               int early_exit, int reps, double* ms, double* flops, double* tests) {
+    if (!robot || !scene || !from || !to || !ms || n_edges == 0 || reps < 1)
+        return set_err(PRRTC_EINVAL, "prrtc_bench_validate_edges: bad argument");
+    if ((int)dof != robot->dof) return set_err(PRRTC_EINVAL, "prrtc_bench_validate_edges: dimension");
+    if (n_cc < 1) return set_err(PRRTC_EINVAL, "validate_edge: resolution_count must be >= 1");
+    int rc = check_device(robot->device);
+    if (rc) return rc;
+    cudaSetDevice(robot->device);
+    double *df = nullptr, *dt = nullptr;
+    uint8_t* dv = nullptr;
+    unsigned long long* dc = nullptr;
+    if ((rc = dmalloc(&df, (size_t)n_edges * dof)) || (rc = dmalloc(&dt, (size_t)n_edges * dof)) ||
+        (rc = dmalloc(&dv, n_edges)) || (rc = dmalloc(&dc, 2))) {
+        cudaFree(df);
+        cudaFree(dt);
+        cudaFree(dv);
+        return rc;
+    }
+    cudaMemcpy(df, from, 8 * (size_t)n_edges * dof, cudaMemcpyHostToDevice);
+    cudaMemcpy(dt, to, 8 * (size_t)n_edges * dof, cudaMemcpyHostToDevice);
+    const RobotArgs ra = robot->args();
+    const SceneArgs sa = scene->args();
+    cudaError_t e = time_launches(
+        [&] { return launch_validate_edges(ra, sa, df, dt, (int)n_edges, n_cc, two_stage, early_exit, dv, 0); },
+        reps, ms);
+    unsigned long long cnt[2] = {0, 0};
+    if (e == cudaSuccess) e = cudaMemset(dc, 0, 16);  // one counted launch (outside the timing)
+    if (e == cudaSuccess)
+        e = launch_validate_edges(ra, sa, df, dt, (int)n_edges, n_cc, two_stage, early_exit, dv, 0, nullptr, dc);
+    if (e == cudaSuccess) e = cudaMemcpy(cnt, dc, 16, cudaMemcpyDeviceToHost);
+    cudaFree(df);
+    cudaFree(dt);
+    cudaFree(dv);
+    cudaFree(dc);
+    if (e != cudaSuccess) return set_err(PRRTC_ECUDA, std::string("prrtc_bench_validate_edges: ") + cudaGetErrorString(e));
+    if (tests) *tests = (double)cnt[0];
+    if (flops) *flops = (double)cnt[1];
+    return PRRTC_OK;
+}
+
+int prrtc_bench_nn(const double* tree, uint32_t count, uint32_t dof, const double* q, uint32_t n_queries,
+                   uint32_t group, int device, int reps, double* ms) {
+    if (!tree || !q || !ms || count == 0 || n_queries == 0 || reps < 1 || group < 1 || group > 32)
+        return set_err(PRRTC_EINVAL, "prrtc_bench_nn: bad argument");
+    if (dof == 0 || dof > PRRTC_MAX_DOF) return set_err(PRRTC_EINVAL, "prrtc_bench_nn: bad dof");
+    int rc = check_device(device);
+    if (rc) return rc;
+    cudaSetDevice(device);
+    const long long cap = ((long long)count + 31) / 32 * 32;
+    std::vector<double> soa((size_t)cap * dof, 0.0);  // the planner's SoA tree layout
+    for (uint32_t i = 0; i < count; ++i)
+        for (uint32_t d = 0; d < dof; ++d) soa[(size_t)d * cap + i] = tree[(size_t)i * dof + d];
+    double *ds = nullptr, *dq = nullptr, *dd = nullptr;
+    uint32_t* di = nullptr;
+    if ((rc = dmalloc(&ds, soa.size())) || (rc = dmalloc(&dq, (size_t)n_queries * dof)) ||
+        (rc = dmalloc(&dd, n_queries)) || (rc = dmalloc(&di, n_queries))) {
+        cudaFree(ds);
+        cudaFree(dq);
+        cudaFree(dd);
+        return rc;
+    }
+    cudaMemcpy(ds, soa.data(), 8 * soa.size(), cudaMemcpyHostToDevice);
+    cudaMemcpy(dq, q, 8 * (size_t)n_queries * dof, cudaMemcpyHostToDevice);
+    cudaError_t e = time_launches(
+        [&] { return launch_debug_nn_multi(ds, cap, (int)count, (int)dof, dq, (int)n_queries, (int)group, di, dd, 0); },
+        reps, ms);
+    cudaFree(ds);
+    cudaFree(dq);
+    cudaFree(dd);
+    cudaFree(di);
+    if (e != cudaSuccess) return set_err(PRRTC_ECUDA, std::string("prrtc_bench_nn: ") + cudaGetErrorString(e));
+    return PRRTC_OK;
+}
+
 int prrtc_debug_sample(const prrtc_robot* robot, uint64_t index0, uint32_t n, double* out) {
     if (!robot || !out) return set_err(PRRTC_EINVAL, "prrtc_debug_sample: null argument");
     if (n == 0) return PRRTC_OK;

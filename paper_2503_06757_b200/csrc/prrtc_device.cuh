@@ -701,7 +701,7 @@ struct StatAcc {
     }
 };
 
-__device__ void brute_chunk(Ctx& c, StatAcc& acc, int cnt, bool early_exit, bool indep) {
+__device__ __noinline__ void brute_chunk(Ctx& c, StatAcc& acc, int cnt, bool early_exit, bool indep) {
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nw = c.nthreads >> 5;
     const int NS = c.NS, S = c.S, NP = c.NP;
     const SceneV v = scene_view(c);
@@ -713,6 +713,7 @@ __device__ void brute_chunk(Ctx& c, StatAcc& acc, int cnt, bool early_exit, bool
     const int* const nfine = sh(c.nfine);
     const int2* const pairs = sh(c.pairs);
     const double* const fine_r64 = c.fine_r64;
+    const int pflops = range_flops(v, 0, v.P);
     for (int j = warp; j < S; j += nw) {
         const int l = flink[j];
         const float4 f = fine[j];
@@ -720,15 +721,25 @@ __device__ void brute_chunk(Ctx& c, StatAcc& acc, int cnt, bool early_exit, bool
         for (int s = lane; s < cnt; s += 32) {
             if (k.sgroup[s] < 0 || skip_state(k, s, early_exit, indep)) continue;
             const float3 x = pose_pt(pose, NS, l, s, f.x, f.y, f.z);
-            for (int p = 0; p < v.P; ++p) {
-                ++acc.t;
-                acc.f += test_flops(v, p);
+            // every primitive in FP32 first (a mask, as the coarse stage):
+            // only those within two guard bands go through the banded test
+            // and its exact fallback — the rest are certainly free (band()
+            // would return 0), so the verdicts are unchanged
+            unsigned long long m = coarse_mask(v, x.x, x.y, x.z, f.w + 2.0f * v.eps, 0, v.P);
+            acc.t += v.P;
+            acc.f += 18 + pflops;
+            while (m) {
+                const int p = __ffsll((long long)m) - 1;
+                m &= m - 1;
                 if (fine_vs_prim(v, x, f.w, rd, p)) {
                     mark_bad(k, s);
-                    if (early_exit) break;
+                    if (early_exit) {  // the tests after the first hit were not executed
+                        acc.t -= v.P - 1 - p;
+                        acc.f -= range_flops(v, p + 1, v.P);
+                        break;
+                    }
                 }
             }
-            acc.f += 18;
         }
     }
     for (int pr = warp; pr < NP; pr += nw) {

@@ -1068,7 +1068,8 @@ __global__ void __launch_bounds__(128) check_configs_kernel(RobotArgs r, SceneAr
 __global__ void __launch_bounds__(128) validate_edges_kernel(RobotArgs r, SceneArgs sa, const double* from,
                                                               const double* to, int n_edges, int n_cc,
                                                               int two_stage, int early_exit,
-                                                              uint8_t* out, int NS, long long* prof) {
+                                                              uint8_t* out, int NS, long long* prof,
+                                                              unsigned long long* counters) {
     extern __shared__ __align__(16) unsigned char smem[];
     const long long t0 = clock64();
     Ctx c;
@@ -1116,13 +1117,25 @@ __global__ void __launch_bounds__(128) validate_edges_kernel(RobotArgs r, SceneA
         bool bad = false;
         for (long long g0 = 0; g0 < n_cc && !(bad && early_exit); g0 += NS) {
             const int cnt = (int)min((long long)NS, n_cc - g0);
-            gen_chain_states(c, A, B, 1, n_cc, g0, cnt, nullptr);
+            const int act = gen_chain_states(c, A, B, 1, n_cc, g0, cnt, nullptr);
+            if (counters && threadIdx.x == 0) sh(c.stat)[1] += (unsigned long long)act * c.fkflops;
             check_chunk(c, cnt, two_stage != 0, early_exit != 0, false);
             bad |= sh(c.ictl)[IC_FIRSTBAD] != kNoBad;
             __syncthreads();
         }
         if (threadIdx.x == 0) out[e] = bad ? 0 : 1;
         __syncthreads();
+    }
+    if (counters) {  // measurement: executed sphere tests and algorithmic flops
+        unsigned long long t = sh(c.stat)[2 * threadIdx.x], f = sh(c.stat)[2 * threadIdx.x + 1];
+        for (int o = 16; o > 0; o >>= 1) {
+            t += __shfl_xor_sync(0xffffffffu, t, o);
+            f += __shfl_xor_sync(0xffffffffu, f, o);
+        }
+        if ((threadIdx.x & 31) == 0) {
+            atomicAdd(&counters[0], t);
+            atomicAdd(&counters[1], f);
+        }
     }
 }
 
@@ -1304,6 +1317,50 @@ double measure_fp32_peak(int sms, cudaStream_t st) {
     return ms > 0 ? flops / (ms * 1e-3) / 1e12 : 0.0;
 }
 
+// L2 read bandwidth: every CTA streams float4s over a buffer that fits in
+// L2 (after one warm pass), several passes per launch
+__global__ void __launch_bounds__(512) l2_read_kernel(const float4* buf, long long n4, int passes, float* out) {
+    float acc = 0.f;
+    const long long stride = (long long)gridDim.x * blockDim.x;
+    for (int p = 0; p < passes; ++p) {
+        // each pass starts at a CTA-dependent offset so CTAs spread over the slices
+        const long long off = ((long long)blockIdx.x * 7919 + p * 104729) % n4;
+        for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n4; i += stride) {
+            long long k = i + off;
+            if (k >= n4) k -= n4;
+            const float4 v = __ldcg(buf + k);
+            acc += v.x + v.y + v.z + v.w;
+        }
+    }
+    if (acc == 1.2345f) out[0] = acc;  // keeps the loads live
+}
+
+double measure_l2_gbs(int sms, cudaStream_t st) {
+    const long long bytes = 32ll << 20;  // 32 MiB: well inside the 126 MB L2
+    float4* buf = nullptr;
+    float* out = nullptr;
+    if (cudaMalloc(&buf, bytes) != cudaSuccess) return 0.0;
+    cudaMalloc(&out, 4);
+    cudaMemsetAsync(buf, 0, bytes, st);
+    cudaEvent_t e0, e1;
+    cudaEventCreate(&e0);
+    cudaEventCreate(&e1);
+    const long long n4 = bytes / 16;
+    const int grid = 4 * sms, passes = 8;
+    l2_read_kernel<<<grid, 512, 0, st>>>(buf, n4, 2, out);  // warm: lines resident in L2
+    cudaEventRecord(e0, st);
+    for (int r = 0; r < 5; ++r) l2_read_kernel<<<grid, 512, 0, st>>>(buf, n4, passes, out);
+    cudaEventRecord(e1, st);
+    cudaEventSynchronize(e1);
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, e0, e1);
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    cudaFree(buf);
+    cudaFree(out);
+    return ms > 0 ? 5.0 * passes * (double)bytes / (ms * 1e-3) / 1e9 : 0.0;
+}
+
 static int chunk_states() { return 32; }
 
 cudaError_t launch_check_configs(const RobotArgs& r, const SceneArgs& s, const double* q, int n,
@@ -1319,7 +1376,8 @@ cudaError_t launch_check_configs(const RobotArgs& r, const SceneArgs& s, const d
 
 cudaError_t launch_validate_edges(const RobotArgs& r, const SceneArgs& s, const double* from,
                                   const double* to, int n_edges, int n_cc, int two_stage,
-                                  int early_exit, uint8_t* out, cudaStream_t st, long long* prof) {
+                                  int early_exit, uint8_t* out, cudaStream_t st, long long* prof,
+                                  unsigned long long* counters) {
     const int NS = chunk_states();
     const size_t sm = smem_bytes(r, NS, 128);
     cudaError_t e = raise_smem_limit(reinterpret_cast<const void*>(validate_edges_kernel), (int)sm);
@@ -1327,7 +1385,7 @@ cudaError_t launch_validate_edges(const RobotArgs& r, const SceneArgs& s, const 
     const int grid = (int)min((long long)n_edges, 148LL * 16);
     if (grid > 0)
         validate_edges_kernel<<<grid, 128, sm, st>>>(r, s, from, to, n_edges, n_cc, two_stage,
-                                                     early_exit, out, NS, prof);
+                                                     early_exit, out, NS, prof, counters);
     return cudaGetLastError();
 }
 

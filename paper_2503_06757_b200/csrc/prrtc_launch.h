@@ -38,7 +38,7 @@ cudaError_t launch_check_configs(const RobotArgs& r, const SceneArgs& s, const d
 cudaError_t launch_validate_edges(const RobotArgs& r, const SceneArgs& s, const double* from,
                                   const double* to, int n_edges, int n_cc, int two_stage,
                                   int early_exit, uint8_t* out, cudaStream_t st,
-                                  long long* prof = nullptr);
+                                  long long* prof = nullptr, unsigned long long* counters = nullptr);
 cudaError_t launch_debug_fk(const RobotArgs& r, const double* q, int n, float* fine_out,
                             float* coarse_out, cudaStream_t st);
 cudaError_t launch_debug_hits(const SceneArgs& s, const float* centers, const double* radii,
@@ -50,6 +50,7 @@ cudaError_t launch_debug_nn_multi(const double* soa, long long cap, int count, i
 cudaError_t launch_debug_halton(const uint32_t* bases, const uint64_t* idx, int n, double* out,
                                 cudaStream_t st);
 double measure_fp32_peak(int sms, cudaStream_t st);
+double measure_l2_gbs(int sms, cudaStream_t st);
 
 cudaError_t launch_debug_sample(const RobotArgs& r, uint64_t index0, int n, double* out,
                                 cudaStream_t st);
