@@ -136,6 +136,22 @@ def dist_max(x: float, world: int) -> float:
     return float(t.item())
 
 
+def dist_sum(x: float, world: int) -> float:
+    if world == 1:
+        return x
+    import torch
+    import torch.distributed as dist
+    dev = "cuda" if dist.get_backend() == "nccl" else "cpu"
+    t = torch.tensor([x], dtype=torch.float64, device=dev)
+    dist.all_reduce(t, op=dist.ReduceOp.SUM)
+    return float(t.item())
+
+
+def shard(n: int, world: int, rank: int) -> list:
+    """This rank's share of n independent problems (round robin, no exchange)."""
+    return list(range(rank, n, world))
+
+
 def dist_barrier(world: int):
     if world > 1:
         import torch.distributed as dist
@@ -211,26 +227,13 @@ def microbench(model, scenes, S, G, dev, fp32_peak):
 
 def bench_extras(dev, params):
     """BASELINE configs 3-5 beside the headline (informational, untimed by the
-    driver): Fetch / Baxter 1000-problem batches (configs 3, 4), a 10k mixed
-    three-robot batch (config 5; three device batches on three streams,
-    tree_capacity 20000 so 10k resident problems fit in HBM) and the
+    driver), rank 0: Fetch / Baxter 1000-problem batches (configs 3, 4) and the
     dynamic-obstacle replanning loop (config 5: 100 frames, 3 spheres moving
-    1 cm/frame, prrtc_scene_update + prrtc_plan per frame)."""
+    1 cm/frame, prrtc_scene_update + prrtc_plan per frame). The 10k mixed
+    batch is mixed_sharded (every rank)."""
     import torch
     from paper_2503_06757_b200 import planner, replan
     from paper_2503_06757_b200.model import PlannerParams, PlanStatus
-    import copy
-
-    def robot_params(robot, base):
-        # the reference's default dynamic-domain radius (4 delta = 2.0,
-        # planner.hpp:37) starves exploration in 14-D (uniform samples are
-        # almost never within 2.0 of a failed node): the reference itself
-        # solves ~6% of these Baxter problems with it. Scale it with the
-        # dimension (4 delta * dof / 7) for the dual-arm robot.
-        p = copy.copy(base)
-        if robot == "baxter":
-            p.dd_radius = 4.0 * p.delta * 14 / 7
-        return p
 
     out = {"robots": {}}
     for robot in ("fetch", "baxter"):
@@ -255,28 +258,6 @@ def bench_extras(dev, params):
                                 "device_ms_p95": float(np.percentile(dv, 95)), "dof": model.dof,
                                 "dd_radius": rp.resolved_dd_radius(), "problems": len(S)}
         del b
-    # 10k mixed batch: three robots' batches concurrently on three streams
-    mp = PlannerParams(tree_capacity=20000)
-    batches, streams = [], []
-    for robot, n in (("panda", 3334), ("fetch", 3333), ("baxter", 3333)):
-        model, scenes, S, G, _ = load_workload(robot, 1000)
-        reps = -(-n // len(S))
-        batches.append(planner.Batch(model, (scenes * reps)[:n], np.tile(S, (reps, 1))[:n], np.tile(G, (reps, 1))[:n],
-                                     robot_params(robot, mp), device=dev))
-        streams.append(torch.cuda.Stream(device=dev))
-    for b, st in zip(batches, streams):
-        b.launch(st.cuda_stream)
-    torch.cuda.synchronize()
-    t0 = time.perf_counter()
-    for b, st in zip(batches, streams):
-        b.launch(st.cuda_stream)
-    torch.cuda.synchronize()
-    mix_ms = (time.perf_counter() - t0) * 1e3
-    mok = [r.status == PlanStatus.Solved for b in batches for r in b.results()]
-    out["mixed_10k"] = {"problems": len(mok), "problems_per_s": len(mok) / (mix_ms / 1e3),
-                        "success_rate": float(np.mean(mok)), "tree_capacity": 20000,
-                        "timing": "host wall clock around three concurrent stream launches + sync"}
-    del batches
     # replanning loop
     model, scenes, S, G, kinds = load_workload("panda", 1000)
     i = int(np.where(kinds == "table_pick")[0][0])
@@ -288,6 +269,57 @@ def bench_extras(dev, params):
                          "api": "prrtc_scene_update + prrtc_plan per frame (host wall clock)",
                          "obstacles": "3 spheres r=0.05 moving 1 cm/frame through a table_pick scene"}
     return out
+
+
+def robot_params(robot, base):
+    """Per-robot planner settings of the extras. The reference's default
+    dynamic-domain radius (4 delta = 2.0, planner.hpp:37) starves exploration
+    in 14-D (uniform samples are almost never within 2.0 of a failed node):
+    the reference itself solves ~6% of these Baxter problems with it. Scale
+    it with the dimension (4 delta * dof / 7) for the dual-arm robot."""
+    import copy
+    p = copy.copy(base)
+    if robot == "baxter":
+        p.dd_radius = 4.0 * p.delta * 14 / 7
+    return p
+
+
+def mixed_sharded(dev, world, rank, total=10000):
+    """BASELINE config 5: a 10k-problem mixed three-robot batch (1/3 per
+    robot) sharded round robin across the ranks (one GPU each, no data-path
+    collective). Each rank solves its share as three device batches on three
+    streams (tree_capacity 20000 so the resident problems fit in HBM); the
+    time is the host wall clock from a barrier to the rank's sync, max over
+    ranks; problems/s is whole-job."""
+    import torch
+    from paper_2503_06757_b200 import planner
+    from paper_2503_06757_b200.model import PlannerParams, PlanStatus
+    mp = PlannerParams(tree_capacity=20000)
+    per = (total - 2 * (total // 3), total // 3, total // 3)
+    batches, streams, mine = [], [], 0
+    for robot, n in zip(("panda", "fetch", "baxter"), per):
+        model, scenes, S, G, _ = load_workload(robot, 1000)
+        idx = [i % len(S) for i in shard(n, world, rank)]
+        mine += len(idx)
+        batches.append(planner.Batch(model, [scenes[i] for i in idx], S[idx], G[idx],
+                                     robot_params(robot, mp), device=dev))
+        streams.append(torch.cuda.Stream(device=dev))
+    for b, st in zip(batches, streams):  # warm (workspace, first-touch)
+        b.launch(st.cuda_stream)
+    torch.cuda.synchronize()
+    dist_barrier(world)
+    t0 = time.perf_counter()
+    for b, st in zip(batches, streams):
+        b.launch(st.cuda_stream)
+    torch.cuda.synchronize()
+    ms = dist_max((time.perf_counter() - t0) * 1e3, world)
+    ok = sum(r.status == PlanStatus.Solved for b in batches for r in b.results())
+    solved, count = dist_sum(float(ok), world), dist_sum(float(mine), world)
+    del batches
+    return {"problems": int(count), "problems_per_s": count / (ms / 1e3), "ms": ms,
+            "success_rate": solved / count, "tree_capacity": 20000, "n_gpus": world,
+            "sharding": "round robin over ranks, no collective on the data path",
+            "timing": "host wall clock, barrier -> three concurrent stream launches + sync, max over ranks"}
 
 
 def run_reference(args):
@@ -368,21 +400,25 @@ def run_b200(args):
     solved = [r.status == PlanStatus.Solved for r in res]
     flops = float(sum(r.flops for r in res))
 
+    # ---- e2e through the host-buffer C-ABI (prrtc_plan_batch), every rank,
+    # barrier + max over ranks (whole-job problems/s) ----
+    dscenes = planner.device_scenes(scenes, dev)  # setup: handles packed once
+    planner.plan_batch_arrays(model, dscenes, S, G, params, device=dev)  # workspace warm
+    e2e_ms = []
+    for _ in range(max(3, min(args.steps, 10))):
+        dist_barrier(world)
+        t0 = time.perf_counter()
+        er = planner.plan_batch_arrays(model, dscenes, S, G, params, device=dev)
+        e2e_ms.append(dist_max((time.perf_counter() - t0) * 1e3, world))
+    e2e_solved = dist_sum(float(np.sum(er.status == PlanStatus.Solved)), world) / (world * n)
+    mixed = None if args.no_extras else mixed_sharded(dev, world, rank)
+
     line = None
     if rank == 0:
         # ---- roofline of the dominant (only) kernel: plan_kernel ----
         peak = _lib.load().prrtc_fp32_peak_tflops(dev)
         kernel_ms = statistics.median(step_ms)
         achieved = flops / (kernel_ms * 1e-3) / 1e12
-        # ---- e2e through the host-buffer C-ABI (prrtc_plan_batch) ----
-        dscenes = planner.device_scenes(scenes, dev)  # setup: handles packed once
-        planner.plan_batch_arrays(model, dscenes, S, G, params, device=dev)  # workspace warm
-        e2e_ms = []
-        for _ in range(max(3, min(args.steps, 10))):
-            t0 = time.perf_counter()
-            er = planner.plan_batch_arrays(model, dscenes, S, G, params, device=dev)
-            e2e_ms.append((time.perf_counter() - t0) * 1e3)
-        e2e_solved = float(np.mean(er.status == PlanStatus.Solved))
         import ctypes
         h2d_c, d2h_c = ctypes.c_uint64(), ctypes.c_uint64()
         _lib.check(_lib.load().prrtc_last_transfer_bytes(dev, ctypes.byref(h2d_c), ctypes.byref(d2h_c)))
@@ -416,9 +452,9 @@ def run_b200(args):
                            "device_median": float(np.median(dlat)), "samples": len(idx),
                            "success_rate": float(np.mean(lst)), "mean_cost": float(np.mean(lcost)),
                            "api": "prrtc_plan (host wall clock), params.workers = 0 (one 256-thread CTA per SM)"},
-            "e2e": {"value": n / (statistics.median(e2e_ms) / 1e3), "unit": UNIT, "h2d_bytes_per_step": int(h2d),
+            "e2e": {"value": world * n / (statistics.median(e2e_ms) / 1e3), "unit": UNIT, "h2d_bytes_per_step": int(h2d),
                     "d2h_bytes_per_step": int(d2h), "success_rate": float(e2e_solved),
-                    "api": "prrtc_plan_batch (host buffers)"},
+                    "api": "prrtc_plan_batch (host buffers), every rank, max over ranks"},
             "roofline": {"bound": "fp32", "kernel": "plan_kernel", "achieved": achieved, "peak": peak,
                          "unit": "TFLOP/s", "frac": achieved / peak if peak else None,
                          "peak_source": "measured FFMA-chain microbenchmark (prrtc_fp32_peak_tflops); "
@@ -429,6 +465,8 @@ def run_b200(args):
             "clocks": clk.summary(),
             **extras,
         }
+        if mixed is not None:
+            line["mixed_10k"] = mixed
         if world == 1 and not args.no_cpu_baseline:
             threads = os.cpu_count() or 1
             _, kind, cres, cms = cpu_reference(model, scenes, S, G, PlannerParams(workers=1), threads)

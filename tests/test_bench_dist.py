@@ -53,3 +53,16 @@ def test_weak_scaling_value_definition():
     # value = whole-job problems/s: N ranks x problems per rank / max step time
     assert bench.UNIT == "problems/s"
     assert "problems/sec" in bench.METRIC
+
+
+def test_shard_partitions_problems():
+    """Config 5 sharding: every problem lands on exactly one rank, shares
+    differ by at most one (weak per-GPU load), no exchange needed."""
+    import bench
+    for n in (0, 1, 7, 10000):
+        for world in (1, 2, 4, 8):
+            parts = [bench.shard(n, world, r) for r in range(world)]
+            flat = sorted(i for p in parts for i in p)
+            assert flat == list(range(n))
+            sizes = [len(p) for p in parts]
+            assert max(sizes) - min(sizes) <= (1 if n else 0)
