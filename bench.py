@@ -211,8 +211,9 @@ def microbench(model, scenes, S, G, dev, fp32_peak):
     rng = np.random.default_rng(7)
     lim = model.limits()
     T = np.ascontiguousarray(rng.uniform(lim[:, 0], lim[:, 1], size=(100000, model.dof)))
-    Q = np.ascontiguousarray(rng.uniform(lim[:, 0], lim[:, 1], size=(2048, model.dof)))
     for g in (1, 32):
+        # enough queries for >= 592 CTAs (one CTA takes g queries per pass)
+        Q = np.ascontiguousarray(rng.uniform(lim[:, 0], lim[:, 1], size=(2048 if g == 1 else 32 * 592, model.dof)))
         ms = ctypes.c_double()
         _lib.check(lib.prrtc_bench_nn(dp(T), T.shape[0], model.dof, dp(Q), Q.shape[0], g, dev, 3, ctypes.byref(ms)))
         gbs = Q.shape[0] * T.shape[0] * model.dof * 8 / (ms.value * 1e-3) / 1e9

@@ -45,7 +45,7 @@ class DeviceRobot:
         del keep
 
     def __del__(self):
-        if getattr(self, "h", None) and _lib._lib is not None:
+        if getattr(self, "h", None) and getattr(_lib, "_lib", None) is not None:  # module globals may be gone at exit
             _lib._lib.prrtc_robot_destroy(self.h)
             self.h = None
 
@@ -73,7 +73,7 @@ class DeviceScene:
         del keep
 
     def __del__(self):
-        if getattr(self, "h", None) and _lib._lib is not None:
+        if getattr(self, "h", None) and getattr(_lib, "_lib", None) is not None:  # module globals may be gone at exit
             _lib._lib.prrtc_scene_destroy(self.h)
             self.h = None
 
@@ -303,7 +303,7 @@ class Batch:
         return out
 
     def __del__(self):
-        if getattr(self, "h", None) and _lib._lib is not None:
+        if getattr(self, "h", None) and getattr(_lib, "_lib", None) is not None:  # module globals may be gone at exit
             _lib._lib.prrtc_batch_destroy(self.h)
             self.h = None
 
