@@ -167,14 +167,20 @@ def cpu_reference(model, scenes, S, G, params, threads):
     return o, kind, res, ms
 
 
-def traffic_from_profiles():
+def ncu_summary() -> dict:
+    """profiles/ncu_summary.json: the committed ncu --set full capture of
+    plan_kernel (tools/summarize_profile.py), or {}."""
     p = ROOT / "profiles" / "ncu_summary.json"
     if p.exists():
         try:
-            return json.loads(p.read_text()).get("plan_kernel_dram_bytes_per_launch")
+            return json.loads(p.read_text())
         except Exception:
-            return None
-    return None
+            return {}
+    return {}
+
+
+def traffic_from_profiles():
+    return ncu_summary().get("plan_kernel_dram_bytes_per_launch")
 
 
 def microbench(model, scenes, S, G, dev, fp32_peak):
@@ -460,7 +466,12 @@ def run_b200(args):
                          "unit": "TFLOP/s", "frac": achieved / peak if peak else None,
                          "peak_source": "measured FFMA-chain microbenchmark (prrtc_fp32_peak_tflops); "
                                         "MEASURED_PEAKS.json has no FP32 figure",
-                         "algorithmic_flops_per_launch": flops, "traffic": traffic_from_profiles()},
+                         "algorithmic_flops_per_launch": flops, "traffic": traffic_from_profiles(),
+                         # the kernel is latency-bound: issue-slot and pipe utilisation
+                         # of the same launch from the committed ncu capture
+                         "ncu": {k.replace("plan_kernel_", ""): v for k, v in ncu_summary().items()
+                                 if k.startswith("plan_kernel_") and k != "plan_kernel_dram_bytes_per_launch"},
+                         "ncu_source": ncu_summary().get("source")},
             "microbench": micro,
             "gpu_launches": args.steps,
             "clocks": clk.summary(),

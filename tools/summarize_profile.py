@@ -68,6 +68,13 @@ rd, wr = num("dram__bytes_read.sum", byte_scale), num("dram__bytes_write.sum", b
 traffic = rd + wr if rd is not None and wr is not None else None
 out += ["", f"dram bytes per launch (read+write): {traffic}"]
 (dst / f"{name}_plan_kernel.md").write_text("\n".join(out) + "\n")
-(dst / "ncu_summary.json").write_text(json.dumps({"source": f"profiles/{name}_plan_kernel.md",
-                                                  "plan_kernel_dram_bytes_per_launch": traffic}, indent=1) + "\n")
+pct = lambda k: (num(k, {"%": 0.01}) if k in m else None)  # noqa: E731
+(dst / "ncu_summary.json").write_text(json.dumps({
+    "source": f"profiles/{name}_plan_kernel.md",
+    "plan_kernel_dram_bytes_per_launch": traffic,
+    "plan_kernel_issue_active": pct("smsp__issue_active.avg.pct_of_peak_sustained_active"),
+    "plan_kernel_fma_pipe_active": pct("sm__pipe_fma_cycles_active.avg.pct_of_peak_sustained_active"),
+    "plan_kernel_warps_active": pct("sm__warps_active.avg.pct_of_peak_sustained_active"),
+    "plan_kernel_l2_hit_rate": pct("lts__t_sector_hit_rate.pct"),
+}, indent=1) + "\n")
 print("\n".join(out))
