@@ -868,6 +868,7 @@ __device__ __noinline__ void check_chunk(Ctx& c, int cnt, bool two_stage, bool e
     const int any_flag = __syncthreads_or(flagged);
     if (prof && tid == 0) prof[5] = clock64();
     if (!any_flag) return;  // nothing flagged: every state free
+    if (stop_flag && k.ictl[IC_STOP]) return;  // settled: the caller abandons the chunk
     if (tid == 0) k.ictl[IC_QN] = 1;
     // stage 2a: fine spheres of flagged links vs the primitives that flagged
     // them. Work units of up to three consecutive fine spheres of one link

@@ -903,7 +903,9 @@ __global__ void __launch_bounds__(NT, MINB) plan_kernel(PlanArgs a) {
         if (tid == 0) leave_problem(a, prob, leave_msg);
         __syncthreads();
         if (tid == 0 && a.cta_trace) g_trace[1] = globaltimer();
-        if (a.p.deterministic && a.n_problems == 1) break;
+        // a single problem: nothing left to claim or help once it is left
+        // (skips the claim / help-scan round trips on the way out)
+        if (a.n_problems == 1) break;
     }
     if (tid == 0 && a.trace) atomicMax(&a.trace[1], (unsigned long long)globaltimer());
     if (tid == 0 && a.cta_trace) {
