@@ -624,6 +624,11 @@ struct Workspace {
     size_t io_bytes = 0;
     void* h_out = nullptr;
     size_t out_bytes = 0;
+    // mapped pinned block the kernel publishes single-problem results into
+    // (publish_result): flag words, then header, controls and arena
+    static constexpr size_t kMapBytes = 64 << 10;
+    void* h_map = nullptr;
+    unsigned char* d_map = nullptr;
     size_t h_out_arena = 0;  // arena doubles h_out holds past the header
     double path_hint = 0.0;  // recent arena doubles used per problem (sizes the D2H prefix)
     uint64_t last_h2d = 0, last_d2h = 0;  // bytes copied by the last plan call
@@ -646,6 +651,7 @@ struct Workspace {
         cudaSetDevice(device);
         cudaFreeHost(h_io);
         cudaFreeHost(h_out);
+        if (h_map) cudaFreeHost(h_map);
         cudaFree(d_in);
         cudaFree(d_cfg);
         cudaFree(d_parent);
@@ -697,6 +703,20 @@ struct Workspace {
         }
         // ready flags are epoch tagged: zero once, launches use epoch >= 1
         cudaMemset(d_ready, 0, 4 * nnodes);
+        // optional: without a mapped block results come back by D2H copy
+        if (cudaHostAlloc(&h_map, kMapBytes, cudaHostAllocMapped) == cudaSuccess) {
+            std::memset(h_map, 0, kMapBytes);
+            void* dm = nullptr;
+            if (cudaHostGetDevicePointer(&dm, h_map, 0) == cudaSuccess) {
+                d_map = static_cast<unsigned char*>(dm);
+            } else {
+                cudaFreeHost(h_map);
+                h_map = nullptr;
+            }
+        } else {
+            h_map = nullptr;
+            cudaGetLastError();
+        }
         cudaEventCreate(&ev0);
         cudaEventCreate(&ev1);
         cudaStreamCreateWithFlags(&stream, cudaStreamNonBlocking);
@@ -732,6 +752,7 @@ struct prrtc_batch {
     int launches = 0;
     unsigned char* d_out = nullptr;  // ws->d_in + out_offset: out-header, controls, arena
     bool timed = true;  // bracket the kernel with events (batch results report the kernel time)
+    bool use_map = false;  // the kernel publishes the result into the workspace's mapped block
     // device views into ws->d_in / d_out
     double *d_starts = nullptr, *d_goals = nullptr;
     const uint32_t** d_scene_words = nullptr;
@@ -950,6 +971,15 @@ int batch_enqueue(prrtc_batch* b, cudaStream_t st, bool upload) {
     a.p.seed = b->params.seed;
     a.ns_max = b->ns_max;
     a.nthreads = b->nthreads;
+    if (b->use_map && ws->d_map) {
+        a.out_map = ws->d_map;
+        a.out_map_bytes = Workspace::kMapBytes;
+        a.out_dev = b->d_out;
+        a.out_hdr_bytes = Workspace::out_hdr(b->n);
+        a.exit_count = reinterpret_cast<unsigned*>(b->d_out + 32);
+    } else {
+        b->use_map = false;
+    }
     const auto e0 = std::chrono::steady_clock::now();
     if (b->timed) CUDA_TRY(cudaEventRecord(ws->ev0, st));
     const auto e1 = std::chrono::steady_clock::now();
@@ -995,9 +1025,39 @@ double path_cost(const double* path, uint32_t len, uint32_t dof) {
 // Copies the header, controls and used arena back and fills out[].
 std::chrono::steady_clock::time_point g_sync_time;  // PRRTC_HOST_TRACE
 
+int fill_results(prrtc_batch* b, prrtc_result* out, const unsigned char* h, const double* arena,
+                 unsigned long long used);
+
 int batch_collect(prrtc_batch* b, prrtc_result* out) {
     Workspace* ws = b->ws;
     cudaSetDevice(b->device);
+    if (b->use_map) {
+        // wait for publish_result's flag (not for the grid to retire); poll
+        // the stream now and then so a failed launch cannot hang the caller
+        const volatile unsigned* f = static_cast<const volatile unsigned*>(ws->h_map);
+        for (unsigned spins = 1; f[0] != ws->epoch; ++spins) {
+            if ((spins & 1023) == 0) {
+                const cudaError_t q = cudaStreamQuery(b->last_stream);
+                if (q == cudaErrorNotReady) continue;
+                if (f[0] == ws->epoch) break;
+                if (q != cudaSuccess) return set_err(PRRTC_ECUDA, std::string("plan: ") + cudaGetErrorString(q));
+                break;  // retired without the flag: read back below
+            }
+        }
+        std::atomic_thread_fence(std::memory_order_acquire);
+        g_sync_time = std::chrono::steady_clock::now();
+        b->use_map = false;
+        if (f[0] == ws->epoch && f[1] == 1u) {
+            const unsigned char* h = static_cast<const unsigned char*>(ws->h_map) + 64;
+            const size_t hdr = Workspace::out_hdr(b->n);
+            const unsigned long long used =
+                std::min<unsigned long long>(*reinterpret_cast<const unsigned long long*>(h), b->arena);
+            ws->last_d2h = hdr + 8 * used;
+            ws->path_hint = (double)used / b->n;
+            return fill_results(b, out, h, reinterpret_cast<const double*>(h + hdr), used);
+        }
+        // did not fit (very long path): the regular copy-back
+    }
     const size_t hdr = Workspace::out_hdr(b->n);
     // one D2H of header + controls + an arena prefix sized from the paths of
     // recent calls (a single problem reads back a few KB, not the whole
@@ -1019,7 +1079,6 @@ int batch_collect(prrtc_batch* b, prrtc_result* out) {
         const double per = (double)used / b->n;
         ws->path_hint = per >= ws->path_hint ? per : 0.9 * ws->path_hint + 0.1 * per;
     }
-    const ProbCtl* ctl = reinterpret_cast<const ProbCtl*>(h + 128);
     const double* arena = reinterpret_cast<const double*>(h + hdr);
     std::vector<double> big;
     if (used > prefix) {
@@ -1030,6 +1089,14 @@ int batch_collect(prrtc_batch* b, prrtc_result* out) {
                             cudaMemcpyDeviceToHost));
         arena = big.data();
     }
+    return fill_results(b, out, h, arena, used);
+}
+
+// Parses a host copy of the out-header (h), controls and arena into out[].
+int fill_results(prrtc_batch* b, prrtc_result* out, const unsigned char* h, const double* arena,
+                 unsigned long long used) {
+    Workspace* ws = b->ws;
+    const ProbCtl* ctl = reinterpret_cast<const ProbCtl*>(h + 128);
     float ms = 0.f;
     if (b->timed) cudaEventElapsedTime(&ms, ws->ev0, ws->ev1);
     if (std::getenv("PRRTC_TRACE")) {  // kernel span vs per-problem span (globaltimer)
@@ -1244,6 +1311,11 @@ int plan_batch_once(const prrtc_robot* robot, const prrtc_scene* const* scenes, 
     Workspace& ws = g_ws[b.device];
     // a single problem reports the host wall clock: no kernel events
     b.timed = n_problems > 1 || std::getenv("PRRTC_TRACE") || std::getenv("PRRTC_HOST_TRACE");
+    // a single problem's result is published by the kernel into mapped host
+    // memory (no D2H, no wait for the grid to retire); path re-validation runs
+    // a second kernel after the planner, so it keeps the copy-back
+    b.use_map = n_problems == 1 && !params->validate_path && !std::getenv("PRRTC_TRACE") &&
+                !std::getenv("PRRTC_NO_MAP");
     const auto t1 = std::chrono::steady_clock::now();
     rc = batch_bind(&b, &ws, scenes, starts, goals);
     const auto t2 = std::chrono::steady_clock::now();

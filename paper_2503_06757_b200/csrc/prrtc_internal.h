@@ -150,6 +150,14 @@ struct PlanArgs {
     PlanParamsDev p;
     int ns_max;                // states per validation chunk
     int nthreads;
+    // single-problem result publication (null out_map: the host copies back):
+    // the last CTA to finish copies the out-header, controls and used arena
+    // to out_map + 64 (mapped pinned host memory) and raises out_map[0] = epoch
+    unsigned char* out_map;
+    unsigned long long out_map_bytes;
+    const unsigned char* out_dev;       // device out-header; controls and arena follow contiguously
+    unsigned long long out_hdr_bytes;   // 128 + sizeof(ProbCtl) * n_problems
+    unsigned* exit_count;               // CTAs finished (zeroed with the controls)
 };
 
 // Dynamic shared memory bytes for a robot/scene/ns_max combination.

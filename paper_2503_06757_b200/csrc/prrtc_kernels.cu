@@ -638,6 +638,39 @@ __device__ void leave_problem(const PlanArgs& a, int prob, int reason_msg) {
 
 __shared__ Ctx g_ctx;  // the planner's CTA context (see ctx_writer)
 
+// Single-problem launches: the last CTA to finish copies the out-header,
+// controls and used path arena into mapped pinned host memory and raises a
+// flag there (out_map[0] = epoch, out_map[1] = 1 if it fit), so the host
+// reads the result without a D2H copy and without waiting for the grid to
+// retire. Every CTA fences its own stores before counting itself out.
+__device__ void publish_result(Ctx& c, const PlanArgs& a) {
+    const int tid = threadIdx.x;
+    __syncthreads();
+    if (tid == 0) {
+        __threadfence();
+        sh(c.ictl)[IC_TMP1] = atomicAdd(a.exit_count, 1u) == gridDim.x - 1;
+    }
+    __syncthreads();
+    if (!sh(c.ictl)[IC_TMP1]) return;
+    __threadfence();
+    const unsigned long long used = min(__ldcg(a.arena_used), a.arena_cap);
+    const unsigned long long words = (a.out_hdr_bytes >> 3) + used;  // 8-byte words: header, controls, arena
+    const bool fits = 64 + 8 * words <= a.out_map_bytes;
+    if (fits) {
+        const unsigned long long* src = reinterpret_cast<const unsigned long long*>(a.out_dev);
+        unsigned long long* dst = reinterpret_cast<unsigned long long*>(a.out_map + 64);
+        for (unsigned long long i = tid; i < words; i += blockDim.x) dst[i] = __ldcg(src + i);
+    }
+    __threadfence_system();
+    __syncthreads();
+    if (tid == 0) {
+        volatile unsigned* f = reinterpret_cast<volatile unsigned*>(a.out_map);
+        f[1] = fits ? 1u : 0u;
+        __threadfence_system();
+        f[0] = a.epoch;
+    }
+}
+
 template <int NT, int MINB>
 __global__ void __launch_bounds__(NT, MINB) plan_kernel(PlanArgs a) {
     extern __shared__ __align__(16) unsigned char smem[];
@@ -913,6 +946,7 @@ __global__ void __launch_bounds__(NT, MINB) plan_kernel(PlanArgs a) {
         g_trace[2] = globaltimer();
         for (int k = 0; k < kTraceStride; ++k) a.cta_trace[blockIdx.x * kTraceStride + k] = g_trace[k];
     }
+    if (a.out_map) publish_result(c, a);
 }
 
 // ---------------------------------------------------------------------------
