@@ -178,6 +178,7 @@ struct TreeRef {
     int* dd;           // [cap]
     int* reserved;
     int* published;
+    const int* done;   // the problem's done flag (a settled problem's trees are never read again)
     int which;         // 0 start tree, 1 goal tree
 };
 
@@ -224,6 +225,7 @@ __device__ __forceinline__ TreeRef tree_ref(const PlanArgs& a, int prob, int t, 
     r.dd = a.dd + pt * a.stride;
     r.reserved = &a.ctl[prob].reserved[t];
     r.published = &a.ctl[prob].published[t];
+    r.done = &a.ctl[prob].done;
     r.which = t;
     return r;
 }
@@ -283,9 +285,14 @@ __device__ int tree_append_many(Ctx& c, const PlanArgs& a, const TreeRef& T, con
                 __threadfence();
                 const long long idx = (long long)p + lane;
                 const bool r = idx < a.cap && ld_acquire_u(&T.ready[idx]) == a.epoch;
+                // under a burst of appends the carrier can stay behind its
+                // successors for a long time; once the problem has settled
+                // (done != DONE_RUNNING) nobody reads its trees again, so
+                // stop carrying (it held the last CTA out for ~30 us)
+                const bool settled = lane == 0 && ld_relaxed(T.done) != 0;
                 const unsigned m = __ballot_sync(0xffffffffu, r);
                 const int run = (m == 0xffffffffu) ? 32 : (__ffs(~m) - 1);
-                if (run == 0) break;
+                if (run == 0 || __any_sync(0xffffffffu, settled)) break;
                 int old = 0;
                 fence_acq_rel();  // release for the carried slots (acquired through their flags)
                 if (lane == 0) old = atomicCAS(T.published, p, p + run);
