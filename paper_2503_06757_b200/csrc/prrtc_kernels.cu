@@ -383,7 +383,7 @@ __device__ long long validate_chain(Ctx& c, const PlanArgs& a, const double* A, 
 // device path assembly (planner.cpp:125-150): walk meet_a -> root of the
 // start tree (reversed), then meet_b's parents -> root of the goal tree.
 // ---------------------------------------------------------------------------
-__device__ void assemble_path(Ctx& c, const PlanArgs& a, int prob, int meet_a, int meet_b) {
+__device__ void assemble_path_serial(Ctx& c, const PlanArgs& a, int prob, int meet_a, int meet_b) {
     const int tid = threadIdx.x;
     const int dof = c.dof;
     const TreeRef Ta = tree_ref(a, prob, 0, dof), Tb = tree_ref(a, prob, 1, dof);
@@ -421,6 +421,61 @@ __device__ void assemble_path(Ctx& c, const PlanArgs& a, int prob, int meet_a, i
         const int v = ib[k];
         const TreeRef& T = (v >> 30) ? Tb : Ta;
         a.arena[off + e] = __ldcg(&T.cfg[(size_t)d * a.stride + (v & ((1 << 30) - 1))]);
+    }
+    __threadfence();
+    __syncthreads();
+}
+
+// The same path with one walk per tree, both trees at once: thread 0 walks
+// meet_a -> root of the start tree, thread 32 meet_b -> root of the goal
+// tree (one dependent L2 load per hop, instead of four passes by one
+// thread); the walks are recorded in the shared pose buffer and read back
+// reversed / shifted by all threads. Falls back to the serial walk when a
+// branch is longer than half the buffer.
+__device__ void assemble_path(Ctx& c, const PlanArgs& a, int prob, int meet_a, int meet_b) {
+    const int tid = threadIdx.x;
+    const int dof = c.dof;
+    const TreeRef Ta = tree_ref(a, prob, 0, dof), Tb = tree_ref(a, prob, 1, dof);
+    int* ib = reinterpret_cast<int*>(c.pose);
+    const int half = (c.L * 12 * c.NS) >> 1;
+    if (tid == 0 || tid == 32) {
+        const bool ta = tid == 0;
+        const int* par = ta ? Ta.parent : Tb.parent;
+        int* w = ib + (ta ? 0 : half);
+        int n = 0;
+        for (int i = ta ? meet_a : meet_b;;) {
+            if (n < half) w[n] = i;
+            ++n;
+            const int p = __ldcg(par + i);
+            if (p < 0) break;
+            i = p;
+        }
+        sh(c.ictl)[ta ? IC_TMP2 : IC_TMP3] = n;
+    }
+    __syncthreads();
+    const int la = sh(c.ictl)[IC_TMP2], lb = sh(c.ictl)[IC_TMP3];
+    __syncthreads();  // read before thread 0 may reuse the slots
+    if (la > half || lb > half) {
+        assemble_path_serial(c, a, prob, meet_a, meet_b);
+        return;
+    }
+    const int len = la + lb - 1;  // the meeting configuration once (planner.cpp:139-147)
+    if (tid == 0) {
+        const unsigned long long need = (unsigned long long)len * dof;
+        const unsigned long long off = atomicAdd(a.arena_used, need);
+        sh(c.ictl)[IC_TMP4] = len;
+        if (off + need > a.arena_cap) sh(c.ictl)[IC_TMP4] = -1;
+        else a.ctl[prob].path_off = off;
+    }
+    __syncthreads();
+    if (sh(c.ictl)[IC_TMP4] < 0) return;
+    const unsigned long long off = a.ctl[prob].path_off;
+    for (int e = tid; e < len * dof; e += c.nthreads) {
+        const int k = e / dof, d = e - k * dof;
+        const bool inA = k < la;
+        const int v = inA ? ib[la - 1 - k] : ib[half + (k - la + 1)];
+        const TreeRef& T = inA ? Ta : Tb;
+        a.arena[off + e] = __ldcg(&T.cfg[(size_t)d * a.stride + v]);
     }
     __threadfence();
     __syncthreads();
