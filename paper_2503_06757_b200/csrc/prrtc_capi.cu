@@ -908,6 +908,8 @@ int batch_bind(prrtc_batch* b, Workspace* ws, const prrtc_scene* const* scenes, 
 }
 
 
+constexpr int kMnnNodesSingle = 2048;
+
 // Enqueues: inputs H2D (optional), header memset, the planner kernel.
 int batch_enqueue(prrtc_batch* b, cudaStream_t st, bool upload) {
     const auto q0 = std::chrono::steady_clock::now();
@@ -971,6 +973,11 @@ int batch_enqueue(prrtc_batch* b, cudaStream_t st, bool upload) {
     a.p.seed = b->params.seed;
     a.ns_max = b->ns_max;
     a.nthreads = b->nthreads;
+    // multi-sample NN bound (samples x tree nodes per pass, ~4-8 node pairs
+    // per thread): batches trade a longer pass for fewer passes; a single
+    // problem is latency-bound (PRRTC_MNN_NODES overrides, for sweeps)
+    a.mnn_nodes = b->n == 1 ? kMnnNodesSingle : 2048;
+    if (const char* e = std::getenv("PRRTC_MNN_NODES")) a.mnn_nodes = std::max(1, std::atoi(e));
     if (b->use_map && ws->d_map) {
         a.out_map = ws->d_map;
         a.out_map_bytes = Workspace::kMapBytes;

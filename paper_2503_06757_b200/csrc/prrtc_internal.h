@@ -158,6 +158,7 @@ struct PlanArgs {
     const unsigned char* out_dev;       // device out-header; controls and arena follow contiguously
     unsigned long long out_hdr_bytes;   // 128 + sizeof(ProbCtl) * n_problems
     unsigned* exit_count;               // CTAs finished (zeroed with the controls)
+    int mnn_nodes;                      // multi-sample NN bound: m <= mnn_nodes / tree size
 };
 
 // Dynamic shared memory bytes for a robot/scene/ns_max combination.

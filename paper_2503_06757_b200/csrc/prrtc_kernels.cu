@@ -876,7 +876,7 @@ __global__ void __launch_bounds__(NT, MINB) plan_kernel(PlanArgs a) {
             // one NN scan and accept test per iteration (planner.cpp:216-219).
             TRACE_PHASE(2);
             int m = 1;
-            if (a.p.balance) m = max(1, min(sh(c.ictl)[IC_TMP5], 2048 / max(1, snap)));
+            if (a.p.balance) m = max(1, min(sh(c.ictl)[IC_TMP5], a.mnn_nodes / max(1, snap)));
             // (the scan also evaluates each sample's acceptance: duplicate,
             // planner.cpp:218 / DynamicDomain::accept, sampling.hpp:61-75)
             nn_scan_multi(c, Ts.cfg, a.stride, snap, sh(c.sbuf) + slot * dof, m,
