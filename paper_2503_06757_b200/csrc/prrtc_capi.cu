@@ -981,6 +981,8 @@ int batch_enqueue(prrtc_batch* b, cudaStream_t st, bool upload) {
     if (b->use_map && ws->d_map) {
         a.out_map = ws->d_map;
         a.out_map_bytes = Workspace::kMapBytes;
+        if (const char* e = std::getenv("PRRTC_MAP_BYTES"))  // tests: force the copy-back fallback
+            a.out_map_bytes = std::min<unsigned long long>(a.out_map_bytes, std::strtoull(e, nullptr, 10));
         a.out_dev = b->d_out;
         a.out_hdr_bytes = Workspace::out_hdr(b->n);
         a.exit_count = reinterpret_cast<unsigned*>(b->d_out + 32);

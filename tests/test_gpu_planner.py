@@ -235,3 +235,40 @@ def test_replanning_loop_with_scene_updates(gpu, oracle):
             ref = oracle.plan(m, f.scene, s, g, PlannerParams(workers=1, tree_capacity=20000))
             assert ref.status != PlanStatus.Solved or r.status == PlanStatus.Failed
     assert solved >= 8
+
+
+@pytest.mark.parametrize("robot", ["panda", "fetch"])
+def test_single_problem_result_paths_agree(gpu, oracle, robot, monkeypatch):
+    """A single problem's result comes back three ways: published by the
+    kernel into mapped host memory (default), the same launch with a mapped
+    block too small for the path (PRRTC_MAP_BYTES: publish_result raises the
+    flag without the payload, the host copies back), and the plain D2H
+    copy-back (PRRTC_NO_MAP). Deterministic mode makes the three runs the
+    same search: identical status, path, iterations, FK and fine-stage
+    counters; repeated calls on the same workspace stay identical."""
+    m = robots.get(robot)
+    probs = load_problems(robot, 12)
+    params = PlannerParams(deterministic=True, tree_capacity=20000)
+    for kind, pid, s, g in probs[:6]:
+        scene, _ = make_scene(robot, kind, pid)
+        runs = []
+        for env in ({}, {"PRRTC_MAP_BYTES": "300"}, {"PRRTC_NO_MAP": "1"}, {}):
+            for k in ("PRRTC_MAP_BYTES", "PRRTC_NO_MAP"):
+                monkeypatch.delenv(k, raising=False)
+            for k, v in env.items():
+                monkeypatch.setenv(k, v)
+            runs.append(planner.plan(m, scene, s, g, params))
+        for k in ("PRRTC_MAP_BYTES", "PRRTC_NO_MAP"):
+            monkeypatch.delenv(k, raising=False)
+        r0 = runs[0]
+        for r in runs[1:]:
+            assert r.status == r0.status and r.message == r0.message
+            assert np.array_equal(r.path, r0.path)
+            assert r.iterations_total == r0.iterations_total
+            # (sphere_tests is timing dependent: the parallel early exit
+            # skips work once a chunk's first bad state is known)
+            assert r.check_stats.fk_calls == r0.check_stats.fk_calls
+            assert r.check_stats.fine_stage_entries == r0.check_stats.fine_stage_entries
+            assert r.tree_nodes == r0.tree_nodes
+        if r0.status == PlanStatus.Solved:
+            assert oracle.path_valid(m, scene, r0.path, params.n_cc)
