@@ -1175,8 +1175,10 @@ int fill_results(prrtc_batch* b, prrtc_result* out, const unsigned char* h, cons
         const ProbCtl& C = ctl[i];
         r.dof = b->dof;
         r.status = C.done == 1 ? PRRTC_SOLVED : C.done == 3 ? PRRTC_INFEASIBLE_ENDPOINT : PRRTC_FAILED;
-        if (C.done == 0) std::snprintf(r.message, sizeof(r.message), "problem did not finish");
-        else std::snprintf(r.message, sizeof(r.message), "%s", message_for(C.msg));
+        {  // (no snprintf per result: ~0.1 ms per 1000-problem batch)
+            const char* msg = C.done == 0 ? "problem did not finish" : message_for(C.msg);
+            if (msg[0]) std::strncpy(r.message, msg, sizeof(r.message) - 1);
+        }
         if (r.status == PRRTC_SOLVED && C.path_len > 0 &&
             C.path_off + (unsigned long long)C.path_len * b->dof <= used) {
             r.path_len = C.path_len;
