@@ -823,8 +823,13 @@ int batch_setup(prrtc_batch* b, const prrtc_robot* robot, const prrtc_scene* con
     const bool heavy = robot->n_fine > 64 || robot->n_pairs > 48;
     b->nthreads = params->threads_per_cta ? (int)params->threads_per_cta : (n_problems == 1 || heavy ? 256 : 128);
     // states per validation chunk: one n_cc = 32 edge; a 256-thread CTA uses
-    // its extra warps to split links / pairs / primitives of the same chunk
-    b->ns_max = std::getenv("PRRTC_NS64") && b->nthreads == 256 ? 64 : 32;
+    // its extra warps to split links / pairs / primitives of the same chunk.
+    // A single problem (latency-bound, one CTA per SM) takes 64-state chunks:
+    // a connect chain needs half the chunk rounds (Panda median wall latency
+    // 0.141 -> 0.121 ms, tools/ab_env.sh); PRRTC_NS32 / PRRTC_NS64 force either
+    const bool ns64 = b->nthreads == 256 && !std::getenv("PRRTC_NS32") &&
+                      (n_problems == 1 || std::getenv("PRRTC_NS64"));
+    b->ns_max = ns64 ? 64 : 32;
     const int okey = b->ns_max / 32 + (b->nthreads == 256 ? 5 : 0);
     int occ = robot->occ[okey].load(std::memory_order_relaxed);
     if (occ == 0) {
