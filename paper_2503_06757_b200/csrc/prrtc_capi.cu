@@ -827,9 +827,10 @@ int batch_setup(prrtc_batch* b, const prrtc_robot* robot, const prrtc_scene* con
     // A single problem (latency-bound, one CTA per SM) takes 64-state chunks:
     // a connect chain needs half the chunk rounds (Panda median wall latency
     // 0.141 -> 0.121 ms, tools/ab_env.sh); PRRTC_NS32 / PRRTC_NS64 force either.
-    // (128-state chunks, PRRTC_NS128: Panda median -5% but p95 +2%, Fetch +4%)
-    const bool ns64 = b->nthreads == 256 && !std::getenv("PRRTC_NS32") &&
-                      (n_problems == 1 || std::getenv("PRRTC_NS64"));
+    // (128-state chunks, PRRTC_NS128: Panda median -5% but p95 +2%, Fetch +4%;
+    // 64-state chunks in the Panda batch: 159k -> 137k problems/s)
+    const bool ns64 = !std::getenv("PRRTC_NS32") &&
+                      ((n_problems == 1 && b->nthreads == 256) || std::getenv("PRRTC_NS64"));
     b->ns_max = ns64 ? (std::getenv("PRRTC_NS128") ? 128 : 64) : 32;
     const int okey = b->ns_max / 32 + (b->nthreads == 256 ? 5 : 0);
     int occ = robot->occ[okey].load(std::memory_order_relaxed);
