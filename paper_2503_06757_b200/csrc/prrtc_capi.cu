@@ -145,6 +145,7 @@ struct prrtc_scene {
     double extent = 0.0;
     uint32_t* d_words = nullptr;
     double* d_f64 = nullptr;
+    size_t cap_words = 0, cap_f64 = 0;  // device allocation sizes (elements)
     SceneArgs args() const {
         SceneArgs s;
         s.words = d_words;
@@ -531,13 +532,25 @@ static void finish_scene_words(prrtc_scene* s, double robot_reach) {
 
 static int upload_scene(prrtc_scene* s) {
     cudaSetDevice(s->device);
-    cudaFree(s->d_words);
-    cudaFree(s->d_f64);
-    s->d_words = nullptr;
-    s->d_f64 = nullptr;
-    if (cudaMalloc(&s->d_words, 4 * s->words.size()) != cudaSuccess ||
-        cudaMalloc(&s->d_f64, 8 * std::max<size_t>(1, s->f64.size())) != cudaSuccess)
-        return set_err(PRRTC_ENOMEM, "scene: device allocation failed");
+    const size_t nf = std::max<size_t>(1, s->f64.size());
+    if (s->d_words && s->words.size() <= s->cap_words && nf <= s->cap_f64) {
+        // dynamic obstacles (prrtc_scene_update): rewrite in place once no
+        // launch on the device can still read the scene (a single-problem
+        // call returns when its result is published, possibly before the
+        // grid has retired)
+        if (cudaDeviceSynchronize() != cudaSuccess) return set_err(PRRTC_ECUDA, "scene: device sync failed");
+    } else {
+        cudaFree(s->d_words);  // (implicitly waits for running launches)
+        cudaFree(s->d_f64);
+        s->d_words = nullptr;
+        s->d_f64 = nullptr;
+        s->cap_words = s->cap_f64 = 0;
+        if (cudaMalloc(&s->d_words, 4 * s->words.size()) != cudaSuccess ||
+            cudaMalloc(&s->d_f64, 8 * nf) != cudaSuccess)
+            return set_err(PRRTC_ENOMEM, "scene: device allocation failed");
+        s->cap_words = s->words.size();
+        s->cap_f64 = nf;
+    }
     cudaMemcpy(s->d_words, s->words.data(), 4 * s->words.size(), cudaMemcpyHostToDevice);
     if (!s->f64.empty()) cudaMemcpy(s->d_f64, s->f64.data(), 8 * s->f64.size(), cudaMemcpyHostToDevice);
     if (cudaGetLastError() != cudaSuccess) return set_err(PRRTC_ECUDA, "scene: upload failed");
