@@ -45,12 +45,16 @@ UNIT = "problems/s"
 
 
 def load_workload(robot: str, n: int):
+    """The first n problems of the robot's 1000-problem set (all of it for
+    n >= 1000); a smaller n takes an evenly spread subset, so every scene
+    kind (the set is ordered table_pick / bookshelf / cage) stays represented."""
     from paper_2503_06757_b200 import robots
     from paper_2503_06757_b200.scenes import make_scene
     d = np.load(ROOT / "tests" / "golden" / f"problems_{robot}.npz")
-    n = min(n, len(d["pid"]))
-    scenes = [make_scene(robot, str(k), int(p))[0] for k, p in zip(d["kind"][:n], d["pid"][:n])]
-    return robots.get(robot), scenes, d["start"][:n].copy(), d["goal"][:n].copy(), d["kind"][:n]
+    N = len(d["pid"])
+    idx = np.arange(N) if n >= N else np.unique(np.linspace(0, N - 1, n).round().astype(int))
+    scenes = [make_scene(robot, str(d["kind"][i]), int(d["pid"][i]))[0] for i in idx]
+    return robots.get(robot), scenes, d["start"][idx].copy(), d["goal"][idx].copy(), d["kind"][idx]
 
 
 def workload_config(robot, n, params, extra=None):
@@ -289,6 +293,104 @@ def robot_params(robot, base):
     if robot == "baxter":
         p.dd_radius = 4.0 * p.delta * 14 / 7
     return p
+
+
+def _stats(ok, cost, res_paths):
+    c = [x for x, o in zip(cost, ok) if o]
+    return {"success": float(np.mean(ok)) if len(ok) else None,
+            "cost_median": float(np.median(c)) if c else None, "cost_mean": float(np.mean(c)) if c else None}
+
+
+def parity_block(robot_names, workers_list, n, device=0, tree_capacity=200000, threads=None):
+    """Equal-budget statistical parity (north_star: success no lower than the
+    reference's, initial path cost reported alongside; every returned path
+    re-validated by the reference checker). Per robot and W: the B200 batch
+    and the reference planner (oracle/_ref, the unmodified sources) run the
+    SAME problems at IDENTICAL PlannerParams — workers = W, so both get the
+    iteration budget max_iters_per_worker x W (planner.cpp:199,287-288) —
+    and the reference checker re-validates every returned path of both at
+    n_cc and at 4 n_cc (fine only, early exit off). The B200
+    arm also runs in sound mode (validate_path). Untimed by the driver:
+    correctness evidence beside the headline."""
+    from paper_2503_06757_b200 import planner
+    from paper_2503_06757_b200.model import PlannerParams, PlanStatus
+    threads = threads or os.cpu_count() or 1
+    out = {"params": "reference defaults (delta 0.5, n_cc 32, max_iters_per_worker 2000, dynamic domain, "
+                     "two-stage, early exit, Halton) with workers = W on both arms",
+           "tree_capacity": tree_capacity, "host_threads": threads, "robots": {}}
+    o = None
+    for robot in robot_names:
+        model, scenes, S, G, kinds = load_workload(robot, n)
+        dsc = planner.device_scenes(scenes, device)
+        rr = {"problems": len(S)}
+        for W in workers_list:
+            params = robot_params(robot, PlannerParams(workers=W, tree_capacity=tree_capacity))
+            planner.plan_batch_arrays(model, dsc, S[:8], G[:8], params, device=device)  # workspace warm-up
+            t0 = time.perf_counter()
+            br = planner.plan_batch_arrays(model, dsc, S, G, params, device=device)
+            g_ms = (time.perf_counter() - t0) * 1e3
+            sound = robot_params(robot, PlannerParams(workers=W, tree_capacity=tree_capacity, validate_path=True))
+            t0 = time.perf_counter()
+            bs = planner.plan_batch_arrays(model, dsc, S, G, sound, device=device)
+            s_ms = (time.perf_counter() - t0) * 1e3
+            if o is None:
+                from oracle import Oracle, available
+                o = Oracle("ref" if available("ref") else "port")
+                out["reference_kind"] = o.kind
+            rth = max(1, threads // W)  # W threads per problem, problems side by side
+            t0 = time.perf_counter()
+            ref, _ = o.plan_many(model, scenes, S, G, params, threads=rth)
+            r_ms = (time.perf_counter() - t0) * 1e3
+            g_ok = br.status == PlanStatus.Solved
+            r_ok = np.array([r.status == PlanStatus.Solved for r in ref])
+            g_paths = [p for p, k in zip(br.paths, g_ok) if k]
+            r_paths = [r.path for r in ref if r.status == PlanStatus.Solved]
+            g_sc = [s for s, k in zip(scenes, g_ok) if k]
+            r_sc = [s for s, k in zip(scenes, r_ok) if k]
+            nc = params.n_cc
+
+            def valid(sc, ps, m):
+                return float(np.mean(o.paths_valid(model, sc, ps, m, threads=threads))) if ps else None
+            both = g_ok & r_ok
+            row = {
+                "b200": {**_stats(g_ok, br.cost, None), "valid_ncc": valid(g_sc, g_paths, nc),
+                         "valid_4ncc": valid(g_sc, g_paths, 4 * nc),
+                         "iterations_mean": float(np.mean(br.iterations_total)),
+                         "problems_per_s_e2e": len(S) / (g_ms / 1e3)},
+                "b200_sound": {**_stats(bs.status == PlanStatus.Solved, bs.cost, None),
+                               "valid_4ncc_device": float(np.mean(bs.path_check[bs.status == PlanStatus.Solved] == 1))
+                               if (bs.status == PlanStatus.Solved).any() else None,
+                               "problems_per_s_e2e": len(S) / (s_ms / 1e3)},
+                "reference": {**_stats(r_ok, [r.cost for r in ref], None), "valid_ncc": valid(r_sc, r_paths, nc),
+                              "valid_4ncc": valid(r_sc, r_paths, 4 * nc),
+                              "iterations_mean": float(np.mean([r.iterations_total for r in ref])),
+                              "problems_per_s": len(S) / (r_ms / 1e3), "threads_per_problem": W,
+                              "problems_in_parallel": rth},
+                "both_solved": int(both.sum()),
+                "cost_mean_both_solved": {"b200": float(np.mean(br.cost[both])) if both.any() else None,
+                                          "reference": float(np.mean([r.cost for r, b in zip(ref, both) if b]))
+                                          if both.any() else None},
+                "dd_radius": params.resolved_dd_radius(),
+            }
+            if W > 1:
+                # single-problem mode: prrtc_plan puts W CTAs on the problem at once,
+                # W concurrent workers like the reference's W threads (the batch
+                # arm above shares its CTAs elastically over 1000 problems, so a
+                # problem there mostly runs as one worker with the W-fold budget)
+                t0 = time.perf_counter()
+                sr = [planner.plan(model, dsc.hs[i], S[i], G[i], params, device=device) for i in range(len(S))]
+                p_ms = (time.perf_counter() - t0) * 1e3
+                s_ok = np.array([r.status == PlanStatus.Solved for r in sr])
+                s_paths = [r.path for r in sr if r.status == PlanStatus.Solved]
+                s_sc = [sc for sc, k in zip(scenes, s_ok) if k]
+                row["b200_single"] = {**_stats(s_ok, [r.cost for r in sr], None),
+                                      "valid_ncc": valid(s_sc, s_paths, nc), "valid_4ncc": valid(s_sc, s_paths, 4 * nc),
+                                      "iterations_mean": float(np.mean([r.iterations_total for r in sr])),
+                                      "problems_per_s_e2e": len(S) / (p_ms / 1e3), "ctas_per_problem": W}
+            row["success_not_below_reference"] = row["b200"]["success"] >= row["reference"]["success"]
+            rr[f"W{W}"] = row
+        out["robots"][robot] = rr
+    return out
 
 
 def mixed_sharded(dev, world, rank, total=10000):

@@ -73,6 +73,11 @@ class Oracle:
             f.restype = res
             f.argtypes = args
             self.fn[name] = f
+        # optional: threaded batch path check (reference build only)
+        self._many = getattr(self.lib, PREFIX[kind] + "paths_valid_many", None)
+        if self._many is not None:
+            self._many.restype = C.c_int
+            self._many.argtypes = [P, C.POINTER(P), C.c_uint32, DP, U64P, C.c_int, C.c_uint32, U8P]
         self._robots = {}
         self._scenes = {}
 
@@ -268,6 +273,22 @@ class Oracle:
         if r < 0:
             raise ValueError(self.err())
         return bool(r)
+
+    def paths_valid(self, model, scenes, paths, n: int, threads: int = 1) -> np.ndarray:
+        """path_valid over a list of paths (one scene each): bool array."""
+        h, dof, _ = self.robot(model)
+        if self._many is None or threads <= 1:
+            return np.array([len(p) > 0 and self.path_valid(model, s, p, n) for s, p in zip(scenes, paths)])
+        ps = [np.ascontiguousarray(np.asarray(p, dtype=np.float64).reshape(-1, dof)) for p in paths]
+        off = np.zeros(len(ps) + 1, dtype=np.uint64)
+        off[1:] = np.cumsum([p.size for p in ps])
+        data = np.concatenate([p.ravel() for p in ps]) if off[-1] else np.zeros(1)
+        sh = (P * len(ps))(*[self.scene(s) for s in scenes])
+        out = np.zeros(len(ps), dtype=np.uint8)
+        self._many(h, sh, len(ps), _dp(data), off.ctypes.data_as(U64P), n, threads, out.ctypes.data_as(U8P))
+        if (out == 2).any():
+            raise ValueError(self.err())
+        return out == 1
 
     def path_cost(self, path) -> float:
         p = np.ascontiguousarray(path, dtype=np.float64)

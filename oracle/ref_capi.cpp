@@ -461,6 +461,30 @@ int ref_path_valid(void* robot, void* scene, const double* path, uint32_t len, i
     }
 }
 
+// ref_path_valid over many paths (path i = doubles [off[i], off[i+1]) of
+// path_data, scene i) on n_threads host threads: out[i] = 1 valid, 0 invalid
+// or empty, 2 error. The per-path check is the reference checker exactly as
+// in ref_path_valid (fine-only, early exit off).
+int ref_paths_valid_many(void* robot, void* const* scenes, uint32_t n, const double* path_data,
+                         const uint64_t* off, int n_cc, uint32_t n_threads, uint8_t* out) {
+    const auto& m = *static_cast<RobotModel*>(robot);
+    std::atomic<uint32_t> next{0};
+    auto work = [&]() {
+        for (;;) {
+            const uint32_t i = next.fetch_add(1);
+            if (i >= n) break;
+            const uint32_t len = (uint32_t)((off[i + 1] - off[i]) / m.dof);
+            const int r = ref_path_valid(robot, scenes[i], path_data + off[i], len, n_cc);
+            out[i] = r < 0 ? 2 : (uint8_t)r;
+        }
+    };
+    std::vector<std::thread> th;
+    for (uint32_t t = 1; t < std::max(1u, n_threads); ++t) th.emplace_back(work);
+    work();
+    for (auto& t : th) t.join();
+    return 0;
+}
+
 // path_cost (planner.cpp:152-158) with the active backend.
 double ref_path_cost(const double* path, uint32_t len, uint32_t dof) {
     std::vector<Config> p;

@@ -14,6 +14,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <atomic>
+#include <memory>
 #include <mutex>
 #include <string>
 #include <vector>
@@ -108,6 +109,48 @@ uint32_t fbits(float f) {
     return u;
 }
 
+// Synchronous upload of setup data (robots, scenes) on a per-device
+// non-blocking stream, waited on before returning: a cudaMemcpy from pageable
+// memory may return before its DMA lands, and the planner's streams are not
+// ordered after the legacy default stream.
+std::mutex g_up_mu[64];
+cudaStream_t g_up_stream[64];
+
+cudaError_t upload_sync(int device, const std::pair<void*, std::pair<const void*, size_t>>* copies, int n) {
+    if (device < 0 || device >= 64) return cudaErrorInvalidDevice;
+    std::lock_guard<std::mutex> lk(g_up_mu[device]);
+    cudaSetDevice(device);
+    if (!g_up_stream[device]) {
+        cudaError_t e = cudaStreamCreateWithFlags(&g_up_stream[device], cudaStreamNonBlocking);
+        if (e != cudaSuccess) return e;
+    }
+    for (int i = 0; i < n; ++i) {
+        if (copies[i].second.second == 0) continue;
+        cudaError_t e = cudaMemcpyAsync(copies[i].first, copies[i].second.first, copies[i].second.second,
+                                        cudaMemcpyHostToDevice, g_up_stream[device]);
+        if (e != cudaSuccess) return e;
+    }
+    return cudaStreamSynchronize(g_up_stream[device]);
+}
+
+// A completion marker of planner launches: an event recorded on a launch's
+// stream after its last kernel. Workspaces own one (re-recorded per launch,
+// so waiting on it is conservative: it covers every earlier launch on that
+// stream); a scene keeps the markers of the workspaces that have read it, so
+// prrtc_scene_update can wait for exactly those launches instead of the
+// whole device.
+struct UseMark {
+    cudaEvent_t ev = nullptr;
+    int device = 0;
+    ~UseMark() {
+        if (ev) {
+            cudaSetDevice(device);
+            cudaEventDestroy(ev);
+        }
+    }
+};
+using UseMarkP = std::shared_ptr<UseMark>;
+
 }  // namespace
 
 // ---------------------------------------------------------------------------
@@ -146,6 +189,31 @@ struct prrtc_scene {
     uint32_t* d_words = nullptr;
     double* d_f64 = nullptr;
     size_t cap_words = 0, cap_f64 = 0;  // device allocation sizes (elements)
+    // bumped by every prrtc_scene_update: a persistent batch re-stages the
+    // scene's device pointers and FP64 section offsets when it changed
+    std::atomic<uint64_t> generation{0};
+    // completion markers of the launches that read this scene (see UseMark)
+    mutable std::mutex mark_mu;
+    mutable std::vector<UseMarkP> marks;
+    void mark_use(const UseMarkP& m) const {
+        std::lock_guard<std::mutex> lk(mark_mu);
+        for (const auto& x : marks)
+            if (x == m) return;
+        marks.push_back(m);
+    }
+    // wait until no launch that read the scene is still running
+    cudaError_t wait_unused() const {
+        std::vector<UseMarkP> ms;
+        {
+            std::lock_guard<std::mutex> lk(mark_mu);
+            ms = marks;
+        }
+        for (const auto& m : ms) {
+            const cudaError_t e = cudaEventSynchronize(m->ev);
+            if (e != cudaSuccess) return e;
+        }
+        return cudaSuccess;
+    }
     SceneArgs args() const {
         SceneArgs s;
         s.words = d_words;
@@ -385,11 +453,11 @@ int prrtc_robot_create(const prrtc_robot_desc* d, int device, prrtc_robot** out)
         prrtc_robot_destroy(r);
         return set_err(PRRTC_ENOMEM, "prrtc_robot_create: device allocation failed");
     }
-    cudaMemcpy(r->d_words, w.data(), 4 * w.size(), cudaMemcpyHostToDevice);
-    if (S) cudaMemcpy(r->d_fine_r64, r->fine_r64.data(), 8 * S, cudaMemcpyHostToDevice);
-    if (!r->limits.empty())
-        cudaMemcpy(r->d_limits, r->limits.data(), 8 * r->limits.size(), cudaMemcpyHostToDevice);
-    if (cudaGetLastError() != cudaSuccess) {
+    const std::pair<void*, std::pair<const void*, size_t>> copies[3] = {
+        {r->d_words, {w.data(), 4 * w.size()}},
+        {r->d_fine_r64, {r->fine_r64.data(), 8 * (size_t)S}},
+        {r->d_limits, {r->limits.data(), 8 * r->limits.size()}}};
+    if (upload_sync(device, copies, 3) != cudaSuccess) {
         prrtc_robot_destroy(r);
         return set_err(PRRTC_ECUDA, "prrtc_robot_create: upload failed");
     }
@@ -530,30 +598,40 @@ static void finish_scene_words(prrtc_scene* s, double robot_reach) {
     s->words[SH_CPAD] = fbits(4.0f * eps + 1e-8f);
 }
 
-static int upload_scene(prrtc_scene* s) {
+// Uploads a built scene (words, f64 and counts already in `s`). With
+// `prev_words`/`prev_f64` (prrtc_scene_update) the existing device buffers are
+// rewritten in place when they are large enough, once every launch that read
+// the scene has finished (its completion markers, not the whole device);
+// otherwise new buffers are allocated, filled, and the old ones freed after
+// those launches. Returns with the data on the device (the copies are waited
+// for). On failure the previous device buffers stay as they were.
+static int upload_scene(prrtc_scene* s, const prrtc_scene* prev) {
     cudaSetDevice(s->device);
     const size_t nf = std::max<size_t>(1, s->f64.size());
-    if (s->d_words && s->words.size() <= s->cap_words && nf <= s->cap_f64) {
-        // dynamic obstacles (prrtc_scene_update): rewrite in place once no
-        // launch on the device can still read the scene (a single-problem
-        // call returns when its result is published, possibly before the
-        // grid has retired)
-        if (cudaDeviceSynchronize() != cudaSuccess) return set_err(PRRTC_ECUDA, "scene: device sync failed");
-    } else {
-        cudaFree(s->d_words);  // (implicitly waits for running launches)
-        cudaFree(s->d_f64);
-        s->d_words = nullptr;
-        s->d_f64 = nullptr;
-        s->cap_words = s->cap_f64 = 0;
-        if (cudaMalloc(&s->d_words, 4 * s->words.size()) != cudaSuccess ||
-            cudaMalloc(&s->d_f64, 8 * nf) != cudaSuccess)
+    const bool in_place = prev && prev->d_words && s->words.size() <= prev->cap_words && nf <= prev->cap_f64;
+    if (prev && prev->wait_unused() != cudaSuccess) return set_err(PRRTC_ECUDA, "scene: waiting for running plans failed");
+    uint32_t* dw = in_place ? prev->d_words : nullptr;
+    double* df = in_place ? prev->d_f64 : nullptr;
+    if (!in_place) {
+        if (cudaMalloc(&dw, 4 * s->words.size()) != cudaSuccess) return set_err(PRRTC_ENOMEM, "scene: device allocation failed");
+        if (cudaMalloc(&df, 8 * nf) != cudaSuccess) {
+            cudaFree(dw);
             return set_err(PRRTC_ENOMEM, "scene: device allocation failed");
-        s->cap_words = s->words.size();
-        s->cap_f64 = nf;
+        }
     }
-    cudaMemcpy(s->d_words, s->words.data(), 4 * s->words.size(), cudaMemcpyHostToDevice);
-    if (!s->f64.empty()) cudaMemcpy(s->d_f64, s->f64.data(), 8 * s->f64.size(), cudaMemcpyHostToDevice);
-    if (cudaGetLastError() != cudaSuccess) return set_err(PRRTC_ECUDA, "scene: upload failed");
+    const std::pair<void*, std::pair<const void*, size_t>> copies[2] = {
+        {dw, {s->words.data(), 4 * s->words.size()}}, {df, {s->f64.data(), 8 * s->f64.size()}}};
+    if (upload_sync(s->device, copies, 2) != cudaSuccess) {
+        if (!in_place) {
+            cudaFree(dw);
+            cudaFree(df);
+        }
+        return set_err(PRRTC_ECUDA, "scene: upload failed");
+    }
+    s->d_words = dw;
+    s->d_f64 = df;
+    s->cap_words = in_place ? prev->cap_words : s->words.size();
+    s->cap_f64 = in_place ? prev->cap_f64 : nf;
     return PRRTC_OK;
 }
 
@@ -572,7 +650,7 @@ int prrtc_scene_create(const prrtc_scene_desc* d, int device, prrtc_scene** out)
         return rc;
     }
     finish_scene_words(s, kDefaultReach);
-    rc = upload_scene(s);
+    rc = upload_scene(s, nullptr);
     if (rc) {
         prrtc_scene_destroy(s);
         return rc;
@@ -583,10 +661,18 @@ int prrtc_scene_create(const prrtc_scene_desc* d, int device, prrtc_scene** out)
 
 int prrtc_scene_update(prrtc_scene* s, const prrtc_scene_desc* d) {
     if (!s || !d) return set_err(PRRTC_EINVAL, "prrtc_scene_update: null argument");
+    // build and upload into a temporary; the handle changes only on success
     prrtc_scene tmp;
     tmp.device = s->device;
     int rc = build_scene(d, &tmp);
     if (rc) return rc;
+    finish_scene_words(&tmp, kDefaultReach);
+    rc = upload_scene(&tmp, s);
+    if (rc) return rc;
+    if (tmp.d_words != s->d_words) {  // reallocated: the old buffers are no longer read (upload_scene waited)
+        cudaFree(s->d_words);
+        cudaFree(s->d_f64);
+    }
     s->words.swap(tmp.words);
     s->f64.swap(tmp.f64);
     s->ns = tmp.ns;
@@ -594,13 +680,20 @@ int prrtc_scene_update(prrtc_scene* s, const prrtc_scene_desc* d) {
     s->nc = tmp.nc;
     s->ny = tmp.ny;
     s->extent = tmp.extent;
-    finish_scene_words(s, kDefaultReach);
-    return upload_scene(s);
+    s->d_words = tmp.d_words;
+    s->d_f64 = tmp.d_f64;
+    s->cap_words = tmp.cap_words;
+    s->cap_f64 = tmp.cap_f64;
+    tmp.d_words = nullptr;
+    tmp.d_f64 = nullptr;
+    s->generation.fetch_add(1, std::memory_order_release);
+    return PRRTC_OK;
 }
 
 int prrtc_scene_destroy(prrtc_scene* s) {
     if (!s) return PRRTC_OK;
     cudaSetDevice(s->device);
+    s->wait_unused();  // a launch that reads the scene may still be running
     cudaFree(s->d_words);
     cudaFree(s->d_f64);
     delete s;
@@ -653,6 +746,7 @@ struct Workspace {
     int* d_vprefix = nullptr;  // [n + 1] path-edge prefix (validate_path)
     cudaEvent_t ev0 = nullptr, ev1 = nullptr;
     cudaStream_t stream = nullptr;
+    UseMarkP mark;  // recorded after every launch (scenes it read wait on it before an update)
 
     static size_t in_bytes(size_t n, size_t dof) {
         return 8 * 2 * n * dof + sizeof(void*) * n + sizeof(SceneF64) * n + 4 * n + 64;
@@ -674,6 +768,7 @@ struct Workspace {
         if (ev0) cudaEventDestroy(ev0);
         if (ev1) cudaEventDestroy(ev1);
         if (stream) cudaStreamDestroy(stream);
+        UseMarkP m = std::move(mark);  // scenes may still hold it; the event dies with the last holder
         *this = Workspace();
     }
 
@@ -733,6 +828,9 @@ struct Workspace {
         cudaEventCreate(&ev0);
         cudaEventCreate(&ev1);
         cudaStreamCreateWithFlags(&stream, cudaStreamNonBlocking);
+        mark = std::make_shared<UseMark>();
+        mark->device = dev;
+        cudaEventCreateWithFlags(&mark->ev, cudaEventDisableTiming);
         n_cap = nn;
         dof_cap = nd;
         nodes_cap = nnodes;
@@ -776,6 +874,9 @@ struct prrtc_batch {
     long long* cta_trace = nullptr;  // PRRTC_TRACE only
     ProbCtl* d_ctl = nullptr;
     double* d_arena = nullptr;
+    // persistent batches: the bound scenes and their generations at staging
+    std::vector<const prrtc_scene*> scenes;
+    std::vector<uint64_t> scene_gen;
 };
 
 namespace {
@@ -896,10 +997,10 @@ int batch_bind(prrtc_batch* b, Workspace* ws, const prrtc_scene* const* scenes, 
     unsigned char* h = static_cast<unsigned char*>(ws->h_io);
     unsigned char* d = ws->d_in;
     size_t o = 0;
-    std::memcpy(h + o, starts, 8 * n * dof);
+    if (starts) std::memcpy(h + o, starts, 8 * n * dof);  // (null: re-staging, inputs already in h_io)
     b->d_starts = reinterpret_cast<double*>(d + o);
     o += 8 * n * dof;
-    std::memcpy(h + o, goals, 8 * n * dof);
+    if (goals) std::memcpy(h + o, goals, 8 * n * dof);
     b->d_goals = reinterpret_cast<double*>(d + o);
     o += 8 * n * dof;
     auto** sw = reinterpret_cast<const uint32_t**>(h + o);
@@ -911,11 +1012,15 @@ int batch_bind(prrtc_batch* b, Workspace* ws, const prrtc_scene* const* scenes, 
     auto* ps = reinterpret_cast<int*>(h + o);
     b->d_prob_scene = reinterpret_cast<int*>(d + o);
     o += 4 * n;
+    b->scenes.assign(scenes, scenes + n);
+    b->scene_gen.resize(n);
     for (size_t i = 0; i < n; ++i) {
+        b->scene_gen[i] = scenes[i]->generation.load(std::memory_order_acquire);
         const SceneArgs sa = scenes[i]->args();
         sw[i] = sa.words;
         sf[i] = sa.f64;
         ps[i] = (int)i;
+        scenes[i]->mark_use(ws->mark);
     }
     std::memset(h + out_offset(b), 0, Workspace::out_hdr(n));  // the zeroed controls ride the upload
     b->d_out = d + out_offset(b);
@@ -1022,6 +1127,7 @@ int batch_enqueue(prrtc_batch* b, cudaStream_t st, bool upload) {
     }
     if (b->params.validate_path)  // stream-ordered after the planner, outside its timing
         CUDA_TRY(launch_validate_paths(b->robot->args(), a, ws->d_vprefix, 4 * sm_count(b->device), st));
+    CUDA_TRY(cudaEventRecord(ws->mark->ev, st));  // the scenes' completion marker
     b->launches = 1;
     return PRRTC_OK;
 }
@@ -1033,6 +1139,7 @@ const char* message_for(int msg) {
         case 3: return "tree capacity exhausted";
         case 4: return "all workers exhausted their iteration budgets";
         case 5: return "path arena exhausted";
+        case 6: return "assemble_path: meeting configurations disagree";
         default: return "";
     }
 }
@@ -1205,6 +1312,17 @@ int fill_results(prrtc_batch* b, prrtc_result* out, const unsigned char* h, cons
             r.path = static_cast<double*>(std::malloc(sizeof(double) * b->dof * C.path_len));
             std::memcpy(r.path, arena + C.path_off, sizeof(double) * b->dof * C.path_len);
             r.cost = path_cost(r.path, r.path_len, b->dof);
+            // planner.cpp:144-148: no zero-length (bitwise-equal) segment
+            for (uint32_t k = 1; k < r.path_len; ++k)
+                if (std::memcmp(r.path + (size_t)(k - 1) * b->dof, r.path + (size_t)k * b->dof,
+                                sizeof(double) * b->dof) == 0) {
+                    prrtc_result_free(&r);
+                    r.status = PRRTC_FAILED;
+                    r.cost = 0.0;
+                    std::snprintf(r.message, sizeof(r.message),
+                                  "assemble_path: zero-length segment in assembled path");
+                    break;
+                }
         } else if (r.status == PRRTC_SOLVED) {
             r.status = PRRTC_FAILED;
             std::snprintf(r.message, sizeof(r.message), "path unavailable");
@@ -1251,6 +1369,24 @@ int prrtc_batch_create(const prrtc_robot* robot, const prrtc_scene* const* scene
 
 int prrtc_batch_launch(prrtc_batch* b, void* stream) {
     if (!b) return set_err(PRRTC_EINVAL, "prrtc_batch_launch: null batch");
+    // a scene updated since the batch staged it (prrtc_scene_update may have
+    // moved its buffers or changed its per-kind counts, i.e. the FP64 section
+    // offsets): re-stage the scene table before launching
+    bool stale = false;
+    for (size_t i = 0; i < b->scenes.size() && !stale; ++i)
+        stale = b->scenes[i]->generation.load(std::memory_order_acquire) != b->scene_gen[i];
+    if (stale) {
+        cudaSetDevice(b->device);
+        // the previous launch (if any) must not see the table change under it
+        if (b->last_stream && cudaStreamSynchronize(b->last_stream) != cudaSuccess)
+            return set_err(PRRTC_ECUDA, "prrtc_batch_launch: sync before re-staging failed");
+        const std::vector<const prrtc_scene*> sc = b->scenes;
+        int rc = batch_bind(b, &b->own, sc.data(), nullptr, nullptr);
+        if (rc) return rc;
+        if (cudaMemcpy(b->own.d_in, b->own.h_io, io_used(b), cudaMemcpyHostToDevice) != cudaSuccess ||
+            cudaDeviceSynchronize() != cudaSuccess)
+            return set_err(PRRTC_ECUDA, "prrtc_batch_launch: scene re-staging failed");
+    }
     return batch_enqueue(b, reinterpret_cast<cudaStream_t>(stream), false);
 }
 
@@ -1276,6 +1412,7 @@ namespace {
 // can return an edge whose collision lies between two of its 32 samples;
 // this mode never returns one.
 constexpr int kSoundRetries = 4;
+constexpr uint64_t kRetrySeedStride = 1ull << 28;
 int plan_batch_once(const prrtc_robot* robot, const prrtc_scene* const* scenes, uint32_t n_problems,
                     const double* starts, const double* goals, uint32_t dof, const prrtc_params* params,
                     prrtc_result* out);
@@ -1300,7 +1437,10 @@ int prrtc_plan_batch(const prrtc_robot* robot, const prrtc_scene* const* scenes,
             s.insert(s.end(), starts + (size_t)i * dof, starts + (size_t)(i + 1) * dof);
             g.insert(g.end(), goals + (size_t)i * dof, goals + (size_t)(i + 1) * dof);
         }
-        p.seed += 1;
+        // a different sample set per attempt: the seed offsets the Halton
+        // index (1 + seed + ticket), so +1 would replay the same sequence
+        // shifted by one sample; a 2^28 stride keeps indices below 2^32
+        p.seed += kRetrySeedStride;
         std::vector<prrtc_result> re(bad.size());
         rc = plan_batch_once(robot, sc.data(), (uint32_t)bad.size(), s.data(), g.data(), dof, &p, re.data());
         if (rc) return rc;

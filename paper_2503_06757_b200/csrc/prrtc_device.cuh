@@ -303,7 +303,13 @@ struct Ctx {
     // stats: per-thread slots [nthreads][2] in shared memory (sphere tests,
     // algorithmic FP32 flops), summed when a CTA leaves a problem
     unsigned long long* stat;
+    // the planner loop's thread-0 state (ticket block, iteration and CheckStats
+    // counters): kept in shared memory so it does not occupy registers
+    // (spilled around every call) in all threads of the CTA
+    unsigned long long* t0;
 };
+
+enum : int { T0_TKBASE = 0, T0_TKPOS, T0_TKCNT, T0_USED, T0_LITER, T0_FK, T0_FINE, T0_COUNT = 8 };
 
 // The planner keeps its Ctx in shared memory (plan_kernel): every field is
 // CTA-uniform, so reads are broadcast LDS instead of local-memory loads that
@@ -490,9 +496,10 @@ __device__ __noinline__ void fk_chunk(Ctx& c, int cnt) {
             }
             float n0, n1, n2, nt;
             if (inf.y < 0) {  // root: world = local
-                n0 = R[3 * r + 0];
-                n1 = R[3 * r + 1];
-                n2 = R[3 * r + 2];
+                // row r by selects (a runtime index into R would put it in local memory)
+                n0 = r == 0 ? R[0] : (r == 1 ? R[3] : R[6]);
+                n1 = r == 0 ? R[1] : (r == 1 ? R[4] : R[7]);
+                n2 = r == 0 ? R[2] : (r == 1 ? R[5] : R[8]);
                 nt = r == 0 ? t0 : (r == 1 ? t1 : t2);
             } else {
                 float a0 = w0, a1 = w1, a2 = w2, tp = wt;
@@ -1089,8 +1096,9 @@ __device__ __noinline__ NnOut nn_scan(Ctx& c, const double* cfg, long long cap, 
         for (int d0 = 0; d0 < dof; d0 += 8) {
             double2 v[8];
 #pragma unroll
-            for (int j = 0; j < 8; ++j)
-                if (d0 + j < dof) v[j] = *reinterpret_cast<const double2*>(cfg + (d0 + j) * cap + n0);
+            for (int j = 0; j < 8; ++j)  // every slot assigned: v stays in registers
+                v[j] = d0 + j < dof ? *reinterpret_cast<const double2*>(cfg + (d0 + j) * cap + n0)
+                                    : make_double2(0.0, 0.0);
 #pragma unroll
             for (int j = 0; j < 8; ++j) {
                 if (d0 + j < dof) {
@@ -1173,8 +1181,9 @@ __device__ __noinline__ void nn_scan_multi(Ctx& c, const double* cfg, long long 
             for (int d0 = 0; d0 < dof; d0 += 8) {
                 double2 v[8];
 #pragma unroll
-                for (int k = 0; k < 8; ++k)
-                    if (d0 + k < dof) v[k] = *reinterpret_cast<const double2*>(cfg + (d0 + k) * cap + n0);
+                for (int k = 0; k < 8; ++k)  // every slot assigned: v stays in registers
+                    v[k] = d0 + k < dof ? *reinterpret_cast<const double2*>(cfg + (d0 + k) * cap + n0)
+                                        : make_double2(0.0, 0.0);
 #pragma unroll
                 for (int k = 0; k < 8; ++k) {
                     if (d0 + k < dof) {

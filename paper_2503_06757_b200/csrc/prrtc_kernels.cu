@@ -30,7 +30,7 @@ using namespace dev;
 // ---------------------------------------------------------------------------
 struct SmemLayout {
     size_t robot, scene, pose, ccen, qf, sgroup, sbad, lmask, ictl, dcfg, red_d, red_i,
-        ends, ends_eq, ttab, sbuf, mnn, stat, htab, total;
+        ends, ends_eq, ttab, sbuf, mnn, stat, htab, t0, total;
 };
 
 __host__ __device__ inline size_t al16(size_t x) { return (x + 15) & ~size_t(15); }
@@ -59,6 +59,7 @@ __host__ __device__ inline SmemLayout smem_layout(int robot_words, int L, int do
     s.mnn = o;   o = al16(o + (8 + 4 + 4) * 32);
     s.stat = o;  o = al16(o + 16 * (size_t)nthreads);
     s.htab = o;  o = al16(o + 8 * (size_t)dof * (kHaltonTab + 2));  // + the [dof][2] limits
+    s.t0 = o;    o = al16(o + 8 * (size_t)T0_COUNT);
     s.total = o;
     return s;
 }
@@ -86,6 +87,7 @@ __device__ void setup_ctx(Ctx& c, unsigned char* smem, const uint32_t* robot_g, 
     // miss the L1 the tree protocol's acquires keep invalidating
     double* htab = reinterpret_cast<double*>(smem + lay.htab);
     for (int i = tid; i < (int)rw[RH_DOF] * (kHaltonTab + 2); i += nthreads) htab[i] = limits[i];
+    if (tid < T0_COUNT) reinterpret_cast<unsigned long long*>(smem + lay.t0)[tid] = 0;
     if (ctx_writer(c)) {
         c.nthreads = nthreads;
         c.L = rw[RH_NLINKS];
@@ -126,6 +128,7 @@ __device__ void setup_ctx(Ctx& c, unsigned char* smem, const uint32_t* robot_g, 
         c.mnn_i = reinterpret_cast<int*>(smem + lay.mnn + 8 * 32);
         c.mnn_ok = reinterpret_cast<int*>(smem + lay.mnn + 12 * 32);
         c.stat = stat;
+        c.t0 = reinterpret_cast<unsigned long long*>(smem + lay.t0);
         c.ttab_n = 0;
         c.nslog = 31 - __clz(NS);
         c.mflog = c.MF > 1 ? 32 - __clz(c.MF - 1) : 0;
@@ -318,8 +321,7 @@ __device__ int tree_append_many(Ctx& c, const PlanArgs& a, const TreeRef& T, con
 // ---------------------------------------------------------------------------
 __device__ long long validate_chain(Ctx& c, const PlanArgs& a, const double* A, const double* B,
                                     long long n_sub, const TreeRef* T, int parent0, int* last,
-                                    const int* done_flag, unsigned long long& fk_states,
-                                    unsigned long long& fine_states, bool* stopped) {
+                                    const int* done_flag, bool* stopped) {
     const int n_cc = a.p.n_cc;
     const long long total = n_sub * (long long)n_cc;
     long long good = 0;
@@ -335,7 +337,7 @@ __device__ long long validate_chain(Ctx& c, const PlanArgs& a, const double* A, 
             return 0;
         }
         if (threadIdx.x == 0) {
-            fk_states += act;
+            sh(c.t0)[T0_FK] += act;
             sh(c.stat)[1] += (unsigned long long)act * c.fkflops;  // thread 0's flop slot
         }
         trace_phase(a, 5);  // FK + collision
@@ -345,7 +347,7 @@ __device__ long long validate_chain(Ctx& c, const PlanArgs& a, const double* A, 
             *stopped = true;
             return 0;
         }
-        if (threadIdx.x == 0 && sh(c.ictl)[IC_QN]) ++fine_states;
+        if (threadIdx.x == 0 && sh(c.ictl)[IC_QN]) ++sh(c.t0)[T0_FINE];
         // (IC_FIRSTBAD is next reset inside the next chunk's FK, after the
         // state-generation barrier: every thread has read it by then)
         const int fb = sh(c.ictl)[IC_FIRSTBAD];
@@ -461,11 +463,23 @@ __device__ void assemble_path(Ctx& c, const PlanArgs& a, int prob, int meet_a, i
     }
     const int len = la + lb - 1;  // the meeting configuration once (planner.cpp:139-147)
     if (tid == 0) {
-        const unsigned long long need = (unsigned long long)len * dof;
-        const unsigned long long off = atomicAdd(a.arena_used, need);
-        sh(c.ictl)[IC_TMP4] = len;
-        if (off + need > a.arena_cap) sh(c.ictl)[IC_TMP4] = -1;
-        else a.ctl[prob].path_off = off;
+        // planner.cpp:127-129: the meeting configurations must agree (the
+        // reference throws logic_error; here the problem fails with that message)
+        double acc = 0.0;
+        for (int d = 0; d < dof; ++d) {
+            const double e = __dsub_rn(__ldcg(&Ta.cfg[(size_t)d * a.stride + meet_a]),
+                                       __ldcg(&Tb.cfg[(size_t)d * a.stride + meet_b]));
+            acc = __dadd_rn(acc, __dmul_rn(e, e));
+        }
+        if (__dsqrt_rn(acc) > 1e-12) {
+            sh(c.ictl)[IC_TMP4] = -2;
+        } else {
+            const unsigned long long need = (unsigned long long)len * dof;
+            const unsigned long long off = atomicAdd(a.arena_used, need);
+            sh(c.ictl)[IC_TMP4] = len;
+            if (off + need > a.arena_cap) sh(c.ictl)[IC_TMP4] = -1;
+            else a.ctl[prob].path_off = off;
+        }
     }
     __syncthreads();
     if (sh(c.ictl)[IC_TMP4] < 0) return;
@@ -491,7 +505,8 @@ enum : int {
     MSG_GOAL = 2,
     MSG_CAPACITY = 3,
     MSG_BUDGET = 4,
-    MSG_ARENA = 5
+    MSG_ARENA = 5,
+    MSG_MEET = 6
 };
 
 __device__ void finish_problem(const PlanArgs& a, int prob, int done, int msg) {
@@ -507,7 +522,7 @@ __device__ void finish_problem(const PlanArgs& a, int prob, int done, int msg) {
 
 // Initialise a freshly claimed problem: endpoint checks (planner.cpp:263-285)
 // and roots (planner.cpp:292-293). Returns true if the search should run.
-__device__ bool init_problem(Ctx& c, const PlanArgs& a, int prob, unsigned long long& fk_states) {
+__device__ bool init_problem(Ctx& c, const PlanArgs& a, int prob) {
     const int tid = threadIdx.x, dof = c.dof;
     ProbCtl& C = a.ctl[prob];
     double* S = dc(c, DC_A);
@@ -528,7 +543,7 @@ __device__ bool init_problem(Ctx& c, const PlanArgs& a, int prob, unsigned long 
     __syncthreads();
     check_chunk(c, 2, a.p.two_stage != 0, a.p.early_exit != 0, true);
     if (tid == 0) {
-        fk_states += 2;
+        sh(c.t0)[T0_FK] += 2;
         sh(c.stat)[1] += 2ull * c.fkflops;  // thread 0's flop slot
         // within_limits (planner.cpp:25-31): inclusive bounds
         bool sl = true, gl = true;
@@ -664,8 +679,7 @@ __device__ int pick_help(Ctx& c, const PlanArgs& a) {
 }
 
 // CheckStats counters (collision.hpp:17-25), reduced per warp then per CTA.
-__device__ void flush_stats(Ctx& c, ProbCtl& C, unsigned long long& fk_states,
-                            unsigned long long& fine_states) {
+__device__ void flush_stats(Ctx& c, ProbCtl& C) {
     unsigned long long* st = sh(c.stat) + 2 * threadIdx.x;
     unsigned long long tests = st[0], flops = st[1];
     st[0] = 0;
@@ -677,11 +691,12 @@ __device__ void flush_stats(Ctx& c, ProbCtl& C, unsigned long long& fk_states,
     if ((threadIdx.x & 31) == 0 && tests) atomicAdd(&C.sphere_tests, tests);
     if ((threadIdx.x & 31) == 0 && flops) atomicAdd(&C.flops, flops);
     if (threadIdx.x == 0) {
-        if (fk_states) atomicAdd(&C.fk_calls, fk_states);
-        if (fine_states) atomicAdd(&C.fine_entries, fine_states);
+        unsigned long long* t0 = sh(c.t0);
+        if (t0[T0_FK]) atomicAdd(&C.fk_calls, t0[T0_FK]);
+        if (t0[T0_FINE]) atomicAdd(&C.fine_entries, t0[T0_FINE]);
+        t0[T0_FK] = 0;
+        t0[T0_FINE] = 0;
     }
-    fk_states = 0;
-    fine_states = 0;
 }
 
 // Leaving a problem: the last worker out of an unsolved problem fails it
@@ -752,7 +767,6 @@ __global__ void __launch_bounds__(NT, MINB) plan_kernel(PlanArgs a) {
     }
 
     for (;;) {
-        unsigned long long fk_states = 0, fine_states = 0;
         int prob = -1;
         // unstarted problems first: claim, stage its scene, initialise
         for (;;) {
@@ -764,11 +778,11 @@ __global__ void __launch_bounds__(NT, MINB) plan_kernel(PlanArgs a) {
             const int si = a.prob_scene[p];
             load_scene(c, sbase, a.scene_words[si], a.scene_f64[si]);
             if (tid == 0) atomicAdd(&a.ctl[p].active, 1);
-            if (init_problem(c, a, p, fk_states)) {
+            if (init_problem(c, a, p)) {
                 prob = p;
                 break;
             }
-            flush_stats(c, a.ctl[p], fk_states, fine_states);
+            flush_stats(c, a.ctl[p]);
             if (tid == 0) atomicSub(&a.ctl[p].active, 1);
             __syncthreads();
         }
@@ -785,17 +799,23 @@ __global__ void __launch_bounds__(NT, MINB) plan_kernel(PlanArgs a) {
             sh(c.ictl)[IC_KNOWN1] = 1;
             sh(c.ictl)[IC_DIRTY] = 1;
         }
-        unsigned long long local_iter = 0;
         // Halton tickets are claimed in blocks of kblk (one atomic per block,
         // every ticket still used once, in order within the CTA); the block's
-        // samples are computed by all threads at once into sbuf
+        // samples are computed by all threads at once into sbuf. The ticket
+        // state and iteration counters are thread 0's, in shared memory (t0).
         const int kblk = 32;
-        unsigned long long tk_base = 0, tk_pos = 0, tk_cnt = 0, used = 0;  // thread 0's copy
+        if (tid == 0) {
+            unsigned long long* t0 = sh(c.t0);
+            t0[T0_TKBASE] = t0[T0_TKPOS] = t0[T0_TKCNT] = t0[T0_USED] = t0[T0_LITER] = 0;
+        }
         int leave_msg = MSG_NONE;
         for (;;) {
             // ---- iteration header (lead thread) ----
             TRACE_PHASE(1);
             if (tid == 0) {
+                unsigned long long* t0 = sh(c.t0);
+                unsigned long long tk_base = t0[T0_TKBASE], tk_pos = t0[T0_TKPOS], tk_cnt = t0[T0_TKCNT];
+                const unsigned long long local_iter = t0[T0_LITER];
                 // the done flag and both published counts are read back to
                 // back (relaxed done, acquire counts)
                 const int dn = ld_relaxed(&C.done);
@@ -827,8 +847,8 @@ __global__ void __launch_bounds__(NT, MINB) plan_kernel(PlanArgs a) {
                 // extend_start_tree (planner.hpp:62-65)
                 const int from_start = a.p.balance ? (la <= lb) : ((local_iter & 1) == 0);
                 const int snap = from_start ? la : lb;
-                ++local_iter;
-                used += leave == 0;
+                t0[T0_LITER] = local_iter + 1;
+                t0[T0_USED] += leave == 0;
                 sh(c.ictl)[IC_TMP0] = leave;
                 sh(c.ictl)[IC_TMP1] = from_start;
                 sh(c.ictl)[IC_TMP2] = snap;
@@ -839,6 +859,9 @@ __global__ void __launch_bounds__(NT, MINB) plan_kernel(PlanArgs a) {
                 sh(c.ictl)[IC_TMP5] = (int)(it < a.p.budget ? min(rem, a.p.budget - it) : 1ull);
                 sh(c.ictl)[IC_TMP4] = (int)tk_pos++;
                 reinterpret_cast<unsigned long long*>(sh(c.red_d))[0] = tk_base;
+                t0[T0_TKBASE] = tk_base;
+                t0[T0_TKPOS] = tk_pos;
+                t0[T0_TKCNT] = tk_cnt;
             }
             __syncthreads();
             const int leave = sh(c.ictl)[IC_TMP0];
@@ -886,9 +909,10 @@ __global__ void __launch_bounds__(NT, MINB) plan_kernel(PlanArgs a) {
             const int first = okm ? __ffs(okm) - 1 : m;
             if (tid == 0) {  // the rejected samples before `first` were iterations too
                 const int extra = (first < m ? first + 1 : m) - 1;
-                tk_pos += extra;
-                used += extra;
-                local_iter += extra;
+                unsigned long long* t0 = sh(c.t0);
+                t0[T0_TKPOS] += extra;
+                t0[T0_USED] += extra;
+                t0[T0_LITER] += extra;
             }
             if (first == m) continue;
             const double* smp = sh(c.sbuf) + (slot + first) * dof;
@@ -911,7 +935,7 @@ __global__ void __launch_bounds__(NT, MINB) plan_kernel(PlanArgs a) {
             // another one solved the problem leaves at the next chunk
             // instead of finishing the iteration — the result is settled)
             const long long ok = validate_chain(c, a, nnc, cnew, 1, &Ts, nn, &last, &C.done,
-                                                fk_states, fine_states, &stopped);
+                                                &stopped);
             if (stopped) continue;  // the header sees the done flag and leaves
             if (ok == 0) {
                 if (a.p.dynamic_domain && tid == 0) Ts.dd[nn] = 1;  // record_failure
@@ -957,7 +981,7 @@ __global__ void __launch_bounds__(NT, MINB) plan_kernel(PlanArgs a) {
                 }
                 __syncthreads();
                 const long long got = validate_chain(c, a, A, tgt, n_ext, &Ts, new_idx, &last,
-                                                     &C.done, fk_states, fine_states, &stopped);
+                                                     &C.done, &stopped);
                 if (got < 0) {
                     leave_msg = MSG_CAPACITY;
                     break;
@@ -980,7 +1004,7 @@ __global__ void __launch_bounds__(NT, MINB) plan_kernel(PlanArgs a) {
                 assemble_path(c, a, prob, meet_a, meet_b);
                 if (tid == 0) {
                     if (sh(c.ictl)[IC_TMP4] < 0) {
-                        finish_problem(a, prob, DONE_FAILED, MSG_ARENA);
+                        finish_problem(a, prob, DONE_FAILED, sh(c.ictl)[IC_TMP4] == -2 ? MSG_MEET : MSG_ARENA);
                     } else {
                         C.path_len = sh(c.ictl)[IC_TMP4];
                         __threadfence();
@@ -992,9 +1016,9 @@ __global__ void __launch_bounds__(NT, MINB) plan_kernel(PlanArgs a) {
         }
         // ---- leave ----
         TRACE_PHASE(10);
-        if (tid == 0 && used) atomicAdd(&C.iters_used, used);
+        if (tid == 0 && sh(c.t0)[T0_USED]) atomicAdd(&C.iters_used, sh(c.t0)[T0_USED]);
         if (tid == 0 && a.cta_trace) g_trace[0] = globaltimer();
-        flush_stats(c, C, fk_states, fine_states);
+        flush_stats(c, C);
         if (tid == 0) leave_problem(a, prob, leave_msg);
         __syncthreads();
         if (tid == 0 && a.cta_trace) g_trace[1] = globaltimer();
@@ -1461,13 +1485,27 @@ double measure_l2_gbs(int sms, cudaStream_t st) {
 
 static int chunk_states() { return 32; }
 
+// SM count of the current device (grids are sized from it, not hard-coded)
+static int cur_sms() {
+    static int cache[64] = {0};
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (dev < 0 || dev >= 64) return 148;
+    if (!cache[dev]) {
+        int n = 0;
+        cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+        cache[dev] = n > 0 ? n : 1;
+    }
+    return cache[dev];
+}
+
 cudaError_t launch_check_configs(const RobotArgs& r, const SceneArgs& s, const double* q, int n,
                                  int two_stage, uint8_t* out, cudaStream_t st) {
     const int NS = chunk_states();
     const size_t sm = smem_bytes(r, NS, 128);
     cudaError_t e = raise_smem_limit(reinterpret_cast<const void*>(check_configs_kernel), (int)sm);
     if (e != cudaSuccess) return e;
-    const int grid = (int)min((long long)(n + NS - 1) / NS, 148LL * 16);
+    const int grid = (int)min((long long)(n + NS - 1) / NS, (long long)cur_sms() * 16);
     if (grid > 0) check_configs_kernel<<<grid, 128, sm, st>>>(r, s, q, n, two_stage, out, NS);
     return cudaGetLastError();
 }
@@ -1480,7 +1518,7 @@ cudaError_t launch_validate_edges(const RobotArgs& r, const SceneArgs& s, const 
     const size_t sm = smem_bytes(r, NS, 128);
     cudaError_t e = raise_smem_limit(reinterpret_cast<const void*>(validate_edges_kernel), (int)sm);
     if (e != cudaSuccess) return e;
-    const int grid = (int)min((long long)n_edges, 148LL * 16);
+    const int grid = (int)min((long long)n_edges, (long long)cur_sms() * 16);
     if (grid > 0)
         validate_edges_kernel<<<grid, 128, sm, st>>>(r, s, from, to, n_edges, n_cc, two_stage,
                                                      early_exit, out, NS, prof, counters);
@@ -1493,7 +1531,7 @@ cudaError_t launch_debug_fk(const RobotArgs& r, const double* q, int n, float* f
     const size_t sm = smem_bytes(r, NS, 128);
     cudaError_t e = raise_smem_limit(reinterpret_cast<const void*>(debug_fk_kernel), (int)sm);
     if (e != cudaSuccess) return e;
-    const int grid = (int)min((long long)(n + NS - 1) / NS, 148LL * 16);
+    const int grid = (int)min((long long)(n + NS - 1) / NS, (long long)cur_sms() * 16);
     if (grid > 0) debug_fk_kernel<<<grid, 128, sm, st>>>(r, q, n, fine_out, coarse_out, NS);
     return cudaGetLastError();
 }
@@ -1501,21 +1539,21 @@ cudaError_t launch_debug_fk(const RobotArgs& r, const double* q, int n, float* f
 cudaError_t launch_debug_hits(const SceneArgs& s, const float* centers, const double* radii,
                               int n, int n_prims, uint8_t* hits, cudaStream_t st) {
     const long long items = (long long)n * n_prims;
-    const int grid = (int)min((items + 127) / 128, 148LL * 8);
+    const int grid = (int)min((items + 127) / 128, (long long)cur_sms() * 8);
     if (grid > 0) debug_hits_kernel<<<grid, 128, 0, st>>>(s, centers, radii, n, n_prims, hits);
     return cudaGetLastError();
 }
 
 cudaError_t launch_debug_nn(const double* soa, long long cap, int count, int dof, const double* q,
                             int nq, uint32_t* idx, double* d2, cudaStream_t st) {
-    const int grid = min(nq, 148 * 8);
+    const int grid = min(nq, cur_sms() * 8);
     if (grid > 0) debug_nn_kernel<<<grid, 128, 8 * kMaxDof, st>>>(soa, cap, count, dof, q, nq, idx, d2);
     return cudaGetLastError();
 }
 
 cudaError_t launch_debug_nn_multi(const double* soa, long long cap, int count, int dof, const double* q,
                                   int nq, int group, uint32_t* idx, double* d2, cudaStream_t st) {
-    const int grid = min((nq + group - 1) / group, 148 * 8);
+    const int grid = min((nq + group - 1) / group, cur_sms() * 8);
     if (grid > 0)
         debug_nn_multi_kernel<<<grid, 128, 8 * 32 * kMaxDof + 8 * 32 + 4 * 32, st>>>(soa, cap, count, dof, q, nq,
                                                                                        group, idx, d2);
