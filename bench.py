@@ -44,33 +44,33 @@ METRIC = "median/p95 ms-to-first-solution per problem; problems/sec at 1/2/4/8 B
 UNIT = "problems/s"
 
 
-def load_workload(robot: str, n: int):
+def load_workload(robot: str, n: int, set_k: int = 0):
     """The first n problems of the robot's 1000-problem set (all of it for
     n >= 1000); a smaller n takes an evenly spread subset, so every scene
     kind (the set is ordered table_pick / bookshelf / cage) stays represented."""
     from paper_2503_06757_b200 import robots
     from paper_2503_06757_b200.scenes import make_scene
-    d = np.load(ROOT / "tests" / "golden" / f"problems_{robot}.npz")
+    d = np.load(ROOT / "tests" / "golden" / (f"problems_{robot}_s{set_k}.npz" if set_k else f"problems_{robot}.npz"))
     N = len(d["pid"])
     idx = np.arange(N) if n >= N else np.unique(np.linspace(0, N - 1, n).round().astype(int))
     scenes = [make_scene(robot, str(d["kind"][i]), int(d["pid"][i]))[0] for i in idx]
     return robots.get(robot), scenes, d["start"][idx].copy(), d["goal"][idx].copy(), d["kind"][idx]
 
 
-def workload_config(robot, n, params, extra=None):
-    cfg = {
+def workload_config(robot, n, params, world):
+    """The workload description, identical on both arms (same keys, same values)."""
+    return {
         "workload": f"{robot}_mbm_{n}",
         "robot": robot,
         "problems_per_gpu": n,
         "scenes": "table_pick/bookshelf/cage 334/333/333 (synthetic MBM-shaped, tests/golden)",
-        "params": {"delta": params.delta, "n_cc": params.n_cc, "tree_capacity": params.tree_capacity,
-                   "max_iters_per_worker": params.max_iters_per_worker, "dynamic_domain": True,
-                   "two_stage": True, "early_exit": True, "sampler": "halton"},
+        "params": {"delta": params.delta, "n_cc": params.n_cc, "workers": params.workers,
+                   "max_iters_per_worker": params.max_iters_per_worker, "tree_capacity": params.tree_capacity,
+                   "dynamic_domain": True, "dd_radius": params.resolved_dd_radius(), "two_stage": True,
+                   "early_exit": True, "sampler": "halton"},
         "l2": "flushed between timed steps (256 MiB write)",
+        "parallelism": f"dp{world} (independent problems per GPU, no collective)",
     }
-    if extra:
-        cfg.update(extra)
-    return cfg
 
 
 class ClockSampler:
@@ -120,12 +120,15 @@ class ClockSampler:
 
 
 def dist_setup():
+    """One process per GPU; the process group (gloo, host memory) carries only
+    the timing barrier and the max / sum of per-rank numbers — nothing on the
+    planning path needs a collective (north_star: no NCCL)."""
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
     if world > 1:
         import torch.distributed as dist
-        dist.init_process_group("nccl" if os.environ.get("PRRTC_BENCH_BACKEND", "nccl") == "nccl" else "gloo")
+        dist.init_process_group("gloo")
     return world, rank, local
 
 
@@ -134,8 +137,7 @@ def dist_max(x: float, world: int) -> float:
         return x
     import torch
     import torch.distributed as dist
-    dev = "cuda" if dist.get_backend() == "nccl" else "cpu"
-    t = torch.tensor([x], dtype=torch.float64, device=dev)
+    t = torch.tensor([x], dtype=torch.float64)
     dist.all_reduce(t, op=dist.ReduceOp.MAX)
     return float(t.item())
 
@@ -145,8 +147,7 @@ def dist_sum(x: float, world: int) -> float:
         return x
     import torch
     import torch.distributed as dist
-    dev = "cuda" if dist.get_backend() == "nccl" else "cpu"
-    t = torch.tensor([x], dtype=torch.float64, device=dev)
+    t = torch.tensor([x], dtype=torch.float64)
     dist.all_reduce(t, op=dist.ReduceOp.SUM)
     return float(t.item())
 
@@ -325,7 +326,7 @@ def parity_block(robot_names, workers_list, n, device=0, tree_capacity=200000, t
         rr = {"problems": len(S)}
         for W in workers_list:
             params = robot_params(robot, PlannerParams(workers=W, tree_capacity=tree_capacity))
-            planner.plan_batch_arrays(model, dsc, S[:8], G[:8], params, device=device)  # workspace warm-up
+            planner.plan_batch_arrays(model, dsc.hs[:8], S[:8], G[:8], params, device=device)  # workspace warm-up
             t0 = time.perf_counter()
             br = planner.plan_batch_arrays(model, dsc, S, G, params, device=device)
             g_ms = (time.perf_counter() - t0) * 1e3
@@ -431,55 +432,205 @@ def mixed_sharded(dev, world, rank, total=10000):
             "timing": "host wall clock, barrier -> three concurrent stream launches + sync, max over ranks"}
 
 
-def run_reference(args):
-    # the CPU reference arm needs no process group: rank 0 runs, the others exit
-    rank = int(os.environ.get("RANK", "0"))
+HEADLINE_WORKERS = 1  # workers per problem on BOTH arms (identical PlannerParams)
+
+
+def headline_params(**kw):
+    """The headline's PlannerParams, identical on both arms: the reference
+    defaults (planner.hpp:21-40) with workers = 1 (per-problem iteration budget
+    max_iters_per_worker x 1 = 2000, planner.cpp:199) and tree_capacity 200000."""
     from paper_2503_06757_b200.model import PlannerParams
+    return PlannerParams(workers=HEADLINE_WORKERS, **kw)
+
+
+def problem_set(robot: str, rank: int, n: int):
+    """Rank r's problems: set 0 = tests/golden/problems_<robot>.npz, set r >= 1 =
+    problems_<robot>_s<r>.npz (disjoint problem ids, same scene-kind mix), so
+    the weak-scaling job solves distinct problems on every GPU. Falls back to
+    set 0 (noted in the config) when a set is not generated."""
+    if rank > 0 and (ROOT / "tests" / "golden" / f"problems_{robot}_s{rank}.npz").exists():
+        return load_workload(robot, n, set_k=rank), f"set {rank}"
+    return load_workload(robot, n), "set 0" + (" (replica: no distinct set generated)" if rank else "")
+
+
+def lscpu_model() -> str:
+    try:
+        out = subprocess.run(["lscpu"], capture_output=True, text=True, timeout=10).stdout
+        for line in out.splitlines():
+            if line.lower().startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except Exception:
+        pass
+    return "unknown"
+
+
+def _lat(vals):
+    v = [x for x in vals if x is not None]
+    return {"median": float(np.median(v)) if v else None, "p95": float(np.percentile(v, 95)) if v else None,
+            "n": len(v)}
+
+
+def cpu_baseline_block(model, scenes, S, G, kinds, gpu_single=None):
+    """SURVEY.md §8(d) / BASELINE.md §3 CPU-baseline protocol on the box's host
+    cores, reference = oracle/_ref (the unmodified reference sources):
+    throughput (nproc threads, workers = 1 per problem) at tree_capacity 200000
+    (the default; its allocation is inside the reference's timer,
+    planner.cpp:254,290-291) and at the right-sized 20000; single-problem
+    latency (the reference's own wall_time_ms, one problem at a time) at
+    workers = 1 and workers = nproc on a 200-problem spread sample at both
+    capacities; BASELINE config 1 (one Panda table_pick problem, seed 0)."""
+    from oracle import Oracle, available
+    from paper_2503_06757_b200.model import PlannerParams, PlanStatus
+    threads = os.cpu_count() or 1
+    o = Oracle("ref" if available("ref") else "port")
+    n = len(S)
+    out = {"kind": "reference" if o.kind == "ref" else "port", "cores": threads, "cpu_model": lscpu_model()}
+    for cap in (200000, 20000):
+        p = PlannerParams(workers=1, tree_capacity=cap)
+        res, ms = o.plan_many(model, scenes, S, G, p, threads=threads)
+        ok = [r.status == PlanStatus.Solved for r in res]
+        out[f"throughput_cap{cap}"] = {
+            "problems_per_s": n / (ms / 1e3), "success": float(np.mean(ok)),
+            "cost_mean": float(np.mean([r.cost for r in res if r.status == PlanStatus.Solved])),
+            "sample": f"all {n} problems, workers=1 per problem, {threads} problems in parallel"}
+    sub = np.unique(np.linspace(0, n - 1, min(n, 200)).round().astype(int))
+    for W in (1, threads):
+        for cap in (200000, 20000):
+            p = PlannerParams(workers=W, tree_capacity=cap)
+            res, _ = o.plan_many(model, [scenes[i] for i in sub], S[sub], G[sub], p, threads=1)
+            ok = [r.status == PlanStatus.Solved for r in res]
+            out[f"latency_w{W}_cap{cap}"] = {
+                **_lat([r.wall_time_ms for r in res if r.status == PlanStatus.Solved]),
+                "success": float(np.mean(ok)),
+                "cost_mean": float(np.mean([r.cost for r in res if r.status == PlanStatus.Solved])),
+                "sample": f"{len(sub)} problems spread over the set, one at a time, reference wall_time_ms"}
+    # BASELINE config 1: Panda table_pick, seed 0 (problem 0 of the set), 20 trials per arm
+    i0 = int(np.where(kinds == "table_pick")[0][0])
+    c1 = {"problem": f"{kinds[i0]} index {i0}", "seed": 0}
+    for W in (1, threads):
+        p = PlannerParams(workers=W)
+        rs = [o.plan(model, scenes[i0], S[i0], G[i0], p) for _ in range(20)]
+        c1[f"reference_w{W}"] = {**_lat([r.wall_time_ms for r in rs if r.status == PlanStatus.Solved]),
+                                 "success": float(np.mean([r.status == PlanStatus.Solved for r in rs])),
+                                 "cost_mean": float(np.mean([r.cost for r in rs if r.status == PlanStatus.Solved]))
+                                 if any(r.status == PlanStatus.Solved for r in rs) else None}
+    if gpu_single is not None:
+        c1.update(gpu_single(i0))
+    out["config1"] = c1
+    return out
+
+
+def run_reference(args):
+    """--impl reference: the reference's own CPU planner (oracle/_ref) on the
+    host cores, on the headline's workload, metric and PlannerParams. Under
+    torchrun only rank 0 runs; the others exit without work."""
+    rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return 0
+    from paper_2503_06757_b200.model import PlanStatus
     model, scenes, S, G, kinds = load_workload(args.robot, args.problems)
-    params = PlannerParams(workers=1)
+    params = headline_params()
     threads = os.cpu_count() or 1
     for _ in range(args.warmup):
         cpu_reference(model, scenes[:64], S[:64], G[:64], params, threads)
-    times, solved, lat = [], [], []
+    times, solved, lat, cost = [], [], [], []
     kind = None
     for _ in range(args.steps):
         o, kind, res, ms = cpu_reference(model, scenes, S, G, params, threads)
         times.append(ms)
-        solved.append(np.mean([r.status == 0 for r in res]))
-        lat += [r.wall_time_ms for r in res if r.status == 0]
+        solved.append(np.mean([r.status == PlanStatus.Solved for r in res]))
+        lat += [r.wall_time_ms for r in res if r.status == PlanStatus.Solved]
+        cost += [r.cost for r in res if r.status == PlanStatus.Solved]
     ms = statistics.median(times)
     value = len(S) / (ms / 1e3)
+    # the right-sized tree capacity (the reference allocates its trees inside plan())
+    r20, ms20 = o.plan_many(model, scenes, S, G, headline_params(tree_capacity=20000), threads=threads)
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": workload_config(args.robot, len(S), params, {"host_threads": threads, "workers_per_problem": 1}),
-        "success_rate": float(np.mean(solved)),
-        "latency_ms": {"median": float(np.median(lat)) if lat else None,
-                       "p95": float(np.percentile(lat, 95)) if lat else None, "threads_per_problem": 1},
+        "config": workload_config(args.robot, len(S), params, args.gpus),
+        "success_rate": float(np.mean(solved)), "mean_cost": float(np.mean(cost)),
+        "host_threads": threads, "cpu_model": lscpu_model(),
+        "tree_capacity_20000": {"problems_per_s": len(S) / (ms20 / 1e3),
+                                "success_rate": float(np.mean([r.status == PlanStatus.Solved for r in r20]))},
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": kind,
                          "sample": f"all {len(S)} problems x {args.steps} steps, workers=1 per problem, "
-                                   f"{threads} host threads"},
+                                   f"{threads} problems in parallel"},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "latency_ms": {**_lat(lat), "note": "reference wall_time_ms of each problem inside the "
+                                            f"{threads}-thread throughput run (workers=1)"},
     }
     print(json.dumps(line))
     return 0
 
 
+def table_one(dev, robot, params_fn, n_lat, peak):
+    """Table-I figures of one robot (statistics as
+    bench.cpp:90-109): single-problem prrtc_plan latency at the device's
+    default worker count (one 256-thread CTA per SM) on a spread sample, its
+    success and cost, and the FP32 roofline fraction of plan_kernel over those
+    launches (algorithmic flops / device time); plus the 1000-problem batch at
+    the headline params (problems/s, success)."""
+    import torch
+    from paper_2503_06757_b200 import planner, suite
+    from paper_2503_06757_b200.model import PlannerParams, PlanStatus
+    model, scenes, S, G, kinds = load_workload(robot, 1000)
+    out = {"dof": model.dof}
+    bp = params_fn(robot, headline_params())
+    b = planner.Batch(model, scenes, S, G, bp, device=dev)
+    b.launch()
+    b.results()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    ms = []
+    for _ in range(3):
+        e0.record()
+        b.launch(torch.cuda.current_stream().cuda_stream)
+        e1.record()
+        torch.cuda.synchronize()
+        ms.append(e0.elapsed_time(e1))
+    res = b.results()
+    fl = float(sum(r.flops for r in res))
+    out["batch"] = {"problems_per_s": len(S) / (statistics.median(ms) / 1e3),
+                    "success_rate": float(np.mean([r.status == PlanStatus.Solved for r in res])),
+                    "fp32_frac": fl / (statistics.median(ms) * 1e-3) / 1e12 / peak if peak else None,
+                    "params": f"workers={bp.workers}, dd_radius={bp.resolved_dd_radius()}"}
+    del b
+    sp = params_fn(robot, PlannerParams())  # workers = 0: one CTA per SM
+    idx = np.unique(np.linspace(0, len(S) - 1, n_lat).round().astype(int))
+    for i in idx[:3]:
+        planner.plan(model, scenes[i], S[i], G[i], sp, device=dev)
+    rs = [planner.plan(model, scenes[i], S[i], G[i], sp, device=dev) for i in idx]
+    ok = [r for r in rs if r.status == PlanStatus.Solved]
+    q = suite.summarize_values([r.wall_time_ms for r in ok])
+    dsum = sum(r.device_time_ms for r in rs)
+    out["single"] = {"median_ms": q.median, "p95_ms": q.p95, "mean_ms": q.mean,
+                     "device_median_ms": float(np.median([r.device_time_ms for r in ok])) if ok else None,
+                     "success_rate": len(ok) / len(rs), "cost_mean": float(np.mean([r.cost for r in ok])) if ok else None,
+                     "fp32_frac": (sum(r.flops for r in rs) / (dsum * 1e-3) / 1e12 / peak) if dsum and peak else None,
+                     "samples": len(rs), "workers": planner.default_workers(dev),
+                     "params": f"workers=0 (budget {planner.default_workers(dev)} x 2000), "
+                               f"dd_radius={sp.resolved_dd_radius()}"}
+    if robot == "baxter":  # also at the reference's default dynamic-domain radius (4 delta)
+        from paper_2503_06757_b200.model import PlannerParams as PP
+        b = planner.plan_batch_arrays(model, planner.device_scenes(scenes, dev), S, G, headline_params(), device=dev)
+        out["batch_reference_dd"] = {"success_rate": float(np.mean(b.status == PlanStatus.Solved)),
+                                     "dd_radius": PP().resolved_dd_radius()}
+    return out
+
+
 def run_b200(args):
     import torch
-    torch.cuda.set_device(int(os.environ.get("LOCAL_RANK", "0")))  # before NCCL init: one GPU per rank
+    torch.cuda.set_device(int(os.environ.get("LOCAL_RANK", "0")))
     world, rank, local = dist_setup()
     from paper_2503_06757_b200 import _lib, planner
     from paper_2503_06757_b200.model import PlannerParams, PlanStatus
     from paper_2503_06757_b200.planner import Batch
 
     dev = local
-    model, scenes, S, G, kinds = load_workload(args.robot, args.problems)
+    (model, scenes, S, G, kinds), set_name = problem_set(args.robot, rank, args.problems)
     n = len(S)
-    params = PlannerParams()
+    params = headline_params()
     batch = Batch(model, scenes, S, G, params, device=dev)
     stream = torch.cuda.Stream(device=dev)
     flush = torch.empty(64 * 1024 * 1024, dtype=torch.float32, device=f"cuda:{dev}")
@@ -487,10 +638,9 @@ def run_b200(args):
         for _ in range(max(3, args.warmup)):
             batch.launch(stream.cuda_stream)
         stream.synchronize()
-    warm_res = batch.results()
+    batch.results()
     # ---- timed region: K steps, L2 flushed between steps (untimed) ----
     ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
-    step_ms = []
     dist_barrier(world)
     torch.cuda.synchronize()
     with ClockSampler(dev) as clk:
@@ -505,9 +655,11 @@ def run_b200(args):
     step_ms = [a.elapsed_time(b) for a, b in ev]
     res = batch.results()  # last step's outcome (copied after the timed region)
     ms = dist_max(sum(step_ms) / len(step_ms), world)
-    value = world * n / (ms / 1e3)
+    total_n = dist_sum(float(n), world)  # problems of the whole job (every rank's own set)
+    value = total_n / (ms / 1e3)
     solved = [r.status == PlanStatus.Solved for r in res]
     flops = float(sum(r.flops for r in res))
+    del batch
 
     # ---- e2e through the host-buffer C-ABI (prrtc_plan_batch), every rank,
     # barrier + max over ranks (whole-job problems/s) ----
@@ -519,77 +671,114 @@ def run_b200(args):
         t0 = time.perf_counter()
         er = planner.plan_batch_arrays(model, dscenes, S, G, params, device=dev)
         e2e_ms.append(dist_max((time.perf_counter() - t0) * 1e3, world))
-    e2e_solved = dist_sum(float(np.sum(er.status == PlanStatus.Solved)), world) / (world * n)
+    e2e_solved = dist_sum(float(np.sum(er.status == PlanStatus.Solved)), world) / total_n
+    # sound mode (validate_path: every path re-checked on the device at 4 n_cc, failures re-planned)
+    sp = headline_params(validate_path=True)
+    planner.plan_batch_arrays(model, dscenes, S, G, sp, device=dev)
+    s_ms = []
+    for _ in range(3):
+        dist_barrier(world)
+        t0 = time.perf_counter()
+        sr = planner.plan_batch_arrays(model, dscenes, S, G, sp, device=dev)
+        s_ms.append(dist_max((time.perf_counter() - t0) * 1e3, world))
+    s_solved = dist_sum(float(np.sum(sr.status == PlanStatus.Solved)), world) / total_n
     mixed = None if args.no_extras else mixed_sharded(dev, world, rank)
 
-    line = None
     if rank == 0:
-        # ---- roofline of the dominant (only) kernel: plan_kernel ----
-        peak = _lib.load().prrtc_fp32_peak_tflops(dev)
+        lib = _lib.load()
+        peak = lib.prrtc_fp32_peak_tflops(dev)
         kernel_ms = statistics.median(step_ms)
         achieved = flops / (kernel_ms * 1e-3) / 1e12
         import ctypes
         h2d_c, d2h_c = ctypes.c_uint64(), ctypes.c_uint64()
-        _lib.check(_lib.load().prrtc_last_transfer_bytes(dev, ctypes.byref(h2d_c), ctypes.byref(d2h_c)))
-        h2d, d2h = h2d_c.value, d2h_c.value  # the library's own count of the last call's copies
-        # ---- single-problem latency (prrtc_plan, host wall clock) ----
-        idx = list(range(0, n, max(1, n // args.latency_samples)))[: args.latency_samples]
-        for i in idx[:5]:
-            planner.plan(model, scenes[i], S[i], G[i], params, device=dev)
-        lat, dlat, lst, lcost = [], [], [], []
-        for i in idx:
-            r = planner.plan(model, scenes[i], S[i], G[i], params, device=dev)
-            lst.append(r.status == PlanStatus.Solved)
-            if r.status == PlanStatus.Solved:
-                lat.append(r.wall_time_ms)
-                dlat.append(r.device_time_ms)
-                lcost.append(r.cost)
+        planner.plan_batch_arrays(model, dscenes, S, G, params, device=dev)  # the e2e call, for its byte count
+        _lib.check(lib.prrtc_last_transfer_bytes(dev, ctypes.byref(h2d_c), ctypes.byref(d2h_c)))
+        # ---- single-problem latency (prrtc_plan, host wall clock), per worker count ----
         from paper_2503_06757_b200 import suite
-        q = suite.summarize_values(lat)  # Table-I statistics (bench.cpp:90-109)
-        extras = {} if args.no_extras else bench_extras(dev, params)
+        idx = np.unique(np.linspace(0, n - 1, args.latency_samples).round().astype(int))
+        lat = {}
+        for W in (0, 16, 1):
+            lp = PlannerParams(workers=W)
+            for i in idx[:3]:
+                planner.plan(model, scenes[i], S[i], G[i], lp, device=dev)
+            rs = [planner.plan(model, scenes[i], S[i], G[i], lp, device=dev) for i in idx]
+            ok = [r for r in rs if r.status == PlanStatus.Solved]
+            q = suite.summarize_values([r.wall_time_ms for r in ok])  # Table-I statistics (bench.cpp:90-109)
+            dsum = sum(r.device_time_ms for r in rs)
+            lat[f"workers{W}"] = {
+                "median": q.median, "p95": q.p95, "mean": q.mean, "q1": q.q1, "q3": q.q3,
+                "device_median": float(np.median([r.device_time_ms for r in ok])) if ok else None,
+                "success_rate": len(ok) / len(rs), "cost_mean": float(np.mean([r.cost for r in ok])) if ok else None,
+                "fp32_frac": (sum(r.flops for r in rs) / (dsum * 1e-3) / 1e12 / peak) if dsum and peak else None,
+                "ctas": planner.default_workers(dev) if W == 0 else W, "samples": len(rs)}
+
+        def gpu_single(i0):
+            out = {}
+            for W in (1, 16, 0):
+                lp = PlannerParams(workers=W)
+                planner.plan(model, scenes[i0], S[i0], G[i0], lp, device=dev)
+                rs = [planner.plan(model, scenes[i0], S[i0], G[i0], lp, device=dev) for _ in range(20)]
+                out[f"b200_w{W}"] = {**_lat([r.wall_time_ms for r in rs if r.status == PlanStatus.Solved]),
+                                     "success": float(np.mean([r.status == PlanStatus.Solved for r in rs]))}
+            return out
+
+        extras = {}
+        if not args.no_extras:
+            extras["robots"] = {r: table_one(dev, r, robot_params, 100, peak) for r in ("panda", "fetch", "baxter")}
+            extras.update(bench_extras(dev, params))
         micro = microbench(model, scenes, S, G, dev, peak)
+        parity = None
+        if not args.no_parity:
+            parity = parity_block(["panda", "fetch", "baxter"], [1, 16], args.parity_problems, device=dev)
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": max(3, args.warmup), "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "f32+f64", "data": "synthetic",
-            "config": workload_config(args.robot, n, params, {"parallelism": f"dp{world} (independent problems per GPU)"}),
+            "config": workload_config(args.robot, n, params, world),
+            "problem_sets": f"rank r solves its own {n}-problem set ({world} sets, rank 0: {set_name})",
             "success_rate": float(np.mean(solved)),
-            "success_by_scene": {k: float(np.mean([s for s, kk in zip(solved, kinds) if kk == k]))
-                                 for k in ("table_pick", "bookshelf", "cage")},
             "mean_cost": float(np.mean([r.cost for r in res if r.status == PlanStatus.Solved])),
-            "latency_ms": {"median": q.median, "p95": q.p95, "mean": q.mean, "q1": q.q1, "q3": q.q3, "max": q.max,
-                           "device_median": float(np.median(dlat)), "samples": len(idx),
-                           "success_rate": float(np.mean(lst)), "mean_cost": float(np.mean(lcost)),
-                           "api": "prrtc_plan (host wall clock), params.workers = 0 (one 256-thread CTA per SM)"},
-            "e2e": {"value": world * n / (statistics.median(e2e_ms) / 1e3), "unit": UNIT, "h2d_bytes_per_step": int(h2d),
-                    "d2h_bytes_per_step": int(d2h), "success_rate": float(e2e_solved),
+            "e2e": {"value": total_n / (statistics.median(e2e_ms) / 1e3), "unit": UNIT,
+                    "h2d_bytes_per_step": int(h2d_c.value), "d2h_bytes_per_step": int(d2h_c.value),
+                    "success_rate": float(e2e_solved),
                     "api": "prrtc_plan_batch (host buffers), every rank, max over ranks"},
+            "sound_mode": {"problems_per_s_e2e": total_n / (statistics.median(s_ms) / 1e3),
+                           "success_rate": float(s_solved),
+                           "api": "prrtc_plan_batch, params.validate_path = 1 (every path re-checked on the "
+                                  "device at 4 n_cc, failures re-planned)"},
             "roofline": {"bound": "fp32", "kernel": "plan_kernel", "achieved": achieved, "peak": peak,
                          "unit": "TFLOP/s", "frac": achieved / peak if peak else None,
                          "peak_source": "measured FFMA-chain microbenchmark (prrtc_fp32_peak_tflops); "
                                         "MEASURED_PEAKS.json has no FP32 figure",
                          "algorithmic_flops_per_launch": flops, "traffic": traffic_from_profiles(),
-                         # the kernel is latency-bound: issue-slot and pipe utilisation
-                         # of the same launch from the committed ncu capture
                          "ncu": {k.replace("plan_kernel_", ""): v for k, v in ncu_summary().items()
                                  if k.startswith("plan_kernel_") and k != "plan_kernel_dram_bytes_per_launch"},
                          "ncu_source": ncu_summary().get("source")},
-            "microbench": micro,
             "gpu_launches": args.steps,
             "clocks": clk.summary(),
+            "microbench": micro,
             **extras,
         }
         if mixed is not None:
             line["mixed_10k"] = mixed
         if world == 1 and not args.no_cpu_baseline:
-            threads = os.cpu_count() or 1
-            _, kind, cres, cms = cpu_reference(model, scenes, S, G, PlannerParams(workers=1), threads)
-            line["cpu_baseline"] = {
-                "value": n / (cms / 1e3), "unit": UNIT, "cores": threads, "kind": kind,
-                "sample": f"all {n} problems once, reference plan() workers=1 per problem on {threads} host threads",
-                "success_rate": float(np.mean([r.status == 0 for r in cres])),
-                "latency_ms_median": float(np.median([r.wall_time_ms for r in cres if r.status == 0])),
-            }
+            cb = cpu_baseline_block(model, scenes, S, G, kinds, gpu_single)
+            t = cb["throughput_cap200000"]
+            line["cpu_baseline"] = {"value": t["problems_per_s"], "unit": UNIT, "cores": cb["cores"],
+                                    "kind": cb["kind"], "sample": t["sample"], **cb}
+        if parity is not None:
+            line["parity"] = parity
+            line["parity_summary"] = {
+                f"{r}_W{w}": {"success_b200": v[f"W{w}"]["b200"]["success"],
+                              "success_ref": v[f"W{w}"]["reference"]["success"],
+                              "success_b200_single": v[f"W{w}"].get("b200_single", {}).get("success"),
+                              "cost_med_b200": v[f"W{w}"]["b200"]["cost_median"],
+                              "cost_med_ref": v[f"W{w}"]["reference"]["cost_median"],
+                              "valid_ncc": [v[f"W{w}"]["b200"]["valid_ncc"], v[f"W{w}"]["reference"]["valid_ncc"]],
+                              "valid_4ncc": [v[f"W{w}"]["b200"]["valid_4ncc"], v[f"W{w}"]["reference"]["valid_4ncc"]]}
+                for r, v in parity["robots"].items() for w in (1, 16)}
+        line["latency_ms"] = {**lat["workers0"], "by_workers": lat,
+                              "api": "prrtc_plan, host wall clock; workers0 = one 256-thread CTA per SM"}
         print(json.dumps(line))
     if world > 1:
         import torch.distributed as dist
@@ -608,6 +797,8 @@ def main():
     ap.add_argument("--latency-samples", type=int, default=100)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-extras", action="store_true", help="skip the Fetch/Baxter/mixed/replanning extras")
+    ap.add_argument("--no-parity", action="store_true", help="skip the equal-budget parity block")
+    ap.add_argument("--parity-problems", type=int, default=1000)
     args = ap.parse_args()
     if args.impl == "reference":
         return run_reference(args)

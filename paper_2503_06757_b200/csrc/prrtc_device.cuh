@@ -431,7 +431,7 @@ __device__ __forceinline__ void sincos_joint(float q, float* sn, float* cs) {
     __sincosf(r, sn, cs);
 }
 
-__device__ __noinline__ void fk_chunk(Ctx& c, int cnt) {
+__device__ __forceinline__ void fk_chunk(Ctx& c, int cnt) {
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nw = c.nthreads >> 5;
     const int NS = c.NS, L = c.L;
     float* const pose = sh(c.pose);
@@ -708,7 +708,10 @@ struct StatAcc {
     }
 };
 
-__device__ __noinline__ void brute_chunk(Ctx& c, StatAcc& acc, int cnt, bool early_exit, bool indep) {
+// (its own StatAcc: a reference to the caller's would put the caller's
+// counters in local memory)
+__device__ __noinline__ void brute_chunk(Ctx& c, int cnt, bool early_exit, bool indep) {
+    StatAcc acc(c);
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nw = c.nthreads >> 5;
     const int NS = c.NS, S = c.S, NP = c.NP;
     const SceneV v = scene_view(c);
@@ -789,8 +792,11 @@ __device__ __noinline__ void brute_chunk(Ctx& c, StatAcc& acc, int cnt, bool ear
 // publishes it in ictl[IC_STOP] at the stage-1 barrier (or the brute-force
 // path's final one), for callers that abandon the chain when the problem
 // has been settled meanwhile; the load's latency hides behind stage 1.
-__device__ __noinline__ void check_chunk(Ctx& c, int cnt, bool two_stage, bool early_exit, bool indep,
-                                         const int* stop_flag = nullptr) {
+// check_chunk_inl is inlined into the planner's single chain-validation site
+// (no call boundary per chunk); check_chunk is the out-of-line copy for the
+// cold callers (endpoint checks, the batched checking kernels).
+__device__ __forceinline__ void check_chunk_inl(Ctx& c, int cnt, bool two_stage, bool early_exit, bool indep,
+                                                const int* stop_flag = nullptr) {
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nw = c.nthreads >> 5;
     const int NS = c.NS, L = c.L, NP = c.NP;
     const ChunkV k = chunk_view(c);
@@ -803,7 +809,7 @@ __device__ __noinline__ void check_chunk(Ctx& c, int cnt, bool two_stage, bool e
     if (prof && tid == 0) prof[4] = clock64();
     const int stop = (stop_flag && tid == 0) ? ld_relaxed(stop_flag) : 0;
     if (!two_stage) {
-        brute_chunk(c, acc, cnt, early_exit, indep);
+        brute_chunk(c, cnt, early_exit, indep);
         if (stop_flag && tid == 0) k.ictl[IC_STOP] = stop;
         __syncthreads();
         return;
@@ -959,6 +965,11 @@ __device__ __noinline__ void check_chunk(Ctx& c, int cnt, bool two_stage, bool e
     __syncthreads();
 }
 
+__device__ __noinline__ void check_chunk(Ctx& c, int cnt, bool two_stage, bool early_exit, bool indep,
+                                         const int* stop_flag = nullptr) {
+    check_chunk_inl(c, cnt, two_stage, early_exit, indep, stop_flag);
+}
+
 // ---------------------------------------------------------------------------
 // chain states. Points p_0 = A, p_k = lerp(A, B, k/n) (k < n), p_n = B
 // (planner.cpp:35-44 step_target; extend is the n = 1 case). State g covers
@@ -983,8 +994,8 @@ __device__ __noinline__ double frac_div(int i, int n) { return __ddiv_rn((double
 // stop_flag (nullable): thread 0 issues a relaxed load of it on entry and
 // publishes the value in ictl[IC_STOP] just before the final barrier, so the
 // caller can abandon the chunk without a barrier pair of its own.
-__device__ __noinline__ int gen_chain_states(Ctx& c, const double* A, const double* B, long long n_sub,
-                                 int n_cc, long long g0l, int cnt, const int* stop_flag) {
+__device__ __forceinline__ int gen_chain_states_inl(Ctx& c, const double* A, const double* B, long long n_sub,
+                                                    int n_cc, long long g0l, int cnt, const int* stop_flag) {
     const int tid = threadIdx.x, dof = c.dof, NS = c.NS, nthreads = c.nthreads;
     const int stop = (stop_flag && tid == 0) ? ld_relaxed(stop_flag) : 0;
     double* const ends = sh(c.ends);
@@ -1054,6 +1065,11 @@ __device__ __noinline__ int gen_chain_states(Ctx& c, const double* A, const doub
     }
     if (tid == 0) sh(c.ictl)[IC_STOP] = stop;
     return __syncthreads_count(mine);
+}
+
+__device__ __noinline__ int gen_chain_states(Ctx& c, const double* A, const double* B, long long n_sub, int n_cc,
+                                             long long g0l, int cnt, const int* stop_flag) {
+    return gen_chain_states_inl(c, A, B, n_sub, n_cc, g0l, cnt, stop_flag);
 }
 
 // ---------------------------------------------------------------------------

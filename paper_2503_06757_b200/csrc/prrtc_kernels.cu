@@ -331,7 +331,7 @@ __device__ long long validate_chain(Ctx& c, const PlanArgs& a, const double* A, 
     for (long long g0 = 0; g0 < total; g0 += c.NS) {
         trace_phase(a, 9);  // PRRTC_TRACE: chain states
         const int cnt = (int)min((long long)c.NS, total - g0);
-        const int act = gen_chain_states(c, A, B, n_sub, n_cc, g0, cnt, done_flag);
+        const int act = gen_chain_states_inl(c, A, B, n_sub, n_cc, g0, cnt, done_flag);
         if (done_flag && sh(c.ictl)[IC_STOP] != 0) {  // stop flag (planner.cpp:112): not running
             *stopped = true;
             return 0;
@@ -341,7 +341,7 @@ __device__ long long validate_chain(Ctx& c, const PlanArgs& a, const double* A, 
             sh(c.stat)[1] += (unsigned long long)act * c.fkflops;  // thread 0's flop slot
         }
         trace_phase(a, 5);  // FK + collision
-        check_chunk(c, cnt, a.p.two_stage != 0, a.p.early_exit != 0, false, done_flag);
+        check_chunk_inl(c, cnt, a.p.two_stage != 0, a.p.early_exit != 0, false, done_flag);
         trace_phase(a, 9);
         if (done_flag && sh(c.ictl)[IC_STOP] != 0) {  // settled while this chunk was checked
             *stopped = true;
@@ -928,51 +928,63 @@ __global__ void __launch_bounds__(NT, MINB) plan_kernel(PlanArgs a) {
                 cnew[tid] = dist <= delta ? smp[tid] : lerp_exact(v, smp[tid], __ddiv_rn(delta, dist));
             }
             __syncthreads();
-            // ---- SIMT edge validation nn -> c_new, then append ----
-            int last = nn;
-            bool stopped = false;
-            // (the done flag is sampled here too: a CTA still extending when
-            // another one solved the problem leaves at the next chunk
+            // ---- SIMT edge validation nn -> c_new, then append (phase 0),
+            // then greedy connect c_new -> the opposite tree (phase 1): one
+            // validate_chain call site for both, so the chain/chunk code is
+            // inlined once (no ABI register saves per chunk)
+            // (the done flag is sampled in every chunk: a CTA still working
+            // when another one solved the problem leaves at the next chunk
             // instead of finishing the iteration — the result is settled)
-            const long long ok = validate_chain(c, a, nnc, cnew, 1, &Ts, nn, &last, &C.done,
-                                                &stopped);
-            if (stopped) continue;  // the header sees the done flag and leaves
-            if (ok == 0) {
-                if (a.p.dynamic_domain && tid == 0) Ts.dd[nn] = 1;  // record_failure
-                continue;
-            }
-            if (ok < 0) {
-                leave_msg = MSG_CAPACITY;
-                break;
-            }
-            const int new_idx = last;
-            // ---- greedy connect toward the opposite tree ----
-            TRACE_PHASE(4);
-            if (tid == 0) {
-                const int po = ld_relaxed(To.published);
-                sh(c.ictl)[IC_TMP3] = ld_relaxed(&C.done);  // settled meanwhile: skip the connect
-                int* known = sh(c.ictl) + IC_KNOWN0 + To.which;
-                if (po > *known || (a.dbg & 1)) {
-                    fence_acq_rel();
-                    *known = po;
+            const double* VA = nnc;
+            const double* VB = cnew;
+            long long nsub = 1;
+            int par0 = nn, phase = 0, new_idx = nn, nno = -1, meet_self = nn;
+            int outcome = 0;  // 0 next iteration, 1 reached, 2 tree full
+#pragma unroll 1
+            for (;;) {
+                int last = par0;
+                bool stopped = false;
+                const long long got = validate_chain(c, a, VA, VB, nsub, &Ts, par0, &last, &C.done, &stopped);
+                if (got < 0) {
+                    outcome = 2;
+                    break;
                 }
-                sh(c.ictl)[IC_TMP2] = po;
-            }
-            __syncthreads();
-            const int snap_o = sh(c.ictl)[IC_TMP2];
-            const int settled = sh(c.ictl)[IC_TMP3];
-            __syncthreads();
-            if (settled != DONE_RUNNING) continue;  // the header leaves
-            nn_scan_multi(c, To.cfg, a.stride, snap_o, cnew, 1, nullptr);
-            const int nno = sh(c.mnn_i)[0];
-            const double d2o = sh(c.mnn_d)[0];
-            bool reached = false;
-            int meet_self = new_idx;
-            if (d2o == 0.0) {
-                reached = true;
-            } else {
+                if (phase == 1) {
+                    outcome = (got == nsub && !stopped) ? 1 : 0;
+                    meet_self = last;
+                    break;
+                }
+                if (stopped) break;  // the header sees the done flag and leaves
+                if (got == 0) {
+                    if (a.p.dynamic_domain && tid == 0) Ts.dd[nn] = 1;  // record_failure
+                    break;
+                }
+                new_idx = meet_self = last;
+                // ---- greedy connect toward the opposite tree ----
+                TRACE_PHASE(4);
+                if (tid == 0) {
+                    const int po = ld_relaxed(To.published);
+                    sh(c.ictl)[IC_TMP3] = ld_relaxed(&C.done);  // settled meanwhile: skip the connect
+                    int* known = sh(c.ictl) + IC_KNOWN0 + To.which;
+                    if (po > *known || (a.dbg & 1)) {
+                        fence_acq_rel();
+                        *known = po;
+                    }
+                    sh(c.ictl)[IC_TMP2] = po;
+                }
+                __syncthreads();
+                const int snap_o = sh(c.ictl)[IC_TMP2];
+                const int settled = sh(c.ictl)[IC_TMP3];
+                __syncthreads();
+                if (settled != DONE_RUNNING) break;  // the header leaves
+                nn_scan_multi(c, To.cfg, a.stride, snap_o, cnew, 1, nullptr);
+                nno = sh(c.mnn_i)[0];
+                const double d2o = sh(c.mnn_d)[0];
+                if (d2o == 0.0) {
+                    outcome = 1;
+                    break;
+                }
                 const double disto = __dsqrt_rn(d2o);
-                const long long n_ext = (long long)ceil(__ddiv_rn(disto, delta));
                 double* tgt = dc(c, DC_TARGET);
                 double* A = dc(c, DC_A);
                 if (tid < dof) {
@@ -980,16 +992,17 @@ __global__ void __launch_bounds__(NT, MINB) plan_kernel(PlanArgs a) {
                     A[tid] = cnew[tid];
                 }
                 __syncthreads();
-                const long long got = validate_chain(c, a, A, tgt, n_ext, &Ts, new_idx, &last,
-                                                     &C.done, &stopped);
-                if (got < 0) {
-                    leave_msg = MSG_CAPACITY;
-                    break;
-                }
-                reached = (got == n_ext) && !stopped;
-                meet_self = last;
+                VA = A;
+                VB = tgt;
+                nsub = (long long)ceil(__ddiv_rn(disto, delta));
+                par0 = new_idx;
+                phase = 1;
             }
-            if (!reached) continue;
+            if (outcome == 2) {
+                leave_msg = MSG_CAPACITY;
+                break;
+            }
+            if (outcome == 0) continue;
             // ---- winner (planner.cpp:232-238) ----
             TRACE_PHASE(6);
             if (tid == 0) sh(c.ictl)[IC_TMP6] = (atomicCAS(&C.winner, 0, blockIdx.x + 1) == 0);

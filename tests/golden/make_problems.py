@@ -1,6 +1,10 @@
 """Generates the committed planning-problem fixtures (TEST/BENCH INFRASTRUCTURE).
 
-    python tests/golden/make_problems.py [robot ...] [--n N]
+    python tests/golden/make_problems.py [robot ...] [--n N] [--set K]
+
+--set K (K >= 1) writes problems_<robot>_s<K>.npz: another N problems with
+problem ids from K * 100000 (disjoint scenes, starts and goals), the shard of
+rank K in the multi-GPU weak-scaling bench (rank 0 uses problems_<robot>.npz).
 
 For every problem id p: the scene is make_scene(robot, kind_for(p, N), p)
 (deterministic, so only start/goal are stored). Start = the robot's home pose
@@ -117,11 +121,11 @@ def sample_start(o, model, scene, rng):
     return None
 
 
-def generate(robot: str, n: int, o: Oracle):
+def generate(robot: str, n: int, o: Oracle, p0: int = 0):
     model = robots.get(robot)
     starts, goals, kinds, pids = [], [], [], []
     t0 = time.time()
-    p = 0
+    p = p0
     while len(pids) < n:
         kind = kind_for(len(pids), n)
         scene, regions = make_scene(robot, kind, p)
@@ -134,13 +138,18 @@ def generate(robot: str, n: int, o: Oracle):
             kinds.append(kind)
             pids.append(p)
         p += 1
-        if p % 100 == 0:
+        if (p - p0) % 100 == 0:
             print(f"{robot}: {len(pids)}/{p} problems, {time.time() - t0:.1f}s", flush=True)
     return (np.array(kinds), np.array(pids, dtype=np.int64), np.array(starts), np.array(goals))
 
 
 def main(argv):
     n_override = None
+    set_k = 0
+    if "--set" in argv:
+        i = argv.index("--set")
+        set_k = int(argv[i + 1])
+        argv = argv[:i] + argv[i + 2:]
     if "--n" in argv:
         i = argv.index("--n")
         n_override = int(argv[i + 1])
@@ -149,8 +158,8 @@ def main(argv):
     o = Oracle("ref")
     for r in names:
         n = n_override or DEFAULT_N[r]
-        kinds, pids, S, G = generate(r, n, o)
-        out = Path(__file__).resolve().parent / f"problems_{r}.npz"
+        kinds, pids, S, G = generate(r, n, o, p0=100000 * set_k)
+        out = Path(__file__).resolve().parent / (f"problems_{r}_s{set_k}.npz" if set_k else f"problems_{r}.npz")
         np.savez_compressed(out, kind=kinds, pid=pids, start=S, goal=G, n=n)
         print(f"wrote {out}: {len(pids)} problems (ids up to {pids.max()})")
 
