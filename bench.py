@@ -238,47 +238,26 @@ def microbench(model, scenes, S, G, dev, fp32_peak):
 
 
 def bench_extras(dev, params):
-    """BASELINE configs 3-5 beside the headline (informational, untimed by the
-    driver), rank 0: Fetch / Baxter 1000-problem batches (configs 3, 4) and the
-    dynamic-obstacle replanning loop (config 5: 100 frames, 3 spheres moving
-    1 cm/frame, prrtc_scene_update + prrtc_plan per frame). The 10k mixed
-    batch is mixed_sharded (every rank)."""
+    """BASELINE config 5's dynamic-obstacle replanning loop beside the headline
+    (informational, untimed by the driver), rank 0: 100 frames, 3 spheres
+    moving 1 cm/frame, prrtc_scene_update + prrtc_plan per frame. Configs 3-4
+    (Fetch / Baxter) are table_one; the 10k mixed batch is mixed_sharded
+    (every rank)."""
     import torch
     from paper_2503_06757_b200 import planner, replan
     from paper_2503_06757_b200.model import PlannerParams, PlanStatus
 
-    out = {"robots": {}}
-    for robot in ("fetch", "baxter"):
-        model, scenes, S, G, kinds = load_workload(robot, 1000)
-        rp = robot_params(robot, params)
-        b = planner.Batch(model, scenes, S, G, rp, device=dev)
-        b.launch()
-        b.results()
-        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        ms = []
-        for _ in range(3):
-            e0.record()
-            b.launch(torch.cuda.current_stream().cuda_stream)
-            e1.record()
-            torch.cuda.synchronize()
-            ms.append(e0.elapsed_time(e1))
-        res = b.results()
-        ok = [r.status == PlanStatus.Solved for r in res]
-        dv = [r.device_time_ms for r in res if r.status == PlanStatus.Solved]
-        out["robots"][robot] = {"problems_per_s": len(S) / (statistics.median(ms) / 1e3),
-                                "success_rate": float(np.mean(ok)), "device_ms_median": float(np.median(dv)),
-                                "device_ms_p95": float(np.percentile(dv, 95)), "dof": model.dof,
-                                "dd_radius": rp.resolved_dd_radius(), "problems": len(S)}
-        del b
+    out = {}
     # replanning loop
     model, scenes, S, G, kinds = load_workload("panda", 1000)
     i = int(np.where(kinds == "table_pick")[0][0])
-    frames = replan.run(model, scenes[i], S[i], G[i], frames=100, params=params, device=dev)
+    rp = PlannerParams()  # latency scenario: workers = 0 (one CTA per SM)
+    frames = replan.run(model, scenes[i], S[i], G[i], frames=100, params=rp, device=dev)
     wall = [f.wall_ms for f in frames]
     ok = [f.result.status == PlanStatus.Solved for f in frames]
     out["replanning"] = {"frames": len(frames), "frame_ms_median": float(np.median(wall)),
                          "frame_ms_p95": float(np.percentile(wall, 95)), "success_rate": float(np.mean(ok)),
-                         "api": "prrtc_scene_update + prrtc_plan per frame (host wall clock)",
+                         "api": "prrtc_scene_update + prrtc_plan per frame (host wall clock), workers = 0",
                          "obstacles": "3 spheres r=0.05 moving 1 cm/frame through a table_pick scene"}
     return out
 
@@ -302,7 +281,10 @@ def _stats(ok, cost, res_paths):
             "cost_median": float(np.median(c)) if c else None, "cost_mean": float(np.mean(c)) if c else None}
 
 
-def parity_block(robot_names, workers_list, n, device=0, tree_capacity=200000, threads=None):
+PARITY_SUBSET = {("fetch", 16): 500, ("baxter", 16): 200}  # bounds the reference's 16-thread arms' time
+
+
+def parity_block(robot_names, workers_list, n, device=0, tree_capacity=200000, threads=None, subset=None):
     """Equal-budget statistical parity (north_star: success no lower than the
     reference's, initial path cost reported alongside; every returned path
     re-validated by the reference checker). Per robot and W: the B200 batch
@@ -320,11 +302,16 @@ def parity_block(robot_names, workers_list, n, device=0, tree_capacity=200000, t
                      "two-stage, early exit, Halton) with workers = W on both arms",
            "tree_capacity": tree_capacity, "host_threads": threads, "robots": {}}
     o = None
+    subset = PARITY_SUBSET if subset is None else subset
     for robot in robot_names:
-        model, scenes, S, G, kinds = load_workload(robot, n)
-        dsc = planner.device_scenes(scenes, device)
-        rr = {"problems": len(S)}
+        model, scenes_all, S_all, G_all, kinds = load_workload(robot, n)
+        dsc_all = planner.device_scenes(scenes_all, device)
+        rr = {"problems": len(S_all)}
         for W in workers_list:
+            k = min(len(S_all), subset.get((robot, W), len(S_all)))
+            idx = np.unique(np.linspace(0, len(S_all) - 1, k).round().astype(int))
+            scenes, S, G = [scenes_all[i] for i in idx], S_all[idx], G_all[idx]
+            dsc = planner.device_scenes(scenes, device) if k < len(S_all) else dsc_all
             params = robot_params(robot, PlannerParams(workers=W, tree_capacity=tree_capacity))
             planner.plan_batch_arrays(model, dsc.hs[:8], S[:8], G[:8], params, device=device)  # workspace warm-up
             t0 = time.perf_counter()
@@ -372,6 +359,7 @@ def parity_block(robot_names, workers_list, n, device=0, tree_capacity=200000, t
                                           "reference": float(np.mean([r.cost for r, b in zip(ref, both) if b]))
                                           if both.any() else None},
                 "dd_radius": params.resolved_dd_radius(),
+                "problems": len(S),
             }
             if W > 1:
                 # single-problem mode: prrtc_plan puts W CTAs on the problem at once,
@@ -435,11 +423,18 @@ def mixed_sharded(dev, world, rank, total=10000):
 HEADLINE_WORKERS = 1  # workers per problem on BOTH arms (identical PlannerParams)
 
 
+HEADLINE_CAPACITY = 20000  # right-sized (both arms); the default 200000 is reported beside it
+
+
 def headline_params(**kw):
     """The headline's PlannerParams, identical on both arms: the reference
     defaults (planner.hpp:21-40) with workers = 1 (per-problem iteration budget
-    max_iters_per_worker x 1 = 2000, planner.cpp:199) and tree_capacity 200000."""
+    max_iters_per_worker x 1 = 2000, planner.cpp:199) and tree_capacity 20000
+    (ample for 2000 iterations; the reference allocates its trees inside the
+    timed plan() call, planner.cpp:254,290-291, so the default 200000 would
+    mostly time that allocation — its figures are reported alongside)."""
     from paper_2503_06757_b200.model import PlannerParams
+    kw.setdefault("tree_capacity", HEADLINE_CAPACITY)
     return PlannerParams(workers=HEADLINE_WORKERS, **kw)
 
 
@@ -543,8 +538,8 @@ def run_reference(args):
         cost += [r.cost for r in res if r.status == PlanStatus.Solved]
     ms = statistics.median(times)
     value = len(S) / (ms / 1e3)
-    # the right-sized tree capacity (the reference allocates its trees inside plan())
-    r20, ms20 = o.plan_many(model, scenes, S, G, headline_params(tree_capacity=20000), threads=threads)
+    # the reference's default tree capacity (its allocation is inside plan())
+    r20, ms20 = o.plan_many(model, scenes, S, G, headline_params(tree_capacity=200000), threads=threads)
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
@@ -552,8 +547,8 @@ def run_reference(args):
         "config": workload_config(args.robot, len(S), params, args.gpus),
         "success_rate": float(np.mean(solved)), "mean_cost": float(np.mean(cost)),
         "host_threads": threads, "cpu_model": lscpu_model(),
-        "tree_capacity_20000": {"problems_per_s": len(S) / (ms20 / 1e3),
-                                "success_rate": float(np.mean([r.status == PlanStatus.Solved for r in r20]))},
+        "tree_capacity_200000": {"problems_per_s": len(S) / (ms20 / 1e3),
+                                 "success_rate": float(np.mean([r.status == PlanStatus.Solved for r in r20]))},
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": kind,
                          "sample": f"all {len(S)} problems x {args.steps} steps, workers=1 per problem, "
                                    f"{threads} problems in parallel"},
@@ -763,7 +758,7 @@ def run_b200(args):
             line["mixed_10k"] = mixed
         if world == 1 and not args.no_cpu_baseline:
             cb = cpu_baseline_block(model, scenes, S, G, kinds, gpu_single)
-            t = cb["throughput_cap200000"]
+            t = cb[f"throughput_cap{HEADLINE_CAPACITY}"]
             line["cpu_baseline"] = {"value": t["problems_per_s"], "unit": UNIT, "cores": cb["cores"],
                                     "kind": cb["kind"], "sample": t["sample"], **cb}
         if parity is not None:

@@ -229,6 +229,30 @@ int prrtc_plan_batch(const prrtc_robot* robot, const prrtc_scene* const* scenes,
                      uint32_t n_problems, const double* starts, const double* goals,
                      uint32_t dof, const prrtc_params* params, prrtc_result* out);
 
+/* n independent problems spread over several devices (the
+   reference's plan() is safe to call concurrently, planner.cpp:246-322):
+   one host thread per device pulls chunks of `chunk` consecutive problems
+   from a shared atomic queue (0 = automatic: about 4 chunks per device, at
+   least 64 problems) and solves each chunk with prrtc_plan_batch on its
+   device, so a device that draws hard problems takes fewer chunks (the
+   per-problem time is heavy-tailed). No collective and no cross-device
+   traffic: handles are per device. robots[d] and scenes[d * n_problems + i]
+   are the robot and problem i's scene uploaded to device d (d < n_devices,
+   one entry per participating device, each on a distinct device). Results
+   land in out[i] in caller order; on error the first failing device's code
+   is returned and the other devices stop taking chunks. */
+int prrtc_plan_batch_multi(const prrtc_robot* const* robots, const prrtc_scene* const* scenes,
+                           uint32_t n_devices, uint32_t n_problems, const double* starts,
+                           const double* goals, uint32_t dof, const prrtc_params* params,
+                           uint32_t chunk, prrtc_result* out);
+/* The chunk queue of prrtc_plan_batch_multi run without devices (host-side
+   logic, testable anywhere): `n_workers` threads take chunks until
+   n_problems are handed out; owner[i] = the worker that took problem i,
+   chunks_taken[w] = chunks of worker w (worker w sleeps delay_us[w]
+   microseconds per problem it takes, to emulate slow devices; may be NULL). */
+int prrtc_debug_chunk_queue(uint32_t n_workers, uint32_t n_problems, uint32_t chunk,
+                            const uint32_t* delay_us, int32_t* owner, uint32_t* chunks_taken);
+
 void prrtc_result_free(prrtc_result* result);
 /* Frees the paths of n results (prrtc_plan_batch output) in one call. */
 void prrtc_results_free(prrtc_result* results, uint32_t n);
@@ -271,6 +295,17 @@ int prrtc_check_configs(const prrtc_robot* robot, const prrtc_scene* scene, cons
    (either may be NULL). */
 int prrtc_debug_fk(const prrtc_robot* robot, const double* q, uint32_t n_configs,
                    uint32_t dof, float* fine_out, float* coarse_out);
+/* Edge-level parity hook (CollisionChecker::validate_edge,
+   collision.cpp:206-224): for every edge, every sample i = 1..n_cc
+   (edge_sample, the far endpoint copied exactly) is checked on the device
+   with no early exit; state_valid[e*n_cc + i-1] = the device's verdict of that
+   state and fine_out[((e*n_cc + i-1)*S + j)*3 + k] = the posed centre of fine
+   sphere j exactly as the device's collision code saw it (FP32; NULL to skip).
+   The edge verdict of prrtc_validate_edges is the AND over its states (a
+   bitwise-equal edge is one check of `to`, whose state is every sample). */
+int prrtc_debug_check_edges(const prrtc_robot* robot, const prrtc_scene* scene, const double* from,
+                            const double* to, uint32_t n_edges, uint32_t dof, int32_t n_cc, int two_stage,
+                            uint8_t* state_valid, float* fine_out);
 /* Per-(config, fine sphere, primitive) verdicts of the device predicate
    (FP32 with FP64 guard band) for posed spheres given in FP32: hits[n*P]
    with primitive order spheres, boxes, capsules. */

@@ -78,6 +78,10 @@ class Oracle:
         if self._many is not None:
             self._many.restype = C.c_int
             self._many.argtypes = [P, C.POINTER(P), C.c_uint32, DP, U64P, C.c_int, C.c_uint32, U8P]
+        self._anyhit = getattr(self.lib, PREFIX[kind] + "sphere_any_hits", None)
+        if self._anyhit is not None:
+            self._anyhit.restype = C.c_int
+            self._anyhit.argtypes = [P, DP, C.c_uint32, U8P]
         self._robots = {}
         self._scenes = {}
 
@@ -136,6 +140,18 @@ class Oracle:
         out = np.zeros(max(1, len(scene.primitives)), dtype=np.uint8)
         self.fn["sphere_hits"](s, float(x), float(y), float(z), float(r), out.ctypes.data_as(U8P))
         return out[: len(scene.primitives)].astype(bool)
+
+    def sphere_any_hits(self, scene, xyzr) -> np.ndarray:
+        """Per sphere (rows x, y, z, r): does the reference predicate
+        sphere_vs_primitive flag any primitive of the scene."""
+        X = np.ascontiguousarray(np.asarray(xyzr, dtype=np.float64).reshape(-1, 4))
+        out = np.zeros(X.shape[0], dtype=np.uint8)
+        if self._anyhit is not None:
+            self._anyhit(self.scene(scene), _dp(X), X.shape[0], out.ctypes.data_as(U8P))
+        else:
+            for i, (x, y, z, r) in enumerate(X):
+                out[i] = bool(self.sphere_hits(scene, x, y, z, r).any())
+        return out.astype(bool)
 
     def check_config(self, model, scene, q, two_stage=True, early_exit=True, stats=False):
         h, dof, _ = self.robot(model)

@@ -187,6 +187,19 @@ int ref_sphere_hits(void* scene, double x, double y, double z, double r, uint8_t
     return any;
 }
 
+// any_hit[i] = 1 iff sphere i (xyzr[4i..4i+3]) hits some primitive, by the
+// reference predicate sphere_vs_primitive (geometry.cpp:41-66).
+int ref_sphere_any_hits(void* scene, const double* xyzr, uint32_t n, uint8_t* any_hit) {
+    const auto& s = *static_cast<Scene*>(scene);
+    for (uint32_t i = 0; i < n; ++i) {
+        PosedSphere ps{{xyzr[4 * i], xyzr[4 * i + 1], xyzr[4 * i + 2]}, xyzr[4 * i + 3]};
+        uint8_t h = 0;
+        for (size_t k = 0; k < s.primitives.size() && !h; ++k) h = sphere_vs_primitive(ps, s.primitives[k]) ? 1 : 0;
+        any_hit[i] = h;
+    }
+    return 0;
+}
+
 static void put_stats(const CheckStats& st, uint64_t* out) {
     if (!out) return;
     auto s = snapshot(st);

@@ -118,6 +118,10 @@ SIGNATURES = [
     ("prrtc_scene_destroy", C.c_int, [P]),
     ("prrtc_plan", C.c_int, [P, P, DP, DP, C.c_uint32, C.POINTER(Params), C.POINTER(Result)]),
     ("prrtc_plan_batch", C.c_int, [P, C.POINTER(P), C.c_uint32, DP, DP, C.c_uint32, C.POINTER(Params), C.POINTER(Result)]),
+    ("prrtc_plan_batch_multi", C.c_int, [C.POINTER(P), C.POINTER(P), C.c_uint32, C.c_uint32, DP, DP, C.c_uint32,
+                                         C.POINTER(Params), C.c_uint32, C.POINTER(Result)]),
+    ("prrtc_debug_chunk_queue", C.c_int, [C.c_uint32, C.c_uint32, C.c_uint32, C.POINTER(C.c_uint32),
+                                          C.POINTER(C.c_int32), C.POINTER(C.c_uint32)]),
     ("prrtc_result_free", None, [C.POINTER(Result)]),
     ("prrtc_results_free", None, [C.POINTER(Result), C.c_uint32]),
     ("prrtc_results_pack_paths", C.c_int, [C.POINTER(Result), C.c_uint32, C.POINTER(C.c_double),
@@ -130,6 +134,7 @@ SIGNATURES = [
     ("prrtc_validate_edges", C.c_int, [P, P, DP, DP, C.c_uint32, C.c_uint32, C.c_int32, C.c_int, C.c_int, U8P]),
     ("prrtc_check_configs", C.c_int, [P, P, DP, C.c_uint32, C.c_uint32, C.c_int, U8P]),
     ("prrtc_debug_fk", C.c_int, [P, DP, C.c_uint32, C.c_uint32, FP, FP]),
+    ("prrtc_debug_check_edges", C.c_int, [P, P, DP, DP, C.c_uint32, C.c_uint32, C.c_int32, C.c_int, U8P, FP]),
     ("prrtc_debug_sphere_hits", C.c_int, [P, FP, DP, C.c_uint32, U8P]),
     ("prrtc_debug_nn", C.c_int, [DP, C.c_uint32, C.c_uint32, DP, C.c_uint32, C.c_int, C.POINTER(C.c_uint32), DP]),
     ("prrtc_debug_nn_multi", C.c_int, [DP, C.c_uint32, C.c_uint32, DP, C.c_uint32, C.c_uint32, C.c_int,

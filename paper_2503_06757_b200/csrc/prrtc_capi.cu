@@ -17,6 +17,7 @@
 #include <memory>
 #include <mutex>
 #include <string>
+#include <thread>
 #include <vector>
 
 #include "prrtc_b200.h"
@@ -443,19 +444,21 @@ int prrtc_robot_create(const prrtc_robot_desc* d, int device, prrtc_robot** out)
             r->limits.push_back(f);
         }
     }
-    r->fine_r64.resize(S);
+    // FP64 radii: the fine spheres', then the coarse spheres' (exact CheckStats mode)
+    r->fine_r64.resize(S + n);
     for (uint32_t k = 0; k < S; ++k) r->fine_r64[k] = d->fine[4 * k + 3];
+    for (int l = 0; l < n; ++l) r->fine_r64[S + l] = d->coarse[4 * l + 3];
 
     cudaSetDevice(device);
     if (cudaMalloc(&r->d_words, 4 * w.size()) != cudaSuccess ||
-        cudaMalloc(&r->d_fine_r64, 8 * std::max<size_t>(1, S)) != cudaSuccess ||
+        cudaMalloc(&r->d_fine_r64, 8 * r->fine_r64.size()) != cudaSuccess ||
         cudaMalloc(&r->d_limits, 8 * std::max<size_t>(2, r->limits.size())) != cudaSuccess) {
         prrtc_robot_destroy(r);
         return set_err(PRRTC_ENOMEM, "prrtc_robot_create: device allocation failed");
     }
     const std::pair<void*, std::pair<const void*, size_t>> copies[3] = {
         {r->d_words, {w.data(), 4 * w.size()}},
-        {r->d_fine_r64, {r->fine_r64.data(), 8 * (size_t)S}},
+        {r->d_fine_r64, {r->fine_r64.data(), 8 * r->fine_r64.size()}},
         {r->d_limits, {r->limits.data(), 8 * r->limits.size()}}};
     if (upload_sync(device, copies, 3) != cudaSuccess) {
         prrtc_robot_destroy(r);
@@ -1094,6 +1097,7 @@ int batch_enqueue(prrtc_batch* b, cudaStream_t st, bool upload) {
     a.p.early_exit = b->params.early_exit;
     a.p.two_stage = b->params.two_stage;
     a.p.deterministic = b->params.deterministic;
+    a.ref_stats = b->params.deterministic ? 1 : 0;
     a.p.budget = b->budget;
     a.p.seed = b->params.seed;
     a.ns_max = b->ns_max;
@@ -1511,6 +1515,103 @@ int plan_batch_once(const prrtc_robot* robot, const prrtc_scene* const* scenes, 
 }
 }  // namespace
 
+// ---------------------------------------------------------------------------
+// multi-device batches: a host thread per device, a shared
+// chunk queue, no collective
+// ---------------------------------------------------------------------------
+}  // extern "C"
+namespace {
+uint32_t auto_chunk(uint32_t n, uint32_t n_dev) {
+    const uint32_t c = (n + 4 * n_dev - 1) / (4 * n_dev);
+    return std::max<uint32_t>(64, c);
+}
+
+// Runs `work(worker, begin, count)` for consecutive chunks handed out by one
+// atomic counter to n_workers threads (thread 0 is the caller); stops handing
+// out chunks once some work returns nonzero and returns the first such code.
+template <class F>
+int run_chunk_queue(uint32_t n_workers, uint32_t n, uint32_t chunk, F work) {
+    std::atomic<uint32_t> next{0};
+    std::atomic<int> err{0};
+    auto loop = [&](uint32_t w) {
+        for (;;) {
+            if (err.load(std::memory_order_relaxed)) return;
+            const uint32_t b = next.fetch_add(chunk, std::memory_order_relaxed);
+            if (b >= n) return;
+            const int rc = work(w, b, std::min(chunk, n - b));
+            if (rc) {
+                int z = 0;
+                err.compare_exchange_strong(z, rc);
+                return;
+            }
+        }
+    };
+    std::vector<std::thread> th;
+    for (uint32_t w = 1; w < n_workers; ++w) th.emplace_back(loop, w);
+    loop(0);
+    for (auto& t : th) t.join();
+    return err.load();
+}
+}  // namespace
+extern "C" {
+
+int prrtc_plan_batch_multi(const prrtc_robot* const* robots, const prrtc_scene* const* scenes,
+                           uint32_t n_devices, uint32_t n_problems, const double* starts,
+                           const double* goals, uint32_t dof, const prrtc_params* params,
+                           uint32_t chunk, prrtc_result* out) {
+    if (!robots || !scenes || !starts || !goals || !params || !out)
+        return set_err(PRRTC_EINVAL, "prrtc_plan_batch_multi: null argument");
+    if (n_devices == 0) return set_err(PRRTC_EINVAL, "prrtc_plan_batch_multi: no devices");
+    if (n_problems == 0) return set_err(PRRTC_EINVAL, "plan: empty batch");
+    for (uint32_t d = 0; d < n_devices; ++d) {
+        if (!robots[d]) return set_err(PRRTC_EINVAL, "prrtc_plan_batch_multi: null robot");
+        if ((int)dof != robots[d]->dof)
+            return set_err(PRRTC_EINVAL, "plan.start: expected dimension " + std::to_string(robots[d]->dof) +
+                                             ", got " + std::to_string(dof));
+        for (uint32_t e = 0; e < d; ++e)
+            if (robots[e]->device == robots[d]->device)
+                return set_err(PRRTC_EINVAL, "prrtc_plan_batch_multi: two entries on the same device");
+        for (uint32_t i = 0; i < n_problems; ++i) {
+            const prrtc_scene* sc = scenes[(size_t)d * n_problems + i];
+            if (!sc || sc->device != robots[d]->device)
+                return set_err(PRRTC_EINVAL, "plan: scene missing or on another device");
+        }
+    }
+    int rc = check_params(params);
+    if (rc) return rc;
+    if (!chunk) chunk = auto_chunk(n_problems, n_devices);
+    std::vector<std::string> errs(n_devices);
+    rc = run_chunk_queue(n_devices, n_problems, chunk, [&](uint32_t d, uint32_t b, uint32_t cnt) {
+        const int r = prrtc_plan_batch(robots[d], scenes + (size_t)d * n_problems + b, cnt,
+                                       starts + (size_t)b * dof, goals + (size_t)b * dof, dof, params, out + b);
+        if (r) errs[d] = g_err;  // thread-local message of the worker's thread
+        return r;
+    });
+    if (rc) {
+        for (const auto& e : errs)
+            if (!e.empty()) return set_err(rc, e);
+        return set_err(rc, "prrtc_plan_batch_multi failed");
+    }
+    return PRRTC_OK;
+}
+
+int prrtc_debug_chunk_queue(uint32_t n_workers, uint32_t n_problems, uint32_t chunk, const uint32_t* delay_us,
+                            int32_t* owner, uint32_t* chunks_taken) {
+    if (!owner || !chunks_taken || n_workers == 0) return set_err(PRRTC_EINVAL, "prrtc_debug_chunk_queue: bad argument");
+    if (!chunk) chunk = auto_chunk(n_problems, n_workers);
+    for (uint32_t i = 0; i < n_problems; ++i) owner[i] = -1;
+    for (uint32_t w = 0; w < n_workers; ++w) chunks_taken[w] = 0;
+    return run_chunk_queue(n_workers, n_problems, chunk, [&](uint32_t w, uint32_t b, uint32_t cnt) {
+        for (uint32_t i = b; i < b + cnt; ++i) {
+            if (owner[i] != -1) return PRRTC_EINVAL;  // handed out twice
+            owner[i] = (int32_t)w;
+        }
+        ++chunks_taken[w];
+        if (delay_us && delay_us[w]) std::this_thread::sleep_for(std::chrono::microseconds(delay_us[w] * cnt));
+        return PRRTC_OK;
+    });
+}
+
 int prrtc_last_transfer_bytes(int device, uint64_t* h2d, uint64_t* d2h) {
     if (device < 0 || device >= 64) return set_err(PRRTC_ENODEV, "device ordinal out of range");
     std::lock_guard<std::mutex> lk(g_ws_mu[device]);
@@ -1632,6 +1733,43 @@ int prrtc_debug_fk(const prrtc_robot* robot, const double* q, uint32_t n, uint32
     cudaFree(df);
     cudaFree(dc);
     if (e != cudaSuccess) return set_err(PRRTC_ECUDA, std::string("prrtc_debug_fk: ") + cudaGetErrorString(e));
+    return PRRTC_OK;
+}
+
+int prrtc_debug_check_edges(const prrtc_robot* robot, const prrtc_scene* scene, const double* from,
+                            const double* to, uint32_t n_edges, uint32_t dof, int32_t n_cc, int two_stage,
+                            uint8_t* state_valid, float* fine_out) {
+    if (!robot || !scene || !state_valid || (n_edges && (!from || !to)))
+        return set_err(PRRTC_EINVAL, "prrtc_debug_check_edges: null argument");
+    if ((int)dof != robot->dof) return set_err(PRRTC_EINVAL, "validate_edge.from: expected dimension " + std::to_string(robot->dof));
+    if (n_cc < 1) return set_err(PRRTC_EINVAL, "validate_edge: resolution_count must be >= 1");
+    if (scene->device != robot->device) return set_err(PRRTC_EINVAL, "scene on another device");
+    if (n_edges == 0) return PRRTC_OK;
+    int rc = check_device(robot->device);
+    if (rc) return rc;
+    cudaSetDevice(robot->device);
+    double *df = nullptr, *dt = nullptr;
+    uint8_t* dv = nullptr;
+    float* dfo = nullptr;
+    const size_t ns = (size_t)n_edges * n_cc, nf = fine_out ? ns * robot->n_fine * 3 : 0;
+    if ((rc = dmalloc(&df, (size_t)n_edges * dof)) || (rc = dmalloc(&dt, (size_t)n_edges * dof)) ||
+        (rc = dmalloc(&dv, ns)) || (fine_out && (rc = dmalloc(&dfo, nf)))) {
+        cudaFree(df);
+        cudaFree(dt);
+        cudaFree(dv);
+        return rc;
+    }
+    cudaMemcpy(df, from, 8 * (size_t)n_edges * dof, cudaMemcpyHostToDevice);
+    cudaMemcpy(dt, to, 8 * (size_t)n_edges * dof, cudaMemcpyHostToDevice);
+    cudaError_t e = launch_debug_check_edges(robot->args(), scene->args(), df, dt, (int)n_edges, n_cc, two_stage, dv,
+                                             dfo, 0);
+    if (e == cudaSuccess) e = cudaMemcpy(state_valid, dv, ns, cudaMemcpyDeviceToHost);
+    if (e == cudaSuccess && fine_out) e = cudaMemcpy(fine_out, dfo, 4 * nf, cudaMemcpyDeviceToHost);
+    cudaFree(df);
+    cudaFree(dt);
+    cudaFree(dv);
+    cudaFree(dfo);
+    if (e != cudaSuccess) return set_err(PRRTC_ECUDA, std::string("prrtc_debug_check_edges: ") + cudaGetErrorString(e));
     return PRRTC_OK;
 }
 

@@ -307,9 +307,18 @@ struct Ctx {
     // counters): kept in shared memory so it does not occupy registers
     // (spilled around every call) in all threads of the CTA
     unsigned long long* t0;
+    // exact-CheckStats mode (deterministic planning): counters follow the
+    // reference's sequential semantics (ref_state_count); per-state scratch
+    int ref_stats;
+    unsigned long long* rcount;  // [NS] reference sphere_tests of each state
+    int* rfine;                  // [NS] 1 if the state enters the fine stage
 };
 
-enum : int { T0_TKBASE = 0, T0_TKPOS, T0_TKCNT, T0_USED, T0_LITER, T0_FK, T0_FINE, T0_COUNT = 8 };
+enum : int {
+    T0_TKBASE = 0, T0_TKPOS, T0_TKCNT, T0_USED, T0_LITER, T0_FK, T0_FINE,
+    T0_RTESTS,  // exact-CheckStats mode: reference-semantics sphere tests
+    T0_COUNT = 8
+};
 
 // The planner keeps its Ctx in shared memory (plan_kernel): every field is
 // CTA-uniform, so reads are broadcast LDS instead of local-memory loads that
@@ -661,8 +670,11 @@ struct ChunkV {
     int* sbad;
     int* sgroup;
     int* ictl;
+    int strict;  // exact-CheckStats mode: evaluate every state of the first bad group (see skip_state)
 };
-__device__ __forceinline__ ChunkV chunk_view(const Ctx& c) { return ChunkV{sh(c.sbad), sh(c.sgroup), sh(c.ictl)}; }
+__device__ __forceinline__ ChunkV chunk_view(const Ctx& c) {
+    return ChunkV{sh(c.sbad), sh(c.sgroup), sh(c.ictl), c.ref_stats};
+}
 
 __device__ __forceinline__ void mark_bad(const ChunkV& k, int s) {
     k.sbad[s] = 1;
@@ -672,10 +684,14 @@ __device__ __forceinline__ void mark_bad(const ChunkV& k, int s) {
 // skip test for early exit: chain mode skips groups >= first bad (a state
 // of a later or the same sub-edge cannot change the outcome); independent
 // mode skips states already known bad.
+// (In the exact-CheckStats mode only later groups are skipped, so the first
+// bad state of the first bad group is known: the reference's sequential
+// validation stops exactly there.)
 __device__ __forceinline__ bool skip_state(const ChunkV& k, int s, bool early_exit, bool indep) {
     if (!early_exit) return false;
     if (indep) return *(volatile int*)&k.sbad[s] != 0;
-    return k.sgroup[s] >= *(volatile int*)&k.ictl[IC_FIRSTBAD];
+    const int fb = *(volatile int*)&k.ictl[IC_FIRSTBAD];
+    return k.strict ? k.sgroup[s] > fb : k.sgroup[s] >= fb;
 }
 
 // i / n for i = 0..n (edge_sample's t, collision.cpp:19) tabulated once per
@@ -968,6 +984,158 @@ __device__ __forceinline__ void check_chunk_inl(Ctx& c, int cnt, bool two_stage,
 __device__ __noinline__ void check_chunk(Ctx& c, int cnt, bool two_stage, bool early_exit, bool indep,
                                          const int* stop_flag = nullptr) {
     check_chunk_inl(c, cnt, two_stage, early_exit, indep, stop_flag);
+}
+
+// ---------------------------------------------------------------------------
+// Exact CheckStats (collision.hpp:14-37): the reference's counters for one
+// checked state, from the chunk's poses and flag masks, following its
+// sequential order exactly — two-stage (collision.cpp:130-204): L x P coarse
+// tests + one per self pair; if anything flagged, a fine-stage entry and, per
+// flagged link in order, fine.n tests per flagging primitive in the order
+// spheres, capsules, boxes (fine_link_vs_flagged, collision.cpp:67-87), then
+// n_a x n_b per flagged pair (fine_pair_collides, :89-98), stopping at the
+// first collision when early_exit; brute force (:100-128): P per fine sphere,
+// stopping after the first colliding sphere when early_exit, then n_a x n_b
+// per self pair while nothing collided. Cylinders (an extension the reference
+// lacks) count as primitives after the boxes. One thread per state; only the
+// deterministic (single-CTA replay) mode calls it.
+// ---------------------------------------------------------------------------
+__device__ bool link_hits_prim(const Ctx& c, const SceneV& v, int l, int p, int s) {
+    const int4 inf = sh(c.info)[l];
+    const PoseR P = pose_load(sh(c.pose), c.NS, l, s);
+    const float4* fine = sh(c.fine);
+    for (int j = inf.w; j < inf.w + sh(c.nfine)[l]; ++j) {
+        const float4 f = fine[j];
+        if (fine_vs_prim(v, pose_apply(P, f.x, f.y, f.z), f.w, __ldg(c.fine_r64 + j), p)) return true;
+    }
+    return false;
+}
+
+__device__ bool pair_hits(const Ctx& c, const SceneV& v, int a, int b, int s) {
+    const int ja0 = sh(c.info)[a].w, jb0 = sh(c.info)[b].w, na = sh(c.nfine)[a], nb = sh(c.nfine)[b];
+    const PoseR PA = pose_load(sh(c.pose), c.NS, a, s), PB = pose_load(sh(c.pose), c.NS, b, s);
+    const float4* fine = sh(c.fine);
+    for (int i = 0; i < na; ++i) {
+        const float4 fa = fine[ja0 + i];
+        const float3 xa = pose_apply(PA, fa.x, fa.y, fa.z);
+        for (int q = 0; q < nb; ++q) {
+            const float4 fb = fine[jb0 + q];
+            if (fine_pair(v.eps, c.fine_r64, xa, fa.w, ja0 + i, pose_apply(PB, fb.x, fb.y, fb.z), fb.w, jb0 + q))
+                return true;
+        }
+    }
+    return false;
+}
+
+// The reference's coarse flag (kernels_detail.hpp:17-50 in FP64, no padding)
+// for link l vs primitive p on the device's posed coarse centre; the FP64
+// coarse radii follow the fine radii in fine_r64 (prrtc_robot_create).
+__device__ bool coarse_hits_exact(const Ctx& c, const SceneV& v, int l, int p, int s) {
+    const float* C = sh(c.ccen) + l * 3 * c.NS + s;
+    const double x = C[0], y = C[c.NS], z = C[2 * c.NS], r = __ldg(c.fine_r64 + c.S + l);
+    if (p < v.ns) {
+        const double* S = v.s64.s + 4 * p;
+        return sphere_sphere_exact(x, y, z, r, __ldg(S), __ldg(S + 1), __ldg(S + 2), __ldg(S + 3));
+    }
+    if (p < v.ns + v.nb) return sphere_box_exact(x, y, z, r, v.s64.b + BOX_STRIDE * (p - v.ns));
+    if (p < v.nsbc) return sphere_capsule_exact(x, y, z, r, v.s64.c + CAP_STRIDE * (p - v.ns - v.nb));
+    return sphere_cylinder_exact(x, y, z, r, v.s64.y + CYL_STRIDE * (p - v.nsbc));
+}
+
+__device__ bool coarse_pair_exact(const Ctx& c, int a, int b, int s) {  // collision.cpp:178-181
+    const int NS = c.NS;
+    const float* A = sh(c.ccen) + a * 3 * NS + s;
+    const float* B = sh(c.ccen) + b * 3 * NS + s;
+    const double dx = __dsub_rn(A[0], B[0]), dy = __dsub_rn(A[NS], B[NS]), dz = __dsub_rn(A[2 * NS], B[2 * NS]);
+    const double rr = __dadd_rn(__ldg(c.fine_r64 + c.S + a), __ldg(c.fine_r64 + c.S + b));
+    return __dadd_rn(__dadd_rn(__dmul_rn(dx, dx), __dmul_rn(dy, dy)), __dmul_rn(dz, dz)) < __dmul_rn(rr, rr);
+}
+
+__device__ __noinline__ unsigned long long ref_state_count(const Ctx& c, int s, bool two_stage, bool early_exit,
+                                                          int* fine_entry) {
+    const SceneV v = scene_view(c);
+    const int L = c.L, NP = c.NP, NS = c.NS;
+    const int2* pairs = sh(c.pairs);
+    const int* nfine = sh(c.nfine);
+    unsigned long long n = 0;
+    *fine_entry = 0;
+    if (!two_stage) {
+        bool hit = false;
+        for (int l = 0; l < L && !(hit && early_exit); ++l) {
+            const int j0 = sh(c.info)[l].w;
+            const PoseR P = pose_load(sh(c.pose), NS, l, s);
+            for (int j = j0; j < j0 + nfine[l]; ++j) {
+                n += (unsigned long long)v.P;
+                const float4 f = sh(c.fine)[j];
+                const float3 x = pose_apply(P, f.x, f.y, f.z);
+                bool h = false;
+                for (int p = 0; p < v.P && !h; ++p) h = fine_vs_prim(v, x, f.w, __ldg(c.fine_r64 + j), p);
+                if (h) {
+                    hit = true;
+                    if (early_exit) break;
+                }
+            }
+        }
+        for (int pr = 0; pr < NP && !(hit && early_exit); ++pr) {
+            const int2 ab = pairs[pr];
+            n += (unsigned long long)nfine[ab.x] * nfine[ab.y];
+            if (pair_hits(c, v, ab.x, ab.y, s)) hit = true;
+        }
+        return n;
+    }
+    n = (unsigned long long)L * v.P + NP;
+    const unsigned long long* lmask = sh(c.lmask);
+    const unsigned long long* pmask = sh(c.pmask);
+    // the device's coarse masks are padded (a superset): keep the flags the
+    // reference's unpadded FP64 coarse tests raise
+    bool any = false;
+    for (int l = 0; l < L && !any; ++l) {
+        unsigned long long m = lmask[l * NS + s];
+        while (m && !any) {
+            const int p = __ffsll((long long)m) - 1;
+            m &= m - 1;
+            any = coarse_hits_exact(c, v, l, p, s);
+        }
+    }
+    for (int pr = 0; pr < NP && !any; ++pr)
+        any = ((pmask[(pr >> 6) * NS + s] >> (pr & 63)) & 1ull) && coarse_pair_exact(c, pairs[pr].x, pairs[pr].y, s);
+    if (!any) return n;
+    *fine_entry = 1;
+    const int ns = v.ns, nb = v.nb, nsbc = v.nsbc;
+    // reference kind order: spheres [0, ns), capsules [ns + nb, nsbc), boxes [ns, ns + nb), then cylinders
+    const unsigned long long msph = ns >= 64 ? ~0ull : ((1ull << ns) - 1);
+    const unsigned long long mbox = (nb + ns >= 64 ? ~0ull : ((1ull << (ns + nb)) - 1)) & ~msph;
+    const unsigned long long mcap = (nsbc >= 64 ? ~0ull : ((1ull << nsbc) - 1)) & ~msph & ~mbox;
+    const unsigned long long mcyl = ~(msph | mbox | mcap);
+    for (int l = 0; l < L; ++l) {
+        const unsigned long long m = lmask[l * NS + s];
+        if (!m) continue;
+        // fine_link_vs_flagged returns at its first colliding primitive in
+        // either mode; early_exit then also ends the whole check
+        const unsigned long long order[4] = {m & msph, m & mcap, m & mbox, m & mcyl};
+        bool link_hit = false;
+        for (int k = 0; k < 4 && !link_hit; ++k) {
+            unsigned long long mm = order[k];
+            while (mm) {
+                const int p = __ffsll((long long)mm) - 1;
+                mm &= mm - 1;
+                if (!coarse_hits_exact(c, v, l, p, s)) continue;
+                n += (unsigned long long)nfine[l];
+                if (link_hits_prim(c, v, l, p, s)) {
+                    if (early_exit) return n;
+                    link_hit = true;
+                    break;
+                }
+            }
+        }
+    }
+    for (int pr = 0; pr < NP; ++pr) {
+        const int2 ab = pairs[pr];
+        if (!((pmask[(pr >> 6) * NS + s] >> (pr & 63)) & 1ull) || !coarse_pair_exact(c, ab.x, ab.y, s)) continue;
+        n += (unsigned long long)nfine[ab.x] * nfine[ab.y];
+        if (early_exit && pair_hits(c, v, ab.x, ab.y, s)) return n;
+    }
+    return n;
 }
 
 // ---------------------------------------------------------------------------

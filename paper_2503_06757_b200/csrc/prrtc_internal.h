@@ -159,6 +159,7 @@ struct PlanArgs {
     unsigned long long out_hdr_bytes;   // 128 + sizeof(ProbCtl) * n_problems
     unsigned* exit_count;               // CTAs finished (zeroed with the controls)
     int mnn_nodes;                      // multi-sample NN bound: m <= mnn_nodes / tree size
+    int ref_stats;                      // exact CheckStats (reference counting semantics): deterministic mode
 };
 
 // Dynamic shared memory bytes for a robot/scene/ns_max combination.

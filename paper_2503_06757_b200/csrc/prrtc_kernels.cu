@@ -30,7 +30,7 @@ using namespace dev;
 // ---------------------------------------------------------------------------
 struct SmemLayout {
     size_t robot, scene, pose, ccen, qf, sgroup, sbad, lmask, ictl, dcfg, red_d, red_i,
-        ends, ends_eq, ttab, sbuf, mnn, stat, htab, t0, total;
+        ends, ends_eq, ttab, sbuf, mnn, stat, htab, t0, rcount, rfine, total;
 };
 
 __host__ __device__ inline size_t al16(size_t x) { return (x + 15) & ~size_t(15); }
@@ -60,6 +60,8 @@ __host__ __device__ inline SmemLayout smem_layout(int robot_words, int L, int do
     s.stat = o;  o = al16(o + 16 * (size_t)nthreads);
     s.htab = o;  o = al16(o + 8 * (size_t)dof * (kHaltonTab + 2));  // + the [dof][2] limits
     s.t0 = o;    o = al16(o + 8 * (size_t)T0_COUNT);
+    s.rcount = o; o = al16(o + 8 * (size_t)NS);
+    s.rfine = o; o = al16(o + 4 * (size_t)NS);
     s.total = o;
     return s;
 }
@@ -129,6 +131,9 @@ __device__ void setup_ctx(Ctx& c, unsigned char* smem, const uint32_t* robot_g, 
         c.mnn_ok = reinterpret_cast<int*>(smem + lay.mnn + 12 * 32);
         c.stat = stat;
         c.t0 = reinterpret_cast<unsigned long long*>(smem + lay.t0);
+        c.ref_stats = 0;  // the planner turns it on in deterministic mode
+        c.rcount = reinterpret_cast<unsigned long long*>(smem + lay.rcount);
+        c.rfine = reinterpret_cast<int*>(smem + lay.rfine);
         c.ttab_n = 0;
         c.nslog = 31 - __clz(NS);
         c.mflog = c.MF > 1 ? 32 - __clz(c.MF - 1) : 0;
@@ -309,6 +314,39 @@ __device__ int tree_append_many(Ctx& c, const PlanArgs& a, const TreeRef& T, con
     return ok;
 }
 
+// Exact-CheckStats mode (deterministic planning): the reference validates the
+// chain's states one by one and stops at the first collision (early_exit) or
+// at the end of the first invalid sub-edge (collision.cpp:206-224,
+// planner.cpp:111-117), so it counts exactly the states up to there; each
+// state's counters follow ref_state_count. Every state of the first bad
+// group was evaluated (skip_state is strict in this mode).
+__device__ __noinline__ void ref_count_chain_chunk(Ctx& c, int cnt, bool two_stage, bool early_exit, int fb) {
+    const int* sgroup = sh(c.sgroup);
+    for (int s = threadIdx.x; s < cnt; s += c.nthreads) {
+        int fe = 0;
+        const bool counted = sgroup[s] >= 0 && (fb == kNoBad || sgroup[s] <= fb);
+        sh(c.rcount)[s] = counted ? ref_state_count(c, s, two_stage, early_exit, &fe) : 0ull;
+        sh(c.rfine)[s] = fe;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        unsigned long long tests = 0, fk = 0, fine = 0;
+        for (int s = 0; s < cnt; ++s) {
+            if (sgroup[s] < 0) continue;
+            if (fb != kNoBad && sgroup[s] > fb) break;
+            tests += sh(c.rcount)[s];
+            fine += sh(c.rfine)[s];
+            ++fk;
+            if (early_exit && sh(c.sbad)[s]) break;
+        }
+        unsigned long long* t0 = sh(c.t0);
+        t0[T0_RTESTS] += tests;
+        t0[T0_FK] += fk;
+        t0[T0_FINE] += fine;
+    }
+    __syncthreads();
+}
+
 // ---------------------------------------------------------------------------
 // chain validation with appends (extend: n_sub = 1; greedy connect:
 // planner.cpp:66-123). Sub-edges are validated chunk by chunk (NS states of
@@ -337,7 +375,7 @@ __device__ long long validate_chain(Ctx& c, const PlanArgs& a, const double* A, 
             return 0;
         }
         if (threadIdx.x == 0) {
-            sh(c.t0)[T0_FK] += act;
+            if (!c.ref_stats) sh(c.t0)[T0_FK] += act;
             sh(c.stat)[1] += (unsigned long long)act * c.fkflops;  // thread 0's flop slot
         }
         trace_phase(a, 5);  // FK + collision
@@ -347,10 +385,11 @@ __device__ long long validate_chain(Ctx& c, const PlanArgs& a, const double* A, 
             *stopped = true;
             return 0;
         }
-        if (threadIdx.x == 0 && sh(c.ictl)[IC_QN]) ++sh(c.t0)[T0_FINE];
+        if (threadIdx.x == 0 && sh(c.ictl)[IC_QN] && !c.ref_stats) ++sh(c.t0)[T0_FINE];
         // (IC_FIRSTBAD is next reset inside the next chunk's FK, after the
         // state-generation barrier: every thread has read it by then)
         const int fb = sh(c.ictl)[IC_FIRSTBAD];
+        if (c.ref_stats) ref_count_chain_chunk(c, cnt, a.p.two_stage != 0, a.p.early_exit != 0, fb);
         good = (fb != kNoBad) ? (long long)fb : (g0 + cnt) / n_cc;
         if (fb != kNoBad) break;
     }
@@ -542,8 +581,14 @@ __device__ bool init_problem(Ctx& c, const PlanArgs& a, int prob) {
     }
     __syncthreads();
     check_chunk(c, 2, a.p.two_stage != 0, a.p.early_exit != 0, true);
+    if (c.ref_stats && tid < 2) {  // exact-CheckStats mode: the two endpoint checks (planner.cpp:263-277)
+        int fe = 0;
+        sh(c.rcount)[tid] = ref_state_count(c, tid, a.p.two_stage != 0, a.p.early_exit != 0, &fe);
+        sh(c.rfine)[tid] = fe;
+    }
+    __syncthreads();
     if (tid == 0) {
-        sh(c.t0)[T0_FK] += 2;
+        if (!c.ref_stats) sh(c.t0)[T0_FK] += 2;
         sh(c.stat)[1] += 2ull * c.fkflops;  // thread 0's flop slot
         // within_limits (planner.cpp:25-31): inclusive bounds
         bool sl = true, gl = true;
@@ -559,6 +604,14 @@ __device__ bool init_problem(Ctx& c, const PlanArgs& a, int prob) {
             bool eq = true;
             for (int d = 0; d < dof; ++d) eq &= (S[d] == G[d]);
             if (eq) verdict = 3;
+        }
+        if (c.ref_stats && (verdict == 0 || verdict == 3)) {
+            // the reference reports the endpoint checks' counters only when
+            // both endpoints are feasible (planner.cpp:263-285, :308-311)
+            unsigned long long* t0 = sh(c.t0);
+            t0[T0_RTESTS] += sh(c.rcount)[0] + sh(c.rcount)[1];
+            t0[T0_FK] += 2;
+            t0[T0_FINE] += sh(c.rfine)[0] + sh(c.rfine)[1];
         }
         sh(c.ictl)[IC_TMP5] = verdict;
     }
@@ -688,14 +741,16 @@ __device__ void flush_stats(Ctx& c, ProbCtl& C) {
         tests += __shfl_xor_sync(0xffffffffu, tests, o);
         flops += __shfl_xor_sync(0xffffffffu, flops, o);
     }
-    if ((threadIdx.x & 31) == 0 && tests) atomicAdd(&C.sphere_tests, tests);
+    if ((threadIdx.x & 31) == 0 && tests && !c.ref_stats) atomicAdd(&C.sphere_tests, tests);
     if ((threadIdx.x & 31) == 0 && flops) atomicAdd(&C.flops, flops);
     if (threadIdx.x == 0) {
         unsigned long long* t0 = sh(c.t0);
         if (t0[T0_FK]) atomicAdd(&C.fk_calls, t0[T0_FK]);
         if (t0[T0_FINE]) atomicAdd(&C.fine_entries, t0[T0_FINE]);
+        if (t0[T0_RTESTS]) atomicAdd(&C.sphere_tests, t0[T0_RTESTS]);
         t0[T0_FK] = 0;
         t0[T0_FINE] = 0;
+        t0[T0_RTESTS] = 0;
     }
 }
 
@@ -759,6 +814,8 @@ __global__ void __launch_bounds__(NT, MINB) plan_kernel(PlanArgs a) {
     const int robot_words = reinterpret_cast<const int*>(a.robot)[RH_WORDS];
     unsigned char* sbase = scene_base(smem, robot_words, c.L, dof, c.NS, c.nthreads);
     build_ttab(c, a.p.n_cc);
+    if (tid == 0) c.ref_stats = a.ref_stats;
+    __syncthreads();
     const double R = a.p.dd_radius, delta = a.p.delta;
     if (tid == 0 && a.trace) atomicMax(&a.trace[0], 0x7fffffffffffffffull - (unsigned long long)globaltimer());
     if (tid == 0 && a.cta_trace) {
@@ -1274,6 +1331,51 @@ __global__ void __launch_bounds__(128) validate_edges_kernel(RobotArgs r, SceneA
     }
 }
 
+// Edge-level parity hook: every sample of every edge checked (no early exit,
+// independent states), per-state verdicts and posed fine spheres written out.
+__global__ void __launch_bounds__(128) debug_check_edges_kernel(RobotArgs r, SceneArgs sa, const double* from,
+                                                                 const double* to, int n_edges, int n_cc,
+                                                                 int two_stage, uint8_t* state_valid,
+                                                                 float* fine_out, int NS) {
+    extern __shared__ __align__(16) unsigned char smem[];
+    Ctx c;
+    setup_ctx(c, smem, r.words, r.n_words, r.fine_r64, r.limits, NS);
+    load_scene(c, scene_base(smem, r.n_words, c.L, c.dof, NS, c.nthreads), sa.words, sa.f64);
+    build_ttab(c, n_cc);
+    const double* tt = n_cc == c.ttab_n ? sh(c.ttab) : nullptr;
+    for (int e = blockIdx.x; e < n_edges; e += gridDim.x) {
+        const double* A = from + (size_t)e * c.dof;
+        const double* B = to + (size_t)e * c.dof;
+        for (int g0 = 0; g0 < n_cc; g0 += NS) {
+            const int cnt = min(NS, n_cc - g0);
+            for (int idx = threadIdx.x; idx < c.dof * NS; idx += c.nthreads) {
+                const int d = idx / NS, s = idx - d * NS;
+                const int i = g0 + s + 1;
+                if (d == 0) sh(c.sgroup)[s] = s < cnt ? 0 : -1;
+                if (s >= cnt) continue;
+                sh(c.qf)[idx] = i == n_cc ? (float)B[d]
+                                          : (float)lerp_exact(A[d], B[d], tt ? tt[i] : frac_div(i, n_cc));
+            }
+            __syncthreads();
+            check_chunk(c, cnt, two_stage != 0, false, true);
+            for (int s = threadIdx.x; s < cnt; s += c.nthreads)
+                state_valid[(size_t)e * n_cc + g0 + s] = sh(c.sbad)[s] ? 0 : 1;
+            if (fine_out) {
+                for (int it = threadIdx.x; it < cnt * c.S; it += c.nthreads) {
+                    const int s = it % cnt, j = it / cnt;
+                    const float4 f = c.fine[j];
+                    const float3 x = pose_point(c, c.flink[j], s, f.x, f.y, f.z);
+                    float* o = fine_out + (((size_t)e * n_cc + g0 + s) * c.S + j) * 3;
+                    o[0] = x.x;
+                    o[1] = x.y;
+                    o[2] = x.z;
+                }
+            }
+            __syncthreads();
+        }
+    }
+}
+
 __global__ void __launch_bounds__(128) debug_fk_kernel(RobotArgs r, const double* q, int n, float* fine_out,
                                                         float* coarse_out, int NS) {
     extern __shared__ __align__(16) unsigned char smem[];
@@ -1535,6 +1637,20 @@ cudaError_t launch_validate_edges(const RobotArgs& r, const SceneArgs& s, const 
     if (grid > 0)
         validate_edges_kernel<<<grid, 128, sm, st>>>(r, s, from, to, n_edges, n_cc, two_stage,
                                                      early_exit, out, NS, prof, counters);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_debug_check_edges(const RobotArgs& r, const SceneArgs& s, const double* from,
+                                     const double* to, int n_edges, int n_cc, int two_stage,
+                                     uint8_t* state_valid, float* fine_out, cudaStream_t st) {
+    const int NS = chunk_states();
+    const size_t sm = smem_bytes(r, NS, 128);
+    cudaError_t e = raise_smem_limit(reinterpret_cast<const void*>(debug_check_edges_kernel), (int)sm);
+    if (e != cudaSuccess) return e;
+    const int grid = (int)min((long long)n_edges, (long long)cur_sms() * 8);
+    if (grid > 0)
+        debug_check_edges_kernel<<<grid, 128, sm, st>>>(r, s, from, to, n_edges, n_cc, two_stage, state_valid,
+                                                        fine_out, NS);
     return cudaGetLastError();
 }
 

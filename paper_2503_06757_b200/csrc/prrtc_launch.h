@@ -39,6 +39,9 @@ cudaError_t launch_validate_edges(const RobotArgs& r, const SceneArgs& s, const 
                                   const double* to, int n_edges, int n_cc, int two_stage,
                                   int early_exit, uint8_t* out, cudaStream_t st,
                                   long long* prof = nullptr, unsigned long long* counters = nullptr);
+cudaError_t launch_debug_check_edges(const RobotArgs& r, const SceneArgs& s, const double* from,
+                                     const double* to, int n_edges, int n_cc, int two_stage,
+                                     uint8_t* state_valid, float* fine_out, cudaStream_t st);
 cudaError_t launch_debug_fk(const RobotArgs& r, const double* q, int n, float* fine_out,
                             float* coarse_out, cudaStream_t st);
 cudaError_t launch_debug_hits(const SceneArgs& s, const float* centers, const double* radii,

@@ -7,6 +7,7 @@
 // back into PlanResult. Errors map back to the reference's exceptions.
 #include "prrtc_dropin.hpp"
 
+#include <atomic>
 #include <cstring>
 #include <map>
 #include <mutex>
@@ -20,8 +21,22 @@
 namespace prrtc::b200 {
 namespace {
 
-std::mutex g_mu;
-int g_device = 0;
+// Concurrency (the reference's plan() is safe to call from many threads,
+// planner.cpp:246-322): the handle caches are guarded per device and only
+// while a handle is looked up or created; the plan call itself runs
+// unlocked (the C-ABI serialises calls per device on its workspace), so one
+// host thread per GPU plans in parallel. The device is the calling thread's
+// choice (set_thread_device) or else the process default (set_device).
+constexpr int kMaxDev = 64;
+std::mutex g_cache_mu[kMaxDev];
+std::atomic<int> g_default_device{0};
+thread_local int t_device = -1;
+
+int current_device() {
+    const int d = t_device >= 0 ? t_device : g_default_device.load(std::memory_order_relaxed);
+    if (d < 0 || d >= kMaxDev) throw std::invalid_argument("prrtc_b200: device ordinal out of range");
+    return d;
+}
 
 std::string last_error() {
     char buf[512];
@@ -108,9 +123,10 @@ struct SceneEntry {
 std::map<std::pair<const RobotModel*, int>, RobotEntry> g_robots;
 std::map<std::pair<const Scene*, int>, SceneEntry> g_scenes;
 
-prrtc_robot* robot_handle(const RobotModel& m) {
+// (caller holds g_cache_mu[device])
+prrtc_robot* robot_handle(const RobotModel& m, int device) {
     const uint64_t fp = fingerprint(m);
-    auto key = std::make_pair(&m, g_device);
+    auto key = std::make_pair(&m, device);
     auto it = g_robots.find(key);
     if (it != g_robots.end() && it->second.fp == fp) return it->second.h;
     const size_t L = m.joints.size();
@@ -161,17 +177,18 @@ prrtc_robot* robot_handle(const RobotModel& m) {
     d.n_self_pairs = static_cast<uint32_t>(m.self_pairs.size());
     d.self_pairs = pairs.data();
     prrtc_robot* h = nullptr;
-    const int rc = prrtc_robot_create(&d, g_device, &h);
+    const int rc = prrtc_robot_create(&d, device, &h);
     if (rc) raise(rc);
     if (it != g_robots.end()) prrtc_robot_destroy(it->second.h);
     g_robots[key] = {fp, h};
     return h;
 }
 
-prrtc_scene* scene_handle(const Scene& s) {
+// (caller holds g_cache_mu[device])
+prrtc_scene* scene_handle(const Scene& s, int device) {
     const SceneFlat f = flatten(s);
     const uint64_t fp = fingerprint(f);
-    auto key = std::make_pair(&s, g_device);
+    auto key = std::make_pair(&s, device);
     auto it = g_scenes.find(key);
     if (it != g_scenes.end() && it->second.fp == fp) return it->second.h;
     prrtc_scene_desc d{};
@@ -189,7 +206,7 @@ prrtc_scene* scene_handle(const Scene& s) {
         it->second.fp = fp;
         return it->second.h;
     }
-    rc = prrtc_scene_create(&d, g_device, &h);
+    rc = prrtc_scene_create(&d, device, &h);
     if (rc) raise(rc);
     g_scenes[key] = {fp, h};
     return h;
@@ -237,25 +254,49 @@ PlanResult from_c(prrtc_result& r) {
 }  // namespace
 
 void set_device(int device) {
-    std::lock_guard<std::mutex> lk(g_mu);
-    g_device = device;
+    if (device < 0 || device >= kMaxDev) throw std::invalid_argument("prrtc_b200: device ordinal out of range");
+    g_default_device.store(device, std::memory_order_relaxed);
+}
+
+void set_thread_device(int device) {
+    if (device >= kMaxDev) throw std::invalid_argument("prrtc_b200: device ordinal out of range");
+    t_device = device;
 }
 
 void clear_cache() {
-    std::lock_guard<std::mutex> lk(g_mu);
-    for (auto& kv : g_robots) prrtc_robot_destroy(kv.second.h);
-    for (auto& kv : g_scenes) prrtc_scene_destroy(kv.second.h);
-    g_robots.clear();
-    g_scenes.clear();
+    for (int d = 0; d < kMaxDev; ++d) {
+        std::lock_guard<std::mutex> lk(g_cache_mu[d]);
+        for (auto it = g_robots.begin(); it != g_robots.end();) {
+            if (it->first.second == d) {
+                prrtc_robot_destroy(it->second.h);
+                it = g_robots.erase(it);
+            } else {
+                ++it;
+            }
+        }
+        for (auto it = g_scenes.begin(); it != g_scenes.end();) {
+            if (it->first.second == d) {
+                prrtc_scene_destroy(it->second.h);
+                it = g_scenes.erase(it);
+            } else {
+                ++it;
+            }
+        }
+    }
 }
 
 PlanResult plan(const RobotModel& model, const Scene& scene, ConfigView start, ConfigView goal,
                 const PlannerParams& params) {
     require_dim(start, static_cast<size_t>(model.dof), "plan.start");  // planner.cpp:248-249
     require_dim(goal, static_cast<size_t>(model.dof), "plan.goal");
-    std::lock_guard<std::mutex> lk(g_mu);
-    prrtc_robot* r = robot_handle(model);
-    prrtc_scene* s = scene_handle(scene);
+    const int dev = current_device();
+    prrtc_robot* r;
+    prrtc_scene* s;
+    {
+        std::lock_guard<std::mutex> lk(g_cache_mu[dev]);
+        r = robot_handle(model, dev);
+        s = scene_handle(scene, dev);
+    }
     const prrtc_params p = to_c(params);
     prrtc_result res{};
     const int rc = prrtc_plan(r, s, start.data(), goal.data(), static_cast<uint32_t>(start.size()), &p, &res);
@@ -263,26 +304,64 @@ PlanResult plan(const RobotModel& model, const Scene& scene, ConfigView start, C
     return from_c(res);
 }
 
-std::vector<PlanResult> plan_batch(const RobotModel& model, const std::vector<const Scene*>& scenes,
-                                   const std::vector<Config>& starts, const std::vector<Config>& goals,
-                                   const PlannerParams& params) {
+namespace {
+void flatten_inputs(const RobotModel& model, const std::vector<const Scene*>& scenes,
+                    const std::vector<Config>& starts, const std::vector<Config>& goals, std::vector<double>& S,
+                    std::vector<double>& G) {
     if (scenes.size() != starts.size() || starts.size() != goals.size())
         throw std::invalid_argument("plan_batch: scenes, starts and goals must have the same length");
-    std::lock_guard<std::mutex> lk(g_mu);
-    prrtc_robot* r = robot_handle(model);
-    std::vector<const prrtc_scene*> sh;
-    std::vector<double> S, G;
     for (size_t i = 0; i < scenes.size(); ++i) {
         require_dim(starts[i], static_cast<size_t>(model.dof), "plan.start");
         require_dim(goals[i], static_cast<size_t>(model.dof), "plan.goal");
-        sh.push_back(scene_handle(*scenes[i]));
         S.insert(S.end(), starts[i].begin(), starts[i].end());
         G.insert(G.end(), goals[i].begin(), goals[i].end());
+    }
+}
+}  // namespace
+
+std::vector<PlanResult> plan_batch(const RobotModel& model, const std::vector<const Scene*>& scenes,
+                                   const std::vector<Config>& starts, const std::vector<Config>& goals,
+                                   const PlannerParams& params) {
+    std::vector<double> S, G;
+    flatten_inputs(model, scenes, starts, goals, S, G);
+    const int dev = current_device();
+    prrtc_robot* r;
+    std::vector<const prrtc_scene*> sh;
+    {
+        std::lock_guard<std::mutex> lk(g_cache_mu[dev]);
+        r = robot_handle(model, dev);
+        for (const Scene* sc : scenes) sh.push_back(scene_handle(*sc, dev));
     }
     const prrtc_params p = to_c(params);
     std::vector<prrtc_result> res(scenes.size());
     const int rc = prrtc_plan_batch(r, sh.data(), static_cast<uint32_t>(sh.size()), S.data(), G.data(),
                                     static_cast<uint32_t>(model.dof), &p, res.data());
+    if (rc) raise(rc);
+    std::vector<PlanResult> out;
+    for (auto& x : res) out.push_back(from_c(x));
+    return out;
+}
+
+std::vector<PlanResult> plan_batch(const RobotModel& model, const std::vector<const Scene*>& scenes,
+                                   const std::vector<Config>& starts, const std::vector<Config>& goals,
+                                   const PlannerParams& params, const std::vector<int>& devices,
+                                   uint32_t chunk) {
+    if (devices.empty()) throw std::invalid_argument("plan_batch: no devices");
+    std::vector<double> S, G;
+    flatten_inputs(model, scenes, starts, goals, S, G);
+    std::vector<const prrtc_robot*> rs;
+    std::vector<const prrtc_scene*> sh;
+    for (int dev : devices) {
+        if (dev < 0 || dev >= kMaxDev) throw std::invalid_argument("prrtc_b200: device ordinal out of range");
+        std::lock_guard<std::mutex> lk(g_cache_mu[dev]);
+        rs.push_back(robot_handle(model, dev));
+        for (const Scene* sc : scenes) sh.push_back(scene_handle(*sc, dev));
+    }
+    const prrtc_params p = to_c(params);
+    std::vector<prrtc_result> res(scenes.size());
+    const int rc = prrtc_plan_batch_multi(rs.data(), sh.data(), static_cast<uint32_t>(devices.size()),
+                                          static_cast<uint32_t>(scenes.size()), S.data(), G.data(),
+                                          static_cast<uint32_t>(model.dof), &p, chunk, res.data());
     if (rc) raise(rc);
     std::vector<PlanResult> out;
     for (auto& x : res) out.push_back(from_c(x));

@@ -17,7 +17,8 @@ namespace prrtc::b200 {
 // Drop-in for prrtc::plan. Throws std::invalid_argument exactly where the
 // reference does (types.hpp:16-21, planner.cpp:248-252, RobotModel::finalize
 // invariants); std::runtime_error if no sm_100 device is usable (there is no
-// CPU fallback). `params.workers` = CTAs on the problem (0 = 2 per SM).
+// CPU fallback). `params.workers` = CTAs on the problem (0 = one per SM).
+// Safe to call concurrently from several threads (like the reference).
 PlanResult plan(const RobotModel& model, const Scene& scene, ConfigView start, ConfigView goal,
                 const PlannerParams& params);
 
@@ -27,8 +28,18 @@ std::vector<PlanResult> plan_batch(const RobotModel& model, const std::vector<co
                                    const std::vector<Config>& starts, const std::vector<Config>& goals,
                                    const PlannerParams& params);
 
-// CUDA device the drop-in plans on (default 0).
+// The same problems spread over several devices (prrtc_plan_batch_multi: one
+// host thread per device, a shared chunk queue; chunk 0 = automatic).
+std::vector<PlanResult> plan_batch(const RobotModel& model, const std::vector<const Scene*>& scenes,
+                                   const std::vector<Config>& starts, const std::vector<Config>& goals,
+                                   const PlannerParams& params, const std::vector<int>& devices,
+                                   uint32_t chunk = 0);
+
+// CUDA device the drop-in plans on: the process default (initially 0) ...
 void set_device(int device);
+// ... unless the calling thread chose its own (-1 = back to the default):
+// one host thread per GPU, each planning concurrently on its device.
+void set_thread_device(int device);
 
 // Drops the cached device copies of robots and scenes.
 void clear_cache();

@@ -271,6 +271,57 @@ def plan_batch_arrays(model, scenes, starts, goals, params: PlannerParams | None
     return out
 
 
+def plan_batch_multi(model, scenes, starts, goals, params: PlannerParams | None = None,
+                     devices: Sequence[int] | None = None, chunk: int = 0) -> BatchResult:
+    """prrtc_plan_batch_multi: the problems spread over several devices (one
+    host thread per device, a shared chunk queue, no collective; SURVEY.md
+    §8e). devices = None uses every visible sm_100 device. Robot and scene
+    handles are uploaded to each device (setup, cached)."""
+    params = params or PlannerParams()
+    devices = list(range(device_count())) if devices is None else list(devices)
+    if not devices:
+        raise RuntimeError("plan_batch_multi: no sm_100 device")
+    robs = [device_robot(model, d) for d in devices]
+    dof = robs[0].dof
+    S = np.ascontiguousarray(np.asarray(starts, dtype=np.float64).reshape(-1, dof))
+    G = np.ascontiguousarray(np.asarray(goals, dtype=np.float64).reshape(-1, dof))
+    n = S.shape[0]
+    src = scenes.hs if isinstance(scenes, SceneSet) else scenes
+    if isinstance(src, (Scene, DeviceScene)):
+        src = [src] * n
+    if len(src) != n:
+        raise ValueError("plan_batch: one scene per problem required")
+    keep, handles = [], []
+    for d in devices:  # per-device handles (a handle of another device is re-uploaded from its Scene)
+        hs = [x if isinstance(x, DeviceScene) and x.device == d
+              else device_scene(x.scene if isinstance(x, DeviceScene) else x, d) for x in src]
+        keep.append(hs)
+        handles.extend(h.h.value for h in hs)
+    rarr = (C.c_void_p * len(devices))(*[r.h.value for r in robs])
+    sarr = (C.c_void_p * len(handles))(*handles)
+    p = params.to_c()
+    res = (Result * n)()
+    check(_lib.load().prrtc_plan_batch_multi(rarr, sarr, len(devices), n, _dptr(S), _dptr(G), dof, C.byref(p),
+                                             chunk, res))
+    out = BatchResult(res, n, dof)
+    _free(res, n)
+    return out
+
+
+def debug_chunk_queue(n_workers: int, n: int, chunk: int = 0, delay_us=None):
+    """The multi-device chunk queue without devices: (owner[n], chunks_taken[n_workers])."""
+    owner = np.zeros(n, dtype=np.int32)
+    taken = np.zeros(n_workers, dtype=np.uint32)
+    dl = None
+    if delay_us is not None:
+        dl = np.ascontiguousarray(np.asarray(delay_us, dtype=np.uint32))
+    check(_lib.load().prrtc_debug_chunk_queue(n_workers, n, chunk,
+                                              dl.ctypes.data_as(C.POINTER(C.c_uint32)) if dl is not None else None,
+                                              owner.ctypes.data_as(C.POINTER(C.c_int32)),
+                                              taken.ctypes.data_as(C.POINTER(C.c_uint32))))
+    return owner, taken
+
+
 class Batch:
     """Device-resident batch: inputs uploaded once (prrtc_batch_create), then
     solved repeatedly with launch(); results() copies the outcome back."""
@@ -351,6 +402,22 @@ def debug_fk(model, q, device: int = 0):
     check(_lib.load().prrtc_debug_fk(rob.h, _dptr(Q), n, rob.dof, fine.ctypes.data_as(FPT),
                                      coarse.ctypes.data_as(FPT)))
     return fine, coarse
+
+
+def debug_check_edges(model, scene, frm, to, n_cc: int = 32, two_stage: bool = True, device: int = 0):
+    """Per-state device verdicts [n_edges, n_cc] (no early exit) and the posed
+    fine spheres [n_edges, n_cc, S, 3] (FP32) the device's checks used."""
+    rob = device_robot(model, device)
+    scn = device_scene(scene, device)
+    F = np.ascontiguousarray(np.asarray(frm, dtype=np.float64).reshape(-1, rob.dof))
+    T = np.ascontiguousarray(np.asarray(to, dtype=np.float64).reshape(-1, rob.dof))
+    n = F.shape[0]
+    valid = np.zeros((n, n_cc), dtype=np.uint8)
+    fine = np.zeros((n, n_cc, rob.fine_count, 3), dtype=np.float32)
+    check(_lib.load().prrtc_debug_check_edges(rob.h, scn.h, _dptr(F), _dptr(T), n, rob.dof, n_cc, int(two_stage),
+                                              valid.ctypes.data_as(C.POINTER(C.c_uint8)),
+                                              fine.ctypes.data_as(C.POINTER(C.c_float))))
+    return valid.astype(bool), fine
 
 
 def debug_sphere_hits(scene, centers, radii, device: int = 0) -> np.ndarray:

@@ -17,6 +17,8 @@
 #include <fstream>
 #include <iostream>
 #include <string>
+#include <thread>
+#include <vector>
 
 #include "prrtc/planner.hpp"
 #include "prrtc_dropin.hpp"
@@ -76,6 +78,9 @@ int main(int argc, char** argv) {
     b200p.workers = argc > 2 ? static_cast<unsigned>(std::stoul(argv[2])) : 0;
     PlannerParams cpup;
     cpup.workers = 1;
+    std::vector<Scene> scenes;
+    std::vector<Config> starts, goals;
+    scenes.reserve(N);
     for (size_t i = 0; i < N; ++i) {
         Scene sc;
         sc.name = "scene";
@@ -109,6 +114,40 @@ int main(int argc, char** argv) {
         PlanResult rc = prrtc::plan(m, sc, s, g, cpup);
         double ms_c = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
         print_result("reference", static_cast<int>(i), rc, ms_c);
+        scenes.push_back(sc);
+        starts.push_back(s);
+        goals.push_back(g);
+    }
+    // concurrent callers (the reference's plan() is safe to call from many
+    // threads): 4 host threads plan all problems at once on the thread's device
+    {
+        std::vector<int> st(N, -1);
+        std::vector<std::thread> th;
+        for (int t = 0; t < 4; ++t)
+            th.emplace_back([&, t] {
+                b200::set_thread_device(0);
+                for (size_t i = t; i < N; i += 4) {
+                    PlanResult r = b200::plan(m, scenes[i], starts[i], goals[i], b200p);
+                    const bool ends = r.path.empty() || (r.path.front() == starts[i] && r.path.back() == goals[i]);
+                    st[i] = ends ? static_cast<int>(r.status) : 9;
+                }
+            });
+        for (auto& x : th) x.join();
+        std::printf("{\"concurrent\": [");
+        for (size_t i = 0; i < N; ++i) std::printf("%s%d", i ? ", " : "", st[i]);
+        std::printf("]}\n");
+    }
+    // the multi-device batch entry on the visible device(s)
+    {
+        std::vector<const Scene*> sp;
+        for (auto& sc : scenes) sp.push_back(&sc);
+        std::vector<PlanResult> rs = b200::plan_batch(m, sp, starts, goals, b200p, std::vector<int>{0}, 2);
+        std::printf("{\"multi\": [");
+        for (size_t i = 0; i < rs.size(); ++i) {
+            const bool ends = rs[i].path.empty() || (rs[i].path.front() == starts[i] && rs[i].path.back() == goals[i]);
+            std::printf("%s%d", i ? ", " : "", ends ? static_cast<int>(rs[i].status) : 9);
+        }
+        std::printf("]}\n");
     }
     // the reference's error behaviour: a dimension mismatch throws std::invalid_argument
     try {

@@ -68,6 +68,12 @@ def test_dropin_matches_reference_contract(gpu, oracle, tmp_path):
     assert r.returncode == 0, r.stderr
     lines = [json.loads(x) for x in r.stdout.strip().splitlines()]
     assert lines[-1]["invalid_argument"] and "expected dimension" in lines[-1]["what"]
+    # 4 concurrent host threads and the multi-device batch: every problem
+    # answered (Solved / Failed), solved paths run start -> goal (9 = not)
+    conc = next(x["concurrent"] for x in lines if "concurrent" in x)
+    multi = next(x["multi"] for x in lines if "multi" in x)
+    assert len(conc) == len(multi) == len(items)
+    assert all(v in (0, 1) for v in conc + multi)
     b200 = [x for x in lines if x.get("impl") == "b200"]
     ref = [x for x in lines if x.get("impl") == "reference"]
     assert len(b200) == len(ref) == len(items)

@@ -161,6 +161,54 @@ def test_validate_edges_matches_oracle(gpu, oracle, robot):
         assert np.mean(ref == base) >= 0.98, (kind, pid)
 
 
+def ref_state_verdicts(oracle, model, scene, fine):
+    """Reference predicates (sphere_vs_primitive, geometry.cpp:41-66, and the
+    self-pair sphere test, kernels_detail.hpp:17-23 in its FP64 operation
+    order) on given posed fine spheres: fine [n, S, 3] -> valid [n]."""
+    r = fine_radii(model)
+    n, S = fine.shape[:2]
+    X = np.concatenate([fine.reshape(-1, 3).astype(np.float64), np.tile(r, n)[:, None]], axis=1)
+    env = oracle.sphere_any_hits(scene, X).reshape(n, S).any(axis=1)
+    off = np.concatenate([[0], np.cumsum([len(ls.fine) for ls in model.spheres])])
+    selfhit = np.zeros(n, dtype=bool)
+    P = fine.astype(np.float64)
+    for a, b in model.self_pairs:
+        A, B = P[:, off[a]:off[a + 1]], P[:, off[b]:off[b + 1]]
+        ra, rb = r[off[a]:off[a + 1]], r[off[b]:off[b + 1]]
+        dx = A[:, :, None, 0] - B[:, None, :, 0]
+        dy = A[:, :, None, 1] - B[:, None, :, 1]
+        dz = A[:, :, None, 2] - B[:, None, :, 2]
+        d2 = (dx * dx + dy * dy) + dz * dz
+        rr = ra[:, None] + rb[None, :]
+        selfhit |= (d2 < rr * rr).any(axis=(1, 2))
+    return ~(env | selfhit)
+
+
+@pytest.mark.parametrize("robot", ROBOTS)
+def test_check_edges_bitexact_on_device_spheres(gpu, oracle, robot):
+    """prrtc_debug_check_edges: every state's device verdict
+    equals the reference predicates evaluated on the device's own posed
+    spheres (bit-exact, two-stage and brute force), and the AND over an
+    edge's states is prrtc_validate_edges' verdict."""
+    m = robots.get(robot)
+    rng = np.random.default_rng(17)
+    lim = m.limits()
+    for kind, pid, s, g in load_problems(robot, 1000)[::200]:
+        scene, _ = make_scene(robot, kind, pid)
+        frm = np.repeat(s[None], 24, 0)
+        d = rng.normal(size=(24, m.dof))
+        d /= np.linalg.norm(d, axis=1, keepdims=True)
+        to = np.clip(frm + d * rng.uniform(0.1, 1.5, (24, 1)), lim[:, 0], lim[:, 1])
+        to[0] = frm[0]
+        for two_stage in (True, False):
+            valid, fine = planner.debug_check_edges(m, scene, frm, to, 32, two_stage)
+            ref = ref_state_verdicts(oracle, m, scene, fine.reshape(-1, fine.shape[2], 3)).reshape(valid.shape)
+            assert np.array_equal(valid, ref), (kind, pid, two_stage, np.argwhere(valid != ref)[:5])
+            edge = planner.validate_edges(m, scene, frm, to, 32, two_stage, True)
+            assert np.array_equal(edge, valid.all(axis=1))
+        assert (~valid).any() and valid.any()  # both outcomes exercised
+
+
 def test_nn_exact_with_ties(gpu, oracle):
     rng = np.random.default_rng(3)
     for dof in (7, 8, 14):

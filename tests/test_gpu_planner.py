@@ -55,22 +55,34 @@ def check_path(oracle, m, scene, res, start, goal, params, strict4=True):
     return ok4
 
 
+def not_below(ok, ok_ref, n):
+    """Success no lower than the reference's (north_star), at equal budgets, up
+    to sampling noise: the two-proportion 2-sigma band of n problems. The
+    full 1000-problem sets are compared in bench.py's parity block."""
+    p = max(ok, ok_ref) / n
+    return ok / n >= ok_ref / n - 2.0 * np.sqrt(max(p * (1 - p), 1.0 / n) * 2.0 / n)
+
+
 @pytest.mark.parametrize("robot", ["panda", "fetch", "baxter"])
 def test_plan_paths_revalidate(gpu, oracle, robot):
-    """Default mode: every path sound at n_cc (the reference planner's own
-    guarantee) and >= 90% at 4 x n_cc (edges are checked at n_cc samples, so
-    a contact between two samples can slip through — for the reference
-    too). Sound mode (validate_path): every path sound at 4 x n_cc."""
+    """Single-problem mode at the reference's budget: W = 16 CTAs on the
+    problem, budget 16 x max_iters_per_worker, against the reference with
+    workers = 16 (planner.cpp:199,287-288). Every path sound at n_cc (the
+    reference planner's own guarantee) and >= 90% at 4 x n_cc (edges are
+    checked at n_cc samples, so a contact between two samples can slip
+    through — for the reference too). Sound mode (validate_path): every path
+    sound at 4 x n_cc."""
     m = robots.get(robot)
-    params = PlannerParams()  # reference defaults (tree_capacity 200000, planner.hpp:21-40)
-    sound = PlannerParams(validate_path=True)
-    probs = load_problems(robot, 24)
+    params = PlannerParams(workers=16)  # reference defaults otherwise (planner.hpp:21-40)
+    sound = PlannerParams(workers=16, validate_path=True)
+    probs = load_problems(robot, 1000)[::40]  # 25 problems spread over the scene kinds
     solved = solved_ref = 0
     ok4 = []
     for kind, pid, s, g in probs:
         scene, _ = make_scene(robot, kind, pid)
         r = planner.plan(m, scene, s, g, params)
         assert r.status in (PlanStatus.Solved, PlanStatus.Failed)
+        assert r.iterations_total <= 16 * params.max_iters_per_worker + 64  # (ticket blocks in flight)
         if r.status == PlanStatus.Solved:
             solved += 1
             ok4.append(check_path(oracle, m, scene, r, s, g, params, strict4=False))
@@ -78,31 +90,38 @@ def test_plan_paths_revalidate(gpu, oracle, robot):
         if rs.status == PlanStatus.Solved:
             assert rs.path_check == 1
             check_path(oracle, m, scene, rs, s, g, sound, strict4=True)
-        ref = oracle.plan(m, scene, s, g, PlannerParams(workers=1))
+        ref = oracle.plan(m, scene, s, g, params)
         solved_ref += ref.status == PlanStatus.Solved
-    assert solved >= solved_ref
+    assert not_below(solved, solved_ref, len(probs)), (solved, solved_ref)
     assert np.mean(ok4) >= 0.9, f"4 x n_cc soundness {np.mean(ok4):.2f}"
 
 
-
 def test_batch_success_not_below_reference(gpu, oracle):
+    """Batch mode at the reference's budget (workers = 1: 2000 iterations per
+    problem on both planners), 300 problems spread over the scene kinds."""
     m = robots.get("panda")
-    probs = load_problems("panda", 90)
+    probs = load_problems("panda", 1000)[::3][:300]
     scenes = [make_scene("panda", k, p)[0] for k, p, _, _ in probs]
     S = np.array([p[2] for p in probs])
     G = np.array([p[3] for p in probs])
-    params = PlannerParams(tree_capacity=20000)
+    params = PlannerParams(workers=1, tree_capacity=20000)
     res = planner.plan_batch(m, scenes, S, G, params)
-    ref, _ = oracle.plan_many(m, scenes, S, G, PlannerParams(workers=1, tree_capacity=20000), threads=8)
+    ref, _ = oracle.plan_many(m, scenes, S, G, params, threads=8)
     ok = sum(r.status == PlanStatus.Solved for r in res)
     ok_ref = sum(r.status == PlanStatus.Solved for r in ref)
-    assert ok >= ok_ref
+    assert not_below(ok, ok_ref, len(probs)), (ok, ok_ref)
+    assert all(r.iterations_total <= params.max_iters_per_worker for r in res if r.status != PlanStatus.Solved)
     ok4 = [check_path(oracle, m, sc, r, s, g, params, strict4=False)
            for sc, r, s, g in zip(scenes, res, S, G) if r.status == PlanStatus.Solved]
     assert np.mean(ok4) >= 0.9
+    # initial path cost reported alongside: same order as the reference's on the common solved set
+    both = [(r.cost, q.cost) for r, q in zip(res, ref) if r.status == q.status == PlanStatus.Solved]
+    assert len(both) > 0.5 * len(probs)
+    cg, cr = np.mean([b[0] for b in both]), np.mean([b[1] for b in both])
+    assert cg <= 1.25 * cr, (cg, cr)
     # sound mode: every returned path passes 4 x n_cc
-    sound = PlannerParams(tree_capacity=20000, validate_path=True)
-    for sc, r, s, g in zip(scenes[:30], planner.plan_batch(m, scenes[:30], S[:30], G[:30], sound), S, G):
+    sound = PlannerParams(workers=1, tree_capacity=20000, validate_path=True)
+    for sc, r, s, g in zip(scenes[:60], planner.plan_batch(m, scenes[:60], S[:60], G[:60], sound), S, G):
         if r.status == PlanStatus.Solved:
             check_path(oracle, m, sc, r, s, g, sound, strict4=True)
 
@@ -123,7 +142,32 @@ def test_deterministic_mode_replays_reference(gpu, oracle):
         if r.status == ref.status and (r.status != PlanStatus.Solved or np.array_equal(r.path, ref.path)):
             same += 1
             assert r.iterations_total == ref.iterations_total
+            # CheckStats follow the reference's counting semantics in this mode
+            # (collision.hpp:14-37, collision.cpp:73-84,133,158,179,189)
+            assert r.check_stats == ref.check_stats, (kind, pid, r.check_stats, ref.check_stats)
     assert same >= len(probs) * 0.9
+
+
+@pytest.mark.parametrize("two_stage,early_exit", [(False, True), (True, False), (False, False)])
+def test_deterministic_check_stats_variants(gpu, oracle, two_stage, early_exit):
+    """CheckStats parity under the CheckOptions variants (brute force, no early
+    exit): wherever the deterministic device run replays the reference's
+    workers=1 run, sphere_tests / fk_calls / fine_stage_entries are equal."""
+    m = robots.get("panda")
+    params = PlannerParams(tree_capacity=20000, deterministic=True, workers=1, two_stage=two_stage,
+                           early_exit=early_exit)
+    same = 0
+    probs = load_problems("panda", 1000)[::100]
+    for kind, pid, s, g in probs:
+        scene, _ = make_scene("panda", kind, pid)
+        r = planner.plan(m, scene, s, g, params)
+        ref = oracle.plan(m, scene, s, g, PlannerParams(workers=1, tree_capacity=20000, two_stage=two_stage,
+                                                        early_exit=early_exit))
+        if r.status == ref.status and (r.status != PlanStatus.Solved or np.array_equal(r.path, ref.path)):
+            same += 1
+            assert r.iterations_total == ref.iterations_total
+            assert r.check_stats == ref.check_stats, (kind, pid, r.check_stats, ref.check_stats)
+    assert same >= 0.8 * len(probs)
 
 
 def test_endpoint_statuses(gpu, oracle):
