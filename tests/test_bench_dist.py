@@ -19,7 +19,8 @@ import torch.distributed as dist
 world, rank, local = bench.dist_setup()
 bench.dist_barrier(world)
 m = bench.dist_max(10.0 + 5 * rank, world)
-print(json.dumps({"rank": rank, "world": world, "max": m}))
+t = bench.dist_sum(100.0 + rank, world)
+print(json.dumps({"rank": rank, "world": world, "max": m, "sum": t}))
 dist.destroy_process_group()
 """
 
@@ -45,7 +46,7 @@ def test_gloo_world2_max_over_ranks(tmp_path):
         assert p.returncode == 0, e
     res = [json.loads(o.strip().splitlines()[-1]) for o, _ in outs]
     assert sorted(r["rank"] for r in res) == [0, 1]
-    assert all(r["world"] == 2 and r["max"] == 15.0 for r in res)
+    assert all(r["world"] == 2 and r["max"] == 15.0 and r["sum"] == 201.0 for r in res)
 
 
 def test_weak_scaling_value_definition():
@@ -66,3 +67,23 @@ def test_shard_partitions_problems():
             assert flat == list(range(n))
             sizes = [len(p) for p in parts]
             assert max(sizes) - min(sizes) <= (1 if n else 0)
+
+
+def test_ranks_solve_distinct_problem_sets():
+    """Weak scaling over DISTINCT problems: rank r's set (problems_panda_s<r>)
+    shares no problem (scene id, start, goal) with any other rank's, and every
+    set keeps the 334/333/333 scene-kind mix."""
+    import numpy as np
+
+    import bench
+    seen, starts = set(), []
+    for r in range(8):
+        (m, scenes, S, G, kinds), name = bench.problem_set("panda", r, 1000)
+        assert "replica" not in name
+        ids = {sc.name for sc in scenes}
+        assert len(ids) == 1000 and not (ids & seen)
+        seen |= ids
+        starts.append(S)
+        assert [int((kinds == k).sum()) for k in ("table_pick", "bookshelf", "cage")] == [334, 333, 333]
+    allS = np.concatenate(starts)
+    assert len(np.unique(allS, axis=0)) == len(allS)
