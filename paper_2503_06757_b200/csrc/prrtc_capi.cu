@@ -890,8 +890,8 @@ int check_params(const prrtc_params* p) {  // planner.cpp:250-252
     if (p->tree_capacity < 2) return set_err(PRRTC_EINVAL, "plan: tree_capacity too small");
     if (p->threads_per_cta != 0 && p->threads_per_cta != 128 && p->threads_per_cta != 256)
         return set_err(PRRTC_EINVAL, "plan: threads_per_cta must be 0, 128 or 256");
-    if (p->sampler != PRRTC_SAMPLER_HALTON)
-        return set_err(PRRTC_EINVAL, "plan: the device sampler is Halton only (SamplerKind::Uniform is a property-test sampler, sampling.hpp:40-54)");
+    if (p->sampler != PRRTC_SAMPLER_HALTON && p->sampler != PRRTC_SAMPLER_UNIFORM)
+        return set_err(PRRTC_EINVAL, "plan: unknown sampler");
     return PRRTC_OK;
 }
 
@@ -1100,6 +1100,7 @@ int batch_enqueue(prrtc_batch* b, cudaStream_t st, bool upload) {
     a.ref_stats = b->params.deterministic ? 1 : 0;
     a.p.budget = b->budget;
     a.p.seed = b->params.seed;
+    a.p.uniform = b->params.sampler == PRRTC_SAMPLER_UNIFORM ? 1 : 0;
     a.ns_max = b->ns_max;
     a.nthreads = b->nthreads;
     // multi-sample NN bound (samples x tree nodes per pass, ~4-8 node pairs
@@ -1331,6 +1332,8 @@ int fill_results(prrtc_batch* b, prrtc_result* out, const unsigned char* h, cons
             r.status = PRRTC_FAILED;
             std::snprintf(r.message, sizeof(r.message), "path unavailable");
         }
+        if (C.inv_bad)  // PRRTC_DEBUG_FLAGS bit 2 only
+            std::snprintf(r.message, sizeof(r.message), "debug: %d tree invariant violations", C.inv_bad);
         // per-problem device time (globaltimer: initialisation -> finish)
         r.device_time_ms = (C.t_end_ns > C.t_start_ns) ? (C.t_end_ns - C.t_start_ns) * 1e-6 : 0.0;
         r.wall_time_ms = ms;  // launch time; prrtc_plan overwrites with the host wall clock

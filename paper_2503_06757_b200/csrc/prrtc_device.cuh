@@ -108,6 +108,95 @@ __device__ __forceinline__ double halton_tab(unsigned base, unsigned long long m
     return r;
 }
 
+// ---------------------------------------------------------------------------
+// SamplerKind::Uniform (sampling.hpp:40-54): std::mt19937_64 seeded with
+// params.seed * 0x9e3779b97f4a7c15 + worker (planner.cpp:194) and libstdc++'s
+// uniform_real_distribution<double>(lo, hi): generate_canonical<double, 53>
+// takes one 64-bit draw x (mt19937_64's range is 2^64), ret = double(x) /
+// 2^64 (nextafter(1, 0) if it rounds to 1), value = ret * (hi - lo) + lo —
+// the same IEEE operations here (__ull2double_rn, exact power-of-two
+// scaling, __dmul_rn, __dadd_rn). One generator per CTA in shared memory
+// (312 words + position); the twist runs CTA-wide in its three dependency
+// phases, the tempering of a block's draws in parallel.
+// ---------------------------------------------------------------------------
+constexpr int kMtN = 312, kMtM = 156;
+constexpr unsigned long long kMtA = 0xB5026F5AA96619E9ull;
+constexpr unsigned long long kMtUpper = ~0ull << 31, kMtLower = ~kMtUpper;
+
+__device__ __forceinline__ unsigned long long mt_mix(unsigned long long xk, unsigned long long xk1) {
+    const unsigned long long y = (xk & kMtUpper) | (xk1 & kMtLower);
+    return (y >> 1) ^ ((y & 1ull) ? kMtA : 0ull);
+}
+
+__device__ __forceinline__ unsigned long long mt_temper(unsigned long long z) {
+    z ^= (z >> 29) & 0x5555555555555555ull;
+    z ^= (z << 17) & 0x71D67FFFEDA60000ull;
+    z ^= (z << 37) & 0xFFF7EEE000000000ull;
+    z ^= z >> 43;
+    return z;
+}
+
+// std::mersenne_twister_engine::seed(value) (one thread; CTA-uniform state)
+__device__ __noinline__ void mt_seed(unsigned long long* mt, unsigned long long seed) {
+    mt[0] = seed;
+    for (int i = 1; i < kMtN; ++i) mt[i] = 6364136223846793005ull * (mt[i - 1] ^ (mt[i - 1] >> 62)) + (unsigned)i;
+    mt[kMtN] = kMtN;  // position: the first draw twists
+}
+
+// _M_gen_rand in its dependency phases (CTA-wide; all threads call; at most
+// two elements per thread and phase, so nthreads >= 78)
+__device__ __noinline__ void mt_twist(unsigned long long* mt, int nthreads) {
+    const int tid = threadIdx.x, k0 = tid, k1 = tid + nthreads;
+    constexpr int n1 = kMtN - kMtM;  // phase 1: k in [0, 156), old values only
+    unsigned long long v0 = 0, v1 = 0;
+    if (k0 < n1) v0 = mt[k0 + kMtM] ^ mt_mix(mt[k0], mt[k0 + 1]);
+    if (k1 < n1) v1 = mt[k1 + kMtM] ^ mt_mix(mt[k1], mt[k1 + 1]);
+    __syncthreads();
+    if (k0 < n1) mt[k0] = v0;
+    if (k1 < n1) mt[k1] = v1;
+    __syncthreads();
+    // phase 2: k in [156, 311): x[k - 156] is new, x[k], x[k + 1] old
+    const int j0 = n1 + k0, j1 = n1 + k1;
+    if (j0 < kMtN - 1) v0 = mt[j0 - n1] ^ mt_mix(mt[j0], mt[j0 + 1]);
+    if (j1 < kMtN - 1) v1 = mt[j1 - n1] ^ mt_mix(mt[j1], mt[j1 + 1]);
+    __syncthreads();
+    if (j0 < kMtN - 1) mt[j0] = v0;
+    if (j1 < kMtN - 1) mt[j1] = v1;
+    __syncthreads();
+    if (tid == 0) {  // the last element wraps to the new x[0]
+        mt[kMtN - 1] = mt[kMtM - 1] ^ mt_mix(mt[kMtN - 1], mt[0]);
+        mt[kMtN] = 0;
+    }
+    __syncthreads();
+}
+
+// uniform_real_distribution<double>(lo, hi)(rng) from one raw draw
+__device__ __forceinline__ double uniform_dim(unsigned long long x, double lo, double hi) {
+    double ret = __dmul_rn(__ull2double_rn(x), 0x1p-64);
+    if (ret >= 1.0) ret = nextafter(1.0, 0.0);
+    return __dadd_rn(__dmul_rn(ret, __dsub_rn(hi, lo)), lo);
+}
+
+// The next `count` draws of the CTA's generator as scaled samples, draw j =
+// (sample j / dof, dimension j % dof), into out[j] (CTA-wide).
+__device__ __noinline__ void mt_fill(unsigned long long* mt, const double* limits, int dof, double* out, int count,
+                                    int nthreads) {
+    int done = 0;
+    while (done < count) {
+        if (mt[kMtN] >= (unsigned long long)kMtN) mt_twist(mt, nthreads);
+        const int pos = (int)mt[kMtN];
+        const int take = min(count - done, kMtN - pos);
+        for (int j = threadIdx.x; j < take; j += nthreads) {
+            const int g = done + j, d = g % dof;
+            out[g] = uniform_dim(mt_temper(mt[pos + j]), limits[2 * d], limits[2 * d + 1]);
+        }
+        __syncthreads();
+        if (threadIdx.x == 0) mt[kMtN] = pos + take;
+        __syncthreads();
+        done += take;
+    }
+}
+
 // sampling.cpp:39-51 (sample_config), one dimension.
 __device__ __forceinline__ double sample_dim(double h, double lo, double hi) {
     double v = __dadd_rn(lo, __dmul_rn(h, __dsub_rn(hi, lo)));
@@ -310,6 +399,7 @@ struct Ctx {
     // exact-CheckStats mode (deterministic planning): counters follow the
     // reference's sequential semantics (ref_state_count); per-state scratch
     int ref_stats;
+    unsigned long long* mt;      // [kMtN + 1] SamplerKind::Uniform generator state + position
     unsigned long long* rcount;  // [NS] reference sphere_tests of each state
     int* rfine;                  // [NS] 1 if the state enters the fine stage
 };

@@ -100,7 +100,7 @@ struct ProbCtl {
     long long t_start_ns;
     long long t_end_ns;
     int path_bad;     // validate_paths_kernel: some edge of the returned path collides
-    int _pad;
+    int inv_bad;      // PRRTC_DEBUG_FLAGS bit 2: tree invariant violations seen at snapshots
 };
 static_assert(sizeof(ProbCtl) <= 128, "ProbCtl must fit 128 bytes");
 
@@ -115,6 +115,7 @@ struct PlanParamsDev {
     int deterministic;
     unsigned long long budget;  // total iterations per problem
     unsigned long long seed;
+    int uniform;                // SamplerKind::Uniform (else Halton)
 };
 
 // Halton reciprocal-power table length per dimension: stored after the
@@ -146,7 +147,8 @@ struct PlanArgs {
     unsigned long long* trace; // [2]: LLONG_MAX - first CTA start, last CTA exit (globaltimer ns)
     long long* cta_trace;      // [grid][4]: per-CTA stamps (PRRTC_TRACE only, else null)
     unsigned epoch;
-    unsigned dbg;              // PRRTC_DEBUG_FLAGS: bit 0 = fence at every snapshot (protocol check; 0 in production)
+    unsigned dbg;              // PRRTC_DEBUG_FLAGS: bit 0 = fence at every snapshot (protocol check; 0 in
+                               // production); bit 2 = check the trees' invariants at every snapshot
     PlanParamsDev p;
     int ns_max;                // states per validation chunk
     int nthreads;

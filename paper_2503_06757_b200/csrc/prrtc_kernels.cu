@@ -30,7 +30,7 @@ using namespace dev;
 // ---------------------------------------------------------------------------
 struct SmemLayout {
     size_t robot, scene, pose, ccen, qf, sgroup, sbad, lmask, ictl, dcfg, red_d, red_i,
-        ends, ends_eq, ttab, sbuf, mnn, stat, htab, t0, rcount, rfine, total;
+        ends, ends_eq, ttab, sbuf, mnn, stat, htab, t0, rcount, rfine, mt, total;
 };
 
 __host__ __device__ inline size_t al16(size_t x) { return (x + 15) & ~size_t(15); }
@@ -62,6 +62,7 @@ __host__ __device__ inline SmemLayout smem_layout(int robot_words, int L, int do
     s.t0 = o;    o = al16(o + 8 * (size_t)T0_COUNT);
     s.rcount = o; o = al16(o + 8 * (size_t)NS);
     s.rfine = o; o = al16(o + 4 * (size_t)NS);
+    s.mt = o;    o = al16(o + 8 * (size_t)(kMtN + 1));
     s.total = o;
     return s;
 }
@@ -134,6 +135,7 @@ __device__ void setup_ctx(Ctx& c, unsigned char* smem, const uint32_t* robot_g, 
         c.ref_stats = 0;  // the planner turns it on in deterministic mode
         c.rcount = reinterpret_cast<unsigned long long*>(smem + lay.rcount);
         c.rfine = reinterpret_cast<int*>(smem + lay.rfine);
+        c.mt = reinterpret_cast<unsigned long long*>(smem + lay.mt);
         c.ttab_n = 0;
         c.nslog = 31 - __clz(NS);
         c.mflog = c.MF > 1 ? 32 - __clz(c.MF - 1) : 0;
@@ -535,6 +537,50 @@ __device__ void assemble_path(Ctx& c, const PlanArgs& a, int prob, int meet_a, i
 }
 
 // ---------------------------------------------------------------------------
+// Debug mode (PRRTC_DEBUG_FLAGS bit 2): the tree invariants of SPEC.md:368 /
+// tree.hpp:27-53 checked at every snapshot the CTA acquires — every slot
+// below the published count of either tree has its ready flag at this
+// launch's epoch, a parent below itself (the root: -1), and an edge to its
+// parent no longer than delta (extend steps and connect sub-edges are <= delta,
+// planner.cpp:35-64). Violations are counted into ctl[prob].inv_bad.
+// ---------------------------------------------------------------------------
+// (fields by value: a reference to the kernel's parameter block would make
+// the compiler copy it to local memory)
+__device__ __noinline__ void check_tree_invariants(Ctx& c, ProbCtl* ctl, const double* cfg0, const int* parent0,
+                                                   const unsigned* ready0, long long stride, unsigned epoch,
+                                                   double delta) {
+    const int dof = c.dof;
+    const double lim = delta * (1.0 + 1e-9) + 1e-12;
+    int bad = 0;
+    for (int t = 0; t < 2; ++t) {
+        const int n = ld_acquire(&ctl->published[t]);  // (the header fenced: a fresh snapshot)
+        const double* cfg = cfg0 + (size_t)t * dof * stride;
+        const int* parent = parent0 + (size_t)t * stride;
+        const unsigned* ready = ready0 + (size_t)t * stride;
+        for (int i = threadIdx.x; i < n; i += c.nthreads) {
+            if (__ldcg(ready + i) != epoch) {
+                ++bad;
+                continue;
+            }
+            const int p = __ldcg(parent + i);
+            if (i == 0 ? p != -1 : (p < 0 || p >= i)) {
+                ++bad;
+                continue;
+            }
+            if (i == 0) continue;
+            double acc = 0.0;
+            for (int d = 0; d < dof; ++d) {
+                const double e = __ldcg(cfg + (size_t)d * stride + i) - __ldcg(cfg + (size_t)d * stride + p);
+                acc += e * e;
+            }
+            if (!(sqrt(acc) <= lim)) ++bad;
+        }
+    }
+    if (bad) atomicAdd(&ctl->inv_bad, bad);
+    __syncthreads();
+}
+
+// ---------------------------------------------------------------------------
 // the persistent planner kernel
 // ---------------------------------------------------------------------------
 enum : int { DONE_RUNNING = 0, DONE_SOLVED = 1, DONE_FAILED = 2, DONE_INFEASIBLE = 3 };
@@ -864,6 +910,10 @@ __global__ void __launch_bounds__(NT, MINB) plan_kernel(PlanArgs a) {
         if (tid == 0) {
             unsigned long long* t0 = sh(c.t0);
             t0[T0_TKBASE] = t0[T0_TKPOS] = t0[T0_TKCNT] = t0[T0_USED] = t0[T0_LITER] = 0;
+            // Uniform sampler: a fresh generator per (problem, worker), seeded as
+            // the reference's worker `blockIdx` (worker 0 in deterministic mode)
+            if (a.p.uniform)
+                mt_seed(sh(c.mt), a.p.seed * 0x9e3779b97f4a7c15ull + (a.p.deterministic ? 0u : blockIdx.x));
         }
         int leave_msg = MSG_NONE;
         for (;;) {
@@ -894,7 +944,7 @@ __global__ void __launch_bounds__(NT, MINB) plan_kernel(PlanArgs a) {
                 // appends and dynamic-domain flags need no fence (IC_DIRTY
                 // only forces one when the CTA joins a problem)
                 int* known = sh(c.ictl) + IC_KNOWN0;
-                if (la > known[0] || lb > known[1] || sh(c.ictl)[IC_DIRTY] || (a.dbg & 1)) {
+                if (la > known[0] || lb > known[1] || sh(c.ictl)[IC_DIRTY] || (a.dbg & 5)) {
                     fence_acq_rel();
                     known[0] = max(known[0], la);
                     known[1] = max(known[1], lb);
@@ -926,6 +976,9 @@ __global__ void __launch_bounds__(NT, MINB) plan_kernel(PlanArgs a) {
                 leave_msg = leave == 2 ? MSG_BUDGET : MSG_NONE;
                 break;
             }
+            if (a.dbg & 4)
+                check_tree_invariants(c, &C, a.cfg + (size_t)prob * 2 * dof * a.stride, a.parent + (size_t)prob * 2 * a.stride,
+                                      a.ready + (size_t)prob * 2 * a.stride, a.stride, a.epoch, a.p.delta);
             const int ts = sh(c.ictl)[IC_TMP1] ? 0 : 1;
             const int snap = sh(c.ictl)[IC_TMP2];
             const int refill = sh(c.ictl)[IC_TMP3];
@@ -938,6 +991,9 @@ __global__ void __launch_bounds__(NT, MINB) plan_kernel(PlanArgs a) {
                 TRACE_PHASE(7);
                 const unsigned long long base = reinterpret_cast<unsigned long long*>(sh(c.red_d))[0];
                 __syncthreads();  // header scalars read before they are reused
+                if (a.p.uniform)  // the CTA's own stream, in draw order (sampling.hpp:44-48)
+                    mt_fill(sh(c.mt), sh(c.limits), dof, sh(c.sbuf), kblk * dof, c.nthreads);
+                else
                 for (int j = tid; j < kblk * dof; j += c.nthreads) {
                     const int k = j / dof, d = j - k * dof;
                     sh(c.sbuf)[j] = sample_dim(halton_tab(sh(c.bases)[d], sh(c.magic)[d], sh(c.htab) + d * kHaltonTab,
@@ -1023,7 +1079,7 @@ __global__ void __launch_bounds__(NT, MINB) plan_kernel(PlanArgs a) {
                     const int po = ld_relaxed(To.published);
                     sh(c.ictl)[IC_TMP3] = ld_relaxed(&C.done);  // settled meanwhile: skip the connect
                     int* known = sh(c.ictl) + IC_KNOWN0 + To.which;
-                    if (po > *known || (a.dbg & 1)) {
+                    if (po > *known || (a.dbg & 5)) {
                         fence_acq_rel();
                         *known = po;
                     }

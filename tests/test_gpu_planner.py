@@ -316,3 +316,50 @@ def test_single_problem_result_paths_agree(gpu, oracle, robot, monkeypatch):
             assert r.tree_nodes == r0.tree_nodes
         if r0.status == PlanStatus.Solved:
             assert oracle.path_valid(m, scene, r0.path, params.n_cc)
+
+
+def test_tree_invariants_under_concurrent_appends(gpu, monkeypatch):
+    """Lock-free tree protocol under load: with
+    PRRTC_DEBUG_FLAGS bit 2 every CTA checks, at every snapshot it acquires,
+    that each published slot of both trees is ready (this launch's epoch), has
+    a parent below itself and an edge no longer than delta (SPEC.md:368,
+    tree.hpp:27-53). All SMs on one problem (maximum append contention), then
+    a batch where CTAs join running problems."""
+    monkeypatch.setenv("PRRTC_DEBUG_FLAGS", "4")
+    m = robots.get("panda")
+    probs = load_problems("panda", 1000)[::50]
+    for kind, pid, s, g in probs:
+        scene, _ = make_scene("panda", kind, pid)
+        r = planner.plan(m, scene, s, g, PlannerParams(workers=0, tree_capacity=20000))
+        assert "invariant" not in r.message, r.message
+        assert r.status in (PlanStatus.Solved, PlanStatus.Failed)
+    scenes = [make_scene("panda", k, p)[0] for k, p, _, _ in probs]
+    S = np.array([p[2] for p in probs])
+    G = np.array([p[3] for p in probs])
+    res = planner.plan_batch(m, scenes, S, G, PlannerParams(tree_capacity=20000))
+    assert all("invariant" not in r.message for r in res)
+
+
+def test_uniform_sampler_replays_reference(gpu, oracle):
+    """SamplerKind::Uniform (sampling.hpp:40-54: std::mt19937_64 seeded
+    seed * 0x9e3779b97f4a7c15 + worker, libstdc++ uniform_real_distribution)
+    in deterministic mode: the device's draws equal the reference's, so the
+    run replays the reference's workers=1 uniform run node for node (up to
+    FP32-FK verdict flips near contact), CheckStats included."""
+    from paper_2503_06757_b200.model import SamplerKind
+    if oracle.kind != "ref":
+        pytest.skip("the uniform sampler is checked against the compiled reference")
+    m = robots.get("panda")
+    probs = load_problems("panda", 1000)[::50]
+    same = 0
+    for seed in (0, 7):
+        for kind, pid, s, g in probs:
+            scene, _ = make_scene("panda", kind, pid)
+            p = PlannerParams(tree_capacity=20000, workers=1, sampler=SamplerKind.Uniform, seed=seed)
+            r = planner.plan(m, scene, s, g, PlannerParams(**{**p.__dict__, "deterministic": True}))
+            ref = oracle.plan(m, scene, s, g, p)
+            if r.status == ref.status and (r.status != PlanStatus.Solved or np.array_equal(r.path, ref.path)):
+                same += 1
+                assert r.iterations_total == ref.iterations_total
+                assert r.check_stats == ref.check_stats
+    assert same >= 0.9 * 2 * len(probs), same

@@ -41,7 +41,9 @@ keys = [
     "smsp__sass_thread_inst_executed_op_ffma_pred_on.sum", "smsp__sass_thread_inst_executed_op_fadd_pred_on.sum",
     "smsp__sass_thread_inst_executed_op_fmul_pred_on.sum", "smsp__inst_executed.sum",
     "dram__bytes_read.sum", "dram__bytes_write.sum", "lts__t_bytes.sum", "lts__t_sector_hit_rate.pct",
-    "l1tex__data_pipe_lsu_wavefronts_mem_shared.sum",
+    "l1tex__data_pipe_lsu_wavefronts_mem_shared.sum", "sass__inst_executed_register_spilling",
+    "smsp__sass_inst_executed_op_local_ld.sum", "smsp__sass_inst_executed_op_local_st.sum",
+    "lts__t_sectors_srcunit_tex_op_write.sum", "l1tex__data_bank_conflicts_pipe_lsu_mem_shared.sum",
 ]
 stalls = sorted(((float(v[i]), k) for i, k in enumerate(h)
                  if k.startswith("smsp__average_warps_issue_stalled_") and k.endswith("_per_issue_active.ratio")),
@@ -76,5 +78,6 @@ pct = lambda k: (num(k, {"%": 0.01}) if k in m else None)  # noqa: E731
     "plan_kernel_fma_pipe_active": pct("sm__pipe_fma_cycles_active.avg.pct_of_peak_sustained_active"),
     "plan_kernel_warps_active": pct("sm__warps_active.avg.pct_of_peak_sustained_active"),
     "plan_kernel_l2_hit_rate": pct("lts__t_sector_hit_rate.pct"),
+    "plan_kernel_spill_insts": num("sass__inst_executed_register_spilling", {"inst": 1, "": 1}),
 }, indent=1) + "\n")
 print("\n".join(out))
