@@ -219,6 +219,7 @@ def microbench(model, scenes, S, G, dev, fp32_peak):
                      "frac_fp32_peak": tf / fp32_peak if fp32_peak else None,
                      "mode": f"two_stage={two} early_exit={early}"}
     l2 = lib.prrtc_l2_peak_gbs(dev)
+    fp64 = lib.prrtc_fp64_peak_tflops(dev)
     rng = np.random.default_rng(7)
     lim = model.limits()
     T = np.ascontiguousarray(rng.uniform(lim[:, 0], lim[:, 1], size=(100000, model.dof)))
@@ -227,13 +228,22 @@ def microbench(model, scenes, S, G, dev, fp32_peak):
         Q = np.ascontiguousarray(rng.uniform(lim[:, 0], lim[:, 1], size=(2048 if g == 1 else 32 * 592, model.dof)))
         ms = ctypes.c_double()
         _lib.check(lib.prrtc_bench_nn(dp(T), T.shape[0], model.dof, dp(Q), Q.shape[0], g, dev, 3, ctypes.byref(ms)))
-        gbs = Q.shape[0] * T.shape[0] * model.dof * 8 / (ms.value * 1e-3) / 1e9
+        # the reference's arithmetic: FP64 keys, 3 un-fused ops (sub, mul, add)
+        # per (query, node, dimension); node coordinates 8 B each (FP64 SoA)
+        pairs = Q.shape[0] * T.shape[0]
+        tf = pairs * model.dof * 3 / (ms.value * 1e-3) / 1e12
+        gbs = pairs * model.dof * 8 / (ms.value * 1e-3) / 1e9
         out[f"nn_group{g}"] = {"kernel": "debug_nn_multi_kernel (the planner's nn_scan_multi)", "tree_nodes": T.shape[0],
                                "queries": Q.shape[0], "queries_per_pass": g, "ms": ms.value,
-                               "algorithmic_gbs": gbs, "frac_l2_peak": gbs / l2 if l2 else None,
-                               "bytes_per_query": T.shape[0] * model.dof * 8}
+                               "bound": "fp64", "achieved_fp64_tflops": tf,
+                               "frac_fp64_peak": tf / fp64 if fp64 else None,
+                               "bytes_per_query_fp64": T.shape[0] * model.dof * 8,
+                               "query_node_bytes_per_s_gbs": gbs,
+                               "note": f"{g} queries share each node load (L1): per-query bytes exceed the L2 "
+                                       "peak by that reuse, so the FP64 pipe is the bound"}
     out["l2_peak_gbs"] = l2
     out["fp32_peak_tflops"] = fp32_peak
+    out["fp64_peak_tflops"] = fp64
     return out
 
 

@@ -341,6 +341,9 @@ int prrtc_debug_chunk_profile(const prrtc_robot* robot, const prrtc_scene* scene
 /* FP32 FMA-pipe peak of the device in TFLOP/s, measured with an FFMA-chain
    microbenchmark (the roofline denominator of the FK / collision work). */
 double prrtc_fp32_peak_tflops(int device);
+/* FP64 peak in TFLOP/s from un-fused DMUL + DADD chains (the NN scan's keys:
+   FP64 multiplies and adds in the reference's order, no FMA). */
+double prrtc_fp64_peak_tflops(int device);
 /* L2 read bandwidth of the device in GB/s (float4 streaming over a 32 MiB
    L2-resident buffer from 4 CTAs per SM): the NN scan's roofline denominator. */
 double prrtc_l2_peak_gbs(int device);

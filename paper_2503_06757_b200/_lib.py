@@ -144,6 +144,7 @@ SIGNATURES = [
     ("prrtc_debug_chunk_profile", C.c_int, [P, P, DP, DP, C.c_uint32, C.c_int32, C.c_int,
                                            C.POINTER(C.c_longlong)]),
     ("prrtc_fp32_peak_tflops", C.c_double, [C.c_int]),
+    ("prrtc_fp64_peak_tflops", C.c_double, [C.c_int]),
     ("prrtc_l2_peak_gbs", C.c_double, [C.c_int]),
     ("prrtc_bench_validate_edges", C.c_int, [P, P, C.POINTER(C.c_double), C.POINTER(C.c_double), C.c_uint32,
                                              C.c_uint32, C.c_int32, C.c_int, C.c_int, C.c_int,

@@ -1098,6 +1098,13 @@ int batch_enqueue(prrtc_batch* b, cudaStream_t st, bool upload) {
     a.p.two_stage = b->params.two_stage;
     a.p.deterministic = b->params.deterministic;
     a.ref_stats = b->params.deterministic ? 1 : 0;
+    {
+        static const int tail = [] {
+            const char* e = std::getenv("PRRTC_TAIL_CLAIM");
+            return e ? std::atoi(e) : 1;
+        }();
+        a.tail_claim = tail;
+    }
     a.p.budget = b->budget;
     a.p.seed = b->params.seed;
     a.p.uniform = b->params.sampler == PRRTC_SAMPLER_UNIFORM ? 1 : 0;
@@ -1252,6 +1259,15 @@ int fill_results(prrtc_batch* b, prrtc_result* out, const unsigned char* h, cons
                      "prrtc trace: events %.3f ms | first CTA -> first init %.3f | inits -> last done %.3f | "
                      "last done -> last CTA exit %.3f | grid %d x %d\n",
                      ms, (p0 - k0) * 1e-6, (p1 - p0) * 1e-6, (k1 - p1) * 1e-6, b->grid, b->nthreads);
+        if (const char* f = std::getenv("PRRTC_DUMP_CTL")) {  // per-problem timeline (analysis tools)
+            if (FILE* o = std::fopen(f, "w")) {
+                for (int i = 0; i < b->n; ++i)
+                    std::fprintf(o, "%d %.6f %.6f %llu %d %d\n", i, (ctl[i].t_start_ns - k0) * 1e-6,
+                                 (ctl[i].t_end_ns - k0) * 1e-6, (unsigned long long)ctl[i].iters_used, ctl[i].done,
+                                 ctl[i].winner);
+                std::fclose(o);
+            }
+        }
         if (b->cta_trace) {
             std::vector<long long> ct(64 * b->grid);
             cudaMemcpy(ct.data(), b->cta_trace, 8 * ct.size(), cudaMemcpyDeviceToHost);
@@ -1907,6 +1923,12 @@ double prrtc_fp32_peak_tflops(int device) {
     if (check_device(device)) return 0.0;
     cudaSetDevice(device);
     return measure_fp32_peak(sm_count(device), 0);
+}
+
+double prrtc_fp64_peak_tflops(int device) {
+    if (check_device(device)) return 0.0;
+    cudaSetDevice(device);
+    return measure_fp64_peak(sm_count(device), 0);
 }
 
 double prrtc_l2_peak_gbs(int device) {

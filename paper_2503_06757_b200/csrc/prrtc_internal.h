@@ -162,6 +162,7 @@ struct PlanArgs {
     unsigned* exit_count;               // CTAs finished (zeroed with the controls)
     int mnn_nodes;                      // multi-sample NN bound: m <= mnn_nodes / tree size
     int ref_stats;                      // exact CheckStats (reference counting semantics): deterministic mode
+    int tail_claim;                     // smaller ticket blocks near a problem's budget end
 };
 
 // Dynamic shared memory bytes for a robot/scene/ns_max combination.

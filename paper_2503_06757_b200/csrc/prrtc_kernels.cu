@@ -928,9 +928,19 @@ __global__ void __launch_bounds__(NT, MINB) plan_kernel(PlanArgs a) {
                 const int dn = ld_relaxed(&C.done);
                 int refill = 0;
                 if (tk_pos == tk_cnt) {
-                    tk_base = a.p.deterministic ? tk_base + tk_cnt : atomicAdd(&C.iters, (unsigned long long)kblk);
+                    // near the end of the problem's budget, smaller blocks: the
+                    // last tickets spread over more CTAs instead of a few CTAs
+                    // holding 32 each while the others idle (a.tail_claim)
+                    unsigned long long want = kblk;
+                    if (a.tail_claim && !a.p.deterministic) {
+                        const unsigned long long seen = tk_cnt ? tk_base + tk_cnt : __ldcg(&C.iters);
+                        const int act = max(1, ld_relaxed(&C.active));
+                        if (seen < a.p.budget)
+                            want = max(4ull, min((unsigned long long)kblk, (a.p.budget - seen) / (2ull * act)));
+                    }
+                    tk_base = a.p.deterministic ? tk_base + tk_cnt : atomicAdd(&C.iters, want);
                     tk_pos = 0;
-                    tk_cnt = kblk;
+                    tk_cnt = want;
                     refill = 1;
                 }
                 const unsigned long long it = tk_base + tk_pos;
@@ -965,6 +975,7 @@ __global__ void __launch_bounds__(NT, MINB) plan_kernel(PlanArgs a) {
                 const unsigned long long rem = tk_cnt - tk_pos;
                 sh(c.ictl)[IC_TMP5] = (int)(it < a.p.budget ? min(rem, a.p.budget - it) : 1ull);
                 sh(c.ictl)[IC_TMP4] = (int)tk_pos++;
+                sh(c.ictl)[IC_TMP7] = (int)tk_cnt;
                 reinterpret_cast<unsigned long long*>(sh(c.red_d))[0] = tk_base;
                 t0[T0_TKBASE] = tk_base;
                 t0[T0_TKPOS] = tk_pos;
@@ -990,11 +1001,12 @@ __global__ void __launch_bounds__(NT, MINB) plan_kernel(PlanArgs a) {
             if (refill) {
                 TRACE_PHASE(7);
                 const unsigned long long base = reinterpret_cast<unsigned long long*>(sh(c.red_d))[0];
+                const int nblk = sh(c.ictl)[IC_TMP7];
                 __syncthreads();  // header scalars read before they are reused
                 if (a.p.uniform)  // the CTA's own stream, in draw order (sampling.hpp:44-48)
-                    mt_fill(sh(c.mt), sh(c.limits), dof, sh(c.sbuf), kblk * dof, c.nthreads);
+                    mt_fill(sh(c.mt), sh(c.limits), dof, sh(c.sbuf), nblk * dof, c.nthreads);
                 else
-                for (int j = tid; j < kblk * dof; j += c.nthreads) {
+                for (int j = tid; j < nblk * dof; j += c.nthreads) {
                     const int k = j / dof, d = j - k * dof;
                     sh(c.sbuf)[j] = sample_dim(halton_tab(sh(c.bases)[d], sh(c.magic)[d], sh(c.htab) + d * kHaltonTab,
                                                             1ull + a.p.seed + base + k),
@@ -1607,6 +1619,48 @@ double measure_fp32_peak(int sms, cudaStream_t st) {
     cudaEventDestroy(e1);
     cudaFree(out);
     const double flops = 5.0 * grid * 256.0 * iters * 16 * 8 * 2;
+    return ms > 0 ? flops / (ms * 1e-3) / 1e12 : 0.0;
+}
+
+// FP64 DMUL/DADD-chain microbenchmark: the roofline denominator of the NN
+// scan, whose keys are un-fused FP64 multiplies and adds in the reference's
+// order (kernels_scalar.cpp:9-16; an FMA would change the bits). 8
+// independent chains per thread; 2 flops per step (one DMUL, one DADD).
+__global__ void __launch_bounds__(256) dpeak_kernel(double* out, int iters) {
+    double a[8];
+#pragma unroll
+    for (int k = 0; k < 8; ++k) a[k] = threadIdx.x * 1e-9 + k;
+    for (int i = 0; i < iters; ++i) {
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+#pragma unroll
+            for (int k = 0; k < 8; ++k) a[k] = __dadd_rn(__dmul_rn(a[k], 0.9999999), 1e-9);
+        }
+    }
+    double s = 0.0;
+#pragma unroll
+    for (int k = 0; k < 8; ++k) s += a[k];
+    if (s == 1234.5) out[blockIdx.x] = s;
+}
+
+double measure_fp64_peak(int sms, cudaStream_t st) {
+    double* out = nullptr;
+    cudaMalloc(&out, 8 * 8 * sms);
+    cudaEvent_t e0, e1;
+    cudaEventCreate(&e0);
+    cudaEventCreate(&e1);
+    const int iters = 512, grid = 8 * sms;
+    dpeak_kernel<<<grid, 256, 0, st>>>(out, iters);  // warm-up
+    cudaEventRecord(e0, st);
+    for (int r = 0; r < 5; ++r) dpeak_kernel<<<grid, 256, 0, st>>>(out, iters);
+    cudaEventRecord(e1, st);
+    cudaEventSynchronize(e1);
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, e0, e1);
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    cudaFree(out);
+    const double flops = 5.0 * grid * 256.0 * iters * 8 * 8 * 2;
     return ms > 0 ? flops / (ms * 1e-3) / 1e12 : 0.0;
 }
 

@@ -53,6 +53,7 @@ cudaError_t launch_debug_nn_multi(const double* soa, long long cap, int count, i
 cudaError_t launch_debug_halton(const uint32_t* bases, const uint64_t* idx, int n, double* out,
                                 cudaStream_t st);
 double measure_fp32_peak(int sms, cudaStream_t st);
+double measure_fp64_peak(int sms, cudaStream_t st);
 double measure_l2_gbs(int sms, cudaStream_t st);
 
 cudaError_t launch_debug_sample(const RobotArgs& r, uint64_t index0, int n, double* out,

@@ -24,7 +24,7 @@ for i in (400, 700):
             print(f"    {r.status.name} dev {r.device_time_ms:.3f} ms iters {r.iterations_total}", file=sys.stderr,
                   flush=True)
 scenes = [make_scene(robot, str(k), int(p))[0] for k, p in zip(d["kind"], d["pid"])]
-b = planner.Batch(m, scenes, d["start"], d["goal"], PlannerParams())
+b = planner.Batch(m, scenes, d["start"], d["goal"], PlannerParams(workers=1, tree_capacity=20000))  # bench headline params
 for rep in range(2):
     print(f"--- batch rep {rep}", file=sys.stderr, flush=True)
     b.launch()
