@@ -319,7 +319,7 @@ int prrtc_debug_nn(const double* tree, uint32_t count, uint32_t dof, const doubl
                    uint32_t n_queries, int device, uint32_t* index, double* sq_dist);
 /* The planner's multi-sample NN pass: queries evaluated `group` (1..32) at a
    time against the same tree, as the planner evaluates the samples of a
-   Halton ticket block; group 0 = prrtc_debug_nn. */
+   Halton ticket block; group 0 = 1 (prrtc_debug_nn). */
 int prrtc_debug_nn_multi(const double* tree, uint32_t count, uint32_t dof, const double* q,
                          uint32_t n_queries, uint32_t group, int device, uint32_t* index, double* sq_dist);
 /* Device Halton values (reference halton_value, sampling.cpp:8-18). */

@@ -1821,7 +1821,8 @@ int prrtc_debug_sphere_hits(const prrtc_scene* scene, const float* centers, cons
 
 int prrtc_debug_nn(const double* tree, uint32_t count, uint32_t dof, const double* q,
                    uint32_t n_queries, int device, uint32_t* index, double* sq_dist) {
-    return prrtc_debug_nn_multi(tree, count, dof, q, n_queries, 0, device, index, sq_dist);
+    // the planner's scan, one query per pass
+    return prrtc_debug_nn_multi(tree, count, dof, q, n_queries, 1, device, index, sq_dist);
 }
 
 int prrtc_debug_nn_multi(const double* tree, uint32_t count, uint32_t dof, const double* q,
@@ -1848,9 +1849,8 @@ int prrtc_debug_nn_multi(const double* tree, uint32_t count, uint32_t dof, const
     }
     cudaMemcpy(ds, soa.data(), 8 * soa.size(), cudaMemcpyHostToDevice);
     cudaMemcpy(dq, q, 8 * (size_t)n_queries * dof, cudaMemcpyHostToDevice);
-    cudaError_t e = group ? launch_debug_nn_multi(ds, cap, (int)count, (int)dof, dq, (int)n_queries, (int)group,
-                                                  di, dd, 0)
-                          : launch_debug_nn(ds, cap, (int)count, (int)dof, dq, (int)n_queries, di, dd, 0);
+    cudaError_t e = launch_debug_nn_multi(ds, cap, (int)count, (int)dof, dq, (int)n_queries, (int)std::max(1u, group),
+                                          di, dd, 0);
     if (e == cudaSuccess) e = cudaMemcpy(index, di, 4 * (size_t)n_queries, cudaMemcpyDeviceToHost);
     if (e == cudaSuccess) e = cudaMemcpy(sq_dist, dd, 8 * (size_t)n_queries, cudaMemcpyDeviceToHost);
     cudaFree(ds);

@@ -1337,93 +1337,14 @@ __device__ __noinline__ int gen_chain_states(Ctx& c, const double* A, const doub
 // loads: every slot below the snapshot was released before the caller's
 // acquire of `published`, which also invalidates stale L1 lines, so the
 // follow-up reads of the winner's config and dynamic-domain flag — both
-// prefetched into L1 here — hit L1), per-thread strict-< argmin
-// over increasing indices, then warp-shuffle and cross-warp argmin with ties
-// to the lowest index. Returned to every thread.
-// ---------------------------------------------------------------------------
-struct NnOut {
-    int index;
-    double d2;
-};
-__device__ __noinline__ NnOut nn_scan(Ctx& c, const double* cfg, long long cap, int count,
-                                      const double* q, int par, const int* ddf = nullptr) {
-    // par: the caller alternates 0/1 between calls (double-buffered
-    // reduction slots: one barrier per call)
-    __shared__ double s_bd[2][32];
-    __shared__ int s_bi[2][32];
-    const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5, nw = c.nthreads >> 5, dof = c.dof;
-    q = sh(q);  // the query lives in the dynamic shared window (every caller)
-
-    double best = __longlong_as_double(0x7ff0000000000000ll);  // +inf
-    int bi = 0x7fffffff;
-    const int npairs = (count + 1) >> 1;
-    // one node pair per thread per step (128-bit load per dimension); the
-    // dimensions' loads are issued 8 at a time before any is consumed, so a
-    // step costs one L2 round trip per 8 dimensions instead of one per
-    // dimension. Candidates are visited in increasing index order per
-    // thread, so strict < keeps the lowest index (kernels_scalar.cpp:30-34);
-    // keys accumulate in the scalar order d = 0, 1, ... (bit-exact).
-    for (int pi = tid; pi < npairs; pi += c.nthreads) {
-        const int n0 = pi * 2;
-        double a0 = 0.0, a1 = 0.0;
-        if (ddf) asm volatile("prefetch.global.L1 [%0];" ::"l"(ddf + n0));
-        for (int d0 = 0; d0 < dof; d0 += 8) {
-            double2 v[8];
-#pragma unroll
-            for (int j = 0; j < 8; ++j)  // every slot assigned: v stays in registers
-                v[j] = d0 + j < dof ? *reinterpret_cast<const double2*>(cfg + (d0 + j) * cap + n0)
-                                    : make_double2(0.0, 0.0);
-#pragma unroll
-            for (int j = 0; j < 8; ++j) {
-                if (d0 + j < dof) {
-                    const double qd = q[d0 + j];
-                    const double e0 = __dsub_rn(v[j].x, qd), e1 = __dsub_rn(v[j].y, qd);
-                    a0 = __dadd_rn(a0, __dmul_rn(e0, e0));
-                    a1 = __dadd_rn(a1, __dmul_rn(e1, e1));
-                }
-            }
-        }
-        if (a0 < best) {
-            best = a0;
-            bi = n0;
-        }
-        if (n0 + 1 < count && a1 < best) {
-            best = a1;
-            bi = n0 + 1;
-        }
-    }
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) {
-        const double ob = __shfl_xor_sync(0xffffffffu, best, o);
-        const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
-        if (ob < best || (ob == best && oi < bi)) {
-            best = ob;
-            bi = oi;
-        }
-    }
-    if (lane == 0) {
-        s_bd[par][w] = best;
-        s_bi[par][w] = bi;
-    }
-    __syncthreads();
-    double b = s_bd[par][0];
-    int i = s_bi[par][0];
-    for (int k = 1; k < nw; ++k) {
-        if (s_bd[par][k] < b || (s_bd[par][k] == b && s_bi[par][k] < i)) {
-            b = s_bd[par][k];
-            i = s_bi[par][k];
-        }
-    }
-    return NnOut{i, b};
-}
-
-// ---------------------------------------------------------------------------
-// nearest neighbours of m <= 32 samples over the same published prefix, in
-// one pass: g = nthreads / next_pow2(m) threads per sample stride the node
-// pairs exactly like nn_scan (same loads, same FP64 keys, strict < over
-// increasing indices per thread), then a segmented shuffle argmin (ties to
-// the lowest index) — or, for g > 32, the cross-warp step. Results for
-// sample j land in mnn_d[j] / mnn_i[j]; ends with a barrier.
+// prefetched into L1 here — hit L1), per-thread strict-< argmin over
+// increasing indices, then warp-shuffle and cross-warp argmin with ties to
+// the lowest index. One routine serves one sample (m = 1) and the planner's
+// multi-sample passes: m <= 32 samples over the same published prefix in one
+// pass, g = nthreads / next_pow2(m) threads per sample striding the node
+// pairs, then a segmented shuffle argmin (ties to the lowest index) — or, for
+// g > 32, the cross-warp step. Results for sample j land in mnn_d[j] /
+// mnn_i[j]; ends with a barrier.
 // ---------------------------------------------------------------------------
 // With `accept` set, the reducing thread of sample j also evaluates the
 // planner's acceptance right away (duplicate, planner.cpp:218; dynamic

@@ -1509,26 +1509,6 @@ __global__ void debug_hits_kernel(SceneArgs sa, const float* centers, const doub
     }
 }
 
-__global__ void debug_nn_kernel(const double* soa, long long cap, int count, int dof, const double* q,
-                                int nq, uint32_t* idx, double* d2) {
-    double* qs = reinterpret_cast<double*>(g_dsmem);  // [kMaxDof], dynamic window (nn_scan uses sh())
-    Ctx c;
-    c.dof = dof;
-    c.nthreads = blockDim.x;
-    int par = 0;
-    for (int i = blockIdx.x; i < nq; i += gridDim.x) {
-        if (threadIdx.x < dof) qs[threadIdx.x] = q[(size_t)i * dof + threadIdx.x];
-        __syncthreads();
-        const NnOut r = nn_scan(c, soa, cap, count, qs, par);
-        par ^= 1;
-        if (threadIdx.x == 0) {
-            idx[i] = r.index;
-            d2[i] = r.d2;
-        }
-        __syncthreads();
-    }
-}
-
 // nn_scan_multi over groups of `group` queries (the planner's multi-sample
 // pass): the parity tests run it against the reference's nearest_serial
 __global__ void debug_nn_multi_kernel(const double* soa, long long cap, int count, int dof, const double* q,
@@ -1780,13 +1760,6 @@ cudaError_t launch_debug_hits(const SceneArgs& s, const float* centers, const do
     const long long items = (long long)n * n_prims;
     const int grid = (int)min((items + 127) / 128, (long long)cur_sms() * 8);
     if (grid > 0) debug_hits_kernel<<<grid, 128, 0, st>>>(s, centers, radii, n, n_prims, hits);
-    return cudaGetLastError();
-}
-
-cudaError_t launch_debug_nn(const double* soa, long long cap, int count, int dof, const double* q,
-                            int nq, uint32_t* idx, double* d2, cudaStream_t st) {
-    const int grid = min(nq, cur_sms() * 8);
-    if (grid > 0) debug_nn_kernel<<<grid, 128, 8 * kMaxDof, st>>>(soa, cap, count, dof, q, nq, idx, d2);
     return cudaGetLastError();
 }
 

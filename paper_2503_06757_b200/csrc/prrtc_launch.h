@@ -46,8 +46,6 @@ cudaError_t launch_debug_fk(const RobotArgs& r, const double* q, int n, float* f
                             float* coarse_out, cudaStream_t st);
 cudaError_t launch_debug_hits(const SceneArgs& s, const float* centers, const double* radii,
                               int n, int n_prims, uint8_t* hits, cudaStream_t st);
-cudaError_t launch_debug_nn(const double* soa, long long cap, int count, int dof, const double* q,
-                            int nq, uint32_t* idx, double* d2, cudaStream_t st);
 cudaError_t launch_debug_nn_multi(const double* soa, long long cap, int count, int dof, const double* q,
                                   int nq, int group, uint32_t* idx, double* d2, cudaStream_t st);
 cudaError_t launch_debug_halton(const uint32_t* bases, const uint64_t* idx, int n, double* out,

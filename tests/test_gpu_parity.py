@@ -220,7 +220,7 @@ def test_nn_exact_with_ties(gpu, oracle):
             q = rng.uniform(-3, 3, (8, dof))
             q[0] = tree[min(1, count - 1)]  # zero distance, first index wins
             q[1] = tree[count // 2]
-            for group in (0, 1, 2, 3, 5, 8):  # single scan, and the planner's multi-sample pass
+            for group in (0, 1, 2, 3, 5, 8):  # one query per pass (0 = 1) and the planner's multi-sample passes
                 idx, d2 = planner.debug_nn(tree, q, group=group)
                 for i in range(len(q)):
                     ri, rd = oracle.nearest_serial(tree, q[i])
