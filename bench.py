@@ -626,13 +626,14 @@ def table_one(dev, robot, params_fn, n_lat, peak):
 
 def run_b200(args):
     import torch
-    torch.cuda.set_device(int(os.environ.get("LOCAL_RANK", "0")))
+    # one GPU per rank (ranks beyond the visible GPUs share them: functional runs only)
+    torch.cuda.set_device(int(os.environ.get("LOCAL_RANK", "0")) % max(1, torch.cuda.device_count()))
     world, rank, local = dist_setup()
     from paper_2503_06757_b200 import _lib, planner
     from paper_2503_06757_b200.model import PlannerParams, PlanStatus
     from paper_2503_06757_b200.planner import Batch
 
-    dev = local
+    dev = local % max(1, torch.cuda.device_count())
     (model, scenes, S, G, kinds), set_name = problem_set(args.robot, rank, args.problems)
     n = len(S)
     params = headline_params()

@@ -705,6 +705,12 @@ __device__ __forceinline__ int test_flops(const SceneV& v, int p) {
     return p < v.ns ? 10 : (p < v.ns + v.nb ? 27 : (p < v.nsbc ? 22 : 26));
 }
 
+#ifndef PRRTC_COARSE_UNROLL
+#define PRRTC_COARSE_UNROLL 2
+#endif
+#define PRRTC_PRAGMA(x) _Pragma(#x)
+#define PRRTC_UNROLL(n) PRRTC_PRAGMA(unroll n)
+
 // coarse (padded) sphere vs primitives [p0, p1): hit bitmask, FP32 only
 // (conservative: the padding covers FP32 error, so no fine hit is missed)
 __device__ __forceinline__ unsigned long long coarse_mask(const SceneV& v, float x, float y, float z,
@@ -712,7 +718,7 @@ __device__ __forceinline__ unsigned long long coarse_mask(const SceneV& v, float
     unsigned long long m = 0;
     const int e1 = min(p1, v.ns), e2 = min(p1, v.ns + v.nb);
     int p = p0;
-#pragma unroll 2
+PRRTC_UNROLL(PRRTC_COARSE_UNROLL)
     for (; p < e1; ++p) {
         float d2;
         const float4 s = v.sph[p];
@@ -720,14 +726,14 @@ __device__ __forceinline__ unsigned long long coarse_mask(const SceneV& v, float
         const float rr = rc + s.w;
         if (d2 < rr * rr) m |= 1ull << p;
     }
-#pragma unroll 2
+PRRTC_UNROLL(PRRTC_COARSE_UNROLL)
     for (; p < e2; ++p) {
         float d2;
         box_d2(x, y, z, v.box + (p - v.ns) * BOX_STRIDE, d2);
         if (d2 < rc * rc) m |= 1ull << p;
     }
     const int e3 = min(p1, v.nsbc);
-#pragma unroll 2
+PRRTC_UNROLL(PRRTC_COARSE_UNROLL)
     for (; p < e3; ++p) {
         float d2;
         const float* C = v.cap + (p - v.ns - v.nb) * CAP_STRIDE;
