@@ -196,8 +196,11 @@ struct prrtc_scene {
     // completion markers of the launches that read this scene (see UseMark)
     mutable std::mutex mark_mu;
     mutable std::vector<UseMarkP> marks;
+    mutable std::atomic<const UseMark*> last_mark{nullptr};  // fast path: the marker most recently added
     void mark_use(const UseMarkP& m) const {
+        if (last_mark.load(std::memory_order_acquire) == m.get()) return;  // (markers are never removed)
         std::lock_guard<std::mutex> lk(mark_mu);
+        last_mark.store(m.get(), std::memory_order_release);
         for (const auto& x : marks)
             if (x == m) return;
         marks.push_back(m);

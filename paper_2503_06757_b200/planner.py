@@ -171,9 +171,11 @@ class BatchResult:
         lib = _lib.load()
         self.path_offsets = np.zeros(n + 1, dtype=np.uint64)
         offp = self.path_offsets.ctypes.data_as(C.POINTER(C.c_uint64))
-        check(lib.prrtc_results_pack_paths(res, n, None, offp))
-        self.path_data = np.empty(int(self.path_offsets[-1]), dtype=np.float64)
+        # sized from the results' own path lengths (a result without a path has path_len 0)
+        total = int(np.sum(a["path_len"].astype(np.uint64) * (a["path"] != 0))) * dof
+        self.path_data = np.empty(total, dtype=np.float64)
         check(lib.prrtc_results_pack_paths(res, n, _dptr(self.path_data), offp))
+        assert int(self.path_offsets[-1]) == total
 
     @property
     def paths(self) -> list:
