@@ -196,6 +196,10 @@ int prrtc_device_count(void);
 /* CTAs prrtc_plan puts on one problem for params.workers == 0 (the analogue of
  * the reference's hardware_concurrency default, planner.cpp:287-288); or an error. */
 int prrtc_default_workers(int device);
+/* Re-reads the PRRTC_* diagnostic environment switches,
+   which the library otherwise reads once: for callers that change one
+   in-process (tests). */
+int prrtc_debug_reload_env(void);
 /* Host<->device bytes the last prrtc_plan / prrtc_plan_batch call on this
  * device copied (inputs up; result header, controls and paths down). */
 int prrtc_last_transfer_bytes(int device, uint64_t* h2d, uint64_t* d2h);

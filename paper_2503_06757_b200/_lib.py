@@ -106,6 +106,7 @@ SIGNATURES = [
     ("prrtc_last_error", C.c_int, [C.c_char_p, C.c_size_t]),
     ("prrtc_device_count", C.c_int, []),
     ("prrtc_default_workers", C.c_int, [C.c_int]),
+    ("prrtc_debug_reload_env", C.c_int, []),
     ("prrtc_last_transfer_bytes", C.c_int, [C.c_int, C.POINTER(C.c_uint64), C.POINTER(C.c_uint64)]),
     ("prrtc_params_default", None, [C.POINTER(Params)]),
     ("prrtc_robot_create", C.c_int, [C.POINTER(RobotDesc), C.c_int, C.POINTER(P)]),

@@ -66,6 +66,49 @@ int check_device(int device) {
     return PRRTC_OK;
 }
 
+// Diagnostic / A-B environment switches, read once and
+// cached: a getenv per switch per plan call cost microseconds of a ~0.1 ms
+// single-problem call. prrtc_debug_reload_env() re-reads them (tests that
+// change a switch in-process).
+struct EnvKnobs {
+    bool ns32 = false, ns64 = false, ns128 = false, trace = false, host_trace = false, no_map = false;
+    unsigned debug_flags = 0;
+    int tail_claim = 1, mnn_nodes = 0;
+    long long map_bytes = -1;
+    std::string dump_ctl;
+};
+std::atomic<const EnvKnobs*> g_env{nullptr};
+std::mutex g_env_mu;
+
+const EnvKnobs* read_env() {
+    auto* k = new EnvKnobs();
+    auto on = [](const char* n) { return std::getenv(n) != nullptr; };
+    k->ns32 = on("PRRTC_NS32");
+    k->ns64 = on("PRRTC_NS64");
+    k->ns128 = on("PRRTC_NS128");
+    k->trace = on("PRRTC_TRACE");
+    k->host_trace = on("PRRTC_HOST_TRACE");
+    k->no_map = on("PRRTC_NO_MAP");
+    if (const char* e = std::getenv("PRRTC_DEBUG_FLAGS")) k->debug_flags = (unsigned)std::atoi(e);
+    if (const char* e = std::getenv("PRRTC_TAIL_CLAIM")) k->tail_claim = std::atoi(e);
+    if (const char* e = std::getenv("PRRTC_MNN_NODES")) k->mnn_nodes = std::max(1, std::atoi(e));
+    if (const char* e = std::getenv("PRRTC_MAP_BYTES")) k->map_bytes = std::strtoll(e, nullptr, 10);
+    if (const char* e = std::getenv("PRRTC_DUMP_CTL")) k->dump_ctl = e;
+    return k;
+}
+
+const EnvKnobs& env() {
+    const EnvKnobs* k = g_env.load(std::memory_order_acquire);
+    if (k) return *k;
+    std::lock_guard<std::mutex> lk(g_env_mu);
+    k = g_env.load(std::memory_order_relaxed);
+    if (!k) {
+        k = read_env();
+        g_env.store(k, std::memory_order_release);
+    }
+    return *k;
+}
+
 // ---- small FP64 math in the reference's operation order (transform.hpp) ----
 struct M3 {
     double m[9];
@@ -949,9 +992,9 @@ int batch_setup(prrtc_batch* b, const prrtc_robot* robot, const prrtc_scene* con
     // 0.141 -> 0.121 ms, tools/ab_env.sh); PRRTC_NS32 / PRRTC_NS64 force either.
     // (128-state chunks, PRRTC_NS128: Panda median -5% but p95 +2%, Fetch +4%;
     // 64-state chunks in the Panda batch: 159k -> 137k problems/s)
-    const bool ns64 = !std::getenv("PRRTC_NS32") &&
-                      ((n_problems == 1 && b->nthreads == 256) || std::getenv("PRRTC_NS64"));
-    b->ns_max = ns64 ? (std::getenv("PRRTC_NS128") ? 128 : 64) : 32;
+    const EnvKnobs& ek = env();
+    const bool ns64 = !ek.ns32 && ((n_problems == 1 && b->nthreads == 256) || ek.ns64);
+    b->ns_max = ns64 ? (ek.ns128 ? 128 : 64) : 32;
     const int okey = b->ns_max / 32 + (b->nthreads == 256 ? 5 : 0);
     int occ = robot->occ[okey].load(std::memory_order_relaxed);
     if (occ == 0) {
@@ -1078,7 +1121,8 @@ int batch_enqueue(prrtc_batch* b, cudaStream_t st, bool upload) {
     a.n_done = b->d_ndone;
     a.trace = reinterpret_cast<unsigned long long*>(b->d_out + 16);
     a.cta_trace = nullptr;
-    if (std::getenv("PRRTC_TRACE")) {
+    const EnvKnobs& ek = env();
+    if (ek.trace) {
         static long long* d_ct = nullptr;
         static int ct_cap = 0;
         if (ct_cap < b->grid) {
@@ -1091,7 +1135,7 @@ int batch_enqueue(prrtc_batch* b, cudaStream_t st, bool upload) {
         b->cta_trace = d_ct;
     }
     a.epoch = ws->epoch;
-    a.dbg = std::getenv("PRRTC_DEBUG_FLAGS") ? (unsigned)std::atoi(std::getenv("PRRTC_DEBUG_FLAGS")) : 0u;
+    a.dbg = ek.debug_flags;
     a.p.delta = b->params.delta;
     a.p.dd_radius = b->params.dd_radius > 0.0 ? b->params.dd_radius : 4.0 * b->params.delta;
     a.p.n_cc = b->params.n_cc;
@@ -1101,13 +1145,7 @@ int batch_enqueue(prrtc_batch* b, cudaStream_t st, bool upload) {
     a.p.two_stage = b->params.two_stage;
     a.p.deterministic = b->params.deterministic;
     a.ref_stats = b->params.deterministic ? 1 : 0;
-    {
-        static const int tail = [] {
-            const char* e = std::getenv("PRRTC_TAIL_CLAIM");
-            return e ? std::atoi(e) : 1;
-        }();
-        a.tail_claim = tail;
-    }
+    a.tail_claim = ek.tail_claim;
     a.p.budget = b->budget;
     a.p.seed = b->params.seed;
     a.p.uniform = b->params.sampler == PRRTC_SAMPLER_UNIFORM ? 1 : 0;
@@ -1117,12 +1155,12 @@ int batch_enqueue(prrtc_batch* b, cudaStream_t st, bool upload) {
     // per thread): batches trade a longer pass for fewer passes; a single
     // problem is latency-bound (PRRTC_MNN_NODES overrides, for sweeps)
     a.mnn_nodes = b->n == 1 ? kMnnNodesSingle : 2048;
-    if (const char* e = std::getenv("PRRTC_MNN_NODES")) a.mnn_nodes = std::max(1, std::atoi(e));
+    if (ek.mnn_nodes) a.mnn_nodes = ek.mnn_nodes;
     if (b->use_map && ws->d_map) {
         a.out_map = ws->d_map;
         a.out_map_bytes = Workspace::kMapBytes;
-        if (const char* e = std::getenv("PRRTC_MAP_BYTES"))  // tests: force the copy-back fallback
-            a.out_map_bytes = std::min<unsigned long long>(a.out_map_bytes, std::strtoull(e, nullptr, 10));
+        if (ek.map_bytes >= 0)  // tests: force the copy-back fallback
+            a.out_map_bytes = std::min<unsigned long long>(a.out_map_bytes, (unsigned long long)ek.map_bytes);
         a.out_dev = b->d_out;
         a.out_hdr_bytes = Workspace::out_hdr(b->n);
         a.exit_count = reinterpret_cast<unsigned*>(b->d_out + 32);
@@ -1135,7 +1173,7 @@ int batch_enqueue(prrtc_batch* b, cudaStream_t st, bool upload) {
     CUDA_TRY(launch_plan(b->robot->args(), a, b->grid, st));
     const auto e2 = std::chrono::steady_clock::now();
     if (b->timed) CUDA_TRY(cudaEventRecord(ws->ev1, st));
-    if (std::getenv("PRRTC_HOST_TRACE")) {
+    if (ek.host_trace) {
         auto us = [](auto x, auto y) { return std::chrono::duration<double, std::micro>(y - x).count(); };
         std::fprintf(stderr, "prrtc enqueue: copies %.1f ev0 %.1f launch %.1f ev1 %.1f us\n", us(q0, e0),
                      us(e0, e1), us(e1, e2), us(e2, std::chrono::steady_clock::now()));
@@ -1250,7 +1288,7 @@ int fill_results(prrtc_batch* b, prrtc_result* out, const unsigned char* h, cons
     const ProbCtl* ctl = reinterpret_cast<const ProbCtl*>(h + 128);
     float ms = 0.f;
     if (b->timed) cudaEventElapsedTime(&ms, ws->ev0, ws->ev1);
-    if (std::getenv("PRRTC_TRACE")) {  // kernel span vs per-problem span (globaltimer)
+    if (env().trace) {  // kernel span vs per-problem span (globaltimer)
         const auto* tr = reinterpret_cast<const unsigned long long*>(h + 16);
         const long long k0 = (long long)(0x7fffffffffffffffull - tr[0]), k1 = (long long)tr[1];
         long long p0 = ctl[0].t_start_ns, p1 = ctl[0].t_end_ns;
@@ -1262,8 +1300,8 @@ int fill_results(prrtc_batch* b, prrtc_result* out, const unsigned char* h, cons
                      "prrtc trace: events %.3f ms | first CTA -> first init %.3f | inits -> last done %.3f | "
                      "last done -> last CTA exit %.3f | grid %d x %d\n",
                      ms, (p0 - k0) * 1e-6, (p1 - p0) * 1e-6, (k1 - p1) * 1e-6, b->grid, b->nthreads);
-        if (const char* f = std::getenv("PRRTC_DUMP_CTL")) {  // per-problem timeline (analysis tools)
-            if (FILE* o = std::fopen(f, "w")) {
+        if (!env().dump_ctl.empty()) {  // per-problem timeline (analysis tools)
+            if (FILE* o = std::fopen(env().dump_ctl.c_str(), "w")) {
                 for (int i = 0; i < b->n; ++i)
                     std::fprintf(o, "%d %.6f %.6f %llu %d %d\n", i, (ctl[i].t_start_ns - k0) * 1e-6,
                                  (ctl[i].t_end_ns - k0) * 1e-6, (unsigned long long)ctl[i].iters_used, ctl[i].done,
@@ -1507,12 +1545,12 @@ int plan_batch_once(const prrtc_robot* robot, const prrtc_scene* const* scenes, 
     std::lock_guard<std::mutex> lk(g_ws_mu[b.device]);
     Workspace& ws = g_ws[b.device];
     // a single problem reports the host wall clock: no kernel events
-    b.timed = n_problems > 1 || std::getenv("PRRTC_TRACE") || std::getenv("PRRTC_HOST_TRACE");
+    const EnvKnobs& ek = env();
+    b.timed = n_problems > 1 || ek.trace || ek.host_trace;
     // a single problem's result is published by the kernel into mapped host
     // memory (no D2H, no wait for the grid to retire); path re-validation runs
     // a second kernel after the planner, so it keeps the copy-back
-    b.use_map = n_problems == 1 && !params->validate_path && !std::getenv("PRRTC_TRACE") &&
-                !std::getenv("PRRTC_NO_MAP");
+    b.use_map = n_problems == 1 && !params->validate_path && !ek.trace && !ek.no_map;
     const auto t1 = std::chrono::steady_clock::now();
     rc = batch_bind(&b, &ws, scenes, starts, goals);
     const auto t2 = std::chrono::steady_clock::now();
@@ -1522,7 +1560,7 @@ int plan_batch_once(const prrtc_robot* robot, const prrtc_scene* const* scenes, 
     if (rc) return rc;
     const auto t4 = std::chrono::steady_clock::now();
     const double wall = std::chrono::duration<double, std::milli>(t4 - t0).count();
-    if (std::getenv("PRRTC_HOST_TRACE")) {
+    if (ek.host_trace) {
         auto us = [](auto x, auto y) { return std::chrono::duration<double, std::micro>(y - x).count(); };
         float ev = 0.f;
         cudaEventElapsedTime(&ev, ws.ev0, ws.ev1);
@@ -1532,7 +1570,7 @@ int plan_batch_once(const prrtc_robot* robot, const prrtc_scene* const* scenes, 
                      out[0].device_time_ms * 1e3);
     }
     if (n_problems == 1) out[0].wall_time_ms = wall;
-    if (std::getenv("PRRTC_TRACE")) std::fprintf(stderr, "prrtc trace: host wall %.3f ms\n", wall);
+    if (ek.trace) std::fprintf(stderr, "prrtc trace: host wall %.3f ms\n", wall);
     return PRRTC_OK;
 }
 }  // namespace
@@ -1632,6 +1670,12 @@ int prrtc_debug_chunk_queue(uint32_t n_workers, uint32_t n_problems, uint32_t ch
         if (delay_us && delay_us[w]) std::this_thread::sleep_for(std::chrono::microseconds(delay_us[w] * cnt));
         return PRRTC_OK;
     });
+}
+
+int prrtc_debug_reload_env(void) {
+    std::lock_guard<std::mutex> lk(g_env_mu);
+    g_env.store(read_env(), std::memory_order_release);  // (the previous snapshot is leaked: readers may hold it)
+    return PRRTC_OK;
 }
 
 int prrtc_last_transfer_bytes(int device, uint64_t* h2d, uint64_t* d2h) {

@@ -462,6 +462,11 @@ def debug_sample(model, index0: int, n: int, device: int = 0) -> np.ndarray:
     return out
 
 
+def reload_env() -> None:
+    """Make the library re-read its PRRTC_* environment switches (it caches them)."""
+    check(_lib.load().prrtc_debug_reload_env())
+
+
 def device_count() -> int:
     return _lib.load().prrtc_device_count()
 

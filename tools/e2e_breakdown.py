@@ -32,4 +32,5 @@ for _ in range(20):
     tb.append((t2 - t1) * 1e3)
 print(f"C call (incl. ctypes setup) median {np.median(tc):.3f} ms; BatchResult + free {np.median(tb):.3f} ms")
 os.environ["PRRTC_HOST_TRACE"] = "1"
+planner.reload_env()
 planner._plan_batch_raw(model, dsc, S, G, params, 0)
