@@ -15,7 +15,7 @@ fi
 timeout 900 python bench.py ${BENCH_ARGS:-} > "$OUT/bench.json" 2> "$OUT/bench.err"; echo "bench rc=$?" >> "$OUT/bench.err"
 if [ "${SKIP_NCU:-0}" != "1" ]; then
   timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -c 60 --csv \
-      --log-file "$OUT/launches.csv" python bench.py --steps 2 --warmup 3 --latency-samples 10 --no-cpu-baseline \
+      --log-file "$OUT/launches.csv" python bench.py --steps 2 --warmup 3 --latency-samples 10 --no-cpu-baseline --no-parity --no-extras \
       > "$OUT/ncu_bench.log" 2>&1
   timeout 900 ncu --set full --clock-control none --import-source on -k regex:plan_kernel -s 2 -c 1 \
       -o "$OUT/plan_batch" python tools/profile_one.py panda 3 batch > "$OUT/ncu_full.log" 2>&1
