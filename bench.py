@@ -291,7 +291,16 @@ def _stats(ok, cost, res_paths):
             "cost_median": float(np.median(c)) if c else None, "cost_mean": float(np.mean(c)) if c else None}
 
 
-PARITY_SUBSET = {("fetch", 16): 500, ("baxter", 16): 200}  # bounds the reference's 16-thread arms' time
+PARITY_SUBSET = {("baxter", 16): 300}  # bounds the reference's 16-thread Baxter arm's time (~0.2 s per problem)
+
+
+def _z(p1, p2, n1, n2):
+    """Two-proportion z score of p1 - p2 (pooled): |z| < 2 is within sampling noise."""
+    if p1 is None or p2 is None:
+        return None
+    p = (p1 * n1 + p2 * n2) / (n1 + n2)
+    se = (p * (1 - p) * (1 / n1 + 1 / n2)) ** 0.5
+    return (p1 - p2) / se if se > 0 else 0.0
 
 
 def parity_block(robot_names, workers_list, n, device=0, tree_capacity=200000, threads=None, subset=None):
@@ -387,6 +396,10 @@ def parity_block(robot_names, workers_list, n, device=0, tree_capacity=200000, t
                                       "iterations_mean": float(np.mean([r.iterations_total for r in sr])),
                                       "problems_per_s_e2e": len(S) / (p_ms / 1e3), "ctas_per_problem": W}
             row["success_not_below_reference"] = row["b200"]["success"] >= row["reference"]["success"]
+            row["success_z_b200_minus_ref"] = _z(row["b200"]["success"], row["reference"]["success"], len(S), len(S))
+            if "b200_single" in row:
+                row["success_z_single_minus_ref"] = _z(row["b200_single"]["success"], row["reference"]["success"],
+                                                       len(S), len(S))
             rr[f"W{W}"] = row
         out["robots"][robot] = rr
     return out
@@ -778,6 +791,10 @@ def run_b200(args):
                 f"{r}_W{w}": {"success_b200": v[f"W{w}"]["b200"]["success"],
                               "success_ref": v[f"W{w}"]["reference"]["success"],
                               "success_b200_single": v[f"W{w}"].get("b200_single", {}).get("success"),
+                              "z_batch": v[f"W{w}"]["success_z_b200_minus_ref"],
+                              "z_single": v[f"W{w}"].get("success_z_single_minus_ref"),
+                              "problems": v[f"W{w}"]["problems"],
+                              "cost_med_b200_single": v[f"W{w}"].get("b200_single", {}).get("cost_median"),
                               "cost_med_b200": v[f"W{w}"]["b200"]["cost_median"],
                               "cost_med_ref": v[f"W{w}"]["reference"]["cost_median"],
                               "valid_ncc": [v[f"W{w}"]["b200"]["valid_ncc"], v[f"W{w}"]["reference"]["valid_ncc"]],
