@@ -594,6 +594,10 @@ enum : int {
     MSG_MEET = 6
 };
 
+// set by the CTA whose finish_problem settled the problem (single-problem
+// launches publish the result from that CTA, see publish_result)
+__shared__ int g_finisher;
+
 __device__ void finish_problem(const PlanArgs& a, int prob, int done, int msg) {
     ProbCtl& C = a.ctl[prob];
     if (atomicCAS(&C.done, DONE_RUNNING, -1) == DONE_RUNNING) {  // claim
@@ -602,6 +606,7 @@ __device__ void finish_problem(const PlanArgs& a, int prob, int done, int msg) {
         __threadfence();
         st_release(&C.done, done);
         atomicAdd(a.n_done, 1);
+        g_finisher = 1;
     }
 }
 
@@ -816,20 +821,18 @@ __device__ void leave_problem(const PlanArgs& a, int prob, int reason_msg) {
 
 __shared__ Ctx g_ctx;  // the planner's CTA context (see ctx_writer)
 
-// Single-problem launches: the last CTA to finish copies the out-header,
-// controls and used path arena into mapped pinned host memory and raises a
-// flag there (out_map[0] = epoch, out_map[1] = 1 if it fit), so the host
-// reads the result without a D2H copy and without waiting for the grid to
-// retire. Every CTA fences its own stores before counting itself out.
+// Single-problem launches: the CTA that settled the problem (the winner, the
+// last worker out of a failed problem, or the endpoint check) copies the
+// out-header, controls and used path arena into mapped pinned host memory as
+// soon as it has left the problem, and raises a flag there (out_map[0] =
+// epoch, out_map[1] = 1 if it fit): the host reads the result without a D2H
+// copy and without waiting for the other CTAs to notice the settled problem
+// and retire. (CheckStats / iteration counters of CTAs still leaving are not
+// in that snapshot; with one CTA — deterministic mode — they are exact.)
 __device__ void publish_result(Ctx& c, const PlanArgs& a) {
     const int tid = threadIdx.x;
     __syncthreads();
-    if (tid == 0) {
-        __threadfence();
-        sh(c.ictl)[IC_TMP1] = atomicAdd(a.exit_count, 1u) == gridDim.x - 1;
-    }
-    __syncthreads();
-    if (!sh(c.ictl)[IC_TMP1]) return;
+    if (!g_finisher) return;
     __threadfence();
     const unsigned long long used = min(__ldcg(a.arena_used), a.arena_cap);
     const unsigned long long words = (a.out_hdr_bytes >> 3) + used;  // 8-byte words: header, controls, arena
@@ -862,6 +865,7 @@ __global__ void __launch_bounds__(NT, MINB) plan_kernel(PlanArgs a) {
     build_ttab(c, a.p.n_cc);
     if (tid == 0) c.ref_stats = a.ref_stats;
     __syncthreads();
+    if (tid == 0) g_finisher = 0;
     const double R = a.p.dd_radius, delta = a.p.delta;
     if (tid == 0 && a.trace) atomicMax(&a.trace[0], 0x7fffffffffffffffull - (unsigned long long)globaltimer());
     if (tid == 0 && a.cta_trace) {
