@@ -793,6 +793,7 @@ struct Workspace {
     int* d_dd = nullptr;
     unsigned* d_ready = nullptr;
     int* d_vprefix = nullptr;  // [n + 1] path-edge prefix (validate_path)
+    unsigned* d_init = nullptr;  // inline-input launches: the init word (epoch of the last zeroing)
     cudaEvent_t ev0 = nullptr, ev1 = nullptr;
     cudaStream_t stream = nullptr;
     UseMarkP mark;  // recorded after every launch (scenes it read wait on it before an update)
@@ -814,6 +815,7 @@ struct Workspace {
         cudaFree(d_dd);
         cudaFree(d_ready);
         cudaFree(d_vprefix);
+        cudaFree(d_init);
         if (ev0) cudaEventDestroy(ev0);
         if (ev1) cudaEventDestroy(ev1);
         if (stream) cudaStreamDestroy(stream);
@@ -853,13 +855,15 @@ struct Workspace {
             cudaMalloc(&d_parent, 4 * nnodes) != cudaSuccess ||
             cudaMalloc(&d_dd, 4 * nnodes) != cudaSuccess ||
             cudaMalloc(&d_ready, 4 * nnodes) != cudaSuccess ||
-            cudaMalloc(&d_vprefix, 4 * (nn + 1)) != cudaSuccess) {
+            cudaMalloc(&d_vprefix, 4 * (nn + 1)) != cudaSuccess ||
+            cudaMalloc(&d_init, 4) != cudaSuccess) {
             release();
             return set_err(PRRTC_ENOMEM, "plan: device workspace allocation failed (" +
                                              std::to_string((8 * nd + 12) * nnodes) + " bytes of trees)");
         }
         // ready flags are epoch tagged: zero once, launches use epoch >= 1
         cudaMemset(d_ready, 0, 4 * nnodes);
+        cudaMemset(d_init, 0, 4);  // epochs start at 1
         // optional: without a mapped block results come back by D2H copy
         if (cudaHostAlloc(&h_map, kMapBytes, cudaHostAllocMapped) == cudaSuccess) {
             std::memset(h_map, 0, kMapBytes);
@@ -1092,12 +1096,29 @@ int batch_enqueue(prrtc_batch* b, cudaStream_t st, bool upload) {
     b->last_stream = st;
     if (++ws->epoch == 0) ++ws->epoch;
     const size_t up = out_offset(b) + Workspace::out_hdr(b->n);
-    ws->last_h2d = upload ? up : 0;
-    if (upload)  // inputs + zeroed out-header in one copy
+    // a single problem published through mapped memory needs no copy at all:
+    // start, goal and scene travel in the kernel parameters and the kernel
+    // zeroes its own controls (PlanArgs::inline_inputs)
+    const bool inline_in = upload && b->n == 1 && b->use_map && ws->d_map && b->dof <= 32 && !env().trace;
+    ws->last_h2d = upload && !inline_in ? up : 0;
+    if (inline_in) {
+        // (no copy)
+    } else if (upload) {  // inputs + zeroed out-header in one copy
         CUDA_TRY(cudaMemcpyAsync(ws->d_in, ws->h_io, up, cudaMemcpyHostToDevice, st));
-    else
+    } else {
         CUDA_TRY(cudaMemsetAsync(b->d_out, 0, Workspace::out_hdr(b->n), st));
+    }
     PlanArgs a{};
+    if (inline_in) {
+        const unsigned char* h = static_cast<const unsigned char*>(ws->h_io);  // batch_bind's staging
+        std::memcpy(a.in_sg, h, 8 * 2 * (size_t)b->dof);
+        size_t o = 8 * 2 * (size_t)b->dof;
+        std::memcpy(&a.scene_words1, h + o, sizeof(void*));
+        o += sizeof(void*);
+        std::memcpy(&a.scene_f64_1, h + o, sizeof(SceneF64));
+        a.inline_inputs = 1;
+        a.init_flag = ws->d_init;
+    }
     a.robot = b->robot->d_words;
     a.fine_r64 = b->robot->d_fine_r64;
     a.limits = b->robot->d_limits;
@@ -1119,7 +1140,7 @@ int batch_enqueue(prrtc_batch* b, cudaStream_t st, bool upload) {
     a.arena_cap = b->arena;
     a.next_problem = b->d_next;
     a.n_done = b->d_ndone;
-    a.trace = reinterpret_cast<unsigned long long*>(b->d_out + 16);
+    a.trace = inline_in ? nullptr : reinterpret_cast<unsigned long long*>(b->d_out + 16);
     a.cta_trace = nullptr;
     const EnvKnobs& ek = env();
     if (ek.trace) {

@@ -163,6 +163,14 @@ struct PlanArgs {
     int mnn_nodes;                      // multi-sample NN bound: m <= mnn_nodes / tree size
     int ref_stats;                      // exact CheckStats (reference counting semantics): deterministic mode
     int tail_claim;                     // smaller ticket blocks near a problem's budget end
+    // single-problem launches with inline inputs (no H2D copy): start and goal
+    // travel in the kernel parameters, CTA 0 zeroes the out-header and the
+    // controls and releases *init_flag = epoch, the other CTAs acquire it
+    int inline_inputs;
+    unsigned* init_flag;
+    const uint32_t* scene_words1;
+    SceneF64 scene_f64_1;
+    double in_sg[2 * 32];               // start[dof], then goal[dof]
 };
 
 // Dynamic shared memory bytes for a robot/scene/ns_max combination.

@@ -618,8 +618,8 @@ __device__ bool init_problem(Ctx& c, const PlanArgs& a, int prob) {
     double* S = dc(c, DC_A);
     double* G = dc(c, DC_B);
     if (tid < dof) {
-        S[tid] = a.starts[(size_t)prob * dof + tid];
-        G[tid] = a.goals[(size_t)prob * dof + tid];
+        S[tid] = a.inline_inputs ? a.in_sg[tid] : a.starts[(size_t)prob * dof + tid];
+        G[tid] = a.inline_inputs ? a.in_sg[dof + tid] : a.goals[(size_t)prob * dof + tid];
     }
     if (tid == 0) C.t_start_ns = globaltimer();
     __syncthreads();
@@ -866,6 +866,24 @@ __global__ void __launch_bounds__(NT, MINB) plan_kernel(PlanArgs a) {
     if (tid == 0) c.ref_stats = a.ref_stats;
     __syncthreads();
     if (tid == 0) g_finisher = 0;
+    if (a.inline_inputs) {
+        // no H2D copy: CTA 0 zeroes the out-header and the problem's
+        // controls, then releases the init word (its own buffer); the other
+        // CTAs acquire it before they touch either (all CTAs of a
+        // single-problem launch are co-resident)
+        if (blockIdx.x == 0) {
+            unsigned* hdr = const_cast<unsigned*>(reinterpret_cast<const unsigned*>(a.out_dev));
+            const int hwords = (int)(a.out_hdr_bytes >> 2);
+            for (int i = tid; i < hwords; i += c.nthreads) hdr[i] = 0u;
+            __threadfence();
+            __syncthreads();
+            if (tid == 0) st_release_u(a.init_flag, a.epoch);
+        } else {
+            if (tid == 0)
+                while (ld_acquire_u(a.init_flag) != a.epoch) __nanosleep(32);
+            __syncthreads();
+        }
+    }
     const double R = a.p.dd_radius, delta = a.p.delta;
     if (tid == 0 && a.trace) atomicMax(&a.trace[0], 0x7fffffffffffffffull - (unsigned long long)globaltimer());
     if (tid == 0 && a.cta_trace) {
@@ -882,8 +900,12 @@ __global__ void __launch_bounds__(NT, MINB) plan_kernel(PlanArgs a) {
             const int p = sh(c.ictl)[IC_TMP1];
             __syncthreads();
             if (p >= a.n_problems) break;
-            const int si = a.prob_scene[p];
-            load_scene(c, sbase, a.scene_words[si], a.scene_f64[si]);
+            if (a.inline_inputs) {
+                load_scene(c, sbase, a.scene_words1, a.scene_f64_1);
+            } else {
+                const int si = a.prob_scene[p];
+                load_scene(c, sbase, a.scene_words[si], a.scene_f64[si]);
+            }
             if (tid == 0) atomicAdd(&a.ctl[p].active, 1);
             if (init_problem(c, a, p)) {
                 prob = p;
@@ -897,8 +919,12 @@ __global__ void __launch_bounds__(NT, MINB) plan_kernel(PlanArgs a) {
             if (a.p.deterministic) break;
             prob = pick_help(c, a);
             if (prob < 0) break;
-            const int si = a.prob_scene[prob];
-            load_scene(c, sbase, a.scene_words[si], a.scene_f64[si]);
+            if (a.inline_inputs) {
+                load_scene(c, sbase, a.scene_words1, a.scene_f64_1);
+            } else {
+                const int si = a.prob_scene[prob];
+                load_scene(c, sbase, a.scene_words[si], a.scene_f64[si]);
+            }
         }
         ProbCtl& C = a.ctl[prob];
         if (tid == 0) {  // the roots: written by this CTA, or acquired through `started` (pick_help)
@@ -1258,11 +1284,23 @@ cudaError_t raise_smem_limit(const void* fn, int sm) {
     static std::map<std::pair<const void*, int>, int> set;
     int dev = 0;
     cudaGetDevice(&dev);
+    // per-thread fast path: the limits only ever grow, so a (kernel, device)
+    // this thread has seen at >= sm needs no lock
+    thread_local const void* last_fn = nullptr;
+    thread_local int last_dev = -1, last_sm = 0;
+    if (fn == last_fn && dev == last_dev && sm <= last_sm) return cudaSuccess;
     std::lock_guard<std::mutex> lk(mu);
     int& cur = set[{fn, dev}];
-    if (sm <= cur) return cudaSuccess;
-    const cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, sm);
-    if (e == cudaSuccess) cur = sm;
+    cudaError_t e = cudaSuccess;
+    if (sm > cur) {
+        e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, sm);
+        if (e == cudaSuccess) cur = sm;
+    }
+    if (e == cudaSuccess) {
+        last_fn = fn;
+        last_dev = dev;
+        last_sm = cur;
+    }
     return e;
 }
 
