@@ -586,7 +586,7 @@ def run_reference(args):
 def table_one(dev, robot, params_fn, n_lat, peak):
     """Table-I figures of one robot (statistics as
     bench.cpp:90-109): single-problem prrtc_plan latency at the device's
-    default worker count (one 256-thread CTA per SM) on a spread sample, its
+    default worker count (one 512-thread CTA per SM) on a spread sample, its
     success and cost, and the FP32 roofline fraction of plan_kernel over those
     launches (algorithmic flops / device time); plus the 1000-problem batch at
     the headline params (problems/s, success)."""
@@ -801,7 +801,7 @@ def run_b200(args):
                               "valid_4ncc": [v[f"W{w}"]["b200"]["valid_4ncc"], v[f"W{w}"]["reference"]["valid_4ncc"]]}
                 for r, v in parity["robots"].items() for w in (1, 16)}
         line["latency_ms"] = {**lat["workers0"], "by_workers": lat,
-                              "api": "prrtc_plan, host wall clock; workers0 = one 256-thread CTA per SM"}
+                              "api": "prrtc_plan, host wall clock; workers0 = one 512-thread CTA per SM"}
         print(json.dumps(line))
     if world > 1:
         import torch.distributed as dist

@@ -123,7 +123,7 @@ typedef struct prrtc_scene_desc {
  *
  *  workers          reference: concurrent worker iterations (0 = hardware
  *                   concurrency). Here: CTAs working on one problem in
- *                   prrtc_plan (0 = one 256-thread CTA per SM). The per-problem iteration
+ *                   prrtc_plan (0 = one 512-thread CTA per SM). The per-problem iteration
  *                   budget is workers_effective * max_iters_per_worker.
  *  tree_capacity    total across both trees, split in half (planner.cpp:290).
  *  nn_partitions    accepted for API parity; the device scan always splits
@@ -147,7 +147,8 @@ typedef struct prrtc_params {
     int32_t sampler;               /* PRRTC_SAMPLER_HALTON */
     uint64_t seed;                 /* 0 */
     /* --- device knobs (no reference equivalent) --- */
-    uint32_t threads_per_cta;      /* 0 = 128 */
+    uint32_t threads_per_cta;      /* 0 = automatic: 512 for one problem, 128 (256 for large
+                                      robots) for batches; else 128, 256 or 512 */
     uint32_t ctas_per_sm;          /* 0 = as many as co-reside */
     uint32_t deterministic;        /* 1 = single CTA, Halton stride 1: replays
                                       the reference's workers=1 mode */
@@ -336,7 +337,9 @@ int prrtc_debug_sample(const prrtc_robot* robot, uint64_t index0, uint32_t n, do
 /* clock64 stamps of one 32-state validation chunk in one CTA (latency
    profiling): [0] kernel start, [7] after setup, [8] after state generation,
    [1] check start, [2] FK local transforms, [3] FK compose, [4] FK done,
-   [5] coarse stage done, [6] fine env stage done (if reached), [9] chunk done. */
+   [10] warp 0's coarse environment tests done, [11] its coarse self pairs
+   done, [5] coarse stage done (all warps), [6] fine env stage done (if
+   reached), [9] chunk done. */
 int prrtc_debug_chunk_profile(const prrtc_robot* robot, const prrtc_scene* scene, const double* from,
                               const double* to, uint32_t dof, int32_t n_cc, int two_stage,
                               long long* stamps);

@@ -210,7 +210,7 @@ struct prrtc_robot {
     double* d_fine_r64 = nullptr;
     double* d_limits = nullptr;
     double reach = 0.0;           // bound on |posed sphere| (m)
-    mutable std::atomic<int> occ[10] = {};  // planner CTAs per SM, by (ns_max / 32, CTA size)
+    mutable std::atomic<int> occ[15] = {};  // planner CTAs per SM, by (ns_max / 32, CTA size)
     RobotArgs args() const {
         RobotArgs r;
         r.words = d_words;
@@ -299,7 +299,7 @@ int prrtc_default_workers(int device) {
     if (rc) return rc;
     int n = 0;
     cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, device);
-    return n > 0 ? n : 1;  // one 256-thread CTA per SM (batch_setup)
+    return n > 0 ? n : 1;  // one 512-thread CTA per SM (batch_setup)
 }
 
 void prrtc_params_default(prrtc_params* p) {  // planner.hpp:21-40
@@ -938,8 +938,8 @@ int check_params(const prrtc_params* p) {  // planner.cpp:250-252
     if (!(p->delta > 0.0)) return set_err(PRRTC_EINVAL, "plan: delta must be positive");
     if (p->n_cc < 1) return set_err(PRRTC_EINVAL, "plan: n_cc must be >= 1");
     if (p->tree_capacity < 2) return set_err(PRRTC_EINVAL, "plan: tree_capacity too small");
-    if (p->threads_per_cta != 0 && p->threads_per_cta != 128 && p->threads_per_cta != 256)
-        return set_err(PRRTC_EINVAL, "plan: threads_per_cta must be 0, 128 or 256");
+    if (p->threads_per_cta != 0 && p->threads_per_cta != 128 && p->threads_per_cta != 256 && p->threads_per_cta != 512)
+        return set_err(PRRTC_EINVAL, "plan: threads_per_cta must be 0, 128, 256 or 512");
     if (p->sampler != PRRTC_SAMPLER_HALTON && p->sampler != PRRTC_SAMPLER_UNIFORM)
         return set_err(PRRTC_EINVAL, "plan: unknown sampler");
     return PRRTC_OK;
@@ -982,13 +982,17 @@ int batch_setup(prrtc_batch* b, const prrtc_robot* robot, const prrtc_scene* con
     b->params = *params;
     b->cap = std::max<long long>(2, (long long)(params->tree_capacity / 2));  // planner.cpp:290
     b->stride = (b->cap + 31) / 32 * 32;
-    // CTA size (threads_per_cta = 0): a single problem gets 256-thread CTAs
+    // CTA size (threads_per_cta = 0): a single problem gets 512-thread CTAs
     // (the extra warps split the chunk's links / primitives / pairs: lower
     // latency per iteration); batches use 128-thread CTAs (more independent
     // workers per SM) unless the robot is large (many fine spheres or self
     // pairs, e.g. the dual-arm Baxter), where the split pays again
     const bool heavy = robot->n_fine > 64 || robot->n_pairs > 48;
-    b->nthreads = params->threads_per_cta ? (int)params->threads_per_cta : (n_problems == 1 || heavy ? 256 : 128);
+    // a single problem: 512-thread CTAs, one per SM (16 warps split each
+    // chunk's links / primitives / pairs: measured -3% / -6% / -21% median
+    // latency for Panda / Fetch / Baxter against 256, tools/lat_variants.py)
+    b->nthreads = params->threads_per_cta ? (int)params->threads_per_cta
+                                          : (n_problems == 1 ? 512 : (heavy ? 256 : 128));
     // states per validation chunk: one n_cc = 32 edge; a 256-thread CTA uses
     // its extra warps to split links / pairs / primitives of the same chunk.
     // A single problem (latency-bound, one CTA per SM) takes 64-state chunks:
@@ -997,9 +1001,9 @@ int batch_setup(prrtc_batch* b, const prrtc_robot* robot, const prrtc_scene* con
     // (128-state chunks, PRRTC_NS128: Panda median -5% but p95 +2%, Fetch +4%;
     // 64-state chunks in the Panda batch: 159k -> 137k problems/s)
     const EnvKnobs& ek = env();
-    const bool ns64 = !ek.ns32 && ((n_problems == 1 && b->nthreads == 256) || ek.ns64);
+    const bool ns64 = !ek.ns32 && ((n_problems == 1 && b->nthreads >= 256) || ek.ns64);
     b->ns_max = ns64 ? (ek.ns128 ? 128 : 64) : 32;
-    const int okey = b->ns_max / 32 + (b->nthreads == 256 ? 5 : 0);
+    const int okey = b->ns_max / 32 + (b->nthreads == 256 ? 5 : (b->nthreads == 512 ? 10 : 0));
     int occ = robot->occ[okey].load(std::memory_order_relaxed);
     if (occ == 0) {
         occ = plan_occupancy(robot->args(), b->ns_max, b->nthreads);
@@ -1011,10 +1015,10 @@ int batch_setup(prrtc_batch* b, const prrtc_robot* robot, const prrtc_scene* con
         b->grid = 1;
         workers_eff = 1;
     } else if (n_problems == 1) {
-        // workers = 0: one 256-thread CTA per SM (measured: ~64-148 CTAs give
+        // workers = 0: one CTA per SM (measured: ~64-148 CTAs give
         // the lowest time-to-solution; 2 per SM only adds redundant work)
         b->grid = (int)(params->workers ? std::min<unsigned>(params->workers, sms * occ)
-                                        : (b->nthreads == 256 ? sms : 2 * sms));
+                                        : (b->nthreads >= 256 ? sms : 2 * sms));
         workers_eff = b->grid;
     } else {
         const unsigned per_sm = params->ctas_per_sm ? std::min<unsigned>(params->ctas_per_sm, occ) : occ;

@@ -942,7 +942,7 @@ __device__ __forceinline__ void check_chunk_inl(Ctx& c, int cnt, bool two_stage,
     // sub-ranges), states over lanes
     int flagged = 0;
     {
-        const int T = L * v.P, nwlog = 31 - __clz(nw);  // nw: 4 or 8
+        const int T = L * v.P, nwlog = 31 - __clz(nw);  // nw: 4, 8 or 16
         const int lo = (T * warp) >> nwlog, hi = (T * (warp + 1)) >> nwlog;
         int l = v.P ? lo / v.P : 0, p0 = lo - l * v.P;  // one division per warp, then walk
         for (int i = lo; i < hi; ++l, p0 = 0) {
@@ -963,6 +963,7 @@ __device__ __forceinline__ void check_chunk_inl(Ctx& c, int cnt, bool two_stage,
             }
         }
     }
+    if (prof && tid == 0) prof[10] = clock64();  // warp 0's share of the coarse env tests done
     // coarse self pairs (collision.cpp:174-183): pairs over warps, states
     // over lanes; a lane collects its state's pair bits of each 64-pair word
     // in a register and ORs them once
@@ -990,6 +991,7 @@ __device__ __forceinline__ void check_chunk_inl(Ctx& c, int cnt, bool two_stage,
         flagged |= pm != 0;
     }
     if (stop_flag && tid == 0) k.ictl[IC_STOP] = stop;
+    if (prof && tid == 0) prof[11] = clock64();  // warp 0's self pairs done
     const int any_flag = __syncthreads_or(flagged);
     if (prof && tid == 0) prof[5] = clock64();
     if (!any_flag) return;  // nothing flagged: every state free

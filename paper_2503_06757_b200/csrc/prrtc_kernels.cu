@@ -1318,6 +1318,7 @@ cudaError_t launch_validate_paths(const RobotArgs& r, const PlanArgs& a, int* pr
 using PlanFn = void (*)(PlanArgs);
 static PlanFn plan_fn(int nthreads) {
     if (nthreads == 256) return plan_kernel<256, 2>;
+    if (nthreads == 512) return plan_kernel<512, 1>;
     static const int minb = [] {
         const char* e = getenv("PRRTC_PLAN_MINB");
         return e ? atoi(e) : 4;

@@ -10,8 +10,9 @@ robot = sys.argv[1] if len(sys.argv) > 1 else "panda"
 d = np.load(Path(__file__).resolve().parents[1] / "tests" / "golden" / f"problems_{robot}.npz")
 m = robots.get(robot)
 rob = planner.device_robot(m)
-names = {0: "start", 7: "setup", 8: "gen", 1: "chk", 2: "fkA", 3: "fkB", 4: "fkC", 5: "coarse", 6: "fine_env", 9: "end"}
-order = [0, 7, 8, 1, 2, 3, 4, 5, 6, 9]
+names = {0: "start", 7: "setup", 8: "gen", 1: "chk", 2: "fkA", 3: "fkB", 4: "fkC", 10: "coarse_env(w0)",
+         11: "self_pairs(w0)", 5: "coarse_sync", 6: "fine_env", 9: "end"}
+order = [0, 7, 8, 1, 2, 3, 4, 10, 11, 5, 6, 9]
 for i in (0, 400, 700):
     sc = planner.device_scene(make_scene(robot, str(d["kind"][i]), int(d["pid"][i]))[0])
     s, g = d["start"][i], d["goal"][i]
