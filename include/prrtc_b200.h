@@ -42,7 +42,7 @@
 extern "C" {
 #endif
 
-#define PRRTC_API_VERSION 1
+#define PRRTC_API_VERSION 2
 
 /* Limits of the device implementation (checked at handle creation). */
 #define PRRTC_MAX_DOF 32
@@ -148,7 +148,9 @@ typedef struct prrtc_params {
     uint64_t seed;                 /* 0 */
     /* --- device knobs (no reference equivalent) --- */
     uint32_t threads_per_cta;      /* 0 = automatic: 512 for one problem, 128 (256 for large
-                                      robots) for batches; else 128, 256 or 512 */
+                                      robots) for batches; else 128, 256 or 512; 32 = a
+                                      batch on the warp-worker planner (one worker per
+                                      warp; not for deterministic / Uniform-sampler runs) */
     uint32_t ctas_per_sm;          /* 0 = as many as co-reside */
     uint32_t deterministic;        /* 1 = single CTA, Halton stride 1: replays
                                       the reference's workers=1 mode */
@@ -159,6 +161,16 @@ typedef struct prrtc_params {
                                       prrtc_plan / prrtc_plan_batch re-plan a problem whose
                                       path fails it with the next seed (up to 4 times) and
                                       never return such a path (status FAILED instead) */
+    uint32_t max_workers_per_problem; /* batches: the most workers (CTAs or warp workers)
+                                      one problem may have at once. 0 = elastic: a worker
+                                      that finds no unstarted problem joins the running
+                                      problem with the fewest workers that still has
+                                      budget (shorter batch tails, more parallel search).
+                                      W = at most W; with workers = 1 and 1 here each
+                                      problem runs exactly the reference's workers=1
+                                      search (planner.cpp:186-242: Halton stream
+                                      1+seed+k, same iterations, same result) */
+    uint32_t _pad2;
 } prrtc_params;
 
 /* Result of one planning problem: reference PlanResult (planner.hpp:42-51). */

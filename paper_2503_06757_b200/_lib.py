@@ -71,6 +71,8 @@ class Params(C.Structure):
         ("ctas_per_sm", C.c_uint32),
         ("deterministic", C.c_uint32),
         ("validate_path", C.c_uint32),
+        ("max_workers_per_problem", C.c_uint32),
+        ("_pad2", C.c_uint32),
     ]
 
 

@@ -22,7 +22,7 @@ CSRC = PKG / "csrc"
 LIB_DIR = PKG / "lib"
 LIB = LIB_DIR / "libprrtc_b200.so"
 SOURCES = ["prrtc_kernels.cu", "prrtc_capi.cu"]
-HEADERS = ["prrtc_device.cuh", "prrtc_internal.h", "prrtc_launch.h"]
+HEADERS = ["prrtc_device.cuh", "prrtc_internal.h", "prrtc_launch.h", "prrtc_warp.cuh"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 NVCC_FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "--expt-relaxed-constexpr"]
 

@@ -74,6 +74,8 @@ struct EnvKnobs {
     bool ns32 = false, ns64 = false, ns128 = false, trace = false, host_trace = false, no_map = false;
     unsigned debug_flags = 0;
     int tail_claim = 1, mnn_nodes = 0;
+    int warp = -1;  // PRRTC_WARP=1: eligible batches on the warp-worker planner (A/B runs)
+    int help_cap = 0;  // PRRTC_HELP_CAP: most workers a help join may bring a problem to (sweeps)
     long long map_bytes = -1;
     std::string dump_ctl;
 };
@@ -91,6 +93,8 @@ const EnvKnobs* read_env() {
     k->no_map = on("PRRTC_NO_MAP");
     if (const char* e = std::getenv("PRRTC_DEBUG_FLAGS")) k->debug_flags = (unsigned)std::atoi(e);
     if (const char* e = std::getenv("PRRTC_TAIL_CLAIM")) k->tail_claim = std::atoi(e);
+    if (const char* e = std::getenv("PRRTC_WARP")) k->warp = std::atoi(e);
+    if (const char* e = std::getenv("PRRTC_HELP_CAP")) k->help_cap = std::atoi(e);
     if (const char* e = std::getenv("PRRTC_MNN_NODES")) k->mnn_nodes = std::max(1, std::atoi(e));
     if (const char* e = std::getenv("PRRTC_MAP_BYTES")) k->map_bytes = std::strtoll(e, nullptr, 10);
     if (const char* e = std::getenv("PRRTC_DUMP_CTL")) k->dump_ctl = e;
@@ -911,6 +915,10 @@ struct prrtc_batch {
     prrtc_params params{};
     long long cap = 0, stride = 0;
     int grid = 0, nthreads = 128, ns_max = 32;
+    // warp-worker planner (plan_warp_kernel): eligible batches run one worker
+    // per warp, `warps` warps in one CTA per SM (0: the CTA planner runs it)
+    bool warp_ok = false;
+    int warps = 0, cta_grid = 0, scene_words_max = 0;
     unsigned long long budget = 0, arena = 0;
     cudaStream_t last_stream = 0;
     int launches = 0;
@@ -938,11 +946,25 @@ int check_params(const prrtc_params* p) {  // planner.cpp:250-252
     if (!(p->delta > 0.0)) return set_err(PRRTC_EINVAL, "plan: delta must be positive");
     if (p->n_cc < 1) return set_err(PRRTC_EINVAL, "plan: n_cc must be >= 1");
     if (p->tree_capacity < 2) return set_err(PRRTC_EINVAL, "plan: tree_capacity too small");
-    if (p->threads_per_cta != 0 && p->threads_per_cta != 128 && p->threads_per_cta != 256 && p->threads_per_cta != 512)
-        return set_err(PRRTC_EINVAL, "plan: threads_per_cta must be 0, 128, 256 or 512");
+    if (p->threads_per_cta != 0 && p->threads_per_cta != 32 && p->threads_per_cta != 128 &&
+        p->threads_per_cta != 256 && p->threads_per_cta != 512)
+        return set_err(PRRTC_EINVAL, "plan: threads_per_cta must be 0, 32, 128, 256 or 512");
     if (p->sampler != PRRTC_SAMPLER_HALTON && p->sampler != PRRTC_SAMPLER_UNIFORM)
         return set_err(PRRTC_EINVAL, "plan: unknown sampler");
     return PRRTC_OK;
+}
+
+// the largest dynamic shared memory a CTA may opt into (cached per device)
+int smem_optin(int device) {
+    static std::atomic<int> cache[64];
+    if (device < 0 || device >= 64) return 48 * 1024;
+    int v = cache[device].load(std::memory_order_relaxed);
+    if (!v) {
+        cudaDeviceGetAttribute(&v, cudaDevAttrMaxSharedMemoryPerBlockOptin, device);
+        if (v <= 0) v = 48 * 1024;
+        cache[device].store(v, std::memory_order_relaxed);
+    }
+    return v;
 }
 
 int sm_count(int device) {
@@ -991,8 +1013,21 @@ int batch_setup(prrtc_batch* b, const prrtc_robot* robot, const prrtc_scene* con
     // a single problem: 512-thread CTAs, one per SM (16 warps split each
     // chunk's links / primitives / pairs: measured -3% / -6% / -21% median
     // latency for Panda / Fetch / Baxter against 256, tools/lat_variants.py)
-    b->nthreads = params->threads_per_cta ? (int)params->threads_per_cta
-                                          : (n_problems == 1 ? 512 : (heavy ? 256 : 128));
+    b->nthreads = params->threads_per_cta && params->threads_per_cta != 32
+                      ? (int)params->threads_per_cta
+                      : (n_problems == 1 ? 512 : (heavy ? 256 : 128));
+    const EnvKnobs& ekw = env();
+    // threads_per_cta = 32: the warp-worker planner (one RRT-Connect worker
+    // per warp, plan_warp_kernel) — for batches whose mode allows it (not
+    // deterministic replay with its exact CheckStats, not the Uniform
+    // sampler's per-CTA generator, no phase tracer or debug flags). Measured
+    // against the CTA planner: Fetch batches of 3k-10k
+    // problems 11-25% faster, Panda's 1000-problem headline 1.6x slower (its
+    // tail is per-problem latency, which one warp stretches), so it is not
+    // the default. PRRTC_WARP=1 selects it for every eligible batch (A/B).
+    b->warp_ok = n_problems > 1 && !params->deterministic && params->sampler == PRRTC_SAMPLER_HALTON &&
+                 !ekw.trace && ekw.debug_flags == 0 &&
+                 (params->threads_per_cta == 32 || (params->threads_per_cta == 0 && ekw.warp == 1));
     // states per validation chunk: one n_cc = 32 edge; a 256-thread CTA uses
     // its extra warps to split links / pairs / primitives of the same chunk.
     // A single problem (latency-bound, one CTA per SM) takes 64-state chunks:
@@ -1031,6 +1066,7 @@ int batch_setup(prrtc_batch* b, const prrtc_robot* robot, const prrtc_scene* con
         workers_eff = params->workers ? params->workers : kBatchWorkers;
     }
     b->budget = params->max_iters_per_worker * (unsigned long long)workers_eff;
+    b->cta_grid = b->grid;
     // path arena: room for a 4096-config path per problem on average
     b->arena = (unsigned long long)dof * std::min<long long>(4096, 2 * b->cap) * n_problems;
     return PRRTC_OK;
@@ -1086,6 +1122,17 @@ int batch_bind(prrtc_batch* b, Workspace* ws, const prrtc_scene* const* scenes, 
     b->d_ndone = reinterpret_cast<int*>(b->d_out + 12);
     b->d_ctl = reinterpret_cast<ProbCtl*>(b->d_out + 128);
     b->d_arena = reinterpret_cast<double*>(b->d_out + Workspace::out_hdr(n));
+    // warp-worker sizing: every warp holds a copy of its problem's scene,
+    // so the per-warp region follows the largest bound scene
+    b->warps = 0;
+    b->grid = b->cta_grid;
+    if (b->warp_ok) {
+        size_t mx = 0;
+        for (size_t i = 0; i < n; ++i) mx = std::max(mx, scenes[i]->words.size());
+        b->scene_words_max = (int)((mx + 3) & ~size_t(3));
+        b->warps = warp_workers_per_sm(b->robot->words.data(), b->scene_words_max, smem_optin(b->device));
+        if (b->warps > 0) b->grid = sm_count(b->device);
+    }
     return PRRTC_OK;
 }
 
@@ -1171,6 +1218,8 @@ int batch_enqueue(prrtc_batch* b, cudaStream_t st, bool upload) {
     a.p.deterministic = b->params.deterministic;
     a.ref_stats = b->params.deterministic ? 1 : 0;
     a.tail_claim = ek.tail_claim;
+    // help joins stop at the problem's worker cap (an env override for sweeps)
+    a.help_cap = ek.help_cap ? ek.help_cap : (int)b->params.max_workers_per_problem;
     a.p.budget = b->budget;
     a.p.seed = b->params.seed;
     a.p.uniform = b->params.sampler == PRRTC_SAMPLER_UNIFORM ? 1 : 0;
@@ -1193,9 +1242,17 @@ int batch_enqueue(prrtc_batch* b, cudaStream_t st, bool upload) {
         b->use_map = false;
     }
     const auto e0 = std::chrono::steady_clock::now();
+    if (b->warps) {
+        // warp workers: a multi-sample NN pass bounded to ~8 node pairs per lane
+        a.mnn_nodes = ek.mnn_nodes ? ek.mnn_nodes : 512;
+        a.scene_words_max = b->scene_words_max;
+    }
     if (b->timed) CUDA_TRY(cudaEventRecord(ws->ev0, st));
     const auto e1 = std::chrono::steady_clock::now();
-    CUDA_TRY(launch_plan(b->robot->args(), a, b->grid, st));
+    if (b->warps)
+        CUDA_TRY(launch_plan_warp(b->robot->args(), b->robot->words.data(), a, b->grid, b->warps, st));
+    else
+        CUDA_TRY(launch_plan(b->robot->args(), a, b->grid, st));
     const auto e2 = std::chrono::steady_clock::now();
     if (b->timed) CUDA_TRY(cudaEventRecord(ws->ev1, st));
     if (ek.host_trace) {

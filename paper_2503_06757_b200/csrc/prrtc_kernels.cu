@@ -13,6 +13,7 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <algorithm>
 #include <map>
 #include <mutex>
 #include <utility>
@@ -730,7 +731,7 @@ __device__ int pick_help(Ctx& c, const PlanArgs& a) {
             if (all_done) return -1;
             __nanosleep(200);
         }
-        int bk = 0x7fffffff, bp = -1;
+        int bk = 0x7fffffff, bp = -1, pending = 0;
         // an L2 scan of every problem's (started, done, winner, active) word
         // and ticket count, two independent 16 / 8-byte loads per problem so
         // they pipeline (a hint only: the chosen problem is acquired below;
@@ -739,11 +740,18 @@ __device__ int pick_help(Ctx& c, const PlanArgs& a) {
             const ProbCtl& C = a.ctl[q];
             const int4 hdr = __ldcg(reinterpret_cast<const int4*>(&C));  // started, done, winner, active
             const unsigned long long it = __ldcg(&C.iters);
-            if (hdr.x == 1 && hdr.y == DONE_RUNNING && it < a.p.budget && hdr.w < bk) {
+            pending |= hdr.x == 0 && hdr.y == DONE_RUNNING;  // claimed, endpoints still being checked
+            if (hdr.x == 1 && hdr.y == DONE_RUNNING && it < a.p.budget && hdr.w < bk &&
+                (a.help_cap == 0 || hdr.w < a.help_cap)) {
                 bk = hdr.w;
                 bp = q;
             }
         }
+        // every problem is claimed (the claim loop ran dry) and every running
+        // one has handed out its whole iteration budget: nothing can ever be
+        // joined again, so leave instead of spinning (the scans of idle CTAs
+        // take issue slots and L2 bandwidth from the ones still working)
+        if (!__syncthreads_or(pending || bp >= 0)) return -1;
         for (int o = 16; o > 0; o >>= 1) {
             const int ok = __shfl_xor_sync(0xffffffffu, bk, o);
             const int op = __shfl_xor_sync(0xffffffffu, bp, o);
@@ -1312,6 +1320,8 @@ cudaError_t launch_validate_paths(const RobotArgs& r, const PlanArgs& a, int* pr
     validate_paths_kernel<<<grid, 128, sm, st>>>(a, prefix, 4 * a.p.n_cc);
     return cudaGetLastError();
 }
+
+#include "prrtc_warp.cuh"  // the warp-worker batch planner (plan_warp_kernel)
 
 // CTA size variants: 128 threads (4 warps, up to 4 CTAs/SM) and 256 threads
 // (8 warps, 2 CTAs/SM: each iteration's parallel phases finish faster).

@@ -27,6 +27,11 @@ size_t smem_bytes(const RobotArgs& r, int ns_max, int nthreads);
 
 // Persistent planner: grid CTAs solve a.n_problems problems.
 cudaError_t launch_plan(const RobotArgs& r, PlanArgs a, int grid, cudaStream_t st);
+// Warp-worker planner (batches): warps per CTA that fit the shared memory
+// (one CTA per SM; 0 = does not fit), and its launch.
+int warp_workers_per_sm(const uint32_t* robot_words_host, int scene_words_max, int max_smem);
+cudaError_t launch_plan_warp(const RobotArgs& r, const uint32_t* robot_words_host, PlanArgs a, int grid, int warps,
+                             cudaStream_t st);
 // Device re-validation of the solved problems' paths (after launch_plan on
 // the same stream): prefix = [n_problems + 1] ints of scratch.
 cudaError_t launch_validate_paths(const RobotArgs& r, const PlanArgs& a, int* prefix, int grid, cudaStream_t st);

@@ -228,6 +228,7 @@ class PlannerParams:  # planner.hpp:21-40 (+ device knobs)
     ctas_per_sm: int = 0
     deterministic: bool = False
     validate_path: bool = False  # device re-validation of returned paths
+    max_workers_per_problem: int = 0  # batches: 0 = elastic help; 1 with workers=1 = the reference's search
 
     def resolved_dd_radius(self) -> float:
         return self.dd_radius if self.dd_radius > 0.0 else 4.0 * self.delta
@@ -253,6 +254,7 @@ class PlannerParams:  # planner.hpp:21-40 (+ device knobs)
         p.ctas_per_sm = self.ctas_per_sm
         p.deterministic = int(self.deterministic)
         p.validate_path = int(self.validate_path)
+        p.max_workers_per_problem = self.max_workers_per_problem
         return p
 
 

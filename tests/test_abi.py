@@ -44,6 +44,7 @@ int main(void) {
   printf("prrtc_params %zu\\nprrtc_result %zu\\nprrtc_robot_desc %zu\\nprrtc_scene_desc %zu\\n",
          sizeof(prrtc_params), sizeof(prrtc_result), sizeof(prrtc_robot_desc), sizeof(prrtc_scene_desc));
   P(prrtc_params, seed) P(prrtc_params, deterministic) P(prrtc_params, nn_partitions)
+  P(prrtc_params, max_workers_per_problem)
   P(prrtc_result, path) P(prrtc_result, flops) P(prrtc_result, tree_nodes) P(prrtc_result, message)
   P(prrtc_robot_desc, self_pairs) P(prrtc_scene_desc, capsules)
   return 0;
@@ -59,6 +60,7 @@ int main(void) {
     assert int(out["prrtc_params.seed"]) == _lib.Params.seed.offset
     assert int(out["prrtc_params.deterministic"]) == _lib.Params.deterministic.offset
     assert int(out["prrtc_params.nn_partitions"]) == _lib.Params.nn_partitions.offset
+    assert int(out["prrtc_params.max_workers_per_problem"]) == _lib.Params.max_workers_per_problem.offset
     assert int(out["prrtc_result.path"]) == _lib.Result.path.offset
     assert int(out["prrtc_result.flops"]) == _lib.Result.flops.offset
     assert int(out["prrtc_result.tree_nodes"]) == _lib.Result.tree_nodes.offset

@@ -126,6 +126,35 @@ def test_batch_success_not_below_reference(gpu, oracle):
             check_path(oracle, m, sc, r, s, g, sound, strict4=True)
 
 
+@pytest.mark.parametrize("robot,threads", [("panda", 0), ("panda", 32), ("fetch", 0), ("fetch", 32)])
+def test_batch_one_worker_per_problem_replays_reference(gpu, oracle, robot, threads):
+    """A batch with workers = 1 and max_workers_per_problem = 1 (no help
+    joins) runs, in ONE launch, each problem's reference workers=1 search:
+    one worker draws Halton indices 1 + seed + k in order (planner.cpp:192-
+    193), the multi-sample NN pass equals the sequential accept loop, tree
+    nodes are the exact FP64 checked configs — so status, iteration count
+    and the path itself equal the reference's, problem by problem, on both
+    device planners (CTA workers, threads 0; warp workers, threads 32), up to
+    an FP32-FK verdict within ~1e-6 m of a contact."""
+    m = robots.get(robot)
+    probs = load_problems(robot, 1000)[::5]  # 200 problems over the scene kinds
+    scenes = [make_scene(robot, k, p)[0] for k, p, _, _ in probs]
+    S = np.array([p[2] for p in probs])
+    G = np.array([p[3] for p in probs])
+    params = PlannerParams(workers=1, tree_capacity=20000, max_workers_per_problem=1, threads_per_cta=threads)
+    res = planner.plan_batch(m, scenes, S, G, params)
+    ref, _ = oracle.plan_many(m, scenes, S, G, PlannerParams(workers=1, tree_capacity=20000), threads=8)
+    same = 0
+    for r, q in zip(res, ref):
+        if r.status == q.status and r.iterations_total == q.iterations_total and (
+                r.status != PlanStatus.Solved or np.array_equal(r.path, q.path)):
+            same += 1
+    assert same >= 0.95 * len(probs), f"{same}/{len(probs)} problems replay the reference"
+    ok = sum(r.status == PlanStatus.Solved for r in res)
+    ok_ref = sum(r.status == PlanStatus.Solved for r in ref)
+    assert abs(ok - ok_ref) <= 0.05 * len(probs), (ok, ok_ref)
+
+
 def test_deterministic_mode_replays_reference(gpu, oracle):
     """One CTA, Halton stride 1, balanced pick: the device replays the
     reference's workers=1 run (scalar backend) node for node, except where an
