@@ -380,6 +380,43 @@ def parity_block(robot_names, workers_list, n, device=0, tree_capacity=200000, t
                 "dd_radius": params.resolved_dd_radius(),
                 "problems": len(S),
             }
+            if W == 1:
+                # exact mode: max_workers_per_problem = 1 keeps every problem on one
+                # worker (no help joins), which is the reference's workers=1 search
+                # itself: same Halton stream, same accept loop, exact FP64 nodes —
+                # so status, iteration count and path match problem by problem
+                # (up to an FP32-FK verdict within ~1e-6 m of a contact)
+                exact = robot_params(robot, PlannerParams(workers=1, tree_capacity=tree_capacity,
+                                                          max_workers_per_problem=1))
+                t0 = time.perf_counter()
+                be = planner.plan_batch_arrays(model, dsc, S, G, exact, device=device)
+                e_ms = (time.perf_counter() - t0) * 1e3
+                e_ok = be.status == PlanStatus.Solved
+                e_paths = be.paths
+                # the reference arm above uses its default kernel dispatch (AVX2),
+                # whose sq_distance summation order differs from the scalar one in
+                # the last bits; the device follows the scalar
+                # order, so the bitwise path identity is taken against a
+                # scalar-backend reference run (kernels.hpp:109 force_backend)
+                o.force_scalar(True)
+                try:
+                    ref_s, _ = o.plan_many(model, scenes, S, G, params, threads=threads)
+                finally:
+                    o.force_scalar(False)
+
+                def same_as(rs, paths_too):
+                    return sum(1 for i, r in enumerate(rs)
+                               if int(be.status[i]) == int(r.status) and int(be.iterations_total[i]) == r.iterations_total
+                               and (not paths_too or r.status != PlanStatus.Solved or np.array_equal(e_paths[i], r.path)))
+                same = same_as(ref_s, True)
+                row["b200_exact"] = {**_stats(e_ok, be.cost, None),
+                                     "iterations_mean": float(np.mean(be.iterations_total)),
+                                     "identical_to_reference": same,
+                                     "identical_to": "reference plan() workers=1, scalar backend: status, "
+                                                     "iterations and path bitwise",
+                                     "status_and_iterations_equal_default_backend": same_as(ref, False),
+                                     "problems_per_s_e2e": len(S) / (e_ms / 1e3),
+                                     "max_workers_per_problem": 1}
             if W > 1:
                 # single-problem mode: prrtc_plan puts W CTAs on the problem at once,
                 # W concurrent workers like the reference's W threads (the batch
@@ -405,6 +442,39 @@ def parity_block(robot_names, workers_list, n, device=0, tree_capacity=200000, t
     return out
 
 
+def planners_block(dev):
+    """The two device planners on the same device-resident batches at the
+    headline params: CTA workers (the default, plan_kernel)
+    and warp workers (threads_per_cta = 32, plan_warp_kernel); kernel time by
+    CUDA events on the launching stream (best of 3 after a warm-up)."""
+    import torch
+    from paper_2503_06757_b200 import planner
+    from paper_2503_06757_b200.model import PlanStatus
+    out = {}
+    st = torch.cuda.Stream(device=dev)
+    for robot, n in (("panda", 1000), ("fetch", 1000), ("fetch", 10000)):
+        model, scenes, S, G, _ = load_workload(robot, 1000)
+        ds = [planner.device_scene(s, dev) for s in scenes]
+        idx = np.arange(n) % len(S)
+        row = {}
+        for name, nt in (("cta", 0), ("warp", 32)):
+            b = planner.Batch(model, [ds[i] for i in idx], S[idx], G[idx],
+                              robot_params(robot, headline_params(threads_per_cta=nt)), device=dev)
+            ms = []
+            for rep in range(4):
+                e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                e0.record(st)
+                b.launch(st.cuda_stream)
+                e1.record(st)
+                st.synchronize()
+                ms.append(e0.elapsed_time(e1))
+            ok = np.mean([r.status == PlanStatus.Solved for r in b.results()])
+            row[name] = {"kernel_ms": min(ms[1:]), "problems_per_s": n / (min(ms[1:]) / 1e3), "success": float(ok)}
+            del b
+        out[f"{robot}_{n}"] = row
+    return out
+
+
 def mixed_sharded(dev, world, rank, total=10000):
     """BASELINE config 5: a 10k-problem mixed three-robot batch (1/3 per
     robot) sharded round robin across the ranks (one GPU each, no data-path
@@ -415,7 +485,7 @@ def mixed_sharded(dev, world, rank, total=10000):
     import torch
     from paper_2503_06757_b200 import planner
     from paper_2503_06757_b200.model import PlannerParams, PlanStatus
-    mp = PlannerParams(tree_capacity=20000)
+    mp = headline_params()  # workers = 1, tree_capacity 20000: the headline's params
     per = (total - 2 * (total // 3), total // 3, total // 3)
     batches, streams, mine = [], [], 0
     for robot, n in zip(("panda", "fetch", "baxter"), per):
@@ -438,7 +508,7 @@ def mixed_sharded(dev, world, rank, total=10000):
     solved, count = dist_sum(float(ok), world), dist_sum(float(mine), world)
     del batches
     return {"problems": int(count), "problems_per_s": count / (ms / 1e3), "ms": ms,
-            "success_rate": solved / count, "tree_capacity": 20000, "n_gpus": world,
+            "success_rate": solved / count, "params": "headline (workers 1, tree_capacity 20000)", "n_gpus": world,
             "sharding": "round robin over ranks, no collective on the data path",
             "timing": "host wall clock, barrier -> three concurrent stream launches + sync, max over ranks"}
 
@@ -745,6 +815,7 @@ def run_b200(args):
         if not args.no_extras:
             extras["robots"] = {r: table_one(dev, r, robot_params, 100, peak) for r in ("panda", "fetch", "baxter")}
             extras.update(bench_extras(dev, params))
+            extras["planners"] = planners_block(dev)
         micro = microbench(model, scenes, S, G, dev, peak)
         parity = None
         if not args.no_parity:
@@ -791,6 +862,8 @@ def run_b200(args):
                 f"{r}_W{w}": {"success_b200": v[f"W{w}"]["b200"]["success"],
                               "success_ref": v[f"W{w}"]["reference"]["success"],
                               "success_b200_single": v[f"W{w}"].get("b200_single", {}).get("success"),
+                              "success_b200_exact": v[f"W{w}"].get("b200_exact", {}).get("success"),
+                              "identical_to_reference": v[f"W{w}"].get("b200_exact", {}).get("identical_to_reference"),
                               "z_batch": v[f"W{w}"]["success_z_b200_minus_ref"],
                               "z_single": v[f"W{w}"].get("success_z_single_minus_ref"),
                               "problems": v[f"W{w}"]["problems"],

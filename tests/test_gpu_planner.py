@@ -134,8 +134,11 @@ def test_batch_one_worker_per_problem_replays_reference(gpu, oracle, robot, thre
     193), the multi-sample NN pass equals the sequential accept loop, tree
     nodes are the exact FP64 checked configs — so status, iteration count
     and the path itself equal the reference's, problem by problem, on both
-    device planners (CTA workers, threads 0; warp workers, threads 32), up to
-    an FP32-FK verdict within ~1e-6 m of a contact."""
+    device planners (CTA workers, threads 0; warp workers, threads 32). The
+    reference runs its scalar backend (its AVX2 sq_distance sums in another
+    order, kernels_avx2.cpp:26-39; the device follows the scalar order).
+    Measured: 1000/1000 identical for each robot on both planners
+    (tools/exact_diff.py); the search is deterministic, so the bar is all."""
     m = robots.get(robot)
     probs = load_problems(robot, 1000)[::5]  # 200 problems over the scene kinds
     scenes = [make_scene(robot, k, p)[0] for k, p, _, _ in probs]
@@ -149,10 +152,7 @@ def test_batch_one_worker_per_problem_replays_reference(gpu, oracle, robot, thre
         if r.status == q.status and r.iterations_total == q.iterations_total and (
                 r.status != PlanStatus.Solved or np.array_equal(r.path, q.path)):
             same += 1
-    assert same >= 0.95 * len(probs), f"{same}/{len(probs)} problems replay the reference"
-    ok = sum(r.status == PlanStatus.Solved for r in res)
-    ok_ref = sum(r.status == PlanStatus.Solved for r in ref)
-    assert abs(ok - ok_ref) <= 0.05 * len(probs), (ok, ok_ref)
+    assert same == len(probs), f"{same}/{len(probs)} problems replay the reference"
 
 
 def test_deterministic_mode_replays_reference(gpu, oracle):
