@@ -214,7 +214,8 @@ struct prrtc_robot {
     double* d_fine_r64 = nullptr;
     double* d_limits = nullptr;
     double reach = 0.0;           // bound on |posed sphere| (m)
-    mutable std::atomic<int> occ[15] = {};  // planner CTAs per SM, by (ns_max / 32, CTA size)
+    // planner CTAs per SM, by (ns_max / 32, CTA size) x (Uniform sampler) x (scene-size bucket)
+    mutable std::atomic<int> occ[15 * 2 * 5] = {};
     RobotArgs args() const {
         RobotArgs r;
         r.words = d_words;
@@ -1038,10 +1039,20 @@ int batch_setup(prrtc_batch* b, const prrtc_robot* robot, const prrtc_scene* con
     const EnvKnobs& ek = env();
     const bool ns64 = !ek.ns32 && ((n_problems == 1 && b->nthreads >= 256) || ek.ns64);
     b->ns_max = ns64 ? (ek.ns128 ? 128 : 64) : 32;
-    const int okey = b->ns_max / 32 + (b->nthreads == 256 ? 5 : (b->nthreads == 512 ? 10 : 0));
+    // shared memory per CTA follows the largest scene of the launch and the
+    // sampler (the Uniform generator's state); occupancy is cached per
+    // scene-size bucket, computed at the bucket's upper bound
+    size_t swm = 0;
+    for (uint32_t i = 0; i < n_problems; ++i) swm = std::max(swm, scenes[i]->words.size());
+    static const int kSceneBucket[5] = {256, 512, 768, 1024, SCENE_MAX_WORDS};
+    int bk = 0;
+    while (bk < 4 && (int)swm > kSceneBucket[bk]) ++bk;
+    const bool uni = params->sampler == PRRTC_SAMPLER_UNIFORM;
+    const int okey = (b->ns_max / 32 + (b->nthreads == 256 ? 5 : (b->nthreads == 512 ? 10 : 0))) * 10 +
+                     (uni ? 5 : 0) + bk;
     int occ = robot->occ[okey].load(std::memory_order_relaxed);
     if (occ == 0) {
-        occ = plan_occupancy(robot->args(), b->ns_max, b->nthreads);
+        occ = plan_occupancy(robot->args(), b->ns_max, b->nthreads, kSceneBucket[bk], uni);
         robot->occ[okey].store(occ, std::memory_order_relaxed);
     }
     const int sms = sm_count(robot->device);
@@ -1126,10 +1137,10 @@ int batch_bind(prrtc_batch* b, Workspace* ws, const prrtc_scene* const* scenes, 
     // so the per-warp region follows the largest bound scene
     b->warps = 0;
     b->grid = b->cta_grid;
+    size_t mx = 0;
+    for (size_t i = 0; i < n; ++i) mx = std::max(mx, scenes[i]->words.size());
+    b->scene_words_max = (int)((mx + 3) & ~size_t(3));
     if (b->warp_ok) {
-        size_t mx = 0;
-        for (size_t i = 0; i < n; ++i) mx = std::max(mx, scenes[i]->words.size());
-        b->scene_words_max = (int)((mx + 3) & ~size_t(3));
         b->warps = warp_workers_per_sm(b->robot->words.data(), b->scene_words_max, smem_optin(b->device));
         if (b->warps > 0) b->grid = sm_count(b->device);
     }
@@ -1242,10 +1253,10 @@ int batch_enqueue(prrtc_batch* b, cudaStream_t st, bool upload) {
         b->use_map = false;
     }
     const auto e0 = std::chrono::steady_clock::now();
+    a.scene_words_max = b->scene_words_max;  // per-CTA (per-warp) scene region size
     if (b->warps) {
         // warp workers: a multi-sample NN pass bounded to ~8 node pairs per lane
         a.mnn_nodes = ek.mnn_nodes ? ek.mnn_nodes : 512;
-        a.scene_words_max = b->scene_words_max;
     }
     if (b->timed) CUDA_TRY(cudaEventRecord(ws->ev0, st));
     const auto e1 = std::chrono::steady_clock::now();

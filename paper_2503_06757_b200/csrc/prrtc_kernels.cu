@@ -36,12 +36,17 @@ struct SmemLayout {
 
 __host__ __device__ inline size_t al16(size_t x) { return (x + 15) & ~size_t(15); }
 
+// scene_words: room for the largest scene the launch stages (the planner
+// sizes it from its batch, other kernels take the maximum); with_mt: the
+// Uniform sampler's generator state (2.5 KB) only when that sampler runs —
+// trimmed so five 128-thread planner CTAs fit one SM's shared memory
 __host__ __device__ inline SmemLayout smem_layout(int robot_words, int L, int dof, int NS,
-                                                  int nthreads) {
+                                                  int nthreads, int scene_words = SCENE_MAX_WORDS,
+                                                  bool with_mt = true) {
     SmemLayout s;
     size_t o = 0;
     s.robot = o; o = al16(o + 4 * (size_t)robot_words);
-    s.scene = o; o = al16(o + 4 * (size_t)SCENE_MAX_WORDS);
+    s.scene = o; o = al16(o + 4 * (size_t)scene_words);
     s.pose = o;  o = al16(o + 4 * (size_t)L * 12 * NS);
     s.ccen = o;  o = al16(o + 4 * (size_t)L * 3 * NS);
     s.qf = o;    o = al16(o + 4 * (size_t)dof * NS);
@@ -63,18 +68,25 @@ __host__ __device__ inline SmemLayout smem_layout(int robot_words, int L, int do
     s.t0 = o;    o = al16(o + 8 * (size_t)T0_COUNT);
     s.rcount = o; o = al16(o + 8 * (size_t)NS);
     s.rfine = o; o = al16(o + 4 * (size_t)NS);
-    s.mt = o;    o = al16(o + 8 * (size_t)(kMtN + 1));
+    s.mt = o;    o = al16(o + (with_mt ? 8 * (size_t)(kMtN + 1) : 0));
     s.total = o;
     return s;
 }
 
-size_t smem_bytes(const RobotArgs& r, int ns_max, int nthreads) {
-    return smem_layout(r.n_words, r.n_links, r.dof, ns_max, nthreads).total;
+size_t smem_bytes(const RobotArgs& r, int ns_max, int nthreads, int scene_words, bool with_mt) {
+    return smem_layout(r.n_words, r.n_links, r.dof, ns_max, nthreads, scene_words, with_mt).total;
+}
+
+// scene words the planner stages per CTA: the launch's largest scene (the
+// host sets a.scene_words_max), else the maximum
+__host__ __device__ inline int plan_scene_words(const PlanArgs& a) {
+    return a.scene_words_max > 0 && a.scene_words_max <= SCENE_MAX_WORDS ? a.scene_words_max : SCENE_MAX_WORDS;
 }
 
 // Copies the packed robot into shared memory and wires the context.
 __device__ void setup_ctx(Ctx& c, unsigned char* smem, const uint32_t* robot_g, int robot_words,
-                          const double* fine_r64, const double* limits, int NS) {
+                          const double* fine_r64, const double* limits, int NS,
+                          int scene_words = SCENE_MAX_WORDS, bool with_mt = true) {
     const int tid = threadIdx.x, nthreads = blockDim.x;
     uint32_t* rw = reinterpret_cast<uint32_t*>(smem);
     // 16-byte vector copy (buffer padded to a multiple of 4 words on host)
@@ -82,7 +94,7 @@ __device__ void setup_ctx(Ctx& c, unsigned char* smem, const uint32_t* robot_g, 
         reinterpret_cast<uint4*>(rw)[i] = __ldg(reinterpret_cast<const uint4*>(robot_g) + i);
     }
     __syncthreads();
-    const SmemLayout lay = smem_layout(robot_words, rw[RH_NLINKS], rw[RH_DOF], NS, nthreads);
+    const SmemLayout lay = smem_layout(robot_words, rw[RH_NLINKS], rw[RH_DOF], NS, nthreads, scene_words, with_mt);
     unsigned long long* stat = reinterpret_cast<unsigned long long*>(smem + lay.stat);
     stat[2 * tid] = 0;
     stat[2 * tid + 1] = 0;
@@ -865,7 +877,7 @@ __global__ void __launch_bounds__(NT, MINB) plan_kernel(PlanArgs a) {
     extern __shared__ __align__(16) unsigned char smem[];
     Ctx& c = g_ctx;
     setup_ctx(c, smem, a.robot, reinterpret_cast<const int*>(a.robot)[RH_WORDS], a.fine_r64,
-              a.limits, a.ns_max);
+              a.limits, a.ns_max, plan_scene_words(a), a.p.uniform != 0);
     const int tid = threadIdx.x;
     const int dof = c.dof;
     const int robot_words = reinterpret_cast<const int*>(a.robot)[RH_WORDS];
@@ -1314,7 +1326,7 @@ cudaError_t raise_smem_limit(const void* fn, int sm) {
 
 cudaError_t launch_validate_paths(const RobotArgs& r, const PlanArgs& a, int* prefix, int grid, cudaStream_t st) {
     path_edges_scan_kernel<<<1, 1024, 0, st>>>(a.ctl, a.n_problems, prefix);
-    const size_t sm = smem_bytes(r, a.ns_max, 128);
+    const size_t sm = smem_bytes(r, a.ns_max, 128, SCENE_MAX_WORDS, true);
     cudaError_t e = raise_smem_limit(reinterpret_cast<const void*>(validate_paths_kernel), (int)sm);
     if (e != cudaSuccess) return e;
     validate_paths_kernel<<<grid, 128, sm, st>>>(a, prefix, 4 * a.p.n_cc);
@@ -1337,7 +1349,7 @@ static PlanFn plan_fn(int nthreads) {
 }
 
 cudaError_t launch_plan(const RobotArgs& r, PlanArgs a, int grid, cudaStream_t st) {
-    const size_t sm = smem_bytes(r, a.ns_max, a.nthreads);
+    const size_t sm = smem_bytes(r, a.ns_max, a.nthreads, plan_scene_words(a), a.p.uniform != 0);
     const PlanFn fn = plan_fn(a.nthreads);
     cudaError_t e = raise_smem_limit(reinterpret_cast<const void*>(fn), (int)sm);
     if (e != cudaSuccess) return e;
@@ -1345,8 +1357,8 @@ cudaError_t launch_plan(const RobotArgs& r, PlanArgs a, int grid, cudaStream_t s
     return cudaLaunchKernel(reinterpret_cast<const void*>(fn), dim3(grid), dim3(a.nthreads), args, sm, st);
 }
 
-int plan_occupancy(const RobotArgs& r, int ns_max, int nthreads) {
-    const size_t sm = smem_bytes(r, ns_max, nthreads);
+int plan_occupancy(const RobotArgs& r, int ns_max, int nthreads, int scene_words, bool with_mt) {
+    const size_t sm = smem_bytes(r, ns_max, nthreads, scene_words, with_mt);
     const PlanFn fn = plan_fn(nthreads);
     raise_smem_limit(reinterpret_cast<const void*>(fn), (int)sm);
     int n = 0;
@@ -1760,7 +1772,7 @@ static int cur_sms() {
 cudaError_t launch_check_configs(const RobotArgs& r, const SceneArgs& s, const double* q, int n,
                                  int two_stage, uint8_t* out, cudaStream_t st) {
     const int NS = chunk_states();
-    const size_t sm = smem_bytes(r, NS, 128);
+    const size_t sm = smem_bytes(r, NS, 128, SCENE_MAX_WORDS, true);
     cudaError_t e = raise_smem_limit(reinterpret_cast<const void*>(check_configs_kernel), (int)sm);
     if (e != cudaSuccess) return e;
     const int grid = (int)min((long long)(n + NS - 1) / NS, (long long)cur_sms() * 16);
@@ -1773,7 +1785,7 @@ cudaError_t launch_validate_edges(const RobotArgs& r, const SceneArgs& s, const 
                                   int early_exit, uint8_t* out, cudaStream_t st, long long* prof,
                                   unsigned long long* counters) {
     const int NS = chunk_states();
-    const size_t sm = smem_bytes(r, NS, 128);
+    const size_t sm = smem_bytes(r, NS, 128, SCENE_MAX_WORDS, true);
     cudaError_t e = raise_smem_limit(reinterpret_cast<const void*>(validate_edges_kernel), (int)sm);
     if (e != cudaSuccess) return e;
     const int grid = (int)min((long long)n_edges, (long long)cur_sms() * 16);
@@ -1787,7 +1799,7 @@ cudaError_t launch_debug_check_edges(const RobotArgs& r, const SceneArgs& s, con
                                      const double* to, int n_edges, int n_cc, int two_stage,
                                      uint8_t* state_valid, float* fine_out, cudaStream_t st) {
     const int NS = chunk_states();
-    const size_t sm = smem_bytes(r, NS, 128);
+    const size_t sm = smem_bytes(r, NS, 128, SCENE_MAX_WORDS, true);
     cudaError_t e = raise_smem_limit(reinterpret_cast<const void*>(debug_check_edges_kernel), (int)sm);
     if (e != cudaSuccess) return e;
     const int grid = (int)min((long long)n_edges, (long long)cur_sms() * 8);
@@ -1800,7 +1812,7 @@ cudaError_t launch_debug_check_edges(const RobotArgs& r, const SceneArgs& s, con
 cudaError_t launch_debug_fk(const RobotArgs& r, const double* q, int n, float* fine_out,
                             float* coarse_out, cudaStream_t st) {
     const int NS = chunk_states();
-    const size_t sm = smem_bytes(r, NS, 128);
+    const size_t sm = smem_bytes(r, NS, 128, SCENE_MAX_WORDS, true);
     cudaError_t e = raise_smem_limit(reinterpret_cast<const void*>(debug_fk_kernel), (int)sm);
     if (e != cudaSuccess) return e;
     const int grid = (int)min((long long)(n + NS - 1) / NS, (long long)cur_sms() * 16);

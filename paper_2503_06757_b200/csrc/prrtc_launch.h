@@ -23,7 +23,7 @@ struct SceneArgs {
     SceneF64 f64;           // device
 };
 
-size_t smem_bytes(const RobotArgs& r, int ns_max, int nthreads);
+size_t smem_bytes(const RobotArgs& r, int ns_max, int nthreads, int scene_words, bool with_mt);
 
 // Persistent planner: grid CTAs solve a.n_problems problems.
 cudaError_t launch_plan(const RobotArgs& r, PlanArgs a, int grid, cudaStream_t st);
@@ -36,7 +36,7 @@ cudaError_t launch_plan_warp(const RobotArgs& r, const uint32_t* robot_words_hos
 // the same stream): prefix = [n_problems + 1] ints of scratch.
 cudaError_t launch_validate_paths(const RobotArgs& r, const PlanArgs& a, int* prefix, int grid, cudaStream_t st);
 // Max co-resident planner CTAs per SM for this configuration.
-int plan_occupancy(const RobotArgs& r, int ns_max, int nthreads);
+int plan_occupancy(const RobotArgs& r, int ns_max, int nthreads, int scene_words, bool with_mt);
 
 cudaError_t launch_check_configs(const RobotArgs& r, const SceneArgs& s, const double* q, int n,
                                  int two_stage, uint8_t* out, cudaStream_t st);
