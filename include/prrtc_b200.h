@@ -178,7 +178,8 @@ typedef struct prrtc_result {
     int32_t status;              /* PRRTC_SOLVED / FAILED / INFEASIBLE_ENDPOINT */
     uint32_t dof;
     uint32_t path_len;           /* number of configs */
-    uint32_t _pad;
+    uint32_t path_block;         /* library-internal: a batch's paths share one host
+                                    block (0 = the path is its own allocation) */
     double* path;                /* [path_len*dof], library-owned; free with
                                     prrtc_result_free() */
     double cost;                 /* arclength (planner.cpp:152-158) */

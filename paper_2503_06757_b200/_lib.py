@@ -81,7 +81,7 @@ class Result(C.Structure):
         ("status", C.c_int32),
         ("dof", C.c_uint32),
         ("path_len", C.c_uint32),
-        ("_pad", C.c_uint32),
+        ("path_block", C.c_uint32),
         ("path", C.POINTER(C.c_double)),
         ("cost", C.c_double),
         ("wall_time_ms", C.c_double),

@@ -1307,8 +1307,87 @@ double path_cost(const double* path, uint32_t len, uint32_t dof) {
 // Copies the header, controls and used arena back and fills out[].
 std::chrono::steady_clock::time_point g_sync_time;  // PRRTC_HOST_TRACE
 
+// ---------------------------------------------------------------------------
+// result path blocks: a batch's paths stay in the pinned block the D2H copy
+// of the path arena landed in; every result of the batch points into it and
+// holds one reference (prrtc_result_free drops it), so a 1000-problem call
+// costs no per-path allocation or host copy (fill was ~0.17 ms of a ~2 ms
+// call). Blocks are pooled: cudaHostAlloc / cudaFreeHost are slow and the
+// latter can synchronise the device.
+// ---------------------------------------------------------------------------
+struct PathBlock {
+    double* data = nullptr;
+    size_t cap = 0;  // doubles
+    std::atomic<int> refs{0};
+};
+constexpr int kMaxPathBlocks = 4096;
+std::atomic<PathBlock*> g_path_blocks[kMaxPathBlocks];
+std::mutex g_path_mu;
+std::vector<PathBlock*> g_path_pool;  // free blocks (refs 0, no slot)
+int g_path_hint = 0;
+
+// A block of >= doubles capacity in a free slot: returns the slot id (1-based)
+// or 0 (no slot or no pinned memory: the caller falls back to copies).
+int path_block_acquire(size_t doubles, PathBlock** out) {
+    std::lock_guard<std::mutex> lk(g_path_mu);
+    int slot = -1;
+    for (int k = 0; k < kMaxPathBlocks; ++k) {
+        const int i = (g_path_hint + k) % kMaxPathBlocks;
+        if (!g_path_blocks[i].load(std::memory_order_relaxed)) {
+            slot = i;
+            break;
+        }
+    }
+    if (slot < 0) return 0;
+    PathBlock* pb = nullptr;
+    size_t best = SIZE_MAX;
+    int bi = -1;
+    for (int i = 0; i < (int)g_path_pool.size(); ++i)
+        if (g_path_pool[i]->cap >= doubles && g_path_pool[i]->cap < best) {
+            best = g_path_pool[i]->cap;
+            bi = i;
+        }
+    if (bi >= 0) {
+        pb = g_path_pool[bi];
+        g_path_pool.erase(g_path_pool.begin() + bi);
+    } else {
+        size_t cap = size_t(1) << 17;  // 1 MB at least, powers of two
+        while (cap < doubles) cap <<= 1;
+        pb = new PathBlock();
+        if (cudaHostAlloc(reinterpret_cast<void**>(&pb->data), 8 * cap, cudaHostAllocPortable) != cudaSuccess) {
+            cudaGetLastError();
+            delete pb;
+            return 0;
+        }
+        pb->cap = cap;
+    }
+    pb->refs.store(0, std::memory_order_relaxed);
+    g_path_blocks[slot].store(pb, std::memory_order_release);
+    g_path_hint = slot + 1;
+    *out = pb;
+    return slot + 1;
+}
+
+void path_block_release(int id) {  // refs reached 0 (or never handed out)
+    std::lock_guard<std::mutex> lk(g_path_mu);
+    PathBlock* pb = g_path_blocks[id - 1].exchange(nullptr, std::memory_order_acq_rel);
+    if (!pb) return;
+    g_path_pool.push_back(pb);
+    while (g_path_pool.size() > 8) {  // keep a few; free the oldest
+        cudaFreeHost(g_path_pool.front()->data);
+        delete g_path_pool.front();
+        g_path_pool.erase(g_path_pool.begin());
+    }
+}
+
+void path_block_unref(int id) {
+    if (id <= 0 || id > kMaxPathBlocks) return;
+    PathBlock* pb = g_path_blocks[id - 1].load(std::memory_order_acquire);
+    if (pb && pb->refs.fetch_sub(1, std::memory_order_acq_rel) == 1) path_block_release(id);
+}
+
 int fill_results(prrtc_batch* b, prrtc_result* out, const unsigned char* h, const double* arena,
-                 unsigned long long used);
+                 unsigned long long used, int block_id = 0, PathBlock* pb = nullptr);
 
 int batch_collect(prrtc_batch* b, prrtc_result* out) {
     Workspace* ws = b->ws;
@@ -1351,8 +1430,21 @@ int batch_collect(prrtc_batch* b, prrtc_result* out) {
         prefix = std::min({(size_t)b->arena, want, ws->h_out_arena});
     }
     ws->last_d2h = hdr + 8 * prefix;
-    CUDA_TRY(cudaMemcpyAsync(ws->h_out, b->d_out, hdr + 8 * prefix, cudaMemcpyDeviceToHost, b->last_stream));
-    CUDA_TRY(cudaStreamSynchronize(b->last_stream));
+    // batches: the arena prefix goes straight into a pooled pinned path block
+    // that the results will point into (a single problem keeps its one copy)
+    PathBlock* pb = nullptr;
+    int bid = b->n > 1 ? path_block_acquire(prefix, &pb) : 0;
+    if (bid) {
+        CUDA_TRY(cudaMemcpyAsync(ws->h_out, b->d_out, hdr, cudaMemcpyDeviceToHost, b->last_stream));
+        CUDA_TRY(cudaMemcpyAsync(pb->data, b->d_arena, 8 * prefix, cudaMemcpyDeviceToHost, b->last_stream));
+    } else {
+        CUDA_TRY(cudaMemcpyAsync(ws->h_out, b->d_out, hdr + 8 * prefix, cudaMemcpyDeviceToHost, b->last_stream));
+    }
+    const cudaError_t se = cudaStreamSynchronize(b->last_stream);
+    if (se != cudaSuccess) {
+        if (bid) path_block_release(bid);
+        return set_err(PRRTC_ECUDA, std::string("plan: ") + cudaGetErrorString(se));
+    }
     g_sync_time = std::chrono::steady_clock::now();
     const unsigned char* h = static_cast<const unsigned char*>(ws->h_out);
     unsigned long long used = *reinterpret_cast<const unsigned long long*>(h);
@@ -1360,6 +1452,29 @@ int batch_collect(prrtc_batch* b, prrtc_result* out) {
     {
         const double per = (double)used / b->n;
         ws->path_hint = per >= ws->path_hint ? per : 0.9 * ws->path_hint + 0.1 * per;
+    }
+    if (bid) {
+        if (used > prefix) {  // fetch the rest, into a block that holds all of it
+            ws->last_d2h += 8 * (used - prefix);
+            if (used > pb->cap) {
+                PathBlock* nb = nullptr;
+                const int nid = path_block_acquire(used, &nb);
+                if (!nid) {
+                    path_block_release(bid);
+                    return set_err(PRRTC_ENOMEM, "plan: pinned path block allocation failed");
+                }
+                std::memcpy(nb->data, pb->data, 8 * prefix);
+                path_block_release(bid);
+                bid = nid;
+                pb = nb;
+            }
+            if (cudaMemcpy(pb->data + prefix, b->d_arena + prefix, 8 * (used - prefix), cudaMemcpyDeviceToHost) !=
+                cudaSuccess) {
+                path_block_release(bid);
+                return set_err(PRRTC_ECUDA, "plan: path read-back failed");
+            }
+        }
+        return fill_results(b, out, h, pb->data, used, bid, pb);
     }
     const double* arena = reinterpret_cast<const double*>(h + hdr);
     std::vector<double> big;
@@ -1376,8 +1491,9 @@ int batch_collect(prrtc_batch* b, prrtc_result* out) {
 
 // Parses a host copy of the out-header (h), controls and arena into out[].
 int fill_results(prrtc_batch* b, prrtc_result* out, const unsigned char* h, const double* arena,
-                 unsigned long long used) {
+                 unsigned long long used, int block_id, PathBlock* pb) {
     Workspace* ws = b->ws;
+    int block_refs = 0;
     const ProbCtl* ctl = reinterpret_cast<const ProbCtl*>(h + 128);
     float ms = 0.f;
     if (b->timed) cudaEventElapsedTime(&ms, ws->ev0, ws->ev1);
@@ -1464,14 +1580,27 @@ int fill_results(prrtc_batch* b, prrtc_result* out, const unsigned char* h, cons
         if (r.status == PRRTC_SOLVED && C.path_len > 0 &&
             C.path_off + (unsigned long long)C.path_len * b->dof <= used) {
             r.path_len = C.path_len;
-            r.path = static_cast<double*>(std::malloc(sizeof(double) * b->dof * C.path_len));
-            std::memcpy(r.path, arena + C.path_off, sizeof(double) * b->dof * C.path_len);
+            if (pb) {  // a view into the batch's path block (one reference per path)
+                r.path = const_cast<double*>(arena) + C.path_off;
+                r.path_block = (uint32_t)block_id;
+                ++block_refs;
+            } else {
+                r.path = static_cast<double*>(std::malloc(sizeof(double) * b->dof * C.path_len));
+                std::memcpy(r.path, arena + C.path_off, sizeof(double) * b->dof * C.path_len);
+            }
             r.cost = path_cost(r.path, r.path_len, b->dof);
             // planner.cpp:144-148: no zero-length (bitwise-equal) segment
             for (uint32_t k = 1; k < r.path_len; ++k)
                 if (std::memcmp(r.path + (size_t)(k - 1) * b->dof, r.path + (size_t)k * b->dof,
                                 sizeof(double) * b->dof) == 0) {
-                    prrtc_result_free(&r);
+                    if (r.path_block) {  // not handed out: drop the view
+                        r.path = nullptr;
+                        r.path_len = 0;
+                        r.path_block = 0;
+                        --block_refs;
+                    } else {
+                        prrtc_result_free(&r);
+                    }
                     r.status = PRRTC_FAILED;
                     r.cost = 0.0;
                     std::snprintf(r.message, sizeof(r.message),
@@ -1496,6 +1625,10 @@ int fill_results(prrtc_batch* b, prrtc_result* out, const unsigned char* h, cons
         r.tree_nodes[1] = (uint64_t)std::max(0, C.published[1]);
         r.solving_worker = C.winner - 1;
         if (b->params.validate_path && r.status == PRRTC_SOLVED) r.path_check = C.path_bad ? 2 : 1;
+    }
+    if (pb) {  // the block lives until the last of its paths is freed
+        if (block_refs > 0) pb->refs.store(block_refs, std::memory_order_release);
+        else path_block_release(block_id);
     }
     return PRRTC_OK;
 }
@@ -1787,9 +1920,11 @@ int prrtc_plan(const prrtc_robot* robot, const prrtc_scene* scene, const double*
 
 void prrtc_result_free(prrtc_result* r) {
     if (r && r->path) {
-        std::free(r->path);
+        if (r->path_block) path_block_unref((int)r->path_block);  // a view into its batch's block
+        else std::free(r->path);
         r->path = nullptr;
         r->path_len = 0;
+        r->path_block = 0;
     }
 }
 
