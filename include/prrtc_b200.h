@@ -181,7 +181,9 @@ typedef struct prrtc_result {
     uint32_t path_block;         /* library-internal: a batch's paths share one host
                                     block (0 = the path is its own allocation) */
     double* path;                /* [path_len*dof], library-owned; free with
-                                    prrtc_result_free() */
+                                    prrtc_result_free() (never free() it: the paths
+                                    of one batch call share a pinned block that
+                                    lives until the last of them is freed) */
     double cost;                 /* arclength (planner.cpp:152-158) */
     double wall_time_ms;         /* host wall clock around the call */
     double device_time_ms;       /* CUDA-event time of the device work */

@@ -24,6 +24,10 @@ namespace dev {
 constexpr int kMaxDof = 32;
 constexpr int kNoBad = 0x7fffffff;
 constexpr int kTTab = 128;  // edge-sample fraction table covers n_cc <= 128
+#ifndef PRRTC_NN_PAIRS
+#define PRRTC_NN_PAIRS 2
+#endif
+constexpr int kNnPairs = PRRTC_NN_PAIRS;  // node pairs per NN scan trip (1, 2, 4 or 8; measured: 2)
 
 // ---------------------------------------------------------------------------
 // memory-model helpers (gpu scope)
@@ -1377,33 +1381,56 @@ __device__ __noinline__ void nn_scan_multi(Ctx& c, const double* cfg, long long 
     const int npairs = (count + 1) >> 1;
     if (j < m) {
         const double* q = Q + j * dof;
-        for (int pi = sub; pi < npairs; pi += g) {
-            const int n0 = pi * 2;
-            double a0 = 0.0, a1 = 0.0;
-            if (ddf) asm volatile("prefetch.global.L1 [%0];" ::"l"(ddf + n0));
-            for (int d0 = 0; d0 < dof; d0 += 8) {
-                double2 v[8];
+        // kNnPairs node pairs per trip (pi, pi + g, ...: 2 x kNnPairs
+        // independent FP64 accumulation chains), dimensions loaded
+        // 8 / kNnPairs at a time for all of them (8 double2 of registers, as
+        // one pair 8 at a time); the pairs are still visited in increasing
+        // index order, so strict-< keeps the lowest index on ties
+        constexpr int NP = kNnPairs, ND = 8 / kNnPairs;
+        for (int pi = sub; pi < npairs; pi += NP * g) {
+            int nn_[NP];
+            bool in_[NP];
 #pragma unroll
-                for (int k = 0; k < 8; ++k)  // every slot assigned: v stays in registers
-                    v[k] = d0 + k < dof ? *reinterpret_cast<const double2*>(cfg + (d0 + k) * cap + n0)
-                                        : make_double2(0.0, 0.0);
+            for (int r = 0; r < NP; ++r) {
+                in_[r] = pi + r * g < npairs;
+                nn_[r] = in_[r] ? (pi + r * g) * 2 : pi * 2;  // (a clamped duplicate load when absent)
+                if (ddf && in_[r]) asm volatile("prefetch.global.L1 [%0];" ::"l"(ddf + nn_[r]));
+            }
+            double acc[NP][2];
 #pragma unroll
-                for (int k = 0; k < 8; ++k) {
+            for (int r = 0; r < NP; ++r) acc[r][0] = acc[r][1] = 0.0;
+            for (int d0 = 0; d0 < dof; d0 += ND) {
+                double2 v[NP][ND];
+#pragma unroll
+                for (int k = 0; k < ND; ++k)  // every slot assigned: v stays in registers
+#pragma unroll
+                    for (int r = 0; r < NP; ++r)
+                        v[r][k] = d0 + k < dof ? *reinterpret_cast<const double2*>(cfg + (d0 + k) * cap + nn_[r])
+                                               : make_double2(0.0, 0.0);
+#pragma unroll
+                for (int k = 0; k < ND; ++k) {
                     if (d0 + k < dof) {
                         const double qd = q[d0 + k];
-                        const double e0 = __dsub_rn(v[k].x, qd), e1 = __dsub_rn(v[k].y, qd);
-                        a0 = __dadd_rn(a0, __dmul_rn(e0, e0));
-                        a1 = __dadd_rn(a1, __dmul_rn(e1, e1));
+#pragma unroll
+                        for (int r = 0; r < NP; ++r) {
+                            const double e0 = __dsub_rn(v[r][k].x, qd), e1 = __dsub_rn(v[r][k].y, qd);
+                            acc[r][0] = __dadd_rn(acc[r][0], __dmul_rn(e0, e0));
+                            acc[r][1] = __dadd_rn(acc[r][1], __dmul_rn(e1, e1));
+                        }
                     }
                 }
             }
-            if (a0 < best) {
-                best = a0;
-                bi = n0;
-            }
-            if (n0 + 1 < count && a1 < best) {
-                best = a1;
-                bi = n0 + 1;
+#pragma unroll
+            for (int r = 0; r < NP; ++r) {
+                if (!in_[r]) continue;
+                if (acc[r][0] < best) {
+                    best = acc[r][0];
+                    bi = nn_[r];
+                }
+                if (nn_[r] + 1 < count && acc[r][1] < best) {
+                    best = acc[r][1];
+                    bi = nn_[r] + 1;
+                }
             }
         }
     }
