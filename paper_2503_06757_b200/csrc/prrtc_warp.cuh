@@ -945,6 +945,7 @@ __global__ void __launch_bounds__(512, 1) plan_warp_kernel(PlanArgs a) {
             // Halton index 1 + seed + ticket ----
             if (refill) {
                 const int nblk = (int)tk_cnt;
+                __syncwarp();  // the previous block's samples are read before they are overwritten
                 for (int j = lane; j < nblk * dof; j += 32) {
                     const int k = j / dof, d = j - k * dof;
                     wr.sbuf[j] = sample_dim(halton_tab(bases[d], magic[d], htab + d * kHaltonTab, 1ull + a.p.seed + tk_base + k),
@@ -973,6 +974,7 @@ __global__ void __launch_bounds__(512, 1) plan_warp_kernel(PlanArgs a) {
             // ---- steer (planner.cpp:48-64) ----
             double* nnc = wr.dcfg + WD_NN * dof;
             double* cnew = wr.dcfg + WD_NEW * dof;
+            __syncwarp();  // every lane's reads of the previous chain's endpoints precede the rewrite
             if (lane < dof) {
                 const double vv = Ts.cfg[(size_t)lane * a.stride + nn];  // L1: the scan read it
                 nnc[lane] = vv;
@@ -1033,6 +1035,7 @@ __global__ void __launch_bounds__(512, 1) plan_warp_kernel(PlanArgs a) {
                 const double disto = __dsqrt_rn(d2o);
                 double* tgt = wr.dcfg + WD_TGT * dof;
                 double* A = wr.dcfg + WD_A * dof;
+                __syncwarp();  // (as at the steer: reads of the old rows first)
                 if (lane < dof) {
                     tgt[lane] = To.cfg[(size_t)lane * a.stride + nno];
                     A[lane] = cnew[lane];
