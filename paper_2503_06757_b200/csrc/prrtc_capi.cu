@@ -76,6 +76,7 @@ struct EnvKnobs {
     int tail_claim = 1, mnn_nodes = 0;
     int warp = -1;  // PRRTC_WARP=1: eligible batches on the warp-worker planner (A/B runs)
     int help_cap = 0;  // PRRTC_HELP_CAP: most workers a help join may bring a problem to (sweeps)
+    int help_policy = 1;  // PRRTC_HELP_POLICY: 1 most unclaimed budget per worker, 0 fewest workers (A/B)
     long long map_bytes = -1;
     std::string dump_ctl;
 };
@@ -95,6 +96,7 @@ const EnvKnobs* read_env() {
     if (const char* e = std::getenv("PRRTC_TAIL_CLAIM")) k->tail_claim = std::atoi(e);
     if (const char* e = std::getenv("PRRTC_WARP")) k->warp = std::atoi(e);
     if (const char* e = std::getenv("PRRTC_HELP_CAP")) k->help_cap = std::atoi(e);
+    if (const char* e = std::getenv("PRRTC_HELP_POLICY")) k->help_policy = std::atoi(e);
     if (const char* e = std::getenv("PRRTC_MNN_NODES")) k->mnn_nodes = std::max(1, std::atoi(e));
     if (const char* e = std::getenv("PRRTC_MAP_BYTES")) k->map_bytes = std::strtoll(e, nullptr, 10);
     if (const char* e = std::getenv("PRRTC_DUMP_CTL")) k->dump_ctl = e;
@@ -1231,6 +1233,7 @@ int batch_enqueue(prrtc_batch* b, cudaStream_t st, bool upload) {
     a.tail_claim = ek.tail_claim;
     // help joins stop at the problem's worker cap (an env override for sweeps)
     a.help_cap = ek.help_cap ? ek.help_cap : (int)b->params.max_workers_per_problem;
+    a.help_policy = ek.help_policy;
     a.p.budget = b->budget;
     a.p.seed = b->params.seed;
     a.p.uniform = b->params.sampler == PRRTC_SAMPLER_UNIFORM ? 1 : 0;

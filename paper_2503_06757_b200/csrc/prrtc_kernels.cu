@@ -726,8 +726,20 @@ __device__ bool init_problem(Ctx& c, const PlanArgs& a, int prob) {
     return true;
 }
 
-// Help mode: join the running problem with the fewest active CTAs (ties to
-// the lowest index). The parallel RRT-Connect iteration is elastic: any
+// Which running problem a free worker joins (lower key first, ties to the
+// lowest index): help_policy 1 = the most unclaimed budget per worker
+// (budget - tickets claimed) / (active + 1) — the longest remaining work,
+// which is what bounds a batch's makespan (the hardest problems are its long
+// poles and they parallelise: tools/scale_one.py); 0 = the fewest active
+// workers.
+__device__ __forceinline__ int help_key(const PlanArgs& a, int active, unsigned long long claimed) {
+    if (a.help_policy == 0) return active;
+    const unsigned long long rem = a.p.budget - claimed;  // (claimed < budget)
+    const unsigned long long per = rem * 16ull / (unsigned long long)(active + 1);
+    return 0x7ffffffe - (int)min(per, 0x7ffffff0ull);
+}
+
+// Help mode: join the running problem chosen by help_key. The parallel RRT-Connect iteration is elastic: any
 // number of workers may join a problem at any time. -1 when none is left.
 __device__ int pick_help(Ctx& c, const PlanArgs& a) {
     const int tid = threadIdx.x;
@@ -753,10 +765,13 @@ __device__ int pick_help(Ctx& c, const PlanArgs& a) {
             const int4 hdr = __ldcg(reinterpret_cast<const int4*>(&C));  // started, done, winner, active
             const unsigned long long it = __ldcg(&C.iters);
             pending |= hdr.x == 0 && hdr.y == DONE_RUNNING;  // claimed, endpoints still being checked
-            if (hdr.x == 1 && hdr.y == DONE_RUNNING && it < a.p.budget && hdr.w < bk &&
+            if (hdr.x == 1 && hdr.y == DONE_RUNNING && it < a.p.budget &&
                 (a.help_cap == 0 || hdr.w < a.help_cap)) {
-                bk = hdr.w;
-                bp = q;
+                const int key = help_key(a, hdr.w, it);
+                if (key < bk) {
+                    bk = key;
+                    bp = q;
+                }
             }
         }
         // every problem is claimed (the claim loop ran dry) and every running

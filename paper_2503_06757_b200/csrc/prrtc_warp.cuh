@@ -662,10 +662,13 @@ __device__ int warp_pick_help(const PlanArgs& a) {
             const int4 hdr = __ldcg(reinterpret_cast<const int4*>(&C));  // started, done, winner, active
             const unsigned long long it = __ldcg(&C.iters);
             pending |= hdr.x == 0 && hdr.y == DONE_RUNNING;  // claimed, endpoints still being checked
-            if (hdr.x == 1 && hdr.y == DONE_RUNNING && it < a.p.budget && hdr.w < bk &&
+            if (hdr.x == 1 && hdr.y == DONE_RUNNING && it < a.p.budget &&
                 (a.help_cap == 0 || hdr.w < a.help_cap)) {
-                bk = hdr.w;
-                bp = q;
+                const int key = help_key(a, hdr.w, it);
+                if (key < bk) {
+                    bk = key;
+                    bp = q;
+                }
             }
         }
         // every problem is claimed (the claim loop ran dry) and every running
