@@ -344,68 +344,85 @@ __device__ __forceinline__ int band(float d2, float rr, float eps) {
 // is a warp-uniform shared-memory broadcast and each state's data is
 // conflict-free (state is the fastest smem index).
 // ---------------------------------------------------------------------------
+// A pointer into the dynamic shared-memory window held as a 32-bit offset
+// (every CTA-context buffer lives there): an access costs one add, where a
+// generic pointer needs two generic->shared conversions (sh()) to let the
+// compiler emit LDS/STS — ~22M instructions and ~3 KB of hot code per
+// headline launch (ncu source view, r2d).
+extern __shared__ __align__(16) unsigned char g_dsmem[];
+template <class T>
+struct SPtr {
+    unsigned off;
+    __device__ __forceinline__ T* get() const { return reinterpret_cast<T*>(g_dsmem + off); }
+    __device__ __forceinline__ operator T*() const { return get(); }
+    __device__ __forceinline__ SPtr& operator=(T* p) {
+        off = (unsigned)__cvta_generic_to_shared(p) - (unsigned)__cvta_generic_to_shared(g_dsmem);
+        return *this;
+    }
+};
+
 struct Ctx {
     // robot (shared memory copy of the packed words)
     int L, dof, S, NP, MF, mflog;  // mflog: log2 of MF rounded up to a power of two
-    const int4* info;      // kind, parent, q_index, fine_off
-    const int* nfine;
-    const float* geo;      // [L][GEO_STRIDE]
-    const float4* fine;    // [S]
-    const int2* pairs;     // [NP]
-    const unsigned* bases; // [dof]
-    const unsigned long long* magic;  // [dof] ceil(2^64 / base)
-    const double* htab;    // [dof][kHaltonTab] Halton reciprocal powers (shared copy of the host table)
-    const int* flink;      // [S] link of each fine sphere
-    const int2* funits;    // [NFU] fine-stage units: (link, first sphere | count << 16)
+    SPtr<const int4> info;      // kind, parent, q_index, fine_off
+    SPtr<const int> nfine;
+    SPtr<const float> geo;      // [L][GEO_STRIDE]
+    SPtr<const float4> fine;    // [S]
+    SPtr<const int2> pairs;     // [NP]
+    SPtr<const unsigned> bases; // [dof]
+    SPtr<const unsigned long long> magic;  // [dof] ceil(2^64 / base)
+    SPtr<const double> htab;    // [dof][kHaltonTab] Halton reciprocal powers (shared copy of the host table)
+    SPtr<const int> flink;      // [S] link of each fine sphere
+    SPtr<const int2> funits;    // [NFU] fine-stage units: (link, first sphere | count << 16)
     int NFU;
     const double* fine_r64;  // global
-    const double* limits;    // global [dof][2]
+    SPtr<const double> limits;    // [dof][2] (shared copy, before the Halton table)
     unsigned fkflops;        // per-state FK + coarse posing flops
     long long* prof;         // per-phase clock64 stamps (debug hook only, else null)
-    double* ttab;            // [kTTab + 1]: i / ttab_n for i = 0..ttab_n (edge sample fractions)
+    SPtr<double> ttab;            // [kTTab + 1]: i / ttab_n for i = 0..ttab_n (edge sample fractions)
     int ttab_n;              // n_cc the table was built for (0 = none)
     // scene (shared memory copy)
     int ns, nb, nc, ny, P;
-    const float4* sph;
-    const float* box;
-    const float* cap;
-    const float* cyl;
+    SPtr<const float4> sph;
+    SPtr<const float> box;
+    SPtr<const float> cap;
+    SPtr<const float> cyl;
     float eps, cpad;
     SceneF64 s64;  // global FP64 mirror
     // per-chunk buffers
     int NS, nslog;   // states per chunk (32, 64 or 128)
-    float* pose;     // [L][12][NS]
-    float* ccen;     // [L][3][NS]
-    float* qf;       // [dof][NS]
-    int* sgroup;     // [NS] group id, -1 = inactive
-    int* sbad;       // [NS]
-    unsigned long long* lmask;  // [L][NS] coarse-flagged primitives per (link, state)
-    unsigned long long* pmask;  // [ceil(NP/64)][NS] coarse-flagged self pairs per state
-    double* ends;    // [NS + 2][dof] chain points of the chunk
-    int* ends_eq;    // [NS + 2] bitwise-equal sub-edge flags
+    SPtr<float> pose;     // [L][12][NS]
+    SPtr<float> ccen;     // [L][3][NS]
+    SPtr<float> qf;       // [dof][NS]
+    SPtr<int> sgroup;     // [NS] group id, -1 = inactive
+    SPtr<int> sbad;       // [NS]
+    SPtr<unsigned long long> lmask;  // [L][NS] coarse-flagged primitives per (link, state)
+    SPtr<unsigned long long> pmask;  // [ceil(NP/64)][NS] coarse-flagged self pairs per state
+    SPtr<double> ends;    // [NS + 2][dof] chain points of the chunk
+    SPtr<int> ends_eq;    // [NS + 2] bitwise-equal sub-edge flags
     // CTA scalars
-    int* ictl;       // [32] misc ints
-    double* dcfg;    // [8][kMaxDof] scratch configs
-    double* sbuf;    // [32][dof] Halton samples of the CTA's current ticket block
-    double* mnn_d;   // [32] multi-sample NN: squared distance per evaluated sample
-    int* mnn_i;      // [32]                  nearest index per evaluated sample
-    int* mnn_ok;     // [32]                  accepted (not duplicate, inside its dynamic domain)
-    double* red_d;   // [nwarps]
-    int* red_i;      // [nwarps]
+    SPtr<int> ictl;       // [32] misc ints
+    SPtr<double> dcfg;    // [8][kMaxDof] scratch configs
+    SPtr<double> sbuf;    // [32][dof] Halton samples of the CTA's current ticket block
+    SPtr<double> mnn_d;   // [32] multi-sample NN: squared distance per evaluated sample
+    SPtr<int> mnn_i;      // [32]                  nearest index per evaluated sample
+    SPtr<int> mnn_ok;     // [32]                  accepted (not duplicate, inside its dynamic domain)
+    SPtr<double> red_d;   // [nwarps]
+    SPtr<int> red_i;      // [nwarps]
     int nthreads;
     // stats: per-thread slots [nthreads][2] in shared memory (sphere tests,
     // algorithmic FP32 flops), summed when a CTA leaves a problem
-    unsigned long long* stat;
+    SPtr<unsigned long long> stat;
     // the planner loop's thread-0 state (ticket block, iteration and CheckStats
     // counters): kept in shared memory so it does not occupy registers
     // (spilled around every call) in all threads of the CTA
-    unsigned long long* t0;
+    SPtr<unsigned long long> t0;
     // exact-CheckStats mode (deterministic planning): counters follow the
     // reference's sequential semantics (ref_state_count); per-state scratch
     int ref_stats;
-    unsigned long long* mt;      // [kMtN + 1] SamplerKind::Uniform generator state + position
-    unsigned long long* rcount;  // [NS] reference sphere_tests of each state
-    int* rfine;                  // [NS] 1 if the state enters the fine stage
+    SPtr<unsigned long long> mt;      // [kMtN + 1] SamplerKind::Uniform generator state + position
+    SPtr<unsigned long long> rcount;  // [NS] reference sphere_tests of each state
+    SPtr<int> rfine;                  // [NS] 1 if the state enters the fine stage
 };
 
 enum : int {
@@ -426,7 +443,10 @@ __device__ __forceinline__ bool ctx_writer(const Ctx& c) { return !__isShared(&c
 // re-derives the pointer from the dynamic shared-memory symbol, which lets the
 // compiler prove the shared address space (LDS/STS, no aliasing with local
 // memory). Hot routines take their pointers into registers through it once.
-extern __shared__ __align__(16) unsigned char g_dsmem[];
+template <class T>
+__device__ __forceinline__ T* sh(const SPtr<T>& p) {
+    return p.get();
+}
 template <class T>
 __device__ __forceinline__ T* sh(T* p) {
     // integer offsets in the shared window (no cross-object pointer arithmetic)
@@ -710,7 +730,7 @@ __device__ __forceinline__ int test_flops(const SceneV& v, int p) {
 }
 
 #ifndef PRRTC_COARSE_UNROLL
-#define PRRTC_COARSE_UNROLL 2
+#define PRRTC_COARSE_UNROLL 1
 #endif
 #define PRRTC_PRAGMA(x) _Pragma(#x)
 #define PRRTC_UNROLL(n) PRRTC_PRAGMA(unroll n)

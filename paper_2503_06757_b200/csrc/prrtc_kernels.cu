@@ -443,7 +443,7 @@ __device__ void assemble_path_serial(Ctx& c, const PlanArgs& a, int prob, int me
     const int tid = threadIdx.x;
     const int dof = c.dof;
     const TreeRef Ta = tree_ref(a, prob, 0, dof), Tb = tree_ref(a, prob, 1, dof);
-    int* ib = reinterpret_cast<int*>(c.pose);
+    int* ib = reinterpret_cast<int*>(c.pose.get());
     const int ib_cap = c.L * 12 * c.NS;
     if (tid == 0) {
         int la = 1, lb = 1;
@@ -492,7 +492,7 @@ __device__ void assemble_path(Ctx& c, const PlanArgs& a, int prob, int meet_a, i
     const int tid = threadIdx.x;
     const int dof = c.dof;
     const TreeRef Ta = tree_ref(a, prob, 0, dof), Tb = tree_ref(a, prob, 1, dof);
-    int* ib = reinterpret_cast<int*>(c.pose);
+    int* ib = reinterpret_cast<int*>(c.pose.get());
     const int half = (c.L * 12 * c.NS) >> 1;
     if (tid == 0 || tid == 32) {
         const bool ta = tid == 0;
