@@ -216,7 +216,9 @@ struct TreeRef {
 constexpr int kTraceStride = 64;
 __shared__ long long g_trace[kTraceStride];
 __device__ __noinline__ void trace_phase_rec(int code);
+template <bool TR = true>
 __device__ __forceinline__ void trace_phase(const PlanArgs& a, int code) {
+    if constexpr (!TR) return;  // production instantiation: no trace code in the loop
     // out of line: ten call sites of the recorder would otherwise bloat the
     // hot loop's instruction footprint even with tracing off
     if (threadIdx.x == 0 && a.cta_trace) trace_phase_rec(code);
@@ -372,6 +374,7 @@ __device__ __noinline__ void ref_count_chain_chunk(Ctx& c, int cnt, bool two_sta
 // sub-edges appended, or -1 - appended if the tree filled up; the last
 // appended slot in *last.
 // ---------------------------------------------------------------------------
+template <bool TR>
 __device__ long long validate_chain(Ctx& c, const PlanArgs& a, const double* A, const double* B,
                                     long long n_sub, const TreeRef* T, int parent0, int* last,
                                     const int* done_flag, bool* stopped) {
@@ -382,7 +385,7 @@ __device__ long long validate_chain(Ctx& c, const PlanArgs& a, const double* A, 
     *last = parent0;
     if (total >= (1ll << 30)) return 0;  // beyond the 32-bit chain indexing: never valid (see gen_chain_states)
     for (long long g0 = 0; g0 < total; g0 += c.NS) {
-        trace_phase(a, 9);  // PRRTC_TRACE: chain states
+        trace_phase<TR>(a, 9);  // PRRTC_TRACE: chain states
         const int cnt = (int)min((long long)c.NS, total - g0);
         const int act = gen_chain_states_inl(c, A, B, n_sub, n_cc, g0, cnt, done_flag);
         if (done_flag && sh(c.ictl)[IC_STOP] != 0) {  // stop flag (planner.cpp:112): not running
@@ -393,9 +396,9 @@ __device__ long long validate_chain(Ctx& c, const PlanArgs& a, const double* A, 
             if (!c.ref_stats) sh(c.t0)[T0_FK] += act;
             sh(c.stat)[1] += (unsigned long long)act * c.fkflops;  // thread 0's flop slot
         }
-        trace_phase(a, 5);  // FK + collision
+        trace_phase<TR>(a, 5);  // FK + collision
         check_chunk_inl(c, cnt, a.p.two_stage != 0, a.p.early_exit != 0, false, done_flag);
-        trace_phase(a, 9);
+        trace_phase<TR>(a, 9);
         if (done_flag && sh(c.ictl)[IC_STOP] != 0) {  // settled while this chunk was checked
             *stopped = true;
             return 0;
@@ -410,7 +413,7 @@ __device__ long long validate_chain(Ctx& c, const PlanArgs& a, const double* A, 
     }
     long long appended = 0;
     int prev = parent0;
-    trace_phase(a, 8);  // append
+    trace_phase<TR>(a, 8);  // append
     while (appended < good) {
         const int cntk = (int)min(good - appended, (long long)c.NS + 1);
         const double* pts = B;  // a single edge appends its far end as is (collision.cpp:19)
@@ -852,7 +855,7 @@ __device__ void leave_problem(const PlanArgs& a, int prob, int reason_msg) {
     }
 }
 
-#define TRACE_PHASE(code) trace_phase(a, code)
+#define TRACE_PHASE(code) trace_phase<TR>(a, code)
 
 __shared__ Ctx g_ctx;  // the planner's CTA context (see ctx_writer)
 
@@ -887,7 +890,10 @@ __device__ void publish_result(Ctx& c, const PlanArgs& a) {
     }
 }
 
-template <int NT, int MINB>
+// TR: the PRRTC_TRACE instantiation (phase ring, per-CTA stamps); the
+// production one carries no trace code in its loop (hot code above the
+// 32 KB L1.5 instruction cache stalls on fetch)
+template <int NT, int MINB, bool TR>
 __global__ void __launch_bounds__(NT, MINB) plan_kernel(PlanArgs a) {
     extern __shared__ __align__(16) unsigned char smem[];
     Ctx& c = g_ctx;
@@ -921,7 +927,7 @@ __global__ void __launch_bounds__(NT, MINB) plan_kernel(PlanArgs a) {
     }
     const double R = a.p.dd_radius, delta = a.p.delta;
     if (tid == 0 && a.trace) atomicMax(&a.trace[0], 0x7fffffffffffffffull - (unsigned long long)globaltimer());
-    if (tid == 0 && a.cta_trace) {
+    if (TR && tid == 0 && a.cta_trace) {
         for (int k = 0; k < kTraceStride; ++k) g_trace[k] = 0;
         g_trace[3] = globaltimer();
     }
@@ -1134,7 +1140,7 @@ __global__ void __launch_bounds__(NT, MINB) plan_kernel(PlanArgs a) {
             for (;;) {
                 int last = par0;
                 bool stopped = false;
-                const long long got = validate_chain(c, a, VA, VB, nsub, &Ts, par0, &last, &C.done, &stopped);
+                const long long got = validate_chain<TR>(c, a, VA, VB, nsub, &Ts, par0, &last, &C.done, &stopped);
                 if (got < 0) {
                     outcome = 2;
                     break;
@@ -1220,17 +1226,17 @@ __global__ void __launch_bounds__(NT, MINB) plan_kernel(PlanArgs a) {
         // ---- leave ----
         TRACE_PHASE(10);
         if (tid == 0 && sh(c.t0)[T0_USED]) atomicAdd(&C.iters_used, sh(c.t0)[T0_USED]);
-        if (tid == 0 && a.cta_trace) g_trace[0] = globaltimer();
+        if (TR && tid == 0 && a.cta_trace) g_trace[0] = globaltimer();
         flush_stats(c, C);
         if (tid == 0) leave_problem(a, prob, leave_msg);
         __syncthreads();
-        if (tid == 0 && a.cta_trace) g_trace[1] = globaltimer();
+        if (TR && tid == 0 && a.cta_trace) g_trace[1] = globaltimer();
         // a single problem: nothing left to claim or help once it is left
         // (skips the claim / help-scan round trips on the way out)
         if (a.n_problems == 1) break;
     }
     if (tid == 0 && a.trace) atomicMax(&a.trace[1], (unsigned long long)globaltimer());
-    if (tid == 0 && a.cta_trace) {
+    if (TR && tid == 0 && a.cta_trace) {
         TRACE_PHASE(0);  // close the last phase
         g_trace[2] = globaltimer();
         for (int k = 0; k < kTraceStride; ++k) a.cta_trace[blockIdx.x * kTraceStride + k] = g_trace[k];
@@ -1359,19 +1365,22 @@ cudaError_t launch_validate_paths(const RobotArgs& r, const PlanArgs& a, int* pr
 // CTA size variants: 128 threads (4 warps, up to 4 CTAs/SM) and 256 threads
 // (8 warps, 2 CTAs/SM: each iteration's parallel phases finish faster).
 using PlanFn = void (*)(PlanArgs);
-static PlanFn plan_fn(int nthreads) {
-    if (nthreads == 256) return plan_kernel<256, 2>;
-    if (nthreads == 512) return plan_kernel<512, 1>;
-    static const int minb = [] {
-        const char* e = getenv("PRRTC_PLAN_MINB");
-        return e ? atoi(e) : 4;
-    }();
-    return minb == 6 ? plan_kernel<128, 6> : (minb == 5 ? plan_kernel<128, 5> : plan_kernel<128, 4>);
+// (5 or 6 CTAs of 128 threads per SM, 96 / 80 registers, spill and were
+// measured 12-25% slower: DESIGN.md §9)
+static PlanFn plan_fn(int nthreads, bool trace) {
+    if (trace) {
+        if (nthreads == 256) return plan_kernel<256, 2, true>;
+        if (nthreads == 512) return plan_kernel<512, 1, true>;
+        return plan_kernel<128, 4, true>;
+    }
+    if (nthreads == 256) return plan_kernel<256, 2, false>;
+    if (nthreads == 512) return plan_kernel<512, 1, false>;
+    return plan_kernel<128, 4, false>;
 }
 
 cudaError_t launch_plan(const RobotArgs& r, PlanArgs a, int grid, cudaStream_t st) {
     const size_t sm = smem_bytes(r, a.ns_max, a.nthreads, plan_scene_words(a), a.p.uniform != 0);
-    const PlanFn fn = plan_fn(a.nthreads);
+    const PlanFn fn = plan_fn(a.nthreads, a.cta_trace != nullptr);
     cudaError_t e = raise_smem_limit(reinterpret_cast<const void*>(fn), (int)sm);
     if (e != cudaSuccess) return e;
     void* args[] = {&a};
@@ -1380,7 +1389,7 @@ cudaError_t launch_plan(const RobotArgs& r, PlanArgs a, int grid, cudaStream_t s
 
 int plan_occupancy(const RobotArgs& r, int ns_max, int nthreads, int scene_words, bool with_mt) {
     const size_t sm = smem_bytes(r, ns_max, nthreads, scene_words, with_mt);
-    const PlanFn fn = plan_fn(nthreads);
+    const PlanFn fn = plan_fn(nthreads, false);
     raise_smem_limit(reinterpret_cast<const void*>(fn), (int)sm);
     int n = 0;
     if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, fn, nthreads, sm) != cudaSuccess) return 1;
