@@ -1294,14 +1294,21 @@ const char* message_for(int msg) {
 }
 
 // path_cost (planner.cpp:152-158) with the scalar distance (nn.cpp:12-20).
-double path_cost(const double* path, uint32_t len, uint32_t dof) {
+// path_cost (planner.cpp:152-158) and, in the same pass, assemble_path's
+// zero-length check (planner.cpp:144-148: no bitwise-equal consecutive
+// configs; a zero distance is confirmed bitwise, so +0 / -0 pairs pass).
+double path_cost(const double* path, uint32_t len, uint32_t dof, bool* zero_segment) {
     double cost = 0.0;
+    *zero_segment = false;
     for (uint32_t i = 1; i < len; ++i) {
         double acc = 0.0;
+        const double* a = path + (size_t)(i - 1) * dof;
+        const double* b = path + (size_t)i * dof;
         for (uint32_t d = 0; d < dof; ++d) {
-            const double e = path[(size_t)(i - 1) * dof + d] - path[(size_t)i * dof + d];
+            const double e = a[d] - b[d];
             acc += e * e;
         }
+        if (acc == 0.0 && std::memcmp(a, b, sizeof(double) * dof) == 0) *zero_segment = true;
         cost += std::sqrt(acc);
     }
     return cost;
@@ -1552,6 +1559,20 @@ int fill_results(prrtc_batch* b, prrtc_result* out, const unsigned char* h, cons
                     max_exit = std::max(max_exit, t[2] - t[1]);
                 }
             }
+            {  // when the CTAs left the kernel (t[2], globaltimer): the share of CTA time a batch's tail idles
+                std::vector<long long> ex;
+                for (int g = 0; g < b->grid; ++g)
+                    if (ct[64 * g + 2]) ex.push_back(ct[64 * g + 2] - k0);
+                std::sort(ex.begin(), ex.end());
+                if (!ex.empty()) {
+                    double busy = 0;
+                    for (long long e : ex) busy += (double)e;
+                    auto q = [&](double f) { return ex[std::min(ex.size() - 1, (size_t)(f * ex.size()))] * 1e-6; };
+                    std::fprintf(stderr,
+                                 "prrtc trace: CTA exits (ms) p10 %.3f p50 %.3f p90 %.3f max %.3f | CTA-time used %.1f%%\n",
+                                 q(0.1), q(0.5), q(0.9), ex.back() * 1e-6, 100.0 * busy / ((double)ex.back() * ex.size()));
+                }
+            }
             std::fprintf(stderr,
                          "prrtc trace: latest CTA start +%.3f ms | latest leave after last done %.3f (CTA %d) | "
                          "max flush+leave %.3f | max leave->exit %.3f\n",
@@ -1591,25 +1612,22 @@ int fill_results(prrtc_batch* b, prrtc_result* out, const unsigned char* h, cons
                 r.path = static_cast<double*>(std::malloc(sizeof(double) * b->dof * C.path_len));
                 std::memcpy(r.path, arena + C.path_off, sizeof(double) * b->dof * C.path_len);
             }
-            r.cost = path_cost(r.path, r.path_len, b->dof);
+            bool zero_segment = false;
+            r.cost = path_cost(r.path, r.path_len, b->dof, &zero_segment);
             // planner.cpp:144-148: no zero-length (bitwise-equal) segment
-            for (uint32_t k = 1; k < r.path_len; ++k)
-                if (std::memcmp(r.path + (size_t)(k - 1) * b->dof, r.path + (size_t)k * b->dof,
-                                sizeof(double) * b->dof) == 0) {
-                    if (r.path_block) {  // not handed out: drop the view
-                        r.path = nullptr;
-                        r.path_len = 0;
-                        r.path_block = 0;
-                        --block_refs;
-                    } else {
-                        prrtc_result_free(&r);
-                    }
-                    r.status = PRRTC_FAILED;
-                    r.cost = 0.0;
-                    std::snprintf(r.message, sizeof(r.message),
-                                  "assemble_path: zero-length segment in assembled path");
-                    break;
+            if (zero_segment) {
+                if (r.path_block) {  // not handed out: drop the view
+                    r.path = nullptr;
+                    r.path_len = 0;
+                    r.path_block = 0;
+                    --block_refs;
+                } else {
+                    prrtc_result_free(&r);
                 }
+                r.status = PRRTC_FAILED;
+                r.cost = 0.0;
+                std::snprintf(r.message, sizeof(r.message), "assemble_path: zero-length segment in assembled path");
+            }
         } else if (r.status == PRRTC_SOLVED) {
             r.status = PRRTC_FAILED;
             std::snprintf(r.message, sizeof(r.message), "path unavailable");

@@ -404,3 +404,35 @@ def test_uniform_sampler_replays_reference(gpu, oracle):
                 assert r.iterations_total == ref.iterations_total
                 assert r.check_stats == ref.check_stats
     assert same >= 0.9 * 2 * len(probs), same
+
+
+def test_batch_paths_live_until_freed(gpu):
+    """A batch's paths share one pooled pinned block (prrtc_capi.cu
+    PathBlock): every path stays valid until its own prrtc_result_free, while
+    later batches take blocks from the pool, and frees in any order release
+    the block once (exercised over repeated batches so blocks are reused)."""
+    import ctypes as C
+    from paper_2503_06757_b200 import _lib
+    m = robots.get("panda")
+    probs = load_problems("panda", 1000)[::10]
+    scenes = planner.device_scenes([make_scene("panda", k, p)[0] for k, p, _, _ in probs])
+    S = np.array([p[2] for p in probs])
+    G = np.array([p[3] for p in probs])
+    params = PlannerParams(workers=1, tree_capacity=20000, max_workers_per_problem=1)
+    lib = _lib.load()
+    kept = []
+    for rep in range(6):
+        _, res, n, _ = planner._plan_batch_raw(m, scenes, S, G, params, 0)
+        copies = [planner._to_result(res[i], m.dof).path for i in range(n)]
+        assert sum(res[i].path_block != 0 for i in range(n)) == sum(len(c) > 0 for c in copies)
+        kept.append((res, n, copies))
+        if rep % 2 == 1:  # free an earlier batch in a scrambled order, one result at a time
+            old, k, _ = kept.pop(0)
+            for i in np.random.default_rng(rep).permutation(k):
+                lib.prrtc_result_free(C.byref(old[int(i)]))
+                assert not old[int(i)].path and old[int(i)].path_block == 0
+    for res, n, copies in kept:  # still intact after the later batches reused the pool
+        for i in range(n):
+            now = planner._to_result(res[i], m.dof).path
+            assert np.array_equal(now, copies[i])
+        planner._free(res, n)
