@@ -77,6 +77,7 @@ struct EnvKnobs {
     int warp = -1;  // PRRTC_WARP=1: eligible batches on the warp-worker planner (A/B runs)
     int help_cap = 0;  // PRRTC_HELP_CAP: most workers a help join may bring a problem to (sweeps)
     int help_policy = 1;  // PRRTC_HELP_POLICY: 1 most unclaimed budget per worker, 0 fewest workers (A/B)
+    bool no_stab = false;  // PRRTC_NO_SAMPLE_TABLE: compute every Halton sample in the loop (A/B)
     long long map_bytes = -1;
     std::string dump_ctl;
 };
@@ -97,6 +98,7 @@ const EnvKnobs* read_env() {
     if (const char* e = std::getenv("PRRTC_WARP")) k->warp = std::atoi(e);
     if (const char* e = std::getenv("PRRTC_HELP_CAP")) k->help_cap = std::atoi(e);
     if (const char* e = std::getenv("PRRTC_HELP_POLICY")) k->help_policy = std::atoi(e);
+    k->no_stab = on("PRRTC_NO_SAMPLE_TABLE");
     if (const char* e = std::getenv("PRRTC_MNN_NODES")) k->mnn_nodes = std::max(1, std::atoi(e));
     if (const char* e = std::getenv("PRRTC_MAP_BYTES")) k->map_bytes = std::strtoll(e, nullptr, 10);
     if (const char* e = std::getenv("PRRTC_DUMP_CTL")) k->dump_ctl = e;
@@ -218,6 +220,9 @@ struct prrtc_robot {
     double reach = 0.0;           // bound on |posed sphere| (m)
     // planner CTAs per SM, by (ns_max / 32, CTA size) x (Uniform sampler) x (scene-size bucket)
     mutable std::atomic<int> occ[15 * 2 * 5] = {};
+    // Halton sample tables per seed (sample_table): [kSampleTab][dof] doubles
+    mutable std::mutex stab_mu;
+    mutable std::vector<std::pair<uint64_t, double*>> stab;
     RobotArgs args() const {
         RobotArgs r;
         r.words = d_words;
@@ -527,6 +532,7 @@ int prrtc_robot_destroy(prrtc_robot* r) {
     cudaFree(r->d_words);
     cudaFree(r->d_fine_r64);
     cudaFree(r->d_limits);
+    for (auto& t : r->stab) cudaFree(t.second);
     delete r;
     return PRRTC_OK;
 }
@@ -957,6 +963,36 @@ int check_params(const prrtc_params* p) {  // planner.cpp:250-252
     return PRRTC_OK;
 }
 
+// The Halton samples of tickets [0, kSampleTab) for (robot, seed): every
+// problem of a batch draws the same ones (sample index 1 + seed + ticket in
+// the robot's limits), so they are computed once — by debug_sample_kernel,
+// the planner's own sampler (bit-exact, test_sample_config_bitexact) — and
+// read from L2 by every CTA instead of recomputed per ticket block (the
+// sample phase was ~5.6% of planner CTA cycles). Built synchronously on first
+// use and kept for the robot's lifetime (a launch may still read an older
+// table, so none is freed early); at most kSampleTabs seeds per robot.
+constexpr unsigned long long kSampleTab = 4096;
+constexpr size_t kSampleTabs = 16;
+const double* sample_table(const prrtc_robot* r, uint64_t seed, cudaStream_t st) {
+    std::lock_guard<std::mutex> lk(r->stab_mu);
+    for (const auto& t : r->stab)
+        if (t.first == seed) return t.second;
+    if (r->stab.size() >= kSampleTabs) return nullptr;
+    double* d = nullptr;
+    if (cudaMalloc(&d, sizeof(double) * kSampleTab * r->dof) != cudaSuccess) {
+        cudaGetLastError();
+        return nullptr;
+    }
+    if (launch_debug_sample(r->args(), 1 + seed, (int)kSampleTab, d, st) != cudaSuccess ||
+        cudaStreamSynchronize(st) != cudaSuccess) {
+        cudaGetLastError();
+        cudaFree(d);
+        return nullptr;
+    }
+    r->stab.emplace_back(seed, d);
+    return d;
+}
+
 // the largest dynamic shared memory a CTA may opt into (cached per device)
 int smem_optin(int device) {
     static std::atomic<int> cache[64];
@@ -1234,6 +1270,12 @@ int batch_enqueue(prrtc_batch* b, cudaStream_t st, bool upload) {
     // help joins stop at the problem's worker cap (an env override for sweeps)
     a.help_cap = ek.help_cap ? ek.help_cap : (int)b->params.max_workers_per_problem;
     a.help_policy = ek.help_policy;
+    a.stab = nullptr;
+    a.stab_n = 0;
+    if (b->params.sampler == PRRTC_SAMPLER_HALTON && !ek.no_stab) {
+        a.stab = sample_table(b->robot, b->params.seed, st);
+        a.stab_n = a.stab ? kSampleTab : 0;
+    }
     a.p.budget = b->budget;
     a.p.seed = b->params.seed;
     a.p.uniform = b->params.sampler == PRRTC_SAMPLER_UNIFORM ? 1 : 0;

@@ -166,6 +166,10 @@ struct PlanArgs {
     int scene_words_max;                // warp-worker planner: words of the largest bound scene
     int help_cap;                       // help mode joins only problems with fewer active workers (0 = any)
     int help_policy;                    // which problem help joins: 1 most unclaimed budget per worker, 0 fewest workers
+    // Halton samples of tickets [0, stab_n): [ticket][dof], computed once per
+    // (robot, seed) by the planner's own sampler (null: compute in the loop)
+    const double* stab;
+    unsigned long long stab_n;
     // single-problem launches with inline inputs (no H2D copy): start and goal
     // travel in the kernel parameters, CTA 0 zeroes the out-header and the
     // controls and releases *init_flag = epoch, the other CTAs acquire it

@@ -1079,9 +1079,14 @@ __global__ void __launch_bounds__(NT, MINB) plan_kernel(PlanArgs a) {
                 else
                 for (int j = tid; j < nblk * dof; j += c.nthreads) {
                     const int k = j / dof, d = j - k * dof;
-                    sh(c.sbuf)[j] = sample_dim(halton_tab(sh(c.bases)[d], sh(c.magic)[d], sh(c.htab) + d * kHaltonTab,
-                                                            1ull + a.p.seed + base + k),
-                                                 sh(c.limits)[2 * d], sh(c.limits)[2 * d + 1]);
+                    // every problem of the launch draws the same samples (same
+                    // robot limits, seed and ticket range): the per-launch
+                    // table holds them, computed by this same routine
+                    const unsigned long long t = base + k;
+                    sh(c.sbuf)[j] = t < a.stab_n ? __ldg(a.stab + t * dof + d)
+                                                 : sample_dim(halton_tab(sh(c.bases)[d], sh(c.magic)[d],
+                                                                         sh(c.htab) + d * kHaltonTab, 1ull + a.p.seed + t),
+                                                              sh(c.limits)[2 * d], sh(c.limits)[2 * d + 1]);
                 }
             }
             __syncthreads();

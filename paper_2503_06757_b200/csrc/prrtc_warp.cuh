@@ -951,8 +951,10 @@ __global__ void __launch_bounds__(512, 1) plan_warp_kernel(PlanArgs a) {
                 __syncwarp();  // the previous block's samples are read before they are overwritten
                 for (int j = lane; j < nblk * dof; j += 32) {
                     const int k = j / dof, d = j - k * dof;
-                    wr.sbuf[j] = sample_dim(halton_tab(bases[d], magic[d], htab + d * kHaltonTab, 1ull + a.p.seed + tk_base + k),
-                                            lim[2 * d], lim[2 * d + 1]);
+                    const unsigned long long t = tk_base + k;  // (the per-launch sample table, see plan_kernel)
+                    wr.sbuf[j] = t < a.stab_n ? __ldg(a.stab + t * dof + d)
+                                              : sample_dim(halton_tab(bases[d], magic[d], htab + d * kHaltonTab, 1ull + a.p.seed + t),
+                                                           lim[2 * d], lim[2 * d + 1]);
                 }
                 __syncwarp();
             }
