@@ -387,11 +387,10 @@ __device__ long long validate_chain(Ctx& c, const PlanArgs& a, const double* A, 
     for (long long g0 = 0; g0 < total; g0 += c.NS) {
         trace_phase<TR>(a, 9);  // PRRTC_TRACE: chain states
         const int cnt = (int)min((long long)c.NS, total - g0);
-        const int act = gen_chain_states_inl(c, A, B, n_sub, n_cc, g0, cnt, done_flag);
-        if (done_flag && sh(c.ictl)[IC_STOP] != 0) {  // stop flag (planner.cpp:112): not running
-            *stopped = true;
-            return 0;
-        }
+        // (the problem's done flag, planner.cpp:112, is sampled once per chunk
+        // by check_chunk after FK, where its L2 round trip is hidden; sampled
+        // here too it held every chunk's state-generation barrier for it)
+        const int act = gen_chain_states_inl(c, A, B, n_sub, n_cc, g0, cnt, nullptr);
         if (threadIdx.x == 0) {
             if (!c.ref_stats) sh(c.t0)[T0_FK] += act;
             sh(c.stat)[1] += (unsigned long long)act * c.fkflops;  // thread 0's flop slot
