@@ -147,10 +147,12 @@ typedef struct prrtc_params {
     int32_t sampler;               /* PRRTC_SAMPLER_HALTON */
     uint64_t seed;                 /* 0 */
     /* --- device knobs (no reference equivalent) --- */
-    uint32_t threads_per_cta;      /* 0 = automatic: 512 for one problem, 128 (256 for large
-                                      robots) for batches; else 128, 256 or 512; 32 = a
-                                      batch on the warp-worker planner (one worker per
-                                      warp; not for deterministic / Uniform-sampler runs) */
+    uint32_t threads_per_cta;      /* 0 = automatic: 512 for one problem; a batch runs on
+                                      128-thread CTAs, or on the warp-worker planner (one
+                                      worker per warp) when it holds >= 3x as many problems
+                                      as the device has warp workers; else 128, 256 or
+                                      512, or 32 = the warp-worker planner (not for
+                                      deterministic / Uniform-sampler runs) */
     uint32_t ctas_per_sm;          /* 0 = as many as co-reside */
     uint32_t deterministic;        /* 1 = single CTA, Halton stride 1: replays
                                       the reference's workers=1 mode */

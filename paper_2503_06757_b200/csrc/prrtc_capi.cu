@@ -926,7 +926,7 @@ struct prrtc_batch {
     int grid = 0, nthreads = 128, ns_max = 32;
     // warp-worker planner (plan_warp_kernel): eligible batches run one worker
     // per warp, `warps` warps in one CTA per SM (0: the CTA planner runs it)
-    bool warp_ok = false;
+    bool warp_ok = false, warp_auto = false;
     int warps = 0, cta_grid = 0, scene_words_max = 0;
     unsigned long long budget = 0, arena = 0;
     cudaStream_t last_stream = 0;
@@ -1048,25 +1048,32 @@ int batch_setup(prrtc_batch* b, const prrtc_robot* robot, const prrtc_scene* con
     // latency per iteration); batches use 128-thread CTAs (more independent
     // workers per SM) unless the robot is large (many fine spheres or self
     // pairs, e.g. the dual-arm Baxter), where the split pays again
-    const bool heavy = robot->n_fine > 64 || robot->n_pairs > 48;
     // a single problem: 512-thread CTAs, one per SM (16 warps split each
     // chunk's links / primitives / pairs: measured -3% / -6% / -21% median
     // latency for Panda / Fetch / Baxter against 256, tools/lat_variants.py)
+    // (batches of large robots used 256-thread CTAs until this round's hot
+    // code changes; 128 is now faster for Baxter too: 1000 problems 12.7 ->
+    // 11.7 ms, 3333 problems 41.0 -> 37.2 ms)
     b->nthreads = params->threads_per_cta && params->threads_per_cta != 32
                       ? (int)params->threads_per_cta
-                      : (n_problems == 1 ? 512 : (heavy ? 256 : 128));
+                      : (n_problems == 1 ? 512 : 128);
     const EnvKnobs& ekw = env();
-    // threads_per_cta = 32: the warp-worker planner (one RRT-Connect worker
-    // per warp, plan_warp_kernel) — for batches whose mode allows it (not
-    // deterministic replay with its exact CheckStats, not the Uniform
-    // sampler's per-CTA generator, no phase tracer or debug flags). Measured
-    // against the CTA planner: Fetch batches of 3k-10k
-    // problems 11-25% faster, Panda's 1000-problem headline 1.6x slower (its
-    // tail is per-problem latency, which one warp stretches), so it is not
-    // the default. PRRTC_WARP=1 selects it for every eligible batch (A/B).
-    b->warp_ok = n_problems > 1 && !params->deterministic && params->sampler == PRRTC_SAMPLER_HALTON &&
-                 !ekw.trace && ekw.debug_flags == 0 &&
-                 (params->threads_per_cta == 32 || (params->threads_per_cta == 0 && ekw.warp == 1));
+    // The warp-worker planner (one RRT-Connect worker per warp,
+    // plan_warp_kernel) for batches whose mode allows it (not deterministic
+    // replay with its exact CheckStats, not the Uniform sampler's per-CTA
+    // generator, no phase tracer or debug flags): asked for with
+    // threads_per_cta = 32, and chosen automatically (threads_per_cta = 0)
+    // when the batch holds at least 3x as many problems as the device has
+    // warp workers (batch_bind): its weakness is per-problem latency, which
+    // only a long tail of problems exposes (Panda 3333
+    // problems 2.9 vs 4.0 ms, 10k 8.1 vs 8.1; Fetch 10k 48.8 vs 37.4;
+    // Baxter 3333 37.2 vs 34.7, 10k 110.5 vs 100.1). PRRTC_WARP=1 / 0 force
+    // it on / off for every eligible batch (A/B).
+    const bool warp_mode_ok = n_problems > 1 && !params->deterministic &&
+                              params->sampler == PRRTC_SAMPLER_HALTON && !ekw.trace && ekw.debug_flags == 0;
+    b->warp_ok = warp_mode_ok && (params->threads_per_cta == 32 ||
+                                  (params->threads_per_cta == 0 && ekw.warp != 0));
+    b->warp_auto = b->warp_ok && params->threads_per_cta == 0 && ekw.warp < 0;
     // states per validation chunk: one n_cc = 32 edge; a 256-thread CTA uses
     // its extra warps to split links / pairs / primitives of the same chunk.
     // A single problem (latency-bound, one CTA per SM) takes 64-state chunks:
@@ -1180,7 +1187,9 @@ int batch_bind(prrtc_batch* b, Workspace* ws, const prrtc_scene* const* scenes, 
     b->scene_words_max = (int)((mx + 3) & ~size_t(3));
     if (b->warp_ok) {
         b->warps = warp_workers_per_sm(b->robot->words.data(), b->scene_words_max, smem_optin(b->device));
-        if (b->warps > 0) b->grid = sm_count(b->device);
+        const int sms = sm_count(b->device);
+        if (b->warp_auto && (long long)b->n < 3ll * b->warps * sms) b->warps = 0;  // the CTA planner
+        if (b->warps > 0) b->grid = sms;
     }
     return PRRTC_OK;
 }
