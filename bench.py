@@ -752,23 +752,28 @@ def run_b200(args):
 
     # ---- e2e through the host-buffer C-ABI (prrtc_plan_batch), every rank,
     # barrier + max over ranks (whole-job problems/s) ----
-    dscenes = planner.device_scenes(scenes, dev)  # setup: handles packed once
-    planner.plan_batch_arrays(model, dscenes, S, G, params, device=dev)  # workspace warm
+    # setup: robot and scene handles uploaded once — a call
+    # then costs the inputs' H2D, the kernel, the results' D2H and unpacking
+    # (passing the RobotModel itself would re-fingerprint it, ~0.12 ms of
+    # Python per call, to catch mutation)
+    drob = planner.device_robot(model, dev)
+    dscenes = planner.device_scenes(scenes, dev)
+    planner.plan_batch_arrays(drob, dscenes, S, G, params, device=dev)  # workspace warm
     e2e_ms = []
     for _ in range(max(3, min(args.steps, 10))):
         dist_barrier(world)
         t0 = time.perf_counter()
-        er = planner.plan_batch_arrays(model, dscenes, S, G, params, device=dev)
+        er = planner.plan_batch_arrays(drob, dscenes, S, G, params, device=dev)
         e2e_ms.append(dist_max((time.perf_counter() - t0) * 1e3, world))
     e2e_solved = dist_sum(float(np.sum(er.status == PlanStatus.Solved)), world) / total_n
     # sound mode (validate_path: every path re-checked on the device at 4 n_cc, failures re-planned)
     sp = headline_params(validate_path=True)
-    planner.plan_batch_arrays(model, dscenes, S, G, sp, device=dev)
+    planner.plan_batch_arrays(drob, dscenes, S, G, sp, device=dev)
     s_ms = []
     for _ in range(3):
         dist_barrier(world)
         t0 = time.perf_counter()
-        sr = planner.plan_batch_arrays(model, dscenes, S, G, sp, device=dev)
+        sr = planner.plan_batch_arrays(drob, dscenes, S, G, sp, device=dev)
         s_ms.append(dist_max((time.perf_counter() - t0) * 1e3, world))
     s_solved = dist_sum(float(np.sum(sr.status == PlanStatus.Solved)), world) / total_n
     mixed = None if args.no_extras else mixed_sharded(dev, world, rank)
@@ -780,7 +785,7 @@ def run_b200(args):
         achieved = flops / (kernel_ms * 1e-3) / 1e12
         import ctypes
         h2d_c, d2h_c = ctypes.c_uint64(), ctypes.c_uint64()
-        planner.plan_batch_arrays(model, dscenes, S, G, params, device=dev)  # the e2e call, for its byte count
+        planner.plan_batch_arrays(drob, dscenes, S, G, params, device=dev)  # the e2e call, for its byte count
         _lib.check(lib.prrtc_last_transfer_bytes(dev, ctypes.byref(h2d_c), ctypes.byref(d2h_c)))
         # ---- single-problem latency (prrtc_plan, host wall clock), per worker count ----
         from paper_2503_06757_b200 import suite

@@ -17,9 +17,9 @@ model, scenes, S, G, kinds = bench.load_workload(robot, n)
 rob = planner.device_robot(model)
 dsc = [planner.device_scene(s) for s in scenes]
 variants = {
-    "default(256t)": bench.robot_params(robot, PlannerParams()),
-    "512t": bench.robot_params(robot, PlannerParams(threads_per_cta=512)),
-    "512t_ns128": None,
+    "default(512t)": bench.robot_params(robot, PlannerParams()),
+    "256t": bench.robot_params(robot, PlannerParams(threads_per_cta=256)),
+    "128t": bench.robot_params(robot, PlannerParams(threads_per_cta=128)),
 }
 for rep in range(reps):
     for name, p in variants.items():
