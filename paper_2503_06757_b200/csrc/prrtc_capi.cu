@@ -232,6 +232,7 @@ struct prrtc_robot {
         r.n_links = n_links;
         r.dof = dof;
         r.n_fine = n_fine;
+        r.host_words = words.data();
         return r;
     }
 };
@@ -280,6 +281,7 @@ struct prrtc_scene {
         s.f64.b = d_f64 + 4 * ns;
         s.f64.c = d_f64 + 4 * ns + BOX_STRIDE * nb;
         s.f64.y = d_f64 + 4 * ns + BOX_STRIDE * nb + CAP_STRIDE * nc;
+        s.n_words = (int)((words.size() + 3) & ~size_t(3));
         return s;
     }
 };

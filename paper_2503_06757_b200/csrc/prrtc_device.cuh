@@ -768,6 +768,40 @@ PRRTC_UNROLL(PRRTC_COARSE_UNROLL)
     if (p < p1) m |= coarse_mask_cyl(v.cyl, v.nsbc, x, y, z, rc, p, p1);  // cylinders (extension)
     return m;
 }
+// coarse_mask unrolled 4x (independent primitive tests in flight): the
+// brute-force checkers' FP32 pre-mask over every primitive per fine sphere
+// (dense checking only, so the planner's hot loop keeps the compact form)
+__device__ __forceinline__ unsigned long long coarse_mask_dense(const SceneV& v, float x, float y, float z,
+                                                          float rc, int p0, int p1) {
+    unsigned long long m = 0;
+    const int e1 = min(p1, v.ns), e2 = min(p1, v.ns + v.nb);
+    int p = p0;
+PRRTC_UNROLL(4)
+    for (; p < e1; ++p) {
+        float d2;
+        const float4 s = v.sph[p];
+        sph_d2(x, y, z, s, d2);
+        const float rr = rc + s.w;
+        if (d2 < rr * rr) m |= 1ull << p;
+    }
+PRRTC_UNROLL(4)
+    for (; p < e2; ++p) {
+        float d2;
+        box_d2(x, y, z, v.box + (p - v.ns) * BOX_STRIDE, d2);
+        if (d2 < rc * rc) m |= 1ull << p;
+    }
+    const int e3 = min(p1, v.nsbc);
+PRRTC_UNROLL(4)
+    for (; p < e3; ++p) {
+        float d2;
+        const float* C = v.cap + (p - v.ns - v.nb) * CAP_STRIDE;
+        cap_d2(x, y, z, C, d2);
+        const float rr = rc + C[7];
+        if (d2 < rr * rr) m |= 1ull << p;
+    }
+    if (p < p1) m |= coarse_mask_cyl(v.cyl, v.nsbc, x, y, z, rc, p, p1);  // cylinders (extension)
+    return m;
+}
 
 __device__ __forceinline__ int range_flops(const SceneV& v, int p0, int p1) {
     const int e1 = min(p1, v.ns), e2 = min(p1, v.ns + v.nb), e3 = min(p1, v.nsbc);
@@ -871,7 +905,7 @@ __device__ __noinline__ void brute_chunk(Ctx& c, int cnt, bool early_exit, bool 
             // only those within two guard bands go through the banded test
             // and its exact fallback — the rest are certainly free (band()
             // would return 0), so the verdicts are unchanged
-            unsigned long long m = coarse_mask(v, x.x, x.y, x.z, f.w + 2.0f * v.eps, 0, v.P);
+            unsigned long long m = coarse_mask_dense(v, x.x, x.y, x.z, f.w + 2.0f * v.eps, 0, v.P);
             acc.t += v.P;
             acc.f += 18 + pflops;
             while (m) {

@@ -1818,6 +1818,16 @@ cudaError_t launch_validate_edges(const RobotArgs& r, const SceneArgs& s, const 
                                   const double* to, int n_edges, int n_cc, int two_stage,
                                   int early_exit, uint8_t* out, cudaStream_t st, long long* prof,
                                   unsigned long long* counters) {
+    // the warp-per-edge checker unless the chunk-profile debug hook asks for
+    // the CTA one (prof) or the robot does not fit a warp region
+    if (!prof && r.host_words && s.n_words > 0) {
+        int dev = 0, optin = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+        if (warp_workers_per_sm(r.host_words, s.n_words, optin) > 0)
+            return launch_validate_edges_warp(r, s, from, to, n_edges, n_cc, two_stage, early_exit, out, st,
+                                              counters, cur_sms(), optin);
+    }
     const int NS = chunk_states();
     const size_t sm = smem_bytes(r, NS, 128, SCENE_MAX_WORDS, true);
     cudaError_t e = raise_smem_limit(reinterpret_cast<const void*>(validate_edges_kernel), (int)sm);

@@ -16,11 +16,13 @@ struct RobotArgs {
     const double* fine_r64; // device
     const double* limits;   // device [dof][2]
     int n_links, dof, n_fine;
+    const uint32_t* host_words;  // the same packed robot on the host (launch sizing)
 };
 
 struct SceneArgs {
     const uint32_t* words;  // packed scene (device)
     SceneF64 f64;           // device
+    int n_words;            // packed scene words (launch sizing)
 };
 
 size_t smem_bytes(const RobotArgs& r, int ns_max, int nthreads, int scene_words, bool with_mt);

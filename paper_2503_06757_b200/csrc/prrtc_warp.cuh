@@ -272,7 +272,7 @@ __device__ __forceinline__ bool lane_check(const SceneV& v, float cpad, const do
                 const float4 f = fine[j];
                 const float3 x = pose_apply(W, f.x, f.y, f.z);
                 const double rd = __ldg(fine_r64 + j);
-                unsigned long long mm = coarse_mask(v, x.x, x.y, x.z, f.w + 2.0f * v.eps, 0, v.P);
+                unsigned long long mm = coarse_mask_dense(v, x.x, x.y, x.z, f.w + 2.0f * v.eps, 0, v.P);
                 acc.t += v.P;
                 acc.f += 18 + pflops;
                 while (mm) {
@@ -303,8 +303,11 @@ __device__ __forceinline__ bool lane_check(const SceneV& v, float cpad, const do
             const PoseR PA = pose_load(pstore + lane, 32, sa, 0);
             const int ja0 = info[a].w, na = nfine[a];
             const float rca = geo[a * GEO_STRIDE + 36] + 2.0f * cpad;
+            // (brute force without early exit runs every fine x fine test,
+            // collision.cpp:89-98 as the dense CheckStats count them)
+            const bool all_tests = !two_stage && !early_exit;
             bool hit = false;
-            for (int i = j0; i < j1 && !hit; ++i) {
+            for (int i = j0; i < j1 && !(hit && !all_tests); ++i) {
                 const float4 fb = fine[i];
                 const float3 xb = pose_apply(W, fb.x, fb.y, fb.z);
                 if (two_stage) {
@@ -320,7 +323,7 @@ __device__ __forceinline__ bool lane_check(const SceneV& v, float cpad, const do
                     acc.f += 28;
                     if (fine_pair(v.eps, fine_r64, xa, fa.w, ja0 + q, xb, fb.w, i)) {
                         hit = true;
-                        break;
+                        if (!all_tests) break;
                     }
                 }
             }
@@ -767,24 +770,21 @@ __device__ bool warp_init_problem(const PlanArgs& a, const WarpRegion& wr, const
     return true;
 }
 
-// ---------------------------------------------------------------------------
-// the kernel
-// ---------------------------------------------------------------------------
-__global__ void __launch_bounds__(512, 1) plan_warp_kernel(PlanArgs a) {
+// CTA setup of the warp-worker kernels: robot words, limits + Halton table,
+// i / n_cc table, self pairs grouped by their higher link, store slots, and
+// the per-warp layout in g_w.
+__device__ void warp_cta_setup(const uint32_t* rg, const double* limits, int n_cc, int scene_words_max) {
     extern __shared__ __align__(16) unsigned char smem[];
-    const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
-    const uint32_t* rg = a.robot;
+    const int tid = threadIdx.x;
     const int robot_words = reinterpret_cast<const int*>(rg)[RH_WORDS];
     const int L = (int)rg[RH_NLINKS], dof = (int)rg[RH_DOF], NP = (int)rg[RH_NPAIRS];
-    // CTA setup: robot words, limits + Halton table, i / n_cc table, pair lists
     {
         const WarpLayout lay = warp_layout(robot_words, L, dof, NP, 0, 0);
         uint32_t* rw = reinterpret_cast<uint32_t*>(smem + lay.robot);
         for (int i = tid; i < robot_words / 4; i += blockDim.x)
             reinterpret_cast<uint4*>(rw)[i] = __ldg(reinterpret_cast<const uint4*>(rg) + i);
         double* lim = reinterpret_cast<double*>(smem + lay.lim);
-        for (int i = tid; i < dof * (kHaltonTab + 2); i += blockDim.x) lim[i] = a.limits[i];  // limits, then table
-        const int n_cc = a.p.n_cc;
+        for (int i = tid; i < dof * (kHaltonTab + 2); i += blockDim.x) lim[i] = limits[i];  // limits, then table
         const bool tt = n_cc >= 1 && n_cc <= kTTab;
         double* ttab = reinterpret_cast<double*>(smem + lay.ttab);
         if (tt)
@@ -804,7 +804,7 @@ __global__ void __launch_bounds__(512, 1) plan_warp_kernel(PlanArgs a) {
                     if (max(pairs[p].x, pairs[p].y) == l) plo[e++] = min(pairs[p].x, pairs[p].y);
             }
             pstart[L] = e;
-            const WarpLayout wl = warp_layout(robot_words, L, dof, NP, nstore, a.scene_words_max);
+            const WarpLayout wl = warp_layout(robot_words, L, dof, NP, nstore, scene_words_max);
             WCtx& w = g_w;
             const unsigned base = (unsigned)__cvta_generic_to_shared(smem) - (unsigned)__cvta_generic_to_shared(g_dsmem);
             w.L = L;
@@ -838,6 +838,16 @@ __global__ void __launch_bounds__(512, 1) plan_warp_kernel(PlanArgs a) {
         }
         __syncthreads();
     }
+}
+
+// ---------------------------------------------------------------------------
+// the kernel
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(512, 1) plan_warp_kernel(PlanArgs a) {
+    const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+    const uint32_t* rg = a.robot;
+    const int dof = (int)rg[RH_DOF];
+    warp_cta_setup(rg, a.limits, a.p.n_cc, a.scene_words_max);
     const WarpRegion wr = warp_region(wid);
     const double R = a.p.dd_radius, delta = a.p.delta;
     const unsigned* const bases = smo<unsigned>(g_w.o_bases);
@@ -1103,6 +1113,59 @@ __global__ void __launch_bounds__(512, 1) plan_warp_kernel(PlanArgs a) {
     if (lane == 0 && a.trace) atomicMax(&a.trace[1], (unsigned long long)globaltimer());
 }
 
+// ---------------------------------------------------------------------------
+// batched edge validation (the product API prrtc_validate_edges and the
+// collision microbenchmark) on the warp planner's checker: one edge per warp,
+// one state per lane end to end (FK, two-stage or brute-force collision,
+// early exit by ballot) — the same verdicts as check_chunk's (the planner's
+// own edge test, collision.cpp:206-224), without the CTA-wide barriers.
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(512, 1) validate_edges_warp_kernel(RobotArgs r, SceneArgs sa, const double* from,
+                                                                     const double* to, int n_edges, int n_cc,
+                                                                     int two_stage, int early_exit, uint8_t* out,
+                                                                     unsigned long long* counters) {
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    warp_cta_setup(r.words, r.limits, n_cc, sa.n_words);
+    const WarpRegion wr = warp_region(wid);
+    const int dof = g_w.dof;
+    warp_load_scene(wr.scene, sa.words, lane);
+    float cpad = 0.f;
+    const SceneV v = warp_scene(wr.scene, sa.f64, &cpad);
+    LaneAcc acc;
+    double* const A = wr.dcfg + WD_A * dof;
+    double* const B = wr.dcfg + WD_NEW * dof;
+    for (int e = blockIdx.x * nw + wid; e < n_edges; e += gridDim.x * nw) {
+        __syncwarp();  // the previous edge's endpoints are read before they are rewritten
+        if (lane < dof) {
+            A[lane] = from[(size_t)e * dof + lane];
+            B[lane] = to[(size_t)e * dof + lane];
+        }
+        __syncwarp();
+        bool bad = false;
+        for (int g0 = 0; g0 < n_cc && !(bad && early_exit); g0 += 32) {
+            int group;
+            const bool act = warp_gen_state(A, B, 1, n_cc, n_cc, g0, wr.qf, &group);
+            acc.f += act ? (unsigned)g_w.fkflops : 0u;
+            bool fl;
+            const bool b = lane_check(v, cpad, r.fine_r64, wr.qf, wr.pose, wr.ccen, act, group, early_exit != 0,
+                                      false, two_stage != 0, acc, &fl) && act;
+            bad = __any_sync(kFull, b) || bad;
+        }
+        if (lane == 0) out[e] = bad ? 0 : 1;
+    }
+    if (counters) {  // measurement: executed sphere tests and algorithmic flops
+        unsigned long long t = acc.t, f = acc.f;
+        for (int o = 16; o > 0; o >>= 1) {
+            t += __shfl_xor_sync(kFull, t, o);
+            f += __shfl_xor_sync(kFull, f, o);
+        }
+        if (lane == 0) {
+            atomicAdd(&counters[0], t);
+            atomicAdd(&counters[1], f);
+        }
+    }
+}
+
 // Warps per CTA for a warp-worker launch (one CTA per SM): as many workers
 // as the shared memory holds, at most 16 (128 registers each); 0 when not
 // even one fits (the CTA planner then runs the batch).
@@ -1138,4 +1201,19 @@ cudaError_t launch_plan_warp(const RobotArgs& r, const uint32_t* robot_words_hos
     void* args[] = {&a};
     return cudaLaunchKernel(reinterpret_cast<const void*>(plan_warp_kernel), dim3(grid), dim3(32 * warps), args, sm,
                             st);
+}
+
+cudaError_t launch_validate_edges_warp(const RobotArgs& r, const SceneArgs& s, const double* from, const double* to,
+                                       int n_edges, int n_cc, int two_stage, int early_exit, uint8_t* out,
+                                       cudaStream_t st, unsigned long long* counters, int sms, int max_smem) {
+    const int warps = warp_workers_per_sm(r.host_words, s.n_words, max_smem);
+    if (warps <= 0) return cudaErrorInvalidConfiguration;
+    const size_t sm = warp_smem_bytes(r.host_words, s.n_words, warps);
+    cudaError_t e = raise_smem_limit(reinterpret_cast<const void*>(validate_edges_warp_kernel), (int)sm);
+    if (e != cudaSuccess) return e;
+    const int grid = (int)std::min<long long>(sms, ((long long)n_edges + warps - 1) / warps);
+    if (grid > 0)
+        validate_edges_warp_kernel<<<grid, 32 * warps, sm, st>>>(r, s, from, to, n_edges, n_cc, two_stage, early_exit,
+                                                                out, counters);
+    return cudaGetLastError();
 }
