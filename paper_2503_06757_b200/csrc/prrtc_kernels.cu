@@ -1355,16 +1355,33 @@ cudaError_t raise_smem_limit(const void* fn, int sm) {
     return e;
 }
 
+#include "prrtc_warp.cuh"  // the warp-worker batch planner (plan_warp_kernel)
+
 cudaError_t launch_validate_paths(const RobotArgs& r, const PlanArgs& a, int* prefix, int grid, cudaStream_t st) {
     path_edges_scan_kernel<<<1, 1024, 0, st>>>(a.ctl, a.n_problems, prefix);
+    // the warp checker (one edge per warp) when the robot and the launch's
+    // largest scene fit a warp region; the CTA-wide kernel otherwise
+    if (r.host_words && a.scene_words_max > 0) {
+        int dev = 0, optin = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+        const int warps = warp_workers_per_sm(r.host_words, a.scene_words_max, optin);
+        if (warps > 0) {
+            const size_t sm = warp_smem_bytes(r.host_words, a.scene_words_max, warps);
+            cudaError_t e = raise_smem_limit(reinterpret_cast<const void*>(validate_paths_warp_kernel), (int)sm);
+            if (e != cudaSuccess) return e;
+            int sms = 0;
+            cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+            validate_paths_warp_kernel<<<sms, 32 * warps, sm, st>>>(a, prefix, 4 * a.p.n_cc);
+            return cudaGetLastError();
+        }
+    }
     const size_t sm = smem_bytes(r, a.ns_max, 128, SCENE_MAX_WORDS, true);
     cudaError_t e = raise_smem_limit(reinterpret_cast<const void*>(validate_paths_kernel), (int)sm);
     if (e != cudaSuccess) return e;
     validate_paths_kernel<<<grid, 128, sm, st>>>(a, prefix, 4 * a.p.n_cc);
     return cudaGetLastError();
 }
-
-#include "prrtc_warp.cuh"  // the warp-worker batch planner (plan_warp_kernel)
 
 // CTA size variants: 128 threads (4 warps, up to 4 CTAs/SM) and 256 threads
 // (8 warps, 2 CTAs/SM: each iteration's parallel phases finish faster).

@@ -1166,6 +1166,57 @@ __global__ void __launch_bounds__(512, 1) validate_edges_warp_kernel(RobotArgs r
     }
 }
 
+// Sound mode's path re-validation (validate_paths_kernel's job) on the warp
+// checker: one path edge per warp, 4 n_cc states in rounds of 32 lanes,
+// two-stage with early exit (the verdict of the reference's fine-only, no
+// early exit check: see validate_paths_kernel), a warp re-stages its scene
+// only when the next edge's problem has another one.
+__global__ void __launch_bounds__(512, 1) validate_paths_warp_kernel(PlanArgs a, const int* prefix, int n_cc4) {
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    warp_cta_setup(a.robot, a.limits, n_cc4, a.scene_words_max);
+    const WarpRegion wr = warp_region(wid);
+    const int dof = g_w.dof;
+    double* const A = wr.dcfg + WD_A * dof;
+    double* const B = wr.dcfg + WD_NEW * dof;
+    const int total = prefix[a.n_problems];
+    int cur_scene = -1;
+    SceneV v{};
+    float cpad = 0.f;
+    LaneAcc acc;
+    for (int E = blockIdx.x * nw + wid; E < total; E += gridDim.x * nw) {
+        int lo = 0, hi = a.n_problems - 1;  // last p with prefix[p] <= E
+        while (lo < hi) {
+            const int mid = (lo + hi + 1) >> 1;
+            if (prefix[mid] <= E) lo = mid;
+            else hi = mid - 1;
+        }
+        const int p = lo, e = E - prefix[p];
+        const int si = a.prob_scene[p];
+        if (si != cur_scene) {
+            warp_load_scene(wr.scene, a.scene_words[si], lane);
+            v = warp_scene(wr.scene, a.scene_f64[si], &cpad);
+            cur_scene = si;
+        }
+        const double* P = a.arena + a.ctl[p].path_off + (size_t)e * dof;
+        __syncwarp();
+        if (lane < dof) {
+            A[lane] = P[lane];
+            B[lane] = P[dof + lane];
+        }
+        __syncwarp();
+        bool bad = false;
+        for (int g0 = 0; g0 < n_cc4 && !bad; g0 += 32) {
+            int group;
+            const bool act = warp_gen_state(A, B, 1, n_cc4, n_cc4, g0, wr.qf, &group);
+            bool fl;
+            const bool b = lane_check(v, cpad, a.fine_r64, wr.qf, wr.pose, wr.ccen, act, group, true, false, true, acc,
+                                      &fl) && act;
+            bad = __any_sync(kFull, b);
+        }
+        if (lane == 0 && bad) atomicOr(&a.ctl[p].path_bad, 1);
+    }
+}
+
 // Warps per CTA for a warp-worker launch (one CTA per SM): as many workers
 // as the shared memory holds, at most 16 (128 registers each); 0 when not
 // even one fits (the CTA planner then runs the batch).
