@@ -460,7 +460,7 @@ def planners_block(dev):
         ds = [planner.device_scene(s, dev) for s in scenes]
         idx = np.arange(n) % len(S)
         row = {}
-        for name, nt in (("cta", 0), ("warp", 32)):
+        for name, nt in (("cta", 128), ("warp", 32)):  # (0 would be the automatic choice between them)
             b = planner.Batch(model, [ds[i] for i in idx], S[idx], G[idx],
                               robot_params(robot, headline_params(threads_per_cta=nt)), device=dev)
             ms = []
