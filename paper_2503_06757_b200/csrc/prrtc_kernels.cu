@@ -741,6 +741,42 @@ __device__ __forceinline__ int help_key(const PlanArgs& a, int active, unsigned 
     return 0x7ffffffe - (int)min(per, 0x7ffffff0ull);
 }
 
+// One pass of the help scan over problems start + i (mod n), i = t0, t0 +
+// step, ... < count: an L2 read of every visited problem's (started, done,
+// winner, active) word and ticket count, two independent 16 / 8-byte loads
+// per problem so they pipeline (a hint only: the chosen problem is acquired
+// by the caller; an acquire per problem would invalidate L1 a thousand
+// times). Keeps the best help_key in bk / bp; pending: a claimed problem
+// whose endpoints are still being checked.
+__device__ __forceinline__ void help_scan(const PlanArgs& a, int t0, int step, int start, int count, int& bk, int& bp,
+                                          int& pending) {
+    for (int i = t0; i < count; i += step) {
+        int q = start + i;
+        if (q >= a.n_problems) q -= a.n_problems;
+        const ProbCtl& C = a.ctl[q];
+        const int4 hdr = __ldcg(reinterpret_cast<const int4*>(&C));  // started, done, winner, active
+        const unsigned long long it = __ldcg(&C.iters);
+        pending |= hdr.x == 0 && hdr.y == DONE_RUNNING;
+        if (hdr.x == 1 && hdr.y == DONE_RUNNING && it < a.p.budget && (a.help_cap == 0 || hdr.w < a.help_cap)) {
+            const int key = help_key(a, hdr.w, it);
+            if (key < bk || (key == bk && q < bp)) {
+                bk = key;
+                bp = q;
+            }
+        }
+    }
+}
+
+// Large batches scan a rotating window of kHelpWindow problems first (every
+// freed worker reading all n headers cost the warp planner ~30% of its stall
+// samples on a 10k-problem batch); the full scan runs when the window holds
+// nothing joinable, so leaving (nothing joinable anywhere) stays exact.
+constexpr int kHelpWindow = 1024;
+__device__ __forceinline__ int help_window_start(int n, int attempt, int who) {
+    return (int)(((unsigned)who * 2654435761u + (unsigned)attempt * 40503u + (unsigned)(clock64() & 0xffff)) %
+                 (unsigned)n);
+}
+
 // Help mode: join the running problem chosen by help_key. The parallel RRT-Connect iteration is elastic: any
 // number of workers may join a problem at any time. -1 when none is left.
 __device__ int pick_help(Ctx& c, const PlanArgs& a) {
@@ -758,24 +794,15 @@ __device__ int pick_help(Ctx& c, const PlanArgs& a) {
             __nanosleep(200);
         }
         int bk = 0x7fffffff, bp = -1, pending = 0;
-        // an L2 scan of every problem's (started, done, winner, active) word
-        // and ticket count, two independent 16 / 8-byte loads per problem so
-        // they pipeline (a hint only: the chosen problem is acquired below;
-        // an acquire per problem would invalidate L1 a thousand times)
-        for (int q = tid; q < a.n_problems; q += c.nthreads) {
-            const ProbCtl& C = a.ctl[q];
-            const int4 hdr = __ldcg(reinterpret_cast<const int4*>(&C));  // started, done, winner, active
-            const unsigned long long it = __ldcg(&C.iters);
-            pending |= hdr.x == 0 && hdr.y == DONE_RUNNING;  // claimed, endpoints still being checked
-            if (hdr.x == 1 && hdr.y == DONE_RUNNING && it < a.p.budget &&
-                (a.help_cap == 0 || hdr.w < a.help_cap)) {
-                const int key = help_key(a, hdr.w, it);
-                if (key < bk) {
-                    bk = key;
-                    bp = q;
-                }
-            }
+        if (a.n_problems > 2 * kHelpWindow) {
+            if (tid == 0) sh(c.ictl)[IC_TMP1] = help_window_start(a.n_problems, attempt, blockIdx.x);
+            __syncthreads();
+            const int start = sh(c.ictl)[IC_TMP1];
+            __syncthreads();
+            help_scan(a, tid, c.nthreads, start, kHelpWindow, bk, bp, pending);
+            pending = 0;  // (the full scan below decides waiting / leaving)
         }
+        if (!__syncthreads_or(bp >= 0)) help_scan(a, tid, c.nthreads, 0, a.n_problems, bk, bp, pending);
         // every problem is claimed (the claim loop ran dry) and every running
         // one has handed out its whole iteration budget: nothing can ever be
         // joined again, so leave instead of spinning (the scans of idle CTAs

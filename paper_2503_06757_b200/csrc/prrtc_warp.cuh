@@ -660,20 +660,14 @@ __device__ int warp_pick_help(const PlanArgs& a) {
             __nanosleep(200);
         }
         int bk = 0x7fffffff, bp = -1, pending = 0;
-        for (int q = lane; q < a.n_problems; q += 32) {
-            const ProbCtl& C = a.ctl[q];
-            const int4 hdr = __ldcg(reinterpret_cast<const int4*>(&C));  // started, done, winner, active
-            const unsigned long long it = __ldcg(&C.iters);
-            pending |= hdr.x == 0 && hdr.y == DONE_RUNNING;  // claimed, endpoints still being checked
-            if (hdr.x == 1 && hdr.y == DONE_RUNNING && it < a.p.budget &&
-                (a.help_cap == 0 || hdr.w < a.help_cap)) {
-                const int key = help_key(a, hdr.w, it);
-                if (key < bk) {
-                    bk = key;
-                    bp = q;
-                }
-            }
+        if (a.n_problems > 2 * kHelpWindow) {  // a rotating window first (see kHelpWindow)
+            int start = 0;
+            if (lane == 0) start = help_window_start(a.n_problems, attempt, blockIdx.x * 32 + (threadIdx.x >> 5));
+            start = __shfl_sync(kFull, start, 0);
+            help_scan(a, lane, 32, start, kHelpWindow, bk, bp, pending);
+            pending = 0;
         }
+        if (!__any_sync(kFull, bp >= 0)) help_scan(a, lane, 32, 0, a.n_problems, bk, bp, pending);
         // every problem is claimed (the claim loop ran dry) and every running
         // one has handed out its whole iteration budget: nothing can ever be
         // joined again, so leave instead of spinning (idle workers' scans

@@ -33,9 +33,10 @@ if mode == "single":
         r = planner.plan(m, sc, d["start"][i], d["goal"][i], params)
         print(r.status.name, r.iterations_total, f"{r.device_time_ms:.3f} ms", r.tree_nodes, r.message)
 else:
-    k = min(n_prob, len(d["pid"]))
-    scenes = [make_scene(robot, str(kk), int(p))[0] for kk, p in zip(d["kind"][:k], d["pid"][:k])]
-    b = planner.Batch(m, scenes, d["start"][:k], d["goal"][:k], params)
+    idx = np.arange(n_prob) % len(d["pid"])  # (n_prob > 1000 repeats the set)
+    scenes0 = [make_scene(robot, str(kk), int(p))[0] for kk, p in zip(d["kind"], d["pid"])]
+    ds = [planner.device_scene(sc) for sc in scenes0]
+    b = planner.Batch(m, [ds[i] for i in idx], d["start"][idx], d["goal"][idx], params)
     for _ in range(n):
         b.launch()
         res = b.results()
