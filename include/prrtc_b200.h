@@ -149,8 +149,9 @@ typedef struct prrtc_params {
     /* --- device knobs (no reference equivalent) --- */
     uint32_t threads_per_cta;      /* 0 = automatic: 512 for one problem; a batch runs on
                                       128-thread CTAs, or on the warp-worker planner (one
-                                      worker per warp) when it holds >= 3x as many problems
-                                      as the device has warp workers; else 128, 256 or
+                                      worker per warp) when it holds at least as many
+                                      problems as the device has warp workers and at
+                                      least 2048; else 128, 256 or
                                       512, or 32 = the warp-worker planner (not for
                                       deterministic / Uniform-sampler runs) */
     uint32_t ctas_per_sm;          /* 0 = as many as co-reside */

@@ -1065,12 +1065,10 @@ int batch_setup(prrtc_batch* b, const prrtc_robot* robot, const prrtc_scene* con
     // replay with its exact CheckStats, not the Uniform sampler's per-CTA
     // generator, no phase tracer or debug flags): asked for with
     // threads_per_cta = 32, and chosen automatically (threads_per_cta = 0)
-    // when the batch holds at least 3x as many problems as the device has
-    // warp workers (batch_bind): its weakness is per-problem latency, which
-    // only a long tail of problems exposes (Panda 3333
-    // problems 2.9 vs 4.0 ms, 10k 8.1 vs 8.1; Fetch 10k 48.8 vs 37.4;
-    // Baxter 3333 37.2 vs 34.7, 10k 110.5 vs 100.1). PRRTC_WARP=1 / 0 force
-    // it on / off for every eligible batch (A/B).
+    // when the batch holds at least as many problems as the device has warp
+    // workers, and at least 2048 (batch_bind): its weakness is per-problem
+    // latency, which only a long tail of problems exposes.
+    // PRRTC_WARP=1 / 0 force it on / off for every eligible batch (A/B).
     const bool warp_mode_ok = n_problems > 1 && !params->deterministic &&
                               params->sampler == PRRTC_SAMPLER_HALTON && !ekw.trace && ekw.debug_flags == 0;
     b->warp_ok = warp_mode_ok && (params->threads_per_cta == 32 ||
@@ -1190,7 +1188,10 @@ int batch_bind(prrtc_batch* b, Workspace* ws, const prrtc_scene* const* scenes, 
     if (b->warp_ok) {
         b->warps = warp_workers_per_sm(b->robot->words.data(), b->scene_words_max, smem_optin(b->device));
         const int sms = sm_count(b->device);
-        if (b->warp_auto && (long long)b->n < 3ll * b->warps * sms) b->warps = 0;  // the CTA planner
+        // (crossover measured with windowed help scans: Panda ~2500
+        // problems, Fetch < 2500, Baxter ~2000; below it the per-problem
+        // latency of a warp worker sets the batch's tail)
+        if (b->warp_auto && (long long)b->n < std::max(2048ll, (long long)b->warps * sms)) b->warps = 0;
         if (b->warps > 0) b->grid = sms;
     }
     return PRRTC_OK;
