@@ -445,7 +445,7 @@ def parity_block(robot_names, workers_list, n, device=0, tree_capacity=200000, t
     return out
 
 
-def planners_block(dev):
+def planners_block(dev, peak=None):
     """The two device planners on the same device-resident batches at the
     headline params: CTA workers (the default, plan_kernel)
     and warp workers (threads_per_cta = 32, plan_warp_kernel); kernel time by
@@ -471,8 +471,11 @@ def planners_block(dev):
                 e1.record(st)
                 st.synchronize()
                 ms.append(e0.elapsed_time(e1))
-            ok = np.mean([r.status == PlanStatus.Solved for r in b.results()])
-            row[name] = {"kernel_ms": min(ms[1:]), "problems_per_s": n / (min(ms[1:]) / 1e3), "success": float(ok)}
+            res = b.results()
+            ok = np.mean([r.status == PlanStatus.Solved for r in res])
+            tf = float(sum(r.flops for r in res)) / (ms[-1] * 1e-3) / 1e12  # the last launch's counted flops
+            row[name] = {"kernel_ms": min(ms[1:]), "problems_per_s": n / (min(ms[1:]) / 1e3), "success": float(ok),
+                         "achieved_tflops": tf, "fp32_frac": tf / peak if peak else None}
             del b
         out[f"{robot}_{n}"] = row
     return out
@@ -823,7 +826,7 @@ def run_b200(args):
         if not args.no_extras:
             extras["robots"] = {r: table_one(dev, r, robot_params, 100, peak) for r in ("panda", "fetch", "baxter")}
             extras.update(bench_extras(dev, params))
-            extras["planners"] = planners_block(dev)
+            extras["planners"] = planners_block(dev, peak)
         micro = microbench(model, scenes, S, G, dev, peak)
         parity = None
         if not args.no_parity:
