@@ -361,6 +361,34 @@ struct SPtr {
     }
 };
 
+// The CTA's fixed-size buffers sit at constant offsets at the start of the
+// dynamic window (sizes for NS <= 128, nthreads <= 512): an access is an
+// immediate shared address, where an SPtr first loads its offset from the
+// shared Ctx — a dependent LDS the compiler must repeat after every barrier
+// (ncu source view, r2i: 11.7% of plan_kernel's stall samples on those
+// offset loads).
+enum : unsigned {
+    FX_ICTL = 0,        // [IC_COUNT] int
+    FX_T0 = 128,        // [T0_COUNT] u64
+    FX_RED_D = 192,     // [16] double
+    FX_RED_I = 320,     // [16] int
+    FX_MNN_D = 384,     // [32] double
+    FX_MNN_I = 640,     // [32] int
+    FX_MNN_OK = 768,    // [32] int
+    FX_DCFG = 896,      // [8][kMaxDof] double
+    FX_SGROUP = 2944,   // [128] int
+    FX_SBAD = 3456,     // [128] int
+    FX_TTAB = 3968,     // [kTTab + 1] double
+    FX_END = 5008
+};
+static_assert(FX_DCFG + 8 * 8 * kMaxDof == FX_SGROUP && FX_TTAB + 8 * (kTTab + 1) <= FX_END && FX_END % 16 == 0,
+              "fixed shared-memory region");
+template <class T, unsigned OFF>
+struct FPtr {
+    __device__ __forceinline__ T* get() const { return reinterpret_cast<T*>(g_dsmem + OFF); }
+    __device__ __forceinline__ operator T*() const { return get(); }
+};
+
 struct Ctx {
     // robot (shared memory copy of the packed words)
     int L, dof, S, NP, MF, mflog;  // mflog: log2 of MF rounded up to a power of two
@@ -379,7 +407,7 @@ struct Ctx {
     SPtr<const double> limits;    // [dof][2] (shared copy, before the Halton table)
     unsigned fkflops;        // per-state FK + coarse posing flops
     long long* prof;         // per-phase clock64 stamps (debug hook only, else null)
-    SPtr<double> ttab;            // [kTTab + 1]: i / ttab_n for i = 0..ttab_n (edge sample fractions)
+    FPtr<double, FX_TTAB> ttab;   // [kTTab + 1]: i / ttab_n for i = 0..ttab_n (edge sample fractions)
     int ttab_n;              // n_cc the table was built for (0 = none)
     // scene (shared memory copy)
     int ns, nb, nc, ny, P;
@@ -394,21 +422,20 @@ struct Ctx {
     SPtr<float> pose;     // [L][12][NS]
     SPtr<float> ccen;     // [L][3][NS]
     SPtr<float> qf;       // [dof][NS]
-    SPtr<int> sgroup;     // [NS] group id, -1 = inactive
-    SPtr<int> sbad;       // [NS]
+    FPtr<int, FX_SGROUP> sgroup;  // [NS] group id, -1 = inactive
+    FPtr<int, FX_SBAD> sbad;      // [NS]
     SPtr<unsigned long long> lmask;  // [L][NS] coarse-flagged primitives per (link, state)
     SPtr<unsigned long long> pmask;  // [ceil(NP/64)][NS] coarse-flagged self pairs per state
     SPtr<double> ends;    // [NS + 2][dof] chain points of the chunk
-    SPtr<int> ends_eq;    // [NS + 2] bitwise-equal sub-edge flags
     // CTA scalars
-    SPtr<int> ictl;       // [32] misc ints
-    SPtr<double> dcfg;    // [8][kMaxDof] scratch configs
+    FPtr<int, FX_ICTL> ictl;      // [32] misc ints
+    FPtr<double, FX_DCFG> dcfg;   // [8][kMaxDof] scratch configs
     SPtr<double> sbuf;    // [32][dof] Halton samples of the CTA's current ticket block
-    SPtr<double> mnn_d;   // [32] multi-sample NN: squared distance per evaluated sample
-    SPtr<int> mnn_i;      // [32]                  nearest index per evaluated sample
-    SPtr<int> mnn_ok;     // [32]                  accepted (not duplicate, inside its dynamic domain)
-    SPtr<double> red_d;   // [nwarps]
-    SPtr<int> red_i;      // [nwarps]
+    FPtr<double, FX_MNN_D> mnn_d; // [32] multi-sample NN: squared distance per evaluated sample
+    FPtr<int, FX_MNN_I> mnn_i;    // [32]                  nearest index per evaluated sample
+    FPtr<int, FX_MNN_OK> mnn_ok;  // [32]                  accepted (not duplicate, inside its dynamic domain)
+    FPtr<double, FX_RED_D> red_d; // [nwarps]
+    FPtr<int, FX_RED_I> red_i;    // [nwarps]
     int nthreads;
     // stats: per-thread slots [nthreads][2] in shared memory (sphere tests,
     // algorithmic FP32 flops), summed when a CTA leaves a problem
@@ -416,7 +443,7 @@ struct Ctx {
     // the planner loop's thread-0 state (ticket block, iteration and CheckStats
     // counters): kept in shared memory so it does not occupy registers
     // (spilled around every call) in all threads of the CTA
-    SPtr<unsigned long long> t0;
+    FPtr<unsigned long long, FX_T0> t0;
     // exact-CheckStats mode (deterministic planning): counters follow the
     // reference's sequential semantics (ref_state_count); per-state scratch
     int ref_stats;
@@ -445,6 +472,10 @@ __device__ __forceinline__ bool ctx_writer(const Ctx& c) { return !__isShared(&c
 // memory). Hot routines take their pointers into registers through it once.
 template <class T>
 __device__ __forceinline__ T* sh(const SPtr<T>& p) {
+    return p.get();
+}
+template <class T, unsigned OFF>
+__device__ __forceinline__ T* sh(const FPtr<T, OFF>& p) {
     return p.get();
 }
 template <class T>
@@ -1323,7 +1354,6 @@ __device__ __forceinline__ int gen_chain_states_inl(Ctx& c, const double* A, con
     const int tid = threadIdx.x, dof = c.dof, NS = c.NS, nthreads = c.nthreads;
     const int stop = (stop_flag && tid == 0) ? ld_relaxed(stop_flag) : 0;
     double* const ends = sh(c.ends);
-    int* const ends_eq = sh(c.ends_eq);
     int* const sgroup = sh(c.sgroup);
     float* const qf = sh(c.qf);
     const double* const ttab = n_cc == c.ttab_n ? sh(c.ttab) : nullptr;
@@ -1356,12 +1386,6 @@ __device__ __forceinline__ int gen_chain_states_inl(Ctx& c, const double* A, con
     }
     if (tid == 0) sh(c.ictl)[IC_KLO] = (int)k_lo;
     __syncthreads();
-    for (int j = tid; j < npts - 1; j += nthreads) {
-        bool eq = true;
-        for (int d = 0; d < dof; ++d) eq &= ends[j * dof + d] == ends[(j + 1) * dof + d];
-        ends_eq[j] = eq;
-    }
-    __syncthreads();
     int mine = 0;
     for (int s = tid; s < NS; s += nthreads) {
         if (s >= cnt) {
@@ -1372,12 +1396,14 @@ __device__ __forceinline__ int gen_chain_states_inl(Ctx& c, const double* A, con
         const unsigned k = g / ncc;
         const int i = (int)(g - k * ncc) + 1;
         const int j = (int)(k - k_lo);
-        if (ends_eq[j] && i != n_cc) {
+        const double* F = ends + j * dof;
+        const double* T = F + dof;
+        bool eq = i != n_cc;  // a bitwise-equal sub-edge: only its far end is checked
+        for (int d = 0; eq && d < dof; ++d) eq = F[d] == T[d];
+        if (eq) {
             sgroup[s] = -1;
             continue;
         }
-        const double* F = ends + j * dof;
-        const double* T = F + dof;
         if (i == n_cc) {
             for (int d = 0; d < dof; ++d) qf[d * NS + s] = (float)T[d];
         } else {

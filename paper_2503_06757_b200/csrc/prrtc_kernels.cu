@@ -31,7 +31,7 @@ using namespace dev;
 // ---------------------------------------------------------------------------
 struct SmemLayout {
     size_t robot, scene, pose, ccen, qf, sgroup, sbad, lmask, ictl, dcfg, red_d, red_i,
-        ends, ends_eq, ttab, sbuf, mnn, stat, htab, t0, rcount, rfine, mt, total;
+        ends, ttab, sbuf, mnn, stat, htab, t0, rcount, rfine, mt, total;
 };
 
 __host__ __device__ inline size_t al16(size_t x) { return (x + 15) & ~size_t(15); }
@@ -44,28 +44,29 @@ __host__ __device__ inline SmemLayout smem_layout(int robot_words, int L, int do
                                                   int nthreads, int scene_words = SCENE_MAX_WORDS,
                                                   bool with_mt = true) {
     SmemLayout s;
-    size_t o = 0;
+    // the fixed-offset CTA buffers first (prrtc_device.cuh FX_*), then the
+    // robot- and scene-sized ones
+    s.ictl = FX_ICTL;
+    s.t0 = FX_T0;
+    s.red_d = FX_RED_D;
+    s.red_i = FX_RED_I;
+    s.mnn = FX_MNN_D;
+    s.dcfg = FX_DCFG;
+    s.sgroup = FX_SGROUP;
+    s.sbad = FX_SBAD;
+    s.ttab = FX_TTAB;
+    size_t o = FX_END;
     s.robot = o; o = al16(o + 4 * (size_t)robot_words);
     s.scene = o; o = al16(o + 4 * (size_t)scene_words);
     s.pose = o;  o = al16(o + 4 * (size_t)L * 12 * NS);
     s.ccen = o;  o = al16(o + 4 * (size_t)L * 3 * NS);
     s.qf = o;    o = al16(o + 4 * (size_t)dof * NS);
-    s.sgroup = o; o = al16(o + 4 * (size_t)NS);
-    s.sbad = o;  o = al16(o + 4 * (size_t)NS);
     // lmask [L][NS] then pmask [ceil(NP/64)][NS] (PRRTC_MAX_SELF_PAIRS = 512)
     s.lmask = o; o = al16(o + 8 * (size_t)(L + 8) * NS);
-    s.ictl = o;  o = al16(o + 4 * (size_t)IC_COUNT);
-    s.dcfg = o;  o = al16(o + 8 * (size_t)8 * kMaxDof);
-    s.red_d = o; o = al16(o + 8 * (size_t)(nthreads / 32));
-    s.red_i = o; o = al16(o + 4 * (size_t)(nthreads / 32));
     s.ends = o;  o = al16(o + 8 * (size_t)(NS + 2) * dof);
-    s.ends_eq = o; o = al16(o + 4 * (size_t)(NS + 2));
-    s.ttab = o;  o = al16(o + 8 * (size_t)(kTTab + 1));
     s.sbuf = o;  o = al16(o + 8 * (size_t)32 * dof);  // one ticket block of 32 samples
-    s.mnn = o;   o = al16(o + (8 + 4 + 4) * 32);
     s.stat = o;  o = al16(o + 16 * (size_t)nthreads);
     s.htab = o;  o = al16(o + 8 * (size_t)dof * (kHaltonTab + 2));  // + the [dof][2] limits
-    s.t0 = o;    o = al16(o + 8 * (size_t)T0_COUNT);
     s.rcount = o; o = al16(o + 8 * (size_t)NS);
     s.rfine = o; o = al16(o + 4 * (size_t)NS);
     s.mt = o;    o = al16(o + (with_mt ? 8 * (size_t)(kMtN + 1) : 0));
@@ -88,7 +89,7 @@ __device__ void setup_ctx(Ctx& c, unsigned char* smem, const uint32_t* robot_g, 
                           const double* fine_r64, const double* limits, int NS,
                           int scene_words = SCENE_MAX_WORDS, bool with_mt = true) {
     const int tid = threadIdx.x, nthreads = blockDim.x;
-    uint32_t* rw = reinterpret_cast<uint32_t*>(smem);
+    uint32_t* rw = reinterpret_cast<uint32_t*>(smem + FX_END);  // the robot words (smem_layout: s.robot)
     // 16-byte vector copy (buffer padded to a multiple of 4 words on host)
     for (int i = tid; i < robot_words / 4; i += nthreads) {
         reinterpret_cast<uint4*>(rw)[i] = __ldg(reinterpret_cast<const uint4*>(robot_g) + i);
@@ -127,24 +128,12 @@ __device__ void setup_ctx(Ctx& c, unsigned char* smem, const uint32_t* robot_g, 
         c.pose = reinterpret_cast<float*>(smem + lay.pose);
         c.ccen = reinterpret_cast<float*>(smem + lay.ccen);
         c.qf = reinterpret_cast<float*>(smem + lay.qf);
-        c.sgroup = reinterpret_cast<int*>(smem + lay.sgroup);
-        c.sbad = reinterpret_cast<int*>(smem + lay.sbad);
         c.lmask = reinterpret_cast<unsigned long long*>(smem + lay.lmask);
         c.pmask = c.lmask + (size_t)c.L * NS;
-        c.ictl = reinterpret_cast<int*>(smem + lay.ictl);
-        c.dcfg = reinterpret_cast<double*>(smem + lay.dcfg);
-        c.red_d = reinterpret_cast<double*>(smem + lay.red_d);
-        c.red_i = reinterpret_cast<int*>(smem + lay.red_i);
         c.ends = reinterpret_cast<double*>(smem + lay.ends);
-        c.ends_eq = reinterpret_cast<int*>(smem + lay.ends_eq);
         c.htab = htab + 2 * c.dof;
-        c.ttab = reinterpret_cast<double*>(smem + lay.ttab);
         c.sbuf = reinterpret_cast<double*>(smem + lay.sbuf);
-        c.mnn_d = reinterpret_cast<double*>(smem + lay.mnn);
-        c.mnn_i = reinterpret_cast<int*>(smem + lay.mnn + 8 * 32);
-        c.mnn_ok = reinterpret_cast<int*>(smem + lay.mnn + 12 * 32);
         c.stat = stat;
-        c.t0 = reinterpret_cast<unsigned long long*>(smem + lay.t0);
         c.ref_stats = 0;  // the planner turns it on in deterministic mode
         c.rcount = reinterpret_cast<unsigned long long*>(smem + lay.rcount);
         c.rfine = reinterpret_cast<int*>(smem + lay.rfine);
@@ -1656,12 +1645,10 @@ __global__ void debug_hits_kernel(SceneArgs sa, const float* centers, const doub
 // pass): the parity tests run it against the reference's nearest_serial
 __global__ void debug_nn_multi_kernel(const double* soa, long long cap, int count, int dof, const double* q,
                                       int nq, int group, uint32_t* idx, double* d2) {
-    double* qs = reinterpret_cast<double*>(g_dsmem);  // [32][kMaxDof]
+    double* qs = reinterpret_cast<double*>(g_dsmem + FX_END);  // [32][kMaxDof], after the fixed region (mnn_*)
     Ctx c;
     c.dof = dof;
     c.nthreads = blockDim.x;
-    c.mnn_d = qs + 32 * kMaxDof;
-    c.mnn_i = reinterpret_cast<int*>(c.mnn_d + 32);
     for (int b = blockIdx.x * group; b < nq; b += gridDim.x * group) {
         const int m = min(group, nq - b);
         for (int k = threadIdx.x; k < m * dof; k += blockDim.x) qs[k] = q[(size_t)b * dof + k];
@@ -1920,7 +1907,7 @@ cudaError_t launch_debug_nn_multi(const double* soa, long long cap, int count, i
                                   int nq, int group, uint32_t* idx, double* d2, cudaStream_t st) {
     const int grid = min((nq + group - 1) / group, cur_sms() * 8);
     if (grid > 0)
-        debug_nn_multi_kernel<<<grid, 128, 8 * 32 * kMaxDof + 8 * 32 + 4 * 32, st>>>(soa, cap, count, dof, q, nq,
+        debug_nn_multi_kernel<<<grid, 128, FX_END + 8 * 32 * kMaxDof, st>>>(soa, cap, count, dof, q, nq,
                                                                                        group, idx, d2);
     return cudaGetLastError();
 }
