@@ -350,6 +350,44 @@ def test_single_problem_result_paths_agree(gpu, oracle, robot, monkeypatch):
             assert oracle.path_valid(m, scene, r0.path, params.n_cc)
 
 
+@pytest.mark.parametrize("robot", ["panda", "baxter"])
+def test_chunk_size_does_not_change_the_search(gpu, oracle, robot, monkeypatch):
+    """Edge states are validated NS at a time (32, 64 or 128 per chunk; the
+    fixed-offset shared region holds per-state buffers for 128). The chunk
+    size is a schedule, not a semantic: in deterministic mode a single
+    problem with 32-, 64- (default) and 128-state chunks is the same search —
+    identical status, path, iterations and reference-semantics CheckStats."""
+    m = robots.get(robot)
+    probs = load_problems(robot, 10)
+    params = PlannerParams(deterministic=True, tree_capacity=20000)
+    if robot == "baxter":
+        params.dd_radius = 4.0
+    knobs = ("PRRTC_NS32", "PRRTC_NS64", "PRRTC_NS128")
+    try:
+        for kind, pid, s, g in probs[:5]:
+            scene, _ = make_scene(robot, kind, pid)
+            runs = []
+            for env in ({}, {"PRRTC_NS32": "1"}, {"PRRTC_NS128": "1"}):
+                for k in knobs:
+                    monkeypatch.delenv(k, raising=False)
+                for k, v in env.items():
+                    monkeypatch.setenv(k, v)
+                planner.reload_env()
+                runs.append(planner.plan(m, scene, s, g, params))
+            r0 = runs[0]
+            for r in runs[1:]:
+                assert r.status == r0.status
+                assert np.array_equal(r.path, r0.path)
+                assert r.iterations_total == r0.iterations_total
+                assert r.check_stats == r0.check_stats
+            if r0.status == PlanStatus.Solved:
+                assert oracle.path_valid(m, scene, r0.path, params.n_cc)
+    finally:
+        for k in knobs:
+            monkeypatch.delenv(k, raising=False)
+        planner.reload_env()
+
+
 def test_tree_invariants_under_concurrent_appends(gpu, monkeypatch):
     """Lock-free tree protocol under load: with
     PRRTC_DEBUG_FLAGS bit 2 every CTA checks, at every snapshot it acquires,
