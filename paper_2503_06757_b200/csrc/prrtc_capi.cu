@@ -74,6 +74,7 @@ struct EnvKnobs {
     bool ns32 = false, ns64 = false, ns128 = false, trace = false, host_trace = false, no_map = false;
     unsigned debug_flags = 0;
     int tail_claim = 1, mnn_nodes = 0;
+    int tail_min = 4, tail_div = 4;  // PRRTC_TAIL_MIN / PRRTC_TAIL_DIV (sweeps)
     int warp = -1;  // PRRTC_WARP=1: eligible batches on the warp-worker planner (A/B runs)
     int help_cap = 0;  // PRRTC_HELP_CAP: most workers a help join may bring a problem to (sweeps)
     int help_policy = 1;  // PRRTC_HELP_POLICY: 1 most unclaimed budget per worker, 0 fewest workers (A/B)
@@ -95,6 +96,8 @@ const EnvKnobs* read_env() {
     k->no_map = on("PRRTC_NO_MAP");
     if (const char* e = std::getenv("PRRTC_DEBUG_FLAGS")) k->debug_flags = (unsigned)std::atoi(e);
     if (const char* e = std::getenv("PRRTC_TAIL_CLAIM")) k->tail_claim = std::atoi(e);
+    if (const char* e = std::getenv("PRRTC_TAIL_MIN")) k->tail_min = std::max(1, std::atoi(e));
+    if (const char* e = std::getenv("PRRTC_TAIL_DIV")) k->tail_div = std::max(1, std::atoi(e));
     if (const char* e = std::getenv("PRRTC_WARP")) k->warp = std::atoi(e);
     if (const char* e = std::getenv("PRRTC_HELP_CAP")) k->help_cap = std::atoi(e);
     if (const char* e = std::getenv("PRRTC_HELP_POLICY")) k->help_policy = std::atoi(e);
@@ -1279,6 +1282,8 @@ int batch_enqueue(prrtc_batch* b, cudaStream_t st, bool upload) {
     a.p.deterministic = b->params.deterministic;
     a.ref_stats = b->params.deterministic ? 1 : 0;
     a.tail_claim = ek.tail_claim;
+    a.tail_min = ek.tail_min;
+    a.tail_div = ek.tail_div;
     // help joins stop at the problem's worker cap (an env override for sweeps)
     a.help_cap = ek.help_cap ? ek.help_cap : (int)b->params.max_workers_per_problem;
     a.help_policy = ek.help_policy;

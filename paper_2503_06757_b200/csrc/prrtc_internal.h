@@ -163,6 +163,7 @@ struct PlanArgs {
     int mnn_nodes;                      // multi-sample NN bound: m <= mnn_nodes / tree size
     int ref_stats;                      // exact CheckStats (reference counting semantics): deterministic mode
     int tail_claim;                     // smaller ticket blocks near a problem's budget end
+    int tail_min, tail_div;             // ... block = max(tail_min, min(32, unclaimed / (tail_div * workers)))
     int scene_words_max;                // warp-worker planner: words of the largest bound scene
     int help_cap;                       // help mode joins only problems with fewer active workers (0 = any)
     int help_policy;                    // which problem help joins: 1 most unclaimed budget per worker, 0 fewest workers

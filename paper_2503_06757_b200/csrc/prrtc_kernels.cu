@@ -1022,7 +1022,8 @@ __global__ void __launch_bounds__(NT, MINB) plan_kernel(PlanArgs a) {
                         const unsigned long long seen = tk_cnt ? tk_base + tk_cnt : __ldcg(&C.iters);
                         const int act = max(1, ld_relaxed(&C.active));
                         if (seen < a.p.budget)
-                            want = max(4ull, min((unsigned long long)kblk, (a.p.budget - seen) / (2ull * act)));
+                            want = max((unsigned long long)a.tail_min,
+                                       min((unsigned long long)kblk, (a.p.budget - seen) / ((unsigned long long)a.tail_div * act)));
                     }
                     tk_base = a.p.deterministic ? tk_base + tk_cnt : atomicAdd(&C.iters, want);
                     tk_pos = 0;

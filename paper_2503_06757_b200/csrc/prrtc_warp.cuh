@@ -914,7 +914,8 @@ __global__ void __launch_bounds__(512, 1) plan_warp_kernel(PlanArgs a) {
                         const unsigned long long seen = tk_cnt ? tk_base + tk_cnt : __ldcg(&C.iters);
                         const int act = max(1, ld_relaxed(&C.active));
                         if (seen < a.p.budget)
-                            want = max(4ull, min((unsigned long long)kblk, (a.p.budget - seen) / (2ull * act)));
+                            want = max((unsigned long long)a.tail_min,
+                                       min((unsigned long long)kblk, (a.p.budget - seen) / ((unsigned long long)a.tail_div * act)));
                     }
                     claimed = atomicAdd(&C.iters, want);
                 }
