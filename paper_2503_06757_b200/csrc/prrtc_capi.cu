@@ -1079,14 +1079,23 @@ int batch_setup(prrtc_batch* b, const prrtc_robot* robot, const prrtc_scene* con
     b->warp_auto = b->warp_ok && params->threads_per_cta == 0 && ekw.warp < 0;
     // states per validation chunk: one n_cc = 32 edge; a 256-thread CTA uses
     // its extra warps to split links / pairs / primitives of the same chunk.
-    // A single problem (latency-bound, one CTA per SM) takes 64-state chunks:
-    // a connect chain needs half the chunk rounds (Panda median wall latency
-    // 0.141 -> 0.121 ms, tools/ab_env.sh); PRRTC_NS32 / PRRTC_NS64 force either.
-    // (128-state chunks, PRRTC_NS128: Panda median -5% but p95 +2%, Fetch +4%;
-    // 64-state chunks in the Panda batch: 159k -> 137k problems/s)
+    // A single problem (latency-bound, one CTA per SM) takes wider chunks: a
+    // connect chain needs fewer chunk rounds. 64 states on 256-thread CTAs
+    // (Panda median wall latency 0.141 -> 0.121 ms); 128 on the default
+    // 512-thread CTAs when they fit the shared memory (Panda median 0.097 ->
+    // 0.089 ms, Fetch and Baxter +-0; tools/lat.py). PRRTC_NS32 / PRRTC_NS64 /
+    // PRRTC_NS128 force a width (64-state chunks in the Panda batch: 159k ->
+    // 137k problems/s).
     const EnvKnobs& ek = env();
-    const bool ns64 = !ek.ns32 && ((n_problems == 1 && b->nthreads >= 256) || ek.ns64);
-    b->ns_max = ns64 ? (ek.ns128 ? 128 : 64) : 32;
+    const bool wide = !ek.ns32 && ((n_problems == 1 && b->nthreads >= 256) || ek.ns64 || ek.ns128);
+    bool ns128 = wide && (ek.ns128 || (n_problems == 1 && b->nthreads >= 512 && !ek.ns64));
+    if (ns128 && !ek.ns128) {
+        size_t swm1 = 0;
+        for (uint32_t i = 0; i < n_problems; ++i) swm1 = std::max(swm1, scenes[i]->words.size());
+        ns128 = smem_bytes(robot->args(), 128, b->nthreads, (int)swm1 + 4,
+                           params->sampler == PRRTC_SAMPLER_UNIFORM) <= (size_t)smem_optin(robot->device);
+    }
+    b->ns_max = wide ? (ns128 ? 128 : 64) : 32;
     // shared memory per CTA follows the largest scene of the launch and the
     // sampler (the Uniform generator's state); occupancy is cached per
     // scene-size bucket, computed at the bucket's upper bound
