@@ -1326,8 +1326,9 @@ int batch_enqueue(prrtc_batch* b, cudaStream_t st, bool upload) {
     const auto e0 = std::chrono::steady_clock::now();
     a.scene_words_max = b->scene_words_max;  // per-CTA (per-warp) scene region size
     if (b->warps) {
-        // warp workers: a multi-sample NN pass bounded to ~8 node pairs per lane
-        a.mnn_nodes = ek.mnn_nodes ? ek.mnn_nodes : 512;
+        // warp workers: a multi-sample NN pass bounded to ~2 node pairs per
+        // lane (128 nodes: 10k batches Baxter -3%, Fetch -2% vs 512)
+        a.mnn_nodes = ek.mnn_nodes ? ek.mnn_nodes : 128;
     }
     if (b->timed) CUDA_TRY(cudaEventRecord(ws->ev0, st));
     const auto e1 = std::chrono::steady_clock::now();
