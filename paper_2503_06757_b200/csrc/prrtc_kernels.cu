@@ -1090,9 +1090,26 @@ __global__ void __launch_bounds__(NT, MINB) plan_kernel(PlanArgs a) {
                 const unsigned long long base = reinterpret_cast<unsigned long long*>(sh(c.red_d))[0];
                 const int nblk = sh(c.ictl)[IC_TMP7];
                 __syncthreads();  // header scalars read before they are reused
-                if (a.p.uniform)  // the CTA's own stream, in draw order (sampling.hpp:44-48)
+                if (a.p.uniform) {  // the CTA's own stream, in draw order (sampling.hpp:44-48)
                     mt_fill(sh(c.mt), sh(c.limits), dof, sh(c.sbuf), nblk * dof, c.nthreads);
-                else
+                } else if (base + nblk <= a.stab_n) {
+                    // every problem of the launch draws the same samples (same
+                    // robot limits, seed and ticket range): the block is one
+                    // contiguous run of the per-launch table, copied with up
+                    // to four independent loads in flight per thread (one L2
+                    // round trip per block instead of one per element)
+                    const double* src = a.stab + base * dof;
+                    double* dst = sh(c.sbuf);
+                    const int tot = nblk * dof, nt = c.nthreads;
+                    for (int j0 = tid; j0 < tot; j0 += 4 * nt) {
+                        double v[4];
+#pragma unroll
+                        for (int u = 0; u < 4; ++u) v[u] = j0 + u * nt < tot ? __ldg(src + j0 + u * nt) : 0.0;
+#pragma unroll
+                        for (int u = 0; u < 4; ++u)
+                            if (j0 + u * nt < tot) dst[j0 + u * nt] = v[u];
+                    }
+                } else
                 for (int j = tid; j < nblk * dof; j += c.nthreads) {
                     const int k = j / dof, d = j - k * dof;
                     // every problem of the launch draws the same samples (same
