@@ -379,9 +379,12 @@ enum : unsigned {
     FX_SGROUP = 2944,   // [128] int
     FX_SBAD = 3456,     // [128] int
     FX_TTAB = 3968,     // [kTTab + 1] double
-    FX_END = 5008
+    FX_PANY = 5008,     // [8] u64: self pairs coarse-flagged for any state of the chunk
+    FX_LANY = 5072,     // u64: links coarse-flagged for any state of the chunk
+    FX_END = 5088
 };
-static_assert(FX_DCFG + 8 * 8 * kMaxDof == FX_SGROUP && FX_TTAB + 8 * (kTTab + 1) <= FX_END && FX_END % 16 == 0,
+static_assert(FX_DCFG + 8 * 8 * kMaxDof == FX_SGROUP && FX_TTAB + 8 * (kTTab + 1) <= FX_PANY &&
+                  FX_PANY + 8 * 8 == FX_LANY && FX_LANY + 8 <= FX_END && FX_END % 16 == 0,
               "fixed shared-memory region");
 template <class T, unsigned OFF>
 struct FPtr {
@@ -424,6 +427,8 @@ struct Ctx {
     SPtr<float> qf;       // [dof][NS]
     FPtr<int, FX_SGROUP> sgroup;  // [NS] group id, -1 = inactive
     FPtr<int, FX_SBAD> sbad;      // [NS]
+    FPtr<unsigned long long, FX_PANY> pany;  // [8] pairs flagged for any state (then lany at [8])
+    FPtr<unsigned long long, FX_LANY> lany;  // links flagged for any state
     SPtr<unsigned long long> lmask;  // [L][NS] coarse-flagged primitives per (link, state)
     SPtr<unsigned long long> pmask;  // [ceil(NP/64)][NS] coarse-flagged self pairs per state
     SPtr<double> ends;    // [NS + 2][dof] chain points of the chunk
@@ -605,6 +610,7 @@ __device__ __forceinline__ void fk_chunk(Ctx& c, int cnt) {
             unsigned long long* const lmask = sh(c.lmask);
             for (int s = t0; s < NS; s += nt) sbad[s] = 0;
             for (int i = t0; i < (L + PW) * NS; i += nt) lmask[i] = 0ull;  // pmask follows lmask
+            if (t0 < 9) sh(c.pany)[t0] = 0ull;  // pany[8] and lany
             if (t0 == 0) {
                 sh(c.ictl)[IC_QN] = 0;
                 sh(c.ictl)[IC_FIRSTBAD] = kNoBad;
@@ -1031,6 +1037,7 @@ __device__ __forceinline__ void check_chunk_inl(Ctx& c, int cnt, bool two_stage,
     // sub-ranges), states over lanes
     int flagged = 0;
     {
+        unsigned long long lbits = 0;  // links this thread flagged: the chunk's summary in lany
         const int T = L * v.P, nwlog = 31 - __clz(nw);  // nw: 4, 8 or 16
         const int lo = (T * warp) >> nwlog, hi = (T * (warp + 1)) >> nwlog;
         int l = v.P ? lo / v.P : 0, p0 = lo - l * v.P;  // one division per warp, then walk
@@ -1047,9 +1054,13 @@ __device__ __forceinline__ void check_chunk_inl(Ctx& c, int cnt, bool two_stage,
                 acc.f += fl;
                 if (m) {
                     or64_shared(&lmask[l * NS + s], m);
-                    flagged = 1;
+                    lbits |= 1ull << l;
                 }
             }
+        }
+        if (lbits) {
+            or64_shared(sh(c.lany), lbits);
+            flagged = 1;
         }
     }
     if (prof && tid == 0) prof[10] = clock64();  // warp 0's share of the coarse env tests done
@@ -1062,7 +1073,10 @@ __device__ __forceinline__ void check_chunk_inl(Ctx& c, int cnt, bool two_stage,
         int blk = warp >> 6;
         for (int pr = warp; pr < NP; pr += nw) {
             if ((pr >> 6) != blk) {
-                if (pm) or64_shared(&pmask[blk * NS + s], pm);
+                if (pm) {
+                    or64_shared(&pmask[blk * NS + s], pm);
+                    or64_shared(sh(c.pany) + blk, pm);
+                }
                 flagged |= pm != 0;
                 pm = 0;
                 blk = pr >> 6;
@@ -1076,7 +1090,10 @@ __device__ __forceinline__ void check_chunk_inl(Ctx& c, int cnt, bool two_stage,
             acc.f += 10;
             if (fmaf(dx, dx, fmaf(dy, dy, dz * dz)) < rr * rr) pm |= 1ull << (pr & 63);
         }
-        if (pm) or64_shared(&pmask[blk * NS + s], pm);
+        if (pm) {
+            or64_shared(&pmask[blk * NS + s], pm);
+            or64_shared(sh(c.pany) + blk, pm);
+        }
         flagged |= pm != 0;
     }
     if (stop_flag && tid == 0) k.ictl[IC_STOP] = stop;
@@ -1094,9 +1111,11 @@ __device__ __forceinline__ void check_chunk_inl(Ctx& c, int cnt, bool two_stage,
     // when one link collects most of the flags.
     {
         const int2* const funits = sh(c.funits);
+        const unsigned long long lany = *sh(c.lany);  // (a unit of a link no state flagged is skipped whole)
         for (int u = warp; u < c.NFU; u += nw) {
             const int2 un = funits[u];
             const int l = un.x, j0 = un.y & 0xffff, j1 = j0 + (un.y >> 16);
+            if (!((lany >> l) & 1ull)) continue;
             for (int s = lane; s < cnt; s += 32) {
                 const unsigned long long m0 = lmask[l * NS + s];
                 if (!m0 || skip_state(k, s, early_exit, indep)) continue;
@@ -1126,8 +1145,11 @@ __device__ __forceinline__ void check_chunk_inl(Ctx& c, int cnt, bool two_stage,
         __syncthreads();
         if (tid == 0) prof[6] = clock64();
     }
-    // stage 2b: flagged (pair, state): fine x fine (collision.cpp:89-98)
+    // stage 2b: flagged (pair, state): fine x fine (collision.cpp:89-98);
+    // a pair no state flagged is skipped whole
+    const unsigned long long* const pany = sh(c.pany);
     for (int pr = warp; pr < NP; pr += nw) {
+        if (!((pany[pr >> 6] >> (pr & 63)) & 1ull)) continue;
         const int2 ab = pairs[pr];
         const int na = nfine[ab.x], nb = nfine[ab.y];
         const int ja0 = info[ab.x].w, jb0 = info[ab.y].w;
