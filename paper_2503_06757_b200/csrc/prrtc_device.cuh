@@ -664,7 +664,8 @@ __device__ __forceinline__ void fk_chunk(Ctx& c, int cnt) {
             } else {
                 float a0 = w0, a1 = w1, a2 = w2, tp = wt;
                 if (inf.y != l - 1) {  // branch point: the parent row this lane stored
-                    const float* Q = pose + inf.y * 12 * NS + sr;
+                    // (its own column s even when inactive: no lane reads another's row)
+                    const float* Q = pose + inf.y * 12 * NS + s;
                     a0 = Q[(3 * r + 0) * NS];
                     a1 = Q[(3 * r + 1) * NS];
                     a2 = Q[(3 * r + 2) * NS];

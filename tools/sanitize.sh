@@ -18,6 +18,7 @@ run synccheck_single    --tool synccheck python tools/profile_one.py panda 1 sin
 run synccheck_batch40   --tool synccheck python tools/profile_one.py panda 1 batch 40
 run racecheck_single4   --tool racecheck --racecheck-report hazard python tools/profile_one.py panda 1 single 1 4
 run racecheck_batch12   --tool racecheck --racecheck-report hazard python tools/profile_one.py panda 1 batch 12
+run racecheck_baxter8   --tool racecheck --racecheck-report hazard python tools/profile_one.py baxter 1 batch 8
 run memcheck_parity     --tool memcheck  python -m pytest tests/test_gpu_parity.py -x -q -k "not nn_exact"
 if [ "${WARP:-1}" = "1" ]; then  # the warp-worker planner (plan_warp_kernel, PRRTC_WARP=1)
   PRRTC_WARP=1 run memcheck_warp_batch100  --tool memcheck  python tools/profile_one.py panda 2 batch 100
