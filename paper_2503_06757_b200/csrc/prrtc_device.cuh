@@ -1148,9 +1148,13 @@ __device__ __forceinline__ void check_chunk_inl(Ctx& c, int cnt, bool two_stage,
     }
     // stage 2b: flagged (pair, state): fine x fine (collision.cpp:89-98);
     // a pair no state flagged is skipped whole
+    // (the pairs some state flagged, pany, dealt to the warps round-robin)
     const unsigned long long* const pany = sh(c.pany);
-    for (int pr = warp; pr < NP; pr += nw) {
-        if (!((pany[pr >> 6] >> (pr & 63)) & 1ull)) continue;
+    int pidx = 0;
+    for (int w = 0; w < ((NP + 63) >> 6); ++w)
+    for (unsigned long long pb = pany[w]; pb; pb &= pb - 1, ++pidx) {
+        if ((pidx & (nw - 1)) != warp) continue;
+        const int pr = (w << 6) + __ffsll((long long)pb) - 1;
         const int2 ab = pairs[pr];
         const int na = nfine[ab.x], nb = nfine[ab.y];
         const int ja0 = info[ab.x].w, jb0 = info[ab.y].w;
