@@ -837,7 +837,12 @@ __device__ void warp_cta_setup(const uint32_t* rg, const double* limits, int n_c
 // ---------------------------------------------------------------------------
 // the kernel
 // ---------------------------------------------------------------------------
-__global__ void __launch_bounds__(512, 1) plan_warp_kernel(PlanArgs a) {
+// MAXW: the most warps the instantiation is launched with (one CTA per SM;
+// fewer warps fit the shared memory for larger robots and scenes). The
+// register cap follows: 128 at 16 warps, 136 at 14, 160 at 12 (a full 64K
+// split, 144 x 14 warps, is refused at launch: "too many resources")
+template <int MAXW>
+__global__ void __maxnreg__(MAXW >= 16 ? 128 : (MAXW >= 14 ? 136 : 160)) plan_warp_kernel(PlanArgs a) {
     const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
     const uint32_t* rg = a.robot;
     const int dof = (int)rg[RH_DOF];
@@ -1242,11 +1247,16 @@ size_t warp_smem_bytes(const uint32_t* robot_words_host, int scene_words_max, in
 cudaError_t launch_plan_warp(const RobotArgs& r, const uint32_t* robot_words_host, PlanArgs a, int grid, int warps,
                              cudaStream_t st) {
     const size_t sm = warp_smem_bytes(robot_words_host, a.scene_words_max, warps);
-    cudaError_t e = raise_smem_limit(reinterpret_cast<const void*>(plan_warp_kernel), (int)sm);
+    const void* fn = warps <= 12 ? reinterpret_cast<const void*>(plan_warp_kernel<12>)
+                     : warps <= 14 ? reinterpret_cast<const void*>(plan_warp_kernel<14>)
+                                   : reinterpret_cast<const void*>(plan_warp_kernel<16>);
+    cudaFuncAttributes fa;  // (the 128-register instantiation if the device refuses the wider one)
+    if (cudaFuncGetAttributes(&fa, fn) != cudaSuccess || fa.maxThreadsPerBlock < 32 * warps)
+        fn = reinterpret_cast<const void*>(plan_warp_kernel<16>);
+    cudaError_t e = raise_smem_limit(fn, (int)sm);
     if (e != cudaSuccess) return e;
     void* args[] = {&a};
-    return cudaLaunchKernel(reinterpret_cast<const void*>(plan_warp_kernel), dim3(grid), dim3(32 * warps), args, sm,
-                            st);
+    return cudaLaunchKernel(fn, dim3(grid), dim3(32 * warps), args, sm, st);
 }
 
 cudaError_t launch_validate_edges_warp(const RobotArgs& r, const SceneArgs& s, const double* from, const double* to,
