@@ -959,6 +959,20 @@ __global__ void __maxnreg__(MAXW >= 16 ? 128 : (MAXW >= 14 ? 136 : 160)) plan_wa
             if (refill) {
                 const int nblk = (int)tk_cnt;
                 __syncwarp();  // the previous block's samples are read before they are overwritten
+                if (tk_base + nblk <= a.stab_n) {
+                    // the block is one contiguous run of the per-launch table:
+                    // up to four independent loads in flight per lane
+                    const double* src = a.stab + tk_base * dof;
+                    const int tot = nblk * dof;
+                    for (int j0 = lane; j0 < tot; j0 += 128) {
+                        double v[4];
+#pragma unroll
+                        for (int u = 0; u < 4; ++u) v[u] = j0 + 32 * u < tot ? __ldg(src + j0 + 32 * u) : 0.0;
+#pragma unroll
+                        for (int u = 0; u < 4; ++u)
+                            if (j0 + 32 * u < tot) wr.sbuf[j0 + 32 * u] = v[u];
+                    }
+                } else
                 for (int j = lane; j < nblk * dof; j += 32) {
                     const int k = j / dof, d = j - k * dof;
                     const unsigned long long t = tk_base + k;  // (the per-launch sample table, see plan_kernel)
