@@ -76,6 +76,7 @@ struct EnvKnobs {
     int tail_claim = 1, mnn_nodes = 0;
     int tail_min = 4, tail_div = 4;  // PRRTC_TAIL_MIN / PRRTC_TAIL_DIV (sweeps)
     int warp = -1;  // PRRTC_WARP=1: eligible batches on the warp-worker planner (A/B runs)
+    int warps_cap = 0;  // PRRTC_WARPS=k: at most k warp workers per SM (sweeps)
     int help_cap = 0;  // PRRTC_HELP_CAP: most workers a help join may bring a problem to (sweeps)
     int help_policy = 1;  // PRRTC_HELP_POLICY: 1 most unclaimed budget per worker, 0 fewest workers (A/B)
     bool no_stab = false;  // PRRTC_NO_SAMPLE_TABLE: compute every Halton sample in the loop (A/B)
@@ -99,6 +100,7 @@ const EnvKnobs* read_env() {
     if (const char* e = std::getenv("PRRTC_TAIL_MIN")) k->tail_min = std::max(1, std::atoi(e));
     if (const char* e = std::getenv("PRRTC_TAIL_DIV")) k->tail_div = std::max(1, std::atoi(e));
     if (const char* e = std::getenv("PRRTC_WARP")) k->warp = std::atoi(e);
+    if (const char* e = std::getenv("PRRTC_WARPS")) k->warps_cap = std::max(0, std::atoi(e));
     if (const char* e = std::getenv("PRRTC_HELP_CAP")) k->help_cap = std::atoi(e);
     if (const char* e = std::getenv("PRRTC_HELP_POLICY")) k->help_policy = std::atoi(e);
     k->no_stab = on("PRRTC_NO_SAMPLE_TABLE");
@@ -1199,6 +1201,7 @@ int batch_bind(prrtc_batch* b, Workspace* ws, const prrtc_scene* const* scenes, 
     b->scene_words_max = (int)((mx + 3) & ~size_t(3));
     if (b->warp_ok) {
         b->warps = warp_workers_per_sm(b->robot->words.data(), b->scene_words_max, smem_optin(b->device));
+        if (env().warps_cap > 0) b->warps = std::min(b->warps, env().warps_cap);
         const int sms = sm_count(b->device);
         // (crossover measured with windowed help scans: Panda ~2500
         // problems, Fetch < 2500, Baxter ~2000; below it the per-problem
