@@ -41,7 +41,8 @@ struct WCtx {
     int L, dof, S, NP, nstore, fkflops;
     unsigned o_info, o_nfine, o_geo, o_fine, o_bases, o_magic;  // robot words
     unsigned o_lim, o_htab, o_ttab;  // [dof][2] limits, [dof][kHaltonTab] Halton table, [n_cc + 1] i / n_cc
-    unsigned o_pstart, o_plo, o_slot;  // self pairs by higher link: [L + 1] starts, [NP] lower links; [L] store slot
+    unsigned o_pstart, o_plo, o_slot;  // self pairs by higher link: [L + 1] starts; [NP] (lower link | its
+                                       // store slot << 16, coarse radius sum bits); [L] store slot
     int ttab_n;
     unsigned warp0, per_warp;           // first warp region, region size
     unsigned w_scene, w_pose, w_ccen, w_qf, w_sbuf, w_dcfg;  // offsets inside a warp region
@@ -71,7 +72,7 @@ __host__ __device__ inline WarpLayout warp_layout(int robot_words, int L, int do
     w.htab = o;  o = al16(o + 8 * (size_t)dof * kHaltonTab);
     w.ttab = o;  o = al16(o + 8 * (size_t)(kTTab + 1));
     w.pstart = o; o = al16(o + 4 * (size_t)(L + 1));
-    w.plo = o;   o = al16(o + 4 * (size_t)(NP > 0 ? NP : 1));
+    w.plo = o;   o = al16(o + 8 * (size_t)(NP > 0 ? NP : 1));
     w.slot = o;  o = al16(o + 4 * (size_t)L);
     w.shared_end = o;
     size_t p = 0;
@@ -147,7 +148,7 @@ __device__ __forceinline__ bool lane_check(const SceneV& v, float cpad, const do
     const float* const geo = smo<float>(g_w.o_geo);
     const float4* const fine = smo<float4>(g_w.o_fine);
     const int* const pstart = smo<int>(g_w.o_pstart);
-    const int* const plo = smo<int>(g_w.o_plo);
+    const int2* const plo = smo<int2>(g_w.o_plo);
     const int* const slot = smo<int>(g_w.o_slot);
     const int pflops = range_flops(v, 0, v.P);
     bool bad = false, live = active, flag = false;
@@ -287,11 +288,12 @@ __device__ __forceinline__ bool lane_check(const SceneV& v, float cpad, const do
         }
         // self pairs whose higher link is l (collision.cpp:174-183, 197-203)
         for (int e = pstart[l]; e < pstart[l + 1] && !(bad && early_exit); ++e) {
-            const int a = plo[e], sa = slot[a];
+            const int2 pe = plo[e];
+            const int a = pe.x & 0xffff, sa = pe.x >> 16;
             const float* CA = cstore + sa * 3 * 32 + lane;
             const float ax = CA[0], ay = CA[32], az = CA[64];
             if (two_stage) {
-                const float rr = geo[a * GEO_STRIDE + 36] + g[36] + 2.0f * cpad;
+                const float rr = __int_as_float(pe.y) + 2.0f * cpad;  // (r_a + r_l) + 2 cpad
                 const float dx = ax - cx, dy = ay - cy, dz = az - cz;
                 ++acc.t;
                 acc.f += 10;
@@ -788,14 +790,21 @@ __device__ void warp_cta_setup(const uint32_t* rg, const double* limits, int n_c
             const int4* info = reinterpret_cast<const int4*>(rw + rw[RH_OFF_INFO]);
             const int2* pairs = reinterpret_cast<const int2*>(rw + rw[RH_OFF_PAIRS]);
             int* pstart = reinterpret_cast<int*>(smem + lay.pstart);
-            int* plo = reinterpret_cast<int*>(smem + lay.plo);
+            int2* plo = reinterpret_cast<int2*>(smem + lay.plo);
+            const float* geo = reinterpret_cast<const float*>(rw + rw[RH_OFF_GEO]);
             int* slot = reinterpret_cast<int*>(smem + lay.slot);
             const int nstore = warp_store_count(info, pairs, L, NP, slot);
             int e = 0;
             for (int l = 0; l < L; ++l) {  // self pairs grouped by their higher link
                 pstart[l] = e;
                 for (int p = 0; p < NP; ++p)
-                    if (max(pairs[p].x, pairs[p].y) == l) plo[e++] = min(pairs[p].x, pairs[p].y);
+                    if (max(pairs[p].x, pairs[p].y) == l) {
+                        // one 64-bit record per pair: the lower link, its pose
+                        // store slot, and r_a + r_l (the coarse test's sum)
+                        const int a = min(pairs[p].x, pairs[p].y);
+                        plo[e++] = make_int2(a | (slot[a] << 16),
+                                             __float_as_int(geo[a * GEO_STRIDE + 36] + geo[l * GEO_STRIDE + 36]));
+                    }
             }
             pstart[L] = e;
             const WarpLayout wl = warp_layout(robot_words, L, dof, NP, nstore, scene_words_max);
